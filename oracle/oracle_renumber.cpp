@@ -1,0 +1,242 @@
+// oracle/oracle_renumber.cpp — O-9: RCM renumbering (George-Liu start),
+// face re-sort, cell->face CSR, block partition and halo lists.
+//
+// TEST INFRASTRUCTURE ONLY (see oracle.h).  The rules are the exact integer
+// specification of SURVEY.md §8(c) O-9 (north_star subsystem (1)); the
+// library must reproduce every map bit for bit.
+#include "oracle.h"
+
+#include <algorithm>
+#include <cstring>
+#include <deque>
+#include <tuple>
+
+namespace orc {
+
+struct Renum {
+  int64_t N = 0, F = 0, NF = 0;
+  int P = 1;
+  std::vector<int32_t> new_of_old;       // cells
+  std::vector<int32_t> face_new_of_old;  // all faces
+  std::vector<int8_t> flip_of_old;       // internal faces (by old index)
+  std::vector<int32_t> row_ptr;          // [N+1] internal incidences (new numbering)
+  std::vector<int32_t> inc_face;         // new face index, bit 31 set when s = -1
+  std::vector<int32_t> inc_nb;           // new neighbour id
+  std::vector<int32_t> brow_ptr, b_face; // boundary CSR (non-empty boundary faces)
+  std::vector<int32_t> part;             // by new id
+  // per part: ghosts (new ids, ordered by (peer, new id)), ghost peer,
+  // and per peer the send list (new ids)
+  std::vector<std::vector<int32_t>> ghost, ghost_peer, send, send_peer;
+  int64_t bandwidth_before = 0, bandwidth_after = 0;
+};
+
+// O-9 steps 1-4.
+static void rcm(const Mesh& m, std::vector<int32_t>& new_of_old) {
+  const int64_t N = m.N;
+  // adjacency with duplicate pairs collapsed
+  std::vector<std::vector<int32_t>> adj(N);
+  for (int64_t f = 0; f < m.F; ++f) {
+    adj[m.owner[f]].push_back(m.neigh[f]);
+    adj[m.neigh[f]].push_back(m.owner[f]);
+  }
+  for (auto& a : adj) { std::sort(a.begin(), a.end()); a.erase(std::unique(a.begin(), a.end()), a.end()); }
+  auto key_less = [&](int32_t a, int32_t b) {
+    return adj[a].size() != adj[b].size() ? adj[a].size() < adj[b].size() : a < b;
+  };
+  // neighbours sorted by key
+  for (auto& a : adj) std::sort(a.begin(), a.end(), key_less);
+  std::vector<char> placed(N, 0);
+  std::vector<int32_t> order;
+  order.reserve(N);
+  std::vector<int64_t> level(N, -1);
+  // BFS levels from r over unplaced cells; returns last level
+  auto bfs_levels = [&](int32_t r, std::vector<int32_t>& visited, int64_t& ecc) {
+    visited.clear();
+    std::vector<int32_t> frontier{r}, next;
+    level[r] = 0;
+    visited.push_back(r);
+    int64_t lv = 0;
+    std::vector<int32_t> last = frontier;
+    while (!frontier.empty()) {
+      next.clear();
+      for (int32_t c : frontier)
+        for (int32_t nb : adj[c])
+          if (!placed[nb] && level[nb] < 0) { level[nb] = lv + 1; next.push_back(nb); visited.push_back(nb); }
+      if (next.empty()) break;
+      ++lv;
+      last = next;
+      frontier.swap(next);
+    }
+    ecc = lv;
+    for (int32_t c : visited) level[c] = -1;
+    return last;
+  };
+  int64_t scan = 0;  // smallest-key unplaced search: keys sorted once
+  std::vector<int32_t> by_key(N);
+  for (int64_t i = 0; i < N; ++i) by_key[i] = (int32_t)i;
+  std::sort(by_key.begin(), by_key.end(), key_less);
+  std::vector<int32_t> visited;
+  while ((int64_t)order.size() < N) {
+    while (placed[by_key[scan]]) ++scan;
+    int32_t r = by_key[scan];
+    // George-Liu pseudo-peripheral start
+    int64_t ecc_r;
+    std::vector<int32_t> last = bfs_levels(r, visited, ecc_r);
+    for (;;) {
+      int32_t x = *std::min_element(last.begin(), last.end(), key_less);
+      int64_t ecc_x;
+      std::vector<int32_t> last_x = bfs_levels(x, visited, ecc_x);
+      if (ecc_x > ecc_r) { r = x; ecc_r = ecc_x; last = last_x; }
+      else break;
+    }
+    // Cuthill-McKee BFS
+    std::deque<int32_t> q;
+    q.push_back(r);
+    placed[r] = 1;
+    while (!q.empty()) {
+      int32_t c = q.front(); q.pop_front();
+      order.push_back(c);
+      for (int32_t nb : adj[c])
+        if (!placed[nb]) { placed[nb] = 1; q.push_back(nb); }
+    }
+  }
+  new_of_old.assign(N, 0);
+  for (int64_t k = 0; k < N; ++k) new_of_old[order[N - 1 - k]] = (int32_t)k;
+}
+
+static Renum* renumber(const Mesh& m, int P, int use_rcm) {
+  Renum* R = new Renum();
+  R->N = m.N; R->F = m.F; R->NF = m.NF; R->P = P;
+  if (use_rcm) rcm(m, R->new_of_old);
+  else { R->new_of_old.resize(m.N); for (int64_t c = 0; c < m.N; ++c) R->new_of_old[c] = (int32_t)c; }
+  const auto& nw = R->new_of_old;
+  for (int64_t f = 0; f < m.F; ++f) {
+    int64_t bw = std::abs((int64_t)m.owner[f] - m.neigh[f]);
+    R->bandwidth_before = std::max(R->bandwidth_before, bw);
+    R->bandwidth_after = std::max(R->bandwidth_after, (int64_t)std::abs(nw[m.owner[f]] - nw[m.neigh[f]]));
+  }
+  // step 5: face re-sort
+  std::vector<std::tuple<int32_t, int32_t, int64_t>> keys(m.F);
+  R->flip_of_old.assign(m.F, 0);
+  for (int64_t f = 0; f < m.F; ++f) {
+    int32_t a = nw[m.owner[f]], b = nw[m.neigh[f]];
+    if (a > b) { std::swap(a, b); R->flip_of_old[f] = 1; }
+    keys[f] = std::make_tuple(a, b, f);
+  }
+  std::sort(keys.begin(), keys.end());
+  R->face_new_of_old.assign(m.NF, 0);
+  std::vector<int32_t> own_new(m.NF), nb_new(m.F);
+  for (int64_t k = 0; k < m.F; ++k) {
+    int64_t f = std::get<2>(keys[k]);
+    R->face_new_of_old[f] = (int32_t)k;
+    own_new[k] = std::get<0>(keys[k]); nb_new[k] = std::get<1>(keys[k]);
+  }
+  for (size_t p = 0; p < m.pkind.size(); ++p) {
+    std::vector<std::pair<int32_t, int64_t>> bk;
+    for (int64_t f = m.pstart[p]; f < m.pstart[p] + m.pn[p]; ++f) bk.push_back({nw[m.owner[f]], f});
+    std::sort(bk.begin(), bk.end());
+    for (size_t i = 0; i < bk.size(); ++i) {
+      R->face_new_of_old[bk[i].second] = (int32_t)(m.pstart[p] + (int64_t)i);
+      own_new[m.pstart[p] + i] = bk[i].first;
+    }
+  }
+  // step 6: CSR of internal incidences in ascending new face index
+  const int64_t N = m.N;
+  R->row_ptr.assign(N + 1, 0);
+  for (int64_t k = 0; k < m.F; ++k) { R->row_ptr[own_new[k] + 1]++; R->row_ptr[nb_new[k] + 1]++; }
+  for (int64_t c = 0; c < N; ++c) R->row_ptr[c + 1] += R->row_ptr[c];
+  R->inc_face.assign(2 * m.F, 0); R->inc_nb.assign(2 * m.F, 0);
+  {
+    std::vector<int32_t> pos(R->row_ptr.begin(), R->row_ptr.end() - 1);
+    for (int64_t k = 0; k < m.F; ++k) {
+      int32_t o = own_new[k], n = nb_new[k];
+      R->inc_face[pos[o]] = (int32_t)k; R->inc_nb[pos[o]++] = n;
+      R->inc_face[pos[n]] = (int32_t)((uint32_t)k | 0x80000000u); R->inc_nb[pos[n]++] = o;
+    }
+  }
+  R->brow_ptr.assign(N + 1, 0);
+  for (int64_t f = m.F; f < m.NF; ++f)
+    if (!m.is_empty_face(f)) R->brow_ptr[own_new[R->face_new_of_old[f]] + 1]++;
+  for (int64_t c = 0; c < N; ++c) R->brow_ptr[c + 1] += R->brow_ptr[c];
+  R->b_face.assign(R->brow_ptr[N], 0);
+  {
+    std::vector<int32_t> pos(R->brow_ptr.begin(), R->brow_ptr.end() - 1);
+    // boundary faces in ascending new index (via the inverse face map)
+    std::vector<int64_t> old_of_new(m.NF);
+    for (int64_t f = 0; f < m.NF; ++f) old_of_new[R->face_new_of_old[f]] = f;
+    for (int64_t k = m.F; k < m.NF; ++k) {
+      int64_t f = old_of_new[k];
+      if (m.is_empty_face(f)) continue;
+      R->b_face[pos[own_new[k]]++] = (int32_t)k;
+    }
+  }
+  // step 7: partition into P contiguous blocks of the new order
+  R->part.assign(N, 0);
+  std::vector<int64_t> lo(P + 1);
+  for (int p = 0; p <= P; ++p) lo[p] = (int64_t)p * N / P;
+  for (int p = 0; p < P; ++p)
+    for (int64_t c = lo[p]; c < lo[p + 1]; ++c) R->part[c] = p;
+  R->ghost.assign(P, {}); R->ghost_peer.assign(P, {});
+  R->send.assign(P, {}); R->send_peer.assign(P, {});
+  for (int p = 0; p < P; ++p) {
+    std::vector<std::pair<int32_t, int32_t>> g;   // (peer, new id)
+    std::vector<std::pair<int32_t, int32_t>> s;   // (peer, new id of owned cell)
+    for (int64_t c = lo[p]; c < lo[p + 1]; ++c)
+      for (int32_t i = R->row_ptr[c]; i < R->row_ptr[c + 1]; ++i) {
+        int32_t nb = R->inc_nb[i];
+        int q = R->part[nb];
+        if (q != p) { g.push_back({q, nb}); s.push_back({q, (int32_t)c}); }
+      }
+    std::sort(g.begin(), g.end()); g.erase(std::unique(g.begin(), g.end()), g.end());
+    std::sort(s.begin(), s.end()); s.erase(std::unique(s.begin(), s.end()), s.end());
+    for (auto& x : g) { R->ghost_peer[p].push_back(x.first); R->ghost[p].push_back(x.second); }
+    for (auto& x : s) { R->send_peer[p].push_back(x.first); R->send[p].push_back(x.second); }
+  }
+  return R;
+}
+
+}  // namespace orc
+
+using namespace orc;
+
+extern "C" {
+
+void* orc_renumber_create(const void* mp, int n_parts, int use_rcm) {
+  return renumber(*(const Mesh*)mp, n_parts, use_rcm);
+}
+void orc_renumber_destroy(void* r) { delete (Renum*)r; }
+// sizes: N, F, NF, I (=2F), nB (non-empty boundary faces), bw_before, bw_after
+void orc_renumber_sizes(const void* rp, int64_t* out) {
+  const Renum* R = (const Renum*)rp;
+  out[0] = R->N; out[1] = R->F; out[2] = R->NF; out[3] = (int64_t)R->inc_face.size();
+  out[4] = (int64_t)R->b_face.size(); out[5] = R->bandwidth_before; out[6] = R->bandwidth_after;
+}
+void orc_renumber_maps(const void* rp, int32_t* cell_new_of_old, int32_t* face_new_of_old, int8_t* flip_of_old,
+                       int32_t* row_ptr, int32_t* inc_face, int32_t* inc_nb, int32_t* brow_ptr, int32_t* b_face,
+                       int32_t* part) {
+  const Renum* R = (const Renum*)rp;
+  std::memcpy(cell_new_of_old, R->new_of_old.data(), 4 * R->new_of_old.size());
+  std::memcpy(face_new_of_old, R->face_new_of_old.data(), 4 * R->face_new_of_old.size());
+  std::memcpy(flip_of_old, R->flip_of_old.data(), R->flip_of_old.size());
+  std::memcpy(row_ptr, R->row_ptr.data(), 4 * R->row_ptr.size());
+  std::memcpy(inc_face, R->inc_face.data(), 4 * R->inc_face.size());
+  std::memcpy(inc_nb, R->inc_nb.data(), 4 * R->inc_nb.size());
+  std::memcpy(brow_ptr, R->brow_ptr.data(), 4 * R->brow_ptr.size());
+  std::memcpy(b_face, R->b_face.data(), 4 * R->b_face.size());
+  std::memcpy(part, R->part.data(), 4 * R->part.size());
+}
+// per part: out[0] = n_ghost, out[1] = n_send
+void orc_renumber_part_sizes(const void* rp, int p, int64_t* out) {
+  const Renum* R = (const Renum*)rp;
+  out[0] = (int64_t)R->ghost[p].size(); out[1] = (int64_t)R->send[p].size();
+}
+void orc_renumber_part(const void* rp, int p, int32_t* ghost, int32_t* ghost_peer, int32_t* send,
+                       int32_t* send_peer) {
+  const Renum* R = (const Renum*)rp;
+  std::memcpy(ghost, R->ghost[p].data(), 4 * R->ghost[p].size());
+  std::memcpy(ghost_peer, R->ghost_peer[p].data(), 4 * R->ghost_peer[p].size());
+  std::memcpy(send, R->send[p].data(), 4 * R->send[p].size());
+  std::memcpy(send_peer, R->send_peer[p].data(), 4 * R->send_peer[p].size());
+}
+
+}  // extern "C"
