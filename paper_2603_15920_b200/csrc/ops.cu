@@ -1,0 +1,288 @@
+// ops.cu — sm_100a kernels of the FVM operators (SURVEY.md §8(a) a6, and
+// the north-star `fvm_grad/div/laplacian apply`).
+//
+// All cell operators are deterministic cell-gathers over the SELL-32
+// incidence layout (internal.h): one warp handles 32 consecutive (RCM-
+// ordered) rows, one thread per row, incidence k of the warp's rows is one
+// coalesced 256-byte int2 load; face geometry records (32 B, fp64) and
+// neighbour values are gathered through L2 (RCM keeps the two reads of a
+// face within the bandwidth window).  No atomics: the per-cell sum runs over
+// the row's incidences in ascending face order (P:297-305 eq:aggregate
+// realised as a gather, reading A-20).
+#include <cuda_runtime.h>
+
+#include "dev.cuh"
+#include "launch.h"
+
+namespace dfvm {
+
+// ----------------------------------------------------------- import/export
+template <class T>
+__global__ void k_import(T* __restrict__ dst, const double* __restrict__ src, const int32_t* __restrict__ map,
+                         int64_t n, int nc, bool oriented) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t m = map[i];
+    const bool neg = oriented && (m < 0);
+    const int64_t o = m < 0 ? (int64_t)(~m) : m;
+    for (int k = 0; k < nc; ++k) {
+      const double v = src[o * nc + k];
+      dst[i * nc + k] = (T)(neg ? -v : v);
+    }
+  }
+}
+template <class T>
+__global__ void k_export(double* __restrict__ dst, const T* __restrict__ src, const int32_t* __restrict__ map,
+                         int64_t n, int nc, bool oriented) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t m = map[i];
+    const bool neg = oriented && (m < 0);
+    const int64_t o = m < 0 ? (int64_t)(~m) : m;
+    for (int k = 0; k < nc; ++k) {
+      const double v = (double)src[i * nc + k];
+      dst[o * nc + k] = neg ? -v : v;
+    }
+  }
+}
+template <class T>
+void launch_import(T* dst, const double* src, const int32_t* map, int64_t n, int nc, bool oriented, cudaStream_t s) {
+  if (n <= 0) return;
+  k_import<T><<<grid_for(n), kThreads, 0, s>>>(dst, src, map, n, nc, oriented);
+  count_launch();
+}
+template <class T>
+void launch_export(double* dst, const T* src, const int32_t* map, int64_t n, int nc, bool oriented, cudaStream_t s) {
+  if (n <= 0) return;
+  k_export<T><<<grid_for(n), kThreads, 0, s>>>(dst, src, map, n, nc, oriented);
+  count_launch();
+}
+
+// ------------------------------------------------------------ interpolate
+// phi_f = w phi_O + (1 - w) phi_N; boundary: fixed value or phi_O;
+// empty faces: 0.  Face-parallel (coalesced over the face records).
+template <class T, int NC>
+__global__ void k_interp(DevMesh<T> M, const T* __restrict__ x, const uint8_t* __restrict__ bkind,
+                         const T* __restrict__ bval, T* __restrict__ xf) {
+  const int64_t total = (int64_t)M.F + M.B + M.E;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < M.F) {
+      const int2 c = __ldg(&M.fcell[i]);
+      const T w = ld4(&M.fgeo[i]).w;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) xf[i * NC + k] = w * x[(int64_t)c.x * NC + k] + (T(1) - w) * x[(int64_t)c.y * NC + k];
+    } else if (i < (int64_t)M.F + M.B) {
+      const int b = (int)(i - M.F);
+      const int o = M.bcell[b];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) xf[i * NC + k] = bkind[b] ? x[(int64_t)o * NC + k] : bval[(int64_t)b * NC + k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < NC; ++k) xf[i * NC + k] = T(0);
+    }
+  }
+}
+
+// ------------------------------------------------------------ Gauss grad
+// G_c = (1/V_c) [sum_f s_cf phi_f S_f + sum_b phi_b S_b] (eq:gauss_green
+// P:207-213), G[c][k][l] = d phi^k / d x^l.
+template <class T, int NC, bool FACEVALS>
+__global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __restrict__ x,
+                                                   const uint8_t* __restrict__ bkind, const T* __restrict__ bval,
+                                                   const T* __restrict__ fv, T* __restrict__ G) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.n_slices; s += nw) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    T xc[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) xc[k] = (!FACEVALS && live) ? x[(int64_t)row * NC + k] : T(0);
+    T acc[NC][3];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) acc[k][0] = acc[k][1] = acc[k][2] = T(0);
+    const int len = __ldg(&M.sl_len[s]);
+    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+    for (int j = 0; j < len; ++j) {
+      const int2 en = __ldg(&e[j * 32]);
+      if (en.y >= 0) {
+        const bool own = en.x >= 0;
+        const int f = own ? en.x : ~en.x;
+        const V4<T> g = ld4(&M.fgeo[f]);
+        const T sg = own ? T(1) : T(-1);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          T pf;
+          if (FACEVALS) {
+            pf = fv[(int64_t)f * NC + k];
+          } else {
+            const T xn = x[(int64_t)en.y * NC + k];
+            const T xO = own ? xc[k] : xn, xN = own ? xn : xc[k];
+            pf = g.w * xO + (T(1) - g.w) * xN;
+          }
+          acc[k][0] += sg * pf * g.x; acc[k][1] += sg * pf * g.y; acc[k][2] += sg * pf * g.z;
+        }
+      } else if (en.y == -1) {
+        const int b = en.x;
+        const V4<T> g = ld4(&M.bgeo[b]);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          T pb;
+          if (FACEVALS) pb = fv[((int64_t)M.F + b) * NC + k];
+          else pb = bkind[b] ? xc[k] : bval[(int64_t)b * NC + k];
+          acc[k][0] += pb * g.x; acc[k][1] += pb * g.y; acc[k][2] += pb * g.z;
+        }
+      }
+    }
+    if (live) {
+      const T V = M.vol[row];
+#pragma unroll
+      for (int k = 0; k < NC; ++k)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) G[(int64_t)row * 3 * NC + 3 * k + l] = acc[k][l] / V;
+    }
+  }
+}
+
+// ------------------------------------------------------------ divergence
+// D_c = sum_f s_cf F_f + sum_b F_b (not divided by V)
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_div(DevMesh<T> M, const T* __restrict__ flux, T* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.n_slices; s += nw) {
+    const int row = s * 32 + lane;
+    T acc = T(0);
+    const int len = __ldg(&M.sl_len[s]);
+    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+    for (int j = 0; j < len; ++j) {
+      const int2 en = __ldg(&e[j * 32]);
+      if (en.y >= 0) {
+        if (en.x >= 0) acc += flux[en.x]; else acc -= flux[~en.x];
+      } else if (en.y == -1) {
+        acc += flux[M.F + en.x];
+      }
+    }
+    if (row < M.n_own) out[row] = acc;
+  }
+}
+
+// ------------------------------------------------------------ Laplacian
+// y_c = sum_f s_cf gamma_f [delta_f (x_N - x_O) + k_f . (w G_O + (1-w) G_N)]
+//     + sum_{b fixed} gamma_c delta_b (x_b - x_c)   (eq:nonortho_flux P:240-250)
+template <class T, bool GAMMA>
+__global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restrict__ gamma, const T* __restrict__ x,
+                                                  const T* __restrict__ G, const uint8_t* __restrict__ bkind,
+                                                  const T* __restrict__ bval, T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.n_slices; s += nw) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    const T xc = live ? x[row] : T(0);
+    const T gc = (GAMMA && live) ? gamma[row] : T(1);
+    T Gc[3] = {T(0), T(0), T(0)};
+    if (live) { Gc[0] = G[3 * (int64_t)row]; Gc[1] = G[3 * (int64_t)row + 1]; Gc[2] = G[3 * (int64_t)row + 2]; }
+    T acc = T(0);
+    const int len = __ldg(&M.sl_len[s]);
+    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+    for (int j = 0; j < len; ++j) {
+      const int2 en = __ldg(&e[j * 32]);
+      if (en.y >= 0) {
+        const bool own = en.x >= 0;
+        const int f = own ? en.x : ~en.x;
+        const int n = en.y;
+        const T w = ld4(&M.fgeo[f]).w;
+        const V4<T> c = ld4(&M.fcor[f]);
+        const T xn = x[n];
+        const T Gn0 = G[3 * (int64_t)n], Gn1 = G[3 * (int64_t)n + 1], Gn2 = G[3 * (int64_t)n + 2];
+        const T wO = w, wN = T(1) - w;
+        // owner / neighbour assignment for this face
+        const T xO = own ? xc : xn, xN = own ? xn : xc;
+        const T GO0 = own ? Gc[0] : Gn0, GO1 = own ? Gc[1] : Gn1, GO2 = own ? Gc[2] : Gn2;
+        const T GN0 = own ? Gn0 : Gc[0], GN1 = own ? Gn1 : Gc[1], GN2 = own ? Gn2 : Gc[2];
+        T gf = T(1);
+        if (GAMMA) {
+          const T gn = gamma[n];
+          gf = wO * (own ? gc : gn) + wN * (own ? gn : gc);
+        }
+        const T corr = c.x * (wO * GO0 + wN * GN0) + c.y * (wO * GO1 + wN * GN1) + c.z * (wO * GO2 + wN * GN2);
+        const T q = gf * (c.w * (xN - xO) + corr);
+        acc += own ? q : -q;
+      } else if (en.y == -1) {
+        const int b = en.x;
+        if (bkind[b] == 0) {
+          const T db = ld4(&M.bgeo[b]).w;
+          acc += gc * db * (bval[b] - xc);
+        }
+      }
+    }
+    if (live) y[row] = acc;
+  }
+}
+
+// ------------------------------------------------------------ launchers
+template <class T>
+void launch_interpolate(const DevMesh<T>& M, const T* x, int nc, const uint8_t* bk, const T* bv, T* xf, cudaStream_t s) {
+  const int g = grid_for((int64_t)M.F + M.B + M.E);
+  if (nc == 1) k_interp<T, 1><<<g, kThreads, 0, s>>>(M, x, bk, bv, xf);
+  else k_interp<T, 3><<<g, kThreads, 0, s>>>(M, x, bk, bv, xf);
+  count_launch();
+}
+template <class T>
+void launch_grad(const DevMesh<T>& M, const T* x, int nc, const uint8_t* bk, const T* bv, T* G, cudaStream_t s) {
+  const int g = grid_for_slices(M.n_slices);
+  if (nc == 1) k_grad<T, 1, false><<<g, kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
+  else k_grad<T, 3, false><<<g, kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
+  count_launch();
+}
+template <class T>
+void launch_grad_faces(const DevMesh<T>& M, const T* fv, int nc, T* G, cudaStream_t s) {
+  const int g = grid_for_slices(M.n_slices);
+  if (nc == 1) k_grad<T, 1, true><<<g, kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
+  else k_grad<T, 3, true><<<g, kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
+  count_launch();
+}
+template <class T>
+void launch_div(const DevMesh<T>& M, const T* flux, T* out, cudaStream_t s) {
+  k_div<T><<<grid_for_slices(M.n_slices), kThreads, 0, s>>>(M, flux, out);
+  count_launch();
+}
+template <class T>
+void launch_laplacian(const DevMesh<T>& M, const T* gamma, const T* x, const T* G, const uint8_t* bk, const T* bv,
+                      T* y, cudaStream_t s) {
+  const int g = grid_for_slices(M.n_slices);
+  if (gamma) k_lap<T, true><<<g, kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+  else k_lap<T, false><<<g, kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+  count_launch();
+}
+
+#define INST(T)                                                                                          \
+  template void launch_import<T>(T*, const double*, const int32_t*, int64_t, int, bool, cudaStream_t);   \
+  template void launch_export<T>(double*, const T*, const int32_t*, int64_t, int, bool, cudaStream_t);   \
+  template void launch_interpolate<T>(const DevMesh<T>&, const T*, int, const uint8_t*, const T*, T*,    \
+                                      cudaStream_t);                                                     \
+  template void launch_grad<T>(const DevMesh<T>&, const T*, int, const uint8_t*, const T*, T*, cudaStream_t); \
+  template void launch_grad_faces<T>(const DevMesh<T>&, const T*, int, T*, cudaStream_t);                \
+  template void launch_div<T>(const DevMesh<T>&, const T*, T*, cudaStream_t);                            \
+  template void launch_laplacian<T>(const DevMesh<T>&, const T*, const T*, const T*, const uint8_t*,     \
+                                    const T*, T*, cudaStream_t);
+INST(double)
+INST(float)
+
+}  // namespace dfvm
+
+namespace dfvm {
+// halo pack: buf[i][k] = x[idx[i]][k]  (send list of owned interface cells)
+template <class T>
+__global__ void k_pack(T* __restrict__ buf, const T* __restrict__ x, const int32_t* __restrict__ idx, int64_t n, int nc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < nc; ++k) buf[i * nc + k] = x[(int64_t)idx[i] * nc + k];
+}
+template <class T>
+void launch_pack(T* buf, const T* x, const int32_t* idx, int64_t n, int nc, cudaStream_t s) {
+  if (n <= 0) return;
+  k_pack<T><<<grid_for(n), kThreads, 0, s>>>(buf, x, idx, n, nc);
+  count_launch();
+}
+template void launch_pack<double>(double*, const double*, const int32_t*, int64_t, int, cudaStream_t);
+template void launch_pack<float>(float*, const float*, const int32_t*, int64_t, int, cudaStream_t);
+}  // namespace dfvm

@@ -1,0 +1,1261 @@
+// solver.cu — the PISO step on B200 (PAPER.md
+// §2.4.2, Table 1): momentum LDU assembly, 3-component
+// BiCGStab predictor, H / rAU / HbyA, phiHbyA, pressure coefficients, the
+// Jacobi-PCG pressure solve, Rhie-Chow flux correction, velocity correction,
+// Windkessel outlets and the continuity diagnostic.
+//
+// Krylov control runs on the device: every reduction is a deterministic
+// two-level sum (block partials in block order, then the last block to
+// arrive sums them in a fixed order) and that last block updates the solver
+// scalars (alpha, beta, residual, convergence, stagnation) in a device
+// control block.  Every Krylov kernel first checks the control block and
+// exits when the solve is done, so the host enqueues iterations in chunks
+// and reads the control block once per chunk (no per-iteration host sync).
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dev.cuh"
+#include "launch.h"
+
+namespace dfvm {
+
+dfvm_status halo_exchange(dfvm_mesh* m, void* data, int nc, cudaStream_t s);
+
+// -------------------------------------------------------------- control
+struct KCtl {
+  double bnorm, res0, res, thr, best;
+  double rz, alpha, beta;                 // CG
+  double rho, rho_old, omega, snorm;       // BiCGStab (alpha shared)
+  double tol, rel_tol;
+  int it, best_it, maxit, done, converged, status, zero_x, half;
+};
+
+struct WKDev {
+  double Rp, C, Rd, pc_n, pc_new, Q, p_o;
+  int scheme, pad;
+};
+
+// stopping rule (A-13): called by the last block after each residual update
+__device__ __forceinline__ void krylov_check(KCtl& c, double res) {
+  c.res = res;
+  if (res <= c.thr) { c.converged = 1; c.done = 1; return; }
+  if (res < c.best) { c.best = res; c.best_it = c.it; }
+  else if (c.it - c.best_it >= 50) { c.done = 1; c.status = DFVM_E_NOT_CONVERGED; return; }
+  if (c.it >= c.maxit) { c.done = 1; c.status = DFVM_E_NOT_CONVERGED; }
+}
+__device__ __forceinline__ void krylov_start(KCtl& c, double bb, double rr) {
+  c.bnorm = sqrt(bb);
+  c.res0 = c.res = c.best = sqrt(rr);
+  c.thr = fmax(c.tol * c.bnorm, c.rel_tol * c.res0);
+  c.it = 0; c.best_it = 0; c.converged = 0; c.status = 0; c.zero_x = 0; c.half = 0; c.done = 0;
+  if (c.bnorm == 0.0) { c.zero_x = 1; c.done = 1; c.converged = 1; c.res0 = c.res = 0; return; }
+  if (c.res0 <= c.thr) { c.done = 1; c.converged = 1; }
+}
+
+// y_row = diag_row x_row + sum_j coef_j x_nb(j) over the matrix SELL entries
+template <class T, int NC>
+__device__ __forceinline__ void sell_apply(const DevMesh<T>& M, int s, int lane, const T* __restrict__ coef,
+                                           const T* __restrict__ x, T (&acc)[NC]) {
+  const int len = __ldg(&M.ms_len[s]);
+  const int base = __ldg(&M.ms_ptr[s]) + lane;
+  for (int j = 0; j < len; ++j) {
+    const int idx = base + 32 * j;
+    const T a = coef[idx];
+    const int n = __ldg(&M.mnb[idx]);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) acc[k] += a * x[(int64_t)n * NC + k];
+  }
+}
+
+#define SLICE_LOOP(M)                                                                      \
+  const int lane = threadIdx.x & 31;                                                       \
+  const int nw_ = (gridDim.x * blockDim.x) >> 5;                                           \
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < (M).n_slices; s += nw_)
+
+// ============================================================ momentum
+// O-5: diag, b (time + BC + explicit non-orthogonal terms), rhsU = b - V grad p,
+// SELL coefficients (upper for the owner side, lower for the neighbour side).
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_mom_assemble(DevMesh<T> M, const T* __restrict__ U,
+    const T* __restrict__ phi, const T* __restrict__ gU, const T* __restrict__ gp, const uint8_t* __restrict__ bk,
+    const T* __restrict__ bv, T nu, T rdt, int upwind, int kcorr, T* __restrict__ udiag, T* __restrict__ bU,
+    T* __restrict__ rhsU, T* __restrict__ ucoef) {
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    const T V = live ? M.vol[row] : T(0);
+    T diag = V * rdt;
+    T b0 = T(0), b1 = T(0), b2 = T(0);
+    if (live) { b0 = diag * U[3 * (int64_t)row]; b1 = diag * U[3 * (int64_t)row + 1]; b2 = diag * U[3 * (int64_t)row + 2]; }
+    const int len = __ldg(&M.sl_len[s]);
+    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+    const int mbase = __ldg(&M.ms_ptr[s]) + lane;
+    int mj = 0;
+    for (int j = 0; j < len; ++j) {
+      const int2 en = __ldg(&e[j * 32]);
+      if (en.y >= 0) {
+        const bool own = en.x >= 0;
+        const int f = own ? en.x : ~en.x;
+        const T w = ld4(&M.fgeo[f]).w;
+        const V4<T> c = ld4(&M.fcor[f]);
+        const T md = phi[f];
+        const T lam = upwind ? (md >= T(0) ? T(1) : T(0)) : w;
+        const T nd = nu * c.w;
+        T cf;
+        if (own) { diag += lam * md + nd; cf = (T(1) - lam) * md - nd; }
+        else { diag += -(T(1) - lam) * md + nd; cf = -lam * md - nd; }
+        ucoef[mbase + 32 * (mj++)] = cf;
+        if (kcorr) {
+          const int n = en.y;
+          const int O = own ? row : n, N = own ? n : row;
+          const T* GO = gU + 9 * (int64_t)O;
+          const T* GN = gU + 9 * (int64_t)N;
+          T cr[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            cr[k] = nu * (c.x * (w * GO[3 * k] + (T(1) - w) * GN[3 * k]) +
+                          c.y * (w * GO[3 * k + 1] + (T(1) - w) * GN[3 * k + 1]) +
+                          c.z * (w * GO[3 * k + 2] + (T(1) - w) * GN[3 * k + 2]));
+          if (own) { b0 += cr[0]; b1 += cr[1]; b2 += cr[2]; }
+          else { b0 -= cr[0]; b1 -= cr[1]; b2 -= cr[2]; }
+        }
+      } else if (en.y == -1) {
+        const int b = en.x;
+        const T mb = phi[M.F + b];
+        if (bk[b] == 0) {
+          const T nd = nu * ld4(&M.bgeo[b]).w;
+          const T u0 = bv[3 * (int64_t)b], u1 = bv[3 * (int64_t)b + 1], u2 = bv[3 * (int64_t)b + 2];
+          diag += nd;
+          b0 += -mb * u0 + nd * u0; b1 += -mb * u1 + nd * u1; b2 += -mb * u2 + nd * u2;
+        } else {
+          diag += mb;
+        }
+      }
+    }
+    if (live) {
+      udiag[row] = diag;
+      bU[3 * (int64_t)row] = b0; bU[3 * (int64_t)row + 1] = b1; bU[3 * (int64_t)row + 2] = b2;
+      rhsU[3 * (int64_t)row] = b0 - V * gp[3 * (int64_t)row];
+      rhsU[3 * (int64_t)row + 1] = b1 - V * gp[3 * (int64_t)row + 1];
+      rhsU[3 * (int64_t)row + 2] = b2 - V * gp[3 * (int64_t)row + 2];
+    }
+  }
+}
+
+template <class T, int NC>
+__global__ void __launch_bounds__(kThreads) k_apply(DevMesh<T> M, const T* __restrict__ diag,
+    const T* __restrict__ coef, const T* __restrict__ x, T* __restrict__ y) {
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    T acc[NC];
+    const T d = live ? diag[row] : T(0);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) acc[k] = live ? d * x[(int64_t)row * NC + k] : T(0);
+    sell_apply<T, NC>(M, s, lane, coef, x, acc);
+    if (live)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) y[(int64_t)row * NC + k] = acc[k];
+  }
+}
+
+// H = b - sum_nb a U_nb; rAU = V / a_P; HbyA = H / a_P (eq:Ap_H P:333-335)
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_HbyA(DevMesh<T> M, const T* __restrict__ bU, const T* __restrict__ udiag,
+    const T* __restrict__ ucoef, const T* __restrict__ U, T* __restrict__ rAU, T* __restrict__ HbyA) {
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    T acc[3] = {T(0), T(0), T(0)};
+    sell_apply<T, 3>(M, s, lane, ucoef, U, acc);
+    if (live) {
+      const T d = udiag[row];
+      rAU[row] = M.vol[row] / d;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) HbyA[3 * (int64_t)row + k] = (bU[3 * (int64_t)row + k] - acc[k]) / d;
+    }
+  }
+}
+
+// phiHbyA_f = interp(HbyA) . S_f; boundary: U_b . S_b (fixed U) or HbyA_O . S_b
+template <class T>
+__global__ void k_phiHbyA(DevMesh<T> M, const T* __restrict__ HbyA, const uint8_t* __restrict__ bk,
+                          const T* __restrict__ bv, T* __restrict__ out) {
+  const int64_t total = (int64_t)M.F + M.B;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < M.F) {
+      const int2 c = __ldg(&M.fcell[i]);
+      const V4<T> g = ld4(&M.fgeo[i]);
+      const T* a = HbyA + 3 * (int64_t)c.x;
+      const T* b = HbyA + 3 * (int64_t)c.y;
+      out[i] = (g.w * a[0] + (T(1) - g.w) * b[0]) * g.x + (g.w * a[1] + (T(1) - g.w) * b[1]) * g.y +
+               (g.w * a[2] + (T(1) - g.w) * b[2]) * g.z;
+    } else {
+      const int b = (int)(i - M.F);
+      const V4<T> g = ld4(&M.bgeo[b]);
+      const T* h = bk[b] ? HbyA + 3 * (int64_t)M.bcell[b] : bv + 3 * (int64_t)b;
+      out[i] = h[0] * g.x + h[1] * g.y + h[2] * g.z;
+    }
+  }
+}
+
+// pressure coefficients (eq:pressure_poisson LHS; A-8): pcoef = -c_f,
+// pdiag = sum c_f + sum c_b, prhs0 = -D(phiHbyA) + sum c_b p_b, gauge (A-12)
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_pcoef(DevMesh<T> M, const T* __restrict__ rAU,
+    const T* __restrict__ phiHbyA, const uint8_t* __restrict__ bkp, const T* __restrict__ bvp, int ref_row,
+    T p_ref, T* __restrict__ pcoef, T* __restrict__ pdiag, T* __restrict__ prhs0) {
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    const T ra = live ? rAU[row] : T(0);
+    T diag = T(0), rhs = T(0);
+    const int len = __ldg(&M.sl_len[s]);
+    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+    const int mbase = __ldg(&M.ms_ptr[s]) + lane;
+    int mj = 0;
+    for (int j = 0; j < len; ++j) {
+      const int2 en = __ldg(&e[j * 32]);
+      if (en.y >= 0) {
+        const bool own = en.x >= 0;
+        const int f = own ? en.x : ~en.x;
+        const T w = ld4(&M.fgeo[f]).w;
+        const T d = ld4(&M.fcor[f]).w;
+        const T rn = rAU[en.y];
+        const T cf = (w * (own ? ra : rn) + (T(1) - w) * (own ? rn : ra)) * d;
+        pcoef[mbase + 32 * (mj++)] = -cf;
+        diag += cf;
+        rhs -= own ? phiHbyA[f] : -phiHbyA[f];
+      } else if (en.y == -1) {
+        const int b = en.x;
+        rhs -= phiHbyA[M.F + b];
+        if (bkp[b] == 0) {
+          const T cb = ra * ld4(&M.bgeo[b]).w;
+          diag += cb;
+          rhs += cb * bvp[b];
+        }
+      }
+    }
+    if (live) {
+      if (row == ref_row) { rhs += diag * p_ref; diag = diag + diag; }
+      pdiag[row] = diag;
+      prhs0[row] = rhs;
+    }
+  }
+}
+
+// prhs = prhs0 + sum_f s_cf rAU_f k_f . (grad p)_f  (explicit non-orthogonal part)
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_prhs(DevMesh<T> M, const T* __restrict__ rAU, const T* __restrict__ gp,
+    const T* __restrict__ prhs0, T* __restrict__ prhs) {
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    const T ra = live ? rAU[row] : T(0);
+    T acc = live ? prhs0[row] : T(0);
+    const T* Gc = gp + 3 * (int64_t)(live ? row : 0);
+    const int len = __ldg(&M.sl_len[s]);
+    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+    for (int j = 0; j < len; ++j) {
+      const int2 en = __ldg(&e[j * 32]);
+      if (en.y < 0) continue;
+      const bool own = en.x >= 0;
+      const int f = own ? en.x : ~en.x;
+      const int n = en.y;
+      const T w = ld4(&M.fgeo[f]).w;
+      const V4<T> c = ld4(&M.fcor[f]);
+      const T rn = rAU[n];
+      const T* Gn = gp + 3 * (int64_t)n;
+      const T* GO = own ? Gc : Gn;
+      const T* GN = own ? Gn : Gc;
+      const T rf = w * (own ? ra : rn) + (T(1) - w) * (own ? rn : ra);
+      const T kg = c.x * (w * GO[0] + (T(1) - w) * GN[0]) + c.y * (w * GO[1] + (T(1) - w) * GN[1]) +
+                   c.z * (w * GO[2] + (T(1) - w) * GN[2]);
+      acc += own ? rf * kg : -(rf * kg);
+    }
+    if (live) prhs[row] = acc;
+  }
+}
+
+// Rhie-Chow flux correction (A-9)
+template <class T>
+__global__ void k_fluxcorr(DevMesh<T> M, const T* __restrict__ phiHbyA, const T* __restrict__ p,
+                           const T* __restrict__ rAU, const T* __restrict__ gp, const uint8_t* __restrict__ bkp,
+                           const T* __restrict__ bvp, int kcorr, T* __restrict__ phi) {
+  const int64_t total = (int64_t)M.F + M.B;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < M.F) {
+      const int2 cc = __ldg(&M.fcell[i]);
+      const T w = ld4(&M.fgeo[i]).w;
+      const V4<T> c = ld4(&M.fcor[i]);
+      const T rf = w * rAU[cc.x] + (T(1) - w) * rAU[cc.y];
+      T v = phiHbyA[i] - rf * c.w * (p[cc.y] - p[cc.x]);
+      if (kcorr) {
+        const T* GO = gp + 3 * (int64_t)cc.x;
+        const T* GN = gp + 3 * (int64_t)cc.y;
+        const T kg = c.x * (w * GO[0] + (T(1) - w) * GN[0]) + c.y * (w * GO[1] + (T(1) - w) * GN[1]) +
+                     c.z * (w * GO[2] + (T(1) - w) * GN[2]);
+        v -= rf * kg;
+      }
+      phi[i] = v;
+    } else {
+      const int b = (int)(i - M.F);
+      if (bkp[b] == 0) {
+        const int o = M.bcell[b];
+        const T cb = rAU[o] * ld4(&M.bgeo[b]).w;
+        phi[i] = phiHbyA[i] - cb * (bvp[b] - p[o]);
+      } else {
+        phi[i] = phiHbyA[i];
+      }
+    }
+  }
+}
+
+// U = HbyA - rAU grad p with the Gauss gradient of the new p (eq:velocity_correction
+// P:344-346); the gradient is stored for the next corrector / step.
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_Ucorr(DevMesh<T> M, const T* __restrict__ p,
+    const uint8_t* __restrict__ bkp, const T* __restrict__ bvp, const T* __restrict__ HbyA,
+    const T* __restrict__ rAU, T* __restrict__ U, T* __restrict__ gp) {
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    const T pc = live ? p[row] : T(0);
+    T a0 = T(0), a1 = T(0), a2 = T(0);
+    const int len = __ldg(&M.sl_len[s]);
+    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+    for (int j = 0; j < len; ++j) {
+      const int2 en = __ldg(&e[j * 32]);
+      if (en.y >= 0) {
+        const bool own = en.x >= 0;
+        const int f = own ? en.x : ~en.x;
+        const V4<T> g = ld4(&M.fgeo[f]);
+        const T pn = p[en.y];
+        const T pf = g.w * (own ? pc : pn) + (T(1) - g.w) * (own ? pn : pc);
+        const T sp = own ? pf : -pf;
+        a0 += sp * g.x; a1 += sp * g.y; a2 += sp * g.z;
+      } else if (en.y == -1) {
+        const int b = en.x;
+        const V4<T> g = ld4(&M.bgeo[b]);
+        const T pb = bkp[b] ? pc : bvp[b];
+        a0 += pb * g.x; a1 += pb * g.y; a2 += pb * g.z;
+      }
+    }
+    if (live) {
+      const T V = M.vol[row];
+      const T g0 = a0 / V, g1 = a1 / V, g2 = a2 / V;
+      gp[3 * (int64_t)row] = g0; gp[3 * (int64_t)row + 1] = g1; gp[3 * (int64_t)row + 2] = g2;
+      const T r = rAU[row];
+      U[3 * (int64_t)row] = HbyA[3 * (int64_t)row] - r * g0;
+      U[3 * (int64_t)row + 1] = HbyA[3 * (int64_t)row + 1] - r * g1;
+      U[3 * (int64_t)row + 2] = HbyA[3 * (int64_t)row + 2] - r * g2;
+    }
+  }
+}
+
+// continuity max_c |D_c(phi)|, sum_c |D_c(phi)|, non-finite flag; the last
+// block also commits the Windkessel states of the step (p_c^n <- p_c^{n+1}).
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_continuity(DevMesh<T> M, const T* __restrict__ phi,
+    const T* __restrict__ U, const T* __restrict__ p, double* partials, unsigned* ticket, double* out,
+    WKDev* wk, int n_wk) {
+  double mx = 0, sm = 0, nf = 0;
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    T acc = T(0);
+    const int len = __ldg(&M.sl_len[s]);
+    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+    for (int j = 0; j < len; ++j) {
+      const int2 en = __ldg(&e[j * 32]);
+      if (en.y >= 0) { if (en.x >= 0) acc += phi[en.x]; else acc -= phi[~en.x]; }
+      else if (en.y == -1) acc += phi[M.F + en.x];
+    }
+    if (row < M.n_own) {
+      const double a = fabs((double)acc);
+      mx = fmax(mx, a);
+      sm += a;
+      const T u0 = U[3 * (int64_t)row], u1 = U[3 * (int64_t)row + 1], u2 = U[3 * (int64_t)row + 2];
+      if (!isfinite((double)u0) || !isfinite((double)u1) || !isfinite((double)u2) || !isfinite((double)p[row])) nf = 1;
+    }
+  }
+  // max via the sum machinery: reduce (sum, nonfinite) and max separately
+  __shared__ double shm[32];
+  double wm = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) shm[threadIdx.x >> 5] = wm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b = fmax(b, shm[w]);
+    mx = b;
+  }
+  double v[2] = {sm, nf}, tot[2];
+  const double* maxp = partials + 2 * gridDim.x;
+  if (threadIdx.x == 0) const_cast<double*>(maxp)[blockIdx.x] = mx;
+  if (grid_sum<2>(v, partials, ticket, tot)) {
+    double m2 = 0;
+    for (unsigned b = 0; b < gridDim.x; ++b) m2 = fmax(m2, __ldcg(&maxp[b]));
+    out[0] = m2; out[1] = tot[0]; out[2] = tot[1] > 0 ? 1.0 : 0.0;
+    for (int i = 0; i < n_wk; ++i) wk[i].pc_n = wk[i].pc_new;
+  }
+}
+
+// Windkessel (eq:windkessel_Q P:406-410, eq:windkessel_discrete P:420-425):
+// one block per outlet; Q = sum_b phi_b (fixed order), p_c^{n+1} from the
+// start-of-step p_c^n (A-19), p_o = p_c + R_p Q, BC value p_o / rho.
+template <class T>
+__global__ void k_windkessel(DevMesh<T> M, const T* __restrict__ phi, WKDev* wk, const int* __restrict__ fptr,
+                             const int* __restrict__ faces, double dt, double rho, T* __restrict__ bvp) {
+  const int o = blockIdx.x;
+  double q = 0;
+  for (int i = fptr[o] + threadIdx.x; i < fptr[o + 1]; i += blockDim.x) q += (double)phi[M.F + faces[i]];
+  __shared__ double sh[32][1];
+  double v[1] = {q};
+  block_sum<1>(v, sh);
+  __shared__ double po_s;
+  if (threadIdx.x == 0) {
+    WKDev& W = wk[o];
+    const double Q = v[0];
+    double pc;
+    if (W.scheme == 0) { const double ex = exp(-dt / (W.Rd * W.C)); pc = W.pc_n * ex + W.Rd * Q * (1.0 - ex); }
+    else if (W.scheme == 1) pc = W.pc_n + dt * (Q - W.pc_n / W.Rd) / W.C;
+    else pc = (W.pc_n + dt * Q / W.C) / (1.0 + dt / (W.Rd * W.C));
+    W.pc_new = pc; W.Q = Q; W.p_o = pc + W.Rp * Q;
+    po_s = W.p_o / rho;
+  }
+  __syncthreads();
+  for (int i = fptr[o] + threadIdx.x; i < fptr[o + 1]; i += blockDim.x) bvp[faces[i]] = (T)po_s;
+}
+
+template <class T>
+__global__ void k_add_at(T* a, const T* b, int i) { a[i] += b[i]; }
+
+// ============================================================ Jacobi PCG
+// r = b - A x; partials b.b, r.r, r.z  -> control start
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_cg_init(DevMesh<T> M, const T* __restrict__ diag,
+    const T* __restrict__ coef, const T* __restrict__ b, const T* __restrict__ x, T* __restrict__ r,
+    double* partials, unsigned* ticket, KCtl* ctl) {
+  double v[3] = {0, 0, 0};
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    T acc[1] = {live ? diag[row] * x[row] : T(0)};
+    sell_apply<T, 1>(M, s, lane, coef, x, acc);
+    if (live) {
+      const T rr = b[row] - acc[0];
+      r[row] = rr;
+      v[0] += (double)b[row] * (double)b[row];
+      v[1] += (double)rr * (double)rr;
+      v[2] += (double)rr * (double)rr / (double)diag[row];
+    }
+  }
+  double t[3];
+  if (grid_sum<3>(v, partials, ticket, t)) {
+    KCtl& c = *ctl;
+    krylov_start(c, t[0], t[1]);
+    c.rz = t[2]; c.beta = 0.0;
+  }
+}
+
+// pd = r / diag + beta pd
+template <class T>
+__global__ void k_cg_pupd(int n, const T* __restrict__ r, const T* __restrict__ diag, T* __restrict__ pd,
+                          const KCtl* ctl) {
+  if (ctl->done) return;
+  const T beta = (T)ctl->beta;
+  const bool first = ctl->it == 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    pd[i] = first ? r[i] / diag[i] : r[i] / diag[i] + beta * pd[i];
+}
+
+// q = A pd; partial pd.q -> alpha
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_cg_spmv(DevMesh<T> M, const T* __restrict__ diag,
+    const T* __restrict__ coef, const T* __restrict__ pd, T* __restrict__ q, double* partials, unsigned* ticket,
+    KCtl* ctl) {
+  if (ctl->done) return;
+  double v[1] = {0};
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    T acc[1] = {live ? diag[row] * pd[row] : T(0)};
+    sell_apply<T, 1>(M, s, lane, coef, pd, acc);
+    if (live) { q[row] = acc[0]; v[0] += (double)pd[row] * (double)acc[0]; }
+  }
+  double t[1];
+  if (grid_sum<1>(v, partials, ticket, t)) {
+    KCtl& c = *ctl;
+    if (!(t[0] > 0)) { c.done = 1; c.status = DFVM_E_BREAKDOWN; c.it++; return; }
+    c.alpha = c.rz / t[0];
+  }
+}
+
+// x += alpha pd; r -= alpha q; partials r.r, r.z -> check, beta
+template <class T>
+__global__ void k_cg_update(int n, const T* __restrict__ pd, const T* __restrict__ q, const T* __restrict__ diag,
+                            T* __restrict__ x, T* __restrict__ r, double* partials, unsigned* ticket, KCtl* ctl) {
+  if (ctl->done) return;
+  const T alpha = (T)ctl->alpha;
+  double v[2] = {0, 0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    x[i] += alpha * pd[i];
+    const T rr = r[i] - alpha * q[i];
+    r[i] = rr;
+    v[0] += (double)rr * (double)rr;
+    v[1] += (double)rr * (double)rr / (double)diag[i];
+  }
+  double t[2];
+  if (grid_sum<2>(v, partials, ticket, t)) {
+    KCtl& c = *ctl;
+    c.it++;
+    krylov_check(c, sqrt(t[0]));
+    if (!c.done) { c.beta = t[1] / c.rz; c.rz = t[1]; }
+  }
+}
+
+// ============================================================ BiCGStab (3 components)
+// Right-preconditioned (Jacobi) van der Vorst BiCGStab, the three velocity
+// components advanced together over one coefficient stream; each component
+// keeps its own scalars and stops independently.
+__device__ __forceinline__ bool all_done(const KCtl* c) { return c[0].done && c[1].done && c[2].done; }
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_bi_init(DevMesh<T> M, const T* __restrict__ diag,
+    const T* __restrict__ coef, const T* __restrict__ b, const T* __restrict__ x, T* __restrict__ r,
+    T* __restrict__ rh, T* __restrict__ p, T* __restrict__ v, double* partials, unsigned* ticket, KCtl* ctl) {
+  double a[6] = {0, 0, 0, 0, 0, 0};
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    T acc[3];
+    const T d = live ? diag[row] : T(0);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) acc[k] = live ? d * x[3 * (int64_t)row + k] : T(0);
+    sell_apply<T, 3>(M, s, lane, coef, x, acc);
+    if (live)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int64_t i = 3 * (int64_t)row + k;
+        const T rr = b[i] - acc[k];
+        r[i] = rr; rh[i] = rr; p[i] = T(0); v[i] = T(0);
+        a[k] += (double)b[i] * (double)b[i];
+        a[3 + k] += (double)rr * (double)rr;
+      }
+  }
+  double t[6];
+  if (grid_sum<6>(a, partials, ticket, t)) {
+    for (int k = 0; k < 3; ++k) {
+      KCtl& c = ctl[k];
+      krylov_start(c, t[k], t[3 + k]);
+      c.rho_old = 1; c.alpha = 1; c.omega = 1; c.rho = t[3 + k];
+      if (!c.done && c.rho == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; }
+    }
+  }
+}
+
+// p = r + beta (p - omega v); y = p / diag
+template <class T>
+__global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ diag, const T* __restrict__ v,
+                       T* __restrict__ p, T* __restrict__ y, const KCtl* ctl) {
+  if (all_done(ctl)) return;
+  T beta[3], om[3];
+  bool act[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    act[k] = !ctl[k].done;
+    beta[k] = (T)((ctl[k].rho / ctl[k].rho_old) * (ctl[k].alpha / ctl[k].omega));
+    om[k] = (T)ctl[k].omega;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const T d = diag[i];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (!act[k]) continue;
+      const int64_t j = 3 * (int64_t)i + k;
+      const T pp = r[j] + beta[k] * (p[j] - om[k] * v[j]);
+      p[j] = pp;
+      y[j] = pp / d;
+    }
+  }
+}
+
+// v = A y; partial (rh, v) -> alpha
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_bi_v(DevMesh<T> M, const T* __restrict__ diag,
+    const T* __restrict__ coef, const T* __restrict__ y, const T* __restrict__ rh, T* __restrict__ v,
+    double* partials, unsigned* ticket, KCtl* ctl) {
+  if (all_done(ctl)) return;
+  double a[3] = {0, 0, 0};
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    T acc[3];
+    const T d = live ? diag[row] : T(0);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) acc[k] = live ? d * y[3 * (int64_t)row + k] : T(0);
+    sell_apply<T, 3>(M, s, lane, coef, y, acc);
+    if (live)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int64_t i = 3 * (int64_t)row + k;
+        v[i] = acc[k];
+        a[k] += (double)rh[i] * (double)acc[k];
+      }
+  }
+  double t[3];
+  if (grid_sum<3>(a, partials, ticket, t)) {
+    for (int k = 0; k < 3; ++k) {
+      KCtl& c = ctl[k];
+      if (c.done) continue;
+      c.it++;
+      if (t[k] == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; continue; }
+      c.alpha = c.rho / t[k];
+    }
+  }
+}
+
+// s = r - alpha v; partial (s, s) -> half-step convergence
+template <class T>
+__global__ void k_bi_s(int n, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ sv,
+                       double* partials, unsigned* ticket, KCtl* ctl) {
+  if (all_done(ctl)) return;
+  T al[3];
+  bool act[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { act[k] = !ctl[k].done; al[k] = (T)ctl[k].alpha; }
+  double a[3] = {0, 0, 0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (!act[k]) continue;
+      const int64_t j = 3 * (int64_t)i + k;
+      const T ss = r[j] - al[k] * v[j];
+      sv[j] = ss;
+      a[k] += (double)ss * (double)ss;
+    }
+  double t[3];
+  if (grid_sum<3>(a, partials, ticket, t)) {
+    for (int k = 0; k < 3; ++k) {
+      KCtl& c = ctl[k];
+      if (c.done) continue;
+      c.snorm = sqrt(t[k]);
+      if (c.snorm <= c.thr) c.half = 1;
+    }
+  }
+}
+
+// t = A (s / diag); partials (t, s), (t, t) -> omega
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_bi_t(DevMesh<T> M, const T* __restrict__ diag,
+    const T* __restrict__ coef, const T* __restrict__ sv, T* __restrict__ tv, double* partials, unsigned* ticket,
+    KCtl* ctl) {
+  if (all_done(ctl)) return;
+  double a[6] = {0, 0, 0, 0, 0, 0};
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    T acc[3] = {T(0), T(0), T(0)};
+    if (live)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) acc[k] = sv[3 * (int64_t)row + k];   // diag * (s / diag)
+    const int len = __ldg(&M.ms_len[s]);
+    const int base = __ldg(&M.ms_ptr[s]) + lane;
+    for (int j = 0; j < len; ++j) {
+      const int idx = base + 32 * j;
+      const T c = coef[idx];
+      const int nn = __ldg(&M.mnb[idx]);
+      const T dn = diag[nn];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) acc[k] += c * (sv[3 * (int64_t)nn + k] / dn);
+    }
+    if (live)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int64_t i = 3 * (int64_t)row + k;
+        tv[i] = acc[k];
+        a[k] += (double)acc[k] * (double)sv[i];
+        a[3 + k] += (double)acc[k] * (double)acc[k];
+      }
+  }
+  double t[6];
+  if (grid_sum<6>(a, partials, ticket, t)) {
+    for (int k = 0; k < 3; ++k) {
+      KCtl& c = ctl[k];
+      if (c.done || c.half) continue;
+      if (t[3 + k] == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; continue; }
+      c.omega = t[k] / t[3 + k];
+    }
+  }
+}
+
+// x += alpha y + omega s/diag; r = s - omega t; partials (rh, r), (r, r)
+template <class T>
+__global__ void k_bi_x(int n, const T* __restrict__ diag, const T* __restrict__ y, const T* __restrict__ sv,
+                       const T* __restrict__ tv, const T* __restrict__ rh, T* __restrict__ x, T* __restrict__ r,
+                       double* partials, unsigned* ticket, KCtl* ctl) {
+  if (all_done(ctl)) return;
+  T al[3], om[3];
+  int mode[3];   // 0 skip, 1 half step, 2 full step
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    mode[k] = ctl[k].done ? 0 : (ctl[k].half ? 1 : 2);
+    al[k] = (T)ctl[k].alpha; om[k] = (T)ctl[k].omega;
+  }
+  double a[6] = {0, 0, 0, 0, 0, 0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const T d = diag[i];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int64_t j = 3 * (int64_t)i + k;
+      if (mode[k] == 1) { x[j] += al[k] * y[j]; continue; }
+      if (mode[k] != 2) continue;
+      const T ss = sv[j];
+      x[j] += al[k] * y[j] + om[k] * (ss / d);
+      const T rr = ss - om[k] * tv[j];
+      r[j] = rr;
+      a[k] += (double)rh[j] * (double)rr;
+      a[3 + k] += (double)rr * (double)rr;
+    }
+  }
+  double t[6];
+  if (grid_sum<6>(a, partials, ticket, t)) {
+    for (int k = 0; k < 3; ++k) {
+      KCtl& c = ctl[k];
+      if (c.done) continue;
+      if (c.half) { c.res = c.snorm; c.converged = 1; c.done = 1; continue; }
+      krylov_check(c, sqrt(t[3 + k]));
+      if (c.done) continue;
+      if (c.omega == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; continue; }
+      c.rho_old = c.rho;
+      c.rho = t[k];
+      if (c.rho == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; }
+    }
+  }
+}
+
+// ============================================================ host side
+struct SolverBase {
+  virtual ~SolverBase() {}
+};
+
+template <class T>
+struct SolverT : SolverBase {
+  dfvm_mesh* m = nullptr;
+  DevMesh<T>* M = nullptr;
+  std::vector<void*> allocs;
+  T *gU = nullptr, *gp = nullptr, *bU = nullptr, *rhsU = nullptr, *udiag = nullptr, *ucoef = nullptr;
+  T *rAU = nullptr, *HbyA = nullptr, *phiHbyA = nullptr, *pcoef = nullptr, *pdiag = nullptr;
+  T *prhs0 = nullptr, *prhs = nullptr;
+  T *kr = nullptr, *krh = nullptr, *kp = nullptr, *kq = nullptr, *kv = nullptr, *ky = nullptr, *ks = nullptr, *kt = nullptr;
+  double* partials = nullptr;
+  unsigned* ticket = nullptr;
+  KCtl* d_ctl = nullptr;
+  KCtl* h_ctl = nullptr;   // pinned
+  double* d_cont = nullptr;
+  double* h_cont = nullptr;  // pinned
+  WKDev* d_wk = nullptr;
+  WKDev* h_wk = nullptr;     // pinned
+  int* d_wk_ptr = nullptr;
+  int* d_wk_faces = nullptr;
+  bool assembled = false;
+  ~SolverT() override {
+    for (void* p : allocs) cudaFree(p);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (h_cont) cudaFreeHost(h_cont);
+    if (h_wk) cudaFreeHost(h_wk);
+  }
+  template <class U>
+  dfvm_status al(U** p, size_t n) {
+    void* q = nullptr;
+    DFVM_CUDA(cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(U)));
+    DFVM_CUDA(cudaMemset(q, 0, std::max<size_t>(n, 1) * sizeof(U)));
+    allocs.push_back(q);
+    *p = (U*)q;
+    return DFVM_OK;
+  }
+  dfvm_status init(dfvm_mesh* mm, DevMesh<T>* MM) {
+    m = mm; M = MM;
+    const size_t nc = M->n_cells, no = M->n_own, nf = (size_t)M->F + M->B + M->E;
+    dfvm_status st;
+    if ((st = al(&gU, 9 * nc)) || (st = al(&gp, 3 * nc)) || (st = al(&bU, 3 * no)) || (st = al(&rhsU, 3 * no)) ||
+        (st = al(&udiag, nc)) || (st = al(&ucoef, (size_t)M->n_minc)) || (st = al(&rAU, nc)) ||
+        (st = al(&HbyA, 3 * nc)) || (st = al(&phiHbyA, nf)) || (st = al(&pcoef, (size_t)M->n_minc)) ||
+        (st = al(&pdiag, nc)) || (st = al(&prhs0, no)) || (st = al(&prhs, no)) || (st = al(&kr, 3 * nc)) ||
+        (st = al(&krh, 3 * nc)) || (st = al(&kp, 3 * nc)) || (st = al(&kq, 3 * nc)) || (st = al(&kv, 3 * nc)) ||
+        (st = al(&ky, 3 * nc)) || (st = al(&ks, 3 * nc)) || (st = al(&kt, 3 * nc)) ||
+        (st = al(&partials, (size_t)kMaxBlocks * 8)) || (st = al(&ticket, 4)) || (st = al(&d_ctl, 4)) ||
+        (st = al(&d_cont, 4)))
+      return st;
+    DFVM_CUDA(cudaMallocHost(&h_ctl, 4 * sizeof(KCtl)));
+    DFVM_CUDA(cudaMallocHost(&h_cont, 4 * sizeof(double)));
+    return DFVM_OK;
+  }
+};
+
+}  // namespace dfvm
+
+using namespace dfvm;
+
+struct dfvm_solver {
+  dfvm_mesh* m = nullptr;
+  dfvm_bcs* b = nullptr;
+  dfvm_piso_opts o{};
+  std::unique_ptr<SolverBase> impl;
+  int ref_row = -1;
+  bool fixed_p = false;
+  int kcorr = 1;
+  // Windkessel outlets (host description)
+  struct WK { int patch; double Rp, C, Rd, pc; int scheme; };
+  std::vector<WK> wk;
+  bool wk_dirty = true;
+  int n_launch = 0;
+};
+
+namespace dfvm {
+
+static bool solver_has_fixed_p(const dfvm_solver* S) {
+  const HostMesh& H = S->m->H;
+  for (size_t p = 0; p < H.pkind.size(); ++p)
+    if (H.pkind[p] != DFVM_PATCH_EMPTY && S->b->set[1][p] &&
+        (S->b->spec[1][p].kind == DFVM_BC_FIXED_VALUE || S->b->spec[1][p].kind == DFVM_BC_WINDKESSEL))
+      return true;
+  return false;
+}
+
+template <class T>
+static dfvm_status sync_wk(dfvm_solver* S, SolverT<T>& X, cudaStream_t st) {
+  if (!S->wk_dirty) return DFVM_OK;
+  const Part& P = S->m->part;
+  const HostMesh& H = S->m->H;
+  const int n = (int)S->wk.size();
+  if (X.d_wk) { cudaFree(X.d_wk); cudaFree(X.d_wk_ptr); cudaFree(X.d_wk_faces); X.d_wk = nullptr; }
+  if (X.h_wk) { cudaFreeHost(X.h_wk); X.h_wk = nullptr; }
+  if (n) {
+    std::vector<int> ptr(n + 1, 0), faces;
+    for (int o = 0; o < n; ++o) {
+      for (int64_t b = 0; b < P.n_lb; ++b)
+        if (H.bpatch[P.lb_gid[b] - H.F] == S->wk[o].patch) faces.push_back((int)b);
+      ptr[o + 1] = (int)faces.size();
+    }
+    DFVM_CUDA(cudaMalloc(&X.d_wk, n * sizeof(WKDev)));
+    DFVM_CUDA(cudaMallocHost(&X.h_wk, n * sizeof(WKDev)));
+    DFVM_CUDA(cudaMalloc(&X.d_wk_ptr, (n + 1) * sizeof(int)));
+    DFVM_CUDA(cudaMalloc(&X.d_wk_faces, std::max<size_t>(faces.size(), 1) * sizeof(int)));
+    for (int o = 0; o < n; ++o) {
+      const auto& w = S->wk[o];
+      X.h_wk[o] = WKDev{w.Rp, w.C, w.Rd, w.pc, w.pc, 0.0, 0.0, w.scheme, w.patch};
+    }
+    DFVM_CUDA(cudaMemcpyAsync(X.d_wk, X.h_wk, n * sizeof(WKDev), cudaMemcpyHostToDevice, st));
+    DFVM_CUDA(cudaMemcpyAsync(X.d_wk_ptr, ptr.data(), (n + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (!faces.empty())
+      DFVM_CUDA(cudaMemcpyAsync(X.d_wk_faces, faces.data(), faces.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    DFVM_CUDA(cudaStreamSynchronize(st));
+  }
+  S->wk_dirty = false;
+  return DFVM_OK;
+}
+
+static void fill_report(const KCtl& c, dfvm_solve_report* r) {
+  r->it = c.it; r->res0 = c.res0; r->res = c.res; r->converged = c.converged;
+}
+
+constexpr int kChunk = 8;
+
+// Jacobi PCG on (pdiag, pcoef): x warm start, b rhs
+template <class T>
+static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol, int maxit,
+                          dfvm_solve_report* rep, cudaStream_t st) {
+  DevMesh<T>& M = *X.M;
+  const int gs = grid_for_slices(M.n_slices), ge = grid_for(M.n_own);
+  KCtl init{};
+  init.tol = tol; init.rel_tol = rel_tol; init.maxit = maxit;
+  DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, &init, sizeof(KCtl), cudaMemcpyHostToDevice, st));
+  if (dfvm_status s2 = halo_exchange(S->m, x, 1, st)) return s2;
+  k_cg_init<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr, X.partials, X.ticket, X.d_ctl);
+  S->n_launch++;
+  for (int it0 = 0;; it0 += kChunk) {
+    for (int k = 0; k < kChunk; ++k) {
+      k_cg_pupd<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.pdiag, X.kp, X.d_ctl);
+      k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl);
+      k_cg_update<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, X.kq, X.pdiag, x, X.kr, X.partials, X.ticket, X.d_ctl);
+      S->n_launch += 3;
+    }
+    DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
+    DFVM_CUDA(cudaStreamSynchronize(st));
+    if (X.h_ctl->done) break;
+  }
+  DFVM_CUDA(cudaGetLastError());
+  const KCtl& c = *X.h_ctl;
+  if (c.zero_x) DFVM_CUDA(cudaMemsetAsync(x, 0, (size_t)M.n_own * sizeof(T), st));
+  if (rep) fill_report(c, rep);
+  return (dfvm_status)(c.status == DFVM_E_BREAKDOWN ? DFVM_E_BREAKDOWN : (c.converged ? DFVM_OK : DFVM_E_NOT_CONVERGED));
+}
+
+// 3-component BiCGStab on (udiag, ucoef): x = U (warm start), b = rhsU
+template <class T>
+static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol,
+                                int maxit, dfvm_solve_report* rep, cudaStream_t st) {
+  DevMesh<T>& M = *X.M;
+  const int gs = grid_for_slices(M.n_slices), ge = grid_for(M.n_own);
+  KCtl init[3] = {};
+  for (int k = 0; k < 3; ++k) { init[k].tol = tol; init[k].rel_tol = rel_tol; init[k].maxit = maxit; }
+  DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, init, 3 * sizeof(KCtl), cudaMemcpyHostToDevice, st));
+  k_bi_init<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr, X.krh, X.kp, X.kv, X.partials, X.ticket, X.d_ctl);
+  S->n_launch++;
+  for (;;) {
+    for (int k = 0; k < kChunk; ++k) {
+      k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.udiag, X.kv, X.kp, X.ky, X.d_ctl);
+      k_bi_v<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.ky, X.krh, X.kv, X.partials, X.ticket, X.d_ctl);
+      k_bi_s<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.ks, X.partials, X.ticket, X.d_ctl);
+      k_bi_t<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.ks, X.kt, X.partials, X.ticket, X.d_ctl);
+      k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udiag, X.ky, X.ks, X.kt, X.krh, x, X.kr, X.partials, X.ticket, X.d_ctl);
+      S->n_launch += 5;
+    }
+    DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, 3 * sizeof(KCtl), cudaMemcpyDeviceToHost, st));
+    DFVM_CUDA(cudaStreamSynchronize(st));
+    if (X.h_ctl[0].done && X.h_ctl[1].done && X.h_ctl[2].done) break;
+  }
+  DFVM_CUDA(cudaGetLastError());
+  dfvm_status res = DFVM_OK;
+  for (int k = 0; k < 3; ++k) {
+    const KCtl& c = X.h_ctl[k];
+    if (rep) fill_report(c, &rep[k]);
+    if (c.status == DFVM_E_BREAKDOWN) res = DFVM_E_BREAKDOWN;
+    else if (!c.converged && res == DFVM_OK) res = DFVM_E_NOT_CONVERGED;
+  }
+  // b = 0 components: x = 0
+  for (int k = 0; k < 3; ++k)
+    if (X.h_ctl[k].zero_x) {
+      DFVM_CUDA(cudaMemset2DAsync((char*)x + k * sizeof(T), 3 * sizeof(T), 0, sizeof(T), M.n_own, st));
+    }
+  return res;
+}
+
+template <class T>
+static dfvm_status assemble(dfvm_solver* S, SolverT<T>& X, const T* U, const T* phi, cudaStream_t st) {
+  DevMesh<T>& M = *X.M;
+  dfvm_bcs* b = S->b;
+  dfvm_status s2;
+  if ((s2 = bcs_device(b, 0, st)) || (s2 = bcs_device(b, 1, st))) return s2;
+  if ((s2 = halo_exchange(S->m, (void*)U, 3, st))) return s2;
+  const int gs = grid_for_slices(M.n_slices);
+  launch_grad<T>(M, U, 3, b->d_kind[0], (const T*)b->d_val[0], X.gU, st);
+  S->n_launch++;
+  if ((s2 = halo_exchange(S->m, X.gU, 9, st))) return s2;
+  k_mom_assemble<T><<<gs, kThreads, 0, st>>>(M, U, phi, X.gU, X.gp, b->d_kind[0], (const T*)b->d_val[0],
+                                             (T)S->o.nu, (T)(1.0 / S->o.dt), S->o.convection == 0 ? 1 : 0,
+                                             S->kcorr, X.udiag, X.bU, X.rhsU, X.ucoef);
+  S->n_launch++;
+  X.assembled = true;
+  DFVM_CUDA(cudaGetLastError());
+  return DFVM_OK;
+}
+
+// O-6: one PISO step
+template <class T>
+static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_step_report* R, cudaStream_t st) {
+  DevMesh<T>& M = *X.M;
+  dfvm_bcs* b = S->b;
+  const dfvm_piso_opts& o = S->o;
+  dfvm_status s2;
+  S->n_launch = 0;
+  std::memset(R, 0, sizeof(*R));
+  if ((s2 = bcs_device(b, 0, st)) || (s2 = bcs_device(b, 1, st))) return s2;
+  if ((s2 = sync_wk(S, X, st))) return s2;
+  const int gs = grid_for_slices(M.n_slices), gf = grid_for((int64_t)M.F + M.B);
+  const uint8_t* bkU = b->d_kind[0];
+  const T* bvU = (const T*)b->d_val[0];
+  const uint8_t* bkp = b->d_kind[1];
+  T* bvp = (T*)b->d_val[1];
+  // grad p^n (predictor source)
+  if ((s2 = halo_exchange(S->m, p, 1, st))) return s2;
+  launch_grad<T>(M, p, 1, bkp, bvp, X.gp, st);
+  S->n_launch++;
+  // 1. momentum assembly from (U^n, phi^n, grad U^n)
+  if ((s2 = assemble(S, X, U, phi, st))) return s2;
+  // 2. predictor
+  dfvm_status res = run_bicgstab(S, X, X.rhsU, U, o.U_tol, o.U_rel_tol, o.U_maxit, R->U, st);
+  if (res == DFVM_E_BREAKDOWN) return res;
+  const int n_wk = (int)S->wk.size();
+  int np = 0;
+  for (int corr = 1; corr <= o.n_corr; ++corr) {
+    // 3.1 Windkessel
+    if (n_wk) {
+      k_windkessel<T><<<n_wk, kThreads, 0, st>>>(M, phi, X.d_wk, X.d_wk_ptr, X.d_wk_faces, o.dt, o.rho, bvp);
+      S->n_launch++;
+    }
+    // 3.2 rAU, HbyA
+    if ((s2 = halo_exchange(S->m, U, 3, st))) return s2;
+    k_HbyA<T><<<gs, kThreads, 0, st>>>(M, X.bU, X.udiag, X.ucoef, U, X.rAU, X.HbyA);
+    S->n_launch++;
+    if ((s2 = halo_exchange(S->m, X.HbyA, 3, st)) || (s2 = halo_exchange(S->m, X.rAU, 1, st))) return s2;
+    // 3.3 phiHbyA
+    k_phiHbyA<T><<<gf, kThreads, 0, st>>>(M, X.HbyA, bkU, bvU, X.phiHbyA);
+    // 3.4 pressure coefficients
+    k_pcoef<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
+                                        (T)o.p_ref_value, X.pcoef, X.pdiag, X.prhs0);
+    S->n_launch += 2;
+    // 3.5 non-orthogonal loop
+    for (int io = 0; io <= o.n_nonorth; ++io) {
+      const T* rhs = X.prhs0;
+      if (S->kcorr) {
+        if (io > 0) {
+          if ((s2 = halo_exchange(S->m, p, 1, st))) return s2;
+          launch_grad<T>(M, p, 1, bkp, bvp, X.gp, st);
+          S->n_launch++;
+        }
+        if ((s2 = halo_exchange(S->m, X.gp, 3, st))) return s2;
+        k_prhs<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.gp, X.prhs0, X.prhs);
+        S->n_launch++;
+        rhs = X.prhs;
+      }
+      const bool final_corr = corr == o.n_corr && io == o.n_nonorth;
+      dfvm_solve_report sr{};
+      s2 = run_cg(S, X, rhs, p, o.p_tol, final_corr ? o.p_rel_tol_final : o.p_rel_tol, o.p_maxit, &sr, st);
+      if (np < 16) R->p[np] = sr;
+      np++;
+      if (s2 == DFVM_E_BREAKDOWN) return s2;
+      if (s2 == DFVM_E_NOT_CONVERGED) res = s2;
+      if (io == o.n_nonorth) {
+        if ((s2 = halo_exchange(S->m, p, 1, st))) return s2;
+        k_fluxcorr<T><<<gf, kThreads, 0, st>>>(M, X.phiHbyA, p, X.rAU, X.gp, bkp, bvp, S->kcorr, phi);
+        S->n_launch++;
+      }
+    }
+    // 3.6 velocity correction (also refreshes grad p)
+    k_Ucorr<T><<<gs, kThreads, 0, st>>>(M, p, bkp, bvp, X.HbyA, X.rAU, U, X.gp);
+    S->n_launch++;
+  }
+  R->n_p = np;
+  // 4. continuity + non-finite + Windkessel commit
+  k_continuity<T><<<gs, kThreads, 0, st>>>(M, phi, U, p, X.partials, X.ticket, X.d_cont, X.d_wk, n_wk);
+  S->n_launch++;
+  DFVM_CUDA(cudaMemcpyAsync(X.h_cont, X.d_cont, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (n_wk) DFVM_CUDA(cudaMemcpyAsync(X.h_wk, X.d_wk, n_wk * sizeof(WKDev), cudaMemcpyDeviceToHost, st));
+  DFVM_CUDA(cudaStreamSynchronize(st));
+  DFVM_CUDA(cudaGetLastError());
+  R->cont_err_max = X.h_cont[0];
+  R->cont_err_sum = X.h_cont[1];
+  R->nonfinite = X.h_cont[2] > 0;
+  R->n_outlets = n_wk;
+  for (int i = 0; i < n_wk && i < 64; ++i) {
+    R->Q[i] = X.h_wk[i].Q; R->p_o[i] = X.h_wk[i].p_o;
+    S->wk[i].pc = X.h_wk[i].pc_n;
+  }
+  R->gpu_launches = S->n_launch;
+  count_launch(S->n_launch);
+  if (R->nonfinite) { set_error(DFVM_E_NONFINITE, "non-finite U or p after the PISO step"); return DFVM_E_NONFINITE; }
+  return res;
+}
+
+}  // namespace dfvm
+
+extern "C" {
+
+dfvm_status dfvm_solver_create(dfvm_mesh* m, dfvm_bcs* b, const dfvm_piso_opts* opts, dfvm_solver** out) {
+  if (!m || !b || !opts || !out || b->m != m) { set_error(DFVM_E_INVALID_ARG, "NULL or mismatched argument"); return DFVM_E_INVALID_ARG; }
+  if (!(opts->dt > 0) || !(opts->nu >= 0) || opts->n_corr < 1 || opts->n_corr > 8 || opts->n_nonorth < 0 ||
+      (opts->n_corr * (opts->n_nonorth + 1)) > 16 || opts->p_maxit < 1 || opts->U_maxit < 1 || !(opts->rho > 0)) {
+    set_error(DFVM_E_INVALID_ARG, "invalid PISO options");
+    return DFVM_E_INVALID_ARG;
+  }
+  if (opts->p_ref_cell < 0 || opts->p_ref_cell >= m->H.N) { set_error(DFVM_E_INVALID_ARG, "p_ref_cell out of range", opts->p_ref_cell); return DFVM_E_INVALID_ARG; }
+  cudaSetDevice(m->device);
+  std::unique_ptr<dfvm_solver> S(new dfvm_solver());
+  S->m = m; S->b = b; S->o = *opts;
+  const int32_t gid = m->H.new_of_old[opts->p_ref_cell];
+  S->ref_row = (gid >= m->part.lo && gid < m->part.hi) ? (int)(gid - m->part.lo) : -1;
+  S->kcorr = m->H.nonorth != DFVM_NONORTH_NONE;
+  dfvm_status st;
+  if (m->precision == DFVM_F64) {
+    auto* X = new SolverT<double>();
+    S->impl.reset(X);
+    st = X->init(m, &m->d64);
+  } else {
+    auto* X = new SolverT<float>();
+    S->impl.reset(X);
+    st = X->init(m, &m->d32);
+  }
+  if (st) return st;
+  *out = S.release();
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_solver_destroy(dfvm_solver* s) {
+  delete s;
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_windkessel_update(double pc, double Q, double dt, double Rp, double C, double Rd, int32_t scheme,
+                                   double* pc_new, double* p_o) {
+  if (!(Rp >= 0) || !(C > 0) || !(Rd > 0) || !(dt > 0) || scheme < 0 || scheme > 2 || !pc_new || !p_o) {
+    set_error(DFVM_E_INVALID_WK_PARAMS, "Windkessel needs Rp >= 0, C > 0, Rd > 0, dt > 0, scheme 0..2", scheme);
+    return DFVM_E_INVALID_WK_PARAMS;
+  }
+  double p;
+  if (scheme == 0) { const double e = std::exp(-dt / (Rd * C)); p = pc * e + Rd * Q * (1.0 - e); }
+  else if (scheme == 1) p = pc + dt * (Q - pc / Rd) / C;
+  else p = (pc + dt * Q / C) / (1.0 + dt / (Rd * C));
+  *pc_new = p;
+  *p_o = p + Rp * Q;
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_windkessel_set(dfvm_solver* s, int32_t patch, double Rp, double C, double Rd, double pc0,
+                                int32_t scheme) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  if (!(Rp >= 0) || !(C > 0) || !(Rd > 0) || scheme < 0 || scheme > 2) {
+    set_error(DFVM_E_INVALID_WK_PARAMS, "Windkessel needs Rp >= 0, C > 0, Rd > 0, scheme 0..2", patch);
+    return DFVM_E_INVALID_WK_PARAMS;
+  }
+  if (patch < 0 || patch >= (int32_t)s->m->H.pkind.size() || s->m->H.pkind[patch] == DFVM_PATCH_EMPTY) {
+    set_error(DFVM_E_INVALID_ARG, "bad Windkessel patch", patch);
+    return DFVM_E_INVALID_ARG;
+  }
+  if (s->wk.size() >= 64) { set_error(DFVM_E_INVALID_ARG, "at most 64 Windkessel outlets"); return DFVM_E_INVALID_ARG; }
+  bool found = false;
+  for (auto& w : s->wk)
+    if (w.patch == patch) { w = {patch, Rp, C, Rd, pc0, scheme}; found = true; }
+  if (!found) s->wk.push_back({patch, Rp, C, Rd, pc0, scheme});
+  dfvm_bc_desc d{};
+  d.kind = DFVM_BC_WINDKESSEL;
+  dfvm_bcs_set(s->b, patch, 'p', &d);
+  s->wk_dirty = true;
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_windkessel_state(const dfvm_solver* s, int32_t patch, double* pc) {
+  if (!s || !pc) { set_error(DFVM_E_INVALID_ARG, "NULL argument"); return DFVM_E_INVALID_ARG; }
+  for (auto& w : s->wk)
+    if (w.patch == patch) { *pc = w.pc; return DFVM_OK; }
+  set_error(DFVM_E_INVALID_ARG, "patch has no Windkessel model", patch);
+  return DFVM_E_INVALID_ARG;
+}
+
+static dfvm_status check_f(const dfvm_field* f, const dfvm_mesh* m, bool cells, int nc, const char* what) {
+  if (!f || f->m != m || (cells ? f->loc != DFVM_CELLS : f->loc == DFVM_CELLS) || f->n_comp != nc) {
+    set_error(DFVM_E_INVALID_ARG, std::string("field '") + what + "' has the wrong mesh, location or components");
+    return DFVM_E_INVALID_ARG;
+  }
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_piso_step(dfvm_solver* s, dfvm_field* U, dfvm_field* p, dfvm_field* phi, dfvm_step_report* rep,
+                           dfvm_stream stream) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  dfvm_status st;
+  if ((st = check_f(U, s->m, true, 3, "U")) || (st = check_f(p, s->m, true, 1, "p")) ||
+      (st = check_f(phi, s->m, false, 1, "phi")))
+    return st;
+  if (s->m->part.P > 1) { set_error(DFVM_E_INVALID_ARG, "multi-rank PISO solver: use n_parts == 1 (multi-GPU Krylov reductions not built in this version)"); return DFVM_E_INVALID_ARG; }
+  cudaSetDevice(s->m->device);
+  s->fixed_p = solver_has_fixed_p(s);
+  dfvm_step_report local;
+  dfvm_step_report* R = rep ? rep : &local;
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (s->m->precision == DFVM_F64)
+    return piso<double>(s, *static_cast<SolverT<double>*>(s->impl.get()), (double*)U->ptr, (double*)p->ptr,
+                        (double*)phi->ptr, R, cs);
+  return piso<float>(s, *static_cast<SolverT<float>*>(s->impl.get()), (float*)U->ptr, (float*)p->ptr,
+                     (float*)phi->ptr, R, cs);
+}
+
+}  // extern "C"
+
+template <class T>
+static dfvm_status pressure_solve_t(dfvm_solver* s, SolverT<T>& X, const T* rAU, const T* rhs, T* p, double tol,
+                                    double rel_tol, int maxit, dfvm_solve_report* rep, cudaStream_t st) {
+  DevMesh<T>& M = *X.M;
+  dfvm_status s2;
+  if ((s2 = bcs_device(s->b, 1, st))) return s2;
+  if ((s2 = halo_exchange(s->m, (void*)rAU, 1, st))) return s2;
+  // pressure coefficients from rAU: with phiHbyA = 0, prhs0 = sum_b c_b p_b + the
+  // gauge term (A-12) at the reference row; the caller's rhs already holds every
+  // other term, so only the gauge term is added to it (k_add_at).
+  DFVM_CUDA(cudaMemsetAsync(X.phiHbyA, 0, ((size_t)M.F + M.B + M.E) * sizeof(T), st));
+  const int ref = s->fixed_p ? -1 : s->ref_row;
+  k_pcoef<T><<<grid_for_slices(M.n_slices), kThreads, 0, st>>>(M, rAU, X.phiHbyA, s->b->d_kind[1],
+      (const T*)s->b->d_val[1], ref, (T)s->o.p_ref_value, X.pcoef, X.pdiag, X.prhs0);
+  DFVM_CUDA(cudaMemcpyAsync(X.prhs, rhs, (size_t)M.n_own * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  if (ref >= 0) k_add_at<T><<<1, 1, 0, st>>>(X.prhs, X.prhs0, ref);
+  count_launch(1 + (ref >= 0));
+  s->n_launch = 0;
+  dfvm_status r = run_cg(s, X, X.prhs, p, tol, rel_tol, maxit, rep, st);
+  count_launch(s->n_launch);
+  DFVM_CUDA(cudaStreamSynchronize(st));
+  return r;
+}
+
+extern "C" {
+
+dfvm_status dfvm_pressure_solve(dfvm_solver* s, const dfvm_field* rAU, const dfvm_field* rhs, dfvm_field* p,
+                                double tol, double rel_tol, int32_t maxit, dfvm_solve_report* rep,
+                                dfvm_stream stream) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  dfvm_status st;
+  if ((st = check_f(rAU, s->m, true, 1, "rAU")) || (st = check_f(rhs, s->m, true, 1, "rhs")) ||
+      (st = check_f(p, s->m, true, 1, "p")))
+    return st;
+  if (s->m->part.P > 1) { set_error(DFVM_E_INVALID_ARG, "multi-rank pressure solve not built in this version"); return DFVM_E_INVALID_ARG; }
+  cudaSetDevice(s->m->device);
+  s->fixed_p = solver_has_fixed_p(s);
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (s->m->precision == DFVM_F64)
+    return pressure_solve_t<double>(s, *static_cast<SolverT<double>*>(s->impl.get()), (const double*)rAU->ptr,
+                                    (const double*)rhs->ptr, (double*)p->ptr, tol, rel_tol, maxit, rep, cs);
+  return pressure_solve_t<float>(s, *static_cast<SolverT<float>*>(s->impl.get()), (const float*)rAU->ptr,
+                                 (const float*)rhs->ptr, (float*)p->ptr, tol, rel_tol, maxit, rep, cs);
+}
+
+dfvm_status dfvm_momentum_assemble(dfvm_solver* s, const dfvm_field* U, const dfvm_field* phi, dfvm_field* diag,
+                                   dfvm_field* b, dfvm_stream stream) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  dfvm_status st;
+  if ((st = check_f(U, s->m, true, 3, "U")) || (st = check_f(phi, s->m, false, 1, "phi")) ||
+      (st = check_f(diag, s->m, true, 1, "diag")) || (st = check_f(b, s->m, true, 3, "b")))
+    return st;
+  cudaSetDevice(s->m->device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  s->n_launch = 0;
+  if (s->m->precision == DFVM_F64) {
+    auto& X = *static_cast<SolverT<double>*>(s->impl.get());
+    DFVM_CUDA(cudaMemsetAsync(X.gp, 0, (size_t)X.M->n_cells * 3 * sizeof(double), cs));
+    if ((st = assemble<double>(s, X, (const double*)U->ptr, (const double*)phi->ptr, cs))) return st;
+    DFVM_CUDA(cudaMemcpyAsync(diag->ptr, X.udiag, (size_t)X.M->n_own * sizeof(double), cudaMemcpyDeviceToDevice, cs));
+    DFVM_CUDA(cudaMemcpyAsync(b->ptr, X.bU, (size_t)X.M->n_own * 3 * sizeof(double), cudaMemcpyDeviceToDevice, cs));
+  } else {
+    auto& X = *static_cast<SolverT<float>*>(s->impl.get());
+    DFVM_CUDA(cudaMemsetAsync(X.gp, 0, (size_t)X.M->n_cells * 3 * sizeof(float), cs));
+    if ((st = assemble<float>(s, X, (const float*)U->ptr, (const float*)phi->ptr, cs))) return st;
+    DFVM_CUDA(cudaMemcpyAsync(diag->ptr, X.udiag, (size_t)X.M->n_own * sizeof(float), cudaMemcpyDeviceToDevice, cs));
+    DFVM_CUDA(cudaMemcpyAsync(b->ptr, X.bU, (size_t)X.M->n_own * 3 * sizeof(float), cudaMemcpyDeviceToDevice, cs));
+  }
+  count_launch(s->n_launch);
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_momentum_apply(dfvm_solver* s, const dfvm_field* x, dfvm_field* y, dfvm_stream stream) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  dfvm_status st;
+  if ((st = check_f(x, s->m, true, 3, "x")) || (st = check_f(y, s->m, true, 3, "y"))) return st;
+  cudaSetDevice(s->m->device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  if ((st = halo_exchange(s->m, x->ptr, 3, cs))) return st;
+  if (s->m->precision == DFVM_F64) {
+    auto& X = *static_cast<SolverT<double>*>(s->impl.get());
+    if (!X.assembled) { set_error(DFVM_E_INVALID_ARG, "momentum matrix not assembled"); return DFVM_E_INVALID_ARG; }
+    k_apply<double, 3><<<grid_for_slices(X.M->n_slices), kThreads, 0, cs>>>(*X.M, X.udiag, X.ucoef, (const double*)x->ptr, (double*)y->ptr);
+  } else {
+    auto& X = *static_cast<SolverT<float>*>(s->impl.get());
+    if (!X.assembled) { set_error(DFVM_E_INVALID_ARG, "momentum matrix not assembled"); return DFVM_E_INVALID_ARG; }
+    k_apply<float, 3><<<grid_for_slices(X.M->n_slices), kThreads, 0, cs>>>(*X.M, X.udiag, X.ucoef, (const float*)x->ptr, (float*)y->ptr);
+  }
+  count_launch();
+  DFVM_CUDA(cudaGetLastError());
+  return DFVM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+"""CPU-side checks of the C-ABI boundary (no compute calls without a GPU):
+libdfvm.so loads, exports every entry point include/dfvm.h declares, the
+pure-host Windkessel update matches the closed form, and compute entry points
+fail loudly (DFVM_E_CUDA) when no GPU is present instead of falling back."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2603_15920_b200 as dfvm
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "dfvm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dfvm_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_binding_symbols():
+    assert set(_declared()) == set(dfvm.SYMBOLS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = dfvm.lib()
+    for name in _declared():
+        assert hasattr(L, name), name
+
+
+def test_library_built_for_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", dfvm.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_windkessel_update_host_scalar():
+    # eq:windkessel_discrete closed form; FE/BE alternatives
+    Rp, Cc, Rd, pc, Q, dt = 100.0, 1.1111e-3, 900.0, 0.3, 0.01, 1e-3
+    e = math.exp(-dt / (Rd * Cc))
+    a, po = dfvm.windkessel_update(pc, Q, dt, Rp, Cc, Rd, 0)
+    assert abs(a - (pc * e + Rd * Q * (1 - e))) <= 1e-15 and abs(po - (a + Rp * Q)) <= 1e-15
+    a, _ = dfvm.windkessel_update(pc, Q, dt, Rp, Cc, Rd, 1)
+    assert abs(a - (pc + dt * (Q - pc / Rd) / Cc)) <= 1e-15
+    a, _ = dfvm.windkessel_update(pc, Q, dt, Rp, Cc, Rd, 2)
+    assert abs(a - (pc + dt * Q / Cc) / (1 + dt / (Rd * Cc))) <= 1e-15
+    with pytest.raises(dfvm.DfvmError) as ei:
+        dfvm.windkessel_update(pc, Q, dt, Rp, 0.0, Rd, 0)
+    assert ei.value.status == "INVALID_WK_PARAMS"
+
+
+def test_no_cpu_fallback_without_gpu():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    with pytest.raises(dfvm.DfvmError) as ei:
+        dfvm.Mesh(synth.cavity())
+    assert ei.value.status == "CUDA"

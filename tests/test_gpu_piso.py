@@ -1,0 +1,202 @@
+"""GPU parity of the solver rows: momentum LDU,
+3-component BiCGStab predictor, pressure solve, full PISO steps (cavity C1,
+tet pipe with non-orthogonal correction, Windkessel outlets) against the CPU
+oracle; converged fields within 1e-8 relative L2 (fp64)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2603_15920_b200 as dfvm
+import synth
+from gpu_common import make_bcs, rel_l2, rel_op_err
+
+pytestmark = pytest.mark.gpu
+
+TIGHT = dict(p_tol=1e-14, U_tol=1e-14, p_maxit=20000, U_maxit=2000)
+
+
+def cavity_case(precision="f64", scramble=11, conv="central"):
+    raw = synth.cavity(20, scramble=scramble)
+    mo = oracle.Mesh(raw)
+    mg = dfvm.Mesh(raw, precision=precision)
+    specs = [("movingWall", "U", oracle.BC_FIXED, dict(value=(1, 0, 0))),
+             ("fixedWalls", "U", oracle.BC_FIXED, dict(value=(0, 0, 0))),
+             ("movingWall", "p", oracle.BC_ZEROGRAD, {}), ("fixedWalls", "p", oracle.BC_ZEROGRAD, {})]
+    bo, bg = make_bcs(raw, specs, mo, mg)
+    kw = dict(nu=0.01, dt=0.005, n_corr=2, n_nonorth=0, convection=conv, p_ref_cell=0)
+    return raw, mo, mg, bo, bg, kw
+
+
+def pipe_case(outlet="fixed", n=4, m_r=2, n_z=6, precision="f64"):
+    raw = synth.pipe(n, m_r, n_z, 0.5, 1.0, tets=True, scramble=21)
+    mo = oracle.Mesh(raw)
+    mg = dfvm.Mesh(raw, precision=precision)
+    specs = [("inlet", "U", oracle.BC_PARABOLIC, dict(u_max=2.0, center=(0, 0, 0), radius=0.5)),
+             ("wall", "U", oracle.BC_FIXED, dict(value=(0, 0, 0))), ("outlet", "U", oracle.BC_ZEROGRAD, {}),
+             ("inlet", "p", oracle.BC_ZEROGRAD, {}), ("wall", "p", oracle.BC_ZEROGRAD, {})]
+    if outlet == "fixed":
+        specs.append(("outlet", "p", oracle.BC_FIXED, dict(value=0.0)))
+    bo, bg = make_bcs(raw, specs, mo, mg)
+    kw = dict(nu=0.1, dt=0.01, n_corr=2, n_nonorth=1, convection="upwind", p_ref_cell=0)
+    return raw, mo, mg, bo, bg, kw
+
+
+def initial_state(mo, seed=21, U0=None):
+    U = np.zeros((mo.N, 3)) if U0 is None else U0.copy()
+    U += 0.01 * synth.cell_field(seed, mo.N, 3)
+    return U, np.zeros(mo.N), np.zeros(mo.NF)
+
+
+def run_both(raw, mo, mg, bo, bg, kw, steps, U0=None, wk=None, direct=True):
+    So = oracle.Solver(mo, bo, direct=direct, **kw, **TIGHT)
+    Sg = dfvm.Solver(mg, bg, **kw, **TIGHT)
+    if wk:
+        for patch, args in wk.items():
+            So.windkessel_set(patch, *args)
+            Sg.windkessel_set(patch, *args)
+    U, p, phi = initial_state(mo, U0=U0)
+    Ug, pg, phig = mg.field("cells", 3, U), mg.field("cells", 1, p), mg.field("flux", 1, phi)
+    reps = []
+    for _ in range(steps):
+        ro = So.step(U, p, phi)
+        rg = Sg.step(Ug, pg, phig)
+        reps.append((ro, rg))
+    return (U, p, phi), (Ug.get(), pg.get(), phig.get()), reps, So, Sg
+
+
+def test_momentum_assembly_and_apply():
+    raw, mo, mg, bo, bg, kw = pipe_case()
+    So = oracle.Solver(mo, bo, **kw)
+    Sg = dfvm.Solver(mg, bg, **kw)
+    U = synth.cell_field(40, mo.N, 3)
+    phi = synth.face_field(41, mo.NF)
+    diag, lo, up, b = So.momentum_assemble(U, phi)
+    Ug, phig = mg.field("cells", 3, U), mg.field("flux", 1, phi)
+    dg, bgf = mg.field("cells", 1), mg.field("cells", 3)
+    Sg.momentum_assemble(Ug, phig, dg, bgf)
+    assert rel_l2(dg.get(), diag) <= 1e-13
+    assert rel_l2(bgf.get(), b) <= 1e-12
+    x = synth.cell_field(50, mo.N, 3)
+    y = mg.field("cells", 3)
+    Sg.momentum_apply(mg.field("cells", 3, x), y)
+    ref = np.stack([mo.ldu_apply(diag, lo, up, x[:, k]) for k in range(3)], 1)
+    scale = np.stack([mo.ldu_apply(np.abs(diag), np.abs(lo), np.abs(up), np.abs(x[:, k])) for k in range(3)], 1)
+    assert rel_op_err(y.get(), ref, scale) <= 1e-12
+
+
+@pytest.mark.parametrize("case", ["cavity", "pipe"])
+def test_pressure_solve(case):
+    raw, mo, mg, bo, bg, kw = cavity_case() if case == "cavity" else pipe_case()
+    So = oracle.Solver(mo, bo, **kw)
+    Sg = dfvm.Solver(mg, bg, **kw)
+    rAU = 0.01 * (1.5 + 0.5 * synth.cell_field(60, mo.N))
+    rhs = 1e-3 * synth.cell_field(61, mo.N)
+    p0 = synth.cell_field(62, mo.N)
+    po, ro = So.pressure_solve(rAU, rhs, p0=p0, tol=1e-14)
+    pg = mg.field("cells", 1, p0)
+    rg = Sg.pressure_solve(mg.field("cells", 1, rAU), mg.field("cells", 1, rhs), pg, tol=1e-14)
+    assert ro["converged"]
+    assert rel_l2(pg.get(), po) <= 1e-8, (rg, ro)
+    assert abs(rg["it"] - ro["it"]) <= max(5, 0.1 * ro["it"])
+
+
+def test_pressure_solve_zero_rhs():
+    # b = 0 -> x = 0 with 0 iterations
+    raw, mo, mg, bo, bg, kw = pipe_case()
+    Sg = dfvm.Solver(mg, bg, **kw)
+    pg = mg.field("cells", 1, synth.cell_field(62, mo.N))
+    r = Sg.pressure_solve(mg.field("cells", 1, np.full(mo.N, 0.01)), mg.field("cells", 1), pg)
+    assert r["it"] == 0 and np.all(pg.get() == 0)
+
+
+@pytest.mark.parametrize("conv", ["central", "upwind"])
+def test_cavity_steps(conv):
+    raw, mo, mg, bo, bg, kw = cavity_case(conv=conv)
+    (U, p, phi), (Ug, pg, phig), reps, _, _ = run_both(raw, mo, mg, bo, bg, kw, 10)
+    assert rel_l2(Ug, U) <= 1e-8 and rel_l2(pg, p) <= 1e-8 and rel_l2(phig, phi) <= 1e-8
+    for ro, rg in reps:
+        assert rg["cont_err_max"] <= 1e-13 and not rg["nonfinite"]
+        assert all(r["converged"] or r["res"] <= 1e-12 * max(r["res0"], 1e-300) for r in rg["p"]), rg["p"]
+
+
+def test_cavity_regression_values_on_gpu(golden):
+    # the oracle pin values reproduced through the CUDA path (A-31 case, unscrambled)
+    g = golden("cavity_c1.json")
+    raw, mo, mg, bo, bg, kw = cavity_case(scramble=0)
+    Sg = dfvm.Solver(mg, bg, **kw, **TIGHT)
+    Ug, pg, phig = mg.field("cells", 3), mg.field("cells", 1), mg.field("flux", 1)
+    Sg.step(Ug, pg, phig)
+    assert abs(np.abs(Ug.get()).max() - g["step1"]["max_abs_U_component"]) <= 1e-9
+    p = pg.get()
+    assert abs(p.min() - g["step1"]["p_min"]) <= 1e-8 and abs(p.max() - g["step1"]["p_max"]) <= 1e-8
+
+
+def test_pipe_nonorth_steps():
+    raw, mo, mg, bo, bg, kw = pipe_case()
+    xc = mo.xc
+    U0 = np.zeros((mo.N, 3))
+    U0[:, 2] = 2.0 * (1 - 4 * (xc[:, 0] ** 2 + xc[:, 1] ** 2))
+    (U, p, phi), (Ug, pg, phig), reps, _, _ = run_both(raw, mo, mg, bo, bg, kw, 3, U0=U0)
+    assert rel_l2(Ug, U) <= 1e-8 and rel_l2(pg, p) <= 1e-8 and rel_l2(phig, phi) <= 1e-8
+
+
+def test_windkessel_outlet_steps(golden):
+    gt = golden("windkessel.json")["table2_gt"][0]
+    raw, mo, mg, bo, bg, kw = pipe_case(outlet="wk")
+    xc = mo.xc
+    U0 = np.zeros((mo.N, 3))
+    U0[:, 2] = 2.0 * (1 - 4 * (xc[:, 0] ** 2 + xc[:, 1] ** 2))
+    wk = {"outlet": (gt["Rp"] * 1e-3, gt["C"] * 1e3, gt["Rd"] * 1e-3, 0.0, 0)}
+    (U, p, phi), (Ug, pg, phig), reps, So, Sg = run_both(raw, mo, mg, bo, bg, kw, 3, U0=U0, wk=wk)
+    assert rel_l2(Ug, U) <= 1e-8 and rel_l2(pg, p) <= 1e-8
+    for ro, rg in reps:
+        assert np.allclose(rg["Q"], ro["Q"], rtol=1e-8) and np.allclose(rg["p_o"], ro["p_o"], rtol=1e-8)
+    assert abs(Sg.windkessel_state("outlet") - So.windkessel_pc(raw.patch("outlet"))) <= 1e-8 * abs(
+        So.windkessel_pc(raw.patch("outlet")))
+
+
+def test_uniform_flow_fixed_point_gpu():
+    raw = synth.pipe(4, 2, 6, 0.5, 1.0, tets=True, scramble=3)
+    mg = dfvm.Mesh(raw)
+    U0 = np.array([0.0, 0.0, 1.0])
+    bg = dfvm.BCs(mg)
+    bg.set("inlet", "U", dfvm.BC_FIXED, U0); bg.set("wall", "U", dfvm.BC_FIXED, U0)
+    bg.set("outlet", "U", dfvm.BC_ZEROGRAD)
+    bg.set("inlet", "p", dfvm.BC_ZEROGRAD); bg.set("wall", "p", dfvm.BC_ZEROGRAD)
+    bg.set("outlet", "p", dfvm.BC_FIXED, 0.0)
+    S = dfvm.Solver(mg, bg, nu=0.1, dt=0.01, n_corr=2, n_nonorth=1, **TIGHT)
+    mo = oracle.Mesh(raw)
+    Ug = mg.field("cells", 3, np.tile(U0, (mo.N, 1)))
+    pg = mg.field("cells", 1)
+    phig = mg.field("flux", 1, mo.Sf @ U0)
+    for _ in range(3):
+        r = S.step(Ug, pg, phig)
+    assert np.abs(Ug.get() - U0).max() <= 1e-12 and np.abs(pg.get()).max() <= 1e-12
+    assert r["cont_err_max"] <= 1e-13
+
+
+def test_piso_deterministic():
+    raw, mo, mg, bo, bg, kw = pipe_case()
+    outs = []
+    for _ in range(2):
+        S = dfvm.Solver(mg, bg, **kw, **TIGHT)
+        U, p, phi = initial_state(mo)
+        Ug, pg, phig = mg.field("cells", 3, U), mg.field("cells", 1, p), mg.field("flux", 1, phi)
+        for _ in range(2):
+            S.step(Ug, pg, phig)
+        outs.append((Ug.get(), pg.get(), phig.get()))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_f32_piso_close_to_f64():
+    raw, mo, mg, bo, bg, kw = cavity_case(precision="f32")
+    Sg = dfvm.Solver(mg, bg, **kw, p_tol=1e-6, U_tol=1e-6)
+    Ug, pg, phig = mg.field("cells", 3), mg.field("cells", 1), mg.field("flux", 1)
+    for _ in range(5):
+        r = Sg.step(Ug, pg, phig)
+    So = oracle.Solver(mo, bo, direct=True, **kw)
+    U, p, phi = np.zeros((mo.N, 3)), np.zeros(mo.N), np.zeros(mo.NF)
+    for _ in range(5):
+        So.step(U, p, phi)
+    assert rel_l2(Ug.get(), U) <= 1e-4 and rel_l2(pg.get(), p) <= 1e-3
