@@ -1,0 +1,314 @@
+#!/usr/bin/env python
+"""bench.py — PISO cell-updates/s of the B200 hot path (BASELINE.json metric
+"PISO cell-updates/s and FVM operator-apply HBM GB/s at 1/2/4/8 B200").
+
+One "step" = one full PISO step (gradients,
+momentum assembly + BiCGStab predictor, n_corr correctors with Windkessel,
+H/rAU/HbyA, phiHbyA, pressure coefficients, PCG pressure solves, Rhie-Chow
+flux correction, velocity correction, continuity) on the configured mesh.
+
+    python bench.py [--gpus N --steps K --warmup W --config c5|c2|c1 --precision f64|f32]
+    python bench.py --impl reference ...   # the CPU oracle arm (bounded sample)
+
+value   = cells x steps / device seconds (max over ranks), whole job.
+e2e     = the same metric through the C ABI with HOST buffers: every step
+          imports U, p, phi from pinned host memory and exports U, p back.
+roofline: the PCG SpMV kernel (dominant kernel of the step), timed live with
+          CUDA events on the launching stream inside the library.
+cpu_baseline: the oracle (oracle/, plain fp64 C++, 1 core) on a bounded
+          sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PISO cell-updates/s"
+UNIT = "cell-updates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [l.strip().split(", ") for l in open(self.f.name) if l.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[0]) for r in rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) < 8:
+                continue
+            for n, v in zip(names, r[4:8]):
+                if v.strip() == "Active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU oracle arm
+def oracle_sample(config, precision):
+    """The oracle (1 core, fp64) on a bounded sample of the same workload:
+    one PISO step of the same generator / physics at a reduced axial length,
+    pressure CG capped at 200 iterations per solve."""
+    import cases
+    import oracle
+    if config == "c5":
+        case = cases.c5(n_z=4)
+        sample = "1 PISO step, C5 generator (n=64, m_r=32) with n_z=4 -> 245,760 tets, C5 physics, CG capped at 200 it/solve"
+    elif config == "c2":
+        case = cases.c2()
+        sample = "1 PISO step of C2 (199,680 tets), CG capped at 200 it/solve"
+    else:
+        case = cases.c1()
+        sample = "1 PISO step of C1 (400 hex)"
+    kw = dict(case.solver)
+    kw["p_maxit"] = min(kw["p_maxit"], 200)
+    t0 = time.time()
+    m = oracle.Mesh(case.raw)
+    b = case.apply_bcs(oracle.BCs(m))
+    S = oracle.Solver(m, b, **kw)
+    U, p, phi = case.initial_state(m.xc, m.xf, m.Sf)
+    t1 = time.time()
+    S.step(U, p, phi)
+    t2 = time.time()
+    return dict(value=m.N / (t2 - t1), unit=UNIT, cores=1, kind="oracle", sample=sample,
+                seconds=round(t2 - t1, 3), setup_seconds=round(t1 - t0, 3))
+
+
+def run_reference(args):
+    steps, warmup = args.steps, args.warmup
+    vals = []
+    res = None
+    for i in range(warmup + steps):
+        res = oracle_sample(args.config, args.precision)
+        if i >= warmup:
+            vals.append(res["value"])
+    value = float(statistics.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "warmup": warmup, "ms_per_step": 1000.0 * res["seconds"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": res["sample"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": res["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dfvm", choices=["dfvm", "reference"])
+    ap.add_argument("--config", default="c5", choices=["c5", "c2", "c1"])
+    ap.add_argument("--nz", type=int, default=None, help="override C5 axial layers (814 = 50.0M cells)")
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args)
+        return
+
+    import torch
+    import paper_2603_15920_b200 as dfvm
+    import cases
+
+    torch.cuda.set_device(local)
+    dist = None
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = dfvm.Comm.unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+        dist.broadcast(t, 0)
+        comm = dfvm.Comm(world, rank, bytes(t.cpu().tolist()), local)
+
+    t_setup = time.time()
+    case = cases.c5(n_z=args.nz) if (args.config == "c5" and args.nz) else cases.CONFIGS[args.config]()
+    t_gen = time.time() - t_setup
+    mesh = dfvm.Mesh(case.raw, precision=args.precision, n_parts=world, rank=rank, device=local, comm=comm)
+    info = mesh.info
+    geo = mesh.export_geometry()
+    U0, p0, phi0 = case.initial_state(geo["xc"], geo["xf"], geo["Sf"])
+    B = case.apply_bcs(dfvm.BCs(mesh))
+    S = dfvm.Solver(mesh, B, **case.solver)
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    U = mesh.field("cells", 3, U0, sp)
+    p = mesh.field("cells", 1, p0, sp)
+    phi = mesh.field("flux", 1, phi0, sp)
+    t_setup = time.time() - t_setup
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        S.step(U, p, phi, sp)
+
+    # ---------------- timed region (device-resident inputs)
+    barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    S.set_timing(True)
+    l0 = dfvm.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    reps = []
+    for _ in range(args.steps):
+        reps.append(S.step(U, p, phi, sp))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = dfvm.kernel_launches() - l0
+    tim = S.timing()
+    S.set_timing(False)
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    N = info["n_cells"]
+    value = N * args.steps / (ms / 1000.0)
+
+    # ---------------- end-to-end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hU = torch.from_numpy(np.ascontiguousarray(U.get(sp))).pin_memory().numpy()
+        hp = torch.from_numpy(np.ascontiguousarray(p.get(sp)).reshape(-1, 1)).pin_memory().numpy()
+        hphi = torch.from_numpy(np.ascontiguousarray(phi.get(sp)).reshape(-1, 1)).pin_memory().numpy()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            U.set(hU, sp); p.set(hp, sp); phi.set(hphi, sp)
+            S.step(U, p, phi, sp)
+            U.get(sp, out=hU); p.get(sp, out=hp); phi.get(sp, out=hphi)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_e2e = max_over_ranks(f0.elapsed_time(f1))
+        h2d = (hU.nbytes + hp.nbytes + hphi.nbytes)
+        d2h = (hU.nbytes + hp.nbytes + hphi.nbytes)
+        e2e = {"value": N * args.steps / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e / args.steps}
+
+    # ---------------- roofline of the dominant kernel (PCG SpMV)
+    hbm, peak_src = peaks()
+    n_own, F_l = info["n_owned"], info["n_local_internal_faces"]
+    vb, ib = (8, 4) if args.precision == "f64" else (4, 4)
+    # ALG bytes per launch (SURVEY.md §8(d4) lap_apply): row meta 4N, I = 2F
+    # incidences x (column 4 B + coefficient vb), diag, x, y: vb N each
+    alg = 4 * n_own + 2 * F_l * (ib + vb) + 3 * vb * n_own
+    spmv_ms = tim["spmv_ms"] / max(tim["spmv_n"], 1)
+    achieved = alg / (spmv_ms / 1000.0) / 1e9 if tim["spmv_n"] else None
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"ncu_spmv_{args.config}_{args.precision}.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("traffic_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": "k_cg_spmv (PCG SpMV + p.q partials)", "achieved": achieved, "peak": hbm,
+            "peak_source": peak_src, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
+            "traffic": traffic, "alg_bytes_per_launch": alg, "launch_ms": spmv_ms, "launches": tim["spmv_n"],
+            "share_of_step": (tim["spmv_ms"] / ms) if ms else None,
+            "pcg_iteration_ms": tim["cg_iter_ms"] / max(tim["cg_iter_n"], 1),
+            "pcg_share_of_step": tim["cg_iter_ms"] / ms if ms else None}
+
+    cg_its = [r["it"] for rep in reps for r in rep["p"]]
+    bi_its = [r["it"] for rep in reps for r in rep["U"]]
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = oracle_sample(args.config, args.precision)
+            cpu.pop("setup_seconds", None)
+        except Exception as ex:  # the baseline must not kill the GPU number
+            cpu = {"error": str(ex)}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": case.name, "description": case.description, "cells": N,
+                   "internal_faces": info["n_internal_faces"], "parallelism": f"mesh-partition x{world} (RCM blocks)",
+                   "l2_policy": "inputs larger than L2 (no flush)" if N > 2_000_000 else "L2-resident (small config)",
+                   "solver": {k: v for k, v in case.solver.items()}},
+        "gpu_launches": int(launches),
+        "krylov": {"pcg_iterations_per_solve": float(np.mean(cg_its)) if cg_its else 0.0,
+                   "bicgstab_iterations_per_component": float(np.mean(bi_its)) if bi_its else 0.0,
+                   "krylov_normalised_cell_iterations_per_s": N * (sum(cg_its)) / (ms / 1000.0)},
+        "continuity_max": max(r["cont_err_max"] for r in reps),
+        "roofline": roof, "e2e": e2e, "clocks": clk, "cpu_baseline": cpu,
+        "setup_seconds": {"mesh_generation": round(t_gen, 2), "mesh_create": round(info["host_seconds"], 2),
+                          "total": round(t_setup, 2)},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,78 @@
+"""Workload recipes of BASELINE.json's configs: mesh
+generator call, boundary conditions, physical constants, solver settings and
+the seeded initial condition.  Data only (no method arithmetic): the same
+recipe drives the CUDA library (bench.py, smoke) and the CPU oracle
+(tests, cpu_baseline), through their own `BCs.set` / `Solver` calls.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import synth
+
+FIXED, ZEROGRAD, PARABOLIC = 0, 1, 2
+
+# throughput-mode Krylov settings (reading A-13: p abs 1e-6 relative to ||b||,
+# relTol 0.05 on non-final correctors, 0 on the final one; U 1e-5)
+THROUGHPUT = dict(p_tol=1e-6, p_rel_tol=0.05, p_rel_tol_final=0.0, p_maxit=20000, U_tol=1e-5, U_rel_tol=0.0,
+                  U_maxit=1000)
+
+
+class Case:
+    def __init__(self, name, raw, bcs, solver, ic, description):
+        self.name, self.raw, self.bcs, self.solver, self.ic, self.description = name, raw, bcs, solver, ic, description
+
+    def apply_bcs(self, B):
+        for patch, fld, kind, kw in self.bcs:
+            B.set(patch, fld, kind, **kw)
+        return B
+
+    def initial_state(self, xc, xf, Sf):
+        """(U [N,3], p [N], phi [n_faces]) in original numbering, from the
+        geometry the caller's own mesh reports."""
+        return self.ic(xc, xf, Sf)
+
+
+def _pipe_bcs(u_max, R):
+    return [("inlet", "U", PARABOLIC, dict(u_max=u_max, center=(0.0, 0.0, 0.0), radius=R)),
+            ("wall", "U", FIXED, dict(value=(0.0, 0.0, 0.0))), ("outlet", "U", ZEROGRAD, {}),
+            ("inlet", "p", ZEROGRAD, {}), ("wall", "p", ZEROGRAD, {}), ("outlet", "p", FIXED, dict(value=0.0))]
+
+
+def _poiseuille_ic(seed, u_max, R):
+    """Poiseuille profile + 1% noise (§8(d2)); phi = u(x_f) . S_f of the
+    noise-free profile."""
+    def ic(xc, xf, Sf):
+        N = len(xc)
+        U = np.zeros((N, 3))
+        U[:, 2] = u_max * (1.0 - (xc[:, 0] ** 2 + xc[:, 1] ** 2) / (R * R))
+        U += 0.01 * u_max * synth.cell_field(seed, N, 3)
+        phi = u_max * (1.0 - (xf[:, 0] ** 2 + xf[:, 1] ** 2) / (R * R)) * Sf[:, 2]
+        return U, np.zeros(N), phi
+    return ic
+
+
+def c1(scramble=11):
+    raw = synth.cavity(20, scramble=scramble)
+    bcs = [("movingWall", "U", FIXED, dict(value=(1.0, 0.0, 0.0))), ("fixedWalls", "U", FIXED, dict(value=(0, 0, 0))),
+           ("movingWall", "p", ZEROGRAD, {}), ("fixedWalls", "p", ZEROGRAD, {})]
+    solver = dict(nu=0.01, dt=0.005, n_corr=2, n_nonorth=0, convection="central", p_ref_cell=0, **THROUGHPUT)
+    ic = lambda xc, xf, Sf: (np.zeros((len(xc), 3)), np.zeros(len(xc)), np.zeros(len(Sf)))
+    return Case("c1_cavity_20x20x1_hex", raw, bcs, solver, ic, "OpenFOAM cavity 20x20x1 hex, Re=10 (A-31)")
+
+
+def c2(scramble=12):
+    raw = synth.pipe_c2(scramble=scramble)
+    solver = dict(nu=0.1, dt=0.01, n_corr=2, n_nonorth=1, convection="upwind", p_ref_cell=0, **THROUGHPUT)
+    return Case("c2_pipe_tet_199680", raw, _pipe_bcs(2.0, 0.5), solver, _poiseuille_ic(21, 2.0, 0.5),
+                "O-grid pipe R=0.5 L=2.6, alternating 5-tet, N=199680, Re_D=10")
+
+
+def c5(n_z=814, scramble=15):
+    raw = synth.pipe_c5(n_z=n_z, scramble=scramble)
+    solver = dict(nu=0.01, dt=0.001, n_corr=2, n_nonorth=1, convection="upwind", p_ref_cell=0, **THROUGHPUT)
+    return Case(f"c5_pipe_tet_{raw.n_cells}", raw, _pipe_bcs(2.0, 0.5), solver, _poiseuille_ic(51, 2.0, 0.5),
+                f"O-grid pipe n=64 m_r=32 n_z={n_z}, alternating 5-tet, N={raw.n_cells}, Re_D=100")
+
+
+CONFIGS = {"c1": c1, "c2": c2, "c5": c5}

@@ -280,6 +280,15 @@ dfvm_status dfvm_windkessel_update(double pc, double Q, double dt, double Rp, do
                                    int32_t scheme, double* pc_new, double* p_o);
 dfvm_status dfvm_solver_destroy(dfvm_solver* s);
 
+/* Live kernel timing for the roofline report: when on, the solver brackets
+ * its pressure-CG kernels with CUDA events on the launching stream and
+ * accumulates the durations of the iterations that actually ran.
+ * ms[0]/count[0]: the PCG SpMV kernel (q = A p, p.q partials); ms[1]/count[1]:
+ * one whole PCG iteration (p update, SpMV, x/r update).  ms[2..3] reserved.
+ * set_timing resets the accumulators. */
+dfvm_status dfvm_solver_set_timing(dfvm_solver* s, int32_t on);
+dfvm_status dfvm_solver_get_timing(const dfvm_solver* s, double ms[4], int64_t count[4]);
+
 /* Kernel launch counter (all kernels this process launched through the
  * library), for bench.py's gpu_launches claim. */
 int64_t dfvm_kernel_launches(void);

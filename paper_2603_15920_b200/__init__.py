@@ -39,6 +39,7 @@ SYMBOLS = [
     "dfvm_fvc_div", "dfvm_fvm_laplacian_apply", "dfvm_solver_create", "dfvm_pressure_solve",
     "dfvm_momentum_assemble", "dfvm_momentum_apply", "dfvm_piso_step", "dfvm_windkessel_set",
     "dfvm_windkessel_state", "dfvm_windkessel_update", "dfvm_solver_destroy", "dfvm_kernel_launches",
+    "dfvm_solver_set_timing", "dfvm_solver_get_timing",
 ]
 
 
@@ -135,6 +136,8 @@ def lib():
         L.dfvm_windkessel_set.argtypes = [vp, i32, f64, f64, f64, f64, i32]
         L.dfvm_windkessel_state.argtypes = [vp, i32, C.POINTER(f64)]
         L.dfvm_windkessel_update.argtypes = [f64, f64, f64, f64, f64, f64, i32, C.POINTER(f64), C.POINTER(f64)]
+        L.dfvm_solver_set_timing.argtypes = [vp, i32]
+        L.dfvm_solver_get_timing.argtypes = [vp, vp, vp]
         L.dfvm_comm_unique_id.argtypes = [vp]
         L.dfvm_comm_create.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
         L.dfvm_comm_destroy.argtypes = [vp]
@@ -303,10 +306,14 @@ class Field:
         _check(lib().dfvm_field_import(self.h, _ptr(a), 1, stream))
         return self
 
-    def get(self, stream=None):
-        """Export to fp64 numpy in ORIGINAL order (synchronises the stream)."""
-        a = np.zeros((self.global_count, self.n_comp), np.float64)
+    def get(self, stream=None, out=None):
+        """Export to fp64 numpy in ORIGINAL order (synchronises the stream);
+        `out` may be a preallocated (e.g. pinned) C-contiguous fp64 array."""
+        a = np.zeros((self.global_count, self.n_comp), np.float64) if out is None else out
+        assert a.dtype == np.float64 and a.flags.c_contiguous and a.size == self.global_count * self.n_comp
         _check(lib().dfvm_field_export(self.h, _ptr(a), 1, stream))
+        if out is not None:
+            return out
         return a[:, 0] if self.n_comp == 1 else a
 
     def import_device(self, dev_ptr, stream=None):
@@ -429,3 +436,11 @@ class Solver:
 
     def momentum_apply(self, x, y, stream=None):
         _check(lib().dfvm_momentum_apply(self.h, x.h, y.h, stream))
+
+    def set_timing(self, on=True):
+        _check(lib().dfvm_solver_set_timing(self.h, 1 if on else 0))
+
+    def timing(self):
+        ms = np.zeros(4); n = np.zeros(4, np.int64)
+        _check(lib().dfvm_solver_get_timing(self.h, _ptr(ms), _ptr(n)))
+        return dict(spmv_ms=float(ms[0]), spmv_n=int(n[0]), cg_iter_ms=float(ms[1]), cg_iter_n=int(n[1]))

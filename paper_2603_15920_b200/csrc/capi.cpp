@@ -448,7 +448,8 @@ dfvm_status dfvm_field_export(const dfvm_field* f, double* dst, int32_t dst_is_h
   void* tmp = nullptr;
   if (dst_is_host) {
     DFVM_CUDA(cudaMallocAsync(&tmp, bytes, s));
-    DFVM_CUDA(cudaMemcpyAsync(tmp, dst, bytes, cudaMemcpyHostToDevice, s));  // keep non-owned entries
+    if (m->part.P > 1)   // keep the entries other ranks own
+      DFVM_CUDA(cudaMemcpyAsync(tmp, dst, bytes, cudaMemcpyHostToDevice, s));
     ddst = (double*)tmp;
   }
   if (m->precision == DFVM_F64) launch_export<double>(ddst, (const double*)f->ptr, map, n, f->n_comp, oriented, s);

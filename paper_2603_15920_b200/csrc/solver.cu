@@ -812,6 +812,13 @@ struct dfvm_solver {
   std::vector<WK> wk;
   bool wk_dirty = true;
   int n_launch = 0;
+  // live kernel timing (CUDA events on the launching stream): class 0 = the
+  // PCG SpMV kernel, class 1 = one full PCG iteration (3 kernels)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  double t_ms[4] = {0, 0, 0, 0};
+  int64_t t_n[4] = {0, 0, 0, 0};
+  ~dfvm_solver() { for (auto e : ev) cudaEventDestroy(e); }
 };
 
 namespace dfvm {
@@ -876,15 +883,39 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
   if (dfvm_status s2 = halo_exchange(S->m, x, 1, st)) return s2;
   k_cg_init<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr, X.partials, X.ticket, X.d_ctl);
   S->n_launch++;
+  if (S->timing && S->ev.size() < 4 * kChunk) {
+    while (S->ev.size() < 4 * kChunk) {
+      cudaEvent_t e;
+      DFVM_CUDA(cudaEventCreate(&e));
+      S->ev.push_back(e);
+    }
+  }
+  int it_before = 0;
   for (int it0 = 0;; it0 += kChunk) {
     for (int k = 0; k < kChunk; ++k) {
+      if (S->timing) cudaEventRecord(S->ev[4 * k], st);
       k_cg_pupd<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.pdiag, X.kp, X.d_ctl);
+      if (S->timing) cudaEventRecord(S->ev[4 * k + 1], st);
       k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl);
+      if (S->timing) cudaEventRecord(S->ev[4 * k + 2], st);
       k_cg_update<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, X.kq, X.pdiag, x, X.kr, X.partials, X.ticket, X.d_ctl);
+      if (S->timing) cudaEventRecord(S->ev[4 * k + 3], st);
       S->n_launch += 3;
     }
     DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
     DFVM_CUDA(cudaStreamSynchronize(st));
+    if (S->timing) {
+      // only iterations that actually ran (the rest exited on the done flag)
+      const int ran = X.h_ctl->it - it_before;
+      for (int k = 0; k < kChunk && k < ran; ++k) {
+        float a = 0, b2 = 0;
+        cudaEventElapsedTime(&a, S->ev[4 * k + 1], S->ev[4 * k + 2]);
+        cudaEventElapsedTime(&b2, S->ev[4 * k], S->ev[4 * k + 3]);
+        S->t_ms[0] += a; S->t_n[0]++;
+        S->t_ms[1] += b2; S->t_n[1]++;
+      }
+      it_before = X.h_ctl->it;
+    }
     if (X.h_ctl->done) break;
   }
   DFVM_CUDA(cudaGetLastError());
@@ -1002,7 +1033,9 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
     for (int io = 0; io <= o.n_nonorth; ++io) {
       const T* rhs = X.prhs0;
       if (S->kcorr) {
-        if (io > 0) {
+        // grad p of the current p: the stored gradient is stale after the
+        // previous solve (io > 0) or after a Windkessel update of p_b
+        if (io > 0 || n_wk > 0) {
           if ((s2 = halo_exchange(S->m, p, 1, st))) return s2;
           launch_grad<T>(M, p, 1, bkp, bvp, X.gp, st);
           S->n_launch++;
@@ -1081,6 +1114,19 @@ dfvm_status dfvm_solver_create(dfvm_mesh* m, dfvm_bcs* b, const dfvm_piso_opts* 
   }
   if (st) return st;
   *out = S.release();
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_solver_set_timing(dfvm_solver* s, int32_t on) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  s->timing = on != 0;
+  for (int i = 0; i < 4; ++i) { s->t_ms[i] = 0; s->t_n[i] = 0; }
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_solver_get_timing(const dfvm_solver* s, double* ms, int64_t* count) {
+  if (!s || !ms || !count) { set_error(DFVM_E_INVALID_ARG, "NULL argument"); return DFVM_E_INVALID_ARG; }
+  for (int i = 0; i < 4; ++i) { ms[i] = s->t_ms[i]; count[i] = s->t_n[i]; }
   return DFVM_OK;
 }
 
