@@ -5,6 +5,7 @@
 // readings of SURVEY.md §8(c) are named where the paper is silent.
 #include "oracle.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -20,8 +21,10 @@ static double dotv(const std::vector<double>& a, const std::vector<double>& b) {
 // --------------------------------------------------------------- O-7
 // Stopping rule shared by CG and BiCGStab (A-13): b = 0 -> x = 0 with 0
 // iterations; otherwise stop when ||r||_2 <= max(tol ||b||_2,
-// rel_tol ||r_0||_2), or on stagnation (no new minimum of ||r||_2 for 50
-// iterations), or at maxit.
+// rel_tol ||r_0||_2), or at maxit.  In parity mode only (tol < 1e-12, a
+// request at round-off level) also on stagnation: no new minimum of ||r||_2
+// for max(50, best_it) iterations.  (||r||_2 of CG is not monotone, so the
+// stagnation test is never applied to throughput-mode solves.)
 static double threshold(double bnorm, double res0, double tol, double rel_tol) {
   double a = tol * bnorm, b = rel_tol * res0;
   return a > b ? a : b;
@@ -55,7 +58,7 @@ SolveReport cg(const Mesh& m, const LDU& A, const double* b, double* x, double t
     rep.it = it;
     if (rep.res <= thr) { rep.converged = 1; return rep; }
     if (rep.res < best) { best = rep.res; best_it = it; }
-    else if (it - best_it >= 50) break;  // stagnation
+    else if (tol < 1e-12 && it - best_it >= std::max(50, best_it)) break;  // stagnation, parity mode (A-13)
     for (int64_t i = 0; i < N; ++i) z[i] = r[i] / A.diag[i];
     const double rz_new = dotv(r, z);
     const double beta = rz_new / rz;
@@ -110,7 +113,7 @@ SolveReport bicgstab(const Mesh& m, const LDU& A, const double* b, double* x, do
     if (rep.res <= thr) { rep.converged = 1; return rep; }
     if (omega == 0.0) { rep.status = E_BREAKDOWN; return rep; }
     if (rep.res < best) { best = rep.res; best_it = it; }
-    else if (it - best_it >= 50) break;
+    else if (tol < 1e-12 && it - best_it >= std::max(50, best_it)) break;
     rho_old = rho;
   }
   rep.status = E_NOT_CONVERGED;
