@@ -165,7 +165,11 @@ dfvm_status dfvm_mesh_destroy(dfvm_mesh* m);
  * Cell fields: [n_owned + n_ghost][n_comp] in internal (RCM) order.
  * Face fields: [n_local_internal + n_local_boundary + n_local_empty][n_comp]
  * in internal face order.  Device element type = mesh precision. */
-typedef enum { DFVM_CELLS = 0, DFVM_FACES = 1 } dfvm_loc;
+/* DFVM_FACES: unoriented face values (e.g. interpolated phi_f);
+ * DFVM_FACE_FLUX: oriented face fluxes (phi, F of fvc_div) whose sign follows
+ * the face orientation: import/export negate them on faces the renumbering
+ * re-oriented (O-9 step 5), so the caller always sees its own orientation. */
+typedef enum { DFVM_CELLS = 0, DFVM_FACES = 1, DFVM_FACE_FLUX = 2 } dfvm_loc;
 typedef struct dfvm_field dfvm_field;
 dfvm_status dfvm_field_bytes(const dfvm_mesh* m, int32_t loc, int32_t n_comp, size_t* bytes);
 /* north-star `field_alloc`: library-owned device memory (zero-filled) */

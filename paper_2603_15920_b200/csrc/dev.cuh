@@ -2,6 +2,7 @@
 // warp-per-SELL-slice iteration, deterministic two-level reductions.
 #pragma once
 #include <cstdint>
+#include <unordered_map>
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -19,6 +20,32 @@ inline int grid_for_slices(int n_slices) {
 inline int grid_for(int64_t n) {
   int64_t b = (n + kThreads - 1) / kThreads;
   return (int)(b < 1 ? 1 : (b > kMaxBlocks ? kMaxBlocks : b));
+}
+
+// Resident-block cap of a kernel: (blocks per SM from the occupancy API) x
+// (SM count), so a grid-stride kernel runs as exactly one full wave.  Cached
+// per kernel; a fixed function of (kernel, device), so the reduction
+// structure (and hence the bits) stays deterministic run to run.
+inline int occ_cap(const void* fn) {
+  static std::unordered_map<const void*, int> cache;
+  auto it = cache.find(fn);
+  if (it != cache.end()) return it->second;
+  int dev = 0, nsm = 148, b = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+  const int cap = b * nsm < kMaxBlocks ? b * nsm : kMaxBlocks;
+  cache[fn] = cap;
+  return cap;
+}
+template <class K> inline int grid_slices(K fn, int n_slices) {
+  const int need = (n_slices + kWarpsPerBlock - 1) / kWarpsPerBlock, cap = occ_cap((const void*)fn);
+  return need < 1 ? 1 : (need > cap ? cap : need);
+}
+template <class K> inline int grid_rows(K fn, int64_t n) {
+  const int64_t need = (n + kThreads - 1) / kThreads;
+  const int cap = occ_cap((const void*)fn);
+  return (int)(need < 1 ? 1 : (need > cap ? cap : need));
 }
 
 template <class T> __device__ __forceinline__ V4<T> ld4(const V4<T>* p);

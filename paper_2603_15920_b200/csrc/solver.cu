@@ -61,9 +61,31 @@ __device__ __forceinline__ void sell_apply(const DevMesh<T>& M, int s, int lane,
                                            const T* __restrict__ x, T (&acc)[NC]) {
   const int len = __ldg(&M.ms_len[s]);
   const int base = __ldg(&M.ms_ptr[s]) + lane;
-  for (int j = 0; j < len; ++j) {
+  int j = 0;
+  // batches of 4 incidences: all coefficient / column loads first, then all
+  // gathers, then the FMAs (same summation order), so each thread keeps 8+4
+  // independent loads in flight instead of a dependent chain per entry
+  for (; j + 4 <= len; j += 4) {
+    T a[4];
+    int n[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = __ldg(&coef[base + 32 * (j + u)]);
+      n[u] = __ldg(&M.mnb[base + 32 * (j + u)]);
+    }
+    T v[4][NC];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) v[u][k] = x[(int64_t)n[u] * NC + k];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) acc[k] += a[u] * v[u][k];
+  }
+  for (; j < len; ++j) {
     const int idx = base + 32 * j;
-    const T a = coef[idx];
+    const T a = __ldg(&coef[idx]);
     const int n = __ldg(&M.mnb[idx]);
 #pragma unroll
     for (int k = 0; k < NC; ++k) acc[k] += a * x[(int64_t)n * NC + k];
@@ -460,15 +482,26 @@ __global__ void __launch_bounds__(kThreads) k_cg_init(DevMesh<T> M, const T* __r
   }
 }
 
-// pd = r / diag + beta pd
+// Three kernels per PCG iteration; the x update of iteration k is deferred
+// into the p update of iteration k+1 (x is never read inside the loop), so
+// per iteration the method moves 108 N + 24 F bytes (fp64) instead of
+// 116 N + 24 F.  k_cg_final applies the last pending x update.
+//   k_cg_p:    x += alpha_{k-1} pd_{k-1};  pd_k = r_k / diag + beta_k pd_{k-1}
+//   k_cg_spmv: q = A pd_k; partial pd.q -> alpha_k
+//   k_cg_r:    r_{k+1} = r_k - alpha_k q; partials r.r, r.z -> check, beta
 template <class T>
-__global__ void k_cg_pupd(int n, const T* __restrict__ r, const T* __restrict__ diag, T* __restrict__ pd,
-                          const KCtl* ctl) {
+__global__ void k_cg_p(int n, const T* __restrict__ r, const T* __restrict__ diag, T* __restrict__ pd,
+                       T* __restrict__ x, const KCtl* ctl) {
   if (ctl->done) return;
-  const T beta = (T)ctl->beta;
+  const T beta = (T)ctl->beta, alpha = (T)ctl->alpha;
   const bool first = ctl->it == 0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    pd[i] = first ? r[i] / diag[i] : r[i] / diag[i] + beta * pd[i];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const T z = r[i] / diag[i];
+    if (first) { pd[i] = z; continue; }
+    const T po = pd[i];
+    x[i] += alpha * po;
+    pd[i] = z + beta * po;
+  }
 }
 
 // q = A pd; partial pd.q -> alpha
@@ -481,97 +514,23 @@ __global__ void __launch_bounds__(kThreads) k_cg_spmv(DevMesh<T> M, const T* __r
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
-    T acc[1] = {live ? diag[row] * pd[row] : T(0)};
+    const T pr = live ? pd[row] : T(0);
+    T acc[1] = {live ? diag[row] * pr : T(0)};
     sell_apply<T, 1>(M, s, lane, coef, pd, acc);
-    if (live) { q[row] = acc[0]; v[0] += (double)pd[row] * (double)acc[0]; }
+    if (live) { q[row] = acc[0]; v[0] += (double)pr * (double)acc[0]; }
   }
   double t[1];
   if (grid_sum<1>(v, partials, ticket, t)) {
     KCtl& c = *ctl;
-    if (!(t[0] > 0)) { c.done = 1; c.status = DFVM_E_BREAKDOWN; c.it++; return; }
-    c.alpha = c.rz / t[0];
-  }
-}
-
-// x += alpha pd; r -= alpha q; partials r.r, r.z -> check, beta
-template <class T>
-__global__ void k_cg_update(int n, const T* __restrict__ pd, const T* __restrict__ q, const T* __restrict__ diag,
-                            T* __restrict__ x, T* __restrict__ r, double* partials, unsigned* ticket, KCtl* ctl) {
-  if (ctl->done) return;
-  const T alpha = (T)ctl->alpha;
-  double v[2] = {0, 0};
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    x[i] += alpha * pd[i];
-    const T rr = r[i] - alpha * q[i];
-    r[i] = rr;
-    v[0] += (double)rr * (double)rr;
-    v[1] += (double)rr * (double)rr / (double)diag[i];
-  }
-  double t[2];
-  if (grid_sum<2>(v, partials, ticket, t)) {
-    KCtl& c = *ctl;
-    c.it++;
-    krylov_check(c, sqrt(t[0]));
-    if (!c.done) { c.beta = t[1] / c.rz; c.rz = t[1]; }
-  }
-}
-
-// ---- fused two-kernel PCG iteration (same arithmetic as the three kernels
-// above, fewer HBM passes):
-//   K_A: pd_new = r/diag + beta pd_old for the row AND, on the fly, for every
-//        neighbour it gathers (identical expression -> identical bits);
-//        x += alpha_prev pd_old (the x update of the previous iteration,
-//        deferred because x is never read inside the loop); q = A pd_new;
-//        partial pd_new . q -> alpha.
-//   K_B: r -= alpha q; partials r.r, r.z -> convergence, beta; on exit the
-//        pending x += alpha pd_new is flagged for k_cg_final.
-// pd ping-pongs between two buffers (neighbours read pd_old while pd_new is
-// written).  HBM bytes per iteration: 92 N + 24 F (fp64) vs 112 N + 24 F.
-template <class T>
-__device__ __forceinline__ T cg_pnew(const T* __restrict__ r, const T* __restrict__ diag,
-                                     const T* __restrict__ pd_old, int i, T beta, bool first) {
-  return first ? r[i] / diag[i] : r[i] / diag[i] + beta * pd_old[i];
-}
-
-template <class T>
-__global__ void __launch_bounds__(kThreads) k_cg_fused_a(DevMesh<T> M, const T* __restrict__ diag,
-    const T* __restrict__ coef, const T* __restrict__ r, const T* __restrict__ pd_old, T* __restrict__ pd_new,
-    T* __restrict__ x, T* __restrict__ q, double* partials, unsigned* ticket, KCtl* ctl) {
-  if (ctl->done) return;
-  const bool first = ctl->it == 0;
-  const T beta = (T)ctl->beta, alpha = (T)ctl->alpha;
-  double v[1] = {0};
-  SLICE_LOOP(M) {
-    const int row = s * 32 + lane;
-    const bool live = row < M.n_own;
-    T pr = T(0), acc = T(0);
-    if (live) {
-      pr = cg_pnew(r, diag, pd_old, row, beta, first);
-      pd_new[row] = pr;
-      if (!first) x[row] += alpha * pd_old[row];
-      acc = diag[row] * pr;
-    }
-    const int len = __ldg(&M.ms_len[s]);
-    const int base = __ldg(&M.ms_ptr[s]) + lane;
-    for (int j = 0; j < len; ++j) {
-      const int idx = base + 32 * j;
-      const T a = coef[idx];
-      const int n = __ldg(&M.mnb[idx]);
-      acc += a * cg_pnew(r, diag, pd_old, n, beta, first);
-    }
-    if (live) { q[row] = acc; v[0] += (double)pr * (double)acc; }
-  }
-  double t[1];
-  if (grid_sum<1>(v, partials, ticket, t)) {
-    KCtl& c = *ctl;
+    // breakdown: x already holds x_k (its update was applied by k_cg_p)
     if (!(t[0] > 0)) { c.done = 1; c.status = DFVM_E_BREAKDOWN; c.half = 0; c.it++; return; }
     c.alpha = c.rz / t[0];
   }
 }
 
 template <class T>
-__global__ void k_cg_fused_b(int n, const T* __restrict__ q, const T* __restrict__ diag, T* __restrict__ r,
-                             double* partials, unsigned* ticket, KCtl* ctl) {
+__global__ void k_cg_r(int n, const T* __restrict__ q, const T* __restrict__ diag, T* __restrict__ r,
+                       double* partials, unsigned* ticket, KCtl* ctl) {
   if (ctl->done) return;
   const T alpha = (T)ctl->alpha;
   double v[2] = {0, 0};
@@ -586,7 +545,7 @@ __global__ void k_cg_fused_b(int n, const T* __restrict__ q, const T* __restrict
     KCtl& c = *ctl;
     c.it++;
     krylov_check(c, sqrt(t[0]));
-    if (c.done) c.half = 1;          // x += alpha pd_new still pending
+    if (c.done) c.half = 1;          // x += alpha pd still pending
     else { c.beta = t[1] / c.rz; c.rz = t[1]; }
   }
 }
@@ -959,12 +918,13 @@ template <class T>
 static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol, int maxit,
                           dfvm_solve_report* rep, cudaStream_t st) {
   DevMesh<T>& M = *X.M;
-  const int gs = grid_for_slices(M.n_slices), ge = grid_for(M.n_own);
+  const int gs = grid_slices(k_cg_spmv<T>, M.n_slices), ge = grid_for(M.n_own);
+  const int gp = grid_rows(k_cg_p<T>, M.n_own), gr = grid_rows(k_cg_r<T>, M.n_own);
   KCtl init{};
   init.tol = tol; init.rel_tol = rel_tol; init.maxit = maxit;
   DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, &init, sizeof(KCtl), cudaMemcpyHostToDevice, st));
   if (dfvm_status s2 = halo_exchange(S->m, x, 1, st)) return s2;
-  k_cg_init<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr, X.partials, X.ticket, X.d_ctl);
+  k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr, X.partials, X.ticket, X.d_ctl);
   S->n_launch++;
   if (S->timing && S->ev.size() < 4 * kChunk) {
     while (S->ev.size() < 4 * kChunk) {
@@ -974,19 +934,16 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
     }
   }
   int it_before = 0;
-  T* pbuf[2] = {X.kp, X.kv};   // ping-pong search directions
   for (int it0 = 0;; it0 += kChunk) {
     for (int k = 0; k < kChunk; ++k) {
-      const int it = it0 + k;
-      T* pd_old = pbuf[it & 1];
-      T* pd_new = pbuf[(it + 1) & 1];
-      if (S->timing) { cudaEventRecord(S->ev[4 * k], st); cudaEventRecord(S->ev[4 * k + 1], st); }
-      k_cg_fused_a<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kr, pd_old, pd_new, x, X.kq, X.partials,
-                                               X.ticket, X.d_ctl);
+      if (S->timing) cudaEventRecord(S->ev[4 * k], st);
+      k_cg_p<T><<<gp, kThreads, 0, st>>>(M.n_own, X.kr, X.pdiag, X.kp, x, X.d_ctl);
+      if (S->timing) cudaEventRecord(S->ev[4 * k + 1], st);
+      k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl);
       if (S->timing) cudaEventRecord(S->ev[4 * k + 2], st);
-      k_cg_fused_b<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.pdiag, X.kr, X.partials, X.ticket, X.d_ctl);
+      k_cg_r<T><<<gr, kThreads, 0, st>>>(M.n_own, X.kq, X.pdiag, X.kr, X.partials, X.ticket, X.d_ctl);
       if (S->timing) cudaEventRecord(S->ev[4 * k + 3], st);
-      S->n_launch += 2;
+      S->n_launch += 3;
     }
     DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
     DFVM_CUDA(cudaStreamSynchronize(st));
@@ -1006,8 +963,8 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
   }
   DFVM_CUDA(cudaGetLastError());
   const KCtl& c = *X.h_ctl;
-  if (c.half) {   // deferred x update of the last iteration (its pd is pbuf[it % 2])
-    k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, pbuf[c.it & 1], x, X.d_ctl);
+  if (c.half) {   // deferred x update of the last iteration
+    k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl);
     S->n_launch++;
   }
   if (c.zero_x) DFVM_CUDA(cudaMemsetAsync(x, 0, (size_t)M.n_own * sizeof(T), st));
