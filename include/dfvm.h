@@ -82,6 +82,11 @@ const char* dfvm_version(void);
 typedef struct dfvm_comm dfvm_comm;
 dfvm_status dfvm_comm_unique_id(uint8_t id[128]);
 dfvm_status dfvm_comm_create(int n_ranks, int rank, const uint8_t id[128], int device, dfvm_comm** out);
+/* In-process group of n_ranks communicators (ranks as host threads of one
+ * process, devices[r] per rank; NULL -> all on device 0).  Same partitioned
+ * solver path as NCCL, with device-to-device copies and host barriers: lets
+ * the multi-rank logic run (and be tested) on a single GPU.  out[n_ranks]. */
+dfvm_status dfvm_comm_create_local(int n_ranks, const int* devices, dfvm_comm** out);
 dfvm_status dfvm_comm_destroy(dfvm_comm* c);
 
 /* ------------------------------------------------------------------ mesh
@@ -114,7 +119,8 @@ typedef struct {
   int32_t nonorth;       /* dfvm_nonorth */
   int32_t n_parts;       /* number of ranks (1 = single GPU) */
   int32_t rank;
-  int32_t device;        /* CUDA device ordinal */
+  int32_t device;        /* CUDA device ordinal; < 0: host-only mesh (integer maps and
+                            halo lists only, no device arrays; compute calls fail) */
   int32_t precision;     /* dfvm_dtype */
 } dfvm_mesh_opts;
 

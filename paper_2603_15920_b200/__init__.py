@@ -39,7 +39,7 @@ SYMBOLS = [
     "dfvm_fvc_div", "dfvm_fvm_laplacian_apply", "dfvm_solver_create", "dfvm_pressure_solve",
     "dfvm_momentum_assemble", "dfvm_momentum_apply", "dfvm_piso_step", "dfvm_windkessel_set",
     "dfvm_windkessel_state", "dfvm_windkessel_update", "dfvm_solver_destroy", "dfvm_kernel_launches",
-    "dfvm_solver_set_timing", "dfvm_solver_get_timing",
+    "dfvm_solver_set_timing", "dfvm_solver_get_timing", "dfvm_comm_create_local",
 ]
 
 
@@ -141,6 +141,7 @@ def lib():
         L.dfvm_comm_unique_id.argtypes = [vp]
         L.dfvm_comm_create.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
         L.dfvm_comm_destroy.argtypes = [vp]
+        L.dfvm_comm_create_local.argtypes = [C.c_int, vp, vp]
         _LIB = L
     return _LIB
 
@@ -181,6 +182,21 @@ class Comm:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         _check(L.dfvm_comm_create(n_ranks, rank, C.cast(buf, C.c_void_p), device, C.byref(h)))
         self.h = h.value
+
+    @staticmethod
+    def local_group(n_ranks, devices=None):
+        """n in-process communicators (ranks = host threads), see dfvm.h."""
+        L = lib()
+        hs = (C.c_void_p * n_ranks)()
+        dv = None if devices is None else (C.c_int * n_ranks)(*devices)
+        _check(L.dfvm_comm_create_local(n_ranks, C.cast(dv, C.c_void_p) if dv is not None else None,
+                                        C.cast(hs, C.c_void_p)))
+        out = []
+        for h in hs:
+            c = Comm.__new__(Comm)
+            c.h = h
+            out.append(c)
+        return out
 
     @staticmethod
     def unique_id() -> bytes:

@@ -247,17 +247,21 @@ dfvm_status dfvm_mesh_create(const double* points, int64_t n_points, const int64
   if (opts) o = *opts;
   CHECK_ARG(o.n_parts >= 1 && o.rank >= 0 && o.rank < o.n_parts, "bad n_parts / rank");
   CHECK_ARG(o.precision == DFVM_F64 || o.precision == DFVM_F32, "bad precision");
-  CHECK_ARG(o.n_parts == 1 || comm, "n_parts > 1 needs a communicator");
+  CHECK_ARG(o.n_parts == 1 || comm || o.device < 0, "n_parts > 1 needs a communicator");
   auto t0 = std::chrono::steady_clock::now();
   std::unique_ptr<dfvm_mesh> m(new (std::nothrow) dfvm_mesh());
   if (!m) return DFVM_E_OOM;
-  int ndev = 0;
-  cudaError_t e = cudaGetDeviceCount(&ndev);
-  if (e != cudaSuccess || ndev == 0) {
-    set_error(DFVM_E_CUDA, "no CUDA device available (libdfvm has no CPU fallback)");
-    return DFVM_E_CUDA;
+  const bool host_only = o.device < 0;   // maps / halo lists only (no device arrays, no compute)
+  if (!host_only) {
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+      set_error(DFVM_E_CUDA, "no CUDA device available (libdfvm has no CPU fallback)");
+      return DFVM_E_CUDA;
+    }
+    DFVM_CUDA(cudaSetDevice(o.device));
   }
-  DFVM_CUDA(cudaSetDevice(o.device));
+  m->host_only = host_only;
   m->device = o.device;
   m->precision = o.precision;
   m->comm = comm;
@@ -265,12 +269,14 @@ dfvm_status dfvm_mesh_create(const double* points, int64_t n_points, const int64
                                    n_internal, patches, n_patches, o.nonorth, o.renumber_rcm);
   if (st) return st;
   build_part(m->H, o.n_parts, o.rank, m->part);
-  st = o.precision == DFVM_F64 ? upload_mesh<double>(m.get(), m->d64) : upload_mesh<float>(m.get(), m->d32);
-  if (st) {
-    for (void* p : m->allocations) cudaFree(p);
-    return st;
+  if (!host_only) {
+    st = o.precision == DFVM_F64 ? upload_mesh<double>(m.get(), m->d64) : upload_mesh<float>(m.get(), m->d32);
+    if (st) {
+      for (void* p : m->allocations) cudaFree(p);
+      return st;
+    }
+    DFVM_CUDA(cudaDeviceSynchronize());
   }
-  DFVM_CUDA(cudaDeviceSynchronize());
   m->host_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = m.release();
   return DFVM_OK;
@@ -352,6 +358,7 @@ dfvm_status dfvm_mesh_export_geometry(const dfvm_mesh* m, double* Sf, double* xf
 
 dfvm_status dfvm_mesh_destroy(dfvm_mesh* m) {
   if (!m) return DFVM_OK;
+  if (m->host_only) { delete m; return DFVM_OK; }
   cudaSetDevice(m->device);
   for (void* p : m->allocations) cudaFree(p);
   if (m->d_send) cudaFree(m->d_send);
@@ -366,6 +373,7 @@ static size_t elem_bytes(const dfvm_mesh* m) { return m->precision == DFVM_F64 ?
 
 dfvm_status dfvm_field_bytes(const dfvm_mesh* m, int32_t loc, int32_t n_comp, size_t* bytes) {
   CHECK_ARG(m && bytes && n_comp >= 1 && n_comp <= 9 && loc >= 0 && loc <= 2, "bad field arguments");
+  if (m->host_only) { set_error(DFVM_E_CUDA, "host-only mesh (device < 0) has no device data"); return DFVM_E_CUDA; }
   const int64_t n = loc == DFVM_CELLS ? m->part.n_own + m->part.n_ghost : m->n_faces_local();
   *bytes = (size_t)std::max<int64_t>(n, 1) * n_comp * elem_bytes(m);
   return DFVM_OK;

@@ -1,22 +1,58 @@
-// comm.cpp — multi-GPU plumbing: NCCL communicator
-// bootstrap (unique id broadcast by the caller through torch.distributed),
-// halo exchange of ghost cells and deterministic all-gather reductions.
+// comm.cpp — multi-GPU plumbing.
+//
+// Two transports behind one interface:
+//  * NCCL (production): communicator bootstrapped from a 128-byte unique id
+//    the caller broadcasts with torch.distributed; one process per GPU over
+//    NVLink / NVSwitch.
+//  * local: n ranks as host threads of one process (any devices, including
+//    all on one GPU), device-to-device copies with CUDA-event handshakes and
+//    host barriers.  It runs the identical partitioned solver code path, so
+//    the multi-rank logic (halo slices, rank-order reductions, Windkessel
+//    shares, gauge ownership) is testable on a single B200.
 //
 // Halo: the owned cells adjacent to peer q are packed (send list, ascending
-// new id) and sent; the receive lands directly in the contiguous ghost slice
-// of q (ghosts are ordered by (peer, new id), §8(c) O-9 step 7), so there is
-// no unpack kernel.  Reductions that steer control flow use ncclAllGather of
-// the per-rank partials followed by a fixed rank-order sum on every rank, so
-// every rank sees bitwise-identical Krylov scalars.
+// new id) and land directly in q's contiguous ghost slice for this rank
+// (ghosts are ordered by (peer, new id), §8(c) O-9 step 7): no unpack.
+// Reductions that steer control flow are all-gathers of the per-rank
+// partial totals followed by a fixed rank-order sum on every rank, so all
+// ranks take bitwise-identical decisions.
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "internal.h"
 
+namespace dfvm {
+
+// in-process group shared by the rank threads
+struct LocalGroup {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long generation = 0;
+  int refs = 0;
+  // mailboxes: published per (src, dst) pointer; per-rank events
+  std::vector<const void*> box;      // [n * n]
+  std::vector<cudaEvent_t> posted;  // [n] recorded after the publisher's pack / kernel
+  std::vector<cudaEvent_t> consumed; // [n] recorded after the rank's copies
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const unsigned long g = generation;
+    if (++arrived == n) { arrived = 0; ++generation; cv.notify_all(); }
+    else cv.wait(lk, [&] { return generation != g; });
+  }
+};
+
+}  // namespace dfvm
+
 struct dfvm_comm {
+  int backend = 0;   // 0 NCCL, 1 local
   ncclComm_t nccl = nullptr;
+  dfvm::LocalGroup* grp = nullptr;
   int n_ranks = 1, rank = 0, device = 0;
 };
 
@@ -47,37 +83,82 @@ static dfvm_status ensure_halo_buffers(dfvm_mesh* m) {
   return DFVM_OK;
 }
 
+// local transport: every rank publishes, all wait for everybody's data,
+// copy, then wait until every peer has consumed before the published
+// buffers may be overwritten by the next stream operation.
+static dfvm_status local_finish(LocalGroup* G, int rank, cudaStream_t s) {
+  DFVM_CUDA(cudaEventRecord(G->consumed[rank], s));
+  G->barrier();
+  for (int q = 0; q < G->n; ++q)
+    if (q != rank) DFVM_CUDA(cudaStreamWaitEvent(s, G->consumed[q], 0));
+  G->barrier();
+  return DFVM_OK;
+}
+
 dfvm_status halo_exchange(dfvm_mesh* m, void* data, int nc, cudaStream_t s) {
   const Part& P = m->part;
-  if (P.P == 1 || P.peers.empty()) return DFVM_OK;
+  if (P.P == 1) return DFVM_OK;
   if (!m->comm) { set_error(DFVM_E_NCCL, "multi-part mesh without communicator"); return DFVM_E_NCCL; }
   if (dfvm_status st = ensure_halo_buffers(m)) return st;
   const bool f64 = m->precision == DFVM_F64;
   const size_t eb = f64 ? 8 : 4;
   const int64_t ns = (int64_t)P.send_gid.size();
-  if (f64) launch_pack<double>((double*)m->d_send, (const double*)data, m->d_send_idx, ns, nc, s);
-  else launch_pack<float>((float*)m->d_send, (const float*)data, m->d_send_idx, ns, nc, s);
-  const ncclDataType_t dt = f64 ? ncclFloat64 : ncclFloat32;
-  DFVM_NCCL(ncclGroupStart());
+  if (ns) {
+    if (f64) launch_pack<double>((double*)m->d_send, (const double*)data, m->d_send_idx, ns, nc, s);
+    else launch_pack<float>((float*)m->d_send, (const float*)data, m->d_send_idx, ns, nc, s);
+  }
+  dfvm_comm* C = m->comm;
+  if (C->backend == 0) {
+    const ncclDataType_t dt = f64 ? ncclFloat64 : ncclFloat32;
+    DFVM_NCCL(ncclGroupStart());
+    for (size_t i = 0; i < P.peers.size(); ++i) {
+      const int q = P.peers[i];
+      const int64_t so = P.peer_send_off[i], sn = P.peer_send_off[i + 1] - so;
+      const int64_t go = P.peer_ghost_off[i], gn = P.peer_ghost_off[i + 1] - go;
+      DFVM_NCCL(ncclSend((const char*)m->d_send + so * nc * eb, (size_t)(sn * nc), dt, q, C->nccl, s));
+      DFVM_NCCL(ncclRecv((char*)data + (P.n_own + go) * nc * eb, (size_t)(gn * nc), dt, q, C->nccl, s));
+    }
+    DFVM_NCCL(ncclGroupEnd());
+    return DFVM_OK;
+  }
+  LocalGroup* G = C->grp;
+  const int me = C->rank;
+  for (size_t i = 0; i < P.peers.size(); ++i)
+    G->box[(size_t)me * G->n + P.peers[i]] = (const char*)m->d_send + P.peer_send_off[i] * nc * eb;
+  DFVM_CUDA(cudaEventRecord(G->posted[me], s));
+  G->barrier();
   for (size_t i = 0; i < P.peers.size(); ++i) {
     const int q = P.peers[i];
-    const int64_t so = P.peer_send_off[i], sn = P.peer_send_off[i + 1] - so;
     const int64_t go = P.peer_ghost_off[i], gn = P.peer_ghost_off[i + 1] - go;
-    DFVM_NCCL(ncclSend((const char*)m->d_send + so * nc * eb, (size_t)(sn * nc), dt, q, m->comm->nccl, s));
-    DFVM_NCCL(ncclRecv((char*)data + (P.n_own + go) * nc * eb, (size_t)(gn * nc), dt, q, m->comm->nccl, s));
+    DFVM_CUDA(cudaStreamWaitEvent(s, G->posted[q], 0));
+    DFVM_CUDA(cudaMemcpyAsync((char*)data + (P.n_own + go) * nc * eb, G->box[(size_t)q * G->n + me],
+                              (size_t)(gn * nc) * eb, cudaMemcpyDeviceToDevice, s));
   }
-  DFVM_NCCL(ncclGroupEnd());
-  return DFVM_OK;
+  return local_finish(G, me, s);
 }
 
-// all-gather of `n` doubles per rank into gathered[n_ranks][n]
+// all-gather of `n` doubles per rank into gathered[n_ranks][n] (rank order)
 dfvm_status allgather_f64(dfvm_mesh* m, const double* local, double* gathered, int n, cudaStream_t s) {
   if (m->part.P == 1) {
     if (local != gathered) DFVM_CUDA(cudaMemcpyAsync(gathered, local, n * 8, cudaMemcpyDeviceToDevice, s));
     return DFVM_OK;
   }
-  DFVM_NCCL(ncclAllGather(local, gathered, (size_t)n, ncclFloat64, m->comm->nccl, s));
-  return DFVM_OK;
+  dfvm_comm* C = m->comm;
+  if (C->backend == 0) {
+    DFVM_NCCL(ncclAllGather(local, gathered, (size_t)n, ncclFloat64, C->nccl, s));
+    return DFVM_OK;
+  }
+  LocalGroup* G = C->grp;
+  const int me = C->rank;
+  G->box[(size_t)me * G->n + me] = local;
+  DFVM_CUDA(cudaEventRecord(G->posted[me], s));
+  G->barrier();
+  for (int q = 0; q < G->n; ++q) {
+    if (q != me) DFVM_CUDA(cudaStreamWaitEvent(s, G->posted[q], 0));
+    DFVM_CUDA(cudaMemcpyAsync(gathered + (size_t)q * n, G->box[(size_t)q * G->n + q], n * 8,
+                              cudaMemcpyDeviceToDevice, s));
+  }
+  return local_finish(G, me, s);
 }
 
 }  // namespace dfvm
@@ -110,9 +191,33 @@ dfvm_status dfvm_comm_create(int n_ranks, int rank, const uint8_t id[128], int d
   return DFVM_OK;
 }
 
+dfvm_status dfvm_comm_create_local(int n_ranks, const int* devices, dfvm_comm** out) {
+  if (!out || n_ranks < 1) { set_error(DFVM_E_INVALID_ARG, "bad local communicator arguments"); return DFVM_E_INVALID_ARG; }
+  LocalGroup* G = new LocalGroup();
+  G->n = n_ranks;
+  G->refs = n_ranks;
+  G->box.assign((size_t)n_ranks * n_ranks, nullptr);
+  G->posted.resize(n_ranks);
+  G->consumed.resize(n_ranks);
+  for (int r = 0; r < n_ranks; ++r) {
+    DFVM_CUDA(cudaSetDevice(devices ? devices[r] : 0));
+    DFVM_CUDA(cudaEventCreateWithFlags(&G->posted[r], cudaEventDisableTiming));
+    DFVM_CUDA(cudaEventCreateWithFlags(&G->consumed[r], cudaEventDisableTiming));
+    dfvm_comm* c = new dfvm_comm();
+    c->backend = 1; c->grp = G; c->n_ranks = n_ranks; c->rank = r; c->device = devices ? devices[r] : 0;
+    out[r] = c;
+  }
+  return DFVM_OK;
+}
+
 dfvm_status dfvm_comm_destroy(dfvm_comm* c) {
   if (!c) return DFVM_OK;
   if (c->nccl) ncclCommDestroy(c->nccl);
+  if (c->grp && --c->grp->refs == 0) {
+    for (auto e : c->grp->posted) cudaEventDestroy(e);
+    for (auto e : c->grp->consumed) cudaEventDestroy(e);
+    delete c->grp;
+  }
   delete c;
   return DFVM_OK;
 }

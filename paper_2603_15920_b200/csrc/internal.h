@@ -118,6 +118,7 @@ struct dfvm_mesh {
   std::vector<void*> allocations;
   int64_t device_bytes = 0;
   double host_seconds = 0;
+  bool host_only = false;
   dfvm_comm* comm = nullptr;
   // lazily built device maps for device-side import/export
   int32_t* d_cell_orig = nullptr;   // [n_cells] original id of local cell

@@ -55,6 +55,111 @@ __device__ __forceinline__ void krylov_start(KCtl& c, double bb, double rr) {
   if (c.res0 <= c.thr) { c.done = 1; c.converged = 1; }
 }
 
+// ---- control steps: applied to the global totals t[] of a reduction,
+// either by the last block of the reducing kernel (one rank) or by the
+// finalize kernel after the cross-rank all-gather (rank-order sum), so every
+// rank applies bitwise-identical updates.
+enum CtlKind { CTL_CG_INIT = 0, CTL_CG_SPMV, CTL_CG_R, CTL_BI_INIT, CTL_BI_V, CTL_BI_S, CTL_BI_T, CTL_BI_X };
+
+__device__ void ctl_apply(int kind, KCtl* ctl, const double* t) {
+  switch (kind) {
+    case CTL_CG_INIT: {
+      KCtl& c = *ctl;
+      krylov_start(c, t[0], t[1]);
+      c.rz = t[2]; c.beta = 0.0;
+      break;
+    }
+    case CTL_CG_SPMV: {
+      KCtl& c = *ctl;
+      // breakdown: x already holds x_k (its update was applied by k_cg_p)
+      if (!(t[0] > 0)) { c.done = 1; c.status = DFVM_E_BREAKDOWN; c.half = 0; c.it++; break; }
+      c.alpha = c.rz / t[0];
+      break;
+    }
+    case CTL_CG_R: {
+      KCtl& c = *ctl;
+      c.it++;
+      krylov_check(c, sqrt(t[0]));
+      if (c.done) c.half = 1;          // x += alpha pd still pending
+      else { c.beta = t[1] / c.rz; c.rz = t[1]; }
+      break;
+    }
+    case CTL_BI_INIT:
+      for (int k = 0; k < 3; ++k) {
+        KCtl& c = ctl[k];
+        krylov_start(c, t[k], t[3 + k]);
+        c.rho_old = 1; c.alpha = 1; c.omega = 1; c.rho = t[3 + k];
+        if (!c.done && c.rho == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; }
+      }
+      break;
+    case CTL_BI_V:
+      for (int k = 0; k < 3; ++k) {
+        KCtl& c = ctl[k];
+        if (c.done) continue;
+        c.it++;
+        if (t[k] == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; continue; }
+        c.alpha = c.rho / t[k];
+      }
+      break;
+    case CTL_BI_S:
+      for (int k = 0; k < 3; ++k) {
+        KCtl& c = ctl[k];
+        if (c.done) continue;
+        c.snorm = sqrt(t[k]);
+        if (c.snorm <= c.thr) c.half = 1;
+      }
+      break;
+    case CTL_BI_T:
+      for (int k = 0; k < 3; ++k) {
+        KCtl& c = ctl[k];
+        if (c.done || c.half) continue;
+        if (t[3 + k] == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; continue; }
+        c.omega = t[k] / t[3 + k];
+      }
+      break;
+    case CTL_BI_X:
+      for (int k = 0; k < 3; ++k) {
+        KCtl& c = ctl[k];
+        if (c.done) continue;
+        if (c.half) { c.res = c.snorm; c.converged = 1; c.done = 1; continue; }
+        krylov_check(c, sqrt(t[3 + k]));
+        if (c.done) continue;
+        if (c.omega == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; continue; }
+        c.rho_old = c.rho;
+        c.rho = t[k];
+        if (c.rho == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; }
+      }
+      break;
+  }
+}
+
+// cross-rank reduction target: with one rank the last block applies the
+// control step itself; with several it stores the rank's totals in `local`
+// and the host enqueues all-gather + k_finalize.
+struct Red {
+  int nranks;
+  double* local;
+};
+template <int NV>
+__device__ __forceinline__ void red_finish(const Red& red, int kind, KCtl* ctl, const double (&t)[NV]) {
+  if (red.nranks == 1) { ctl_apply(kind, ctl, t); return; }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) red.local[i] = t[i];
+}
+__global__ void k_finalize(int kind, int nv, const double* __restrict__ all, int P, KCtl* ctl) {
+  // the reducing kernel exited early (and produced no totals) when the solve
+  // was already done; init kernels always run
+  if (kind == CTL_CG_SPMV || kind == CTL_CG_R) { if (ctl->done) return; }
+  else if (kind != CTL_CG_INIT && kind != CTL_BI_INIT) { if (ctl[0].done && ctl[1].done && ctl[2].done) return; }
+  double t[8];
+  for (int i = 0; i < nv; ++i) {
+    double s = 0;
+    for (int r = 0; r < P; ++r) s += all[r * nv + i];   // fixed rank order
+    t[i] = s;
+  }
+  ctl_apply(kind, ctl, t);
+}
+
 // y_row = diag_row x_row + sum_j coef_j x_nb(j) over the matrix SELL entries
 template <class T, int NC>
 __device__ __forceinline__ void sell_apply(const DevMesh<T>& M, int s, int lane, const T* __restrict__ coef,
@@ -383,7 +488,7 @@ __global__ void __launch_bounds__(kThreads) k_Ucorr(DevMesh<T> M, const T* __res
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_continuity(DevMesh<T> M, const T* __restrict__ phi,
     const T* __restrict__ U, const T* __restrict__ p, double* partials, unsigned* ticket, double* out,
-    WKDev* wk, int n_wk) {
+    WKDev* wk, int n_wk, Red red) {
   double mx = 0, sm = 0, nf = 0;
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
@@ -419,33 +524,63 @@ __global__ void __launch_bounds__(kThreads) k_continuity(DevMesh<T> M, const T* 
   if (grid_sum<2>(v, partials, ticket, tot)) {
     double m2 = 0;
     for (unsigned b = 0; b < gridDim.x; ++b) m2 = fmax(m2, __ldcg(&maxp[b]));
+    if (red.nranks > 1) { red.local[0] = m2; red.local[1] = tot[0]; red.local[2] = tot[1]; return; }
     out[0] = m2; out[1] = tot[0]; out[2] = tot[1] > 0 ? 1.0 : 0.0;
     for (int i = 0; i < n_wk; ++i) wk[i].pc_n = wk[i].pc_new;
   }
 }
 
+// cross-rank continuity: max / sum / non-finite over ranks, then the
+// Windkessel commit (every rank holds the same outlet states)
+__global__ void k_continuity_fin(const double* __restrict__ all, int P, double* out, WKDev* wk, int n_wk) {
+  double mx = 0, sm = 0, nf = 0;
+  for (int r = 0; r < P; ++r) { mx = fmax(mx, all[3 * r]); sm += all[3 * r + 1]; nf += all[3 * r + 2]; }
+  out[0] = mx; out[1] = sm; out[2] = nf > 0 ? 1.0 : 0.0;
+  for (int i = 0; i < n_wk; ++i) wk[i].pc_n = wk[i].pc_new;
+}
+
 // Windkessel (eq:windkessel_Q P:406-410, eq:windkessel_discrete P:420-425):
 // one block per outlet; Q = sum_b phi_b (fixed order), p_c^{n+1} from the
 // start-of-step p_c^n (A-19), p_o = p_c + R_p Q, BC value p_o / rho.
+__device__ __forceinline__ double wk_update(WKDev& W, double Q, double dt) {
+  double pc;
+  if (W.scheme == 0) { const double ex = exp(-dt / (W.Rd * W.C)); pc = W.pc_n * ex + W.Rd * Q * (1.0 - ex); }
+  else if (W.scheme == 1) pc = W.pc_n + dt * (Q - W.pc_n / W.Rd) / W.C;
+  else pc = (W.pc_n + dt * Q / W.C) / (1.0 + dt / (W.Rd * W.C));
+  W.pc_new = pc; W.Q = Q; W.p_o = pc + W.Rp * Q;
+  return W.p_o;
+}
+
 template <class T>
 __global__ void k_windkessel(DevMesh<T> M, const T* __restrict__ phi, WKDev* wk, const int* __restrict__ fptr,
-                             const int* __restrict__ faces, double dt, double rho, T* __restrict__ bvp) {
+                             const int* __restrict__ faces, double dt, double rho, T* __restrict__ bvp, Red red) {
   const int o = blockIdx.x;
   double q = 0;
   for (int i = fptr[o] + threadIdx.x; i < fptr[o + 1]; i += blockDim.x) q += (double)phi[M.F + faces[i]];
   __shared__ double sh[32][1];
   double v[1] = {q};
   block_sum<1>(v, sh);
+  if (red.nranks > 1) {          // this rank's share of Q; k_windkessel_fin completes it
+    if (threadIdx.x == 0) red.local[o] = v[0];
+    return;
+  }
+  __shared__ double po_s;
+  if (threadIdx.x == 0) po_s = wk_update(wk[o], v[0], dt) / rho;
+  __syncthreads();
+  for (int i = fptr[o] + threadIdx.x; i < fptr[o + 1]; i += blockDim.x) bvp[faces[i]] = (T)po_s;
+}
+
+// cross-rank Windkessel: Q = rank-order sum of the gathered shares
+template <class T>
+__global__ void k_windkessel_fin(const double* __restrict__ all, int P, int n_wk, WKDev* wk,
+                                 const int* __restrict__ fptr, const int* __restrict__ faces, double dt, double rho,
+                                 T* __restrict__ bvp) {
+  const int o = blockIdx.x;
   __shared__ double po_s;
   if (threadIdx.x == 0) {
-    WKDev& W = wk[o];
-    const double Q = v[0];
-    double pc;
-    if (W.scheme == 0) { const double ex = exp(-dt / (W.Rd * W.C)); pc = W.pc_n * ex + W.Rd * Q * (1.0 - ex); }
-    else if (W.scheme == 1) pc = W.pc_n + dt * (Q - W.pc_n / W.Rd) / W.C;
-    else pc = (W.pc_n + dt * Q / W.C) / (1.0 + dt / (W.Rd * W.C));
-    W.pc_new = pc; W.Q = Q; W.p_o = pc + W.Rp * Q;
-    po_s = W.p_o / rho;
+    double Q = 0;
+    for (int r = 0; r < P; ++r) Q += all[r * n_wk + o];
+    po_s = wk_update(wk[o], Q, dt) / rho;
   }
   __syncthreads();
   for (int i = fptr[o] + threadIdx.x; i < fptr[o + 1]; i += blockDim.x) bvp[faces[i]] = (T)po_s;
@@ -459,7 +594,7 @@ __global__ void k_add_at(T* a, const T* b, int i) { a[i] += b[i]; }
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_cg_init(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ coef, const T* __restrict__ b, const T* __restrict__ x, T* __restrict__ r,
-    double* partials, unsigned* ticket, KCtl* ctl) {
+    double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   double v[3] = {0, 0, 0};
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
@@ -475,11 +610,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_init(DevMesh<T> M, const T* __r
     }
   }
   double t[3];
-  if (grid_sum<3>(v, partials, ticket, t)) {
-    KCtl& c = *ctl;
-    krylov_start(c, t[0], t[1]);
-    c.rz = t[2]; c.beta = 0.0;
-  }
+  if (grid_sum<3>(v, partials, ticket, t)) red_finish<3>(red, CTL_CG_INIT, ctl, t);
 }
 
 // Three kernels per PCG iteration; the x update of iteration k is deferred
@@ -508,7 +639,7 @@ __global__ void k_cg_p(int n, const T* __restrict__ r, const T* __restrict__ dia
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_cg_spmv(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ coef, const T* __restrict__ pd, T* __restrict__ q, double* partials, unsigned* ticket,
-    KCtl* ctl) {
+    KCtl* ctl, Red red) {
   if (ctl->done) return;
   double v[1] = {0};
   SLICE_LOOP(M) {
@@ -520,17 +651,12 @@ __global__ void __launch_bounds__(kThreads) k_cg_spmv(DevMesh<T> M, const T* __r
     if (live) { q[row] = acc[0]; v[0] += (double)pr * (double)acc[0]; }
   }
   double t[1];
-  if (grid_sum<1>(v, partials, ticket, t)) {
-    KCtl& c = *ctl;
-    // breakdown: x already holds x_k (its update was applied by k_cg_p)
-    if (!(t[0] > 0)) { c.done = 1; c.status = DFVM_E_BREAKDOWN; c.half = 0; c.it++; return; }
-    c.alpha = c.rz / t[0];
-  }
+  if (grid_sum<1>(v, partials, ticket, t)) red_finish<1>(red, CTL_CG_SPMV, ctl, t);
 }
 
 template <class T>
 __global__ void k_cg_r(int n, const T* __restrict__ q, const T* __restrict__ diag, T* __restrict__ r,
-                       double* partials, unsigned* ticket, KCtl* ctl) {
+                       double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   if (ctl->done) return;
   const T alpha = (T)ctl->alpha;
   double v[2] = {0, 0};
@@ -541,13 +667,7 @@ __global__ void k_cg_r(int n, const T* __restrict__ q, const T* __restrict__ dia
     v[1] += (double)rr * (double)rr / (double)diag[i];
   }
   double t[2];
-  if (grid_sum<2>(v, partials, ticket, t)) {
-    KCtl& c = *ctl;
-    c.it++;
-    krylov_check(c, sqrt(t[0]));
-    if (c.done) c.half = 1;          // x += alpha pd still pending
-    else { c.beta = t[1] / c.rz; c.rz = t[1]; }
-  }
+  if (grid_sum<2>(v, partials, ticket, t)) red_finish<2>(red, CTL_CG_R, ctl, t);
 }
 
 // the deferred x update of the final iteration
@@ -567,7 +687,7 @@ __device__ __forceinline__ bool all_done(const KCtl* c) { return c[0].done && c[
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_bi_init(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ coef, const T* __restrict__ b, const T* __restrict__ x, T* __restrict__ r,
-    T* __restrict__ rh, T* __restrict__ p, T* __restrict__ v, double* partials, unsigned* ticket, KCtl* ctl) {
+    T* __restrict__ rh, T* __restrict__ p, T* __restrict__ v, double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   double a[6] = {0, 0, 0, 0, 0, 0};
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
@@ -588,14 +708,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(DevMesh<T> M, const T* __r
       }
   }
   double t[6];
-  if (grid_sum<6>(a, partials, ticket, t)) {
-    for (int k = 0; k < 3; ++k) {
-      KCtl& c = ctl[k];
-      krylov_start(c, t[k], t[3 + k]);
-      c.rho_old = 1; c.alpha = 1; c.omega = 1; c.rho = t[3 + k];
-      if (!c.done && c.rho == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; }
-    }
-  }
+  if (grid_sum<6>(a, partials, ticket, t)) red_finish<6>(red, CTL_BI_INIT, ctl, t);
 }
 
 // p = r + beta (p - omega v); y = p / diag
@@ -628,7 +741,7 @@ __global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ dia
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_bi_v(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ coef, const T* __restrict__ y, const T* __restrict__ rh, T* __restrict__ v,
-    double* partials, unsigned* ticket, KCtl* ctl) {
+    double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   if (all_done(ctl)) return;
   double a[3] = {0, 0, 0};
   SLICE_LOOP(M) {
@@ -648,21 +761,13 @@ __global__ void __launch_bounds__(kThreads) k_bi_v(DevMesh<T> M, const T* __rest
       }
   }
   double t[3];
-  if (grid_sum<3>(a, partials, ticket, t)) {
-    for (int k = 0; k < 3; ++k) {
-      KCtl& c = ctl[k];
-      if (c.done) continue;
-      c.it++;
-      if (t[k] == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; continue; }
-      c.alpha = c.rho / t[k];
-    }
-  }
+  if (grid_sum<3>(a, partials, ticket, t)) red_finish<3>(red, CTL_BI_V, ctl, t);
 }
 
 // s = r - alpha v; partial (s, s) -> half-step convergence
 template <class T>
 __global__ void k_bi_s(int n, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ sv,
-                       double* partials, unsigned* ticket, KCtl* ctl) {
+                       double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   if (all_done(ctl)) return;
   T al[3];
   bool act[3];
@@ -679,21 +784,14 @@ __global__ void k_bi_s(int n, const T* __restrict__ r, const T* __restrict__ v, 
       a[k] += (double)ss * (double)ss;
     }
   double t[3];
-  if (grid_sum<3>(a, partials, ticket, t)) {
-    for (int k = 0; k < 3; ++k) {
-      KCtl& c = ctl[k];
-      if (c.done) continue;
-      c.snorm = sqrt(t[k]);
-      if (c.snorm <= c.thr) c.half = 1;
-    }
-  }
+  if (grid_sum<3>(a, partials, ticket, t)) red_finish<3>(red, CTL_BI_S, ctl, t);
 }
 
 // t = A (s / diag); partials (t, s), (t, t) -> omega
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_bi_t(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ coef, const T* __restrict__ sv, T* __restrict__ tv, double* partials, unsigned* ticket,
-    KCtl* ctl) {
+    KCtl* ctl, Red red) {
   if (all_done(ctl)) return;
   double a[6] = {0, 0, 0, 0, 0, 0};
   SLICE_LOOP(M) {
@@ -723,21 +821,14 @@ __global__ void __launch_bounds__(kThreads) k_bi_t(DevMesh<T> M, const T* __rest
       }
   }
   double t[6];
-  if (grid_sum<6>(a, partials, ticket, t)) {
-    for (int k = 0; k < 3; ++k) {
-      KCtl& c = ctl[k];
-      if (c.done || c.half) continue;
-      if (t[3 + k] == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; continue; }
-      c.omega = t[k] / t[3 + k];
-    }
-  }
+  if (grid_sum<6>(a, partials, ticket, t)) red_finish<6>(red, CTL_BI_T, ctl, t);
 }
 
 // x += alpha y + omega s/diag; r = s - omega t; partials (rh, r), (r, r)
 template <class T>
 __global__ void k_bi_x(int n, const T* __restrict__ diag, const T* __restrict__ y, const T* __restrict__ sv,
                        const T* __restrict__ tv, const T* __restrict__ rh, T* __restrict__ x, T* __restrict__ r,
-                       double* partials, unsigned* ticket, KCtl* ctl) {
+                       double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   if (all_done(ctl)) return;
   T al[3], om[3];
   int mode[3];   // 0 skip, 1 half step, 2 full step
@@ -763,19 +854,7 @@ __global__ void k_bi_x(int n, const T* __restrict__ diag, const T* __restrict__ 
     }
   }
   double t[6];
-  if (grid_sum<6>(a, partials, ticket, t)) {
-    for (int k = 0; k < 3; ++k) {
-      KCtl& c = ctl[k];
-      if (c.done) continue;
-      if (c.half) { c.res = c.snorm; c.converged = 1; c.done = 1; continue; }
-      krylov_check(c, sqrt(t[3 + k]));
-      if (c.done) continue;
-      if (c.omega == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; continue; }
-      c.rho_old = c.rho;
-      c.rho = t[k];
-      if (c.rho == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; }
-    }
-  }
+  if (grid_sum<6>(a, partials, ticket, t)) red_finish<6>(red, CTL_BI_X, ctl, t);
 }
 
 // ============================================================ host side
@@ -798,6 +877,8 @@ struct SolverT : SolverBase {
   KCtl* h_ctl = nullptr;   // pinned
   double* d_cont = nullptr;
   double* h_cont = nullptr;  // pinned
+  double* red_local = nullptr;  // [8] this rank's reduction totals (P > 1)
+  double* red_all = nullptr;    // [P][8] all-gathered totals
   WKDev* d_wk = nullptr;
   WKDev* h_wk = nullptr;     // pinned
   int* d_wk_ptr = nullptr;
@@ -829,7 +910,7 @@ struct SolverT : SolverBase {
         (st = al(&krh, 3 * nc)) || (st = al(&kp, 3 * nc)) || (st = al(&kq, 3 * nc)) || (st = al(&kv, 3 * nc)) ||
         (st = al(&ky, 3 * nc)) || (st = al(&ks, 3 * nc)) || (st = al(&kt, 3 * nc)) ||
         (st = al(&partials, (size_t)kMaxBlocks * 8)) || (st = al(&ticket, 4)) || (st = al(&d_ctl, 4)) ||
-        (st = al(&d_cont, 4)))
+        (st = al(&d_cont, 8)) || (st = al(&red_local, 128)) || (st = al(&red_all, (size_t)128 * mm->part.P)))
       return st;
     DFVM_CUDA(cudaMallocHost(&h_ctl, 4 * sizeof(KCtl)));
     DFVM_CUDA(cudaMallocHost(&h_cont, 4 * sizeof(double)));
@@ -913,24 +994,42 @@ static void fill_report(const KCtl& c, dfvm_solve_report* r) {
 
 constexpr int kChunk = 8;
 
+dfvm_status allgather_f64(dfvm_mesh* m, const double* local, double* gathered, int n, cudaStream_t s);
+
+// cross-rank completion of a reduction: all-gather of the per-rank totals
+// then the rank-order sum + control step (k_finalize); no-op on one rank
+template <class T>
+static dfvm_status fin(dfvm_solver* S, SolverT<T>& X, int kind, int nv, cudaStream_t st) {
+  if (S->m->part.P == 1) return DFVM_OK;
+  if (dfvm_status e = allgather_f64(S->m, X.red_local, X.red_all, nv, st)) return e;
+  k_finalize<<<1, 1, 0, st>>>(kind, nv, X.red_all, S->m->part.P, X.d_ctl);
+  S->n_launch++;
+  return DFVM_OK;
+}
+
 // Jacobi PCG on (pdiag, pcoef): x warm start, b rhs
 template <class T>
 static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol, int maxit,
                           dfvm_solve_report* rep, cudaStream_t st) {
   DevMesh<T>& M = *X.M;
+  dfvm_mesh* m = S->m;
+  const Red red{m->part.P, X.red_local};
   const int gs = grid_slices(k_cg_spmv<T>, M.n_slices), ge = grid_for(M.n_own);
   const int gp = grid_rows(k_cg_p<T>, M.n_own), gr = grid_rows(k_cg_r<T>, M.n_own);
   KCtl init{};
   init.tol = tol; init.rel_tol = rel_tol; init.maxit = maxit;
   DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, &init, sizeof(KCtl), cudaMemcpyHostToDevice, st));
-  if (dfvm_status s2 = halo_exchange(S->m, x, 1, st)) return s2;
-  k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr, X.partials, X.ticket, X.d_ctl);
+  dfvm_status e;
+  if ((e = halo_exchange(m, x, 1, st))) return e;
+  k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr,
+                                                                          X.partials, X.ticket, X.d_ctl, red);
   S->n_launch++;
+  if ((e = fin(S, X, CTL_CG_INIT, 3, st))) return e;
   if (S->timing && S->ev.size() < 4 * kChunk) {
     while (S->ev.size() < 4 * kChunk) {
-      cudaEvent_t e;
-      DFVM_CUDA(cudaEventCreate(&e));
-      S->ev.push_back(e);
+      cudaEvent_t ev;
+      DFVM_CUDA(cudaEventCreate(&ev));
+      S->ev.push_back(ev);
     }
   }
   int it_before = 0;
@@ -938,10 +1037,13 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
     for (int k = 0; k < kChunk; ++k) {
       if (S->timing) cudaEventRecord(S->ev[4 * k], st);
       k_cg_p<T><<<gp, kThreads, 0, st>>>(M.n_own, X.kr, X.pdiag, X.kp, x, X.d_ctl);
+      if ((e = halo_exchange(m, X.kp, 1, st))) return e;
       if (S->timing) cudaEventRecord(S->ev[4 * k + 1], st);
-      k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl);
+      k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red);
       if (S->timing) cudaEventRecord(S->ev[4 * k + 2], st);
-      k_cg_r<T><<<gr, kThreads, 0, st>>>(M.n_own, X.kq, X.pdiag, X.kr, X.partials, X.ticket, X.d_ctl);
+      if ((e = fin(S, X, CTL_CG_SPMV, 1, st))) return e;
+      k_cg_r<T><<<gr, kThreads, 0, st>>>(M.n_own, X.kq, X.pdiag, X.kr, X.partials, X.ticket, X.d_ctl, red);
+      if ((e = fin(S, X, CTL_CG_R, 2, st))) return e;
       if (S->timing) cudaEventRecord(S->ev[4 * k + 3], st);
       S->n_launch += 3;
     }
@@ -972,24 +1074,39 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
   return (dfvm_status)(c.status == DFVM_E_BREAKDOWN ? DFVM_E_BREAKDOWN : (c.converged ? DFVM_OK : DFVM_E_NOT_CONVERGED));
 }
 
-// 3-component BiCGStab on (udiag, ucoef): x = U (warm start), b = rhsU
+// 3-component BiCGStab on (udiag, ucoef): x = U (warm start), b = rhsU.
+// Ghosts: x and udiag are exchanged by the caller (assemble); y and s are
+// exchanged before the applies that gather them.
 template <class T>
 static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol,
                                 int maxit, dfvm_solve_report* rep, cudaStream_t st) {
   DevMesh<T>& M = *X.M;
-  const int gs = grid_for_slices(M.n_slices), ge = grid_for(M.n_own);
+  dfvm_mesh* m = S->m;
+  const Red red{m->part.P, X.red_local};
+  const int gs = grid_slices(k_bi_v<T>, M.n_slices), gt = grid_slices(k_bi_t<T>, M.n_slices);
+  const int ge = grid_for(M.n_own);
   KCtl init[3] = {};
   for (int k = 0; k < 3; ++k) { init[k].tol = tol; init[k].rel_tol = rel_tol; init[k].maxit = maxit; }
   DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, init, 3 * sizeof(KCtl), cudaMemcpyHostToDevice, st));
-  k_bi_init<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr, X.krh, X.kp, X.kv, X.partials, X.ticket, X.d_ctl);
+  dfvm_status e;
+  k_bi_init<T><<<grid_slices(k_bi_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr, X.krh,
+                                                                          X.kp, X.kv, X.partials, X.ticket, X.d_ctl, red);
   S->n_launch++;
+  if ((e = fin(S, X, CTL_BI_INIT, 6, st))) return e;
   for (;;) {
     for (int k = 0; k < kChunk; ++k) {
       k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.udiag, X.kv, X.kp, X.ky, X.d_ctl);
-      k_bi_v<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.ky, X.krh, X.kv, X.partials, X.ticket, X.d_ctl);
-      k_bi_s<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.ks, X.partials, X.ticket, X.d_ctl);
-      k_bi_t<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.ks, X.kt, X.partials, X.ticket, X.d_ctl);
-      k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udiag, X.ky, X.ks, X.kt, X.krh, x, X.kr, X.partials, X.ticket, X.d_ctl);
+      if ((e = halo_exchange(m, X.ky, 3, st))) return e;
+      k_bi_v<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.ky, X.krh, X.kv, X.partials, X.ticket, X.d_ctl, red);
+      if ((e = fin(S, X, CTL_BI_V, 3, st))) return e;
+      k_bi_s<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.ks, X.partials, X.ticket, X.d_ctl, red);
+      if ((e = fin(S, X, CTL_BI_S, 3, st))) return e;
+      if ((e = halo_exchange(m, X.ks, 3, st))) return e;
+      k_bi_t<T><<<gt, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.ks, X.kt, X.partials, X.ticket, X.d_ctl, red);
+      if ((e = fin(S, X, CTL_BI_T, 6, st))) return e;
+      k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udiag, X.ky, X.ks, X.kt, X.krh, x, X.kr, X.partials, X.ticket,
+                                         X.d_ctl, red);
+      if ((e = fin(S, X, CTL_BI_X, 6, st))) return e;
       S->n_launch += 5;
     }
     DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, 3 * sizeof(KCtl), cudaMemcpyDeviceToHost, st));
@@ -1027,6 +1144,7 @@ static dfvm_status assemble(dfvm_solver* S, SolverT<T>& X, const T* U, const T* 
                                              (T)S->o.nu, (T)(1.0 / S->o.dt), S->o.convection == 0 ? 1 : 0,
                                              S->kcorr, X.udiag, X.bU, X.rhsU, X.ucoef);
   S->n_launch++;
+  if ((s2 = halo_exchange(S->m, X.udiag, 1, st))) return s2;   // k_bi_t gathers s / diag
   X.assembled = true;
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
@@ -1062,8 +1180,15 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   for (int corr = 1; corr <= o.n_corr; ++corr) {
     // 3.1 Windkessel
     if (n_wk) {
-      k_windkessel<T><<<n_wk, kThreads, 0, st>>>(M, phi, X.d_wk, X.d_wk_ptr, X.d_wk_faces, o.dt, o.rho, bvp);
+      k_windkessel<T><<<n_wk, kThreads, 0, st>>>(M, phi, X.d_wk, X.d_wk_ptr, X.d_wk_faces, o.dt, o.rho, bvp,
+                                                 Red{S->m->part.P, X.red_local});
       S->n_launch++;
+      if (S->m->part.P > 1) {
+        if ((s2 = allgather_f64(S->m, X.red_local, X.red_all, n_wk, st))) return s2;
+        k_windkessel_fin<T><<<n_wk, kThreads, 0, st>>>(X.red_all, S->m->part.P, n_wk, X.d_wk, X.d_wk_ptr,
+                                                       X.d_wk_faces, o.dt, o.rho, bvp);
+        S->n_launch++;
+      }
     }
     // 3.2 rAU, HbyA
     if ((s2 = halo_exchange(S->m, U, 3, st))) return s2;
@@ -1111,8 +1236,14 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   }
   R->n_p = np;
   // 4. continuity + non-finite + Windkessel commit
-  k_continuity<T><<<gs, kThreads, 0, st>>>(M, phi, U, p, X.partials, X.ticket, X.d_cont, X.d_wk, n_wk);
+  k_continuity<T><<<gs, kThreads, 0, st>>>(M, phi, U, p, X.partials, X.ticket, X.d_cont, X.d_wk, n_wk,
+                                           Red{S->m->part.P, X.red_local});
   S->n_launch++;
+  if (S->m->part.P > 1) {
+    if ((s2 = allgather_f64(S->m, X.red_local, X.red_all, 3, st))) return s2;
+    k_continuity_fin<<<1, 1, 0, st>>>(X.red_all, S->m->part.P, X.d_cont, X.d_wk, n_wk);
+    S->n_launch++;
+  }
   DFVM_CUDA(cudaMemcpyAsync(X.h_cont, X.d_cont, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   if (n_wk) DFVM_CUDA(cudaMemcpyAsync(X.h_wk, X.d_wk, n_wk * sizeof(WKDev), cudaMemcpyDeviceToHost, st));
   DFVM_CUDA(cudaStreamSynchronize(st));
@@ -1243,7 +1374,6 @@ dfvm_status dfvm_piso_step(dfvm_solver* s, dfvm_field* U, dfvm_field* p, dfvm_fi
   if ((st = check_f(U, s->m, true, 3, "U")) || (st = check_f(p, s->m, true, 1, "p")) ||
       (st = check_f(phi, s->m, false, 1, "phi")))
     return st;
-  if (s->m->part.P > 1) { set_error(DFVM_E_INVALID_ARG, "multi-rank PISO solver: use n_parts == 1 (multi-GPU Krylov reductions not built in this version)"); return DFVM_E_INVALID_ARG; }
   cudaSetDevice(s->m->device);
   s->fixed_p = solver_has_fixed_p(s);
   dfvm_step_report local;
@@ -1292,7 +1422,6 @@ dfvm_status dfvm_pressure_solve(dfvm_solver* s, const dfvm_field* rAU, const dfv
   if ((st = check_f(rAU, s->m, true, 1, "rAU")) || (st = check_f(rhs, s->m, true, 1, "rhs")) ||
       (st = check_f(p, s->m, true, 1, "p")))
     return st;
-  if (s->m->part.P > 1) { set_error(DFVM_E_INVALID_ARG, "multi-rank pressure solve not built in this version"); return DFVM_E_INVALID_ARG; }
   cudaSetDevice(s->m->device);
   s->fixed_p = solver_has_fixed_p(s);
   cudaStream_t cs = (cudaStream_t)stream;

@@ -1,0 +1,144 @@
+"""Multi-rank CUDA path on one B200: P ranks as host
+threads sharing the device through the library's in-process communicator
+(same partitioned kernels, halo slices and rank-order reductions as the
+NCCL path).  Results gathered from the ranks must match the 1-rank run:
+operators <= 1e-12 relative (only the per-cell summation order may differ —
+in fact it does not, so they are bitwise equal), PISO fields <= 1e-10
+relative (Krylov scalars are summed in a different grouping)."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2603_15920_b200 as dfvm
+import synth
+from gpu_common import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TIGHT = dict(p_tol=1e-13, U_tol=1e-13, p_maxit=20000, U_maxit=2000)
+
+
+def _run_threads(fns):
+    errs = []
+
+    def wrap(f):
+        try:
+            f()
+        except Exception as e:   # surface in the main thread
+            errs.append(e)
+    ts = [threading.Thread(target=wrap, args=(f,), daemon=True) for f in fns]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0]
+
+
+def _streams(P):
+    import torch
+    torch.cuda.set_device(0)
+    ss = [torch.cuda.Stream() for _ in range(P)]
+    return ss, [dfvm.C.c_void_p(s.cuda_stream) for s in ss]
+
+
+def _pipe():
+    return synth.pipe(6, 3, 24, 0.5, 1.2, tets=True, scramble=21)
+
+
+PIPE_BCS = [("inlet", "U", dfvm.BC_PARABOLIC, dict(u_max=2.0, center=(0, 0, 0), radius=0.5)),
+            ("wall", "U", dfvm.BC_FIXED, dict(value=(0, 0, 0))), ("outlet", "U", dfvm.BC_ZEROGRAD, {}),
+            ("inlet", "p", dfvm.BC_ZEROGRAD, {}), ("wall", "p", dfvm.BC_ZEROGRAD, {})]
+
+
+def _bcs(m, outlet_p=True):
+    b = dfvm.BCs(m)
+    for pn, f, k, kw in PIPE_BCS:
+        b.set(pn, f, k, **kw)
+    if outlet_p:
+        b.set("outlet", "p", dfvm.BC_FIXED, 0.0)
+    return b
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_operators_partitioned_equal_single(P):
+    raw = _pipe()
+    x = synth.cell_field(100, raw.n_cells)
+    m1 = dfvm.Mesh(raw)
+    b1 = _bcs(m1)
+    y1 = m1.field("cells", 1)
+    dfvm.laplacian(m1, b1, "p", m1.field("cells", 1, x), y1)
+    G1 = m1.field("cells", 3)
+    dfvm.grad(m1, m1.field("cells", 1, x), b1, "p", G1)
+    ref_y, ref_G = y1.get(), G1.get()
+    comms = dfvm.Comm.local_group(P)
+    ms = [dfvm.Mesh(raw, n_parts=P, rank=r, comm=comms[r]) for r in range(P)]
+    bs = [_bcs(m) for m in ms]
+    ys = [m.field("cells", 1) for m in ms]
+    Gs = [m.field("cells", 3) for m in ms]
+    xs = [m.field("cells", 1, x) for m in ms]
+    _, sp = _streams(P)
+
+    def work(r):
+        def f():
+            dfvm.laplacian(ms[r], bs[r], "p", xs[r], ys[r], stream=sp[r])
+            dfvm.grad(ms[r], xs[r], bs[r], "p", Gs[r], stream=sp[r])
+        return f
+    _run_threads([work(r) for r in range(P)])
+    y = np.zeros(raw.n_cells)
+    G = np.zeros((raw.n_cells, 3))
+    for r in range(P):
+        ys[r].get(sp[r], out=y.reshape(-1, 1))
+        Gs[r].get(sp[r], out=G)
+    assert np.array_equal(y, ref_y) and np.array_equal(G, ref_G)
+
+
+@pytest.mark.parametrize("P,wk", [(2, False), (3, False), (2, True)])
+def test_piso_partitioned_matches_single(P, wk):
+    raw = _pipe()
+    mo = oracle.Mesh(raw)
+    U0 = np.zeros((raw.n_cells, 3))
+    U0[:, 2] = 2.0 * (1 - 4 * (mo.xc[:, 0] ** 2 + mo.xc[:, 1] ** 2))
+    U0 += 0.01 * synth.cell_field(21, raw.n_cells, 3)
+    phi0 = np.zeros(mo.NF)
+    kw = dict(nu=0.1, dt=0.005, n_corr=2, n_nonorth=1, convection="upwind", **TIGHT)
+    wkargs = (0.1, 1.1111, 0.9, 0.0, 0)
+
+    def setup(m):
+        b = _bcs(m, outlet_p=not wk)
+        S = dfvm.Solver(m, b, **kw)
+        if wk:
+            S.windkessel_set("outlet", *wkargs)
+        return b, S, m.field("cells", 3, U0), m.field("cells", 1), m.field("flux", 1, phi0)
+    m1 = dfvm.Mesh(raw)
+    b1, S1, U1, p1, f1 = setup(m1)
+    for _ in range(3):
+        r1 = S1.step(U1, p1, f1)
+    refU, refp, refphi = U1.get(), p1.get(), f1.get()
+
+    comms = dfvm.Comm.local_group(P)
+    ms = [dfvm.Mesh(raw, n_parts=P, rank=r, comm=comms[r]) for r in range(P)]
+    st = [setup(m) for m in ms]
+    _, sp = _streams(P)
+    reps = [None] * P
+
+    def work(r):
+        def f():
+            for _ in range(3):
+                reps[r] = st[r][1].step(st[r][2], st[r][3], st[r][4], stream=sp[r])
+        return f
+    _run_threads([work(r) for r in range(P)])
+    U = np.zeros((raw.n_cells, 3)); p = np.zeros((raw.n_cells, 1)); phi = np.zeros((mo.NF, 1))
+    for r in range(P):
+        st[r][2].get(sp[r], out=U); st[r][3].get(sp[r], out=p); st[r][4].get(sp[r], out=phi)
+    assert rel_l2(U, refU) <= 1e-10 and rel_l2(p[:, 0], refp) <= 1e-10 and rel_l2(phi[:, 0], refphi) <= 1e-10
+    # every rank took the same Krylov decisions and sees the same global reports
+    for r in range(1, P):
+        assert [x["it"] for x in reps[r]["p"]] == [x["it"] for x in reps[0]["p"]]
+        assert reps[r]["cont_err_max"] == reps[0]["cont_err_max"]
+    assert abs(reps[0]["cont_err_max"] - r1["cont_err_max"]) <= 1e-12
+    if wk:
+        for r in range(P):
+            assert np.allclose(reps[r]["Q"], r1["Q"], rtol=1e-10) and np.allclose(reps[r]["p_o"], r1["p_o"], rtol=1e-10)
