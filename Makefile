@@ -36,7 +36,7 @@ build/%.cu.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; exit 1)
 
 $(PKG)/libdfvm.so: $(HOST_OBJ) $(DEV_OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lcudart -lnccl
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -fopenmp -lcudart -ldl
 
 clean:
 	rm -rf build synth/libsynth.so oracle/liboracle.so $(PKG)/libdfvm.so

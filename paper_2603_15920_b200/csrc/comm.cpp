@@ -16,6 +16,7 @@
 // Reductions that steer control flow are all-gathers of the per-rank
 // partial totals followed by a fixed rank-order sum on every rank, so all
 // ranks take bitwise-identical decisions.
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <condition_variable>
@@ -58,11 +59,44 @@ struct dfvm_comm {
 
 namespace dfvm {
 
+// NCCL is resolved lazily (dlopen) when the first NCCL communicator is
+// created: the library has no link-time NCCL dependency, so loading it never
+// shadows the NCCL build a host framework (torch) brings; dlopen of the
+// soname returns the copy already loaded in the process.
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  const char* (*GetErrorString)(ncclResult_t);
+};
+static NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a{};
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+#define SYM(name, field) a.field = reinterpret_cast<decltype(a.field)>(dlsym(h, name)); if (!a.field) return a;
+    SYM("ncclGetUniqueId", GetUniqueId) SYM("ncclCommInitRank", CommInitRank) SYM("ncclCommDestroy", CommDestroy)
+    SYM("ncclGroupStart", GroupStart) SYM("ncclGroupEnd", GroupEnd) SYM("ncclSend", Send) SYM("ncclRecv", Recv)
+    SYM("ncclAllGather", AllGather) SYM("ncclGetErrorString", GetErrorString)
+#undef SYM
+    a.ok = true;
+    return a;
+  }();
+  return api;
+}
+
 template <class T>
 void launch_pack(T* buf, const T* x, const int32_t* idx, int64_t n, int nc, cudaStream_t s);
 
 static dfvm_status nccl_error(ncclResult_t r, const char* where) {
-  set_error(DFVM_E_NCCL, std::string(where) + ": " + ncclGetErrorString(r));
+  set_error(DFVM_E_NCCL, std::string(where) + ": " + (nccl().ok ? nccl().GetErrorString(r) : "libnccl.so.2 not loadable"));
   return DFVM_E_NCCL;
 }
 #define DFVM_NCCL(call)                                          \
@@ -110,15 +144,15 @@ dfvm_status halo_exchange(dfvm_mesh* m, void* data, int nc, cudaStream_t s) {
   dfvm_comm* C = m->comm;
   if (C->backend == 0) {
     const ncclDataType_t dt = f64 ? ncclFloat64 : ncclFloat32;
-    DFVM_NCCL(ncclGroupStart());
+    DFVM_NCCL(nccl().GroupStart());
     for (size_t i = 0; i < P.peers.size(); ++i) {
       const int q = P.peers[i];
       const int64_t so = P.peer_send_off[i], sn = P.peer_send_off[i + 1] - so;
       const int64_t go = P.peer_ghost_off[i], gn = P.peer_ghost_off[i + 1] - go;
-      DFVM_NCCL(ncclSend((const char*)m->d_send + so * nc * eb, (size_t)(sn * nc), dt, q, C->nccl, s));
-      DFVM_NCCL(ncclRecv((char*)data + (P.n_own + go) * nc * eb, (size_t)(gn * nc), dt, q, C->nccl, s));
+      DFVM_NCCL(nccl().Send((const char*)m->d_send + so * nc * eb, (size_t)(sn * nc), dt, q, C->nccl, s));
+      DFVM_NCCL(nccl().Recv((char*)data + (P.n_own + go) * nc * eb, (size_t)(gn * nc), dt, q, C->nccl, s));
     }
-    DFVM_NCCL(ncclGroupEnd());
+    DFVM_NCCL(nccl().GroupEnd());
     return DFVM_OK;
   }
   LocalGroup* G = C->grp;
@@ -145,7 +179,7 @@ dfvm_status allgather_f64(dfvm_mesh* m, const double* local, double* gathered, i
   }
   dfvm_comm* C = m->comm;
   if (C->backend == 0) {
-    DFVM_NCCL(ncclAllGather(local, gathered, (size_t)n, ncclFloat64, C->nccl, s));
+    DFVM_NCCL(nccl().AllGather(local, gathered, (size_t)n, ncclFloat64, C->nccl, s));
     return DFVM_OK;
   }
   LocalGroup* G = C->grp;
@@ -169,7 +203,8 @@ extern "C" {
 
 dfvm_status dfvm_comm_unique_id(uint8_t id[128]) {
   ncclUniqueId u;
-  DFVM_NCCL(ncclGetUniqueId(&u));
+  if (!nccl().ok) return nccl_error(ncclSystemError, "dlopen(libnccl.so.2)");
+  DFVM_NCCL(nccl().GetUniqueId(&u));
   static_assert(sizeof(u) == 128, "ncclUniqueId must be 128 bytes");
   std::memcpy(id, &u, 128);
   return DFVM_OK;
@@ -185,7 +220,8 @@ dfvm_status dfvm_comm_create(int n_ranks, int rank, const uint8_t id[128], int d
   std::memcpy(&u, id, 128);
   dfvm_comm* c = new dfvm_comm();
   c->n_ranks = n_ranks; c->rank = rank; c->device = device;
-  ncclResult_t r = ncclCommInitRank(&c->nccl, n_ranks, u, rank);
+  if (!nccl().ok) { delete c; return nccl_error(ncclSystemError, "dlopen(libnccl.so.2)"); }
+  ncclResult_t r = nccl().CommInitRank(&c->nccl, n_ranks, u, rank);
   if (r != ncclSuccess) { delete c; return nccl_error(r, "ncclCommInitRank"); }
   *out = c;
   return DFVM_OK;
@@ -212,7 +248,7 @@ dfvm_status dfvm_comm_create_local(int n_ranks, const int* devices, dfvm_comm** 
 
 dfvm_status dfvm_comm_destroy(dfvm_comm* c) {
   if (!c) return DFVM_OK;
-  if (c->nccl) ncclCommDestroy(c->nccl);
+  if (c->nccl) nccl().CommDestroy(c->nccl);
   if (c->grp && --c->grp->refs == 0) {
     for (auto e : c->grp->posted) cudaEventDestroy(e);
     for (auto e : c->grp->consumed) cudaEventDestroy(e);
