@@ -11,8 +11,9 @@ flux correction, velocity correction, continuity) on the configured mesh.
     python bench.py --impl reference ...   # the CPU oracle arm (bounded sample)
 
 value   = cells x steps / device seconds (max over ranks), whole job.
-e2e     = the same metric through the C ABI with HOST buffers: every step
-          imports U, p, phi from pinned host memory and exports U, p back.
+e2e     = the same metric through the C ABI with HOST buffers: replaying
+          the same K steps from the same state, every step imports U, p, phi
+          from pinned host memory and exports U, p, phi back.
 roofline: the PCG SpMV kernel (dominant kernel of the step), timed live with
           CUDA events on the launching stream inside the library.
 cpu_baseline: the oracle (oracle/, plain fp64 C++, 1 core) on a bounded
@@ -136,7 +137,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dfvm", choices=["dfvm", "reference"])
     ap.add_argument("--config", default="c5", choices=["c5", "c2", "c1"])
@@ -207,6 +208,12 @@ def main():
 
     for _ in range(args.warmup):
         S.step(U, p, phi, sp)
+    # the e2e leg replays exactly these timed steps from the same state
+    if not args.no_e2e:
+        import torch as _t
+        hU = _t.from_numpy(np.ascontiguousarray(U.get(sp))).pin_memory().numpy()
+        hp = _t.from_numpy(np.ascontiguousarray(p.get(sp)).reshape(-1, 1)).pin_memory().numpy()
+        hphi = _t.from_numpy(np.ascontiguousarray(phi.get(sp)).reshape(-1, 1)).pin_memory().numpy()
 
     # ---------------- timed region (device-resident inputs)
     barrier()
@@ -233,9 +240,6 @@ def main():
     # ---------------- end-to-end through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
-        hU = torch.from_numpy(np.ascontiguousarray(U.get(sp))).pin_memory().numpy()
-        hp = torch.from_numpy(np.ascontiguousarray(p.get(sp)).reshape(-1, 1)).pin_memory().numpy()
-        hphi = torch.from_numpy(np.ascontiguousarray(phi.get(sp)).reshape(-1, 1)).pin_memory().numpy()
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
