@@ -143,6 +143,8 @@ def main():
     ap.add_argument("--config", default="c5", choices=["c5", "c2", "c1"])
     ap.add_argument("--nz", type=int, default=None, help="override C5 axial layers (814 = 50.0M cells)")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "amg"],
+                    help="pressure CG preconditioner (jacobi: A-14; amg: SURVEY NEXT-2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -180,6 +182,7 @@ def main():
     geo = mesh.export_geometry()
     U0, p0, phi0 = case.initial_state(geo["xc"], geo["xf"], geo["Sf"])
     B = case.apply_bcs(dfvm.BCs(mesh))
+    case.solver["p_precond"] = args.precond
     S = dfvm.Solver(mesh, B, **case.solver)
     stream = torch.cuda.current_stream()
     sp = C.c_void_p(stream.cuda_stream)

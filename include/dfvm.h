@@ -244,6 +244,8 @@ typedef struct {
   double p_ref_value;
   double p_tol, p_rel_tol, p_rel_tol_final; int32_t p_maxit;  /* A-13 stopping rule */
   double U_tol, U_rel_tol; int32_t U_maxit;
+  int32_t p_precond;            /* pressure CG preconditioner: 0 Jacobi (A-14), 1 aggregation-AMG
+                                   V(1,1) cycle (amg.cu) */
 } dfvm_piso_opts;
 
 /* Krylov stopping rule (A-13): b = 0 -> x = 0, 0 iterations; else

@@ -78,7 +78,7 @@ class PisoOpts(C.Structure):
                 ("n_nonorth", C.c_int32), ("convection", C.c_int32), ("p_ref_cell", C.c_int64),
                 ("p_ref_value", C.c_double), ("p_tol", C.c_double), ("p_rel_tol", C.c_double),
                 ("p_rel_tol_final", C.c_double), ("p_maxit", C.c_int32), ("U_tol", C.c_double),
-                ("U_rel_tol", C.c_double), ("U_maxit", C.c_int32)]
+                ("U_rel_tol", C.c_double), ("U_maxit", C.c_int32), ("p_precond", C.c_int32)]
 
 
 class SolveReport(C.Structure):
@@ -404,10 +404,11 @@ class Solver:
 
     def __init__(self, mesh, bcs, nu, dt, rho=1.0, n_corr=2, n_nonorth=0, convection="upwind", p_ref_cell=0,
                  p_ref_value=0.0, p_tol=1e-14, p_rel_tol=0.0, p_rel_tol_final=0.0, p_maxit=50000, U_tol=1e-14,
-                 U_rel_tol=0.0, U_maxit=50000):
+                 U_rel_tol=0.0, U_maxit=50000, p_precond="jacobi"):
         self.mesh, self.bcs = mesh, bcs
         o = PisoOpts(nu, dt, rho, n_corr, n_nonorth, {"upwind": 0, "central": 1}[convection], p_ref_cell,
-                     p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, p_maxit, U_tol, U_rel_tol, U_maxit)
+                     p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, p_maxit, U_tol, U_rel_tol, U_maxit,
+                     {"jacobi": 0, "amg": 1}[p_precond])
         h = C.c_void_p()
         _check(lib().dfvm_solver_create(mesh.h, bcs.h, C.byref(o), C.byref(h)))
         self.h = h.value

@@ -1,0 +1,470 @@
+// amg.cu — aggregation AMG preconditioner for the pressure PCG (SURVEY.md
+// §8(f) NEXT-2: "ILU ... and/or aggregation AMG for the pressure").
+//
+// Jacobi-PCG on the pressure Laplacian needs O(10^3) iterations on the 50M
+// cell pipe (iterations grow with the longest mesh dimension, SURVEY §7 hard
+// part 2); the paper's own choice, ILU, is sequential on a GPU.  A
+// plain-aggregation V-cycle keeps everything data-parallel and deterministic:
+//
+//  * hierarchy (host, once per mesh, topology only): greedy aggregation of
+//    the owned rows in RCM order (root + its unaggregated neighbours; leftovers
+//    join a neighbouring aggregate; isolated rows become singletons), until
+//    <= 2048 rows.  Coarse levels are rank-local (couplings to ghost rows are
+//    dropped: the coarse operator is the Galerkin product of the owned block,
+//    still SPD).
+//  * values (device, whenever the pressure matrix changes): Galerkin
+//    A_c = P^T A P with piecewise-constant P, as fixed-order gather sums over
+//    precomputed contribution lists (no atomics); l1-Jacobi diagonals
+//    d1_i = a_ii + sum_j |a_ij|.
+//  * V(1,1) cycle: pre-smooth x = D1^-1 b, residual, restriction (sum over
+//    aggregate members), coarse correction, prolongation x += x_c[agg],
+//    post-smooth x += D1^-1 (b - A x); coarsest level: 24 l1-Jacobi sweeps in
+//    one block (shared memory).  Pre/post smoothers are adjoint and the
+//    coarse solve is a fixed symmetric polynomial, so M^-1 is SPD and CG
+//    stays CG.  The converged pressure is preconditioner independent (A-14).
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "amg.h"
+#include "dev.cuh"
+
+namespace dfvm {
+
+dfvm_status halo_exchange(dfvm_mesh* m, void* data, int nc, cudaStream_t s);
+
+constexpr int kCoarseMax = 2048;
+constexpr int kCoarseSweeps = 24;
+constexpr int kMaxLevels = 16;
+
+// ------------------------------------------------------------ host setup
+namespace {
+
+struct HostLevel {
+  int n = 0;
+  // SELL-32 of this level's matrix (level 0: the mesh's matrix layout)
+  std::vector<int> ms_ptr, ms_len, mnb;
+  // CSR view of the real entries: (col, SELL position), owned cols only
+  std::vector<int> rp, col, pos;
+};
+
+void sell_to_csr(HostLevel& L, int n_owned_cols) {
+  const int n = L.n;
+  L.rp.assign(n + 1, 0);
+  for (int r = 0; r < n; ++r) {
+    const int s = r / 32, lane = r % 32;
+    for (int j = 0; j < L.ms_len[s]; ++j) {
+      const int c = L.mnb[L.ms_ptr[s] + 32 * j + lane];
+      if (c != r && c < n_owned_cols) L.rp[r + 1]++;
+    }
+  }
+  for (int r = 0; r < n; ++r) L.rp[r + 1] += L.rp[r];
+  L.col.assign(L.rp[n], 0);
+  L.pos.assign(L.rp[n], 0);
+  for (int r = 0; r < n; ++r) {
+    const int s = r / 32, lane = r % 32;
+    int k = L.rp[r];
+    for (int j = 0; j < L.ms_len[s]; ++j) {
+      const int p = L.ms_ptr[s] + 32 * j + lane;
+      const int c = L.mnb[p];
+      if (c != r && c < n_owned_cols) { L.col[k] = c; L.pos[k] = p; ++k; }
+    }
+  }
+}
+
+std::vector<int> aggregate(const HostLevel& L, int& nagg) {
+  const int n = L.n;
+  std::vector<int> agg(n, -1);
+  nagg = 0;
+  for (int i = 0; i < n; ++i) {          // pass 1: roots with all neighbours free
+    if (agg[i] >= 0) continue;
+    bool free_nb = true;
+    for (int k = L.rp[i]; k < L.rp[i + 1] && free_nb; ++k) free_nb = agg[L.col[k]] < 0;
+    if (!free_nb) continue;
+    agg[i] = nagg;
+    for (int k = L.rp[i]; k < L.rp[i + 1]; ++k) agg[L.col[k]] = nagg;
+    ++nagg;
+  }
+  std::vector<int> a1 = agg;             // pass 2: join a pass-1 neighbour aggregate
+  for (int i = 0; i < n; ++i) {
+    if (a1[i] >= 0) continue;
+    for (int k = L.rp[i]; k < L.rp[i + 1]; ++k)
+      if (a1[L.col[k]] >= 0) { agg[i] = a1[L.col[k]]; break; }
+  }
+  for (int i = 0; i < n; ++i)            // pass 3: leftovers with their free neighbours
+    if (agg[i] < 0) {
+      agg[i] = nagg;
+      for (int k = L.rp[i]; k < L.rp[i + 1]; ++k)
+        if (agg[L.col[k]] < 0) agg[L.col[k]] = nagg;
+      ++nagg;
+    }
+  return agg;
+}
+
+}  // namespace
+
+template <class T>
+struct AmgLevelDev {
+  int n = 0, n_slices = 0;
+  int64_t n_sell = 0;
+  const int *ms_ptr = nullptr, *ms_len = nullptr, *mnb = nullptr;
+  const T* coef = nullptr;   // level 0: the solver's pcoef
+  const T* diag = nullptr;   // level 0: the solver's pdiag
+  T* coef_own = nullptr;
+  T* diag_own = nullptr;
+  T* dl1 = nullptr;
+  // Galerkin maps of this (coarse) level from the finer level
+  int *gal_ptr = nullptr, *gal_idx = nullptr;     // per coarse SELL position
+  int *dg_ptr = nullptr, *dg_idx = nullptr;       // per coarse row: internal fine positions
+  int *mem_ptr = nullptr, *mem = nullptr;         // per coarse row: fine member rows
+  int* agg = nullptr;                             // on the FINE level: fine row -> coarse row
+  T *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr;
+};
+
+template <class T>
+struct Amg {
+  dfvm_mesh* m = nullptr;
+  int nlev = 0;
+  AmgLevelDev<T> L[kMaxLevels];
+  std::vector<void*> allocs;
+  int64_t bytes = 0;
+  ~Amg() { for (void* p : allocs) cudaFree(p); }
+  template <class U>
+  dfvm_status up(U** d, const std::vector<U>& h) {
+    void* q = nullptr;
+    const size_t sz = std::max<size_t>(h.size(), 1) * sizeof(U);
+    DFVM_CUDA(cudaMalloc(&q, sz));
+    if (!h.empty()) DFVM_CUDA(cudaMemcpy(q, h.data(), h.size() * sizeof(U), cudaMemcpyHostToDevice));
+    allocs.push_back(q);
+    bytes += (int64_t)sz;
+    *d = (U*)q;
+    return DFVM_OK;
+  }
+  template <class U>
+  dfvm_status zalloc(U** d, size_t n) {
+    void* q = nullptr;
+    const size_t sz = std::max<size_t>(n, 1) * sizeof(U);
+    DFVM_CUDA(cudaMalloc(&q, sz));
+    DFVM_CUDA(cudaMemset(q, 0, sz));
+    allocs.push_back(q);
+    bytes += (int64_t)sz;
+    *d = (U*)q;
+    return DFVM_OK;
+  }
+};
+
+template <class T>
+dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, Amg<T>** out) {
+  Amg<T>* A = new Amg<T>();
+  A->m = m;
+  std::vector<HostLevel> H(1);
+  H[0].n = M.n_own;
+  H[0].ms_ptr = m->h_ms_ptr; H[0].ms_len = m->h_ms_len; H[0].mnb = m->h_mnb;
+  sell_to_csr(H[0], M.n_own);
+  // device view of level 0 (the mesh's matrix layout; coef / diag bound per update)
+  AmgLevelDev<T>& L0 = A->L[0];
+  L0.n = M.n_own; L0.n_slices = M.n_slices; L0.n_sell = M.n_minc;
+  L0.ms_ptr = M.ms_ptr; L0.ms_len = M.ms_len; L0.mnb = M.mnb;
+  dfvm_status st;
+  if ((st = A->zalloc(&L0.dl1, M.n_own)) || (st = A->zalloc(&L0.x, M.n_cells)) || (st = A->zalloc(&L0.r, M.n_own)) ||
+      (st = A->zalloc(&L0.t, M.n_cells))) { delete A; return st; }
+  int lev = 0;
+  while (H[lev].n > kCoarseMax && lev + 1 < kMaxLevels) {
+    const HostLevel& F = H[lev];
+    int nc = 0;
+    std::vector<int> agg = aggregate(F, nc);
+    if (nc >= F.n * 0.85) break;           // coarsening stalled
+    // members
+    std::vector<int> mem_ptr(nc + 1, 0), mem(F.n);
+    for (int i = 0; i < F.n; ++i) mem_ptr[agg[i] + 1]++;
+    for (int I = 0; I < nc; ++I) mem_ptr[I + 1] += mem_ptr[I];
+    {
+      std::vector<int> p(mem_ptr.begin(), mem_ptr.end() - 1);
+      for (int i = 0; i < F.n; ++i) mem[p[agg[i]]++] = i;
+    }
+    // coarse rows: (J, fine position) pairs, sorted; internal -> diag list
+    HostLevel C;
+    C.n = nc;
+    std::vector<int> crow_ptr(nc + 1, 0), ccol, dg_ptr(nc + 1, 0), dg_idx;
+    std::vector<std::vector<int>> gal_lists;   // per coarse CSR entry
+    std::vector<std::pair<int, int>> buf;
+    for (int I = 0; I < nc; ++I) {
+      buf.clear();
+      for (int q = mem_ptr[I]; q < mem_ptr[I + 1]; ++q) {
+        const int i = mem[q];
+        for (int k = F.rp[i]; k < F.rp[i + 1]; ++k) buf.push_back({agg[F.col[k]], F.pos[k]});
+      }
+      std::sort(buf.begin(), buf.end());
+      for (size_t k = 0; k < buf.size();) {
+        const int J = buf[k].first;
+        size_t e = k;
+        while (e < buf.size() && buf[e].first == J) ++e;
+        if (J == I) {
+          for (size_t u = k; u < e; ++u) dg_idx.push_back(buf[u].second);
+        } else {
+          ccol.push_back(J);
+          gal_lists.emplace_back();
+          for (size_t u = k; u < e; ++u) gal_lists.back().push_back(buf[u].second);
+        }
+        k = e;
+      }
+      crow_ptr[I + 1] = (int)ccol.size();
+      dg_ptr[I + 1] = (int)dg_idx.size();
+    }
+    // coarse SELL-32 layout
+    const int S = (nc + 31) / 32;
+    C.ms_ptr.assign(S + 1, 0);
+    C.ms_len.assign(S, 0);
+    for (int s = 0; s < S; ++s) {
+      int w = 0;
+      for (int I = s * 32; I < std::min(nc, s * 32 + 32); ++I) w = std::max(w, crow_ptr[I + 1] - crow_ptr[I]);
+      C.ms_len[s] = w;
+      C.ms_ptr[s + 1] = C.ms_ptr[s] + 32 * w;
+    }
+    C.mnb.assign(C.ms_ptr[S], 0);
+    std::vector<int> gal_ptr(C.ms_ptr[S] + 1, 0), gal_idx;
+    std::vector<int> slot_entry(C.ms_ptr[S], -1);
+    for (int I = 0; I < nc; ++I) {
+      const int s = I / 32, lane = I % 32;
+      for (int j = 0; j < C.ms_len[s]; ++j) {
+        const int p = C.ms_ptr[s] + 32 * j + lane;
+        const int e = crow_ptr[I] + j;
+        if (e < crow_ptr[I + 1]) { C.mnb[p] = ccol[e]; slot_entry[p] = e; }
+        else C.mnb[p] = I;   // padding: self, coefficient 0
+      }
+    }
+    for (int p = 0; p < C.ms_ptr[S]; ++p) {
+      if (slot_entry[p] >= 0) for (int f : gal_lists[slot_entry[p]]) gal_idx.push_back(f);
+      gal_ptr[p + 1] = (int)gal_idx.size();
+    }
+    sell_to_csr(C, nc);
+    // upload
+    AmgLevelDev<T>& D = A->L[lev + 1];
+    D.n = nc; D.n_slices = S; D.n_sell = C.ms_ptr[S];
+    int *p0, *p1, *p2;
+    if ((st = A->up(&p0, C.ms_ptr)) || (st = A->up(&p1, C.ms_len)) || (st = A->up(&p2, C.mnb)) ||
+        (st = A->up(&D.gal_ptr, gal_ptr)) || (st = A->up(&D.gal_idx, gal_idx)) || (st = A->up(&D.dg_ptr, dg_ptr)) ||
+        (st = A->up(&D.dg_idx, dg_idx)) || (st = A->up(&D.mem_ptr, mem_ptr)) || (st = A->up(&D.mem, mem)) ||
+        (st = A->up(&A->L[lev].agg, agg)) || (st = A->zalloc(&D.coef_own, (size_t)D.n_sell)) ||
+        (st = A->zalloc(&D.diag_own, nc)) || (st = A->zalloc(&D.dl1, nc)) || (st = A->zalloc(&D.x, nc)) ||
+        (st = A->zalloc(&D.b, nc)) || (st = A->zalloc(&D.r, nc)) || (st = A->zalloc(&D.t, nc))) {
+      delete A;
+      return st;
+    }
+    D.ms_ptr = p0; D.ms_len = p1; D.mnb = p2;
+    D.coef = D.coef_own; D.diag = D.diag_own;
+    H.push_back(std::move(C));
+    ++lev;
+  }
+  A->nlev = lev + 1;
+  *out = A;
+  return DFVM_OK;
+}
+
+template <class T>
+void amg_destroy(Amg<T>* A) { delete A; }
+
+template <class T>
+int amg_levels(const Amg<T>* A, int* sizes) {
+  for (int l = 0; l < A->nlev; ++l) sizes[l] = A->L[l].n;
+  return A->nlev;
+}
+
+// ------------------------------------------------------------ kernels
+template <class T>
+__global__ void k_gal_off(int64_t n_sell, const int* __restrict__ gp, const int* __restrict__ gi,
+                          const T* __restrict__ fcoef, T* __restrict__ ccoef) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_sell; e += (int64_t)gridDim.x * blockDim.x) {
+    T s = T(0);
+    for (int k = gp[e]; k < gp[e + 1]; ++k) s += fcoef[gi[k]];
+    ccoef[e] = s;
+  }
+}
+
+template <class T>
+__global__ void k_gal_diag(int n, const int* __restrict__ mp, const int* __restrict__ mem,
+                           const int* __restrict__ dp, const int* __restrict__ di, const T* __restrict__ fdiag,
+                           const T* __restrict__ fcoef, T* __restrict__ cdiag) {
+  for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < n; I += gridDim.x * blockDim.x) {
+    T s = T(0);
+    for (int k = mp[I]; k < mp[I + 1]; ++k) s += fdiag[mem[k]];
+    for (int k = dp[I]; k < dp[I + 1]; ++k) s += fcoef[di[k]];
+    cdiag[I] = s;
+  }
+}
+
+// l1 diagonal: a_ii + sum_j |a_ij| over the row's SELL entries
+template <class T>
+__global__ void k_dl1(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                      const T* __restrict__ coef, const T* __restrict__ diag, T* __restrict__ dl1) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int s = r >> 5, lane = r & 31;
+    T a = diag[r];
+    for (int j = 0; j < ms_len[s]; ++j) a += fabs(coef[ms_ptr[s] + 32 * j + lane]);
+    dl1[r] = a;
+  }
+}
+
+template <class T>
+__device__ __forceinline__ T row_apply(int r, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                                       const int* __restrict__ mnb, const T* __restrict__ coef,
+                                       const T* __restrict__ diag, const T* __restrict__ x) {
+  const int s = r >> 5, lane = r & 31;
+  const int len = ms_len[s], base = ms_ptr[s] + lane;
+  T acc = diag[r] * x[r];
+  int j = 0;
+  for (; j + 4 <= len; j += 4) {
+    T a[4];
+    int c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&mnb[base + 32 * (j + u)]); }
+    T v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = x[c[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
+  }
+  for (; j < len; ++j) acc += __ldg(&coef[base + 32 * j]) * x[__ldg(&mnb[base + 32 * j])];
+  return acc;
+}
+
+// x = b / d1 (pre-smoothing from a zero guess)
+template <class T>
+__global__ void k_amg_pre(int n, const T* __restrict__ b, const T* __restrict__ dl1, T* __restrict__ x,
+                          const int* done) {
+  if (*done) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = b[i] / dl1[i];
+}
+// r = b - A x
+template <class T>
+__global__ void k_amg_resid(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                            const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
+                            const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ r, const int* done) {
+  if (*done) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    r[i] = b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x);
+}
+// b_c[I] = sum over the aggregate's members of r_f
+template <class T>
+__global__ void k_amg_restrict(int nc, const int* __restrict__ mp, const int* __restrict__ mem,
+                               const T* __restrict__ rf, T* __restrict__ bc, const int* done) {
+  if (*done) return;
+  for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
+    T s = T(0);
+    for (int k = mp[I]; k < mp[I + 1]; ++k) s += rf[mem[k]];
+    bc[I] = s;
+  }
+}
+// t = x + x_c[agg[i]]  (coarse correction, out of place: t feeds the smoother)
+template <class T>
+__global__ void k_amg_prolong(int n, const int* __restrict__ agg, const T* __restrict__ xc, const T* __restrict__ x,
+                              T* __restrict__ t, const int* done) {
+  if (*done) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = x[i] + xc[agg[i]];
+}
+// out = x + (b - A x) / d1
+template <class T>
+__global__ void k_amg_smooth(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                             const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
+                             const T* __restrict__ dl1, const T* __restrict__ x, const T* __restrict__ b,
+                             T* __restrict__ out, const int* done) {
+  if (*done) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = x[i] + (b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x)) / dl1[i];
+}
+// coarsest level: kCoarseSweeps l1-Jacobi sweeps from zero, one block, in shared memory
+template <class T>
+__global__ void __launch_bounds__(1024) k_amg_coarse(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                                                    const int* __restrict__ mnb, const T* __restrict__ coef,
+                                                    const T* __restrict__ diag, const T* __restrict__ dl1,
+                                                    const T* __restrict__ b, T* __restrict__ xout, const int* done) {
+  if (*done) return;
+  __shared__ T xs[2][kCoarseMax];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xs[0][i] = b[i] / dl1[i];
+  __syncthreads();
+  int cur = 0;
+  for (int it = 1; it < kCoarseSweeps; ++it) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      xs[cur ^ 1][i] = xs[cur][i] + (b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, xs[cur])) / dl1[i];
+    __syncthreads();
+    cur ^= 1;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = xs[cur][i];
+}
+
+// ------------------------------------------------------------ host drivers
+template <class T>
+dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s, int* nl) {
+  AmgLevelDev<T>& L0 = A->L[0];
+  L0.coef = pcoef; L0.diag = pdiag;
+  k_dl1<T><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, L0.ms_ptr, L0.ms_len, L0.coef, L0.diag, L0.dl1);
+  ++*nl;
+  for (int l = 1; l < A->nlev; ++l) {
+    AmgLevelDev<T>& F = A->L[l - 1];
+    AmgLevelDev<T>& C = A->L[l];
+    k_gal_off<T><<<grid_for(C.n_sell), kThreads, 0, s>>>(C.n_sell, C.gal_ptr, C.gal_idx, F.coef, C.coef_own);
+    k_gal_diag<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, C.dg_ptr, C.dg_idx, F.diag, F.coef,
+                                                      C.diag_own);
+    k_dl1<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.coef, C.diag, C.dl1);
+    *nl += 3;
+  }
+  DFVM_CUDA(cudaGetLastError());
+  return DFVM_OK;
+}
+
+// z = M^-1 r (one V(1,1) cycle); skipped on the device when *done is set
+template <class T>
+dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl) {
+  const int nlev = A->nlev;
+  dfvm_status e;
+  // descend
+  for (int l = 0; l < nlev - 1; ++l) {
+    AmgLevelDev<T>& F = A->L[l];
+    AmgLevelDev<T>& C = A->L[l + 1];
+    const T* b = l == 0 ? r : F.b;
+    T* x = l == 0 ? z : F.x;
+    k_amg_pre<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, b, F.dl1, x, done);
+    if (l == 0 && (e = halo_exchange(A->m, x, 1, s))) return e;
+    k_amg_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, x, b, F.r, done);
+    k_amg_restrict<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
+    *nl += 3;
+  }
+  // coarsest
+  {
+    AmgLevelDev<T>& C = A->L[nlev - 1];
+    if (nlev == 1) {
+      // single level: plain l1-Jacobi sweep pair
+      k_amg_pre<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, r, C.dl1, z, done);
+      *nl += 1;
+      return DFVM_OK;
+    }
+    k_amg_coarse<T><<<1, 1024, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.dl1, C.b, C.x, done);
+    *nl += 1;
+  }
+  // ascend
+  for (int l = nlev - 2; l >= 0; --l) {
+    AmgLevelDev<T>& F = A->L[l];
+    AmgLevelDev<T>& C = A->L[l + 1];
+    const T* b = l == 0 ? r : F.b;
+    T* x = l == 0 ? z : F.x;
+    k_amg_prolong<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, x, F.t, done);
+    if (l == 0 && (e = halo_exchange(A->m, F.t, 1, s))) return e;
+    k_amg_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, F.t, b,
+                                                        x, done);
+    *nl += 2;
+  }
+  DFVM_CUDA(cudaGetLastError());
+  return DFVM_OK;
+}
+
+#define INST(T)                                                                           \
+  template dfvm_status amg_create<T>(dfvm_mesh*, const DevMesh<T>&, Amg<T>**);            \
+  template void amg_destroy<T>(Amg<T>*);                                                  \
+  template int amg_levels<T>(const Amg<T>*, int*);                                        \
+  template dfvm_status amg_update<T>(Amg<T>*, const T*, const T*, cudaStream_t, int*);    \
+  template dfvm_status amg_apply<T>(Amg<T>*, const T*, T*, const int*, cudaStream_t, int*);
+INST(double)
+INST(float)
+
+}  // namespace dfvm

@@ -1,0 +1,19 @@
+// amg.h — aggregation-AMG preconditioner for the pressure PCG (amg.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace dfvm {
+
+template <class T> struct Amg;
+// hierarchy from the mesh topology (host, once per mesh)
+template <class T> dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, Amg<T>** out);
+template <class T> void amg_destroy(Amg<T>* A);
+template <class T> int amg_levels(const Amg<T>* A, int* sizes);
+// Galerkin values + l1 diagonals for the current pressure matrix (pcoef, pdiag)
+template <class T> dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s, int* n_launch);
+// z = M^-1 r, one V(1,1) cycle; every kernel exits early when *done != 0
+template <class T> dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t s, int* n_launch);
+
+}  // namespace dfvm

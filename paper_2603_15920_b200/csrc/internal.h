@@ -119,6 +119,8 @@ struct dfvm_mesh {
   int64_t device_bytes = 0;
   double host_seconds = 0;
   bool host_only = false;
+  // host copy of the matrix SELL structure (AMG hierarchy setup)
+  std::vector<int> h_ms_ptr, h_ms_len, h_mnb;
   dfvm_comm* comm = nullptr;
   // lazily built device maps for device-side import/export
   int32_t* d_cell_orig = nullptr;   // [n_cells] original id of local cell

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "dev.cuh"
+#include "amg.h"
 #include "launch.h"
 
 namespace dfvm {
@@ -59,10 +60,22 @@ __device__ __forceinline__ void krylov_start(KCtl& c, double bb, double rr) {
 // either by the last block of the reducing kernel (one rank) or by the
 // finalize kernel after the cross-rank all-gather (rank-order sum), so every
 // rank applies bitwise-identical updates.
-enum CtlKind { CTL_CG_INIT = 0, CTL_CG_SPMV, CTL_CG_R, CTL_BI_INIT, CTL_BI_V, CTL_BI_S, CTL_BI_T, CTL_BI_X };
+enum CtlKind { CTL_CG_INIT = 0, CTL_CG_SPMV, CTL_CG_R, CTL_BI_INIT, CTL_BI_V, CTL_BI_S, CTL_BI_T, CTL_BI_X,
+               CTL_CG_R2, CTL_CG_RZ0, CTL_CG_RZ };
 
 __device__ void ctl_apply(int kind, KCtl* ctl, const double* t) {
   switch (kind) {
+    // AMG-preconditioned CG: the residual check uses r.r; r.z comes from a
+    // separate reduction after the V-cycle
+    case CTL_CG_R2: {
+      KCtl& c = *ctl;
+      c.it++;
+      krylov_check(c, sqrt(t[0]));
+      if (c.done) c.half = 1;
+      break;
+    }
+    case CTL_CG_RZ0: ctl->rz = t[0]; ctl->beta = 0.0; break;
+    case CTL_CG_RZ: ctl->beta = t[0] / ctl->rz; ctl->rz = t[0]; break;
     case CTL_CG_INIT: {
       KCtl& c = *ctl;
       krylov_start(c, t[0], t[1]);
@@ -149,7 +162,9 @@ __device__ __forceinline__ void red_finish(const Red& red, int kind, KCtl* ctl, 
 __global__ void k_finalize(int kind, int nv, const double* __restrict__ all, int P, KCtl* ctl) {
   // the reducing kernel exited early (and produced no totals) when the solve
   // was already done; init kernels always run
-  if (kind == CTL_CG_SPMV || kind == CTL_CG_R) { if (ctl->done) return; }
+  if (kind == CTL_CG_SPMV || kind == CTL_CG_R || kind == CTL_CG_R2 || kind == CTL_CG_RZ0 || kind == CTL_CG_RZ) {
+    if (ctl->done) return;
+  }
   else if (kind != CTL_CG_INIT && kind != CTL_BI_INIT) { if (ctl[0].done && ctl[1].done && ctl[2].done) return; }
   double t[8];
   for (int i = 0; i < nv; ++i) {
@@ -670,6 +685,44 @@ __global__ void k_cg_r(int n, const T* __restrict__ q, const T* __restrict__ dia
   if (grid_sum<2>(v, partials, ticket, t)) red_finish<2>(red, CTL_CG_R, ctl, t);
 }
 
+// ---- AMG-preconditioned variant: z = M^-1 r comes from amg_apply
+template <class T>
+__global__ void k_cg_p2(int n, const T* __restrict__ z, T* __restrict__ pd, T* __restrict__ x, const KCtl* ctl) {
+  if (ctl->done) return;
+  const T beta = (T)ctl->beta, alpha = (T)ctl->alpha;
+  const bool first = ctl->it == 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (first) { pd[i] = z[i]; continue; }
+    const T po = pd[i];
+    x[i] += alpha * po;
+    pd[i] = z[i] + beta * po;
+  }
+}
+template <class T>
+__global__ void k_cg_r2(int n, const T* __restrict__ q, T* __restrict__ r, double* partials, unsigned* ticket,
+                        KCtl* ctl, Red red) {
+  if (ctl->done) return;
+  const T alpha = (T)ctl->alpha;
+  double v[1] = {0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const T rr = r[i] - alpha * q[i];
+    r[i] = rr;
+    v[0] += (double)rr * (double)rr;
+  }
+  double t[1];
+  if (grid_sum<1>(v, partials, ticket, t)) red_finish<1>(red, CTL_CG_R2, ctl, t);
+}
+template <class T>
+__global__ void k_cg_dot(int n, const T* __restrict__ a, const T* __restrict__ b, double* partials, unsigned* ticket,
+                         KCtl* ctl, Red red, int kind) {
+  if (ctl->done) return;
+  double v[1] = {0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    v[0] += (double)a[i] * (double)b[i];
+  double t[1];
+  if (grid_sum<1>(v, partials, ticket, t)) red_finish<1>(red, kind, ctl, t);
+}
+
 // the deferred x update of the final iteration
 template <class T>
 __global__ void k_cg_final(int n, const T* __restrict__ pd, T* __restrict__ x, const KCtl* ctl) {
@@ -879,12 +932,16 @@ struct SolverT : SolverBase {
   double* h_cont = nullptr;  // pinned
   double* red_local = nullptr;  // [8] this rank's reduction totals (P > 1)
   double* red_all = nullptr;    // [P][8] all-gathered totals
+  Amg<T>* amg = nullptr;        // pressure preconditioner (p_precond == 1), built lazily
+  bool amg_dirty = true;        // pressure matrix changed since the last Galerkin update
+  T* kz = nullptr;              // preconditioned residual z = M^-1 r
   WKDev* d_wk = nullptr;
   WKDev* h_wk = nullptr;     // pinned
   int* d_wk_ptr = nullptr;
   int* d_wk_faces = nullptr;
   bool assembled = false;
   ~SolverT() override {
+    if (amg) amg_destroy<T>(amg);
     for (void* p : allocs) cudaFree(p);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (h_cont) cudaFreeHost(h_cont);
@@ -908,7 +965,7 @@ struct SolverT : SolverBase {
         (st = al(&HbyA, 3 * nc)) || (st = al(&phiHbyA, nf)) || (st = al(&pcoef, (size_t)M->n_minc)) ||
         (st = al(&pdiag, nc)) || (st = al(&prhs0, no)) || (st = al(&prhs, no)) || (st = al(&kr, 3 * nc)) ||
         (st = al(&krh, 3 * nc)) || (st = al(&kp, 3 * nc)) || (st = al(&kq, 3 * nc)) || (st = al(&kv, 3 * nc)) ||
-        (st = al(&ky, 3 * nc)) || (st = al(&ks, 3 * nc)) || (st = al(&kt, 3 * nc)) ||
+        (st = al(&ky, 3 * nc)) || (st = al(&ks, 3 * nc)) || (st = al(&kt, 3 * nc)) || (st = al(&kz, nc)) ||
         (st = al(&partials, (size_t)kMaxBlocks * 8)) || (st = al(&ticket, 4)) || (st = al(&d_ctl, 4)) ||
         (st = al(&d_cont, 8)) || (st = al(&red_local, 128)) || (st = al(&red_all, (size_t)128 * mm->part.P)))
       return st;
@@ -1007,10 +1064,15 @@ static dfvm_status fin(dfvm_solver* S, SolverT<T>& X, int kind, int nv, cudaStre
   return DFVM_OK;
 }
 
+template <class T>
+static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol,
+                              int maxit, dfvm_solve_report* rep, cudaStream_t st);
+
 // Jacobi PCG on (pdiag, pcoef): x warm start, b rhs
 template <class T>
 static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol, int maxit,
                           dfvm_solve_report* rep, cudaStream_t st) {
+  if (S->o.p_precond == 1) return run_cg_amg(S, X, b, x, tol, rel_tol, maxit, rep, st);
   DevMesh<T>& M = *X.M;
   dfvm_mesh* m = S->m;
   const Red red{m->part.P, X.red_local};
@@ -1066,6 +1128,88 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
   DFVM_CUDA(cudaGetLastError());
   const KCtl& c = *X.h_ctl;
   if (c.half) {   // deferred x update of the last iteration
+    k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl);
+    S->n_launch++;
+  }
+  if (c.zero_x) DFVM_CUDA(cudaMemsetAsync(x, 0, (size_t)M.n_own * sizeof(T), st));
+  if (rep) fill_report(c, rep);
+  return (dfvm_status)(c.status == DFVM_E_BREAKDOWN ? DFVM_E_BREAKDOWN : (c.converged ? DFVM_OK : DFVM_E_NOT_CONVERGED));
+}
+
+// PCG preconditioned by one AMG V(1,1) cycle (amg.cu).
+// Same stopping rule, same deferred x update; per iteration:
+//   p update (z + beta p) | halo(p) | SpMV + p.q -> alpha | r update + r.r ->
+//   check | z = M^-1 r | r.z -> beta.   The V-cycle kernels exit early on the
+//   done flag, so the chunked host loop costs nothing after convergence.
+template <class T>
+static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol,
+                              int maxit, dfvm_solve_report* rep, cudaStream_t st) {
+  DevMesh<T>& M = *X.M;
+  dfvm_mesh* m = S->m;
+  dfvm_status e;
+  if (!X.amg && (e = amg_create<T>(m, M, &X.amg))) return e;
+  if (X.amg_dirty) {
+    if ((e = amg_update<T>(X.amg, X.pcoef, X.pdiag, st, &S->n_launch))) return e;
+    X.amg_dirty = false;
+  }
+  const Red red{m->part.P, X.red_local};
+  const int* done = &X.d_ctl->done;
+  const int gs = grid_slices(k_cg_spmv<T>, M.n_slices), ge = grid_for(M.n_own);
+  KCtl init{};
+  init.tol = tol; init.rel_tol = rel_tol; init.maxit = maxit;
+  DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, &init, sizeof(KCtl), cudaMemcpyHostToDevice, st));
+  if ((e = halo_exchange(m, x, 1, st))) return e;
+  k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr,
+                                                                          X.partials, X.ticket, X.d_ctl, red);
+  S->n_launch++;
+  if ((e = fin(S, X, CTL_CG_INIT, 3, st))) return e;
+  if ((e = amg_apply<T>(X.amg, X.kr, X.kz, done, st, &S->n_launch))) return e;
+  k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ0);
+  S->n_launch++;
+  if ((e = fin(S, X, CTL_CG_RZ0, 1, st))) return e;
+  if (S->timing && S->ev.size() < 4 * kChunk) {
+    while (S->ev.size() < 4 * kChunk) {
+      cudaEvent_t ev;
+      DFVM_CUDA(cudaEventCreate(&ev));
+      S->ev.push_back(ev);
+    }
+  }
+  int it_before = 0;
+  for (;;) {
+    for (int k = 0; k < kChunk; ++k) {
+      if (S->timing) cudaEventRecord(S->ev[4 * k], st);
+      k_cg_p2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kz, X.kp, x, X.d_ctl);
+      if ((e = halo_exchange(m, X.kp, 1, st))) return e;
+      if (S->timing) cudaEventRecord(S->ev[4 * k + 1], st);
+      k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red);
+      if (S->timing) cudaEventRecord(S->ev[4 * k + 2], st);
+      if ((e = fin(S, X, CTL_CG_SPMV, 1, st))) return e;
+      k_cg_r2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, X.partials, X.ticket, X.d_ctl, red);
+      if ((e = fin(S, X, CTL_CG_R2, 1, st))) return e;
+      if ((e = amg_apply<T>(X.amg, X.kr, X.kz, done, st, &S->n_launch))) return e;
+      k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ);
+      if ((e = fin(S, X, CTL_CG_RZ, 1, st))) return e;
+      if (S->timing) cudaEventRecord(S->ev[4 * k + 3], st);
+      S->n_launch += 4;
+    }
+    DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
+    DFVM_CUDA(cudaStreamSynchronize(st));
+    if (S->timing) {
+      const int ran = X.h_ctl->it - it_before;
+      for (int k = 0; k < kChunk && k < ran; ++k) {
+        float a = 0, b2 = 0;
+        cudaEventElapsedTime(&a, S->ev[4 * k + 1], S->ev[4 * k + 2]);
+        cudaEventElapsedTime(&b2, S->ev[4 * k], S->ev[4 * k + 3]);
+        S->t_ms[0] += a; S->t_n[0]++;
+        S->t_ms[1] += b2; S->t_n[1]++;
+      }
+      it_before = X.h_ctl->it;
+    }
+    if (X.h_ctl->done) break;
+  }
+  DFVM_CUDA(cudaGetLastError());
+  const KCtl& c = *X.h_ctl;
+  if (c.half) {
     k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl);
     S->n_launch++;
   }
@@ -1200,6 +1344,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
     // 3.4 pressure coefficients
     k_pcoef<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
                                         (T)o.p_ref_value, X.pcoef, X.pdiag, X.prhs0);
+    X.amg_dirty = true;
     S->n_launch += 2;
     // 3.5 non-orthogonal loop
     for (int io = 0; io <= o.n_nonorth; ++io) {
@@ -1269,7 +1414,8 @@ extern "C" {
 dfvm_status dfvm_solver_create(dfvm_mesh* m, dfvm_bcs* b, const dfvm_piso_opts* opts, dfvm_solver** out) {
   if (!m || !b || !opts || !out || b->m != m) { set_error(DFVM_E_INVALID_ARG, "NULL or mismatched argument"); return DFVM_E_INVALID_ARG; }
   if (!(opts->dt > 0) || !(opts->nu >= 0) || opts->n_corr < 1 || opts->n_corr > 8 || opts->n_nonorth < 0 ||
-      (opts->n_corr * (opts->n_nonorth + 1)) > 16 || opts->p_maxit < 1 || opts->U_maxit < 1 || !(opts->rho > 0)) {
+      (opts->n_corr * (opts->n_nonorth + 1)) > 16 || opts->p_maxit < 1 || opts->U_maxit < 1 || !(opts->rho > 0) ||
+      opts->p_precond < 0 || opts->p_precond > 1) {
     set_error(DFVM_E_INVALID_ARG, "invalid PISO options");
     return DFVM_E_INVALID_ARG;
   }
@@ -1402,6 +1548,7 @@ static dfvm_status pressure_solve_t(dfvm_solver* s, SolverT<T>& X, const T* rAU,
   const int ref = s->fixed_p ? -1 : s->ref_row;
   k_pcoef<T><<<grid_for_slices(M.n_slices), kThreads, 0, st>>>(M, rAU, X.phiHbyA, s->b->d_kind[1],
       (const T*)s->b->d_val[1], ref, (T)s->o.p_ref_value, X.pcoef, X.pdiag, X.prhs0);
+  X.amg_dirty = true;
   DFVM_CUDA(cudaMemcpyAsync(X.prhs, rhs, (size_t)M.n_own * sizeof(T), cudaMemcpyDeviceToDevice, st));
   if (ref >= 0) k_add_at<T><<<1, 1, 0, st>>>(X.prhs, X.prhs0, ref);
   count_launch(1 + (ref >= 0));

@@ -95,15 +95,16 @@ def test_operators_partitioned_equal_single(P):
     assert np.array_equal(y, ref_y) and np.array_equal(G, ref_G)
 
 
-@pytest.mark.parametrize("P,wk", [(2, False), (3, False), (2, True)])
-def test_piso_partitioned_matches_single(P, wk):
+@pytest.mark.parametrize("P,wk,precond", [(2, False, "jacobi"), (3, False, "jacobi"), (2, True, "jacobi"),
+                                          (2, False, "amg")])
+def test_piso_partitioned_matches_single(P, wk, precond):
     raw = _pipe()
     mo = oracle.Mesh(raw)
     U0 = np.zeros((raw.n_cells, 3))
     U0[:, 2] = 2.0 * (1 - 4 * (mo.xc[:, 0] ** 2 + mo.xc[:, 1] ** 2))
     U0 += 0.01 * synth.cell_field(21, raw.n_cells, 3)
     phi0 = np.zeros(mo.NF)
-    kw = dict(nu=0.1, dt=0.005, n_corr=2, n_nonorth=1, convection="upwind", **TIGHT)
+    kw = dict(nu=0.1, dt=0.005, n_corr=2, n_nonorth=1, convection="upwind", p_precond=precond, **TIGHT)
     wkargs = (0.1, 1.1111, 0.9, 0.0, 0)
 
     def setup(m):
@@ -137,6 +138,8 @@ def test_piso_partitioned_matches_single(P, wk):
     # every rank took the same Krylov decisions and sees the same global reports
     for r in range(1, P):
         assert [x["it"] for x in reps[r]["p"]] == [x["it"] for x in reps[0]["p"]]
+    # (with AMG the coarse levels are rank-local, so the iteration counts may
+    # differ from the single-rank run; the converged fields may not)
         assert reps[r]["cont_err_max"] == reps[0]["cont_err_max"]
     assert abs(reps[0]["cont_err_max"] - r1["cont_err_max"]) <= 1e-12
     if wk:
