@@ -434,8 +434,13 @@ dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t
   {
     AmgLevelDev<T>& C = A->L[nlev - 1];
     if (nlev == 1) {
-      // single level: plain l1-Jacobi sweep pair
-      k_amg_pre<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, r, C.dl1, z, done);
+      // single level (<= 2048 rows): on one rank the one-block smoother is the
+      // whole preconditioner; with ghost columns (several ranks) it cannot run
+      // in shared memory, so one l1-Jacobi step is used instead
+      if (A->m->part.P == 1)
+        k_amg_coarse<T><<<1, 1024, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.dl1, r, z, done);
+      else
+        k_amg_pre<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, r, C.dl1, z, done);
       *nl += 1;
       return DFVM_OK;
     }
