@@ -95,6 +95,9 @@ def oracle_sample(config, precision):
     if config == "c5":
         case = cases.c5(n_z=4)
         sample = "1 PISO step, C5 generator (n=64, m_r=32) with n_z=4 -> 245,760 tets, C5 physics, CG capped at 200 it/solve"
+    elif config == "c4":
+        case = cases.c4(target_cells=2.0e5)
+        sample = "1 PISO step, C4 H-tree generator at ~2e5 tets, C4 physics + 8 RCR outlets, CG capped at 200 it/solve"
     elif config == "c2":
         case = cases.c2()
         sample = "1 PISO step of C2 (199,680 tets), CG capped at 200 it/solve"
@@ -107,6 +110,8 @@ def oracle_sample(config, precision):
     m = oracle.Mesh(case.raw)
     b = case.apply_bcs(oracle.BCs(m))
     S = oracle.Solver(m, b, **kw)
+    for patch, (Rp, Cc, Rd) in getattr(case, "windkessel", []):
+        S.windkessel_set(patch, Rp, Cc, Rd, 0.0, 0)
     U, p, phi = case.initial_state(m.xc, m.xf, m.Sf)
     t1 = time.time()
     S.step(U, p, phi)
@@ -140,7 +145,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dfvm", choices=["dfvm", "reference"])
-    ap.add_argument("--config", default="c5", choices=["c5", "c2", "c1"])
+    ap.add_argument("--config", default="c5", choices=["c5", "c4", "c2", "c1"])
     ap.add_argument("--nz", type=int, default=None, help="override C5 axial layers (814 = 50.0M cells)")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--precond", default="jacobi", choices=["jacobi", "amg"],
@@ -184,6 +189,8 @@ def main():
     B = case.apply_bcs(dfvm.BCs(mesh))
     case.solver["p_precond"] = args.precond
     S = dfvm.Solver(mesh, B, **case.solver)
+    for patch, (Rp, Cc, Rd) in getattr(case, "windkessel", []):
+        S.windkessel_set(patch, Rp, Cc, Rd, 0.0, 0)
     stream = torch.cuda.current_stream()
     sp = C.c_void_p(stream.cuda_stream)
     U = mesh.field("cells", 3, U0, sp)

@@ -78,4 +78,26 @@ def c5(n_z=814, scramble=15):
                 f"O-grid pipe n=64 m_r=32 n_z={n_z}, alternating 5-tet, N={raw.n_cells}, Re_D=100")
 
 
-CONFIGS = {"c1": c1, "c2": c2, "c5": c5}
+def c4(target_cells=1.0e7, scramble=14):
+    """configs[3]: voxelised H-tree (Murray radii, 8 terminal outlets) ->
+    alternating 5-tet, CGS units (rho 1.06, mu 0.04 -> nu 0.0377 cm^2/s),
+    parabolic inlet of mean 10 cm/s, 8 Windkessel RCR outlets alternating the
+    Table 2 ground-truth parameters."""
+    raw = synth.htree(depth=3, r0=1.0, l0=8.0, target_cells=target_cells, scramble=scramble)
+    bcs = [("inlet", "U", PARABOLIC, dict(u_max=20.0, center=(0.0, 0.0, 0.0), radius=1.0)),
+           ("wall", "U", FIXED, dict(value=(0.0, 0.0, 0.0))), ("inlet", "p", ZEROGRAD, {}), ("wall", "p", ZEROGRAD, {})]
+    outlets = [p.name for p in raw.patches if p.name.startswith("outlet")]
+    for o in outlets:
+        bcs.append((o, "U", ZEROGRAD, {}))
+    gt = [(100.0, 1.1111e-3, 900.0), (160.0, 6.9444e-4, 1440.0)]
+    wk = [(o, gt[i % 2]) for i, o in enumerate(outlets)]
+    solver = dict(nu=0.04 / 1.06, dt=1e-3, rho=1.06, n_corr=2, n_nonorth=1, convection="upwind", p_ref_cell=0,
+                  **THROUGHPUT)
+    ic = lambda xc, xf, Sf: (np.zeros((len(xc), 3)), np.zeros(len(xc)), np.zeros(len(Sf)))
+    case = Case(f"c4_htree_tet_{raw.n_cells}", raw, bcs, solver, ic,
+                f"voxelised H-tree, alternating 5-tet, N={raw.n_cells}, 8 RCR outlets (Table 2 values)")
+    case.windkessel = wk     # list of (patch, (Rp, C, Rd)); pc0 = 0, exact integrator
+    return case
+
+
+CONFIGS = {"c1": c1, "c2": c2, "c4": c4, "c5": c5}

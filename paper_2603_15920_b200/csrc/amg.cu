@@ -23,6 +23,7 @@
 //    coarse solve is a fixed symmetric polynomial, so M^-1 is SPD and CG
 //    stays CG.  The converged pressure is preconditioner independent (A-14).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -34,9 +35,27 @@ namespace dfvm {
 
 dfvm_status halo_exchange(dfvm_mesh* m, void* data, int nc, cudaStream_t s);
 
-constexpr int kCoarseMax = 2048;
-constexpr int kCoarseSweeps = 24;
+constexpr int kCoarseMax = 2048;     // shared-memory capacity of the one-block coarse solve
 constexpr int kMaxLevels = 16;
+
+// Tunables (defaults chosen from B200 measurements on the C5 pipe, DESIGN.md
+// §6); overridable through the environment for experiments:
+//   DFVM_AMG_COARSE  coarsest-level size bound (rows)           default 256
+//   DFVM_AMG_SWEEPS  l1-Jacobi sweeps of the coarsest solve       default 32
+//   DFVM_AMG_CYCLE   'V' or 'W'                                   default W
+//   DFVM_AMG_WMAX    deepest level visited twice by the W-cycle   default 3
+//                    (deeper levels use V-cycles: the W launch count
+//                    doubles per level, and deep levels are launch-bound)
+struct AmgParams {
+  int coarse = 256, sweeps = 32, wmax = 3;
+  bool wcycle = true;
+  AmgParams() {
+    if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kCoarseMax, atoi(e)));
+    if (const char* e = getenv("DFVM_AMG_SWEEPS")) sweeps = std::max(1, atoi(e));
+    if (const char* e = getenv("DFVM_AMG_CYCLE")) wcycle = (e[0] == 'W' || e[0] == 'w');
+    if (const char* e = getenv("DFVM_AMG_WMAX")) wmax = std::max(0, atoi(e));
+  }
+};
 
 // ------------------------------------------------------------ host setup
 namespace {
@@ -120,12 +139,14 @@ struct AmgLevelDev {
   int *mem_ptr = nullptr, *mem = nullptr;         // per coarse row: fine member rows
   int* agg = nullptr;                             // on the FINE level: fine row -> coarse row
   T *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr;
+  T *e = nullptr, *r2 = nullptr;                  // W-cycle: second-visit solution / rhs
 };
 
 template <class T>
 struct Amg {
   dfvm_mesh* m = nullptr;
   int nlev = 0;
+  AmgParams prm;
   AmgLevelDev<T> L[kMaxLevels];
   std::vector<void*> allocs;
   int64_t bytes = 0;
@@ -170,7 +191,7 @@ dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, Amg<T>** out) {
   if ((st = A->zalloc(&L0.dl1, M.n_own)) || (st = A->zalloc(&L0.x, M.n_cells)) || (st = A->zalloc(&L0.r, M.n_own)) ||
       (st = A->zalloc(&L0.t, M.n_cells))) { delete A; return st; }
   int lev = 0;
-  while (H[lev].n > kCoarseMax && lev + 1 < kMaxLevels) {
+  while (H[lev].n > A->prm.coarse && lev + 1 < kMaxLevels) {
     const HostLevel& F = H[lev];
     int nc = 0;
     std::vector<int> agg = aggregate(F, nc);
@@ -248,7 +269,8 @@ dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, Amg<T>** out) {
         (st = A->up(&D.dg_idx, dg_idx)) || (st = A->up(&D.mem_ptr, mem_ptr)) || (st = A->up(&D.mem, mem)) ||
         (st = A->up(&A->L[lev].agg, agg)) || (st = A->zalloc(&D.coef_own, (size_t)D.n_sell)) ||
         (st = A->zalloc(&D.diag_own, nc)) || (st = A->zalloc(&D.dl1, nc)) || (st = A->zalloc(&D.x, nc)) ||
-        (st = A->zalloc(&D.b, nc)) || (st = A->zalloc(&D.r, nc)) || (st = A->zalloc(&D.t, nc))) {
+        (st = A->zalloc(&D.b, nc)) || (st = A->zalloc(&D.r, nc)) || (st = A->zalloc(&D.t, nc)) ||
+        (st = A->zalloc(&D.e, nc)) || (st = A->zalloc(&D.r2, nc))) {
       delete A;
       return st;
     }
@@ -363,6 +385,12 @@ __global__ void k_amg_prolong(int n, const int* __restrict__ agg, const T* __res
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = x[i] + xc[agg[i]];
 }
+// x += e
+template <class T>
+__global__ void k_amg_add(int n, const T* __restrict__ e, T* __restrict__ x, const int* done) {
+  if (*done) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] += e[i];
+}
 // out = x + (b - A x) / d1
 template <class T>
 __global__ void k_amg_smooth(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
@@ -373,18 +401,19 @@ __global__ void k_amg_smooth(int n, const int* __restrict__ ms_ptr, const int* _
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = x[i] + (b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x)) / dl1[i];
 }
-// coarsest level: kCoarseSweeps l1-Jacobi sweeps from zero, one block, in shared memory
+// coarsest level: `sweeps` l1-Jacobi sweeps from zero, one block, in shared memory
 template <class T>
 __global__ void __launch_bounds__(1024) k_amg_coarse(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
                                                     const int* __restrict__ mnb, const T* __restrict__ coef,
                                                     const T* __restrict__ diag, const T* __restrict__ dl1,
-                                                    const T* __restrict__ b, T* __restrict__ xout, const int* done) {
+                                                    const T* __restrict__ b, T* __restrict__ xout, int sweeps,
+                                                    const int* done) {
   if (*done) return;
   __shared__ T xs[2][kCoarseMax];
   for (int i = threadIdx.x; i < n; i += blockDim.x) xs[0][i] = b[i] / dl1[i];
   __syncthreads();
   int cur = 0;
-  for (int it = 1; it < kCoarseSweeps; ++it) {
+  for (int it = 1; it < sweeps; ++it) {
     for (int i = threadIdx.x; i < n; i += blockDim.x)
       xs[cur ^ 1][i] = xs[cur][i] + (b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, xs[cur])) / dl1[i];
     __syncthreads();
@@ -413,52 +442,55 @@ dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s
   return DFVM_OK;
 }
 
-// z = M^-1 r (one V(1,1) cycle); skipped on the device when *done is set
+// x = M_l^-1 b from a zero guess: pre-smooth, residual, restriction, coarse
+// correction (twice on coarse levels for the W-cycle: the second visit
+// solves for the residual of the first), prolongation, post-smooth.  Each
+// level's operator is symmetric (adjoint pre/post Jacobi, symmetric coarse
+// polynomial, and two successive symmetric corrections 2B - BAB), so the
+// preconditioner stays SPD.  Level 0 exchanges ghosts before its SpMVs.
+template <class T>
+static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cudaStream_t s, int* nl) {
+  AmgLevelDev<T>& F = A->L[l];
+  dfvm_status e;
+  if (l == A->nlev - 1) {
+    if (l == 0 && A->m->part.P > 1) {   // single level with ghost columns: one l1-Jacobi step
+      k_amg_pre<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, b, F.dl1, x, done);
+    } else {
+      k_amg_coarse<T><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b, x,
+                                         A->prm.sweeps, done);
+    }
+    ++*nl;
+    return DFVM_OK;
+  }
+  AmgLevelDev<T>& C = A->L[l + 1];
+  k_amg_pre<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, b, F.dl1, x, done);
+  if (l == 0 && (e = halo_exchange(A->m, x, 1, s))) return e;
+  k_amg_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, x, b, F.r, done);
+  k_amg_restrict<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
+  *nl += 3;
+  if ((e = cycle(A, l + 1, C.b, C.x, done, s, nl))) return e;
+  if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax) {
+    // second visit: C.x += M^-1 (C.b - A C.x)
+    k_amg_resid<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b,
+                                                       C.r2, done);
+    ++*nl;
+    if ((e = cycle(A, l + 1, C.r2, C.e, done, s, nl))) return e;
+    k_amg_add<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done);
+    ++*nl;
+  }
+  k_amg_prolong<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, x, F.t, done);
+  if (l == 0 && (e = halo_exchange(A->m, F.t, 1, s))) return e;
+  k_amg_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, F.t, b,
+                                                      x, done);
+  *nl += 2;
+  return DFVM_OK;
+}
+
+// z = M^-1 r; skipped on the device when *done is set
 template <class T>
 dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl) {
-  const int nlev = A->nlev;
-  dfvm_status e;
-  // descend
-  for (int l = 0; l < nlev - 1; ++l) {
-    AmgLevelDev<T>& F = A->L[l];
-    AmgLevelDev<T>& C = A->L[l + 1];
-    const T* b = l == 0 ? r : F.b;
-    T* x = l == 0 ? z : F.x;
-    k_amg_pre<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, b, F.dl1, x, done);
-    if (l == 0 && (e = halo_exchange(A->m, x, 1, s))) return e;
-    k_amg_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, x, b, F.r, done);
-    k_amg_restrict<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
-    *nl += 3;
-  }
-  // coarsest
-  {
-    AmgLevelDev<T>& C = A->L[nlev - 1];
-    if (nlev == 1) {
-      // single level (<= 2048 rows): on one rank the one-block smoother is the
-      // whole preconditioner; with ghost columns (several ranks) it cannot run
-      // in shared memory, so one l1-Jacobi step is used instead
-      if (A->m->part.P == 1)
-        k_amg_coarse<T><<<1, 1024, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.dl1, r, z, done);
-      else
-        k_amg_pre<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, r, C.dl1, z, done);
-      *nl += 1;
-      return DFVM_OK;
-    }
-    k_amg_coarse<T><<<1, 1024, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.dl1, C.b, C.x, done);
-    *nl += 1;
-  }
-  // ascend
-  for (int l = nlev - 2; l >= 0; --l) {
-    AmgLevelDev<T>& F = A->L[l];
-    AmgLevelDev<T>& C = A->L[l + 1];
-    const T* b = l == 0 ? r : F.b;
-    T* x = l == 0 ? z : F.x;
-    k_amg_prolong<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, x, F.t, done);
-    if (l == 0 && (e = halo_exchange(A->m, F.t, 1, s))) return e;
-    k_amg_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, F.t, b,
-                                                        x, done);
-    *nl += 2;
-  }
+  dfvm_status e = cycle(A, 0, r, z, done, s, nl);
+  if (e) return e;
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
 }

@@ -209,3 +209,33 @@ def test_f32_piso_close_to_f64():
     for _ in range(5):
         So.step(U, p, phi)
     assert rel_l2(Ug.get(), U) <= 1e-4 and rel_l2(pg.get(), p) <= 1e-3
+
+
+@pytest.mark.parametrize("precond", ["jacobi", "amg"])
+def test_htree_windkessel_outlets(precond):
+    # C4 recipe at small size: voxelised H-tree, 8 RCR outlets (Table 2 values)
+    import cases
+    case = cases.c4(target_cells=6e4)
+    mo = oracle.Mesh(case.raw)
+    mg = dfvm.Mesh(case.raw)
+    kw = dict(case.solver, **TIGHT)
+    kw["p_tol"], kw["U_tol"] = 1e-13, 1e-13
+    So = oracle.Solver(mo, case.apply_bcs(oracle.BCs(mo)), **kw)
+    Sg = dfvm.Solver(mg, case.apply_bcs(dfvm.BCs(mg)), p_precond=precond, **kw)
+    for patch, (Rp, Cc, Rd) in case.windkessel:
+        So.windkessel_set(patch, Rp, Cc, Rd, 0.0, 0)
+        Sg.windkessel_set(patch, Rp, Cc, Rd, 0.0, 0)
+    U, p, phi = case.initial_state(mo.xc, mo.xf, mo.Sf)
+    Ug, pg, phig = mg.field("cells", 3, U), mg.field("cells", 1, p), mg.field("flux", 1, phi)
+    for _ in range(3):
+        ro = So.step(U, p, phi)
+        rg = Sg.step(Ug, pg, phig)
+        assert np.allclose(rg["Q"], ro["Q"], rtol=1e-8, atol=1e-12) and np.allclose(rg["p_o"], ro["p_o"], rtol=1e-8)
+    assert rel_l2(Ug.get(), U) <= 1e-8 and rel_l2(pg.get(), p) <= 1e-8
+    # mass balance of the final fluxes: outlets carry what the inlet brings
+    # (walls carry none), to the continuity tolerance
+    phig_h = phig.get()
+    raw = case.raw
+    inflow = sum(phig_h[pt.start:pt.start + pt.n].sum() for pt in raw.patches if pt.name == "inlet")
+    outflow = sum(phig_h[pt.start:pt.start + pt.n].sum() for pt in raw.patches if pt.name.startswith("outlet"))
+    assert abs(inflow + outflow) <= 1e-9 * abs(inflow)
