@@ -46,10 +46,13 @@ constexpr int kMaxLevels = 16;
 //   DFVM_AMG_WMAX    deepest level visited twice by the W-cycle   default 3
 //                    (deeper levels use V-cycles: the W launch count
 //                    doubles per level, and deep levels are launch-bound)
+//   DFVM_AMG_OMEGA   coarse-correction scale (symmetric over-correction) default 1
 struct AmgParams {
   int coarse = 256, sweeps = 32, wmax = 3;
   bool wcycle = true;
+  double omega = 1.0;
   AmgParams() {
+    if (const char* e = getenv("DFVM_AMG_OMEGA")) omega = atof(e);
     if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kCoarseMax, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_SWEEPS")) sweeps = std::max(1, atoi(e));
     if (const char* e = getenv("DFVM_AMG_CYCLE")) wcycle = (e[0] == 'W' || e[0] == 'w');
@@ -378,12 +381,12 @@ __global__ void k_amg_restrict(int nc, const int* __restrict__ mp, const int* __
     bc[I] = s;
   }
 }
-// t = x + x_c[agg[i]]  (coarse correction, out of place: t feeds the smoother)
+// t = x + w x_c[agg[i]]  (coarse correction, out of place: t feeds the smoother)
 template <class T>
 __global__ void k_amg_prolong(int n, const int* __restrict__ agg, const T* __restrict__ xc, const T* __restrict__ x,
-                              T* __restrict__ t, const int* done) {
+                              T* __restrict__ t, T w, const int* done) {
   if (*done) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = x[i] + xc[agg[i]];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = x[i] + w * xc[agg[i]];
 }
 // x += e
 template <class T>
@@ -478,7 +481,7 @@ static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cu
     k_amg_add<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done);
     ++*nl;
   }
-  k_amg_prolong<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, x, F.t, done);
+  k_amg_prolong<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, x, F.t, (T)A->prm.omega, done);
   if (l == 0 && (e = halo_exchange(A->m, F.t, 1, s))) return e;
   k_amg_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, F.t, b,
                                                       x, done);
