@@ -388,6 +388,51 @@ __global__ void k_amg_prolong(int n, const int* __restrict__ agg, const T* __res
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = x[i] + w * xc[agg[i]];
 }
+// fused pre-smooth + residual (rows without ghost columns): x0 = b / d1 for
+// the row and, on the fly, for every neighbour; writes x0 and r = b - A x0
+template <class T>
+__global__ void k_amg_pre_resid(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                                const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
+                                const T* __restrict__ dl1, const T* __restrict__ b, T* __restrict__ x0,
+                                T* __restrict__ r, const int* done) {
+  if (*done) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = i >> 5, lane = i & 31;
+    const int len = ms_len[s], base = ms_ptr[s] + lane;
+    const T bi = b[i];
+    const T xi = bi / dl1[i];
+    T acc = diag[i] * xi;
+    for (int j = 0; j < len; ++j) {
+      const int c = __ldg(&mnb[base + 32 * j]);
+      acc += __ldg(&coef[base + 32 * j]) * (b[c] / dl1[c]);
+    }
+    x0[i] = xi;
+    r[i] = bi - acc;
+  }
+}
+// fused prolongation + post-smooth: t = x0 + w P x_c (on the fly for the row
+// and its neighbours), out = t + (b - A t) / d1
+template <class T>
+__global__ void k_amg_prolong_smooth(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                                     const int* __restrict__ mnb, const T* __restrict__ coef,
+                                     const T* __restrict__ diag, const T* __restrict__ dl1,
+                                     const int* __restrict__ agg, const T* __restrict__ xc, T w,
+                                     const T* __restrict__ x0, const T* __restrict__ b, T* __restrict__ out,
+                                     const int* done) {
+  if (*done) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = i >> 5, lane = i & 31;
+    const int len = ms_len[s], base = ms_ptr[s] + lane;
+    const T ti = x0[i] + w * xc[agg[i]];
+    T acc = diag[i] * ti;
+    for (int j = 0; j < len; ++j) {
+      const int c = __ldg(&mnb[base + 32 * j]);
+      acc += __ldg(&coef[base + 32 * j]) * (x0[c] + w * xc[agg[c]]);
+    }
+    out[i] = ti + (b[i] - acc) / dl1[i];
+  }
+}
+
 // x += e
 template <class T>
 __global__ void k_amg_add(int n, const T* __restrict__ e, T* __restrict__ x, const int* done) {
@@ -466,11 +511,21 @@ static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cu
     return DFVM_OK;
   }
   AmgLevelDev<T>& C = A->L[l + 1];
-  k_amg_pre<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, b, F.dl1, x, done);
-  if (l == 0 && (e = halo_exchange(A->m, x, 1, s))) return e;
-  k_amg_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, x, b, F.r, done);
+  // ghost columns exist only on level 0 with several ranks: there the
+  // pre-smoothed x (and later t) must be exchanged, so the unfused kernels run
+  const bool ghosts = (l == 0 && A->m->part.P > 1);
+  T* x0 = ghosts ? x : F.t;
+  if (ghosts) {
+    k_amg_pre<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, b, F.dl1, x, done);
+    if ((e = halo_exchange(A->m, x, 1, s))) return e;
+    k_amg_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, x, b, F.r, done);
+    ++*nl;
+  } else {
+    k_amg_pre_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b,
+                                                           x0, F.r, done);
+  }
   k_amg_restrict<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
-  *nl += 3;
+  *nl += 2;
   if ((e = cycle(A, l + 1, C.b, C.x, done, s, nl))) return e;
   if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax) {
     // second visit: C.x += M^-1 (C.b - A C.x)
@@ -481,11 +536,17 @@ static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cu
     k_amg_add<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done);
     ++*nl;
   }
-  k_amg_prolong<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, x, F.t, (T)A->prm.omega, done);
-  if (l == 0 && (e = halo_exchange(A->m, F.t, 1, s))) return e;
-  k_amg_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, F.t, b,
-                                                      x, done);
-  *nl += 2;
+  if (ghosts) {
+    k_amg_prolong<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, x, F.t, (T)A->prm.omega, done);
+    if ((e = halo_exchange(A->m, F.t, 1, s))) return e;
+    k_amg_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, F.t,
+                                                        b, x, done);
+    *nl += 2;
+  } else {
+    k_amg_prolong_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag,
+                                                                F.dl1, F.agg, C.x, (T)A->prm.omega, x0, b, x, done);
+    *nl += 1;
+  }
   return DFVM_OK;
 }
 
