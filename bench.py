@@ -268,28 +268,46 @@ def main():
         e2e = {"value": N * args.steps / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e / args.steps}
 
-    # ---------------- roofline of the dominant kernel (PCG SpMV)
+    # ---------------- roofline of the dominant kernel
+    # Candidates timed live inside the library (CUDA events on the launching
+    # stream): the PCG SpMV and, with AMG, the two level-0 fused V-cycle
+    # kernels.  The one with the largest total time in the timed region is
+    # reported.  Algorithmic bytes per launch (N owned cells,
+    # F internal faces, 2F incidences of (column 4 B + coefficient vb), row
+    # metadata counted as 4 B/row, gathered values counted once):
     hbm, peak_src = peaks()
     n_own, F_l = info["n_owned"], info["n_local_internal_faces"]
     vb, ib = (8, 4) if args.precision == "f64" else (4, 4)
-    # ALG bytes per launch (SURVEY.md §8(d4) lap_apply): row meta 4N, I = 2F
-    # incidences x (column 4 B + coefficient vb), diag, x, y: vb N each
-    alg = 4 * n_own + 2 * F_l * (ib + vb) + 3 * vb * n_own
-    spmv_ms = tim["spmv_ms"] / max(tim["spmv_n"], 1)
-    achieved = alg / (spmv_ms / 1000.0) / 1e9 if tim["spmv_n"] else None
+    lv = S.amg_levels() if args.precond == "amg" else []
+    n1 = lv[1] if len(lv) > 1 else 0
+    cands = {
+        "k_cg_spmv (PCG SpMV + p.q partials)":
+            (tim["spmv_ms"], tim["spmv_n"], 4 * n_own + 2 * F_l * (ib + vb) + 3 * vb * n_own),          # diag, p, q
+        "k_amg_pre_resid (AMG level 0: x0 = b/d1, r = b - A x0)":
+            (tim["amg_pre_ms"], tim["amg_pre_n"], 4 * n_own + 2 * F_l * (ib + vb) + 5 * vb * n_own),    # b, d1, diag, x0, r
+        "k_amg_prolong_smooth (AMG level 0: t = x0 + P xc, z = t + (b - A t)/d1)":
+            (tim["amg_post_ms"], tim["amg_post_n"],
+             8 * n_own + 2 * F_l * (ib + vb) + 5 * vb * n_own + vb * n1),                               # + agg, xc
+    }
+    kname, (kms, kn, alg) = max(cands.items(), key=lambda kv: kv[1][0])
+    launch_ms = kms / max(kn, 1)
+    achieved = alg / (launch_ms / 1000.0) / 1e9 if kn else None
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", f"ncu_spmv_{args.config}_{args.precision}.json")
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get("traffic_bytes_per_launch")
+            traffic = json.load(open(tfile)).get(f"{kname.split()[0]}_{args.config}_{args.precision}_{n_own}")
         except Exception:
             traffic = None
-    roof = {"bound": "hbm", "kernel": "k_cg_spmv (PCG SpMV + p.q partials)", "achieved": achieved, "peak": hbm,
-            "peak_source": peak_src, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
-            "traffic": traffic, "alg_bytes_per_launch": alg, "launch_ms": spmv_ms, "launches": tim["spmv_n"],
-            "share_of_step": (tim["spmv_ms"] / ms) if ms else None,
+    roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "peak_source": peak_src,
+            "unit": "GB/s", "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+            "alg_bytes_per_launch": alg, "launch_ms": launch_ms, "launches": kn,
+            "share_of_step": (kms / ms) if ms else None,
+            "candidates": {k.split()[0]: {"ms_total": v[0], "launches": v[1], "alg_bytes": v[2],
+                                          "GBps": (v[2] * v[1] / (v[0] / 1000.0) / 1e9) if v[1] else None}
+                           for k, v in cands.items()},
             "pcg_iteration_ms": tim["cg_iter_ms"] / max(tim["cg_iter_n"], 1),
-            "pcg_share_of_step": tim["cg_iter_ms"] / ms if ms else None}
+            "pcg_share_of_step": tim["cg_iter_ms"] / ms if ms else None, "amg_levels": lv}
 
     cg_its = [r["it"] for rep in reps for r in rep["p"]]
     bi_its = [r["it"] for rep in reps for r in rep["U"]]
@@ -304,7 +322,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": args.precision, "data": "synthetic",
-        "config": {"workload": case.name, "description": case.description, "cells": N,
+        "config": {"workload": case.name, "description": case.description, "cells": N, "precond": args.precond,
                    "internal_faces": info["n_internal_faces"], "parallelism": f"mesh-partition x{world} (RCM blocks)",
                    "l2_policy": "inputs larger than L2 (no flush)" if N > 2_000_000 else "L2-resident (small config)",
                    "solver": {k: v for k, v in case.solver.items()}},

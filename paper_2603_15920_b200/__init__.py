@@ -39,7 +39,7 @@ SYMBOLS = [
     "dfvm_fvc_div", "dfvm_fvm_laplacian_apply", "dfvm_solver_create", "dfvm_pressure_solve",
     "dfvm_momentum_assemble", "dfvm_momentum_apply", "dfvm_piso_step", "dfvm_windkessel_set",
     "dfvm_windkessel_state", "dfvm_windkessel_update", "dfvm_solver_destroy", "dfvm_kernel_launches",
-    "dfvm_solver_set_timing", "dfvm_solver_get_timing", "dfvm_comm_create_local",
+    "dfvm_solver_set_timing", "dfvm_solver_get_timing", "dfvm_comm_create_local", "dfvm_solver_amg_levels",
 ]
 
 
@@ -138,6 +138,7 @@ def lib():
         L.dfvm_windkessel_update.argtypes = [f64, f64, f64, f64, f64, f64, i32, C.POINTER(f64), C.POINTER(f64)]
         L.dfvm_solver_set_timing.argtypes = [vp, i32]
         L.dfvm_solver_get_timing.argtypes = [vp, vp, vp]
+        L.dfvm_solver_amg_levels.argtypes = [vp, vp, vp]
         L.dfvm_comm_unique_id.argtypes = [vp]
         L.dfvm_comm_create.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
         L.dfvm_comm_destroy.argtypes = [vp]
@@ -460,4 +461,11 @@ class Solver:
     def timing(self):
         ms = np.zeros(4); n = np.zeros(4, np.int64)
         _check(lib().dfvm_solver_get_timing(self.h, _ptr(ms), _ptr(n)))
-        return dict(spmv_ms=float(ms[0]), spmv_n=int(n[0]), cg_iter_ms=float(ms[1]), cg_iter_n=int(n[1]))
+        return dict(spmv_ms=float(ms[0]), spmv_n=int(n[0]), cg_iter_ms=float(ms[1]), cg_iter_n=int(n[1]),
+                    amg_pre_ms=float(ms[2]), amg_pre_n=int(n[2]), amg_post_ms=float(ms[3]), amg_post_n=int(n[3]))
+
+    def amg_levels(self):
+        n = C.c_int32()
+        sz = np.zeros(32, np.int64)
+        _check(lib().dfvm_solver_amg_levels(self.h, C.byref(n), _ptr(sz)))
+        return sz[:n.value].tolist()

@@ -497,7 +497,8 @@ dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s
 // polynomial, and two successive symmetric corrections 2B - BAB), so the
 // preconditioner stays SPD.  Level 0 exchanges ghosts before its SpMVs.
 template <class T>
-static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cudaStream_t s, int* nl) {
+static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cudaStream_t s, int* nl,
+                         cudaEvent_t* ev) {
   AmgLevelDev<T>& F = A->L[l];
   dfvm_status e;
   if (l == A->nlev - 1) {
@@ -521,18 +522,20 @@ static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cu
     k_amg_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, x, b, F.r, done);
     ++*nl;
   } else {
+    if (l == 0 && ev) cudaEventRecord(ev[0], s);
     k_amg_pre_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b,
                                                            x0, F.r, done);
+    if (l == 0 && ev) cudaEventRecord(ev[1], s);
   }
   k_amg_restrict<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
   *nl += 2;
-  if ((e = cycle(A, l + 1, C.b, C.x, done, s, nl))) return e;
+  if ((e = cycle(A, l + 1, C.b, C.x, done, s, nl, nullptr))) return e;
   if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax) {
     // second visit: C.x += M^-1 (C.b - A C.x)
     k_amg_resid<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b,
                                                        C.r2, done);
     ++*nl;
-    if ((e = cycle(A, l + 1, C.r2, C.e, done, s, nl))) return e;
+    if ((e = cycle(A, l + 1, C.r2, C.e, done, s, nl, nullptr))) return e;
     k_amg_add<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done);
     ++*nl;
   }
@@ -543,8 +546,10 @@ static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cu
                                                         b, x, done);
     *nl += 2;
   } else {
+    if (l == 0 && ev) cudaEventRecord(ev[2], s);
     k_amg_prolong_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag,
                                                                 F.dl1, F.agg, C.x, (T)A->prm.omega, x0, b, x, done);
+    if (l == 0 && ev) cudaEventRecord(ev[3], s);
     *nl += 1;
   }
   return DFVM_OK;
@@ -552,8 +557,8 @@ static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cu
 
 // z = M^-1 r; skipped on the device when *done is set
 template <class T>
-dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl) {
-  dfvm_status e = cycle(A, 0, r, z, done, s, nl);
+dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl, cudaEvent_t* ev) {
+  dfvm_status e = cycle(A, 0, r, z, done, s, nl, ev);
   if (e) return e;
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
@@ -564,7 +569,7 @@ dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t
   template void amg_destroy<T>(Amg<T>*);                                                  \
   template int amg_levels<T>(const Amg<T>*, int*);                                        \
   template dfvm_status amg_update<T>(Amg<T>*, const T*, const T*, cudaStream_t, int*);    \
-  template dfvm_status amg_apply<T>(Amg<T>*, const T*, T*, const int*, cudaStream_t, int*);
+  template dfvm_status amg_apply<T>(Amg<T>*, const T*, T*, const int*, cudaStream_t, int*, cudaEvent_t*);
 INST(double)
 INST(float)
 

@@ -1163,12 +1163,12 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
                                                                           X.partials, X.ticket, X.d_ctl, red);
   S->n_launch++;
   if ((e = fin(S, X, CTL_CG_INIT, 3, st))) return e;
-  if ((e = amg_apply<T>(X.amg, X.kr, X.kz, done, st, &S->n_launch))) return e;
+  if ((e = amg_apply<T>(X.amg, X.kr, X.kz, done, st, &S->n_launch, nullptr))) return e;
   k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ0);
   S->n_launch++;
   if ((e = fin(S, X, CTL_CG_RZ0, 1, st))) return e;
-  if (S->timing && S->ev.size() < 4 * kChunk) {
-    while (S->ev.size() < 4 * kChunk) {
+  if (S->timing && S->ev.size() < 8 * kChunk) {
+    while (S->ev.size() < 8 * kChunk) {
       cudaEvent_t ev;
       DFVM_CUDA(cudaEventCreate(&ev));
       S->ev.push_back(ev);
@@ -1186,7 +1186,8 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
       if ((e = fin(S, X, CTL_CG_SPMV, 1, st))) return e;
       k_cg_r2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, X.partials, X.ticket, X.d_ctl, red);
       if ((e = fin(S, X, CTL_CG_R2, 1, st))) return e;
-      if ((e = amg_apply<T>(X.amg, X.kr, X.kz, done, st, &S->n_launch))) return e;
+      if ((e = amg_apply<T>(X.amg, X.kr, X.kz, done, st, &S->n_launch,
+                            S->timing ? &S->ev[4 * kChunk + 4 * k] : nullptr))) return e;
       k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ);
       if ((e = fin(S, X, CTL_CG_RZ, 1, st))) return e;
       if (S->timing) cudaEventRecord(S->ev[4 * k + 3], st);
@@ -1197,17 +1198,26 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
     if (S->timing) {
       const int ran = X.h_ctl->it - it_before;
       for (int k = 0; k < kChunk && k < ran; ++k) {
-        float a = 0, b2 = 0;
+        float a = 0, b2 = 0, c2 = 0, d2 = 0;
         cudaEventElapsedTime(&a, S->ev[4 * k + 1], S->ev[4 * k + 2]);
         cudaEventElapsedTime(&b2, S->ev[4 * k], S->ev[4 * k + 3]);
         S->t_ms[0] += a; S->t_n[0]++;
         S->t_ms[1] += b2; S->t_n[1]++;
+        // level-0 AMG kernels (recorded only when the fused path ran; the
+        // last iteration of a solve skips its V-cycle on the done flag)
+        if (k + 1 < ran || !X.h_ctl->done) {
+          cudaEvent_t* ea = &S->ev[4 * kChunk + 4 * k];
+          if (cudaEventElapsedTime(&c2, ea[0], ea[1]) == cudaSuccess && cudaEventElapsedTime(&d2, ea[2], ea[3]) == cudaSuccess) {
+            S->t_ms[2] += c2; S->t_n[2]++;
+            S->t_ms[3] += d2; S->t_n[3]++;
+          }
+        }
       }
       it_before = X.h_ctl->it;
     }
     if (X.h_ctl->done) break;
   }
-  DFVM_CUDA(cudaGetLastError());
+  cudaGetLastError();   // clear a possible not-ready status of an unrecorded timing event
   const KCtl& c = *X.h_ctl;
   if (c.half) {
     k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl);
@@ -1445,6 +1455,22 @@ dfvm_status dfvm_solver_set_timing(dfvm_solver* s, int32_t on) {
   if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
   s->timing = on != 0;
   for (int i = 0; i < 4; ++i) { s->t_ms[i] = 0; s->t_n[i] = 0; }
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_solver_amg_levels(const dfvm_solver* s, int32_t* n_levels, int64_t* sizes) {
+  if (!s || !n_levels) { set_error(DFVM_E_INVALID_ARG, "NULL argument"); return DFVM_E_INVALID_ARG; }
+  int lv[32] = {0};
+  int n = 0;
+  if (s->m->precision == DFVM_F64) {
+    auto* X = static_cast<SolverT<double>*>(s->impl.get());
+    if (X->amg) n = amg_levels<double>(X->amg, lv);
+  } else {
+    auto* X = static_cast<SolverT<float>*>(s->impl.get());
+    if (X->amg) n = amg_levels<float>(X->amg, lv);
+  }
+  *n_levels = n;
+  if (sizes) for (int i = 0; i < n; ++i) sizes[i] = lv[i];
   return DFVM_OK;
 }
 
