@@ -74,6 +74,7 @@ def lib():
         L.orc_piso_step.argtypes = [vp, vp, vp, vp, vp]
         L.orc_momentum_assemble.argtypes = [vp] * 7
         L.orc_pressure_solve.argtypes = [vp, vp, vp, vp, f64, f64, i32, i32, vp]
+        L.orc_transport_step.argtypes = [vp, vp, vp, f64, vp]
         L.orc_poisson_steady.restype = i32
         L.orc_poisson_steady.argtypes = [vp, vp, vp, vp, f64, i32, i32, f64]
         L.orc_renumber_create.restype = vp
@@ -239,7 +240,7 @@ class Solver:
         # depend on the preconditioner (A-14)
         self.mesh, self.bcs = mesh, bcs
         d = np.array([nu, dt, rho, p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, U_tol, U_rel_tol], np.float64)
-        i = np.array([n_corr, n_nonorth, {"upwind": 0, "central": 1}[convection], p_ref_cell,
+        i = np.array([n_corr, n_nonorth, {"upwind": 0, "central": 1, "sou": 2, "quick": 3}[convection], p_ref_cell,
                       1 if direct else 0, p_maxit, U_maxit], np.int64)
         self.h = lib().orc_solver_create(mesh.h, bcs.h, _p(d), _p(i))
 
@@ -270,6 +271,13 @@ class Solver:
         U, phi = _f64(U), _f64(phi)
         _check(lib().orc_momentum_assemble(self.h, _p(U), _p(phi), _p(diag), _p(lo), _p(up), _p(b)))
         return diag, lo, up, b
+
+    def transport_step(self, x, phi, gamma):
+        """One implicit step of passive-scalar transport (field 's' BCs), x updated in place."""
+        rep = np.zeros(4)
+        phi = _f64(phi)
+        st = lib().orc_transport_step(self.h, _p(x), _p(phi), gamma, _p(rep))
+        return dict(it=int(rep[0]), res0=rep[1], res=rep[2], converged=bool(rep[3]), status=STATUS[st])
 
     def pressure_solve(self, rAU, rhs, p0=None, tol=1e-14, rel_tol=0.0, maxit=50000, direct=False):
         p = np.zeros(self.mesh.N) if p0 is None else _f64(p0).copy()

@@ -217,31 +217,40 @@ static SolveReport solve(const Solver& S, const LDU& A, const double* rhs, doubl
              : bicgstab(*S.m, A, rhs, x, tol, rel_tol, maxit);
 }
 
-// O-5: momentum LDU from (U^n, phi^n, grad U^n) — eq:fvm_momentum P:157-168,
-// eq:conv_face_flux P:174-181, eq:upwind P:185-191 (tie -> owner, A-17),
-// central = linear weight (A-7), eq:diff_ortho / eq:nonortho_flux with the
-// explicit correction from grad U^n (A-16), implicit Euler (A-11).
-static void assemble_momentum(const Solver& S, const double* U, const double* phi,
-                              LDU& M, std::vector<double>& bvec) {
+// O-5: transport LDU for the momentum (ncomp 3, field 'U', diffusivity nu)
+// or a passive scalar (ncomp 1, field 's', diffusivity Gamma) from
+// (x^n, phi^n, grad x^n) — eq:fvm_momentum P:157-168, eq:conv_face_flux
+// P:174-181, eq:upwind P:185-191 (tie -> owner, A-17), central = linear
+// weight (A-7), eq:diff_ortho / eq:nonortho_flux with the explicit
+// correction from grad x^n (A-16), implicit Euler (A-11).
+// Convection 2 (SOU) / 3 (QUICK): upwind implicit part plus the explicit
+// deferred correction m_f (x_f^HO - x_f^U) (eq:deferred_correction
+// P:193-199), SOU x_f^HO = x_C + (grad x)_C . d_Cf (eq:sou P:200-206), QUICK
+// x_f^HO = x_C + 1/2 [(grad x)_C . d_Cf + (x_D - x_C)(d_Cf . d_CD)/|d_CD|^2]
+// (SPEC.md:233 reading), C the upwind and D the downwind cell; the
+// correction leaves the owner row (b_O -= c) and enters the neighbour row.
+static void assemble_transport(const Solver& S, int nc, int fi, double diffusivity, const double* U,
+                               const double* phi, LDU& M, std::vector<double>& bvec) {
   const Mesh& m = *S.m;
   const BCs& b = *S.b;
-  const double nu = S.o.nu, dt = S.o.dt;
+  const double nu = diffusivity, dt = S.o.dt;
+  const int conv = S.o.convection;
   const int64_t N = m.N;
   M.diag.assign(N, 0); M.lower.assign(m.F, 0); M.upper.assign(m.F, 0);
-  bvec.assign(3 * N, 0);
-  std::vector<double> G(9 * N);
-  grad(m, b, 0, 3, U, G.data());
-  // cell-wise accumulation in ascending face order (time term last is a
-  // per-cell constant and is added first to keep the order explicit)
+  bvec.assign((size_t)nc * N, 0);
+  std::vector<double> G((size_t)3 * nc * N);
+  grad(m, b, fi, nc, U, G.data());
+  auto lambda = [&](int64_t f, double md) { return conv == 1 ? m.w[f] : (md >= 0 ? 1.0 : 0.0); };
+  // cell-wise accumulation in ascending face order (the time term, a
+  // per-cell constant, is added first to keep the order explicit)
   for (int64_t c = 0; c < N; ++c) {
     const double vdt = m.V[c] / dt;
     M.diag[c] = vdt;
-    for (int k = 0; k < 3; ++k) bvec[3 * c + k] = vdt * U[3 * c + k];
+    for (int k = 0; k < nc; ++k) bvec[(size_t)nc * c + k] = vdt * U[(size_t)nc * c + k];
   }
   for (int64_t f = 0; f < m.F; ++f) {
-    const int64_t O = m.owner[f], Nn = m.neigh[f];
     const double md = phi[f];
-    const double lam = S.o.convection == 0 ? (md >= 0 ? 1.0 : 0.0) : m.w[f];
+    const double lam = lambda(f, md);
     const double nd = nu * m.delta[f];
     M.upper[f] = (1.0 - lam) * md - nd;
     M.lower[f] = -lam * md - nd;
@@ -252,39 +261,59 @@ static void assemble_momentum(const Solver& S, const double* U, const double* ph
       if (f < m.F) {
         const int64_t O = m.owner[f], Nn = m.neigh[f];
         const double md = phi[f];
-        const double lam = S.o.convection == 0 ? (md >= 0 ? 1.0 : 0.0) : m.w[f];
+        const double lam = lambda(f, md);
         const double nd = nu * m.delta[f];
         const double w = m.w[f];
-        double corr[3];
-        for (int k = 0; k < 3; ++k) {
-          double s = 0;
+        double corr[3] = {0, 0, 0};
+        for (int k = 0; k < nc; ++k) {
+          double s2 = 0;
           for (int l = 0; l < 3; ++l)
-            s += m.kf[3 * f + l] * (w * G[9 * O + 3 * k + l] + (1.0 - w) * G[9 * Nn + 3 * k + l]);
-          corr[k] = nu * s;
+            s2 += m.kf[3 * f + l] * (w * G[(size_t)3 * nc * O + 3 * k + l] + (1.0 - w) * G[(size_t)3 * nc * Nn + 3 * k + l]);
+          corr[k] = nu * s2;
+        }
+        double dc[3] = {0, 0, 0};   // deferred convection correction
+        if (conv >= 2) {
+          const int64_t Cc = md >= 0 ? O : Nn, D = md >= 0 ? Nn : O;
+          double dCf[3], dCD[3];
+          for (int l = 0; l < 3; ++l) { dCf[l] = m.xf[3 * f + l] - m.xc[3 * Cc + l]; dCD[l] = m.xc[3 * D + l] - m.xc[3 * Cc + l]; }
+          const double fCD = (dCf[0] * dCD[0] + dCf[1] * dCD[1] + dCf[2] * dCD[2]) /
+                             (dCD[0] * dCD[0] + dCD[1] * dCD[1] + dCD[2] * dCD[2]);
+          for (int k = 0; k < nc; ++k) {
+            const double* Gc = &G[(size_t)3 * nc * Cc + 3 * k];
+            const double gd = Gc[0] * dCf[0] + Gc[1] * dCf[1] + Gc[2] * dCf[2];
+            const double xC = U[(size_t)nc * Cc + k], xD = U[(size_t)nc * D + k];
+            const double hi = conv == 2 ? xC + gd : xC + 0.5 * (gd + (xD - xC) * fCD);
+            dc[k] = md * (hi - xC);
+          }
         }
         if (O == c) {
           M.diag[c] += lam * md + nd;
-          for (int k = 0; k < 3; ++k) bvec[3 * c + k] += corr[k];
+          for (int k = 0; k < nc; ++k) bvec[(size_t)nc * c + k] += corr[k] - dc[k];
         } else {
           M.diag[c] += -(1.0 - lam) * md + nd;
-          for (int k = 0; k < 3; ++k) bvec[3 * c + k] -= corr[k];
+          for (int k = 0; k < nc; ++k) bvec[(size_t)nc * c + k] += -corr[k] + dc[k];
         }
       } else {
         const int p = m.face_patch[f - m.F];
         if (m.pkind[p] == PK_EMPTY) continue;
         const double mb = phi[f];
-        if (is_fixed(b, 0, p)) {
+        if (is_fixed(b, fi, p)) {
           double Ub[3];
-          boundary_value(m, b, 0, 3, U, f, Ub);
+          boundary_value(m, b, fi, nc, U, f, Ub);
           const double nd = nu * m.delta_b[f - m.F];
           M.diag[c] += nd;
-          for (int k = 0; k < 3; ++k) bvec[3 * c + k] += -mb * Ub[k] + nd * Ub[k];
+          for (int k = 0; k < nc; ++k) bvec[(size_t)nc * c + k] += -mb * Ub[k] + nd * Ub[k];
         } else {
-          M.diag[c] += mb;  // zeroGradient: outflow m_b U_O
+          M.diag[c] += mb;  // zeroGradient: outflow m_b x_O
         }
       }
     }
   }
+}
+
+static void assemble_momentum(const Solver& S, const double* U, const double* phi, LDU& M,
+                              std::vector<double>& bvec) {
+  assemble_transport(S, 3, 0, S.o.nu, U, phi, M, bvec);
 }
 
 // H_c(U) = b_c - sum_nb a_{c,nb} U_nb (eq:Ap_H P:333-335, pressure excluded)
@@ -578,6 +607,19 @@ int orc_momentum_assemble(void* sp, const double* U, const double* phi, double* 
   std::memcpy(upper, M.upper.data(), 8 * M.upper.size());
   std::memcpy(b, bv.data(), 8 * bv.size());
   return OK;
+}
+
+// One implicit-Euler step of passive-scalar transport (NEXT-1 workload,
+// PAPER.md §3.1.2): d(x)/dt + div(phi x) - div(Gamma grad x) = 0
+// with the face flux phi fixed, field 's' boundary conditions and the
+// solver's convection scheme; BiCGStab (or dense LU in direct mode) from x^n.
+int orc_transport_step(void* sp, double* x, const double* phi, double gamma, double* rep) {
+  Solver* S = (Solver*)sp;
+  LDU M; std::vector<double> bv;
+  assemble_transport(*S, 1, 2, gamma, x, phi, M, bv);
+  SolveReport r = solve(*S, M, bv.data(), x, false, S->o.U_tol, S->o.U_rel_tol, S->o.U_maxit);
+  rep[0] = r.it; rep[1] = r.res0; rep[2] = r.res; rep[3] = r.converged;
+  return r.status;
 }
 
 // Pressure solve of O-6 step 3.5 on its own: A_p(rAU) p = rhs with the gauge

@@ -319,3 +319,33 @@ def cell_field(seed, n_cells, n_comp=1):
 
 def face_field(seed, n_faces):
     return urand(seed, np.arange(n_faces, dtype=np.uint64))
+
+
+def square_tri(n=20, jitter=0.25, seed=7, scramble=5, y_step=0.5):
+    """Unit square [0,1]^2 triangulated (Delaunay of an (n+1)^2 lattice with
+    interior vertices jittered by jitter*h, order-independent splitmix64) and
+    extruded one layer (dz = 1/n, empty front/back) — the paper's step
+    advection domain (§3.1.2, unstructured triangular mesh).
+    Patches: inlet_lower (x=0, y<y_step, and y=0), inlet_upper (x=0,
+    y>=y_step), outlet (x=1 and y=1), frontAndBack (empty)."""
+    from scipy.spatial import Delaunay
+    h = 1.0 / n
+    ij = np.array([(i, j) for j in range(n + 1) for i in range(n + 1)], np.float64)
+    pts = ij * h
+    vid = np.arange(len(pts), dtype=np.uint64)
+    interior = (ij[:, 0] > 0) & (ij[:, 0] < n) & (ij[:, 1] > 0) & (ij[:, 1] < n)
+    pts[interior, 0] += jitter * h * urand(seed, 2 * vid[interior])
+    pts[interior, 1] += jitter * h * urand(seed, 2 * vid[interior] + np.uint64(1))
+    tri = Delaunay(pts).simplices
+    polys = []
+    for t in tri:
+        a, b, c = pts[t[0]], pts[t[1]], pts[t[2]]
+        cross = (b[0] - a[0]) * (c[1] - a[1]) - (b[1] - a[1]) * (c[0] - a[0])
+        polys.append([int(t[0]), int(t[1]), int(t[2])] if cross > 0 else [int(t[0]), int(t[2]), int(t[1])])
+    e = 1e-9
+    rules = [(-1.0, e, -1.0, y_step - e, 0), (-1.0, e, -1.0, 2.0, 1), (-1.0, 2.0, -1.0, e, 0),
+             (1 - e, 2.0, -1.0, 2.0, 2), (-1.0, 2.0, 1 - e, 2.0, 2)]
+    m = extrude_polygons(pts, polys, h, ["inlet_lower", "inlet_upper", "outlet", "frontAndBack"],
+                         [PATCH_GENERIC, PATCH_GENERIC, PATCH_GENERIC, PATCH_EMPTY], rules, 3, scramble)
+    m.meta = dict(kind="square_tri", n=n, dz=h, y_step=y_step)
+    return m
