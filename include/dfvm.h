@@ -239,7 +239,9 @@ typedef struct {
   double nu, dt, rho;           /* kinematic viscosity, time step, density (Windkessel only, A-23) */
   int32_t n_corr;               /* PISO correctors ("typically twice") */
   int32_t n_nonorth;            /* non-orthogonal correctors per pressure solve (A-15) */
-  int32_t convection;           /* 0 upwind (eq:upwind), 1 central (A-7) */
+  int32_t convection;           /* 0 upwind (eq:upwind), 1 central (A-7), 2 SOU and 3 QUICK by
+                                   deferred correction (eq:deferred_correction P:193-199,
+                                   eq:sou P:200-206, QUICK reading of SPEC.md:233) */
   int64_t p_ref_cell;           /* original numbering; used when no fixed-value p patch exists (A-12) */
   double p_ref_value;
   double p_tol, p_rel_tol, p_rel_tol_final; int32_t p_maxit;  /* A-13 stopping rule */
@@ -278,6 +280,13 @@ dfvm_status dfvm_momentum_assemble(dfvm_solver* s, const dfvm_field* U, const df
                                    dfvm_field* b, dfvm_stream stream);
 /* y = M x with the last assembled momentum matrix, x, y: [cells][3] */
 dfvm_status dfvm_momentum_apply(dfvm_solver* s, const dfvm_field* x, dfvm_field* y, dfvm_stream stream);
+/* One implicit-Euler step of passive-scalar transport (NEXT-1; §3.1.2
+ * P:477-491): dx/dt + div(phi x) - div(gamma grad x) = 0 with the face flux
+ * phi [faces] fixed, field 's' boundary conditions, the solver's dt,
+ * convection scheme and U_* tolerances; x [cells] updated in place.
+ * Uses (and overwrites) the solver's transport matrix workspace. */
+dfvm_status dfvm_transport_step(dfvm_solver* s, dfvm_field* x, const dfvm_field* phi, double gamma,
+                                dfvm_solve_report* rep, dfvm_stream stream);
 /* One PISO step (§8(c) O-6) advancing U [cells][3], p [cells],
  * phi [faces] in place. */
 dfvm_status dfvm_piso_step(dfvm_solver* s, dfvm_field* U, dfvm_field* p, dfvm_field* phi, dfvm_step_report* rep,

@@ -40,6 +40,7 @@ SYMBOLS = [
     "dfvm_momentum_assemble", "dfvm_momentum_apply", "dfvm_piso_step", "dfvm_windkessel_set",
     "dfvm_windkessel_state", "dfvm_windkessel_update", "dfvm_solver_destroy", "dfvm_kernel_launches",
     "dfvm_solver_set_timing", "dfvm_solver_get_timing", "dfvm_comm_create_local", "dfvm_solver_amg_levels",
+    "dfvm_transport_step",
 ]
 
 
@@ -139,6 +140,7 @@ def lib():
         L.dfvm_solver_set_timing.argtypes = [vp, i32]
         L.dfvm_solver_get_timing.argtypes = [vp, vp, vp]
         L.dfvm_solver_amg_levels.argtypes = [vp, vp, vp]
+        L.dfvm_transport_step.argtypes = [vp, vp, vp, f64, C.POINTER(SolveReport), vp]
         L.dfvm_comm_unique_id.argtypes = [vp]
         L.dfvm_comm_create.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
         L.dfvm_comm_destroy.argtypes = [vp]
@@ -407,7 +409,8 @@ class Solver:
                  p_ref_value=0.0, p_tol=1e-14, p_rel_tol=0.0, p_rel_tol_final=0.0, p_maxit=50000, U_tol=1e-14,
                  U_rel_tol=0.0, U_maxit=50000, p_precond="jacobi"):
         self.mesh, self.bcs = mesh, bcs
-        o = PisoOpts(nu, dt, rho, n_corr, n_nonorth, {"upwind": 0, "central": 1}[convection], p_ref_cell,
+        o = PisoOpts(nu, dt, rho, n_corr, n_nonorth, {"upwind": 0, "central": 1, "sou": 2, "quick": 3}[convection],
+                     p_ref_cell,
                      p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, p_maxit, U_tol, U_rel_tol, U_maxit,
                      {"jacobi": 0, "amg": 1}[p_precond])
         h = C.c_void_p()
@@ -445,6 +448,14 @@ class Solver:
         r = SolveReport()
         st = _check(lib().dfvm_pressure_solve(self.h, rAU.h, rhs.h, p.h, tol, rel_tol, maxit, C.byref(r), stream),
                     allow=(8,))
+        d = _rep(r)
+        d["status"] = STATUS[st]
+        return d
+
+    def transport_step(self, x, phi, gamma, stream=None):
+        """One implicit passive-scalar transport step (field 's' BCs); x updated in place."""
+        r = SolveReport()
+        st = _check(lib().dfvm_transport_step(self.h, x.h, phi.h, gamma, C.byref(r), stream), allow=(8,))
         d = _rep(r)
         d["status"] = STATUS[st]
         return d

@@ -217,21 +217,29 @@ __device__ __forceinline__ void sell_apply(const DevMesh<T>& M, int s, int lane,
   const int nw_ = (gridDim.x * blockDim.x) >> 5;                                           \
   for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < (M).n_slices; s += nw_)
 
-// ============================================================ momentum
-// O-5: diag, b (time + BC + explicit non-orthogonal terms), rhsU = b - V grad p,
-// SELL coefficients (upper for the owner side, lower for the neighbour side).
-template <class T>
-__global__ void __launch_bounds__(kThreads) k_mom_assemble(DevMesh<T> M, const T* __restrict__ U,
+// ============================================================ momentum / transport
+// O-5 transport LDU for NC components (momentum: NC = 3, field 'U', nu;
+// passive scalar: NC = 1, field 's', Gamma): diag, b (time + BC + explicit
+// non-orthogonal terms), rhs = b - V grad p (when gp != NULL), SELL
+// coefficients (upper for the owner side, lower for the neighbour side).
+// conv: 0 upwind, 1 central (implicit via the face weight), 2 SOU, 3 QUICK —
+// 2/3: implicit upwind + explicit deferred correction m (x^HO - x_C)
+// (eq:deferred_correction, eq:sou P:200-206, SPEC.md:233 QUICK),
+// with dO = x_f - x_O, dN = x_f - x_N per face.
+template <class T, int NC>
+__global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, const T* __restrict__ U,
     const T* __restrict__ phi, const T* __restrict__ gU, const T* __restrict__ gp, const uint8_t* __restrict__ bk,
-    const T* __restrict__ bv, T nu, T rdt, int upwind, int kcorr, T* __restrict__ udiag, T* __restrict__ bU,
-    T* __restrict__ rhsU, T* __restrict__ ucoef) {
+    const T* __restrict__ bv, T nu, T rdt, int conv, int kcorr, const V4<T>* __restrict__ fdO,
+    const V4<T>* __restrict__ fdN, T* __restrict__ udiag, T* __restrict__ bU, T* __restrict__ rhsU,
+    T* __restrict__ ucoef) {
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
     const T V = live ? M.vol[row] : T(0);
     T diag = V * rdt;
-    T b0 = T(0), b1 = T(0), b2 = T(0);
-    if (live) { b0 = diag * U[3 * (int64_t)row]; b1 = diag * U[3 * (int64_t)row + 1]; b2 = diag * U[3 * (int64_t)row + 2]; }
+    T bb[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) bb[k] = live ? diag * U[NC * (int64_t)row + k] : T(0);
     const int len = __ldg(&M.sl_len[s]);
     const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
     const int mbase = __ldg(&M.ms_ptr[s]) + lane;
@@ -244,34 +252,63 @@ __global__ void __launch_bounds__(kThreads) k_mom_assemble(DevMesh<T> M, const T
         const T w = ld4(&M.fgeo[f]).w;
         const V4<T> c = ld4(&M.fcor[f]);
         const T md = phi[f];
-        const T lam = upwind ? (md >= T(0) ? T(1) : T(0)) : w;
+        const T lam = conv == 1 ? w : (md >= T(0) ? T(1) : T(0));
         const T nd = nu * c.w;
         T cf;
         if (own) { diag += lam * md + nd; cf = (T(1) - lam) * md - nd; }
         else { diag += -(T(1) - lam) * md + nd; cf = -lam * md - nd; }
         ucoef[mbase + 32 * (mj++)] = cf;
-        if (kcorr) {
-          const int n = en.y;
-          const int O = own ? row : n, N = own ? n : row;
-          const T* GO = gU + 9 * (int64_t)O;
-          const T* GN = gU + 9 * (int64_t)N;
-          T cr[3];
+        const int n = en.y;
+        const int O = own ? row : n, N = own ? n : row;
+        T cr[NC];
 #pragma unroll
-          for (int k = 0; k < 3; ++k)
+        for (int k = 0; k < NC; ++k) cr[k] = T(0);
+        if (kcorr) {
+          const T* GO = gU + 3 * NC * (int64_t)O;
+          const T* GN = gU + 3 * NC * (int64_t)N;
+#pragma unroll
+          for (int k = 0; k < NC; ++k)
             cr[k] = nu * (c.x * (w * GO[3 * k] + (T(1) - w) * GN[3 * k]) +
                           c.y * (w * GO[3 * k + 1] + (T(1) - w) * GN[3 * k + 1]) +
                           c.z * (w * GO[3 * k + 2] + (T(1) - w) * GN[3 * k + 2]));
-          if (own) { b0 += cr[0]; b1 += cr[1]; b2 += cr[2]; }
-          else { b0 -= cr[0]; b1 -= cr[1]; b2 -= cr[2]; }
+        }
+        if (conv >= 2) {
+          const bool up_own = md >= T(0);
+          const int Cc = up_own ? O : N, D = up_own ? N : O;
+          const V4<T> a = ld4(up_own ? &fdO[f] : &fdN[f]);            // d_Cf = x_f - x_C
+          const V4<T> o4 = ld4(&fdO[f]), n4 = ld4(&fdN[f]);
+          T dCD[3] = {o4.x - n4.x, o4.y - n4.y, o4.z - n4.z};           // x_N - x_O
+          if (!up_own) { dCD[0] = -dCD[0]; dCD[1] = -dCD[1]; dCD[2] = -dCD[2]; }
+          const T fCD = (a.x * dCD[0] + a.y * dCD[1] + a.z * dCD[2]) /
+                        (dCD[0] * dCD[0] + dCD[1] * dCD[1] + dCD[2] * dCD[2]);
+          const T* GC = gU + 3 * NC * (int64_t)Cc;
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            const T gd = GC[3 * k] * a.x + GC[3 * k + 1] * a.y + GC[3 * k + 2] * a.z;
+            const T xC = U[NC * (int64_t)Cc + k], xD = U[NC * (int64_t)D + k];
+            const T hi = conv == 2 ? xC + gd : xC + T(0.5) * (gd + (xD - xC) * fCD);
+            const T dc = md * (hi - xC);
+            cr[k] = cr[k] - dc;        // owner row: + (corr - dc); neighbour row: - (corr - dc)
+          }
+        }
+        if (own) {
+#pragma unroll
+          for (int k = 0; k < NC; ++k) bb[k] += cr[k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < NC; ++k) bb[k] -= cr[k];
         }
       } else if (en.y == -1) {
         const int b = en.x;
         const T mb = phi[M.F + b];
         if (bk[b] == 0) {
           const T nd = nu * ld4(&M.bgeo[b]).w;
-          const T u0 = bv[3 * (int64_t)b], u1 = bv[3 * (int64_t)b + 1], u2 = bv[3 * (int64_t)b + 2];
           diag += nd;
-          b0 += -mb * u0 + nd * u0; b1 += -mb * u1 + nd * u1; b2 += -mb * u2 + nd * u2;
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            const T ub = bv[NC * (int64_t)b + k];
+            bb[k] += -mb * ub + nd * ub;
+          }
         } else {
           diag += mb;
         }
@@ -279,10 +316,11 @@ __global__ void __launch_bounds__(kThreads) k_mom_assemble(DevMesh<T> M, const T
     }
     if (live) {
       udiag[row] = diag;
-      bU[3 * (int64_t)row] = b0; bU[3 * (int64_t)row + 1] = b1; bU[3 * (int64_t)row + 2] = b2;
-      rhsU[3 * (int64_t)row] = b0 - V * gp[3 * (int64_t)row];
-      rhsU[3 * (int64_t)row + 1] = b1 - V * gp[3 * (int64_t)row + 1];
-      rhsU[3 * (int64_t)row + 2] = b2 - V * gp[3 * (int64_t)row + 2];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        bU[NC * (int64_t)row + k] = bb[k];
+        rhsU[NC * (int64_t)row + k] = gp ? bb[k] - V * gp[3 * (int64_t)row + k] : bb[k];
+      }
     }
   }
 }
@@ -603,6 +641,19 @@ __global__ void k_windkessel_fin(const double* __restrict__ all, int P, int n_wk
 
 template <class T>
 __global__ void k_add_at(T* a, const T* b, int i) { a[i] += b[i]; }
+
+// scalar <-> component 0 of a 3-vector (the scalar transport reuses the
+// 3-component BiCGStab; components 1, 2 have b = 0 and stop at iteration 0)
+template <class T>
+__global__ void k_pack3(int n, const T* __restrict__ a, T* __restrict__ a3) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    a3[3 * (int64_t)i] = a[i]; a3[3 * (int64_t)i + 1] = T(0); a3[3 * (int64_t)i + 2] = T(0);
+  }
+}
+template <class T>
+__global__ void k_unpack3(int n, const T* __restrict__ a3, T* __restrict__ a) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = a3[3 * (int64_t)i];
+}
 
 // ============================================================ Jacobi PCG
 // r = b - A x; partials b.b, r.r, r.z  -> control start
@@ -932,6 +983,8 @@ struct SolverT : SolverBase {
   double* h_cont = nullptr;  // pinned
   double* red_local = nullptr;  // [8] this rank's reduction totals (P > 1)
   double* red_all = nullptr;    // [P][8] all-gathered totals
+  V4<T>* fdO = nullptr;         // x_f - x_O / x_f - x_N per local internal face (SOU / QUICK)
+  V4<T>* fdN = nullptr;
   Amg<T>* amg = nullptr;        // pressure preconditioner (p_precond == 1), built lazily
   bool amg_dirty = true;        // pressure matrix changed since the last Galerkin update
   T* kz = nullptr;              // preconditioned residual z = M^-1 r
@@ -954,6 +1007,28 @@ struct SolverT : SolverBase {
     DFVM_CUDA(cudaMemset(q, 0, std::max<size_t>(n, 1) * sizeof(U)));
     allocs.push_back(q);
     *p = (U*)q;
+    return DFVM_OK;
+  }
+  // face-to-cell displacements for the deferred-correction schemes (O-1 fp64
+  // geometry in the renumbered orientation)
+  dfvm_status build_face_offsets() {
+    if (fdO) return DFVM_OK;
+    const HostMesh& H = m->H;
+    const Part& P = m->part;
+    const size_t F = P.lf_gid.size();
+    std::vector<V4<T>> o(std::max<size_t>(F, 1)), n(std::max<size_t>(F, 1));
+    for (size_t i = 0; i < F; ++i) {
+      const int64_t k = P.lf_gid[i];
+      const double* xf = &H.xf0[3 * (int64_t)H.fold_of_new[k]];
+      const double* xo = &H.xc0[3 * (int64_t)H.old_of_new[H.own[k]]];
+      const double* xn = &H.xc0[3 * (int64_t)H.old_of_new[H.nb[k]]];
+      o[i] = V4<T>{(T)(xf[0] - xo[0]), (T)(xf[1] - xo[1]), (T)(xf[2] - xo[2]), T(0)};
+      n[i] = V4<T>{(T)(xf[0] - xn[0]), (T)(xf[1] - xn[1]), (T)(xf[2] - xn[2]), T(0)};
+    }
+    dfvm_status st;
+    if ((st = al(&fdO, o.size())) || (st = al(&fdN, n.size()))) return st;
+    DFVM_CUDA(cudaMemcpy(fdO, o.data(), o.size() * sizeof(V4<T>), cudaMemcpyHostToDevice));
+    DFVM_CUDA(cudaMemcpy(fdN, n.data(), n.size() * sizeof(V4<T>), cudaMemcpyHostToDevice));
     return DFVM_OK;
   }
   dfvm_status init(dfvm_mesh* mm, DevMesh<T>* MM) {
@@ -1294,9 +1369,9 @@ static dfvm_status assemble(dfvm_solver* S, SolverT<T>& X, const T* U, const T* 
   launch_grad<T>(M, U, 3, b->d_kind[0], (const T*)b->d_val[0], X.gU, st);
   S->n_launch++;
   if ((s2 = halo_exchange(S->m, X.gU, 9, st))) return s2;
-  k_mom_assemble<T><<<gs, kThreads, 0, st>>>(M, U, phi, X.gU, X.gp, b->d_kind[0], (const T*)b->d_val[0],
-                                             (T)S->o.nu, (T)(1.0 / S->o.dt), S->o.convection == 0 ? 1 : 0,
-                                             S->kcorr, X.udiag, X.bU, X.rhsU, X.ucoef);
+  k_transport_assemble<T, 3><<<gs, kThreads, 0, st>>>(M, U, phi, X.gU, X.gp, b->d_kind[0], (const T*)b->d_val[0],
+                                                      (T)S->o.nu, (T)(1.0 / S->o.dt), S->o.convection, S->kcorr,
+                                                      X.fdO, X.fdN, X.udiag, X.bU, X.rhsU, X.ucoef);
   S->n_launch++;
   if ((s2 = halo_exchange(S->m, X.udiag, 1, st))) return s2;   // k_bi_t gathers s / diag
   X.assembled = true;
@@ -1419,13 +1494,53 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
 
 }  // namespace dfvm
 
+namespace dfvm {
+
+// One implicit-Euler step of passive-scalar transport (NEXT-1 workload,
+// PAPER.md §3.1.2): d x/dt + div(phi x) - div(Gamma grad x) = 0
+// with the face flux phi fixed, field 's' boundary conditions and the
+// solver's convection scheme (upwind / central / SOU / QUICK deferred
+// correction); BiCGStab from x^n.
+template <class T>
+static dfvm_status transport_step_t(dfvm_solver* S, SolverT<T>& X, T* x, const T* phi, double gamma,
+                                    dfvm_solve_report* rep, cudaStream_t st) {
+  DevMesh<T>& M = *X.M;
+  dfvm_bcs* b = S->b;
+  dfvm_status e;
+  if ((e = bcs_device(b, 2, st))) return e;
+  S->n_launch = 0;
+  if ((e = halo_exchange(S->m, x, 1, st))) return e;
+  launch_grad<T>(M, x, 1, b->d_kind[2], (const T*)b->d_val[2], X.gp, st);
+  if ((e = halo_exchange(S->m, X.gp, 3, st))) return e;
+  const int gs = grid_for_slices(M.n_slices), ge = grid_for(M.n_own);
+  k_transport_assemble<T, 1><<<gs, kThreads, 0, st>>>(M, x, phi, X.gp, nullptr, b->d_kind[2], (const T*)b->d_val[2],
+                                                      (T)gamma, (T)(1.0 / S->o.dt), S->o.convection, S->kcorr,
+                                                      X.fdO, X.fdN, X.udiag, X.prhs0, X.prhs, X.ucoef);
+  if ((e = halo_exchange(S->m, X.udiag, 1, st))) return e;
+  k_pack3<T><<<ge, kThreads, 0, st>>>(M.n_own, X.prhs, X.bU);
+  k_pack3<T><<<grid_for(M.n_cells), kThreads, 0, st>>>(M.n_cells, x, X.HbyA);
+  S->n_launch += 4;
+  X.assembled = true;
+  dfvm_solve_report r3[3];
+  dfvm_status res = run_bicgstab(S, X, X.bU, X.HbyA, S->o.U_tol, S->o.U_rel_tol, S->o.U_maxit, r3, st);
+  k_unpack3<T><<<ge, kThreads, 0, st>>>(M.n_own, X.HbyA, x);
+  S->n_launch++;
+  DFVM_CUDA(cudaStreamSynchronize(st));
+  DFVM_CUDA(cudaGetLastError());
+  count_launch(S->n_launch);
+  if (rep) *rep = r3[0];
+  return res;
+}
+
+}  // namespace dfvm
+
 extern "C" {
 
 dfvm_status dfvm_solver_create(dfvm_mesh* m, dfvm_bcs* b, const dfvm_piso_opts* opts, dfvm_solver** out) {
   if (!m || !b || !opts || !out || b->m != m) { set_error(DFVM_E_INVALID_ARG, "NULL or mismatched argument"); return DFVM_E_INVALID_ARG; }
   if (!(opts->dt > 0) || !(opts->nu >= 0) || opts->n_corr < 1 || opts->n_corr > 8 || opts->n_nonorth < 0 ||
       (opts->n_corr * (opts->n_nonorth + 1)) > 16 || opts->p_maxit < 1 || opts->U_maxit < 1 || !(opts->rho > 0) ||
-      opts->p_precond < 0 || opts->p_precond > 1) {
+      opts->p_precond < 0 || opts->p_precond > 1 || opts->convection < 0 || opts->convection > 3) {
     set_error(DFVM_E_INVALID_ARG, "invalid PISO options");
     return DFVM_E_INVALID_ARG;
   }
@@ -1441,10 +1556,12 @@ dfvm_status dfvm_solver_create(dfvm_mesh* m, dfvm_bcs* b, const dfvm_piso_opts* 
     auto* X = new SolverT<double>();
     S->impl.reset(X);
     st = X->init(m, &m->d64);
+    if (!st && opts->convection >= 2) st = X->build_face_offsets();
   } else {
     auto* X = new SolverT<float>();
     S->impl.reset(X);
     st = X->init(m, &m->d32);
+    if (!st && opts->convection >= 2) st = X->build_face_offsets();
   }
   if (st) return st;
   *out = S.release();
@@ -1537,6 +1654,21 @@ static dfvm_status check_f(const dfvm_field* f, const dfvm_mesh* m, bool cells, 
     return DFVM_E_INVALID_ARG;
   }
   return DFVM_OK;
+}
+
+dfvm_status dfvm_transport_step(dfvm_solver* s, dfvm_field* x, const dfvm_field* phi, double gamma,
+                                dfvm_solve_report* rep, dfvm_stream stream) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  dfvm_status st;
+  if ((st = check_f(x, s->m, true, 1, "x")) || (st = check_f(phi, s->m, false, 1, "phi"))) return st;
+  if (!(gamma >= 0)) { set_error(DFVM_E_INVALID_ARG, "diffusivity must be >= 0"); return DFVM_E_INVALID_ARG; }
+  cudaSetDevice(s->m->device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (s->m->precision == DFVM_F64)
+    return transport_step_t<double>(s, *static_cast<SolverT<double>*>(s->impl.get()), (double*)x->ptr,
+                                    (const double*)phi->ptr, gamma, rep, cs);
+  return transport_step_t<float>(s, *static_cast<SolverT<float>*>(s->impl.get()), (float*)x->ptr,
+                                 (const float*)phi->ptr, gamma, rep, cs);
 }
 
 dfvm_status dfvm_piso_step(dfvm_solver* s, dfvm_field* U, dfvm_field* p, dfvm_field* phi, dfvm_step_report* rep,

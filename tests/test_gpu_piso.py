@@ -64,8 +64,10 @@ def run_both(raw, mo, mg, bo, bg, kw, steps, U0=None, wk=None, direct=True):
     return (U, p, phi), (Ug.get(), pg.get(), phig.get()), reps, So, Sg
 
 
-def test_momentum_assembly_and_apply():
+@pytest.mark.parametrize("conv", ["upwind", "central", "sou", "quick"])
+def test_momentum_assembly_and_apply(conv):
     raw, mo, mg, bo, bg, kw = pipe_case()
+    kw = dict(kw, convection=conv)
     So = oracle.Solver(mo, bo, **kw)
     Sg = dfvm.Solver(mg, bg, **kw)
     U = synth.cell_field(40, mo.N, 3)
@@ -138,10 +140,11 @@ def test_cavity_regression_values_on_gpu(golden):
     assert abs(p.min() - g["step1"]["p_min"]) <= 1e-8 and abs(p.max() - g["step1"]["p_max"]) <= 1e-8
 
 
-@pytest.mark.parametrize("precond", ["jacobi", "amg"])
-def test_pipe_nonorth_steps(precond):
+@pytest.mark.parametrize("precond,conv", [("jacobi", "upwind"), ("amg", "upwind"), ("amg", "sou"),
+                                          ("jacobi", "quick")])
+def test_pipe_nonorth_steps(precond, conv):
     raw, mo, mg, bo, bg, kw = pipe_case()
-    kw = dict(kw, p_precond=precond)
+    kw = dict(kw, p_precond=precond, convection=conv)
     xc = mo.xc
     U0 = np.zeros((mo.N, 3))
     U0[:, 2] = 2.0 * (1 - 4 * (xc[:, 0] ** 2 + xc[:, 1] ** 2))
@@ -239,3 +242,31 @@ def test_htree_windkessel_outlets(precond):
     inflow = sum(phig_h[pt.start:pt.start + pt.n].sum() for pt in raw.patches if pt.name == "inlet")
     outflow = sum(phig_h[pt.start:pt.start + pt.n].sum() for pt in raw.patches if pt.name.startswith("outlet"))
     assert abs(inflow + outflow) <= 1e-9 * abs(inflow)
+
+
+@pytest.mark.parametrize("conv", ["upwind", "central", "sou", "quick"])
+def test_scalar_transport_step_advection(conv):
+    # NEXT-1 workload (§3.1.2): step profile, u = (2, 1, 0), Gamma = 1e-3
+    raw = synth.square_tri(16, jitter=0.2)
+    mo = oracle.Mesh(raw)
+    mg = dfvm.Mesh(raw)
+    specs = [("inlet_lower", "s", oracle.BC_FIXED, dict(value=1.0)), ("inlet_upper", "s", oracle.BC_FIXED, dict(value=0.0)),
+             ("outlet", "s", oracle.BC_ZEROGRAD, {})]
+    for pn in ("inlet_lower", "inlet_upper", "outlet"):
+        specs += [(pn, "U", oracle.BC_ZEROGRAD, {}), (pn, "p", oracle.BC_ZEROGRAD, {})]
+    bo, bg = make_bcs(raw, specs, mo, mg)
+    kw = dict(nu=0.0, dt=0.02, convection=conv, U_tol=1e-13, U_maxit=2000)
+    So = oracle.Solver(mo, bo, **kw)
+    Sg = dfvm.Solver(mg, bg, **kw)
+    phi = mo.Sf @ np.array([2.0, 1.0, 0.0])
+    for p in raw.patches:
+        if p.kind == synth.PATCH_EMPTY:
+            phi[p.start:p.start + p.n] = 0.0
+    x = np.zeros(mo.N)
+    xg = mg.field("cells", 1, x)
+    fg = mg.field("flux", 1, phi)
+    for _ in range(20):
+        So.transport_step(x, phi, 1e-3)
+        r = Sg.transport_step(xg, fg, 1e-3)
+        assert r["converged"]
+    assert rel_l2(xg.get(), x) <= 1e-10
