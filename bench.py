@@ -270,8 +270,8 @@ def main():
 
     # ---------------- roofline of the dominant kernel
     # Candidates timed live inside the library (CUDA events on the launching
-    # stream): the PCG SpMV and, with AMG, the two level-0 fused V-cycle
-    # kernels.  The one with the largest total time in the timed region is
+    # stream): the PCG SpMV and, with AMG, the two level-0 V-cycle SpMV
+    # kernels (residual, post-smoother).  The one with the largest total time in the timed region is
     # reported.  Algorithmic bytes per launch (N owned cells,
     # F internal faces, 2F incidences of (column 4 B + coefficient vb), row
     # metadata counted as 4 B/row, gathered values counted once):
@@ -279,15 +279,13 @@ def main():
     n_own, F_l = info["n_owned"], info["n_local_internal_faces"]
     vb, ib = (8, 4) if args.precision == "f64" else (4, 4)
     lv = S.amg_levels() if args.precond == "amg" else []
-    n1 = lv[1] if len(lv) > 1 else 0
     cands = {
         "k_cg_spmv (PCG SpMV + p.q partials)":
             (tim["spmv_ms"], tim["spmv_n"], 4 * n_own + 2 * F_l * (ib + vb) + 3 * vb * n_own),          # diag, p, q
-        "k_amg_pre_resid (AMG level 0: x0 = b/d1, r = b - A x0)":
-            (tim["amg_pre_ms"], tim["amg_pre_n"], 4 * n_own + 2 * F_l * (ib + vb) + 5 * vb * n_own),    # b, d1, diag, x0, r
-        "k_amg_prolong_smooth (AMG level 0: t = x0 + P xc, z = t + (b - A t)/d1)":
-            (tim["amg_post_ms"], tim["amg_post_n"],
-             8 * n_own + 2 * F_l * (ib + vb) + 5 * vb * n_own + vb * n1),                               # + agg, xc
+        "k_amg_resid (AMG level-0 residual: r = b - A x)":
+            (tim["amg_pre_ms"], tim["amg_pre_n"], 4 * n_own + 2 * F_l * (ib + vb) + 4 * vb * n_own),    # x, diag, b, r
+        "k_amg_smooth (AMG level-0 post-smoother: z = t + (b - A t)/d1)":
+            (tim["amg_post_ms"], tim["amg_post_n"], 4 * n_own + 2 * F_l * (ib + vb) + 5 * vb * n_own),  # t, diag, d1, b, z
     }
     kname, (kms, kn, alg) = max(cands.items(), key=lambda kv: kv[1][0])
     launch_ms = kms / max(kn, 1)

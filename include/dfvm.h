@@ -306,9 +306,9 @@ dfvm_status dfvm_solver_destroy(dfvm_solver* s);
  * accumulates the durations of the iterations that actually ran.
  * ms[0]/count[0]: the PCG SpMV kernel (q = A p, p.q partials); ms[1]/count[1]:
  * one whole PCG iteration (p update, SpMV, r update, and with AMG the
- * preconditioner cycle and r.z).  With AMG: ms[2]/count[2] the level-0 fused
- * pre-smooth + residual kernel, ms[3]/count[3] the level-0 fused
- * prolongation + post-smooth kernel.  set_timing resets the accumulators. */
+ * preconditioner cycle and r.z).  With AMG: ms[2]/count[2] the level-0
+ * residual SpMV of the V-cycle, ms[3]/count[3] the level-0 post-smoothing
+ * SpMV.  set_timing resets the accumulators. */
 dfvm_status dfvm_solver_set_timing(dfvm_solver* s, int32_t on);
 dfvm_status dfvm_solver_get_timing(const dfvm_solver* s, double ms[4], int64_t count[4]);
 /* AMG hierarchy (built at the first AMG pressure solve): number of levels and

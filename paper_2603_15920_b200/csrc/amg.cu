@@ -43,14 +43,15 @@ constexpr int kMaxLevels = 16;
 //   DFVM_AMG_COARSE  coarsest-level size bound (rows)           default 256
 //   DFVM_AMG_SWEEPS  l1-Jacobi sweeps of the coarsest solve       default 32
 //   DFVM_AMG_CYCLE   'V' or 'W'                                   default W
-//   DFVM_AMG_WMAX    deepest level visited twice by the W-cycle   default 3
+//   DFVM_AMG_WMAX    deepest level visited twice by the W-cycle   default 4
 //                    (deeper levels use V-cycles: the W launch count
 //                    doubles per level, and deep levels are launch-bound)
-//   DFVM_AMG_OMEGA   coarse-correction scale (symmetric over-correction) default 1
+//   DFVM_AMG_OMEGA   coarse-correction scale (symmetric over-correction,
+//                    < 2 keeps M SPD with adjoint smoothers)   default 1.8
 struct AmgParams {
-  int coarse = 256, sweeps = 32, wmax = 3;
+  int coarse = 256, sweeps = 32, wmax = 4;
   bool wcycle = true;
-  double omega = 1.0;
+  double omega = 1.8;
   AmgParams() {
     if (const char* e = getenv("DFVM_AMG_OMEGA")) omega = atof(e);
     if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kCoarseMax, atoi(e)));
@@ -514,18 +515,23 @@ static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cu
   AmgLevelDev<T>& C = A->L[l + 1];
   // ghost columns exist only on level 0 with several ranks: there the
   // pre-smoothed x (and later t) must be exchanged, so the unfused kernels run
-  const bool ghosts = (l == 0 && A->m->part.P > 1);
+  // Level 0 uses the unfused kernels (measured on B200: the fused versions
+  // re-gather b/d1 (x0/agg/xc) per neighbour and ran 20 % slower per
+  // iteration at 50 M rows); on coarse levels fusion saves launches, which
+  // dominate there.  With several ranks level 0 must be unfused anyway (the
+  // pre-smoothed x and t need a halo exchange).
+  const bool ghosts = (l == 0);
   T* x0 = ghosts ? x : F.t;
   if (ghosts) {
     k_amg_pre<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, b, F.dl1, x, done);
     if ((e = halo_exchange(A->m, x, 1, s))) return e;
+    if (ev) cudaEventRecord(ev[0], s);
     k_amg_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, x, b, F.r, done);
+    if (ev) cudaEventRecord(ev[1], s);
     ++*nl;
   } else {
-    if (l == 0 && ev) cudaEventRecord(ev[0], s);
     k_amg_pre_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b,
                                                            x0, F.r, done);
-    if (l == 0 && ev) cudaEventRecord(ev[1], s);
   }
   k_amg_restrict<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
   *nl += 2;
@@ -542,14 +548,14 @@ static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cu
   if (ghosts) {
     k_amg_prolong<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, x, F.t, (T)A->prm.omega, done);
     if ((e = halo_exchange(A->m, F.t, 1, s))) return e;
+    if (ev) cudaEventRecord(ev[2], s);
     k_amg_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, F.t,
                                                         b, x, done);
+    if (ev) cudaEventRecord(ev[3], s);
     *nl += 2;
   } else {
-    if (l == 0 && ev) cudaEventRecord(ev[2], s);
     k_amg_prolong_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag,
                                                                 F.dl1, F.agg, C.x, (T)A->prm.omega, x0, b, x, done);
-    if (l == 0 && ev) cudaEventRecord(ev[3], s);
     *nl += 1;
   }
   return DFVM_OK;

@@ -14,8 +14,8 @@ template <class T> int amg_levels(const Amg<T>* A, int* sizes);
 // Galerkin values + l1 diagonals for the current pressure matrix (pcoef, pdiag)
 template <class T> dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s, int* n_launch);
 // z = M^-1 r, one cycle; every kernel exits early when *done != 0.  ev (may be
-// NULL): 4 events recorded around the level-0 fused kernels (pre-smooth +
-// residual: ev[0..1], prolongation + post-smooth: ev[2..3]) for live timing.
+// NULL): 4 events recorded around the level-0 residual SpMV (ev[0..1]) and
+// the level-0 post-smoothing SpMV (ev[2..3]) for live timing.
 template <class T> dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t s, int* n_launch,
                                          cudaEvent_t* ev);
 
