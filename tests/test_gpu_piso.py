@@ -222,7 +222,9 @@ def test_htree_windkessel_outlets(precond):
     mo = oracle.Mesh(case.raw)
     mg = dfvm.Mesh(case.raw)
     kw = dict(case.solver, **TIGHT)
-    kw["p_tol"], kw["U_tol"] = 1e-13, 1e-13
+    # parity needs converged solves: the recipe's loose non-final corrector
+    # tolerance (rel 0.05) would compare two different partial iterates
+    kw.update(p_tol=1e-13, U_tol=1e-13, p_rel_tol=0.0, p_rel_tol_final=0.0, U_rel_tol=0.0)
     So = oracle.Solver(mo, case.apply_bcs(oracle.BCs(mo)), **kw)
     Sg = dfvm.Solver(mg, case.apply_bcs(dfvm.BCs(mg)), p_precond=precond, **kw)
     for patch, (Rp, Cc, Rd) in case.windkessel:
