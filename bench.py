@@ -148,7 +148,7 @@ def main():
     ap.add_argument("--config", default="c5", choices=["c5", "c4", "c2", "c1"])
     ap.add_argument("--nz", type=int, default=None, help="override C5 axial layers (814 = 50.0M cells)")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--precond", default="jacobi", choices=["jacobi", "amg"],
+    ap.add_argument("--precond", default="amg", choices=["jacobi", "amg"],
                     help="pressure CG preconditioner (jacobi: A-14; amg: SURVEY NEXT-2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -23,8 +23,10 @@ static double dotv(const std::vector<double>& a, const std::vector<double>& b) {
 // iterations; otherwise stop when ||r||_2 <= max(tol ||b||_2,
 // rel_tol ||r_0||_2), or at maxit.  In parity mode only (tol < 1e-12, a
 // request at round-off level) also on stagnation: no new minimum of ||r||_2
-// for max(50, best_it) iterations.  (||r||_2 of CG is not monotone, so the
-// stagnation test is never applied to throughput-mode solves.)
+// for max(50, best_it) iterations once the best residual is at the round-off
+// plateau, best <= 1e-8 ||r_0||_2 (A-13'').  (||r||_2 of CG is not monotone:
+// it can rise for > 50 iterations early in a solve, so the test is neither
+// applied to throughput-mode solves nor before the residual has dropped.)
 static double threshold(double bnorm, double res0, double tol, double rel_tol) {
   double a = tol * bnorm, b = rel_tol * res0;
   return a > b ? a : b;
@@ -58,7 +60,7 @@ SolveReport cg(const Mesh& m, const LDU& A, const double* b, double* x, double t
     rep.it = it;
     if (rep.res <= thr) { rep.converged = 1; return rep; }
     if (rep.res < best) { best = rep.res; best_it = it; }
-    else if (tol < 1e-12 && it - best_it >= std::max(50, best_it)) break;  // stagnation, parity mode (A-13)
+    else if (tol < 1e-12 && best <= 1e-8 * rep.res0 && it - best_it >= std::max(50, best_it)) break;  // stagnation, parity mode (A-13)
     for (int64_t i = 0; i < N; ++i) z[i] = r[i] / A.diag[i];
     const double rz_new = dotv(r, z);
     const double beta = rz_new / rz;
@@ -113,7 +115,7 @@ SolveReport bicgstab(const Mesh& m, const LDU& A, const double* b, double* x, do
     if (rep.res <= thr) { rep.converged = 1; return rep; }
     if (omega == 0.0) { rep.status = E_BREAKDOWN; return rep; }
     if (rep.res < best) { best = rep.res; best_it = it; }
-    else if (tol < 1e-12 && it - best_it >= std::max(50, best_it)) break;
+    else if (tol < 1e-12 && best <= 1e-8 * rep.res0 && it - best_it >= std::max(50, best_it)) break;
     rho_old = rho;
   }
   rep.status = E_NOT_CONVERGED;

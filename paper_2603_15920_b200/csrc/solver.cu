@@ -39,12 +39,12 @@ struct WKDev {
   int scheme, pad;
 };
 
-// stopping rule (A-13): called by the last block after each residual update
+// stopping rule (A-13, stagnation per A-13''): called by the last block after each residual update
 __device__ __forceinline__ void krylov_check(KCtl& c, double res) {
   c.res = res;
   if (res <= c.thr) { c.converged = 1; c.done = 1; return; }
   if (res < c.best) { c.best = res; c.best_it = c.it; }
-  else if (c.tol < 1e-12 && c.it - c.best_it >= max(50, c.best_it)) { c.done = 1; c.status = DFVM_E_NOT_CONVERGED; return; }
+  else if (c.tol < 1e-12 && c.best <= 1e-8 * c.res0 && c.it - c.best_it >= max(50, c.best_it)) { c.done = 1; c.status = DFVM_E_NOT_CONVERGED; return; }
   if (c.it >= c.maxit) { c.done = 1; c.status = DFVM_E_NOT_CONVERGED; }
 }
 __device__ __forceinline__ void krylov_start(KCtl& c, double bb, double rr) {
