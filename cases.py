@@ -100,4 +100,29 @@ def c4(target_cells=1.0e7, scramble=14):
     return case
 
 
-CONFIGS = {"c1": c1, "c2": c2, "c4": c4, "c5": c5}
+def c3(target_cells=1.0e6, scramble=13):
+    """configs[2]: flow past a cylinder (D = 0.2, Re = 200 with U = 1,
+    nu = 1e-3), 2-D polygon dual of a Delaunay triangulation extruded
+    one layer; free stream U = (1,0,0) on inlet and sides,
+    outlet p = 0, no-slip cylinder; dt = 1e-3, n_corr 2, n_nonorth 1,
+    upwind (A-28); U0 = (1,0,0) + 1% noise (seed 31), p0 = 0."""
+    raw = synth.cylinder_poly(target_cells=target_cells, scramble=scramble)
+    one = dict(value=(1.0, 0.0, 0.0))
+    bcs = [("inlet", "U", FIXED, one), ("sides", "U", FIXED, one), ("cylinder", "U", FIXED, dict(value=(0.0, 0.0, 0.0))),
+           ("outlet", "U", ZEROGRAD, {}), ("inlet", "p", ZEROGRAD, {}), ("sides", "p", ZEROGRAD, {}),
+           ("cylinder", "p", ZEROGRAD, {}), ("outlet", "p", FIXED, dict(value=0.0))]
+    solver = dict(nu=1e-3, dt=1e-3, n_corr=2, n_nonorth=1, convection="upwind", p_ref_cell=0, **THROUGHPUT)
+
+    def ic(xc, xf, Sf):
+        N = len(xc)
+        U = np.zeros((N, 3))
+        U[:, 0] = 1.0
+        U[:, :2] += 0.01 * synth.cell_field(31, N, 2)
+        # free-stream flux, zero on the cylinder wall (face centroids at r <= 0.1)
+        phi = Sf[:, 0] * (np.hypot(xf[:, 0], xf[:, 1]) > 0.1 + 1e-9)
+        return U, np.zeros(N), phi
+    return Case(f"c3_cylinder_poly_{raw.n_cells}", raw, bcs, solver, ic,
+                f"cylinder D=0.2 in [-1,3]x[-1,1], polygon dual, 1 layer, N={raw.n_cells}, Re=200")
+
+
+CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}

@@ -203,11 +203,17 @@ def htree(depth=3, r0=1.0, l0=8.0, h=None, target_cells=1.0e7, tets=True, scramb
 
 
 def extrude_polygons(pts2, polys, dz, patch_names, patch_kinds, rules, empty_patch, scramble=0):
-    """Assemble a one-layer extruded polygon slab (C3 building block)."""
+    """Assemble a one-layer extruded polygon slab (C3 building block).
+    polys: list of CCW vertex-id lists, or a pair (offsets[n+1], ids)."""
     pts2 = np.ascontiguousarray(pts2, np.float64)
-    off = np.zeros(len(polys) + 1, np.int64)
-    off[1:] = np.cumsum([len(p) for p in polys])
-    ids = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in polys]), np.int32)
+    if isinstance(polys, tuple):
+        off = np.ascontiguousarray(polys[0], np.int64)
+        ids = np.ascontiguousarray(polys[1], np.int32)
+        polys = range(len(off) - 1)
+    else:
+        off = np.zeros(len(polys) + 1, np.int64)
+        off[1:] = np.cumsum([len(p) for p in polys])
+        ids = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in polys]), np.int32)
     names = (C.c_char_p * len(patch_names))(*[s.encode() for s in patch_names])
     kinds = np.asarray(patch_kinds, np.int32)
     R = np.ascontiguousarray(rules, np.float64)
@@ -348,4 +354,106 @@ def square_tri(n=20, jitter=0.25, seed=7, scramble=5, y_step=0.5):
     m = extrude_polygons(pts, polys, h, ["inlet_lower", "inlet_upper", "outlet", "frontAndBack"],
                          [PATCH_GENERIC, PATCH_GENERIC, PATCH_GENERIC, PATCH_EMPTY], rules, 3, scramble)
     m.meta = dict(kind="square_tri", n=n, dz=h, y_step=y_step)
+    return m
+
+
+def cylinder_poly(target_cells=1.0e6, seed=3, scramble=13, jitter=0.25, dz=0.01):
+    """C3: flow past a cylinder, 2-D channel
+    [-1, 3] x [-1, 1] around a cylinder of diameter 0.2 at the origin.
+    Points: staggered polar rings r in [0.1, 0.6) (geometric, near-square
+    spacing, jittered except the cylinder ring's radius) and a jittered
+    lattice outside; Delaunay; triangles inside the cylinder dropped; the
+    POLYGON DUAL (one cell per primal vertex, dual vertices at triangle
+    circumcentres, or at the centroid where the circumcentre is not well
+    inside its triangle; boundary cells closed through the boundary-edge
+    midpoints and the vertex itself) extruded one layer (dz, empty
+    front/back).  N = number of primal vertices; F/N ~ 3.
+    Patches: inlet (x=-1), outlet (x=3), sides (y=+-1), cylinder (wall),
+    frontAndBack (empty)."""
+    from scipy.spatial import Delaunay
+    x0, x1, y0, y1, rc, rr = -1.0, 3.0, -1.0, 1.0, 0.1, 0.6
+    h = np.sqrt(((x1 - x0) * (y1 - y0) - np.pi * rr * rr + 2 * np.pi * rr * rr * np.log(rr / rc)) / target_cells)
+    nth = int(round(2 * np.pi * rr / h))
+    q = 1.0 + 2 * np.pi / nth
+    nring = int(np.floor(np.log(rr / rc) / np.log(q))) + 1
+    k, j = np.meshgrid(np.arange(nring), np.arange(nth), indexing="ij")
+    k, j = k.ravel(), j.ravel()
+    rid = np.arange(len(k), dtype=np.uint64)
+    dth = 2 * np.pi / nth
+    th = (j + 0.5 * (k % 2)) * dth + 0.1 * dth * urand(seed, 3 * rid)
+    r = rc * q ** k * np.where(k > 0, 1.0 + 0.1 * (q - 1.0) * urand(seed, 3 * rid + np.uint64(1)), 1.0)
+    ring = np.stack([r * np.cos(th), r * np.sin(th)], 1)
+    nx, ny = int(round((x1 - x0) / h)), int(round((y1 - y0) / h))
+    I, J = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), indexing="ij")
+    I, J = I.ravel(), J.ravel()
+    lat = np.stack([x0 + I * (x1 - x0) / nx, y0 + J * (y1 - y0) / ny], 1)
+    inner = (I > 0) & (I < nx) & (J > 0) & (J < ny)
+    lid = np.arange(len(I), dtype=np.uint64) + np.uint64(1 << 40)
+    lat[inner, 0] += jitter * h * urand(seed, 2 * lid[inner])
+    lat[inner, 1] += jitter * h * urand(seed, 2 * lid[inner] + np.uint64(1))
+    lat = lat[np.hypot(lat[:, 0], lat[:, 1]) > rr + 0.5 * h]
+    pts = np.concatenate([ring, lat])
+    nv = len(pts)
+    tri = Delaunay(pts).simplices.astype(np.int64)
+    A, B, Cc = pts[tri[:, 0]], pts[tri[:, 1]], pts[tri[:, 2]]
+    cross = (B[:, 0] - A[:, 0]) * (Cc[:, 1] - A[:, 1]) - (B[:, 1] - A[:, 1]) * (Cc[:, 0] - A[:, 0])
+    flip = cross < 0
+    tri[flip, 1], tri[flip, 2] = tri[flip, 2].copy(), tri[flip, 1].copy()
+    A, B, Cc = pts[tri[:, 0]], pts[tri[:, 1]], pts[tri[:, 2]]
+    cen = (A + B + Cc) / 3.0
+    keep = np.hypot(cen[:, 0], cen[:, 1]) > rc
+    tri, A, B, Cc, cen = tri[keep], A[keep], B[keep], Cc[keep], cen[keep]
+    nt = len(tri)
+    # circumcentre and its barycentric coordinates
+    bx, by, cx, cy = B[:, 0] - A[:, 0], B[:, 1] - A[:, 1], Cc[:, 0] - A[:, 0], Cc[:, 1] - A[:, 1]
+    d = 2.0 * (bx * cy - by * cx)
+    ux = (cy * (bx * bx + by * by) - by * (cx * cx + cy * cy)) / d
+    uy = (bx * (cx * cx + cy * cy) - cx * (bx * bx + by * by)) / d
+    l1 = (ux * cy - uy * cx) / (bx * cy - by * cx)
+    l2 = (bx * uy - by * ux) / (bx * cy - by * cx)
+    inside = (l1 > 0.02) & (l2 > 0.02) & (1.0 - l1 - l2 > 0.02)
+    dual_t = np.where(inside[:, None], A + np.stack([ux, uy], 1), cen)
+    # boundary edges (edges of one kept triangle), oriented as in the CCW triangle
+    e = np.concatenate([tri[:, [0, 1]], tri[:, [1, 2]], tri[:, [2, 0]]])
+    key = np.minimum(e[:, 0], e[:, 1]) * nv + np.maximum(e[:, 0], e[:, 1])
+    uk, cnt = np.unique(key, return_counts=True)
+    be = e[np.isin(key, uk[cnt == 1])]
+    nb = len(be)
+    mid = 0.5 * (pts[be[:, 0]] + pts[be[:, 1]])
+    bv = np.unique(be.ravel())
+    isb = np.zeros(nv, bool); isb[bv] = True
+    vpid = np.full(nv, -1, np.int64); vpid[bv] = nt + nb + np.arange(len(bv))
+    dual = np.concatenate([dual_t, mid, pts[bv]])
+    # items around each primal vertex: (vertex, angle, dual point, is-midpoint)
+    iv = np.concatenate([tri.T.ravel(), be[:, 0], be[:, 1]])
+    ip = np.concatenate([np.tile(np.arange(nt), 3), nt + np.arange(nb), nt + np.arange(nb)])
+    im = np.concatenate([np.zeros(3 * nt, bool), np.ones(2 * nb, bool)])
+    vec = dual[ip] - pts[iv]
+    ang = np.arctan2(vec[:, 1], vec[:, 0])
+    o = np.lexsort((ang, iv))
+    iv, ip, im = iv[o], ip[o], im[o]
+    cntv = np.bincount(iv, minlength=nv)
+    in_off = np.zeros(nv + 1, np.int64); in_off[1:] = np.cumsum(cntv)
+    out_len = cntv + isb
+    out_off = np.zeros(nv + 1, np.int64); out_off[1:] = np.cumsum(out_len)
+    ids = np.empty(out_off[-1], np.int64)
+    pos = np.arange(len(iv)) - in_off[iv]
+    inter = ~isb[iv]
+    ids[out_off[iv[inter]] + pos[inter]] = ip[inter]
+    for v in bv:
+        a, b = in_off[v], in_off[v + 1]
+        seg_p, seg_m = ip[a:b], im[a:b]
+        n = b - a
+        gaps = [i for i in range(n) if seg_m[i] and seg_m[(i + 1) % n]]
+        if len(gaps) != 1:
+            raise ValueError(f"cylinder_poly: boundary vertex {v} has {len(gaps)} exterior gaps")
+        i = gaps[0]
+        rot = np.concatenate([seg_p[i + 1:], seg_p[:i + 1]])
+        ids[out_off[v]:out_off[v + 1]] = np.concatenate([rot, [vpid[v]]])
+    eps = 1e-9
+    rules = [(-0.2, 0.2, -0.2, 0.2, 3), (x0 - 1, x0 + eps, y0 - 1, y1 + 1, 0), (x1 - eps, x1 + 1, y0 - 1, y1 + 1, 1),
+             (x0 - 1, x1 + 1, y0 - 1, y0 + eps, 2), (x0 - 1, x1 + 1, y1 - eps, y1 + 1, 2)]
+    m = extrude_polygons(dual, (out_off, ids), dz, ["inlet", "outlet", "sides", "cylinder", "frontAndBack"],
+                         [PATCH_GENERIC, PATCH_GENERIC, PATCH_GENERIC, PATCH_WALL, PATCH_EMPTY], rules, 4, scramble)
+    m.meta = dict(kind="cylinder_poly", h=h, dz=dz, n_theta=nth, n_ring=nring)
     return m

@@ -38,6 +38,9 @@ MESHES = {
     "kuhn8": lambda: synth.box(8, 8, 8, split=6, scramble=3),
     "pipe_tet": lambda: synth.pipe(6, 3, 20, 0.5, 2.0, tets=True, scramble=12),
     "pipe_hex": lambda: synth.pipe(8, 4, 10, 0.5, 1.0, tets=False, scramble=5),
+    "cylinder_poly": lambda: synth.cylinder_poly(6e3, scramble=13),     # C3 family: polygon prisms, F/N ~ 3
+    "square_tri": lambda: synth.square_tri(12, jitter=0.2),             # NEXT-1 domain: triangle prisms
+    "htree_tet": lambda: synth.htree(target_cells=2e4, scramble=14),    # C4 family: voxel tree, 5-tet
 }
 
 
