@@ -148,7 +148,7 @@ def main():
     ap.add_argument("--config", default="c5", choices=["c5", "c4", "c2", "c1"])
     ap.add_argument("--nz", type=int, default=None, help="override C5 axial layers (814 = 50.0M cells)")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--precond", default="amg", choices=["jacobi", "amg"],
+    ap.add_argument("--precond", default="amg", choices=["jacobi", "amg", "amg32"],
                     help="pressure CG preconditioner (jacobi: A-14; amg: SURVEY NEXT-2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -278,14 +278,17 @@ def main():
     hbm, peak_src = peaks()
     n_own, F_l = info["n_owned"], info["n_local_internal_faces"]
     vb, ib = (8, 4) if args.precision == "f64" else (4, 4)
-    lv = S.amg_levels() if args.precond == "amg" else []
+    lv = S.amg_levels() if args.precond != "jacobi" else []
+    pb = 4 if args.precond == "amg32" else vb       # AMG hierarchy element bytes
     cands = {
         "k_cg_spmv (PCG SpMV + p.q partials)":
             (tim["spmv_ms"], tim["spmv_n"], 4 * n_own + 2 * F_l * (ib + vb) + 3 * vb * n_own),          # diag, p, q
         "k_amg_resid (AMG level-0 residual: r = b - A x)":
-            (tim["amg_pre_ms"], tim["amg_pre_n"], 4 * n_own + 2 * F_l * (ib + vb) + 4 * vb * n_own),    # x, diag, b, r
+            (tim["amg_pre_ms"], tim["amg_pre_n"],
+             4 * n_own + 2 * F_l * (ib + pb) + (3 * pb + vb) * n_own),                                # x, diag, r; b
         "k_amg_smooth (AMG level-0 post-smoother: z = t + (b - A t)/d1)":
-            (tim["amg_post_ms"], tim["amg_post_n"], 4 * n_own + 2 * F_l * (ib + vb) + 5 * vb * n_own),  # t, diag, d1, b, z
+            (tim["amg_post_ms"], tim["amg_post_n"],
+             4 * n_own + 2 * F_l * (ib + pb) + (3 * pb + 2 * vb) * n_own),                            # t, diag, d1; b, z
     }
     kname, (kms, kn, alg) = max(cands.items(), key=lambda kv: kv[1][0])
     launch_ms = kms / max(kn, 1)

@@ -247,12 +247,16 @@ typedef struct {
   double p_tol, p_rel_tol, p_rel_tol_final; int32_t p_maxit;  /* A-13 stopping rule */
   double U_tol, U_rel_tol; int32_t U_maxit;
   int32_t p_precond;            /* pressure CG preconditioner: 0 Jacobi (A-14), 1 aggregation-AMG
-                                   V(1,1) cycle (amg.cu) */
+                                   cycle in the solver's precision (amg.cu),
+                                   2 the same AMG with its hierarchy stored and cycled in fp32 under
+                                   an fp64 PCG (residual, dots and iterates stay fp64; = 1 for fp32
+                                   solvers).  Out of range -> DFVM_E_ARG. */
 } dfvm_piso_opts;
 
 /* Krylov stopping rule (A-13): b = 0 -> x = 0, 0 iterations; else
- * stop when ||r||_2 <= max(tol ||b||_2, rel_tol ||r_0||_2), on stagnation
- * (no new minimum for 50 iterations) or at maxit. */
+ * stop when ||r||_2 <= max(tol ||b||_2, rel_tol ||r_0||_2), or at maxit; for
+ * tol < 1e-12 also on stagnation at the round-off plateau (no new minimum for
+ * max(50, best_it) iterations once the best residual is <= 1e-8 ||r_0||, A-13''). */
 typedef struct { int32_t it; double res0, res; int32_t converged; } dfvm_solve_report;
 typedef struct {
   dfvm_solve_report U[3];

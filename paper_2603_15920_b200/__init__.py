@@ -412,7 +412,7 @@ class Solver:
         o = PisoOpts(nu, dt, rho, n_corr, n_nonorth, {"upwind": 0, "central": 1, "sou": 2, "quick": 3}[convection],
                      p_ref_cell,
                      p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, p_maxit, U_tol, U_rel_tol, U_maxit,
-                     {"jacobi": 0, "amg": 1}[p_precond])
+                     {"jacobi": 0, "amg": 1, "amg32": 2}[p_precond])
         h = C.c_void_p()
         _check(lib().dfvm_solver_create(mesh.h, bcs.h, C.byref(o), C.byref(h)))
         self.h = h.value

@@ -22,10 +22,15 @@
 //    one block (shared memory).  Pre/post smoothers are adjoint and the
 //    coarse solve is a fixed symmetric polynomial, so M^-1 is SPD and CG
 //    stays CG.  The converged pressure is preconditioner independent (A-14).
+//  * precision: the hierarchy's type P is the solver's T ("amg"), or fp32
+//    under an fp64 solver ("amg32": matrix copies, smoother and every level
+//    vector in fp32; the PCG itself — residual, dots, x, p — stays fp64).
+//    Level 0 reads the PCG residual in T and writes z = M^-1 r in T.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "amg.h"
@@ -33,7 +38,7 @@
 
 namespace dfvm {
 
-dfvm_status halo_exchange(dfvm_mesh* m, void* data, int nc, cudaStream_t s);
+dfvm_status halo_exchange_p(dfvm_mesh* m, void* data, int nc, bool f64, cudaStream_t s);
 
 constexpr int kCoarseMax = 2048;     // shared-memory capacity of the one-block coarse solve
 constexpr int kMaxLevels = 16;
@@ -127,34 +132,35 @@ std::vector<int> aggregate(const HostLevel& L, int& nagg) {
 
 }  // namespace
 
-template <class T>
+template <class P>
 struct AmgLevelDev {
   int n = 0, n_slices = 0;
   int64_t n_sell = 0;
   const int *ms_ptr = nullptr, *ms_len = nullptr, *mnb = nullptr;
-  const T* coef = nullptr;   // level 0: the solver's pcoef
-  const T* diag = nullptr;   // level 0: the solver's pdiag
-  T* coef_own = nullptr;
-  T* diag_own = nullptr;
-  T* dl1 = nullptr;
+  const P* coef = nullptr;   // level 0: the solver's pcoef (P == T) or coef_own (fp32 copy)
+  const P* diag = nullptr;   // level 0: the solver's pdiag (P == T) or diag_own
+  P* coef_own = nullptr;
+  P* diag_own = nullptr;
+  P* dl1 = nullptr;
   // Galerkin maps of this (coarse) level from the finer level
   int *gal_ptr = nullptr, *gal_idx = nullptr;     // per coarse SELL position
   int *dg_ptr = nullptr, *dg_idx = nullptr;       // per coarse row: internal fine positions
   int *mem_ptr = nullptr, *mem = nullptr;         // per coarse row: fine member rows
   int* agg = nullptr;                             // on the FINE level: fine row -> coarse row
-  T *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr;
-  T *e = nullptr, *r2 = nullptr;                  // W-cycle: second-visit solution / rhs
+  P *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr;
+  P *e = nullptr, *r2 = nullptr;                  // W-cycle: second-visit solution / rhs
 };
 
-template <class T>
-struct Amg {
+// hierarchy stored and cycled in type P
+template <class P>
+struct AmgH {
   dfvm_mesh* m = nullptr;
   int nlev = 0;
   AmgParams prm;
-  AmgLevelDev<T> L[kMaxLevels];
+  AmgLevelDev<P> L[kMaxLevels];
   std::vector<void*> allocs;
   int64_t bytes = 0;
-  ~Amg() { for (void* p : allocs) cudaFree(p); }
+  ~AmgH() { for (void* p : allocs) cudaFree(p); }
   template <class U>
   dfvm_status up(U** d, const std::vector<U>& h) {
     void* q = nullptr;
@@ -179,21 +185,33 @@ struct Amg {
   }
 };
 
+// the solver-facing handle: exactly one of the two hierarchies is built
 template <class T>
-dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, Amg<T>** out) {
-  Amg<T>* A = new Amg<T>();
+struct Amg {
+  AmgH<T>* same = nullptr;       // "amg": hierarchy in the solver's precision
+  AmgH<float>* lo = nullptr;     // "amg32": fp32 hierarchy under an fp64 solver
+  ~Amg() { delete same; delete lo; }
+};
+
+template <class P, class T>
+static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
   A->m = m;
   std::vector<HostLevel> H(1);
   H[0].n = M.n_own;
   H[0].ms_ptr = m->h_ms_ptr; H[0].ms_len = m->h_ms_len; H[0].mnb = m->h_mnb;
   sell_to_csr(H[0], M.n_own);
   // device view of level 0 (the mesh's matrix layout; coef / diag bound per update)
-  AmgLevelDev<T>& L0 = A->L[0];
+  AmgLevelDev<P>& L0 = A->L[0];
   L0.n = M.n_own; L0.n_slices = M.n_slices; L0.n_sell = M.n_minc;
   L0.ms_ptr = M.ms_ptr; L0.ms_len = M.ms_len; L0.mnb = M.mnb;
   dfvm_status st;
   if ((st = A->zalloc(&L0.dl1, M.n_own)) || (st = A->zalloc(&L0.x, M.n_cells)) || (st = A->zalloc(&L0.r, M.n_own)) ||
-      (st = A->zalloc(&L0.t, M.n_cells))) { delete A; return st; }
+      (st = A->zalloc(&L0.t, M.n_cells)))
+    return st;
+  if (!std::is_same<P, T>::value) {
+    if ((st = A->zalloc(&L0.coef_own, (size_t)M.n_minc)) || (st = A->zalloc(&L0.diag_own, M.n_own))) return st;
+    L0.coef = L0.coef_own; L0.diag = L0.diag_own;
+  }
   int lev = 0;
   while (H[lev].n > A->prm.coarse && lev + 1 < kMaxLevels) {
     const HostLevel& F = H[lev];
@@ -265,7 +283,7 @@ dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, Amg<T>** out) {
     }
     sell_to_csr(C, nc);
     // upload
-    AmgLevelDev<T>& D = A->L[lev + 1];
+    AmgLevelDev<P>& D = A->L[lev + 1];
     D.n = nc; D.n_slices = S; D.n_sell = C.ms_ptr[S];
     int *p0, *p1, *p2;
     if ((st = A->up(&p0, C.ms_ptr)) || (st = A->up(&p1, C.ms_len)) || (st = A->up(&p2, C.mnb)) ||
@@ -274,16 +292,29 @@ dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, Amg<T>** out) {
         (st = A->up(&A->L[lev].agg, agg)) || (st = A->zalloc(&D.coef_own, (size_t)D.n_sell)) ||
         (st = A->zalloc(&D.diag_own, nc)) || (st = A->zalloc(&D.dl1, nc)) || (st = A->zalloc(&D.x, nc)) ||
         (st = A->zalloc(&D.b, nc)) || (st = A->zalloc(&D.r, nc)) || (st = A->zalloc(&D.t, nc)) ||
-        (st = A->zalloc(&D.e, nc)) || (st = A->zalloc(&D.r2, nc))) {
-      delete A;
+        (st = A->zalloc(&D.e, nc)) || (st = A->zalloc(&D.r2, nc)))
       return st;
-    }
     D.ms_ptr = p0; D.ms_len = p1; D.mnb = p2;
     D.coef = D.coef_own; D.diag = D.diag_own;
     H.push_back(std::move(C));
     ++lev;
   }
   A->nlev = lev + 1;
+  return DFVM_OK;
+}
+
+template <class T>
+dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** out) {
+  Amg<T>* A = new Amg<T>();
+  dfvm_status st;
+  if (fp32 && !std::is_same<T, float>::value) {
+    A->lo = new AmgH<float>();
+    st = build<float, T>(m, M, A->lo);
+  } else {
+    A->same = new AmgH<T>();
+    st = build<T, T>(m, M, A->same);
+  }
+  if (st) { delete A; return st; }
   *out = A;
   return DFVM_OK;
 }
@@ -291,13 +322,21 @@ dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, Amg<T>** out) {
 template <class T>
 void amg_destroy(Amg<T>* A) { delete A; }
 
-template <class T>
-int amg_levels(const Amg<T>* A, int* sizes) {
+template <class P>
+static int levels(const AmgH<P>* A, int* sizes) {
   for (int l = 0; l < A->nlev; ++l) sizes[l] = A->L[l].n;
   return A->nlev;
 }
+template <class T>
+int amg_levels(const Amg<T>* A, int* sizes) { return A->same ? levels(A->same, sizes) : levels(A->lo, sizes); }
 
 // ------------------------------------------------------------ kernels
+template <class P, class T>
+__global__ void k_amg_cvt(int64_t n, const T* __restrict__ a, P* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (P)a[i];
+}
+
 template <class T>
 __global__ void k_gal_off(int64_t n_sell, const int* __restrict__ gp, const int* __restrict__ gi,
                           const T* __restrict__ fcoef, T* __restrict__ ccoef) {
@@ -355,21 +394,22 @@ __device__ __forceinline__ T row_apply(int r, const int* __restrict__ ms_ptr, co
   return acc;
 }
 
-// x = b / d1 (pre-smoothing from a zero guess)
-template <class T>
-__global__ void k_amg_pre(int n, const T* __restrict__ b, const T* __restrict__ dl1, T* __restrict__ x,
+// x = b / d1 (pre-smoothing from a zero guess); b in the caller's type TB
+template <class P, class TB, class TX>
+__global__ void k_amg_pre(int n, const TB* __restrict__ b, const P* __restrict__ dl1, TX* __restrict__ x,
                           const int* done) {
   if (*done) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = b[i] / dl1[i];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = (TX)((P)b[i] / dl1[i]);
 }
 // r = b - A x
-template <class T>
+template <class P, class TB>
 __global__ void k_amg_resid(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                            const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
-                            const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ r, const int* done) {
+                            const int* __restrict__ mnb, const P* __restrict__ coef, const P* __restrict__ diag,
+                            const P* __restrict__ x, const TB* __restrict__ b, P* __restrict__ r, const int* done) {
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    r[i] = b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x);
+    r[i] = (P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x);
 }
 // b_c[I] = sum over the aggregate's members of r_f
 template <class T>
@@ -440,138 +480,160 @@ __global__ void k_amg_add(int n, const T* __restrict__ e, T* __restrict__ x, con
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] += e[i];
 }
-// out = x + (b - A x) / d1
-template <class T>
+// out = x + (b - A x) / d1   (b in TB, out in TO: level 0 reads / writes the PCG's type)
+template <class P, class TB, class TO>
 __global__ void k_amg_smooth(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                             const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
-                             const T* __restrict__ dl1, const T* __restrict__ x, const T* __restrict__ b,
-                             T* __restrict__ out, const int* done) {
+                             const int* __restrict__ mnb, const P* __restrict__ coef, const P* __restrict__ diag,
+                             const P* __restrict__ dl1, const P* __restrict__ x, const TB* __restrict__ b,
+                             TO* __restrict__ out, const int* done) {
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    out[i] = x[i] + (b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x)) / dl1[i];
+    out[i] = (TO)(x[i] + ((P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x)) / dl1[i]);
 }
 // coarsest level: `sweeps` l1-Jacobi sweeps from zero, one block, in shared memory
-template <class T>
+template <class P, class TB, class TO>
 __global__ void __launch_bounds__(1024) k_amg_coarse(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                                                    const int* __restrict__ mnb, const T* __restrict__ coef,
-                                                    const T* __restrict__ diag, const T* __restrict__ dl1,
-                                                    const T* __restrict__ b, T* __restrict__ xout, int sweeps,
+                                                    const int* __restrict__ mnb, const P* __restrict__ coef,
+                                                    const P* __restrict__ diag, const P* __restrict__ dl1,
+                                                    const TB* __restrict__ b, TO* __restrict__ xout, int sweeps,
                                                     const int* done) {
   if (*done) return;
-  __shared__ T xs[2][kCoarseMax];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) xs[0][i] = b[i] / dl1[i];
+  __shared__ P xs[2][kCoarseMax];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xs[0][i] = (P)b[i] / dl1[i];
   __syncthreads();
   int cur = 0;
   for (int it = 1; it < sweeps; ++it) {
     for (int i = threadIdx.x; i < n; i += blockDim.x)
-      xs[cur ^ 1][i] = xs[cur][i] + (b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, xs[cur])) / dl1[i];
+      xs[cur ^ 1][i] = xs[cur][i] + ((P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, xs[cur])) / dl1[i];
     __syncthreads();
     cur ^= 1;
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = xs[cur][i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = (TO)xs[cur][i];
 }
 
 // ------------------------------------------------------------ host drivers
-template <class T>
-dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s, int* nl) {
-  AmgLevelDev<T>& L0 = A->L[0];
-  L0.coef = pcoef; L0.diag = pdiag;
-  k_dl1<T><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, L0.ms_ptr, L0.ms_len, L0.coef, L0.diag, L0.dl1);
+template <class P, class T>
+static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream_t s, int* nl) {
+  AmgLevelDev<P>& L0 = A->L[0];
+  if (std::is_same<P, T>::value) {
+    L0.coef = (const P*)pcoef; L0.diag = (const P*)pdiag;
+  } else {
+    k_amg_cvt<P, T><<<grid_for(L0.n_sell), kThreads, 0, s>>>(L0.n_sell, pcoef, L0.coef_own);
+    k_amg_cvt<P, T><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, pdiag, L0.diag_own);
+    *nl += 2;
+  }
+  k_dl1<P><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, L0.ms_ptr, L0.ms_len, L0.coef, L0.diag, L0.dl1);
   ++*nl;
   for (int l = 1; l < A->nlev; ++l) {
-    AmgLevelDev<T>& F = A->L[l - 1];
-    AmgLevelDev<T>& C = A->L[l];
-    k_gal_off<T><<<grid_for(C.n_sell), kThreads, 0, s>>>(C.n_sell, C.gal_ptr, C.gal_idx, F.coef, C.coef_own);
-    k_gal_diag<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, C.dg_ptr, C.dg_idx, F.diag, F.coef,
+    AmgLevelDev<P>& F = A->L[l - 1];
+    AmgLevelDev<P>& C = A->L[l];
+    k_gal_off<P><<<grid_for(C.n_sell), kThreads, 0, s>>>(C.n_sell, C.gal_ptr, C.gal_idx, F.coef, C.coef_own);
+    k_gal_diag<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, C.dg_ptr, C.dg_idx, F.diag, F.coef,
                                                       C.diag_own);
-    k_dl1<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.coef, C.diag, C.dl1);
+    k_dl1<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.coef, C.diag, C.dl1);
     *nl += 3;
   }
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
 }
 
-// x = M_l^-1 b from a zero guess: pre-smooth, residual, restriction, coarse
-// correction (twice on coarse levels for the W-cycle: the second visit
-// solves for the residual of the first), prolongation, post-smooth.  Each
-// level's operator is symmetric (adjoint pre/post Jacobi, symmetric coarse
-// polynomial, and two successive symmetric corrections 2B - BAB), so the
-// preconditioner stays SPD.  Level 0 exchanges ghosts before its SpMVs.
 template <class T>
-static dfvm_status cycle(Amg<T>* A, int l, const T* b, T* x, const int* done, cudaStream_t s, int* nl,
-                         cudaEvent_t* ev) {
-  AmgLevelDev<T>& F = A->L[l];
-  dfvm_status e;
+dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s, int* nl) {
+  return A->same ? update<T, T>(A->same, pcoef, pdiag, s, nl) : update<float, T>(A->lo, pcoef, pdiag, s, nl);
+}
+
+// Coarse level l >= 1 (no ghost columns): x = M_l^-1 b from a zero guess with
+// the fused kernels (launches dominate there): pre-smooth + residual,
+// restriction, coarse correction (twice for the W-cycle: the second visit
+// solves for the residual of the first), prolongation + post-smooth.  Each
+// level's operator is symmetric (adjoint pre/post Jacobi, symmetric coarse
+// polynomial, two successive symmetric corrections 2B - BAB), so the
+// preconditioner stays SPD.
+template <class P>
+static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl) {
+  AmgLevelDev<P>& F = A->L[l];
   if (l == A->nlev - 1) {
-    if (l == 0 && A->m->part.P > 1) {   // single level with ghost columns: one l1-Jacobi step
-      k_amg_pre<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, b, F.dl1, x, done);
+    k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b, x,
+                                             A->prm.sweeps, done);
+    ++*nl;
+    return;
+  }
+  AmgLevelDev<P>& C = A->L[l + 1];
+  k_amg_pre_resid<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b,
+                                                         F.t, F.r, done);
+  k_amg_restrict<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
+  *nl += 2;
+  cycle_coarse(A, l + 1, C.b, C.x, done, s, nl);
+  if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax) {
+    k_amg_resid<P, P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b,
+                                                         C.r2, done);
+    cycle_coarse(A, l + 1, C.r2, C.e, done, s, nl);
+    k_amg_add<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done);
+    *nl += 2;
+  }
+  k_amg_prolong_smooth<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag,
+                                                              F.dl1, F.agg, C.x, (P)A->prm.omega, F.t, b, x, done);
+  ++*nl;
+}
+
+// Level 0: reads the PCG residual r (type T), writes z (type T); its own
+// vectors are in P and carry ghost slices (exchanged before each SpMV).
+// Level 0 uses the unfused kernels (measured on B200: the fused versions
+// re-gather b/d1 (x0/agg/xc) per neighbour and ran 20 % slower per iteration
+// at 50 M rows), and must with several ranks (x0 and t need a halo exchange).
+template <class P, class T>
+static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl, cudaEvent_t* ev) {
+  AmgLevelDev<P>& F = A->L[0];
+  const bool f64 = std::is_same<P, double>::value;
+  dfvm_status e;
+  if (A->nlev == 1) {
+    if (A->m->part.P > 1) {   // single level with ghost columns: one l1-Jacobi step
+      k_amg_pre<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.dl1, z, done);
     } else {
-      k_amg_coarse<T><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b, x,
-                                         A->prm.sweeps, done);
+      k_amg_coarse<P, T, T><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, r, z,
+                                               A->prm.sweeps, done);
     }
     ++*nl;
     return DFVM_OK;
   }
-  AmgLevelDev<T>& C = A->L[l + 1];
-  // ghost columns exist only on level 0 with several ranks: there the
-  // pre-smoothed x (and later t) must be exchanged, so the unfused kernels run
-  // Level 0 uses the unfused kernels (measured on B200: the fused versions
-  // re-gather b/d1 (x0/agg/xc) per neighbour and ran 20 % slower per
-  // iteration at 50 M rows); on coarse levels fusion saves launches, which
-  // dominate there.  With several ranks level 0 must be unfused anyway (the
-  // pre-smoothed x and t need a halo exchange).
-  const bool ghosts = (l == 0);
-  T* x0 = ghosts ? x : F.t;
-  if (ghosts) {
-    k_amg_pre<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, b, F.dl1, x, done);
-    if ((e = halo_exchange(A->m, x, 1, s))) return e;
-    if (ev) cudaEventRecord(ev[0], s);
-    k_amg_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, x, b, F.r, done);
-    if (ev) cudaEventRecord(ev[1], s);
-    ++*nl;
-  } else {
-    k_amg_pre_resid<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b,
-                                                           x0, F.r, done);
-  }
-  k_amg_restrict<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
-  *nl += 2;
-  if ((e = cycle(A, l + 1, C.b, C.x, done, s, nl, nullptr))) return e;
-  if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax) {
-    // second visit: C.x += M^-1 (C.b - A C.x)
-    k_amg_resid<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b,
-                                                       C.r2, done);
-    ++*nl;
-    if ((e = cycle(A, l + 1, C.r2, C.e, done, s, nl, nullptr))) return e;
-    k_amg_add<T><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done);
-    ++*nl;
-  }
-  if (ghosts) {
-    k_amg_prolong<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, x, F.t, (T)A->prm.omega, done);
-    if ((e = halo_exchange(A->m, F.t, 1, s))) return e;
-    if (ev) cudaEventRecord(ev[2], s);
-    k_amg_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, F.t,
-                                                        b, x, done);
-    if (ev) cudaEventRecord(ev[3], s);
+  AmgLevelDev<P>& C = A->L[1];
+  k_amg_pre<P, T, P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.dl1, F.x, done);
+  if ((e = halo_exchange_p(A->m, F.x, 1, f64, s))) return e;
+  if (ev) cudaEventRecord(ev[0], s);
+  k_amg_resid<P, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.x, r, F.r,
+                                                       done);
+  if (ev) cudaEventRecord(ev[1], s);
+  k_amg_restrict<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
+  *nl += 3;
+  cycle_coarse(A, 1, C.b, C.x, done, s, nl);
+  if (A->prm.wcycle && 1 < A->nlev - 1 && 1 <= A->prm.wmax) {
+    k_amg_resid<P, P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b,
+                                                         C.r2, done);
+    cycle_coarse(A, 1, C.r2, C.e, done, s, nl);
+    k_amg_add<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done);
     *nl += 2;
-  } else {
-    k_amg_prolong_smooth<T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag,
-                                                                F.dl1, F.agg, C.x, (T)A->prm.omega, x0, b, x, done);
-    *nl += 1;
   }
+  k_amg_prolong<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, F.x, F.t, (P)A->prm.omega, done);
+  if ((e = halo_exchange_p(A->m, F.t, 1, f64, s))) return e;
+  if (ev) cudaEventRecord(ev[2], s);
+  k_amg_smooth<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1,
+                                                           F.t, r, z, done);
+  if (ev) cudaEventRecord(ev[3], s);
+  *nl += 2;
   return DFVM_OK;
 }
 
 // z = M^-1 r; skipped on the device when *done is set
 template <class T>
 dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl, cudaEvent_t* ev) {
-  dfvm_status e = cycle(A, 0, r, z, done, s, nl, ev);
+  dfvm_status e = A->same ? cycle0<T, T>(A->same, r, z, done, s, nl, ev) : cycle0<float, T>(A->lo, r, z, done, s, nl, ev);
   if (e) return e;
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
 }
 
 #define INST(T)                                                                           \
-  template dfvm_status amg_create<T>(dfvm_mesh*, const DevMesh<T>&, Amg<T>**);            \
+  template dfvm_status amg_create<T>(dfvm_mesh*, const DevMesh<T>&, bool, Amg<T>**);      \
   template void amg_destroy<T>(Amg<T>*);                                                  \
   template int amg_levels<T>(const Amg<T>*, int*);                                        \
   template dfvm_status amg_update<T>(Amg<T>*, const T*, const T*, cudaStream_t, int*);    \

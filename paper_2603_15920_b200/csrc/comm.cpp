@@ -105,6 +105,8 @@ static dfvm_status nccl_error(ncclResult_t r, const char* where) {
     if (r_ != ncclSuccess) return nccl_error(r_, #call);         \
   } while (0)
 
+dfvm_status halo_exchange_p(dfvm_mesh* m, void* data, int nc, bool f64, cudaStream_t s);
+
 static dfvm_status ensure_halo_buffers(dfvm_mesh* m) {
   const Part& P = m->part;
   if (m->d_send_idx || P.send_gid.empty()) return DFVM_OK;
@@ -130,11 +132,16 @@ static dfvm_status local_finish(LocalGroup* G, int rank, cudaStream_t s) {
 }
 
 dfvm_status halo_exchange(dfvm_mesh* m, void* data, int nc, cudaStream_t s) {
+  return halo_exchange_p(m, data, nc, m->precision == DFVM_F64, s);
+}
+
+// element type given explicitly (f64 or f32), e.g. the fp32 AMG hierarchy of
+// an fp64 solver; the send buffer is sized for 9 fp64 components
+dfvm_status halo_exchange_p(dfvm_mesh* m, void* data, int nc, bool f64, cudaStream_t s) {
   const Part& P = m->part;
   if (P.P == 1) return DFVM_OK;
   if (!m->comm) { set_error(DFVM_E_NCCL, "multi-part mesh without communicator"); return DFVM_E_NCCL; }
   if (dfvm_status st = ensure_halo_buffers(m)) return st;
-  const bool f64 = m->precision == DFVM_F64;
   const size_t eb = f64 ? 8 : 4;
   const int64_t ns = (int64_t)P.send_gid.size();
   if (ns) {

@@ -985,7 +985,7 @@ struct SolverT : SolverBase {
   double* red_all = nullptr;    // [P][8] all-gathered totals
   V4<T>* fdO = nullptr;         // x_f - x_O / x_f - x_N per local internal face (SOU / QUICK)
   V4<T>* fdN = nullptr;
-  Amg<T>* amg = nullptr;        // pressure preconditioner (p_precond == 1), built lazily
+  Amg<T>* amg = nullptr;        // pressure preconditioner (p_precond 1 / 2), built lazily
   bool amg_dirty = true;        // pressure matrix changed since the last Galerkin update
   T* kz = nullptr;              // preconditioned residual z = M^-1 r
   WKDev* d_wk = nullptr;
@@ -1147,7 +1147,7 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
 template <class T>
 static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol, int maxit,
                           dfvm_solve_report* rep, cudaStream_t st) {
-  if (S->o.p_precond == 1) return run_cg_amg(S, X, b, x, tol, rel_tol, maxit, rep, st);
+  if (S->o.p_precond >= 1) return run_cg_amg(S, X, b, x, tol, rel_tol, maxit, rep, st);
   DevMesh<T>& M = *X.M;
   dfvm_mesh* m = S->m;
   const Red red{m->part.P, X.red_local};
@@ -1222,7 +1222,7 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   DevMesh<T>& M = *X.M;
   dfvm_mesh* m = S->m;
   dfvm_status e;
-  if (!X.amg && (e = amg_create<T>(m, M, &X.amg))) return e;
+  if (!X.amg && (e = amg_create<T>(m, M, S->o.p_precond == 2, &X.amg))) return e;
   if (X.amg_dirty) {
     if ((e = amg_update<T>(X.amg, X.pcoef, X.pdiag, st, &S->n_launch))) return e;
     X.amg_dirty = false;
@@ -1540,7 +1540,7 @@ dfvm_status dfvm_solver_create(dfvm_mesh* m, dfvm_bcs* b, const dfvm_piso_opts* 
   if (!m || !b || !opts || !out || b->m != m) { set_error(DFVM_E_INVALID_ARG, "NULL or mismatched argument"); return DFVM_E_INVALID_ARG; }
   if (!(opts->dt > 0) || !(opts->nu >= 0) || opts->n_corr < 1 || opts->n_corr > 8 || opts->n_nonorth < 0 ||
       (opts->n_corr * (opts->n_nonorth + 1)) > 16 || opts->p_maxit < 1 || opts->U_maxit < 1 || !(opts->rho > 0) ||
-      opts->p_precond < 0 || opts->p_precond > 1 || opts->convection < 0 || opts->convection > 3) {
+      opts->p_precond < 0 || opts->p_precond > 2 || opts->convection < 0 || opts->convection > 3) {
     set_error(DFVM_E_INVALID_ARG, "invalid PISO options");
     return DFVM_E_INVALID_ARG;
   }

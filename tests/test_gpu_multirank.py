@@ -96,7 +96,7 @@ def test_operators_partitioned_equal_single(P):
 
 
 @pytest.mark.parametrize("P,wk,precond", [(2, False, "jacobi"), (3, False, "jacobi"), (2, True, "jacobi"),
-                                          (2, False, "amg")])
+                                          (2, False, "amg"), (2, True, "amg32")])
 def test_piso_partitioned_matches_single(P, wk, precond):
     raw = _pipe()
     mo = oracle.Mesh(raw)

@@ -86,7 +86,7 @@ def test_momentum_assembly_and_apply(conv):
     assert rel_op_err(y.get(), ref, scale) <= 1e-12
 
 
-@pytest.mark.parametrize("precond", ["jacobi", "amg"])
+@pytest.mark.parametrize("precond", ["jacobi", "amg", "amg32"])
 @pytest.mark.parametrize("case", ["cavity", "pipe", "pipe_big"])
 def test_pressure_solve(case, precond):
     if case == "pipe_big":
@@ -141,7 +141,7 @@ def test_cavity_regression_values_on_gpu(golden):
 
 
 @pytest.mark.parametrize("precond,conv", [("jacobi", "upwind"), ("amg", "upwind"), ("amg", "sou"),
-                                          ("jacobi", "quick")])
+                                          ("jacobi", "quick"), ("amg32", "upwind")])
 def test_pipe_nonorth_steps(precond, conv):
     raw, mo, mg, bo, bg, kw = pipe_case()
     kw = dict(kw, p_precond=precond, convection=conv)
