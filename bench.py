@@ -139,6 +139,63 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------ GPU arm
+def operator_bench(dfvm, torch, mesh, case, info, stream, sp, hbm, args, max_over_ranks, barrier, reps=10):
+    """FVM operator-apply HBM GB/s (BASELINE metric, second half; SURVEY
+    §8(d1)/(d4)): each north-star operator applied `reps` times back to back
+    on the benchmark mesh, CUDA events on the launching stream, max over
+    ranks.  Inputs: x_c = u(100+k, id), face flux u(300, id) (§8(d2)).
+    Algorithmic bytes per apply (N owned rows, F internal
+    faces, B boundary faces, E empty faces; vb value bytes; int2 incidence
+    records 8 B each side of a face; a face record (32/16 B) counted once; SELL
+    slice metadata (0.25 B/row) omitted)."""
+    import synth
+    vb = 8 if args.precision == "f64" else 4
+    N, F = info["n_owned"], info["n_local_internal_faces"]
+    Bf, E = info["n_local_boundary_faces"], (info["n_empty_faces"] if info["n_peers"] == 0 else 0)
+    rec = 4 * vb                                        # {S, w} / {k, delta} / {S, delta_b} records
+    bc = 8 + rec + 1 + vb                               # boundary incidence + record + kind + value
+    Bo = dfvm.BCs(mesh)
+    for pt in case.raw.patches:
+        if pt.kind != synth.PATCH_EMPTY:
+            Bo.set(pt.name, "s", 0, value=0.5)
+            Bo.set(pt.name, "U", 0, value=(0.3, -0.2, 0.1))
+            Bo.set(pt.name, "p", 0, value=0.0)
+    n = case.raw.n_cells
+    x = mesh.field("cells", 1, synth.cell_field(100, n), sp)
+    X3 = mesh.field("cells", 3, synth.cell_field(100, n, 3), sp)
+    G = mesh.field("cells", 3, None, sp)
+    G9 = mesh.field("cells", 9, None, sp)
+    y = mesh.field("cells", 1, None, sp)
+    xf = mesh.field("faces", 1, None, sp)
+    fl = mesh.field("flux", 1, synth.face_field(300, case.raw.n_faces), sp)
+    dfvm.grad(mesh, x, Bo, "s", G, sp)
+    cases_ = {
+        "interpolate_s": (lambda: dfvm.interpolate(mesh, x, Bo, "s", xf, sp),
+                          vb * N + (8 + 2 * vb) * F + (5 + 2 * vb) * Bf + vb * E),
+        "grad_s": (lambda: dfvm.grad(mesh, x, Bo, "s", G, sp), 5 * vb * N + (16 + rec) * F + bc * Bf),
+        "grad_U": (lambda: dfvm.grad(mesh, X3, Bo, "U", G9, sp),
+                   (3 + 9 + 1) * vb * N + 16 * F + rec * F + (bc + 2 * vb) * Bf),
+        "div": (lambda: dfvm.div(mesh, fl, y, sp), vb * N + 16 * F + vb * F + (8 + vb) * Bf),
+        "laplacian_p": (lambda: dfvm.laplacian(mesh, Bo, "p", x, y, grad=G, stream=sp),
+                        5 * vb * N + 16 * F + vb * F + rec * F + bc * Bf),
+    }
+    out = {}
+    for name, (fn, alg) in cases_.items():
+        fn(); fn()
+        barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(a.elapsed_time(b)) / reps
+        gbs = alg / (ms / 1000.0) / 1e9
+        out[name] = {"ms": ms, "alg_bytes": int(alg), "GBps": gbs, "frac": gbs / hbm}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -152,6 +209,7 @@ def main():
                     help="pressure CG preconditioner (jacobi: A-14; amg: SURVEY NEXT-2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-operators", action="store_true", help="skip the FVM operator-apply GB/s section")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -310,6 +368,9 @@ def main():
             "pcg_iteration_ms": tim["cg_iter_ms"] / max(tim["cg_iter_n"], 1),
             "pcg_share_of_step": tim["cg_iter_ms"] / ms if ms else None, "amg_levels": lv}
 
+    ops = None if args.no_operators else operator_bench(dfvm, torch, mesh, case, info, stream, sp, hbm, args,
+                                                         max_over_ranks, barrier)
+
     cg_its = [r["it"] for rep in reps for r in rep["p"]]
     bi_its = [r["it"] for rep in reps for r in rep["U"]]
     cpu = None
@@ -332,7 +393,7 @@ def main():
                    "bicgstab_iterations_per_component": float(np.mean(bi_its)) if bi_its else 0.0,
                    "krylov_normalised_cell_iterations_per_s": N * (sum(cg_its)) / (ms / 1000.0)},
         "continuity_max": max(r["cont_err_max"] for r in reps),
-        "roofline": roof, "e2e": e2e, "clocks": clk, "cpu_baseline": cpu,
+        "roofline": roof, "operators": ops, "e2e": e2e, "clocks": clk, "cpu_baseline": cpu,
         "setup_seconds": {"mesh_generation": round(t_gen, 2), "mesh_create": round(info["host_seconds"], 2),
                           "total": round(t_setup, 2)},
     }

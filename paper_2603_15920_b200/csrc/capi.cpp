@@ -365,6 +365,7 @@ dfvm_status dfvm_mesh_destroy(dfvm_mesh* m) {
   if (m->d_send) cudaFree(m->d_send);
   if (m->d_recv) cudaFree(m->d_recv);
   if (m->d_send_idx) cudaFree(m->d_send_idx);
+  if (m->d_stage) cudaFree(m->d_stage);
   delete m;
   return DFVM_OK;
 }
@@ -420,6 +421,17 @@ static int64_t global_count(const dfvm_field* f) {
   return f->loc == DFVM_CELLS ? f->m->H.N : f->m->H.NF;
 }
 
+// grow the mesh's persistent staging buffer (a per-call cudaMallocAsync of
+// GBs per call returns and re-maps pool memory each time; the C5 e2e leg
+// spent ~1.3 s/step in import/export with it)
+static dfvm_status stage(dfvm_mesh* m, size_t bytes) {
+  if (m->stage_bytes >= bytes) return DFVM_OK;
+  if (m->d_stage) { DFVM_CUDA(cudaDeviceSynchronize()); DFVM_CUDA(cudaFree(m->d_stage)); m->d_stage = nullptr; }
+  DFVM_CUDA(cudaMalloc(&m->d_stage, bytes));
+  m->stage_bytes = bytes;
+  return DFVM_OK;
+}
+
 dfvm_status dfvm_field_import(dfvm_field* f, const double* src, int32_t src_is_host, dfvm_stream stream) {
   CHECK_ARG(f && src, "NULL argument");
   dfvm_mesh* m = f->m;
@@ -428,20 +440,18 @@ dfvm_status dfvm_field_import(dfvm_field* f, const double* src, int32_t src_is_h
   const int32_t* map = f->loc == DFVM_CELLS ? m->d_cell_orig : m->d_face_orig;
   const bool oriented = f->loc == 2;
   const double* dsrc = src;
-  void* tmp = nullptr;
+  std::unique_lock<std::mutex> lk(m->stage_mu, std::defer_lock);
   if (src_is_host) {
     const size_t bytes = (size_t)global_count(f) * f->n_comp * 8;
-    DFVM_CUDA(cudaMallocAsync(&tmp, bytes, s));
-    DFVM_CUDA(cudaMemcpyAsync(tmp, src, bytes, cudaMemcpyHostToDevice, s));
-    dsrc = (const double*)tmp;
+    lk.lock();
+    if (dfvm_status st = stage(m, bytes)) return st;
+    DFVM_CUDA(cudaMemcpyAsync(m->d_stage, src, bytes, cudaMemcpyHostToDevice, s));
+    dsrc = (const double*)m->d_stage;
   }
   if (m->precision == DFVM_F64) launch_import<double>((double*)f->ptr, dsrc, map, n, f->n_comp, oriented, s);
   else launch_import<float>((float*)f->ptr, dsrc, map, n, f->n_comp, oriented, s);
   DFVM_CUDA(cudaGetLastError());
-  if (tmp) {
-    DFVM_CUDA(cudaFreeAsync(tmp, s));
-    DFVM_CUDA(cudaStreamSynchronize(s));
-  }
+  if (src_is_host) DFVM_CUDA(cudaStreamSynchronize(s));   // the caller may free src; staging reusable
   return DFVM_OK;
 }
 
@@ -454,19 +464,19 @@ dfvm_status dfvm_field_export(const dfvm_field* f, double* dst, int32_t dst_is_h
   const bool oriented = f->loc == 2;
   const size_t bytes = (size_t)global_count(f) * f->n_comp * 8;
   double* ddst = dst;
-  void* tmp = nullptr;
+  std::unique_lock<std::mutex> lk(m->stage_mu, std::defer_lock);
   if (dst_is_host) {
-    DFVM_CUDA(cudaMallocAsync(&tmp, bytes, s));
+    lk.lock();
+    if (dfvm_status st = stage(m, bytes)) return st;
     if (m->part.P > 1)   // keep the entries other ranks own
-      DFVM_CUDA(cudaMemcpyAsync(tmp, dst, bytes, cudaMemcpyHostToDevice, s));
-    ddst = (double*)tmp;
+      DFVM_CUDA(cudaMemcpyAsync(m->d_stage, dst, bytes, cudaMemcpyHostToDevice, s));
+    ddst = (double*)m->d_stage;
   }
   if (m->precision == DFVM_F64) launch_export<double>(ddst, (const double*)f->ptr, map, n, f->n_comp, oriented, s);
   else launch_export<float>(ddst, (const float*)f->ptr, map, n, f->n_comp, oriented, s);
   DFVM_CUDA(cudaGetLastError());
-  if (tmp) {
-    DFVM_CUDA(cudaMemcpyAsync(dst, tmp, bytes, cudaMemcpyDeviceToHost, s));
-    DFVM_CUDA(cudaFreeAsync(tmp, s));
+  if (dst_is_host) {
+    DFVM_CUDA(cudaMemcpyAsync(dst, m->d_stage, bytes, cudaMemcpyDeviceToHost, s));
     DFVM_CUDA(cudaStreamSynchronize(s));
   }
   return DFVM_OK;

@@ -20,6 +20,7 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <mutex>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -128,6 +129,11 @@ struct dfvm_mesh {
   // halo exchange buffers (P > 1)
   void* d_send = nullptr; void* d_recv = nullptr; int32_t* d_send_idx = nullptr;
   size_t halo_bytes = 0;
+  // persistent device staging buffer of host<->device field import/export
+  // (grown on demand, guarded: one import/export at a time per mesh)
+  void* d_stage = nullptr;
+  size_t stage_bytes = 0;
+  std::mutex stage_mu;
   int64_t n_faces_local() const { return (int64_t)part.lf_gid.size() + (int64_t)part.lb_gid.size(); }
 };
 
