@@ -33,12 +33,15 @@
 #include <type_traits>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "amg.h"
 #include "dev.cuh"
 
 namespace dfvm {
 
 dfvm_status halo_exchange_p(dfvm_mesh* m, void* data, int nc, bool f64, cudaStream_t s);
+bool comm_is_local(const dfvm_comm* c);
 
 constexpr int kCoarseMax = 2048;     // shared-memory capacity of the one-block coarse solve
 constexpr int kMaxLevels = 16;
@@ -53,11 +56,15 @@ constexpr int kMaxLevels = 16;
 //                    doubles per level, and deep levels are launch-bound)
 //   DFVM_AMG_OMEGA   coarse-correction scale (symmetric over-correction,
 //                    < 2 keeps M SPD with adjoint smoothers)   default 1.8
+//   DFVM_AMG_TAIL    levels with <= this many rows (below level 0) run as
+//                    one cooperative kernel with grid-wide barriers instead
+//                    of one launch per phase (0: off)           default 131072
 struct AmgParams {
-  int coarse = 256, sweeps = 32, wmax = 4;
+  int coarse = 256, sweeps = 32, wmax = 4, tail = 131072;
   bool wcycle = true;
   double omega = 1.8;
   AmgParams() {
+    if (const char* e = getenv("DFVM_AMG_TAIL")) tail = std::max(0, atoi(e));
     if (const char* e = getenv("DFVM_AMG_OMEGA")) omega = atof(e);
     if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kCoarseMax, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_SWEEPS")) sweeps = std::max(1, atoi(e));
@@ -151,6 +158,17 @@ struct AmgLevelDev {
   P *e = nullptr, *r2 = nullptr;                  // W-cycle: second-visit solution / rhs
 };
 
+// device copy of a level for the cooperative tail kernel
+template <class P>
+struct TailLevel {
+  int n;
+  const int *ms_ptr, *ms_len, *mnb;
+  const P *coef, *diag, *dl1;
+  const int* agg;                   // this level's rows -> next level's rows
+  const int *mem_ptr, *mem;         // this level's rows <- members on the finer level
+  P *x, *b, *r, *t, *e, *r2;
+};
+
 // hierarchy stored and cycled in type P
 template <class P>
 struct AmgH {
@@ -158,6 +176,9 @@ struct AmgH {
   int nlev = 0;
   AmgParams prm;
   AmgLevelDev<P> L[kMaxLevels];
+  int tail = 0;                     // first level run by the cooperative tail kernel (0: none)
+  int tail_grid = 0;
+  TailLevel<P>* d_tail = nullptr;
   std::vector<void*> allocs;
   int64_t bytes = 0;
   ~AmgH() { for (void* p : allocs) cudaFree(p); }
@@ -303,6 +324,9 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
   return DFVM_OK;
 }
 
+template <class P>
+static dfvm_status setup_tail(AmgH<P>* A);
+
 template <class T>
 dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** out) {
   Amg<T>* A = new Amg<T>();
@@ -310,9 +334,11 @@ dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** ou
   if (fp32 && !std::is_same<T, float>::value) {
     A->lo = new AmgH<float>();
     st = build<float, T>(m, M, A->lo);
+    if (!st) st = setup_tail(A->lo);
   } else {
     A->same = new AmgH<T>();
     st = build<T, T>(m, M, A->same);
+    if (!st) st = setup_tail(A->same);
   }
   if (st) { delete A; return st; }
   *out = A;
@@ -511,6 +537,122 @@ __global__ void __launch_bounds__(1024) k_amg_coarse(int n, const int* __restric
   for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = (TO)xs[cur][i];
 }
 
+// ------------------------------------------------------------ cooperative tail
+// The deep levels (a few thousand to ~1e5 rows) are launch-bound: one
+// W-cycle visit of a level below ~1e5 rows is a dozen launches of 3-30 us
+// each.  The tail kernel runs the whole sub-cycle from level `l` down in one
+// cooperative launch: every phase is a grid-stride loop over the level's
+// rows, phases are separated by grid-wide barriers, and the arithmetic is
+// that of the per-phase kernels above (same formulas, same order), so the
+// result is bitwise identical to the launched cycle.
+namespace cg = cooperative_groups;
+constexpr int kTailThreads = 512;
+
+template <class P>
+__device__ void tail_cycle(cg::grid_group& g, const TailLevel<P>* __restrict__ L, int l, int nlev, const P* b, P* x,
+                           P w, int sweeps, int wc, int wmax) {
+  const TailLevel<P>& F = L[l];
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  if (l == nlev - 1) {                      // coarsest: l1-Jacobi sweeps in block 0 (shared memory)
+    if (blockIdx.x == 0) {
+      __shared__ P xs[2][kCoarseMax];
+      for (int i = threadIdx.x; i < F.n; i += blockDim.x) xs[0][i] = b[i] / F.dl1[i];
+      __syncthreads();
+      int cur = 0;
+      for (int it = 1; it < sweeps; ++it) {
+        for (int i = threadIdx.x; i < F.n; i += blockDim.x)
+          xs[cur ^ 1][i] = xs[cur][i] + (b[i] - row_apply(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, xs[cur])) / F.dl1[i];
+        __syncthreads();
+        cur ^= 1;
+      }
+      for (int i = threadIdx.x; i < F.n; i += blockDim.x) x[i] = xs[cur][i];
+    }
+    g.sync();
+    return;
+  }
+  const TailLevel<P>& C = L[l + 1];
+  for (int i = tid; i < F.n; i += nt) {     // pre-smooth + residual (k_amg_pre_resid)
+    const int s = i >> 5, lane = i & 31;
+    const int len = F.ms_len[s], base = F.ms_ptr[s] + lane;
+    const P bi = b[i];
+    const P xi = bi / F.dl1[i];
+    P acc = F.diag[i] * xi;
+    for (int j = 0; j < len; ++j) {
+      const int c = F.mnb[base + 32 * j];
+      acc += F.coef[base + 32 * j] * (b[c] / F.dl1[c]);
+    }
+    F.t[i] = xi;
+    F.r[i] = bi - acc;
+  }
+  g.sync();
+  for (int I = tid; I < C.n; I += nt) {     // restriction (k_amg_restrict)
+    P sum = P(0);
+    for (int k = C.mem_ptr[I]; k < C.mem_ptr[I + 1]; ++k) sum += F.r[C.mem[k]];
+    C.b[I] = sum;
+  }
+  g.sync();
+  tail_cycle(g, L, l + 1, nlev, C.b, C.x, w, sweeps, wc, wmax);
+  if (wc && l + 1 < nlev - 1 && l + 1 <= wmax) {
+    for (int I = tid; I < C.n; I += nt)     // second visit (k_amg_resid, k_amg_add)
+      C.r2[I] = C.b[I] - row_apply(I, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x);
+    g.sync();
+    tail_cycle(g, L, l + 1, nlev, C.r2, C.e, w, sweeps, wc, wmax);
+    for (int I = tid; I < C.n; I += nt) C.x[I] += C.e[I];
+    g.sync();
+  }
+  for (int i = tid; i < F.n; i += nt) {     // prolongation + post-smooth (k_amg_prolong_smooth)
+    const int s = i >> 5, lane = i & 31;
+    const int len = F.ms_len[s], base = F.ms_ptr[s] + lane;
+    const P ti = F.t[i] + w * C.x[F.agg[i]];
+    P acc = F.diag[i] * ti;
+    for (int j = 0; j < len; ++j) {
+      const int c = F.mnb[base + 32 * j];
+      acc += F.coef[base + 32 * j] * (F.t[c] + w * C.x[F.agg[c]]);
+    }
+    x[i] = ti + (b[i] - acc) / F.dl1[i];
+  }
+  g.sync();
+}
+
+template <class P>
+__global__ void __launch_bounds__(kTailThreads) k_amg_tail(const TailLevel<P>* __restrict__ L, int l, int nlev,
+                                                          const P* b, P* x, P w, int sweeps, int wc, int wmax,
+                                                          const int* done) {
+  if (*done) return;
+  cg::grid_group g = cg::this_grid();
+  tail_cycle(g, L, l, nlev, b, x, w, sweeps, wc, wmax);
+}
+
+template <class P>
+static dfvm_status setup_tail(AmgH<P>* A) {
+  A->tail = 0;
+  if (A->prm.tail <= 0) return DFVM_OK;
+  // ranks of an in-process group may share one GPU: grids sized to the whole
+  // device from several streams would not be co-resident
+  if (comm_is_local(A->m->comm)) return DFVM_OK;
+  int l = 1;
+  while (l < A->nlev && A->L[l].n > A->prm.tail) ++l;
+  if (l >= A->nlev - 1) return DFVM_OK;     // nothing but the coarsest solve below: keep the launches
+  int dev = 0, occ = 0, sms = 0, coop = 0;
+  DFVM_CUDA(cudaGetDevice(&dev));
+  DFVM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (!coop) return DFVM_OK;
+  DFVM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DFVM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_amg_tail<P>, kTailThreads, 0));
+  if (occ < 1) return DFVM_OK;
+  std::vector<TailLevel<P>> h(A->nlev);
+  for (int k = 0; k < A->nlev; ++k) {
+    const AmgLevelDev<P>& D = A->L[k];
+    h[k] = TailLevel<P>{D.n, D.ms_ptr, D.ms_len, D.mnb, D.coef, D.diag, D.dl1, D.agg, D.mem_ptr, D.mem,
+                        D.x, D.b, D.r, D.t, D.e, D.r2};
+  }
+  dfvm_status st;
+  if ((st = A->up(&A->d_tail, h))) return st;
+  A->tail = l;
+  A->tail_grid = occ * sms;
+  return DFVM_OK;
+}
+
 // ------------------------------------------------------------ host drivers
 template <class P, class T>
 static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream_t s, int* nl) {
@@ -552,6 +694,16 @@ dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s
 template <class P>
 static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl) {
   AmgLevelDev<P>& F = A->L[l];
+  if (A->tail && l == A->tail) {
+    const TailLevel<P>* d = A->d_tail;
+    int nlev = A->nlev, sweeps = A->prm.sweeps, wc = A->prm.wcycle ? 1 : 0, wmax = A->prm.wmax;
+    P w = (P)A->prm.omega;
+    void* args[] = {(void*)&d, (void*)&l, (void*)&nlev, (void*)&b, (void*)&x, (void*)&w, (void*)&sweeps, (void*)&wc,
+                    (void*)&wmax, (void*)&done};
+    cudaLaunchCooperativeKernel((const void*)k_amg_tail<P>, dim3(A->tail_grid), dim3(kTailThreads), args, 0, s);
+    ++*nl;
+    return;
+  }
   if (l == A->nlev - 1) {
     k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b, x,
                                              A->prm.sweeps, done);

@@ -178,6 +178,8 @@ dfvm_status halo_exchange_p(dfvm_mesh* m, void* data, int nc, bool f64, cudaStre
   return local_finish(G, me, s);
 }
 
+bool comm_is_local(const dfvm_comm* c) { return c && c->backend == 1; }
+
 // all-gather of `n` doubles per rank into gathered[n_ranks][n] (rank order)
 dfvm_status allgather_f64(dfvm_mesh* m, const double* local, double* gathered, int n, cudaStream_t s) {
   if (m->part.P == 1) {
