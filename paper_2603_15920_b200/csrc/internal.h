@@ -91,6 +91,7 @@ struct DevMesh {
   int n_slices = 0, max_row = 0;
   V4<T>* fgeo = nullptr;   // [F]
   V4<T>* fcor = nullptr;   // [F]
+  T* fw = nullptr;         // [F] copy of the weights (kernels that need w alone read 8 B, not a 32 B record)
   int2* fcell = nullptr;   // [F]
   V4<T>* bgeo = nullptr;   // [B]
   int* bcell = nullptr;    // [B]

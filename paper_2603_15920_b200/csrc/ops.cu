@@ -56,21 +56,49 @@ void launch_export(double* dst, const T* src, const int32_t* map, int64_t n, int
   count_launch();
 }
 
+// Gather kernels load their incidences in batches of kB: first the kB int2
+// records of the row, then every face record / neighbour value they point
+// to, then the arithmetic in ascending incidence order (the summation order
+// of the one-at-a-time loop, so results are bitwise unchanged).  Each thread
+// keeps ~kB x (record + value) independent loads in flight instead of a
+// dependent chain per face.
+constexpr int kB = 4;
+
 // ------------------------------------------------------------ interpolate
 // phi_f = w phi_O + (1 - w) phi_N; boundary: fixed value or phi_O;
-// empty faces: 0.  Face-parallel (coalesced over the face records).
+// empty faces: 0.  Face-parallel (coalesced over the face arrays); internal
+// faces in batches of kB per thread.
 template <class T, int NC>
 __global__ void k_interp(DevMesh<T> M, const T* __restrict__ x, const uint8_t* __restrict__ bkind,
                          const T* __restrict__ bval, T* __restrict__ xf) {
-  const int64_t total = (int64_t)M.F + M.B + M.E;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < M.F) {
-      const int2 c = __ldg(&M.fcell[i]);
-      const T w = ld4(&M.fgeo[i]).w;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = tid; i0 < M.F; i0 += kB * nt) {
+    int2 c[kB];
+    T w[kB];
 #pragma unroll
-      for (int k = 0; k < NC; ++k) xf[i * NC + k] = w * x[(int64_t)c.x * NC + k] + (T(1) - w) * x[(int64_t)c.y * NC + k];
-    } else if (i < (int64_t)M.F + M.B) {
-      const int b = (int)(i - M.F);
+    for (int u = 0; u < kB; ++u) {
+      const int64_t i = i0 + u * nt;
+      c[u] = i < M.F ? __ldg(&M.fcell[i]) : make_int2(0, 0);
+      w[u] = i < M.F ? __ldg(&M.fw[i]) : T(0);
+    }
+    T xo[kB][NC], xn[kB][NC];
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) { xo[u][k] = x[(int64_t)c[u].x * NC + k]; xn[u][k] = x[(int64_t)c[u].y * NC + k]; }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int64_t i = i0 + u * nt;
+      if (i < M.F)
+#pragma unroll
+        for (int k = 0; k < NC; ++k) xf[i * NC + k] = w[u] * xo[u][k] + (T(1) - w[u]) * xn[u][k];
+    }
+  }
+  const int64_t nb = (int64_t)M.B + M.E;
+  for (int64_t j = tid; j < nb; j += nt) {
+    const int64_t i = M.F + j;
+    if (j < M.B) {
+      const int b = (int)j;
       const int o = M.bcell[b];
 #pragma unroll
       for (int k = 0; k < NC; ++k) xf[i * NC + k] = bkind[b] ? x[(int64_t)o * NC + k] : bval[(int64_t)b * NC + k];
@@ -101,34 +129,52 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
     for (int k = 0; k < NC; ++k) acc[k][0] = acc[k][1] = acc[k][2] = T(0);
     const int len = __ldg(&M.sl_len[s]);
     const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
-    for (int j = 0; j < len; ++j) {
-      const int2 en = __ldg(&e[j * 32]);
-      if (en.y >= 0) {
-        const bool own = en.x >= 0;
-        const int f = own ? en.x : ~en.x;
-        const V4<T> g = ld4(&M.fgeo[f]);
-        const T sg = own ? T(1) : T(-1);
+    for (int j0 = 0; j0 < len; j0 += kB) {
+      int2 en[kB];
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          T pf;
-          if (FACEVALS) {
-            pf = fv[(int64_t)f * NC + k];
-          } else {
-            const T xn = x[(int64_t)en.y * NC + k];
-            const T xO = own ? xc[k] : xn, xN = own ? xn : xc[k];
-            pf = g.w * xO + (T(1) - g.w) * xN;
-          }
-          acc[k][0] += sg * pf * g.x; acc[k][1] += sg * pf * g.y; acc[k][2] += sg * pf * g.z;
+      for (int u = 0; u < kB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
+      V4<T> g[kB];
+      T v[kB][NC];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        g[u] = V4<T>{T(0), T(0), T(0), T(0)};
+#pragma unroll
+        for (int k = 0; k < NC; ++k) v[u][k] = T(0);
+        if (en[u].y >= 0) {
+          const int f = en[u].x >= 0 ? en[u].x : ~en[u].x;
+          g[u] = ld4(&M.fgeo[f]);
+#pragma unroll
+          for (int k = 0; k < NC; ++k) v[u][k] = FACEVALS ? fv[(int64_t)f * NC + k] : x[(int64_t)en[u].y * NC + k];
+        } else if (en[u].y == -1) {
+          const int b = en[u].x;
+          g[u] = ld4(&M.bgeo[b]);
+#pragma unroll
+          for (int k = 0; k < NC; ++k)
+            v[u][k] = FACEVALS ? fv[((int64_t)M.F + b) * NC + k] : (bkind[b] ? xc[k] : bval[(int64_t)b * NC + k]);
         }
-      } else if (en.y == -1) {
-        const int b = en.x;
-        const V4<T> g = ld4(&M.bgeo[b]);
+      }
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          T pb;
-          if (FACEVALS) pb = fv[((int64_t)M.F + b) * NC + k];
-          else pb = bkind[b] ? xc[k] : bval[(int64_t)b * NC + k];
-          acc[k][0] += pb * g.x; acc[k][1] += pb * g.y; acc[k][2] += pb * g.z;
+      for (int u = 0; u < kB; ++u) {
+        if (en[u].y >= 0) {
+          const bool own = en[u].x >= 0;
+          const T sg = own ? T(1) : T(-1);
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            T pf;
+            if (FACEVALS) {
+              pf = v[u][k];
+            } else {
+              const T xO = own ? xc[k] : v[u][k], xN = own ? v[u][k] : xc[k];
+              pf = g[u].w * xO + (T(1) - g[u].w) * xN;
+            }
+            acc[k][0] += sg * pf * g[u].x; acc[k][1] += sg * pf * g[u].y; acc[k][2] += sg * pf * g[u].z;
+          }
+        } else if (en[u].y == -1) {
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            const T pb = v[u][k];
+            acc[k][0] += pb * g[u].x; acc[k][1] += pb * g[u].y; acc[k][2] += pb * g[u].z;
+          }
         }
       }
     }
@@ -153,12 +199,24 @@ __global__ void __launch_bounds__(kThreads) k_div(DevMesh<T> M, const T* __restr
     T acc = T(0);
     const int len = __ldg(&M.sl_len[s]);
     const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
-    for (int j = 0; j < len; ++j) {
-      const int2 en = __ldg(&e[j * 32]);
-      if (en.y >= 0) {
-        if (en.x >= 0) acc += flux[en.x]; else acc -= flux[~en.x];
-      } else if (en.y == -1) {
-        acc += flux[M.F + en.x];
+    for (int j0 = 0; j0 < len; j0 += kB) {
+      int2 en[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
+      T v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        v[u] = T(0);
+        if (en[u].y >= 0) v[u] = flux[en[u].x >= 0 ? en[u].x : ~en[u].x];
+        else if (en[u].y == -1) v[u] = flux[M.F + en[u].x];
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        if (en[u].y >= 0) {
+          if (en[u].x >= 0) acc += v[u]; else acc -= v[u];
+        } else if (en[u].y == -1) {
+          acc += v[u];
+        }
       }
     }
     if (row < M.n_own) out[row] = acc;
@@ -184,34 +242,45 @@ __global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restr
     T acc = T(0);
     const int len = __ldg(&M.sl_len[s]);
     const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
-    for (int j = 0; j < len; ++j) {
-      const int2 en = __ldg(&e[j * 32]);
-      if (en.y >= 0) {
-        const bool own = en.x >= 0;
-        const int f = own ? en.x : ~en.x;
-        const int n = en.y;
-        const T w = ld4(&M.fgeo[f]).w;
-        const V4<T> c = ld4(&M.fcor[f]);
-        const T xn = x[n];
-        const T Gn0 = G[3 * (int64_t)n], Gn1 = G[3 * (int64_t)n + 1], Gn2 = G[3 * (int64_t)n + 2];
-        const T wO = w, wN = T(1) - w;
-        // owner / neighbour assignment for this face
-        const T xO = own ? xc : xn, xN = own ? xn : xc;
-        const T GO0 = own ? Gc[0] : Gn0, GO1 = own ? Gc[1] : Gn1, GO2 = own ? Gc[2] : Gn2;
-        const T GN0 = own ? Gn0 : Gc[0], GN1 = own ? Gn1 : Gc[1], GN2 = own ? Gn2 : Gc[2];
-        T gf = T(1);
-        if (GAMMA) {
-          const T gn = gamma[n];
-          gf = wO * (own ? gc : gn) + wN * (own ? gn : gc);
+    for (int j0 = 0; j0 < len; j0 += kB) {
+      int2 en[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
+      T w[kB], xn[kB], Gn[kB][3], gn[kB];
+      V4<T> c[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        w[u] = xn[u] = gn[u] = T(0);
+        Gn[u][0] = Gn[u][1] = Gn[u][2] = T(0);
+        c[u] = V4<T>{T(0), T(0), T(0), T(0)};
+        if (en[u].y >= 0) {
+          const int f = en[u].x >= 0 ? en[u].x : ~en[u].x;
+          const int n = en[u].y;
+          w[u] = __ldg(&M.fw[f]);
+          c[u] = ld4(&M.fcor[f]);
+          xn[u] = x[n];
+          Gn[u][0] = G[3 * (int64_t)n]; Gn[u][1] = G[3 * (int64_t)n + 1]; Gn[u][2] = G[3 * (int64_t)n + 2];
+          if (GAMMA) gn[u] = gamma[n];
+        } else if (en[u].y == -1) {
+          const int b = en[u].x;
+          if (bkind[b] == 0) { c[u].w = ld4(&M.bgeo[b]).w; xn[u] = bval[b]; }
         }
-        const T corr = c.x * (wO * GO0 + wN * GN0) + c.y * (wO * GO1 + wN * GN1) + c.z * (wO * GO2 + wN * GN2);
-        const T q = gf * (c.w * (xN - xO) + corr);
-        acc += own ? q : -q;
-      } else if (en.y == -1) {
-        const int b = en.x;
-        if (bkind[b] == 0) {
-          const T db = ld4(&M.bgeo[b]).w;
-          acc += gc * db * (bval[b] - xc);
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        if (en[u].y >= 0) {
+          const bool own = en[u].x >= 0;
+          const T wO = w[u], wN = T(1) - w[u];
+          const T xO = own ? xc : xn[u], xN = own ? xn[u] : xc;
+          const T GO0 = own ? Gc[0] : Gn[u][0], GO1 = own ? Gc[1] : Gn[u][1], GO2 = own ? Gc[2] : Gn[u][2];
+          const T GN0 = own ? Gn[u][0] : Gc[0], GN1 = own ? Gn[u][1] : Gc[1], GN2 = own ? Gn[u][2] : Gc[2];
+          T gf = T(1);
+          if (GAMMA) gf = wO * (own ? gc : gn[u]) + wN * (own ? gn[u] : gc);
+          const T corr = c[u].x * (wO * GO0 + wN * GN0) + c[u].y * (wO * GO1 + wN * GN1) + c[u].z * (wO * GO2 + wN * GN2);
+          const T q = gf * (c[u].w * (xN - xO) + corr);
+          acc += own ? q : -q;
+        } else if (en[u].y == -1) {
+          if (bkind[en[u].x] == 0) acc += gc * c[u].w * (xn[u] - xc);
         }
       }
     }

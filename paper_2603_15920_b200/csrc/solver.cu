@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, c
       if (en.y >= 0) {
         const bool own = en.x >= 0;
         const int f = own ? en.x : ~en.x;
-        const T w = ld4(&M.fgeo[f]).w;
+        const T w = __ldg(&M.fw[f]);
         const V4<T> c = ld4(&M.fcor[f]);
         const T md = phi[f];
         const T lam = conv == 1 ? w : (md >= T(0) ? T(1) : T(0));
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(kThreads) k_pcoef(DevMesh<T> M, const T* __res
       if (en.y >= 0) {
         const bool own = en.x >= 0;
         const int f = own ? en.x : ~en.x;
-        const T w = ld4(&M.fgeo[f]).w;
+        const T w = __ldg(&M.fw[f]);
         const T d = ld4(&M.fcor[f]).w;
         const T rn = rAU[en.y];
         const T cf = (w * (own ? ra : rn) + (T(1) - w) * (own ? rn : ra)) * d;
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kThreads) k_prhs(DevMesh<T> M, const T* __rest
       const bool own = en.x >= 0;
       const int f = own ? en.x : ~en.x;
       const int n = en.y;
-      const T w = ld4(&M.fgeo[f]).w;
+      const T w = __ldg(&M.fw[f]);
       const V4<T> c = ld4(&M.fcor[f]);
       const T rn = rAU[n];
       const T* Gn = gp + 3 * (int64_t)n;
@@ -469,7 +469,7 @@ __global__ void k_fluxcorr(DevMesh<T> M, const T* __restrict__ phiHbyA, const T*
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < M.F) {
       const int2 cc = __ldg(&M.fcell[i]);
-      const T w = ld4(&M.fgeo[i]).w;
+      const T w = __ldg(&M.fw[i]);
       const V4<T> c = ld4(&M.fcor[i]);
       const T rf = w * rAU[cc.x] + (T(1) - w) * rAU[cc.y];
       T v = phiHbyA[i] - rf * c.w * (p[cc.y] - p[cc.x]);
