@@ -355,7 +355,9 @@ def main():
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(f"{kname.split()[0]}_{args.config}_{args.precision}_{n_own}")
+            kk = kname.split()[0]
+            pc = f"_{args.precond}" if kk.startswith("k_amg") else ""
+            traffic = json.load(open(tfile)).get(f"{kk}_{args.config}_{args.precision}{pc}_{n_own}")
         except Exception:
             traffic = None
     roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "peak_source": peak_src,
