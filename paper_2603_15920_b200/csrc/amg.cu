@@ -148,7 +148,7 @@ struct AmgLevelDev {
   const P* diag = nullptr;   // level 0: the solver's pdiag (P == T) or diag_own
   P* coef_own = nullptr;
   P* diag_own = nullptr;
-  P* dl1 = nullptr;
+  P* il1 = nullptr;
   // Galerkin maps of this (coarse) level from the finer level
   int *gal_ptr = nullptr, *gal_idx = nullptr;     // per coarse SELL position
   int *dg_ptr = nullptr, *dg_idx = nullptr;       // per coarse row: internal fine positions
@@ -163,7 +163,7 @@ template <class P>
 struct TailLevel {
   int n;
   const int *ms_ptr, *ms_len, *mnb;
-  const P *coef, *diag, *dl1;
+  const P *coef, *diag, *il1;
   const int* agg;                   // this level's rows -> next level's rows
   const int *mem_ptr, *mem;         // this level's rows <- members on the finer level
   P *x, *b, *r, *t, *e, *r2;
@@ -226,7 +226,7 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
   L0.n = M.n_own; L0.n_slices = M.n_slices; L0.n_sell = M.n_minc;
   L0.ms_ptr = M.ms_ptr; L0.ms_len = M.ms_len; L0.mnb = M.mnb;
   dfvm_status st;
-  if ((st = A->zalloc(&L0.dl1, M.n_own)) || (st = A->zalloc(&L0.x, M.n_cells)) || (st = A->zalloc(&L0.r, M.n_own)) ||
+  if ((st = A->zalloc(&L0.il1, M.n_own)) || (st = A->zalloc(&L0.x, M.n_cells)) || (st = A->zalloc(&L0.r, M.n_own)) ||
       (st = A->zalloc(&L0.t, M.n_cells)))
     return st;
   if (!std::is_same<P, T>::value) {
@@ -311,7 +311,7 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
         (st = A->up(&D.gal_ptr, gal_ptr)) || (st = A->up(&D.gal_idx, gal_idx)) || (st = A->up(&D.dg_ptr, dg_ptr)) ||
         (st = A->up(&D.dg_idx, dg_idx)) || (st = A->up(&D.mem_ptr, mem_ptr)) || (st = A->up(&D.mem, mem)) ||
         (st = A->up(&A->L[lev].agg, agg)) || (st = A->zalloc(&D.coef_own, (size_t)D.n_sell)) ||
-        (st = A->zalloc(&D.diag_own, nc)) || (st = A->zalloc(&D.dl1, nc)) || (st = A->zalloc(&D.x, nc)) ||
+        (st = A->zalloc(&D.diag_own, nc)) || (st = A->zalloc(&D.il1, nc)) || (st = A->zalloc(&D.x, nc)) ||
         (st = A->zalloc(&D.b, nc)) || (st = A->zalloc(&D.r, nc)) || (st = A->zalloc(&D.t, nc)) ||
         (st = A->zalloc(&D.e, nc)) || (st = A->zalloc(&D.r2, nc)))
       return st;
@@ -385,15 +385,16 @@ __global__ void k_gal_diag(int n, const int* __restrict__ mp, const int* __restr
   }
 }
 
-// l1 diagonal: a_ii + sum_j |a_ij| over the row's SELL entries
+// inverse l1 diagonal: 1 / (a_ii + sum_j |a_ij|) over the row's SELL entries
+// (stored inverted: the smoothers multiply, no fp64 division per gather)
 template <class T>
-__global__ void k_dl1(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                      const T* __restrict__ coef, const T* __restrict__ diag, T* __restrict__ dl1) {
+__global__ void k_il1(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                      const T* __restrict__ coef, const T* __restrict__ diag, T* __restrict__ il1) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     const int s = r >> 5, lane = r & 31;
     T a = diag[r];
     for (int j = 0; j < ms_len[s]; ++j) a += fabs(coef[ms_ptr[s] + 32 * j + lane]);
-    dl1[r] = a;
+    il1[r] = T(1) / a;
   }
 }
 
@@ -420,13 +421,77 @@ __device__ __forceinline__ T row_apply(int r, const int* __restrict__ ms_ptr, co
   return acc;
 }
 
+// One row of the fused pre-smooth + residual: x0_i = b_i / d1_i and
+// r_i = b_i - (A x0)_i with x0 of the neighbours formed on the fly.  Loads in
+// batches of 4 entries (columns + coefficients, then the gathered b and 1/d1),
+// accumulation in entry order.
+template <class T>
+__device__ __forceinline__ void pre_resid_row(int i, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                                              const int* __restrict__ mnb, const T* __restrict__ coef,
+                                              const T* __restrict__ diag, const T* __restrict__ il1,
+                                              const T* __restrict__ b, T& x0, T& r) {
+  const int s = i >> 5, lane = i & 31;
+  const int len = ms_len[s], base = ms_ptr[s] + lane;
+  const T bi = b[i];
+  const T xi = bi * il1[i];
+  T acc = diag[i] * xi;
+  int j = 0;
+  for (; j + 4 <= len; j += 4) {
+    T a[4], v[4];
+    int c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&mnb[base + 32 * (j + u)]); }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = b[c[u]] * il1[c[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
+  }
+  for (; j < len; ++j) {
+    const int c = __ldg(&mnb[base + 32 * j]);
+    acc += __ldg(&coef[base + 32 * j]) * (b[c] * il1[c]);
+  }
+  x0 = xi;
+  r = bi - acc;
+}
+// One row of the fused prolongation + post-smooth: t = x0 + w x_c[agg] (on
+// the fly for the row and its neighbours), returns t_i + (b - A t)_i / d1_i.
+template <class T>
+__device__ __forceinline__ T prolong_smooth_row(int i, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                                                const int* __restrict__ mnb, const T* __restrict__ coef,
+                                                const T* __restrict__ diag, const T* __restrict__ il1,
+                                                const int* __restrict__ agg, const T* __restrict__ xc, T w,
+                                                const T* __restrict__ x0, const T* __restrict__ b) {
+  const int s = i >> 5, lane = i & 31;
+  const int len = ms_len[s], base = ms_ptr[s] + lane;
+  const T ti = x0[i] + w * xc[agg[i]];
+  T acc = diag[i] * ti;
+  int j = 0;
+  for (; j + 4 <= len; j += 4) {
+    T a[4], v[4];
+    int c[4], g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&mnb[base + 32 * (j + u)]); }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { g[u] = agg[c[u]]; v[u] = x0[c[u]]; }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = v[u] + w * xc[g[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
+  }
+  for (; j < len; ++j) {
+    const int c = __ldg(&mnb[base + 32 * j]);
+    acc += __ldg(&coef[base + 32 * j]) * (x0[c] + w * xc[agg[c]]);
+  }
+  return ti + (b[i] - acc) * il1[i];
+}
+
 // x = b / d1 (pre-smoothing from a zero guess); b in the caller's type TB
 template <class P, class TB, class TX>
-__global__ void k_amg_pre(int n, const TB* __restrict__ b, const P* __restrict__ dl1, TX* __restrict__ x,
+__global__ void k_amg_pre(int n, const TB* __restrict__ b, const P* __restrict__ il1, TX* __restrict__ x,
                           const int* done) {
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    x[i] = (TX)((P)b[i] / dl1[i]);
+    x[i] = (TX)((P)b[i] * il1[i]);
 }
 // r = b - A x
 template <class P, class TB>
@@ -460,21 +525,14 @@ __global__ void k_amg_prolong(int n, const int* __restrict__ agg, const T* __res
 template <class T>
 __global__ void k_amg_pre_resid(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
                                 const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
-                                const T* __restrict__ dl1, const T* __restrict__ b, T* __restrict__ x0,
+                                const T* __restrict__ il1, const T* __restrict__ b, T* __restrict__ x0,
                                 T* __restrict__ r, const int* done) {
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int s = i >> 5, lane = i & 31;
-    const int len = ms_len[s], base = ms_ptr[s] + lane;
-    const T bi = b[i];
-    const T xi = bi / dl1[i];
-    T acc = diag[i] * xi;
-    for (int j = 0; j < len; ++j) {
-      const int c = __ldg(&mnb[base + 32 * j]);
-      acc += __ldg(&coef[base + 32 * j]) * (b[c] / dl1[c]);
-    }
-    x0[i] = xi;
-    r[i] = bi - acc;
+    T xv, rv;
+    pre_resid_row(i, ms_ptr, ms_len, mnb, coef, diag, il1, b, xv, rv);
+    x0[i] = xv;
+    r[i] = rv;
   }
 }
 // fused prolongation + post-smooth: t = x0 + w P x_c (on the fly for the row
@@ -482,22 +540,13 @@ __global__ void k_amg_pre_resid(int n, const int* __restrict__ ms_ptr, const int
 template <class T>
 __global__ void k_amg_prolong_smooth(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
                                      const int* __restrict__ mnb, const T* __restrict__ coef,
-                                     const T* __restrict__ diag, const T* __restrict__ dl1,
+                                     const T* __restrict__ diag, const T* __restrict__ il1,
                                      const int* __restrict__ agg, const T* __restrict__ xc, T w,
                                      const T* __restrict__ x0, const T* __restrict__ b, T* __restrict__ out,
                                      const int* done) {
   if (*done) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int s = i >> 5, lane = i & 31;
-    const int len = ms_len[s], base = ms_ptr[s] + lane;
-    const T ti = x0[i] + w * xc[agg[i]];
-    T acc = diag[i] * ti;
-    for (int j = 0; j < len; ++j) {
-      const int c = __ldg(&mnb[base + 32 * j]);
-      acc += __ldg(&coef[base + 32 * j]) * (x0[c] + w * xc[agg[c]]);
-    }
-    out[i] = ti + (b[i] - acc) / dl1[i];
-  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = prolong_smooth_row(i, ms_ptr, ms_len, mnb, coef, diag, il1, agg, xc, w, x0, b);
 }
 
 // x += e
@@ -510,27 +559,27 @@ __global__ void k_amg_add(int n, const T* __restrict__ e, T* __restrict__ x, con
 template <class P, class TB, class TO>
 __global__ void k_amg_smooth(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
                              const int* __restrict__ mnb, const P* __restrict__ coef, const P* __restrict__ diag,
-                             const P* __restrict__ dl1, const P* __restrict__ x, const TB* __restrict__ b,
+                             const P* __restrict__ il1, const P* __restrict__ x, const TB* __restrict__ b,
                              TO* __restrict__ out, const int* done) {
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    out[i] = (TO)(x[i] + ((P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x)) / dl1[i]);
+    out[i] = (TO)(x[i] + ((P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x)) * il1[i]);
 }
 // coarsest level: `sweeps` l1-Jacobi sweeps from zero, one block, in shared memory
 template <class P, class TB, class TO>
 __global__ void __launch_bounds__(1024) k_amg_coarse(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
                                                     const int* __restrict__ mnb, const P* __restrict__ coef,
-                                                    const P* __restrict__ diag, const P* __restrict__ dl1,
+                                                    const P* __restrict__ diag, const P* __restrict__ il1,
                                                     const TB* __restrict__ b, TO* __restrict__ xout, int sweeps,
                                                     const int* done) {
   if (*done) return;
   __shared__ P xs[2][kCoarseMax];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) xs[0][i] = (P)b[i] / dl1[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xs[0][i] = (P)b[i] * il1[i];
   __syncthreads();
   int cur = 0;
   for (int it = 1; it < sweeps; ++it) {
     for (int i = threadIdx.x; i < n; i += blockDim.x)
-      xs[cur ^ 1][i] = xs[cur][i] + ((P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, xs[cur])) / dl1[i];
+      xs[cur ^ 1][i] = xs[cur][i] + ((P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, xs[cur])) * il1[i];
     __syncthreads();
     cur ^= 1;
   }
@@ -556,12 +605,12 @@ __device__ void tail_cycle(cg::grid_group& g, const TailLevel<P>* __restrict__ L
   if (l == nlev - 1) {                      // coarsest: l1-Jacobi sweeps in block 0 (shared memory)
     if (blockIdx.x == 0) {
       __shared__ P xs[2][kCoarseMax];
-      for (int i = threadIdx.x; i < F.n; i += blockDim.x) xs[0][i] = b[i] / F.dl1[i];
+      for (int i = threadIdx.x; i < F.n; i += blockDim.x) xs[0][i] = b[i] * F.il1[i];
       __syncthreads();
       int cur = 0;
       for (int it = 1; it < sweeps; ++it) {
         for (int i = threadIdx.x; i < F.n; i += blockDim.x)
-          xs[cur ^ 1][i] = xs[cur][i] + (b[i] - row_apply(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, xs[cur])) / F.dl1[i];
+          xs[cur ^ 1][i] = xs[cur][i] + (b[i] - row_apply(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, xs[cur])) * F.il1[i];
         __syncthreads();
         cur ^= 1;
       }
@@ -572,17 +621,10 @@ __device__ void tail_cycle(cg::grid_group& g, const TailLevel<P>* __restrict__ L
   }
   const TailLevel<P>& C = L[l + 1];
   for (int i = tid; i < F.n; i += nt) {     // pre-smooth + residual (k_amg_pre_resid)
-    const int s = i >> 5, lane = i & 31;
-    const int len = F.ms_len[s], base = F.ms_ptr[s] + lane;
-    const P bi = b[i];
-    const P xi = bi / F.dl1[i];
-    P acc = F.diag[i] * xi;
-    for (int j = 0; j < len; ++j) {
-      const int c = F.mnb[base + 32 * j];
-      acc += F.coef[base + 32 * j] * (b[c] / F.dl1[c]);
-    }
-    F.t[i] = xi;
-    F.r[i] = bi - acc;
+    P xv, rv;
+    pre_resid_row(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, xv, rv);
+    F.t[i] = xv;
+    F.r[i] = rv;
   }
   g.sync();
   for (int I = tid; I < C.n; I += nt) {     // restriction (k_amg_restrict)
@@ -600,17 +642,8 @@ __device__ void tail_cycle(cg::grid_group& g, const TailLevel<P>* __restrict__ L
     for (int I = tid; I < C.n; I += nt) C.x[I] += C.e[I];
     g.sync();
   }
-  for (int i = tid; i < F.n; i += nt) {     // prolongation + post-smooth (k_amg_prolong_smooth)
-    const int s = i >> 5, lane = i & 31;
-    const int len = F.ms_len[s], base = F.ms_ptr[s] + lane;
-    const P ti = F.t[i] + w * C.x[F.agg[i]];
-    P acc = F.diag[i] * ti;
-    for (int j = 0; j < len; ++j) {
-      const int c = F.mnb[base + 32 * j];
-      acc += F.coef[base + 32 * j] * (F.t[c] + w * C.x[F.agg[c]]);
-    }
-    x[i] = ti + (b[i] - acc) / F.dl1[i];
-  }
+  for (int i = tid; i < F.n; i += nt)       // prolongation + post-smooth (k_amg_prolong_smooth)
+    x[i] = prolong_smooth_row(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.agg, C.x, w, F.t, b);
   g.sync();
 }
 
@@ -643,7 +676,7 @@ static dfvm_status setup_tail(AmgH<P>* A) {
   std::vector<TailLevel<P>> h(A->nlev);
   for (int k = 0; k < A->nlev; ++k) {
     const AmgLevelDev<P>& D = A->L[k];
-    h[k] = TailLevel<P>{D.n, D.ms_ptr, D.ms_len, D.mnb, D.coef, D.diag, D.dl1, D.agg, D.mem_ptr, D.mem,
+    h[k] = TailLevel<P>{D.n, D.ms_ptr, D.ms_len, D.mnb, D.coef, D.diag, D.il1, D.agg, D.mem_ptr, D.mem,
                         D.x, D.b, D.r, D.t, D.e, D.r2};
   }
   dfvm_status st;
@@ -664,7 +697,7 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
     k_amg_cvt<P, T><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, pdiag, L0.diag_own);
     *nl += 2;
   }
-  k_dl1<P><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, L0.ms_ptr, L0.ms_len, L0.coef, L0.diag, L0.dl1);
+  k_il1<P><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, L0.ms_ptr, L0.ms_len, L0.coef, L0.diag, L0.il1);
   ++*nl;
   for (int l = 1; l < A->nlev; ++l) {
     AmgLevelDev<P>& F = A->L[l - 1];
@@ -672,7 +705,7 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
     k_gal_off<P><<<grid_for(C.n_sell), kThreads, 0, s>>>(C.n_sell, C.gal_ptr, C.gal_idx, F.coef, C.coef_own);
     k_gal_diag<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, C.dg_ptr, C.dg_idx, F.diag, F.coef,
                                                       C.diag_own);
-    k_dl1<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.coef, C.diag, C.dl1);
+    k_il1<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.coef, C.diag, C.il1);
     *nl += 3;
   }
   DFVM_CUDA(cudaGetLastError());
@@ -705,13 +738,13 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
     return;
   }
   if (l == A->nlev - 1) {
-    k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b, x,
+    k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, x,
                                              A->prm.sweeps, done);
     ++*nl;
     return;
   }
   AmgLevelDev<P>& C = A->L[l + 1];
-  k_amg_pre_resid<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, b,
+  k_amg_pre_resid<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b,
                                                          F.t, F.r, done);
   k_amg_restrict<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
   *nl += 2;
@@ -724,7 +757,7 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
     *nl += 2;
   }
   k_amg_prolong_smooth<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag,
-                                                              F.dl1, F.agg, C.x, (P)A->prm.omega, F.t, b, x, done);
+                                                              F.il1, F.agg, C.x, (P)A->prm.omega, F.t, b, x, done);
   ++*nl;
 }
 
@@ -740,16 +773,16 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   dfvm_status e;
   if (A->nlev == 1) {
     if (A->m->part.P > 1) {   // single level with ghost columns: one l1-Jacobi step
-      k_amg_pre<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.dl1, z, done);
+      k_amg_pre<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.il1, z, done);
     } else {
-      k_amg_coarse<P, T, T><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1, r, z,
+      k_amg_coarse<P, T, T><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, r, z,
                                                A->prm.sweeps, done);
     }
     ++*nl;
     return DFVM_OK;
   }
   AmgLevelDev<P>& C = A->L[1];
-  k_amg_pre<P, T, P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.dl1, F.x, done);
+  k_amg_pre<P, T, P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.il1, F.x, done);
   if ((e = halo_exchange_p(A->m, F.x, 1, f64, s))) return e;
   if (ev) cudaEventRecord(ev[0], s);
   k_amg_resid<P, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.x, r, F.r,
@@ -768,7 +801,7 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   k_amg_prolong<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, F.x, F.t, (P)A->prm.omega, done);
   if ((e = halo_exchange_p(A->m, F.t, 1, f64, s))) return e;
   if (ev) cudaEventRecord(ev[2], s);
-  k_amg_smooth<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.dl1,
+  k_amg_smooth<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1,
                                                            F.t, r, z, done);
   if (ev) cudaEventRecord(ev[3], s);
   *nl += 2;

@@ -815,7 +815,13 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(DevMesh<T> M, const T* __r
   if (grid_sum<6>(a, partials, ticket, t)) red_finish<6>(red, CTL_BI_INIT, ctl, t);
 }
 
-// p = r + beta (p - omega v); y = p / diag
+// 1 / diag for own + ghost rows (the Jacobi preconditioner applied as a product)
+template <class T>
+__global__ void k_recip(int n, const T* __restrict__ d, T* __restrict__ di) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) di[i] = T(1) / d[i];
+}
+
+// p = r + beta (p - omega v); y = p / diag   (dinv = 1 / diag)
 template <class T>
 __global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ diag, const T* __restrict__ v,
                        T* __restrict__ p, T* __restrict__ y, const KCtl* ctl) {
@@ -836,7 +842,7 @@ __global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ dia
       const int64_t j = 3 * (int64_t)i + k;
       const T pp = r[j] + beta[k] * (p[j] - om[k] * v[j]);
       p[j] = pp;
-      y[j] = pp / d;
+      y[j] = pp * d;
     }
   }
 }
@@ -891,7 +897,7 @@ __global__ void k_bi_s(int n, const T* __restrict__ r, const T* __restrict__ v, 
   if (grid_sum<3>(a, partials, ticket, t)) red_finish<3>(red, CTL_BI_S, ctl, t);
 }
 
-// t = A (s / diag); partials (t, s), (t, t) -> omega
+// t = A (s / diag); partials (t, s), (t, t) -> omega   (diag argument = 1 / diag)
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_bi_t(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ coef, const T* __restrict__ sv, T* __restrict__ tv, double* partials, unsigned* ticket,
@@ -907,13 +913,30 @@ __global__ void __launch_bounds__(kThreads) k_bi_t(DevMesh<T> M, const T* __rest
       for (int k = 0; k < 3; ++k) acc[k] = sv[3 * (int64_t)row + k];   // diag * (s / diag)
     const int len = __ldg(&M.ms_len[s]);
     const int base = __ldg(&M.ms_ptr[s]) + lane;
-    for (int j = 0; j < len; ++j) {
+    int j = 0;
+    for (; j + 4 <= len; j += 4) {       // batched: columns + coefficients, then gathers, then FMAs
+      T c[4], dn[4], sn[4][3];
+      int nn[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { c[u] = __ldg(&coef[base + 32 * (j + u)]); nn[u] = __ldg(&M.mnb[base + 32 * (j + u)]); }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        dn[u] = diag[nn[u]];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) sn[u][k] = sv[3 * (int64_t)nn[u] + k];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += c[u] * (sn[u][k] * dn[u]);
+    }
+    for (; j < len; ++j) {
       const int idx = base + 32 * j;
       const T c = coef[idx];
       const int nn = __ldg(&M.mnb[idx]);
       const T dn = diag[nn];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) acc[k] += c * (sv[3 * (int64_t)nn + k] / dn);
+      for (int k = 0; k < 3; ++k) acc[k] += c * (sv[3 * (int64_t)nn + k] * dn);
     }
     if (live)
 #pragma unroll
@@ -928,7 +951,7 @@ __global__ void __launch_bounds__(kThreads) k_bi_t(DevMesh<T> M, const T* __rest
   if (grid_sum<6>(a, partials, ticket, t)) red_finish<6>(red, CTL_BI_T, ctl, t);
 }
 
-// x += alpha y + omega s/diag; r = s - omega t; partials (rh, r), (r, r)
+// x += alpha y + omega s/diag; r = s - omega t; partials (rh, r), (r, r)   (diag argument = 1 / diag)
 template <class T>
 __global__ void k_bi_x(int n, const T* __restrict__ diag, const T* __restrict__ y, const T* __restrict__ sv,
                        const T* __restrict__ tv, const T* __restrict__ rh, T* __restrict__ x, T* __restrict__ r,
@@ -950,7 +973,7 @@ __global__ void k_bi_x(int n, const T* __restrict__ diag, const T* __restrict__ 
       if (mode[k] == 1) { x[j] += al[k] * y[j]; continue; }
       if (mode[k] != 2) continue;
       const T ss = sv[j];
-      x[j] += al[k] * y[j] + om[k] * (ss / d);
+      x[j] += al[k] * y[j] + om[k] * (ss * d);
       const T rr = ss - om[k] * tv[j];
       r[j] = rr;
       a[k] += (double)rh[j] * (double)rr;
@@ -971,7 +994,7 @@ struct SolverT : SolverBase {
   dfvm_mesh* m = nullptr;
   DevMesh<T>* M = nullptr;
   std::vector<void*> allocs;
-  T *gU = nullptr, *gp = nullptr, *bU = nullptr, *rhsU = nullptr, *udiag = nullptr, *ucoef = nullptr;
+  T *gU = nullptr, *gp = nullptr, *bU = nullptr, *rhsU = nullptr, *udiag = nullptr, *udinv = nullptr, *ucoef = nullptr;
   T *rAU = nullptr, *HbyA = nullptr, *phiHbyA = nullptr, *pcoef = nullptr, *pdiag = nullptr;
   T *prhs0 = nullptr, *prhs = nullptr;
   T *kr = nullptr, *krh = nullptr, *kp = nullptr, *kq = nullptr, *kv = nullptr, *ky = nullptr, *ks = nullptr, *kt = nullptr;
@@ -1036,7 +1059,7 @@ struct SolverT : SolverBase {
     const size_t nc = M->n_cells, no = M->n_own, nf = (size_t)M->F + M->B + M->E;
     dfvm_status st;
     if ((st = al(&gU, 9 * nc)) || (st = al(&gp, 3 * nc)) || (st = al(&bU, 3 * no)) || (st = al(&rhsU, 3 * no)) ||
-        (st = al(&udiag, nc)) || (st = al(&ucoef, (size_t)M->n_minc)) || (st = al(&rAU, nc)) ||
+        (st = al(&udiag, nc)) || (st = al(&udinv, nc)) || (st = al(&ucoef, (size_t)M->n_minc)) || (st = al(&rAU, nc)) ||
         (st = al(&HbyA, 3 * nc)) || (st = al(&phiHbyA, nf)) || (st = al(&pcoef, (size_t)M->n_minc)) ||
         (st = al(&pdiag, nc)) || (st = al(&prhs0, no)) || (st = al(&prhs, no)) || (st = al(&kr, 3 * nc)) ||
         (st = al(&krh, 3 * nc)) || (st = al(&kp, 3 * nc)) || (st = al(&kq, 3 * nc)) || (st = al(&kv, 3 * nc)) ||
@@ -1318,22 +1341,24 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   for (int k = 0; k < 3; ++k) { init[k].tol = tol; init[k].rel_tol = rel_tol; init[k].maxit = maxit; }
   DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, init, 3 * sizeof(KCtl), cudaMemcpyHostToDevice, st));
   dfvm_status e;
+  k_recip<T><<<grid_for(M.n_cells), kThreads, 0, st>>>(M.n_cells, X.udiag, X.udinv);
+  S->n_launch++;
   k_bi_init<T><<<grid_slices(k_bi_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr, X.krh,
                                                                           X.kp, X.kv, X.partials, X.ticket, X.d_ctl, red);
   S->n_launch++;
   if ((e = fin(S, X, CTL_BI_INIT, 6, st))) return e;
   for (;;) {
     for (int k = 0; k < kChunk; ++k) {
-      k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.udiag, X.kv, X.kp, X.ky, X.d_ctl);
+      k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.udinv, X.kv, X.kp, X.ky, X.d_ctl);
       if ((e = halo_exchange(m, X.ky, 3, st))) return e;
       k_bi_v<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.ky, X.krh, X.kv, X.partials, X.ticket, X.d_ctl, red);
       if ((e = fin(S, X, CTL_BI_V, 3, st))) return e;
       k_bi_s<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.ks, X.partials, X.ticket, X.d_ctl, red);
       if ((e = fin(S, X, CTL_BI_S, 3, st))) return e;
       if ((e = halo_exchange(m, X.ks, 3, st))) return e;
-      k_bi_t<T><<<gt, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.ks, X.kt, X.partials, X.ticket, X.d_ctl, red);
+      k_bi_t<T><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.ks, X.kt, X.partials, X.ticket, X.d_ctl, red);
       if ((e = fin(S, X, CTL_BI_T, 6, st))) return e;
-      k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udiag, X.ky, X.ks, X.kt, X.krh, x, X.kr, X.partials, X.ticket,
+      k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.ky, X.ks, X.kt, X.krh, x, X.kr, X.partials, X.ticket,
                                          X.d_ctl, red);
       if ((e = fin(S, X, CTL_BI_X, 6, st))) return e;
       S->n_launch += 5;
