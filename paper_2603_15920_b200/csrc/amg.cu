@@ -44,6 +44,7 @@ dfvm_status halo_exchange_p(dfvm_mesh* m, void* data, int nc, bool f64, cudaStre
 bool comm_is_local(const dfvm_comm* c);
 
 constexpr int kCoarseMax = 2048;     // shared-memory capacity of the one-block coarse solve
+constexpr int kDirectMax = 512;      // largest coarsest level solved with a dense inverse
 constexpr int kMaxLevels = 16;
 
 // Tunables (defaults chosen from B200 measurements on the C5 pipe, DESIGN.md
@@ -58,13 +59,21 @@ constexpr int kMaxLevels = 16;
 //                    < 2 keeps M SPD with adjoint smoothers)   default 1.8
 //   DFVM_AMG_TAIL    levels with <= this many rows (below level 0) run as
 //                    one cooperative kernel with grid-wide barriers instead
-//                    of one launch per phase (0: off)           default 131072
+//                    of one launch per phase (0: off)           default 0
+//                    (measured on B200, C5: the barrier-separated phases
+//                    ran 2x slower than the launched kernels, 406 vs ~195 us
+//                    per level-3 visit; kept as an option)
+//   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
+//                    exactly with a dense inverse (Gauss-Jordan once per
+//                    matrix update, one block), larger ones with
+//                    DFVM_AMG_SWEEPS l1-Jacobi sweeps (0: always sweeps)  default 512
 struct AmgParams {
-  int coarse = 256, sweeps = 32, wmax = 4, tail = 131072;
+  int coarse = 256, sweeps = 32, wmax = 4, tail = 0, direct = kDirectMax;
   bool wcycle = true;
   double omega = 1.8;
   AmgParams() {
     if (const char* e = getenv("DFVM_AMG_TAIL")) tail = std::max(0, atoi(e));
+    if (const char* e = getenv("DFVM_AMG_DIRECT")) direct = std::max(0, std::min(kDirectMax, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_OMEGA")) omega = atof(e);
     if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kCoarseMax, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_SWEEPS")) sweeps = std::max(1, atoi(e));
@@ -177,6 +186,7 @@ struct AmgH {
   AmgParams prm;
   AmgLevelDev<P> L[kMaxLevels];
   int tail = 0;                     // first level run by the cooperative tail kernel (0: none)
+  P* ainv = nullptr;                // dense inverse of the coarsest matrix (column-major n x n), or NULL
   int tail_grid = 0;
   TailLevel<P>* d_tail = nullptr;
   std::vector<void*> allocs;
@@ -321,6 +331,8 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     ++lev;
   }
   A->nlev = lev + 1;
+  const int nc = A->L[lev].n;
+  if (lev > 0 && nc <= A->prm.direct && (st = A->zalloc(&A->ainv, (size_t)nc * nc))) return st;
   return DFVM_OK;
 }
 
@@ -586,6 +598,61 @@ __global__ void __launch_bounds__(1024) k_amg_coarse(int n, const int* __restric
   for (int i = threadIdx.x; i < n; i += blockDim.x) xout[i] = (TO)xs[cur][i];
 }
 
+// Dense inverse of the coarsest matrix, one block: densify the SELL rows,
+// then in-place Gauss-Jordan without pivoting (the Galerkin coarse matrix of
+// an SPD operator is SPD).  Step k: row k <- row k / a_kk (with a_kk <- 1 first),
+// row i <- row i - a_ik row k (with a_ik <- 0 first).
+template <class P>
+__global__ void __launch_bounds__(1024) k_amg_dense_inv(int n, const int* __restrict__ ms_ptr,
+                                                        const int* __restrict__ ms_len, const int* __restrict__ mnb,
+                                                        const P* __restrict__ coef, const P* __restrict__ diag,
+                                                        P* __restrict__ A) {
+  __shared__ P colk[kDirectMax], rowk[kDirectMax];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) A[e] = P(0);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {      // thread i owns row i
+    A[(size_t)i * n + i] = diag[i];
+    const int s = i >> 5, lane = i & 31;
+    for (int j = 0; j < ms_len[s]; ++j) {
+      const int p = ms_ptr[s] + 32 * j + lane;
+      A[(size_t)i * n + mnb[p]] += coef[p];
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    const P piv = A[(size_t)k * n + k];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      colk[i] = A[(size_t)i * n + k];
+      rowk[i] = (i == k ? P(1) : A[(size_t)k * n + i]) / piv;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      const P a = A[e];
+      A[e] = (i == k) ? rowk[j] : ((j == k ? P(0) : a) - colk[i] * rowk[j]);
+    }
+    __syncthreads();
+  }
+}
+
+// coarsest solve with the dense inverse: x_i = sum_j Ainv_ij b_j (one block;
+// Ainv is symmetric, read column-wise for coalescing)
+template <class P, class TB, class TO>
+__device__ __forceinline__ void dense_solve_block(int n, const P* __restrict__ Ai, const TB* __restrict__ b,
+                                                  TO* __restrict__ x) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    P acc = P(0);
+    for (int j = 0; j < n; ++j) acc += Ai[(size_t)j * n + i] * (P)b[j];
+    x[i] = (TO)acc;
+  }
+}
+template <class P, class TB, class TO>
+__global__ void __launch_bounds__(1024) k_amg_dense(int n, const P* __restrict__ Ai, const TB* __restrict__ b,
+                                                    TO* __restrict__ x, const int* done) {
+  if (*done) return;
+  dense_solve_block<P, TB, TO>(n, Ai, b, x);
+}
+
 // ------------------------------------------------------------ cooperative tail
 // The deep levels (a few thousand to ~1e5 rows) are launch-bound: one
 // W-cycle visit of a level below ~1e5 rows is a dozen launches of 3-30 us
@@ -599,11 +666,12 @@ constexpr int kTailThreads = 512;
 
 template <class P>
 __device__ void tail_cycle(cg::grid_group& g, const TailLevel<P>* __restrict__ L, int l, int nlev, const P* b, P* x,
-                           P w, int sweeps, int wc, int wmax) {
+                           P w, int sweeps, int wc, int wmax, const P* ainv) {
   const TailLevel<P>& F = L[l];
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
-  if (l == nlev - 1) {                      // coarsest: l1-Jacobi sweeps in block 0 (shared memory)
-    if (blockIdx.x == 0) {
+  if (l == nlev - 1) {                      // coarsest: dense inverse, or l1-Jacobi sweeps in block 0
+    if (blockIdx.x == 0 && ainv) dense_solve_block<P, P, P>(F.n, ainv, b, x);
+    if (blockIdx.x == 0 && !ainv) {
       __shared__ P xs[2][kCoarseMax];
       for (int i = threadIdx.x; i < F.n; i += blockDim.x) xs[0][i] = b[i] * F.il1[i];
       __syncthreads();
@@ -633,12 +701,12 @@ __device__ void tail_cycle(cg::grid_group& g, const TailLevel<P>* __restrict__ L
     C.b[I] = sum;
   }
   g.sync();
-  tail_cycle(g, L, l + 1, nlev, C.b, C.x, w, sweeps, wc, wmax);
+  tail_cycle(g, L, l + 1, nlev, C.b, C.x, w, sweeps, wc, wmax, ainv);
   if (wc && l + 1 < nlev - 1 && l + 1 <= wmax) {
     for (int I = tid; I < C.n; I += nt)     // second visit (k_amg_resid, k_amg_add)
       C.r2[I] = C.b[I] - row_apply(I, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x);
     g.sync();
-    tail_cycle(g, L, l + 1, nlev, C.r2, C.e, w, sweeps, wc, wmax);
+    tail_cycle(g, L, l + 1, nlev, C.r2, C.e, w, sweeps, wc, wmax, ainv);
     for (int I = tid; I < C.n; I += nt) C.x[I] += C.e[I];
     g.sync();
   }
@@ -650,10 +718,10 @@ __device__ void tail_cycle(cg::grid_group& g, const TailLevel<P>* __restrict__ L
 template <class P>
 __global__ void __launch_bounds__(kTailThreads) k_amg_tail(const TailLevel<P>* __restrict__ L, int l, int nlev,
                                                           const P* b, P* x, P w, int sweeps, int wc, int wmax,
-                                                          const int* done) {
+                                                          const P* ainv, const int* done) {
   if (*done) return;
   cg::grid_group g = cg::this_grid();
-  tail_cycle(g, L, l, nlev, b, x, w, sweeps, wc, wmax);
+  tail_cycle(g, L, l, nlev, b, x, w, sweeps, wc, wmax, ainv);
 }
 
 template <class P>
@@ -708,6 +776,11 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
     k_il1<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.coef, C.diag, C.il1);
     *nl += 3;
   }
+  if (A->ainv) {
+    const AmgLevelDev<P>& C = A->L[A->nlev - 1];
+    k_amg_dense_inv<P><<<1, 1024, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, A->ainv);
+    ++*nl;
+  }
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
 }
@@ -731,15 +804,17 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
     const TailLevel<P>* d = A->d_tail;
     int nlev = A->nlev, sweeps = A->prm.sweeps, wc = A->prm.wcycle ? 1 : 0, wmax = A->prm.wmax;
     P w = (P)A->prm.omega;
+    const P* ai = A->ainv;
     void* args[] = {(void*)&d, (void*)&l, (void*)&nlev, (void*)&b, (void*)&x, (void*)&w, (void*)&sweeps, (void*)&wc,
-                    (void*)&wmax, (void*)&done};
+                    (void*)&wmax, (void*)&ai, (void*)&done};
     cudaLaunchCooperativeKernel((const void*)k_amg_tail<P>, dim3(A->tail_grid), dim3(kTailThreads), args, 0, s);
     ++*nl;
     return;
   }
   if (l == A->nlev - 1) {
-    k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, x,
-                                             A->prm.sweeps, done);
+    if (A->ainv) k_amg_dense<P, P, P><<<1, 1024, 0, s>>>(F.n, A->ainv, b, x, done);
+    else k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, x,
+                                                  A->prm.sweeps, done);
     ++*nl;
     return;
   }

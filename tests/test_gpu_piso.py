@@ -313,3 +313,20 @@ def test_amg_cooperative_tail_bitwise(precond, monkeypatch):
         out.append((pg.get(), r["it"], len(Sg.amg_levels())))
     assert out[0][2] >= 3
     assert out[0][1] == out[1][1] and np.array_equal(out[0][0], out[1][0])
+
+
+@pytest.mark.parametrize("direct", ["0", "512"])
+def test_amg_coarsest_direct_or_sweeps(direct, monkeypatch):
+    # coarsest AMG level solved by a dense inverse (default) or by l1-Jacobi
+    # sweeps: the converged pressure is the same discrete solution (A-14')
+    monkeypatch.setenv("DFVM_AMG_DIRECT", direct)
+    raw, mo, mg, bo, bg, kw = pipe_case(n=8, m_r=4, n_z=40)
+    So = oracle.Solver(mo, bo, **kw)
+    Sg = dfvm.Solver(mg, bg, p_precond="amg", **kw)
+    rAU = 0.01 * (1.5 + 0.5 * synth.cell_field(60, mo.N))
+    rhs = 1e-3 * synth.cell_field(61, mo.N)
+    po, ro = So.pressure_solve(rAU, rhs, p0=np.zeros(mo.N), tol=1e-14)
+    pg = mg.field("cells", 1)
+    rg = Sg.pressure_solve(mg.field("cells", 1, rAU), mg.field("cells", 1, rhs), pg, tol=1e-14)
+    assert rg["converged"] and len(Sg.amg_levels()) >= 2
+    assert rel_l2(pg.get(), po) <= 1e-8
