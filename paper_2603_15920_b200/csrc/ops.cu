@@ -116,6 +116,7 @@ template <class T, int NC, bool FACEVALS>
 __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __restrict__ x,
                                                    const uint8_t* __restrict__ bkind, const T* __restrict__ bval,
                                                    const T* __restrict__ fv, T* __restrict__ G) {
+  constexpr int KB = NC == 1 ? kB : 2;     // batch depth: register budget of the 3-component case
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.n_slices; s += nw) {
@@ -129,14 +130,14 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
     for (int k = 0; k < NC; ++k) acc[k][0] = acc[k][1] = acc[k][2] = T(0);
     const int len = __ldg(&M.sl_len[s]);
     const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
-    for (int j0 = 0; j0 < len; j0 += kB) {
-      int2 en[kB];
+    for (int j0 = 0; j0 < len; j0 += KB) {
+      int2 en[KB];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
-      V4<T> g[kB];
-      T v[kB][NC];
+      for (int u = 0; u < KB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
+      V4<T> g[KB];
+      T v[KB][NC];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) {
+      for (int u = 0; u < KB; ++u) {
         g[u] = V4<T>{T(0), T(0), T(0), T(0)};
 #pragma unroll
         for (int k = 0; k < NC; ++k) v[u][k] = T(0);
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
         }
       }
 #pragma unroll
-      for (int u = 0; u < kB; ++u) {
+      for (int u = 0; u < KB; ++u) {
         if (en[u].y >= 0) {
           const bool own = en[u].x >= 0;
           const T sg = own ? T(1) : T(-1);
@@ -230,6 +231,7 @@ template <class T, bool GAMMA>
 __global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restrict__ gamma, const T* __restrict__ x,
                                                   const T* __restrict__ G, const uint8_t* __restrict__ bkind,
                                                   const T* __restrict__ bval, T* __restrict__ y) {
+  constexpr int KB = 2;                    // batch depth (9 gathered values per incidence)
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.n_slices; s += nw) {
@@ -242,14 +244,14 @@ __global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restr
     T acc = T(0);
     const int len = __ldg(&M.sl_len[s]);
     const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
-    for (int j0 = 0; j0 < len; j0 += kB) {
-      int2 en[kB];
+    for (int j0 = 0; j0 < len; j0 += KB) {
+      int2 en[KB];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
-      T w[kB], xn[kB], Gn[kB][3], gn[kB];
-      V4<T> c[kB];
+      for (int u = 0; u < KB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
+      T w[KB], xn[KB], Gn[KB][3], gn[KB];
+      V4<T> c[KB];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) {
+      for (int u = 0; u < KB; ++u) {
         w[u] = xn[u] = gn[u] = T(0);
         Gn[u][0] = Gn[u][1] = Gn[u][2] = T(0);
         c[u] = V4<T>{T(0), T(0), T(0), T(0)};
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restr
         }
       }
 #pragma unroll
-      for (int u = 0; u < kB; ++u) {
+      for (int u = 0; u < KB; ++u) {
         if (en[u].y >= 0) {
           const bool own = en[u].x >= 0;
           const T wO = w[u], wN = T(1) - w[u];
