@@ -205,8 +205,8 @@ def main():
     ap.add_argument("--config", default="c5", choices=["c5", "c4", "c2", "c1"])
     ap.add_argument("--nz", type=int, default=None, help="override C5 axial layers (814 = 50.0M cells)")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--precond", default="amg", choices=["jacobi", "amg", "amg32"],
-                    help="pressure CG preconditioner (jacobi: A-14; amg: SURVEY NEXT-2)")
+    ap.add_argument("--precond", default="amg32", choices=["jacobi", "amg", "amg32"],
+                    help="pressure CG preconditioner (jacobi: A-14; amg: SURVEY NEXT-2 aggregation AMG in the solver precision; amg32: the same hierarchy in fp32 under the fp64 PCG, A-38)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-operators", action="store_true", help="skip the FVM operator-apply GB/s section")

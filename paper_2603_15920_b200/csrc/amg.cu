@@ -27,6 +27,7 @@
 //    vector in fp32; the PCG itself — residual, dots, x, p — stays fp64).
 //    Level 0 reads the PCG residual in T and writes z = M^-1 r in T.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -331,6 +332,11 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     ++lev;
   }
   A->nlev = lev + 1;
+  if (getenv("DFVM_AMG_VERBOSE"))
+    for (int k = 0; k <= lev; ++k)
+      fprintf(stderr, "[amg] level %d: rows %d, SELL slots %lld, entries %d (%.2f per row, padding %.1f %%)\n", k,
+              H[k].n, (long long)H[k].ms_ptr.back(), H[k].rp[H[k].n], (double)H[k].rp[H[k].n] / std::max(1, H[k].n),
+              100.0 * (1.0 - (double)H[k].rp[H[k].n] / std::max<double>(1.0, (double)H[k].ms_ptr.back())));
   const int nc = A->L[lev].n;
   if (lev > 0 && nc <= A->prm.direct && (st = A->zalloc(&A->ainv, (size_t)nc * nc))) return st;
   return DFVM_OK;
