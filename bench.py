@@ -387,6 +387,8 @@ def main():
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": args.precision, "data": "synthetic",
         "config": {"workload": case.name, "description": case.description, "cells": N, "precond": args.precond,
+                   "precond_dtype": ("f32" if args.precond == "amg32" else args.precision)
+                   if args.precond != "jacobi" else args.precision,
                    "internal_faces": info["n_internal_faces"], "parallelism": f"mesh-partition x{world} (RCM blocks)",
                    "l2_policy": "inputs larger than L2 (no flush)" if N > 2_000_000 else "L2-resident (small config)",
                    "solver": {k: v for k, v in case.solver.items()}},
