@@ -119,7 +119,26 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
   constexpr int KB = NC == 1 ? kB : 2;     // batch depth: register budget of the 3-component case
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.n_slices; s += nw) {
+  // software pipeline over the warp's slices: the next slice's metadata and
+  // first incidence batch are in flight while this slice's face records load
+  int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int len = 0;
+  const int2* e = M.inc;
+  int2 en[KB];
+  if (s < M.n_slices) {
+    len = __ldg(&M.sl_len[s]);
+    e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+  }
+#pragma unroll
+  for (int u = 0; u < KB; ++u) en[u] = (u < len) ? __ldg(&e[u * 32]) : make_int2(0, -2);
+  for (; s < M.n_slices; s += nw) {
+    const int sn = s + nw;
+    int len_n = 0;
+    const int2* e_n = M.inc;
+    if (sn < M.n_slices) {
+      len_n = __ldg(&M.sl_len[sn]);
+      e_n = M.inc + __ldg(&M.sl_ptr[sn]) + lane;
+    }
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
     T xc[NC];
@@ -128,12 +147,11 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
     T acc[NC][3];
 #pragma unroll
     for (int k = 0; k < NC; ++k) acc[k][0] = acc[k][1] = acc[k][2] = T(0);
-    const int len = __ldg(&M.sl_len[s]);
-    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+    int2 en_n[KB];
     for (int j0 = 0; j0 < len; j0 += KB) {
-      int2 en[KB];
+      if (j0 > 0)
 #pragma unroll
-      for (int u = 0; u < KB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
+        for (int u = 0; u < KB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
       V4<T> g[KB];
       T v[KB][NC];
 #pragma unroll
@@ -154,6 +172,9 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
             v[u][k] = FACEVALS ? fv[((int64_t)M.F + b) * NC + k] : (bkind[b] ? xc[k] : bval[(int64_t)b * NC + k]);
         }
       }
+      if (j0 + KB >= len)                    // last batch: prefetch the next slice's first batch
+#pragma unroll
+        for (int u = 0; u < KB; ++u) en_n[u] = (u < len_n) ? __ldg(&e_n[u * 32]) : make_int2(0, -2);
 #pragma unroll
       for (int u = 0; u < KB; ++u) {
         if (en[u].y >= 0) {
@@ -179,6 +200,9 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
         }
       }
     }
+    if (len == 0)
+#pragma unroll
+      for (int u = 0; u < KB; ++u) en_n[u] = (u < len_n) ? __ldg(&e_n[u * 32]) : make_int2(0, -2);
     if (live) {
       const T V = M.vol[row];
 #pragma unroll
@@ -186,6 +210,10 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
 #pragma unroll
         for (int l = 0; l < 3; ++l) G[(int64_t)row * 3 * NC + 3 * k + l] = acc[k][l] / V;
     }
+#pragma unroll
+    for (int u = 0; u < KB; ++u) en[u] = en_n[u];
+    len = len_n;
+    e = e_n;
   }
 }
 
@@ -234,7 +262,26 @@ __global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restr
   constexpr int KB = 2;                    // batch depth (9 gathered values per incidence)
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.n_slices; s += nw) {
+  // software pipeline over the warp's slices (as in k_grad)
+  int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int len = 0;
+  const int2* e = M.inc;
+  int2 en[KB];
+  if (s < M.n_slices) {
+    len = __ldg(&M.sl_len[s]);
+    e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+  }
+#pragma unroll
+  for (int u = 0; u < KB; ++u) en[u] = (u < len) ? __ldg(&e[u * 32]) : make_int2(0, -2);
+  for (; s < M.n_slices; s += nw) {
+    const int sn = s + nw;
+    int len_n = 0;
+    const int2* e_n = M.inc;
+    if (sn < M.n_slices) {
+      len_n = __ldg(&M.sl_len[sn]);
+      e_n = M.inc + __ldg(&M.sl_ptr[sn]) + lane;
+    }
+    int2 en_n[KB];
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
     const T xc = live ? x[row] : T(0);
@@ -242,12 +289,10 @@ __global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restr
     T Gc[3] = {T(0), T(0), T(0)};
     if (live) { Gc[0] = G[3 * (int64_t)row]; Gc[1] = G[3 * (int64_t)row + 1]; Gc[2] = G[3 * (int64_t)row + 2]; }
     T acc = T(0);
-    const int len = __ldg(&M.sl_len[s]);
-    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
     for (int j0 = 0; j0 < len; j0 += KB) {
-      int2 en[KB];
+      if (j0 > 0)
 #pragma unroll
-      for (int u = 0; u < KB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
+        for (int u = 0; u < KB; ++u) en[u] = (j0 + u < len) ? __ldg(&e[(j0 + u) * 32]) : make_int2(0, -2);
       T w[KB], xn[KB], Gn[KB][3], gn[KB];
       V4<T> c[KB];
 #pragma unroll
@@ -268,6 +313,9 @@ __global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restr
           if (bkind[b] == 0) { c[u].w = ld4(&M.bgeo[b]).w; xn[u] = bval[b]; }
         }
       }
+      if (j0 + KB >= len)                    // last batch: prefetch the next slice's first batch
+#pragma unroll
+        for (int u = 0; u < KB; ++u) en_n[u] = (u < len_n) ? __ldg(&e_n[u * 32]) : make_int2(0, -2);
 #pragma unroll
       for (int u = 0; u < KB; ++u) {
         if (en[u].y >= 0) {
@@ -286,7 +334,14 @@ __global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restr
         }
       }
     }
+    if (len == 0)
+#pragma unroll
+      for (int u = 0; u < KB; ++u) en_n[u] = (u < len_n) ? __ldg(&e_n[u * 32]) : make_int2(0, -2);
     if (live) y[row] = acc;
+#pragma unroll
+    for (int u = 0; u < KB; ++u) en[u] = en_n[u];
+    len = len_n;
+    e = e_n;
   }
 }
 
