@@ -74,6 +74,9 @@ def lib():
         L.orc_piso_step.argtypes = [vp, vp, vp, vp, vp]
         L.orc_momentum_assemble.argtypes = [vp] * 7
         L.orc_pressure_solve.argtypes = [vp, vp, vp, vp, f64, f64, i32, i32, vp]
+        L.orc_ldu_apply_transpose.argtypes = [vp] * 6
+        L.orc_pressure_adjoint.argtypes = [vp, vp, vp, vp, f64, i32, i32, vp]
+        L.orc_pressure_vjp.argtypes = [vp, vp, vp, vp, vp]
         L.orc_transport_step.argtypes = [vp, vp, vp, f64, vp]
         L.orc_poisson_steady.restype = i32
         L.orc_poisson_steady.argtypes = [vp, vp, vp, vp, f64, i32, i32, f64]
@@ -187,6 +190,13 @@ class Mesh:
         lib().orc_ldu_apply(self.h, *[_p(a) for a in keep], _p(y))
         return y
 
+    def ldu_apply_transpose(self, diag, lower, upper, x):
+        """y = A^T x (NEXT-3; written as a face scatter, independent of ldu_apply)."""
+        y = np.empty(self.N)
+        keep = [_f64(a) for a in (diag, lower, upper, x)]
+        lib().orc_ldu_apply_transpose(self.h, *[_p(a) for a in keep], _p(y))
+        return y
+
     def poisson_steady(self, bcs, src, phi0=None, picard_tol=1e-12, max_picard=200, direct=False, cg_tol=1e-15):
         phi = np.zeros(self.N) if phi0 is None else _f64(phi0).copy()
         src = _f64(src)
@@ -286,6 +296,22 @@ class Solver:
         st = lib().orc_pressure_solve(self.h, _p(rAU), _p(rhs), _p(p), tol, rel_tol, maxit,
                                       2 if direct else 0, _p(rep))
         return p, dict(it=int(rep[0]), res0=rep[1], res=rep[2], converged=bool(rep[3]), status=STATUS[st])
+
+
+    def pressure_adjoint(self, rAU, g, tol=1e-14, maxit=50000, direct=False):
+        """lambda with A_p(rAU)^T lambda = g (eq:implicit_diff P:366-370)."""
+        lam = np.zeros(self.mesh.N)
+        rep = np.zeros(4)
+        rAU, g = _f64(rAU), _f64(g)
+        st = lib().orc_pressure_adjoint(self.h, _p(rAU), _p(g), _p(lam), tol, maxit, 2 if direct else 0, _p(rep))
+        return lam, dict(it=int(rep[0]), res0=rep[1], res=rep[2], converged=bool(rep[3]), status=STATUS[st])
+
+    def pressure_vjp(self, rAU, p, lam):
+        """dL/drAU through the converged solve A(rAU) p = rhs, given lambda = A^-T dL/dp."""
+        out = np.empty(self.mesh.N)
+        rAU, p, lam = _f64(rAU), _f64(p), _f64(lam)
+        _check(lib().orc_pressure_vjp(self.h, _p(rAU), _p(p), _p(lam), _p(out)))
+        return out
 
 
 def parse_report(rep):

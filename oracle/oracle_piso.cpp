@@ -639,6 +639,82 @@ int orc_pressure_solve(void* sp, const double* rAU, const double* rhs_in, double
   return r.status;
 }
 
+// ------------------------------------------------------------- NEXT-3
+// Adjoint (transposed) LDU apply, written as the definition
+// (A^T x)_c = sum_r A_rc x_r over the faces (a scatter, unlike ldu_apply's
+// gather): A_ON = upper_f sends x_O to row N, A_NO = lower_f sends x_N to
+// row O (the transpose apply behind eq:vjp P:352-358).
+int orc_ldu_apply_transpose(const void* mp, const double* diag, const double* lower, const double* upper,
+                            const double* x, double* y) {
+  const Mesh& m = *(const Mesh*)mp;
+  for (int64_t c = 0; c < m.N; ++c) y[c] = diag[c] * x[c];
+  for (int64_t f = 0; f < m.F; ++f) {
+    const int64_t O = m.owner[f], N = m.neigh[f];
+    y[N] += upper[f] * x[O];
+    y[O] += lower[f] * x[N];
+  }
+  return OK;
+}
+
+// Adjoint pressure solve of the implicit differentiation (eq:implicit_diff
+// P:366-370): (dF/dp)^T lambda = g with F(p) = A_p(rAU) p - rhs, i.e. the
+// transposed pressure matrix (gauge of A-12 included), solved "using the same
+// iterative solver as the forward pass" (CG; mode 2: dense LU).
+int orc_pressure_adjoint(void* sp, const double* rAU, const double* g, double* lambda, double tol, int maxit,
+                         int mode, double* rep) {
+  Solver* S = (Solver*)sp;
+  const Mesh& m = *S->m;
+  LDU A; std::vector<double> cf, cb;
+  pressure_matrix(*S, rAU, A, cf, cb);
+  std::vector<double> rhs(m.N, 0.0);
+  if (!has_fixed_p(*S)) apply_reference(*S, A, rhs.data());   // only the matrix part matters here
+  LDU At;
+  At.diag = A.diag; At.lower = A.upper; At.upper = A.lower;    // transpose: swap the off-diagonal halves
+  std::vector<double> gg(g, g + m.N);
+  SolveReport r = mode == 2 ? dense_solve(m, At, gg.data(), lambda) : cg(m, At, gg.data(), lambda, tol, 0.0, maxit);
+  rep[0] = r.it; rep[1] = r.res0; rep[2] = r.res; rep[3] = r.converged;
+  return r.status;
+}
+
+// Gradient of L with respect to rAU through a converged pressure solve
+// A(rAU) p = rhs(rAU) (implicit function theorem, eq:implicit_diff):
+//   dL/dtheta = lambda^T (d rhs/dtheta - (dA/dtheta) p),  A^T lambda = dL/dp.
+// Per face coefficient (pressure_matrix): c_f = (w rAU_O + (1-w) rAU_N) delta_f
+// enters rows O and N as c_f (p_O - p_N) and (p_N - p_O):
+//   dL/dc_f = -(lambda_O - lambda_N) (p_O - p_N);
+// a fixed-value boundary face, c_b = rAU_O delta_b, enters row O of A as
+// c_b p_O (rhs, which holds its c_b p_b part, is an input of the solve and
+// held fixed): dL/dc_b = -lambda_O p_O;
+// with the gauge (A-12, no fixed-value p): A_rr -> 2 A_rr and rhs_r += A_rr p_ref,
+// so every coefficient in A_rr adds lambda_r (p_ref - p_r).
+// Chain rule to rAU: dc_f/drAU_O = w delta_f, dc_f/drAU_N = (1-w) delta_f,
+// dc_b/drAU_O = delta_b.  (rhs — divergence, non-orthogonal correction,
+// boundary values — is the solve's input and held fixed, as in
+// orc_pressure_solve; the gauge's rhs term is part of the solve.)
+int orc_pressure_vjp(void* sp, const double* rAU, const double* p, const double* lambda, double* grad) {
+  Solver* S = (Solver*)sp;
+  const Mesh& m = *S->m;
+  BCs& b = *S->b;
+  (void)rAU;
+  const bool gauge = !has_fixed_p(*S);
+  const int64_t r = S->o.p_ref_cell;
+  for (int64_t c = 0; c < m.N; ++c) grad[c] = 0.0;
+  for (int64_t f = 0; f < m.F; ++f) {
+    const int64_t O = m.owner[f], N = m.neigh[f];
+    double d = -(lambda[O] - lambda[N]) * (p[O] - p[N]);
+    if (gauge && (O == r || N == r)) d += lambda[r] * (S->o.p_ref_value - p[r]);
+    grad[O] += d * m.w[f] * m.delta[f];
+    grad[N] += d * (1.0 - m.w[f]) * m.delta[f];
+  }
+  for (int64_t f = m.F; f < m.NF; ++f) {
+    const int pt = m.face_patch[f - m.F];
+    if (m.pkind[pt] == PK_EMPTY || !is_fixed(b, 1, pt)) continue;
+    const int64_t O = m.owner[f];
+    grad[O] += -lambda[O] * p[O] * m.delta_b[f - m.F];
+  }
+  return OK;
+}
+
 // Steady Poisson pin (E1, eq:poisson_3d P:445-448) with field 's' BCs:
 // sum_f s[delta (phi_N - phi_O) + k . grad phi_f] + sum_b delta_b (phi_b - phi_c) = src_c
 // where src_c = f(x_c) V_c (A-33).  Two-point part implicit, correction
