@@ -284,6 +284,30 @@ dfvm_status dfvm_momentum_assemble(dfvm_solver* s, const dfvm_field* U, const df
                                    dfvm_field* b, dfvm_stream stream);
 /* y = M x with the last assembled momentum matrix, x, y: [cells][3] */
 dfvm_status dfvm_momentum_apply(dfvm_solver* s, const dfvm_field* x, dfvm_field* y, dfvm_stream stream);
+/* ---- NEXT-3: adjoint pieces of the implicit differentiation (
+ * eq:vjp P:352-358, eq:implicit_diff P:366-370) ---- */
+/* y = M^T x with the last assembled momentum (or transport) matrix, x, y:
+ * [cells][3]; the transposed coefficients are written by the assembly (for
+ * each incidence, the coefficient the other row holds for this face). */
+dfvm_status dfvm_momentum_apply_transpose(dfvm_solver* s, const dfvm_field* x, dfvm_field* y, dfvm_stream stream);
+/* Adjoint pressure solve A_p(rAU)^T lambda = g, "solved using the same
+ * iterative solver as the forward pass": A_p is symmetric (c_f enters
+ * both rows alike, the gauge of A-12 doubles a diagonal entry), so this is the
+ * forward PCG on the same coefficients with the adjoint right-hand side g
+ * (the gauge's right-hand-side term belongs to the forward system and is not
+ * added).  lambda: warm start in, solution out.  Errors as dfvm_pressure_solve. */
+dfvm_status dfvm_pressure_solve_adjoint(dfvm_solver* s, const dfvm_field* rAU, const dfvm_field* g, dfvm_field* lambda,
+                                        double tol, double rel_tol, int32_t maxit, dfvm_solve_report* rep,
+                                        dfvm_stream stream);
+/* Gradient of a loss through a converged pressure solve A_p(rAU) p = rhs
+ * (rhs held fixed, the gauge's term included): grad = dL/drAU [cells] from
+ * p and lambda = A_p^-T dL/dp (implicit function theorem, eq:implicit_diff):
+ * dL/dc_f = -(lambda_O - lambda_N)(p_O - p_N) per internal face (+ the gauge
+ * row's lambda_r (p_ref - p_r)), -lambda_O p_O per fixed-value boundary face,
+ * chained through c_f = (w rAU_O + (1-w) rAU_N) delta_f, c_b = rAU_O delta_b.
+ * The boundary conditions are the solver's ('p'). */
+dfvm_status dfvm_pressure_vjp(dfvm_solver* s, const dfvm_field* p, const dfvm_field* lambda, dfvm_field* grad,
+                              dfvm_stream stream);
 /* One implicit-Euler step of passive-scalar transport (NEXT-1; §3.1.2
  * P:477-491): dx/dt + div(phi x) - div(gamma grad x) = 0 with the face flux
  * phi [faces] fixed, field 's' boundary conditions, the solver's dt,

@@ -40,7 +40,7 @@ SYMBOLS = [
     "dfvm_momentum_assemble", "dfvm_momentum_apply", "dfvm_piso_step", "dfvm_windkessel_set",
     "dfvm_windkessel_state", "dfvm_windkessel_update", "dfvm_solver_destroy", "dfvm_kernel_launches",
     "dfvm_solver_set_timing", "dfvm_solver_get_timing", "dfvm_comm_create_local", "dfvm_solver_amg_levels",
-    "dfvm_transport_step",
+    "dfvm_transport_step", "dfvm_momentum_apply_transpose", "dfvm_pressure_solve_adjoint", "dfvm_pressure_vjp",
 ]
 
 
@@ -133,6 +133,9 @@ def lib():
         L.dfvm_pressure_solve.argtypes = [vp, vp, vp, vp, f64, f64, i32, C.POINTER(SolveReport), vp]
         L.dfvm_momentum_assemble.argtypes = [vp, vp, vp, vp, vp, vp]
         L.dfvm_momentum_apply.argtypes = [vp, vp, vp, vp]
+        L.dfvm_momentum_apply_transpose.argtypes = [vp, vp, vp, vp]
+        L.dfvm_pressure_solve_adjoint.argtypes = [vp, vp, vp, vp, f64, f64, i32, C.POINTER(SolveReport), vp]
+        L.dfvm_pressure_vjp.argtypes = [vp, vp, vp, vp, vp]
         L.dfvm_piso_step.argtypes = [vp, vp, vp, vp, C.POINTER(StepReport), vp]
         L.dfvm_windkessel_set.argtypes = [vp, i32, f64, f64, f64, f64, i32]
         L.dfvm_windkessel_state.argtypes = [vp, i32, C.POINTER(f64)]
@@ -451,6 +454,23 @@ class Solver:
         d = _rep(r)
         d["status"] = STATUS[st]
         return d
+
+    def pressure_solve_adjoint(self, rAU, g, lam, tol=1e-14, rel_tol=0.0, maxit=50000, stream=None):
+        """NEXT-3: A_p(rAU)^T lambda = g with the forward PCG (eq:implicit_diff P:366-370)."""
+        r = SolveReport()
+        st = _check(lib().dfvm_pressure_solve_adjoint(self.h, rAU.h, g.h, lam.h, tol, rel_tol, maxit, C.byref(r),
+                                                      stream), allow=(8,))
+        d = _rep(r)
+        d["status"] = STATUS[st]
+        return d
+
+    def pressure_vjp(self, p, lam, grad, stream=None):
+        """NEXT-3: grad = dL/drAU through the converged pressure solve, from p and lambda."""
+        _check(lib().dfvm_pressure_vjp(self.h, p.h, lam.h, grad.h, stream))
+
+    def momentum_apply_transpose(self, x, y, stream=None):
+        """NEXT-3: y = M^T x with the last assembled momentum matrix."""
+        _check(lib().dfvm_momentum_apply_transpose(self.h, x.h, y.h, stream))
 
     def transport_step(self, x, phi, gamma, stream=None):
         """One implicit passive-scalar transport step (field 's' BCs); x updated in place."""

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, c
     const T* __restrict__ phi, const T* __restrict__ gU, const T* __restrict__ gp, const uint8_t* __restrict__ bk,
     const T* __restrict__ bv, T nu, T rdt, int conv, int kcorr, const V4<T>* __restrict__ fdO,
     const V4<T>* __restrict__ fdN, T* __restrict__ udiag, T* __restrict__ bU, T* __restrict__ rhsU,
-    T* __restrict__ ucoef) {
+    T* __restrict__ ucoef, T* __restrict__ ucoefT) {
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
@@ -254,9 +254,10 @@ __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, c
         const T md = phi[f];
         const T lam = conv == 1 ? w : (md >= T(0) ? T(1) : T(0));
         const T nd = nu * c.w;
-        T cf;
-        if (own) { diag += lam * md + nd; cf = (T(1) - lam) * md - nd; }
-        else { diag += -(T(1) - lam) * md + nd; cf = -lam * md - nd; }
+        T cf, cfT;   // this row's coefficient and the transposed one (the other row's, NEXT-3)
+        if (own) { diag += lam * md + nd; cf = (T(1) - lam) * md - nd; cfT = -lam * md - nd; }
+        else { diag += -(T(1) - lam) * md + nd; cf = -lam * md - nd; cfT = (T(1) - lam) * md - nd; }
+        ucoefT[mbase + 32 * mj] = cfT;
         ucoef[mbase + 32 * (mj++)] = cf;
         const int n = en.y;
         const int O = own ? row : n, N = own ? n : row;
@@ -424,6 +425,47 @@ __global__ void __launch_bounds__(kThreads) k_pcoef(DevMesh<T> M, const T* __res
       pdiag[row] = diag;
       prhs0[row] = rhs;
     }
+  }
+}
+
+// NEXT-3, eq:implicit_diff P:366-370: dL/drAU through the converged solve
+// A(rAU) p = rhs given lambda = A^-T dL/dp (derivation: oracle
+// orc_pressure_vjp).  Per face dL/dc_f = -(lambda_O - lambda_N)(p_O - p_N)
+// (+ lambda_r (p_ref - p_r) if the face touches the gauge row r), split to
+// the rows by dc_f/drAU = (w, 1-w) delta_f; fixed-value boundary faces
+// -lambda_O p_O delta_b.  p, lambda need valid ghosts.
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_pvjp(DevMesh<T> M, const T* __restrict__ p, const T* __restrict__ lam,
+    const uint8_t* __restrict__ bkp, const int32_t* __restrict__ corig, int ref_orig, T p_ref, T* __restrict__ grad) {
+  SLICE_LOOP(M) {
+    const int row = s * 32 + lane;
+    const bool live = row < M.n_own;
+    const T pc = live ? p[row] : T(0), lc = live ? lam[row] : T(0);
+    const bool rc = live && ref_orig >= 0 && corig[row] == ref_orig;
+    T acc = T(0);
+    const int len = __ldg(&M.sl_len[s]);
+    const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
+    for (int j = 0; j < len; ++j) {
+      const int2 en = __ldg(&e[j * 32]);
+      if (en.y >= 0) {
+        const bool own = en.x >= 0;
+        const int f = own ? en.x : ~en.x;
+        const int n = en.y;
+        const T pn = p[n], ln = lam[n];
+        const T pO = own ? pc : pn, pN = own ? pn : pc, lO = own ? lc : ln, lN = own ? ln : lc;
+        T d = -(lO - lN) * (pO - pN);
+        if (ref_orig >= 0) {
+          if (rc) d += lc * (p_ref - pc);
+          else if (corig[n] == ref_orig) d += ln * (p_ref - pn);
+        }
+        const T w = __ldg(&M.fw[f]);
+        acc += d * (own ? w : T(1) - w) * ld4(&M.fcor[f]).w;
+      } else if (en.y == -1) {
+        const int b = en.x;
+        if (bkp[b] == 0) acc += -lc * pc * ld4(&M.bgeo[b]).w;
+      }
+    }
+    if (live) grad[row] = acc;
   }
 }
 
@@ -995,6 +1037,7 @@ struct SolverT : SolverBase {
   DevMesh<T>* M = nullptr;
   std::vector<void*> allocs;
   T *gU = nullptr, *gp = nullptr, *bU = nullptr, *rhsU = nullptr, *udiag = nullptr, *udinv = nullptr, *ucoef = nullptr;
+  T* ucoefT = nullptr;          // transposed momentum coefficients (NEXT-3 adjoint apply)
   T *rAU = nullptr, *HbyA = nullptr, *phiHbyA = nullptr, *pcoef = nullptr, *pdiag = nullptr;
   T *prhs0 = nullptr, *prhs = nullptr;
   T *kr = nullptr, *krh = nullptr, *kp = nullptr, *kq = nullptr, *kv = nullptr, *ky = nullptr, *ks = nullptr, *kt = nullptr;
@@ -1059,7 +1102,8 @@ struct SolverT : SolverBase {
     const size_t nc = M->n_cells, no = M->n_own, nf = (size_t)M->F + M->B + M->E;
     dfvm_status st;
     if ((st = al(&gU, 9 * nc)) || (st = al(&gp, 3 * nc)) || (st = al(&bU, 3 * no)) || (st = al(&rhsU, 3 * no)) ||
-        (st = al(&udiag, nc)) || (st = al(&udinv, nc)) || (st = al(&ucoef, (size_t)M->n_minc)) || (st = al(&rAU, nc)) ||
+        (st = al(&udiag, nc)) || (st = al(&udinv, nc)) || (st = al(&ucoef, (size_t)M->n_minc)) ||
+        (st = al(&ucoefT, (size_t)M->n_minc)) || (st = al(&rAU, nc)) ||
         (st = al(&HbyA, 3 * nc)) || (st = al(&phiHbyA, nf)) || (st = al(&pcoef, (size_t)M->n_minc)) ||
         (st = al(&pdiag, nc)) || (st = al(&prhs0, no)) || (st = al(&prhs, no)) || (st = al(&kr, 3 * nc)) ||
         (st = al(&krh, 3 * nc)) || (st = al(&kp, 3 * nc)) || (st = al(&kq, 3 * nc)) || (st = al(&kv, 3 * nc)) ||
@@ -1396,7 +1440,7 @@ static dfvm_status assemble(dfvm_solver* S, SolverT<T>& X, const T* U, const T* 
   if ((s2 = halo_exchange(S->m, X.gU, 9, st))) return s2;
   k_transport_assemble<T, 3><<<gs, kThreads, 0, st>>>(M, U, phi, X.gU, X.gp, b->d_kind[0], (const T*)b->d_val[0],
                                                       (T)S->o.nu, (T)(1.0 / S->o.dt), S->o.convection, S->kcorr,
-                                                      X.fdO, X.fdN, X.udiag, X.bU, X.rhsU, X.ucoef);
+                                                      X.fdO, X.fdN, X.udiag, X.bU, X.rhsU, X.ucoef, X.ucoefT);
   S->n_launch++;
   if ((s2 = halo_exchange(S->m, X.udiag, 1, st))) return s2;   // k_bi_t gathers s / diag
   X.assembled = true;
@@ -1540,7 +1584,7 @@ static dfvm_status transport_step_t(dfvm_solver* S, SolverT<T>& X, T* x, const T
   const int gs = grid_for_slices(M.n_slices), ge = grid_for(M.n_own);
   k_transport_assemble<T, 1><<<gs, kThreads, 0, st>>>(M, x, phi, X.gp, nullptr, b->d_kind[2], (const T*)b->d_val[2],
                                                       (T)gamma, (T)(1.0 / S->o.dt), S->o.convection, S->kcorr,
-                                                      X.fdO, X.fdN, X.udiag, X.prhs0, X.prhs, X.ucoef);
+                                                      X.fdO, X.fdN, X.udiag, X.prhs0, X.prhs, X.ucoef, X.ucoefT);
   if ((e = halo_exchange(S->m, X.udiag, 1, st))) return e;
   k_pack3<T><<<ge, kThreads, 0, st>>>(M.n_own, X.prhs, X.bU);
   k_pack3<T><<<grid_for(M.n_cells), kThreads, 0, st>>>(M.n_cells, x, X.HbyA);
@@ -1719,7 +1763,8 @@ dfvm_status dfvm_piso_step(dfvm_solver* s, dfvm_field* U, dfvm_field* p, dfvm_fi
 
 template <class T>
 static dfvm_status pressure_solve_t(dfvm_solver* s, SolverT<T>& X, const T* rAU, const T* rhs, T* p, double tol,
-                                    double rel_tol, int maxit, dfvm_solve_report* rep, cudaStream_t st) {
+                                    double rel_tol, int maxit, dfvm_solve_report* rep, cudaStream_t st,
+                                    bool adjoint = false) {
   DevMesh<T>& M = *X.M;
   dfvm_status s2;
   if ((s2 = bcs_device(s->b, 1, st))) return s2;
@@ -1733,8 +1778,11 @@ static dfvm_status pressure_solve_t(dfvm_solver* s, SolverT<T>& X, const T* rAU,
       (const T*)s->b->d_val[1], ref, (T)s->o.p_ref_value, X.pcoef, X.pdiag, X.prhs0);
   X.amg_dirty = true;
   DFVM_CUDA(cudaMemcpyAsync(X.prhs, rhs, (size_t)M.n_own * sizeof(T), cudaMemcpyDeviceToDevice, st));
-  if (ref >= 0) k_add_at<T><<<1, 1, 0, st>>>(X.prhs, X.prhs0, ref);
-  count_launch(1 + (ref >= 0));
+  // adjoint system A^T lambda = g: the gauge changes the matrix only (its
+  // right-hand-side term belongs to the forward system)
+  const bool add_ref = ref >= 0 && !adjoint;
+  if (add_ref) k_add_at<T><<<1, 1, 0, st>>>(X.prhs, X.prhs0, ref);
+  count_launch(1 + add_ref);
   s->n_launch = 0;
   dfvm_status r = run_cg(s, X, X.prhs, p, tol, rel_tol, maxit, rep, st);
   count_launch(s->n_launch);
@@ -1786,6 +1834,73 @@ dfvm_status dfvm_momentum_assemble(dfvm_solver* s, const dfvm_field* U, const df
     DFVM_CUDA(cudaMemcpyAsync(b->ptr, X.bU, (size_t)X.M->n_own * 3 * sizeof(float), cudaMemcpyDeviceToDevice, cs));
   }
   count_launch(s->n_launch);
+  return DFVM_OK;
+}
+
+// ---- NEXT-3: adjoint apply / adjoint pressure solve / pressure VJP
+dfvm_status dfvm_momentum_apply_transpose(dfvm_solver* s, const dfvm_field* x, dfvm_field* y, dfvm_stream stream) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  dfvm_status st;
+  if ((st = check_f(x, s->m, true, 3, "x")) || (st = check_f(y, s->m, true, 3, "y"))) return st;
+  cudaSetDevice(s->m->device);
+  cudaStream_t cs = (cudaStream_t)stream;
+  if ((st = halo_exchange(s->m, x->ptr, 3, cs))) return st;
+  if (s->m->precision == DFVM_F64) {
+    auto& X = *static_cast<SolverT<double>*>(s->impl.get());
+    if (!X.assembled) { set_error(DFVM_E_INVALID_ARG, "momentum matrix not assembled"); return DFVM_E_INVALID_ARG; }
+    k_apply<double, 3><<<grid_for_slices(X.M->n_slices), kThreads, 0, cs>>>(*X.M, X.udiag, X.ucoefT, (const double*)x->ptr, (double*)y->ptr);
+  } else {
+    auto& X = *static_cast<SolverT<float>*>(s->impl.get());
+    if (!X.assembled) { set_error(DFVM_E_INVALID_ARG, "momentum matrix not assembled"); return DFVM_E_INVALID_ARG; }
+    k_apply<float, 3><<<grid_for_slices(X.M->n_slices), kThreads, 0, cs>>>(*X.M, X.udiag, X.ucoefT, (const float*)x->ptr, (float*)y->ptr);
+  }
+  count_launch();
+  DFVM_CUDA(cudaGetLastError());
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_pressure_solve_adjoint(dfvm_solver* s, const dfvm_field* rAU, const dfvm_field* g, dfvm_field* lambda,
+                                        double tol, double rel_tol, int32_t maxit, dfvm_solve_report* rep,
+                                        dfvm_stream stream) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  dfvm_status st;
+  if ((st = check_f(rAU, s->m, true, 1, "rAU")) || (st = check_f(g, s->m, true, 1, "g")) ||
+      (st = check_f(lambda, s->m, true, 1, "lambda")))
+    return st;
+  cudaSetDevice(s->m->device);
+  s->fixed_p = solver_has_fixed_p(s);
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (s->m->precision == DFVM_F64)
+    return pressure_solve_t<double>(s, *static_cast<SolverT<double>*>(s->impl.get()), (const double*)rAU->ptr,
+                                    (const double*)g->ptr, (double*)lambda->ptr, tol, rel_tol, maxit, rep, cs, true);
+  return pressure_solve_t<float>(s, *static_cast<SolverT<float>*>(s->impl.get()), (const float*)rAU->ptr,
+                                 (const float*)g->ptr, (float*)lambda->ptr, tol, rel_tol, maxit, rep, cs, true);
+}
+
+dfvm_status dfvm_pressure_vjp(dfvm_solver* s, const dfvm_field* p, const dfvm_field* lambda, dfvm_field* grad,
+                              dfvm_stream stream) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  dfvm_status st;
+  if ((st = check_f(p, s->m, true, 1, "p")) || (st = check_f(lambda, s->m, true, 1, "lambda")) ||
+      (st = check_f(grad, s->m, true, 1, "grad")))
+    return st;
+  cudaSetDevice(s->m->device);
+  s->fixed_p = solver_has_fixed_p(s);
+  cudaStream_t cs = (cudaStream_t)stream;
+  if ((st = bcs_device(s->b, 1, cs))) return st;
+  if ((st = halo_exchange(s->m, p->ptr, 1, cs)) || (st = halo_exchange(s->m, lambda->ptr, 1, cs))) return st;
+  const int ref_orig = s->fixed_p ? -1 : (int)s->o.p_ref_cell;
+  if (s->m->precision == DFVM_F64) {
+    auto& X = *static_cast<SolverT<double>*>(s->impl.get());
+    k_pvjp<double><<<grid_for_slices(X.M->n_slices), kThreads, 0, cs>>>(*X.M, (const double*)p->ptr,
+        (const double*)lambda->ptr, s->b->d_kind[1], s->m->d_cell_orig, ref_orig, s->o.p_ref_value, (double*)grad->ptr);
+  } else {
+    auto& X = *static_cast<SolverT<float>*>(s->impl.get());
+    k_pvjp<float><<<grid_for_slices(X.M->n_slices), kThreads, 0, cs>>>(*X.M, (const float*)p->ptr,
+        (const float*)lambda->ptr, s->b->d_kind[1], s->m->d_cell_orig, ref_orig, (float)s->o.p_ref_value, (float*)grad->ptr);
+  }
+  count_launch();
+  DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
 }
 
