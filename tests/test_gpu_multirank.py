@@ -145,3 +145,44 @@ def test_piso_partitioned_matches_single(P, wk, precond):
     if wk:
         for r in range(P):
             assert np.allclose(reps[r]["Q"], r1["Q"], rtol=1e-10) and np.allclose(reps[r]["p_o"], r1["p_o"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_adjoint_pieces_partitioned_equal_single(P):
+    # NEXT-3 on a partitioned mesh: the transposed momentum apply (interface
+    # faces: each rank writes the other row's coefficient itself) and the
+    # pressure VJP (gauge row on one rank, its neighbours' ghosts on another)
+    # equal the single-rank results bitwise
+    raw = _pipe()
+    n = raw.n_cells
+    U, phi = synth.cell_field(40, n, 3), synth.face_field(41, raw.n_faces)
+    x, pv, lv = synth.cell_field(50, n, 3), synth.cell_field(51, n), synth.cell_field(52, n)
+    kw = dict(nu=0.1, dt=0.005, n_corr=2, n_nonorth=1, convection="upwind", p_ref_cell=raw.n_cells // 2)
+
+    def run(m, S, sp=None):
+        keep = [m.field("cells", 3, U, sp), m.field("flux", 1, phi, sp), m.field("cells", 1), m.field("cells", 3),
+                m.field("cells", 3, x, sp), m.field("cells", 1, pv, sp), m.field("cells", 1, lv, sp)]
+        S.momentum_assemble(keep[0], keep[1], keep[2], keep[3], sp)
+        y, g = m.field("cells", 3), m.field("cells", 1)
+        S.momentum_apply_transpose(keep[4], y, sp)
+        S.pressure_vjp(keep[5], keep[6], g, sp)
+        return y, g, keep
+    m1 = dfvm.Mesh(raw)
+    y1, g1, _k = run(m1, dfvm.Solver(m1, _bcs(m1, outlet_p=False), **kw))
+    ref_y, ref_g = y1.get(), g1.get()
+    comms = dfvm.Comm.local_group(P)
+    ms = [dfvm.Mesh(raw, n_parts=P, rank=r, comm=comms[r]) for r in range(P)]
+    Ss = [dfvm.Solver(m, _bcs(m, outlet_p=False), **kw) for m in ms]
+    _, sp = _streams(P)
+    outs = [None] * P
+
+    def work(r):
+        def f():
+            outs[r] = run(ms[r], Ss[r], sp[r])
+        return f
+    _run_threads([work(r) for r in range(P)])
+    y, g = np.zeros((n, 3)), np.zeros((n, 1))
+    for r in range(P):
+        outs[r][0].get(sp[r], out=y)
+        outs[r][1].get(sp[r], out=g)
+    assert np.array_equal(y, ref_y) and np.array_equal(g[:, 0], ref_g)
