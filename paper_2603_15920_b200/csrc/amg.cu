@@ -34,8 +34,6 @@
 #include <type_traits>
 #include <vector>
 
-#include <cooperative_groups.h>
-
 #include "amg.h"
 #include "dev.cuh"
 
@@ -58,22 +56,15 @@ constexpr int kMaxLevels = 16;
 //                    doubles per level, and deep levels are launch-bound)
 //   DFVM_AMG_OMEGA   coarse-correction scale (symmetric over-correction,
 //                    < 2 keeps M SPD with adjoint smoothers)   default 1.8
-//   DFVM_AMG_TAIL    levels with <= this many rows (below level 0) run as
-//                    one cooperative kernel with grid-wide barriers instead
-//                    of one launch per phase (0: off)           default 0
-//                    (measured on B200, C5: the barrier-separated phases
-//                    ran 2x slower than the launched kernels, 406 vs ~195 us
-//                    per level-3 visit; kept as an option)
 //   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
 //                    exactly with a dense inverse (Gauss-Jordan once per
 //                    matrix update, one block), larger ones with
 //                    DFVM_AMG_SWEEPS l1-Jacobi sweeps (0: always sweeps)  default 512
 struct AmgParams {
-  int coarse = 256, sweeps = 32, wmax = 4, tail = 0, direct = kDirectMax;
+  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax;
   bool wcycle = true;
   double omega = 1.8;
   AmgParams() {
-    if (const char* e = getenv("DFVM_AMG_TAIL")) tail = std::max(0, atoi(e));
     if (const char* e = getenv("DFVM_AMG_DIRECT")) direct = std::max(0, std::min(kDirectMax, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_OMEGA")) omega = atof(e);
     if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kCoarseMax, atoi(e)));
@@ -152,6 +143,7 @@ std::vector<int> aggregate(const HostLevel& L, int& nagg) {
 template <class P>
 struct AmgLevelDev {
   int n = 0, n_slices = 0;
+  int G = 1;                 // lanes per row in the coarse-level kernels (1, 4 or 8)
   int64_t n_sell = 0;
   const int *ms_ptr = nullptr, *ms_len = nullptr, *mnb = nullptr;
   const P* coef = nullptr;   // level 0: the solver's pcoef (P == T) or coef_own (fp32 copy)
@@ -168,17 +160,6 @@ struct AmgLevelDev {
   P *e = nullptr, *r2 = nullptr;                  // W-cycle: second-visit solution / rhs
 };
 
-// device copy of a level for the cooperative tail kernel
-template <class P>
-struct TailLevel {
-  int n;
-  const int *ms_ptr, *ms_len, *mnb;
-  const P *coef, *diag, *il1;
-  const int* agg;                   // this level's rows -> next level's rows
-  const int *mem_ptr, *mem;         // this level's rows <- members on the finer level
-  P *x, *b, *r, *t, *e, *r2;
-};
-
 // hierarchy stored and cycled in type P
 template <class P>
 struct AmgH {
@@ -186,10 +167,7 @@ struct AmgH {
   int nlev = 0;
   AmgParams prm;
   AmgLevelDev<P> L[kMaxLevels];
-  int tail = 0;                     // first level run by the cooperative tail kernel (0: none)
   P* ainv = nullptr;                // dense inverse of the coarsest matrix (column-major n x n), or NULL
-  int tail_grid = 0;
-  TailLevel<P>* d_tail = nullptr;
   std::vector<void*> allocs;
   int64_t bytes = 0;
   ~AmgH() { for (void* p : allocs) cudaFree(p); }
@@ -250,6 +228,33 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     int nc = 0;
     std::vector<int> agg = aggregate(F, nc);
     if (nc >= F.n * 0.85) break;           // coarsening stalled
+    {   // SELL-32-sigma: renumber the aggregates so that, within windows of 256
+        // (8 slices, locality kept), rows are sorted by length: less padding
+        // in the coarse SELL (35 % -> a few % on the C5 level 1)
+      std::vector<std::vector<int>> members(nc);
+      for (int i = 0; i < F.n; ++i) members[agg[i]].push_back(i);
+      std::vector<int> len(nc), nb;
+      for (int I = 0; I < nc; ++I) {
+        nb.clear();
+        for (int i : members[I])
+          for (int k = F.rp[i]; k < F.rp[i + 1]; ++k) nb.push_back(agg[F.col[k]]);
+        std::sort(nb.begin(), nb.end());
+        int u = 0;
+        for (size_t k = 0; k < nb.size(); ++k)
+          if ((k == 0 || nb[k] != nb[k - 1]) && nb[k] != I) ++u;
+        len[I] = u;
+      }
+      std::vector<int> order(nc);
+      std::iota(order.begin(), order.end(), 0);
+      constexpr int kSigma = 256;
+      for (int w0 = 0; w0 < nc; w0 += kSigma) {
+        const int w1 = std::min(nc, w0 + kSigma);
+        std::stable_sort(order.begin() + w0, order.begin() + w1, [&](int a, int b) { return len[a] > len[b]; });
+      }
+      std::vector<int> newid(nc);
+      for (int k = 0; k < nc; ++k) newid[order[k]] = k;
+      for (int i = 0; i < F.n; ++i) agg[i] = newid[agg[i]];
+    }
     // members
     std::vector<int> mem_ptr(nc + 1, 0), mem(F.n);
     for (int i = 0; i < F.n; ++i) mem_ptr[agg[i] + 1]++;
@@ -317,6 +322,10 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     // upload
     AmgLevelDev<P>& D = A->L[lev + 1];
     D.n = nc; D.n_slices = S; D.n_sell = C.ms_ptr[S];
+    {   // grouped kernels where rows are long or few (latency-bound otherwise)
+      const double avg = (double)ccol.size() / std::max(1, nc);
+      D.G = (avg >= 12.0 || nc < 50000) ? 8 : (avg >= 6.0 ? 4 : 1);
+    }
     int *p0, *p1, *p2;
     if ((st = A->up(&p0, C.ms_ptr)) || (st = A->up(&p1, C.ms_len)) || (st = A->up(&p2, C.mnb)) ||
         (st = A->up(&D.gal_ptr, gal_ptr)) || (st = A->up(&D.gal_idx, gal_idx)) || (st = A->up(&D.dg_ptr, dg_ptr)) ||
@@ -342,9 +351,6 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
   return DFVM_OK;
 }
 
-template <class P>
-static dfvm_status setup_tail(AmgH<P>* A);
-
 template <class T>
 dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** out) {
   Amg<T>* A = new Amg<T>();
@@ -352,11 +358,9 @@ dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** ou
   if (fp32 && !std::is_same<T, float>::value) {
     A->lo = new AmgH<float>();
     st = build<float, T>(m, M, A->lo);
-    if (!st) st = setup_tail(A->lo);
   } else {
     A->same = new AmgH<T>();
     st = build<T, T>(m, M, A->same);
-    if (!st) st = setup_tail(A->same);
   }
   if (st) { delete A; return st; }
   *out = A;
@@ -567,6 +571,88 @@ __global__ void k_amg_prolong_smooth(int n, const int* __restrict__ ms_ptr, cons
     out[i] = prolong_smooth_row(i, ms_ptr, ms_len, mnb, coef, diag, il1, agg, xc, w, x0, b);
 }
 
+// Grouped coarse-level kernels: G consecutive lanes share a row, lane g sums
+// the row's entries j = g, g + G, ..., and a shuffle tree within the group
+// adds the partials (fixed order: deterministic).  A warp takes 32 / G rows
+// per step and every lane joins the shuffles (rows past n add zeros).
+template <int G, class T>
+__device__ __forceinline__ T group_sum(T v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+#define GROUP_LOOP(n)                                                                              \
+  const int lane = threadIdx.x & 31, sub = lane % G;                                               \
+  const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;                                      \
+  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c * (32 / G) < (n); c += nwg)
+
+template <class T, int G>
+__global__ void k_amg_pre_resid_g(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                                  const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
+                                  const T* __restrict__ il1, const T* __restrict__ b, T* __restrict__ x0,
+                                  T* __restrict__ r, const int* done) {
+  if (*done) return;
+  GROUP_LOOP(n) {
+    const int row = (int)(c * (32 / G) + lane / G);
+    T part = T(0);
+    if (row < n) {
+      const int base = ms_ptr[row >> 5] + (row & 31), len = ms_len[row >> 5];
+      for (int j = sub; j < len; j += G) {
+        const int cc = __ldg(&mnb[base + 32 * j]);
+        part += __ldg(&coef[base + 32 * j]) * (b[cc] * il1[cc]);
+      }
+    }
+    const T sum = group_sum<G>(part);
+    if (row < n && sub == 0) {
+      const T bi = b[row], xi = bi * il1[row];
+      x0[row] = xi;
+      r[row] = bi - (diag[row] * xi + sum);
+    }
+  }
+}
+template <class T, int G>
+__global__ void k_amg_prolong_smooth_g(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                                       const int* __restrict__ mnb, const T* __restrict__ coef,
+                                       const T* __restrict__ diag, const T* __restrict__ il1,
+                                       const int* __restrict__ agg, const T* __restrict__ xc, T w,
+                                       const T* __restrict__ x0, const T* __restrict__ b, T* __restrict__ out,
+                                       const int* done) {
+  if (*done) return;
+  GROUP_LOOP(n) {
+    const int row = (int)(c * (32 / G) + lane / G);
+    T part = T(0);
+    if (row < n) {
+      const int base = ms_ptr[row >> 5] + (row & 31), len = ms_len[row >> 5];
+      for (int j = sub; j < len; j += G) {
+        const int cc = __ldg(&mnb[base + 32 * j]);
+        part += __ldg(&coef[base + 32 * j]) * (x0[cc] + w * xc[agg[cc]]);
+      }
+    }
+    const T sum = group_sum<G>(part);
+    if (row < n && sub == 0) {
+      const T ti = x0[row] + w * xc[agg[row]];
+      out[row] = ti + (b[row] - (diag[row] * ti + sum)) * il1[row];
+    }
+  }
+}
+template <class T, int G>
+__global__ void k_amg_resid_g(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
+                              const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
+                              const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ r, const int* done) {
+  if (*done) return;
+  GROUP_LOOP(n) {
+    const int row = (int)(c * (32 / G) + lane / G);
+    T part = T(0);
+    if (row < n) {
+      const int base = ms_ptr[row >> 5] + (row & 31), len = ms_len[row >> 5];
+      for (int j = sub; j < len; j += G) part += __ldg(&coef[base + 32 * j]) * x[__ldg(&mnb[base + 32 * j])];
+    }
+    const T sum = group_sum<G>(part);
+    if (row < n && sub == 0) r[row] = b[row] - (diag[row] * x[row] + sum);
+  }
+}
+#undef GROUP_LOOP
+
 // x += e
 template <class T>
 __global__ void k_amg_add(int n, const T* __restrict__ e, T* __restrict__ x, const int* done) {
@@ -641,15 +727,18 @@ __global__ void __launch_bounds__(1024) k_amg_dense_inv(int n, const int* __rest
   }
 }
 
-// coarsest solve with the dense inverse: x_i = sum_j Ainv_ij b_j (one block;
-// Ainv is symmetric, read column-wise for coalescing)
+// coarsest solve with the dense inverse: x_i = sum_j Ainv_ij b_j (one block)
 template <class P, class TB, class TO>
 __device__ __forceinline__ void dense_solve_block(int n, const P* __restrict__ Ai, const TB* __restrict__ b,
                                                   TO* __restrict__ x) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  // one warp per row (row-major Ainv: coalesced across the lanes), shuffle tree
+  const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int i = threadIdx.x >> 5; i < n; i += nwarps) {
     P acc = P(0);
-    for (int j = 0; j < n; ++j) acc += Ai[(size_t)j * n + i] * (P)b[j];
-    x[i] = (TO)acc;
+    for (int j = lane; j < n; j += 32) acc += Ai[(size_t)i * n + j] * (P)b[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) x[i] = (TO)acc;
   }
 }
 template <class P, class TB, class TO>
@@ -657,107 +746,6 @@ __global__ void __launch_bounds__(1024) k_amg_dense(int n, const P* __restrict__
                                                     TO* __restrict__ x, const int* done) {
   if (*done) return;
   dense_solve_block<P, TB, TO>(n, Ai, b, x);
-}
-
-// ------------------------------------------------------------ cooperative tail
-// The deep levels (a few thousand to ~1e5 rows) are launch-bound: one
-// W-cycle visit of a level below ~1e5 rows is a dozen launches of 3-30 us
-// each.  The tail kernel runs the whole sub-cycle from level `l` down in one
-// cooperative launch: every phase is a grid-stride loop over the level's
-// rows, phases are separated by grid-wide barriers, and the arithmetic is
-// that of the per-phase kernels above (same formulas, same order), so the
-// result is bitwise identical to the launched cycle.
-namespace cg = cooperative_groups;
-constexpr int kTailThreads = 512;
-
-template <class P>
-__device__ void tail_cycle(cg::grid_group& g, const TailLevel<P>* __restrict__ L, int l, int nlev, const P* b, P* x,
-                           P w, int sweeps, int wc, int wmax, const P* ainv) {
-  const TailLevel<P>& F = L[l];
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
-  if (l == nlev - 1) {                      // coarsest: dense inverse, or l1-Jacobi sweeps in block 0
-    if (blockIdx.x == 0 && ainv) dense_solve_block<P, P, P>(F.n, ainv, b, x);
-    if (blockIdx.x == 0 && !ainv) {
-      __shared__ P xs[2][kCoarseMax];
-      for (int i = threadIdx.x; i < F.n; i += blockDim.x) xs[0][i] = b[i] * F.il1[i];
-      __syncthreads();
-      int cur = 0;
-      for (int it = 1; it < sweeps; ++it) {
-        for (int i = threadIdx.x; i < F.n; i += blockDim.x)
-          xs[cur ^ 1][i] = xs[cur][i] + (b[i] - row_apply(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, xs[cur])) * F.il1[i];
-        __syncthreads();
-        cur ^= 1;
-      }
-      for (int i = threadIdx.x; i < F.n; i += blockDim.x) x[i] = xs[cur][i];
-    }
-    g.sync();
-    return;
-  }
-  const TailLevel<P>& C = L[l + 1];
-  for (int i = tid; i < F.n; i += nt) {     // pre-smooth + residual (k_amg_pre_resid)
-    P xv, rv;
-    pre_resid_row(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, xv, rv);
-    F.t[i] = xv;
-    F.r[i] = rv;
-  }
-  g.sync();
-  for (int I = tid; I < C.n; I += nt) {     // restriction (k_amg_restrict)
-    P sum = P(0);
-    for (int k = C.mem_ptr[I]; k < C.mem_ptr[I + 1]; ++k) sum += F.r[C.mem[k]];
-    C.b[I] = sum;
-  }
-  g.sync();
-  tail_cycle(g, L, l + 1, nlev, C.b, C.x, w, sweeps, wc, wmax, ainv);
-  if (wc && l + 1 < nlev - 1 && l + 1 <= wmax) {
-    for (int I = tid; I < C.n; I += nt)     // second visit (k_amg_resid, k_amg_add)
-      C.r2[I] = C.b[I] - row_apply(I, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x);
-    g.sync();
-    tail_cycle(g, L, l + 1, nlev, C.r2, C.e, w, sweeps, wc, wmax, ainv);
-    for (int I = tid; I < C.n; I += nt) C.x[I] += C.e[I];
-    g.sync();
-  }
-  for (int i = tid; i < F.n; i += nt)       // prolongation + post-smooth (k_amg_prolong_smooth)
-    x[i] = prolong_smooth_row(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.agg, C.x, w, F.t, b);
-  g.sync();
-}
-
-template <class P>
-__global__ void __launch_bounds__(kTailThreads) k_amg_tail(const TailLevel<P>* __restrict__ L, int l, int nlev,
-                                                          const P* b, P* x, P w, int sweeps, int wc, int wmax,
-                                                          const P* ainv, const int* done) {
-  if (*done) return;
-  cg::grid_group g = cg::this_grid();
-  tail_cycle(g, L, l, nlev, b, x, w, sweeps, wc, wmax, ainv);
-}
-
-template <class P>
-static dfvm_status setup_tail(AmgH<P>* A) {
-  A->tail = 0;
-  if (A->prm.tail <= 0) return DFVM_OK;
-  // ranks of an in-process group may share one GPU: grids sized to the whole
-  // device from several streams would not be co-resident
-  if (comm_is_local(A->m->comm)) return DFVM_OK;
-  int l = 1;
-  while (l < A->nlev && A->L[l].n > A->prm.tail) ++l;
-  if (l >= A->nlev - 1) return DFVM_OK;     // nothing but the coarsest solve below: keep the launches
-  int dev = 0, occ = 0, sms = 0, coop = 0;
-  DFVM_CUDA(cudaGetDevice(&dev));
-  DFVM_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-  if (!coop) return DFVM_OK;
-  DFVM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  DFVM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_amg_tail<P>, kTailThreads, 0));
-  if (occ < 1) return DFVM_OK;
-  std::vector<TailLevel<P>> h(A->nlev);
-  for (int k = 0; k < A->nlev; ++k) {
-    const AmgLevelDev<P>& D = A->L[k];
-    h[k] = TailLevel<P>{D.n, D.ms_ptr, D.ms_len, D.mnb, D.coef, D.diag, D.il1, D.agg, D.mem_ptr, D.mem,
-                        D.x, D.b, D.r, D.t, D.e, D.r2};
-  }
-  dfvm_status st;
-  if ((st = A->up(&A->d_tail, h))) return st;
-  A->tail = l;
-  A->tail_grid = occ * sms;
-  return DFVM_OK;
 }
 
 // ------------------------------------------------------------ host drivers
@@ -806,17 +794,6 @@ dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s
 template <class P>
 static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl) {
   AmgLevelDev<P>& F = A->L[l];
-  if (A->tail && l == A->tail) {
-    const TailLevel<P>* d = A->d_tail;
-    int nlev = A->nlev, sweeps = A->prm.sweeps, wc = A->prm.wcycle ? 1 : 0, wmax = A->prm.wmax;
-    P w = (P)A->prm.omega;
-    const P* ai = A->ainv;
-    void* args[] = {(void*)&d, (void*)&l, (void*)&nlev, (void*)&b, (void*)&x, (void*)&w, (void*)&sweeps, (void*)&wc,
-                    (void*)&wmax, (void*)&ai, (void*)&done};
-    cudaLaunchCooperativeKernel((const void*)k_amg_tail<P>, dim3(A->tail_grid), dim3(kTailThreads), args, 0, s);
-    ++*nl;
-    return;
-  }
   if (l == A->nlev - 1) {
     if (A->ainv) k_amg_dense<P, P, P><<<1, 1024, 0, s>>>(F.n, A->ainv, b, x, done);
     else k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, x,
@@ -825,20 +802,31 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
     return;
   }
   AmgLevelDev<P>& C = A->L[l + 1];
-  k_amg_pre_resid<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b,
-                                                         F.t, F.r, done);
+  const P w = (P)A->prm.omega;
+  const int gF = grid_for((int64_t)F.n * F.G), gC = grid_for((int64_t)C.n * C.G);
+  switch (F.G) {
+    case 8: k_amg_pre_resid_g<P, 8><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, F.t, F.r, done); break;
+    case 4: k_amg_pre_resid_g<P, 4><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, F.t, F.r, done); break;
+    default: k_amg_pre_resid<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, F.t, F.r, done);
+  }
   k_amg_restrict<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
   *nl += 2;
   cycle_coarse(A, l + 1, C.b, C.x, done, s, nl);
   if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax) {
-    k_amg_resid<P, P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b,
-                                                         C.r2, done);
+    switch (C.G) {
+      case 8: k_amg_resid_g<P, 8><<<gC, kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b, C.r2, done); break;
+      case 4: k_amg_resid_g<P, 4><<<gC, kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b, C.r2, done); break;
+      default: k_amg_resid<P, P><<<gC, kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b, C.r2, done);
+    }
     cycle_coarse(A, l + 1, C.r2, C.e, done, s, nl);
     k_amg_add<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done);
     *nl += 2;
   }
-  k_amg_prolong_smooth<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag,
-                                                              F.il1, F.agg, C.x, (P)A->prm.omega, F.t, b, x, done);
+  switch (F.G) {
+    case 8: k_amg_prolong_smooth_g<P, 8><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.agg, C.x, w, F.t, b, x, done); break;
+    case 4: k_amg_prolong_smooth_g<P, 4><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.agg, C.x, w, F.t, b, x, done); break;
+    default: k_amg_prolong_smooth<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.agg, C.x, w, F.t, b, x, done);
+  }
   ++*nl;
 }
 

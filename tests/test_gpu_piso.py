@@ -295,26 +295,6 @@ def test_c3_cylinder_poly_piso():
     assert np.abs(Ug.get()[:, 2]).max() <= 1e-12      # A-24: 2-D slab keeps U_z ~ 0
 
 
-@pytest.mark.parametrize("precond", ["amg", "amg32"])
-def test_amg_cooperative_tail_bitwise(precond, monkeypatch):
-    # the cooperative tail kernel (deep AMG levels in one launch) repeats the
-    # per-phase kernels' arithmetic: PCG iterates and iteration counts must be
-    # bitwise identical with and without it (DFVM_AMG_TAIL, amg.cu)
-    raw, mo, mg, bo, bg, kw = pipe_case(n=8, m_r=4, n_z=40)
-    rAU = 0.01 * (1.5 + 0.5 * synth.cell_field(60, mo.N))
-    rhs = 1e-3 * synth.cell_field(61, mo.N)
-    out = []
-    for tail in ("0", "1000000000"):
-        monkeypatch.setenv("DFVM_AMG_TAIL", tail)
-        monkeypatch.setenv("DFVM_AMG_COARSE", "16")       # several levels below the tail start
-        Sg = dfvm.Solver(mg, bg, p_precond=precond, **kw)
-        pg = mg.field("cells", 1, synth.cell_field(62, mo.N))
-        r = Sg.pressure_solve(mg.field("cells", 1, rAU), mg.field("cells", 1, rhs), pg, tol=1e-13)
-        out.append((pg.get(), r["it"], len(Sg.amg_levels())))
-    assert out[0][2] >= 3
-    assert out[0][1] == out[1][1] and np.array_equal(out[0][0], out[1][0])
-
-
 @pytest.mark.parametrize("direct", ["0", "512"])
 def test_amg_coarsest_direct_or_sweeps(direct, monkeypatch):
     # coarsest AMG level solved by a dense inverse (default) or by l1-Jacobi
