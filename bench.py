@@ -249,7 +249,10 @@ def main():
     S = dfvm.Solver(mesh, B, **case.solver)
     for patch, (Rp, Cc, Rd) in getattr(case, "windkessel", []):
         S.windkessel_set(patch, Rp, Cc, Rd, 0.0, 0)
-    stream = torch.cuda.current_stream()
+    # a dedicated stream: the library captures its AMG-PCG chunks as CUDA
+    # graphs on non-default streams (all timing events are on this stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sp = C.c_void_p(stream.cuda_stream)
     U = mesh.field("cells", 3, U0, sp)
     p = mesh.field("cells", 1, p0, sp)

@@ -1059,7 +1059,12 @@ struct SolverT : SolverBase {
   int* d_wk_ptr = nullptr;
   int* d_wk_faces = nullptr;
   bool assembled = false;
+  // CUDA graphs of the AMG-PCG chunk (one per (x, b, timing) in use)
+  struct ChunkGraph { const void* x; const void* b; bool timing; cudaGraphExec_t exec; int launches; };
+  std::vector<ChunkGraph> graphs;
+  bool graphs_off = false;
   ~SolverT() override {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (amg) amg_destroy<T>(amg);
     for (void* p : allocs) cudaFree(p);
     if (h_ctl) cudaFreeHost(h_ctl);
@@ -1316,24 +1321,63 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
       S->ev.push_back(ev);
     }
   }
-  int it_before = 0;
-  for (;;) {
+  // one chunk of kChunk iterations (every kernel exits early on the done flag)
+  auto enqueue_chunk = [&](int* nl) -> dfvm_status {
+    dfvm_status e2;
     for (int k = 0; k < kChunk; ++k) {
       if (S->timing) cudaEventRecord(S->ev[4 * k], st);
       k_cg_p2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kz, X.kp, x, X.d_ctl);
-      if ((e = halo_exchange(m, X.kp, 1, st))) return e;
+      if ((e2 = halo_exchange(m, X.kp, 1, st))) return e2;
       if (S->timing) cudaEventRecord(S->ev[4 * k + 1], st);
       k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red);
       if (S->timing) cudaEventRecord(S->ev[4 * k + 2], st);
-      if ((e = fin(S, X, CTL_CG_SPMV, 1, st))) return e;
+      if ((e2 = fin(S, X, CTL_CG_SPMV, 1, st))) return e2;
       k_cg_r2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, X.partials, X.ticket, X.d_ctl, red);
-      if ((e = fin(S, X, CTL_CG_R2, 1, st))) return e;
-      if ((e = amg_apply<T>(X.amg, X.kr, X.kz, done, st, &S->n_launch,
-                            S->timing ? &S->ev[4 * kChunk + 4 * k] : nullptr))) return e;
+      if ((e2 = fin(S, X, CTL_CG_R2, 1, st))) return e2;
+      if ((e2 = amg_apply<T>(X.amg, X.kr, X.kz, done, st, nl, S->timing ? &S->ev[4 * kChunk + 4 * k] : nullptr)))
+        return e2;
       k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ);
-      if ((e = fin(S, X, CTL_CG_RZ, 1, st))) return e;
+      if ((e2 = fin(S, X, CTL_CG_RZ, 1, st))) return e2;
       if (S->timing) cudaEventRecord(S->ev[4 * k + 3], st);
-      S->n_launch += 4;
+      *nl += 4;
+    }
+    return DFVM_OK;
+  };
+  // Unpartitioned meshes replay the chunk as a CUDA graph (~1300 launches per
+  // chunk with the W-cycle: host enqueue, not the GPU, bounded the deep AMG
+  // levels).  Captured on first use for this (x, b, timing); DFVM_GRAPHS=0
+  // disables.
+  typename SolverT<T>::ChunkGraph* graph = nullptr;
+  if (m->part.P == 1 && !X.graphs_off && st != nullptr) {   // (the legacy default stream cannot be captured)
+    static const bool env_off = getenv("DFVM_GRAPHS") && getenv("DFVM_GRAPHS")[0] == '0';
+    if (env_off) X.graphs_off = true;
+    for (auto& g : X.graphs)
+      if (g.x == x && g.b == b && g.timing == S->timing) graph = &g;
+    if (!graph && !X.graphs_off) {
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ge2 = nullptr;
+      int nl = 0;
+      bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      dfvm_status ce = ok ? enqueue_chunk(&nl) : DFVM_OK;
+      ok = (cudaStreamEndCapture(st, &g) == cudaSuccess) && ok && ce == DFVM_OK && g;
+      ok = ok && cudaGraphInstantiate(&ge2, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      if (ok) {
+        X.graphs.push_back({x, b, S->timing, ge2, nl});
+        graph = &X.graphs.back();
+      } else {
+        X.graphs_off = true;   // capture unsupported here: enqueue directly from now on
+      }
+    }
+  }
+  int it_before = 0;
+  for (;;) {
+    if (graph) {
+      DFVM_CUDA(cudaGraphLaunch(graph->exec, st));
+      S->n_launch += graph->launches;
+    } else if ((e = enqueue_chunk(&S->n_launch))) {
+      return e;
     }
     DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
     DFVM_CUDA(cudaStreamSynchronize(st));

@@ -310,3 +310,23 @@ def test_amg_coarsest_direct_or_sweeps(direct, monkeypatch):
     rg = Sg.pressure_solve(mg.field("cells", 1, rAU), mg.field("cells", 1, rhs), pg, tol=1e-14)
     assert rg["converged"] and len(Sg.amg_levels()) >= 2
     assert rel_l2(pg.get(), po) <= 1e-8
+
+
+@pytest.mark.parametrize("precond", ["amg", "amg32"])
+def test_graph_replay_bitwise(precond):
+    # on a non-default stream the AMG-PCG chunks are captured once and replayed
+    # as CUDA graphs; the fields must be bitwise those of the direct enqueue
+    import ctypes
+    import torch
+    raw, mo, mg, bo, bg, kw = pipe_case(n=8, m_r=4, n_z=40)
+    U0, p0, phi0 = initial_state(mo)
+    out = []
+    s = torch.cuda.Stream()
+    for sp in (None, ctypes.c_void_p(s.cuda_stream)):
+        Sg = dfvm.Solver(mg, bg, p_precond=precond, **kw, **TIGHT)
+        Ug, pg, phig = mg.field("cells", 3, U0), mg.field("cells", 1, p0), mg.field("flux", 1, phi0)
+        reps = [Sg.step(Ug, pg, phig, sp) for _ in range(3)]
+        out.append((Ug.get(sp), pg.get(sp), phig.get(sp), [r["it"] for rep in reps for r in rep["p"]]))
+    assert out[0][3] == out[1][3]
+    for a, b in zip(out[0][:3], out[1][:3]):
+        assert np.array_equal(a, b)
