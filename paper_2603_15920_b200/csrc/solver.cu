@@ -122,10 +122,12 @@ __device__ void ctl_apply(int kind, KCtl* ctl, const double* t) {
         if (c.snorm <= c.thr) c.half = 1;
       }
       break;
-    case CTL_BI_T:
+    case CTL_BI_T:   // t[0..2] = t.s, t[3..5] = t.t, t[6..8] = s.s (s formed inside k_bi_t)
       for (int k = 0; k < 3; ++k) {
         KCtl& c = ctl[k];
-        if (c.done || c.half) continue;
+        if (c.done) continue;
+        c.snorm = sqrt(t[6 + k]);
+        if (c.snorm <= c.thr) { c.half = 1; continue; }
         if (t[3 + k] == 0.0) { c.done = 1; c.status = DFVM_E_BREAKDOWN; continue; }
         c.omega = t[k] / t[3 + k];
       }
@@ -166,7 +168,7 @@ __global__ void k_finalize(int kind, int nv, const double* __restrict__ all, int
     if (ctl->done) return;
   }
   else if (kind != CTL_CG_INIT && kind != CTL_BI_INIT) { if (ctl[0].done && ctl[1].done && ctl[2].done) return; }
-  double t[8];
+  double t[16];
   for (int i = 0; i < nv; ++i) {
     double s = 0;
     for (int r = 0; r < P; ++r) s += all[r * nv + i];   // fixed rank order
@@ -863,10 +865,14 @@ __global__ void k_recip(int n, const T* __restrict__ d, T* __restrict__ di) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) di[i] = T(1) / d[i];
 }
 
-// p = r + beta (p - omega v); y = p / diag   (dinv = 1 / diag)
+// Per iteration (4 kernels): p update | v = A M^-1 p, rh.v -> alpha |
+// s = r - alpha v formed on the fly, t = A M^-1 s, t.s, t.t, s.s -> half-step
+// check, omega | x, r update, rh.r, r.r -> rho, check.  Neither y = M^-1 p nor
+// s is stored: the kernels that need them form them from p (r, v) and dinv.
+
+// p = r + beta (p - omega v)
 template <class T>
-__global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ diag, const T* __restrict__ v,
-                       T* __restrict__ p, T* __restrict__ y, const KCtl* ctl) {
+__global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ p, const KCtl* ctl) {
   if (all_done(ctl)) return;
   T beta[3], om[3];
   bool act[3];
@@ -877,33 +883,55 @@ __global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ dia
     om[k] = (T)ctl[k].omega;
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const T d = diag[i];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       if (!act[k]) continue;
       const int64_t j = 3 * (int64_t)i + k;
-      const T pp = r[j] + beta[k] * (p[j] - om[k] * v[j]);
-      p[j] = pp;
-      y[j] = pp * d;
+      p[j] = r[j] + beta[k] * (p[j] - om[k] * v[j]);
     }
   }
 }
 
-// v = A y; partial (rh, v) -> alpha
+// v = A (p / diag); partial (rh, v) -> alpha   (dinv = 1 / diag)
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_bi_v(DevMesh<T> M, const T* __restrict__ diag,
-    const T* __restrict__ coef, const T* __restrict__ y, const T* __restrict__ rh, T* __restrict__ v,
-    double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+    const T* __restrict__ dinv, const T* __restrict__ coef, const T* __restrict__ p, const T* __restrict__ rh,
+    T* __restrict__ v, double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   if (all_done(ctl)) return;
   double a[3] = {0, 0, 0};
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
     T acc[3];
-    const T d = live ? diag[row] : T(0);
+    const T d = live ? diag[row] : T(0), di = live ? dinv[row] : T(0);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) acc[k] = live ? d * y[3 * (int64_t)row + k] : T(0);
-    sell_apply<T, 3>(M, s, lane, coef, y, acc);
+    for (int k = 0; k < 3; ++k) acc[k] = live ? d * (p[3 * (int64_t)row + k] * di) : T(0);
+    const int len = __ldg(&M.ms_len[s]);
+    const int base = __ldg(&M.ms_ptr[s]) + lane;
+    int j = 0;
+    for (; j + 4 <= len; j += 4) {
+      T c[4], dn[4], pn[4][3];
+      int nn[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { c[u] = __ldg(&coef[base + 32 * (j + u)]); nn[u] = __ldg(&M.mnb[base + 32 * (j + u)]); }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        dn[u] = dinv[nn[u]];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) pn[u][k] = p[3 * (int64_t)nn[u] + k];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += c[u] * (pn[u][k] * dn[u]);
+    }
+    for (; j < len; ++j) {
+      const T c = __ldg(&coef[base + 32 * j]);
+      const int nn = __ldg(&M.mnb[base + 32 * j]);
+      const T dn = dinv[nn];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) acc[k] += c * (p[3 * (int64_t)nn + k] * dn);
+    }
     if (live)
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
@@ -916,86 +944,71 @@ __global__ void __launch_bounds__(kThreads) k_bi_v(DevMesh<T> M, const T* __rest
   if (grid_sum<3>(a, partials, ticket, t)) red_finish<3>(red, CTL_BI_V, ctl, t);
 }
 
-// s = r - alpha v; partial (s, s) -> half-step convergence
+// s = r - alpha v (own row and, on the fly, every neighbour); t = A (s / diag);
+// partials (t, s), (t, t), (s, s) -> half-step check, omega
 template <class T>
-__global__ void k_bi_s(int n, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ sv,
-                       double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+__global__ void __launch_bounds__(kThreads) k_bi_t(DevMesh<T> M, const T* __restrict__ dinv,
+    const T* __restrict__ coef, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ tv,
+    double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   if (all_done(ctl)) return;
   T al[3];
-  bool act[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) { act[k] = !ctl[k].done; al[k] = (T)ctl[k].alpha; }
-  double a[3] = {0, 0, 0};
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      if (!act[k]) continue;
-      const int64_t j = 3 * (int64_t)i + k;
-      const T ss = r[j] - al[k] * v[j];
-      sv[j] = ss;
-      a[k] += (double)ss * (double)ss;
-    }
-  double t[3];
-  if (grid_sum<3>(a, partials, ticket, t)) red_finish<3>(red, CTL_BI_S, ctl, t);
-}
-
-// t = A (s / diag); partials (t, s), (t, t) -> omega   (diag argument = 1 / diag)
-template <class T>
-__global__ void __launch_bounds__(kThreads) k_bi_t(DevMesh<T> M, const T* __restrict__ diag,
-    const T* __restrict__ coef, const T* __restrict__ sv, T* __restrict__ tv, double* partials, unsigned* ticket,
-    KCtl* ctl, Red red) {
-  if (all_done(ctl)) return;
-  double a[6] = {0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < 3; ++k) al[k] = (T)ctl[k].alpha;
+  double a[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
-    T acc[3] = {T(0), T(0), T(0)};
+    T acc[3] = {T(0), T(0), T(0)}, sr[3] = {T(0), T(0), T(0)};
     if (live)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) acc[k] = sv[3 * (int64_t)row + k];   // diag * (s / diag)
+      for (int k = 0; k < 3; ++k) {
+        const int64_t i = 3 * (int64_t)row + k;
+        sr[k] = r[i] - al[k] * v[i];
+        acc[k] = sr[k];                    // diag * (s / diag)
+      }
     const int len = __ldg(&M.ms_len[s]);
     const int base = __ldg(&M.ms_ptr[s]) + lane;
     int j = 0;
-    for (; j + 4 <= len; j += 4) {       // batched: columns + coefficients, then gathers, then FMAs
-      T c[4], dn[4], sn[4][3];
+    for (; j + 4 <= len; j += 4) {
+      T c[4], dn[4], rn[4][3], vn[4][3];
       int nn[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) { c[u] = __ldg(&coef[base + 32 * (j + u)]); nn[u] = __ldg(&M.mnb[base + 32 * (j + u)]); }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        dn[u] = diag[nn[u]];
+        dn[u] = dinv[nn[u]];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) sn[u][k] = sv[3 * (int64_t)nn[u] + k];
+        for (int k = 0; k < 3; ++k) { rn[u][k] = r[3 * (int64_t)nn[u] + k]; vn[u][k] = v[3 * (int64_t)nn[u] + k]; }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) acc[k] += c[u] * (sn[u][k] * dn[u]);
+        for (int k = 0; k < 3; ++k) acc[k] += c[u] * ((rn[u][k] - al[k] * vn[u][k]) * dn[u]);
     }
     for (; j < len; ++j) {
-      const int idx = base + 32 * j;
-      const T c = coef[idx];
-      const int nn = __ldg(&M.mnb[idx]);
-      const T dn = diag[nn];
+      const T c = __ldg(&coef[base + 32 * j]);
+      const int nn = __ldg(&M.mnb[base + 32 * j]);
+      const T dn = dinv[nn];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) acc[k] += c * (sv[3 * (int64_t)nn + k] * dn);
+      for (int k = 0; k < 3; ++k) acc[k] += c * ((r[3 * (int64_t)nn + k] - al[k] * v[3 * (int64_t)nn + k]) * dn);
     }
     if (live)
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const int64_t i = 3 * (int64_t)row + k;
-        tv[i] = acc[k];
-        a[k] += (double)acc[k] * (double)sv[i];
+        tv[3 * (int64_t)row + k] = acc[k];
+        a[k] += (double)acc[k] * (double)sr[k];
         a[3 + k] += (double)acc[k] * (double)acc[k];
+        a[6 + k] += (double)sr[k] * (double)sr[k];
       }
   }
-  double t[6];
-  if (grid_sum<6>(a, partials, ticket, t)) red_finish<6>(red, CTL_BI_T, ctl, t);
+  double t[9];
+  if (grid_sum<9>(a, partials, ticket, t)) red_finish<9>(red, CTL_BI_T, ctl, t);
 }
 
-// x += alpha y + omega s/diag; r = s - omega t; partials (rh, r), (r, r)   (diag argument = 1 / diag)
+// s = r - alpha v; x += alpha p/diag + omega s/diag; r = s - omega t;
+// partials (rh, r), (r, r)   (dinv = 1 / diag)
 template <class T>
-__global__ void k_bi_x(int n, const T* __restrict__ diag, const T* __restrict__ y, const T* __restrict__ sv,
+__global__ void k_bi_x(int n, const T* __restrict__ dinv, const T* __restrict__ p, const T* __restrict__ v,
                        const T* __restrict__ tv, const T* __restrict__ rh, T* __restrict__ x, T* __restrict__ r,
                        double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   if (all_done(ctl)) return;
@@ -1008,14 +1021,14 @@ __global__ void k_bi_x(int n, const T* __restrict__ diag, const T* __restrict__ 
   }
   double a[6] = {0, 0, 0, 0, 0, 0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const T d = diag[i];
+    const T d = dinv[i];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const int64_t j = 3 * (int64_t)i + k;
-      if (mode[k] == 1) { x[j] += al[k] * y[j]; continue; }
+      if (mode[k] == 1) { x[j] += al[k] * (p[j] * d); continue; }
       if (mode[k] != 2) continue;
-      const T ss = sv[j];
-      x[j] += al[k] * y[j] + om[k] * (ss * d);
+      const T ss = r[j] - al[k] * v[j];
+      x[j] += al[k] * (p[j] * d) + om[k] * (ss * d);
       const T rr = ss - om[k] * tv[j];
       r[j] = rr;
       a[k] += (double)rh[j] * (double)rr;
@@ -1040,7 +1053,7 @@ struct SolverT : SolverBase {
   T* ucoefT = nullptr;          // transposed momentum coefficients (NEXT-3 adjoint apply)
   T *rAU = nullptr, *HbyA = nullptr, *phiHbyA = nullptr, *pcoef = nullptr, *pdiag = nullptr;
   T *prhs0 = nullptr, *prhs = nullptr;
-  T *kr = nullptr, *krh = nullptr, *kp = nullptr, *kq = nullptr, *kv = nullptr, *ky = nullptr, *ks = nullptr, *kt = nullptr;
+  T *kr = nullptr, *krh = nullptr, *kp = nullptr, *kq = nullptr, *kv = nullptr, *kt = nullptr;
   double* partials = nullptr;
   unsigned* ticket = nullptr;
   KCtl* d_ctl = nullptr;
@@ -1112,8 +1125,8 @@ struct SolverT : SolverBase {
         (st = al(&HbyA, 3 * nc)) || (st = al(&phiHbyA, nf)) || (st = al(&pcoef, (size_t)M->n_minc)) ||
         (st = al(&pdiag, nc)) || (st = al(&prhs0, no)) || (st = al(&prhs, no)) || (st = al(&kr, 3 * nc)) ||
         (st = al(&krh, 3 * nc)) || (st = al(&kp, 3 * nc)) || (st = al(&kq, 3 * nc)) || (st = al(&kv, 3 * nc)) ||
-        (st = al(&ky, 3 * nc)) || (st = al(&ks, 3 * nc)) || (st = al(&kt, 3 * nc)) || (st = al(&kz, nc)) ||
-        (st = al(&partials, (size_t)kMaxBlocks * 8)) || (st = al(&ticket, 4)) || (st = al(&d_ctl, 4)) ||
+        (st = al(&kt, 3 * nc)) || (st = al(&kz, nc)) ||
+        (st = al(&partials, (size_t)kMaxBlocks * 16)) || (st = al(&ticket, 4)) || (st = al(&d_ctl, 4)) ||
         (st = al(&d_cont, 8)) || (st = al(&red_local, 128)) || (st = al(&red_all, (size_t)128 * mm->part.P)))
       return st;
     DFVM_CUDA(cudaMallocHost(&h_ctl, 4 * sizeof(KCtl)));
@@ -1415,7 +1428,7 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
 }
 
 // 3-component BiCGStab on (udiag, ucoef): x = U (warm start), b = rhsU.
-// Ghosts: x and udiag are exchanged by the caller (assemble); y and s are
+// Ghosts: x and udiag are exchanged by the caller (assemble); p, r and v are
 // exchanged before the applies that gather them.
 template <class T>
 static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol,
@@ -1437,19 +1450,18 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   if ((e = fin(S, X, CTL_BI_INIT, 6, st))) return e;
   for (;;) {
     for (int k = 0; k < kChunk; ++k) {
-      k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.udinv, X.kv, X.kp, X.ky, X.d_ctl);
-      if ((e = halo_exchange(m, X.ky, 3, st))) return e;
-      k_bi_v<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.ky, X.krh, X.kv, X.partials, X.ticket, X.d_ctl, red);
+      k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.kp, X.d_ctl);
+      if ((e = halo_exchange(m, X.kp, 3, st))) return e;
+      k_bi_v<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.udinv, X.ucoef, X.kp, X.krh, X.kv, X.partials, X.ticket,
+                                         X.d_ctl, red);
       if ((e = fin(S, X, CTL_BI_V, 3, st))) return e;
-      k_bi_s<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.ks, X.partials, X.ticket, X.d_ctl, red);
-      if ((e = fin(S, X, CTL_BI_S, 3, st))) return e;
-      if ((e = halo_exchange(m, X.ks, 3, st))) return e;
-      k_bi_t<T><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.ks, X.kt, X.partials, X.ticket, X.d_ctl, red);
-      if ((e = fin(S, X, CTL_BI_T, 6, st))) return e;
-      k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.ky, X.ks, X.kt, X.krh, x, X.kr, X.partials, X.ticket,
+      if ((e = halo_exchange(m, X.kr, 3, st)) || (e = halo_exchange(m, X.kv, 3, st))) return e;
+      k_bi_t<T><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket, X.d_ctl, red);
+      if ((e = fin(S, X, CTL_BI_T, 9, st))) return e;
+      k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.kp, X.kv, X.kt, X.krh, x, X.kr, X.partials, X.ticket,
                                          X.d_ctl, red);
       if ((e = fin(S, X, CTL_BI_X, 6, st))) return e;
-      S->n_launch += 5;
+      S->n_launch += 4;
     }
     DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, 3 * sizeof(KCtl), cudaMemcpyDeviceToHost, st));
     DFVM_CUDA(cudaStreamSynchronize(st));
