@@ -56,16 +56,22 @@ constexpr int kMaxLevels = 16;
 //                    doubles per level, and deep levels are launch-bound)
 //   DFVM_AMG_OMEGA   coarse-correction scale (symmetric over-correction,
 //                    < 2 keeps M SPD with adjoint smoothers)   default 1.8
+//   DFVM_AMG_SIGMA   1: renumber aggregates by row length within windows of
+//                    256 (less SELL padding); 0: creation order      default 1
+//   DFVM_AMG_GROUP   1: 4/8 lanes per row on long or few coarse rows; 0: one
+//                    thread per row                                  default 1
 //   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
 //                    exactly with a dense inverse (Gauss-Jordan once per
 //                    matrix update, one block), larger ones with
 //                    DFVM_AMG_SWEEPS l1-Jacobi sweeps (0: always sweeps)  default 512
 struct AmgParams {
-  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax;
+  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, sigma = 1, group = 1;
   bool wcycle = true;
   double omega = 1.8;
   AmgParams() {
     if (const char* e = getenv("DFVM_AMG_DIRECT")) direct = std::max(0, std::min(kDirectMax, atoi(e)));
+    if (const char* e = getenv("DFVM_AMG_SIGMA")) sigma = atoi(e);
+    if (const char* e = getenv("DFVM_AMG_GROUP")) group = atoi(e);
     if (const char* e = getenv("DFVM_AMG_OMEGA")) omega = atof(e);
     if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kCoarseMax, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_SWEEPS")) sweeps = std::max(1, atoi(e));
@@ -228,7 +234,7 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     int nc = 0;
     std::vector<int> agg = aggregate(F, nc);
     if (nc >= F.n * 0.85) break;           // coarsening stalled
-    {   // SELL-32-sigma: renumber the aggregates so that, within windows of 256
+    if (A->prm.sigma) {   // SELL-32-sigma: renumber the aggregates so that, within windows of 256
         // (8 slices, locality kept), rows are sorted by length: less padding
         // in the coarse SELL (35 % -> a few % on the C5 level 1)
       std::vector<std::vector<int>> members(nc);
@@ -324,7 +330,7 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     D.n = nc; D.n_slices = S; D.n_sell = C.ms_ptr[S];
     {   // grouped kernels where rows are long or few (latency-bound otherwise)
       const double avg = (double)ccol.size() / std::max(1, nc);
-      D.G = (avg >= 12.0 || nc < 50000) ? 8 : (avg >= 6.0 ? 4 : 1);
+      D.G = !A->prm.group ? 1 : (avg >= 12.0 || nc < 50000) ? 8 : (avg >= 6.0 ? 4 : 1);
     }
     int *p0, *p1, *p2;
     if ((st = A->up(&p0, C.ms_ptr)) || (st = A->up(&p1, C.ms_len)) || (st = A->up(&p2, C.mnb)) ||

@@ -1362,8 +1362,8 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   // disables.
   typename SolverT<T>::ChunkGraph* graph = nullptr;
   if (m->part.P == 1 && !X.graphs_off && st != nullptr) {   // (the legacy default stream cannot be captured)
-    static const bool env_off = getenv("DFVM_GRAPHS") && getenv("DFVM_GRAPHS")[0] == '0';
-    if (env_off) X.graphs_off = true;
+    const char* genv = getenv("DFVM_GRAPHS");
+    if (genv && genv[0] == '0') X.graphs_off = true;
     for (auto& g : X.graphs)
       if (g.x == x && g.b == b && g.timing == S->timing) graph = &g;
     if (!graph && !X.graphs_off) {

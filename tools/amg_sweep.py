@@ -25,7 +25,8 @@ mesh = dfvm.Mesh(case.raw)
 geo = mesh.export_geometry()
 U0, p0, phi0 = case.initial_state(geo["xc"], geo["xf"], geo["Sf"])
 B = case.apply_bcs(dfvm.BCs(mesh))
-stream = torch.cuda.current_stream()
+stream = torch.cuda.Stream()          # non-default: the library replays CUDA graphs there
+torch.cuda.set_stream(stream)
 import ctypes as C  # noqa: E402
 sp = C.c_void_p(stream.cuda_stream)
 keys = ["DFVM_AMG_COARSE", "DFVM_AMG_SWEEPS", "DFVM_AMG_CYCLE", "DFVM_AMG_WMAX", "DFVM_AMG_OMEGA",
