@@ -57,6 +57,8 @@ def lib():
         L.orc_bcs_destroy.argtypes = [vp]
         L.orc_bcs_set.argtypes = [vp, i32, ch, i32, vp, f64, vp, f64]
         L.orc_bcs_set_wk_value.argtypes = [vp, i32, f64]
+        L.orc_bcs_set_waveform.argtypes = [vp, i32, ch, f64, i32, vp, vp]
+        L.orc_bcs_set_time.argtypes = [vp, f64]
         L.orc_interpolate.argtypes = [vp, vp, ch, i32, vp, vp]
         L.orc_grad.argtypes = [vp, vp, ch, i32, vp, vp]
         L.orc_grad_faces.argtypes = [vp, i32, vp, vp]
@@ -231,6 +233,18 @@ class BCs:
     def set_wk_value(self, patch, v):
         lib().orc_bcs_set_wk_value(self.h, patch, v)
 
+    def set_waveform(self, patch, fld, period, a, b=None):
+        """Time-varying multiplier g(t) = a0 + sum_k a_k cos(2 pi k t/T) + b_k sin(2 pi k t/T)
+        of the patch's fixed-value / parabolic value (reading A-41)."""
+        a = np.ascontiguousarray(a, np.float64)
+        nh = len(a) - 1
+        bb = np.zeros(nh + 1) if b is None else np.ascontiguousarray(b, np.float64)
+        assert len(bb) == nh + 1
+        _check(lib().orc_bcs_set_waveform(self.h, patch, fld.encode(), period, nh, _p(a), _p(bb)))
+
+    def set_time(self, t):
+        lib().orc_bcs_set_time(self.h, t)
+
 
 def windkessel_update(pc, Q, dt, Rp, Cc, Rd, scheme=0):
     """O-8 (eq:windkessel_discrete P:420-425; scheme 0 exact, 1 FE, 2 BE)."""
@@ -244,12 +258,16 @@ class Solver:
 
     def __init__(self, mesh, bcs, nu, dt, rho=1.0, n_corr=2, n_nonorth=0, convection="upwind",
                  p_ref_cell=0, p_ref_value=0.0, direct=False, p_tol=1e-14, p_rel_tol=0.0,
-                 p_rel_tol_final=0.0, p_maxit=50000, U_tol=1e-14, U_rel_tol=0.0, U_maxit=50000, p_precond=None):
+                 p_rel_tol_final=0.0, p_maxit=50000, U_tol=1e-14, U_rel_tol=0.0, U_maxit=50000, p_precond=None,
+                 theta=1.0):
         # p_precond is accepted for recipe compatibility and ignored: the oracle
         # always uses Jacobi CG (or dense LU); the converged pressure does not
         # depend on the preconditioner (A-14)
         self.mesh, self.bcs = mesh, bcs
-        d = np.array([nu, dt, rho, p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, U_tol, U_rel_tol], np.float64)
+        # theta: time scheme of the momentum / transport predictor (Table 1 P:388,
+        # reading A-40): 1 backward Euler, 0.5 Crank-Nicolson, 0 forward Euler
+        d = np.array([nu, dt, rho, p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, U_tol, U_rel_tol, theta],
+                     np.float64)
         i = np.array([n_corr, n_nonorth, {"upwind": 0, "central": 1, "sou": 2, "quick": 3}[convection], p_ref_cell,
                       1 if direct else 0, p_maxit, U_maxit], np.int64)
         self.h = lib().orc_solver_create(mesh.h, bcs.h, _p(d), _p(i))

@@ -58,6 +58,10 @@ struct BC {
   int kind = BC_UNSET;
   double value[3] = {0, 0, 0};
   double u_max = 0, center[3] = {0, 0, 0}, radius = 1;
+  // time-varying multiplier of a fixed / parabolic value (
+  // reading A-41): g(t) = a_0 + sum_{k=1..nh} a_k cos(2 pi k t/T) + b_k sin(2 pi k t/T)
+  int nh = -1;                 // -1: steady
+  double period = 1, wa[17] = {0}, wb[17] = {0};
 };
 
 struct BCs {
@@ -65,7 +69,9 @@ struct BCs {
   // per patch, per field 0 = 'U', 1 = 'p', 2 = 's' (generic scalar)
   std::vector<BC> bc[3];
   std::vector<double> wk_value;   // per patch: current Windkessel p BC value (p_o / rho)
+  double t_eval = 0;              // time at which time-varying values are evaluated (t^{n+1} in a step)
 };
+double waveform(const BC& bc, double t);
 
 int field_index(char fld);
 

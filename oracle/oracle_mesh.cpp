@@ -281,6 +281,18 @@ bool is_fixed(const BCs& b, int fi, int64_t p) {
 // phi_b (SURVEY.md §8(c) O-4 "Interpolation"): fixedValue -> value, parabolic
 // u_b = -U_max (1 - r^2/R^2) n_out (A-18), zeroGradient -> phi_O,
 // Windkessel p -> p_o / rho (A-19).
+// time-varying inflow multiplier ("time-varying inflow profiles",
+// P:582 "pulsatile parabolic velocity profile"; reading A-41: a truncated
+// Fourier series of period T, the harmonics summed in ascending k)
+double waveform(const BC& bc, double t) {
+  double g = bc.wa[0];
+  for (int k = 1; k <= bc.nh; ++k) {
+    const double w = 2.0 * M_PI * k * t / bc.period;
+    g += bc.wa[k] * std::cos(w) + bc.wb[k] * std::sin(w);
+  }
+  return g;
+}
+
 void boundary_value(const Mesh& m, const BCs& b, int fi, int ncomp, const double* x,
                     int64_t f, double* out) {
   const int p = m.face_patch[f - m.F];
@@ -289,6 +301,7 @@ void boundary_value(const Mesh& m, const BCs& b, int fi, int ncomp, const double
   switch (bc.kind) {
     case BC_FIXED:
       for (int k = 0; k < ncomp; ++k) out[k] = bc.value[k];
+      if (bc.nh >= 0) { const double g = waveform(bc, b.t_eval); for (int k = 0; k < ncomp; ++k) out[k] *= g; }
       break;
     case BC_PARABOLIC: {
       const double* S = &m.Sf[3 * f];
@@ -298,6 +311,7 @@ void boundary_value(const Mesh& m, const BCs& b, int fi, int ncomp, const double
       const double A = norm3(S);
       const double mag = bc.u_max * (1.0 - rr / (bc.radius * bc.radius));
       for (int k = 0; k < ncomp; ++k) out[k] = -mag * S[k] / A;
+      if (bc.nh >= 0) { const double g = waveform(bc, b.t_eval); for (int k = 0; k < ncomp; ++k) out[k] *= g; }
       break;
     }
     case BC_WINDKESSEL:
@@ -499,6 +513,20 @@ int orc_bcs_set(void* bp, int32_t patch, char fld, int kind, const double* value
   return OK;
 }
 void orc_bcs_set_wk_value(void* bp, int32_t patch, double v) { ((BCs*)bp)->wk_value[patch] = v; }
+// time-varying multiplier g(t) of patch's fixed / parabolic value of field fld ('U' or 'p')
+int orc_bcs_set_waveform(void* bp, int32_t patch, char fld, double period, int32_t nh, const double* a,
+                         const double* bcoef) {
+  BCs* b = (BCs*)bp;
+  const int fi = field_index(fld);
+  if (fi < 0 || fi > 1 || patch < 0 || patch >= (int)b->m->pkind.size() || nh < 0 || nh > 16 || !(period > 0) || !a) {
+    set_error(E_INVALID_ARG, "bad waveform", patch); return E_INVALID_ARG;
+  }
+  BC& c = b->bc[fi][patch];
+  c.nh = nh; c.period = period;
+  for (int k = 0; k <= 16; ++k) { c.wa[k] = k <= nh ? a[k] : 0; c.wb[k] = (k <= nh && k > 0 && bcoef) ? bcoef[k] : 0; }
+  return OK;
+}
+void orc_bcs_set_time(void* bp, double t) { ((BCs*)bp)->t_eval = t; }
 
 int orc_interpolate(const void* mp, const void* bp, char fld, int ncomp, const double* x, double* xf) {
   const Mesh& m = *(const Mesh*)mp; const BCs& b = *(const BCs*)bp;

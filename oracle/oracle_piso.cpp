@@ -184,6 +184,7 @@ static int windkessel(double pc, double Q, double dt, double Rp, double Cc, doub
 // --------------------------------------------------------------- solver
 struct Opts {
   double nu, dt, rho;
+  double theta;                       // time scheme (Table 1): 1 backward Euler, 0.5 Crank-Nicolson, 0 forward Euler
   int n_corr, n_nonorth, convection;  // convection 0 upwind, 1 central
   int64_t p_ref_cell;
   double p_ref_value;
@@ -231,6 +232,10 @@ static SolveReport solve(const Solver& S, const LDU& A, const double* rhs, doubl
 // x_f^HO = x_C + 1/2 [(grad x)_C . d_Cf + (x_D - x_C)(d_Cf . d_CD)/|d_CD|^2]
 // (SPEC.md:233 reading), C the upwind and D the downwind cell; the
 // correction leaves the owner row (b_O -= c) and enters the neighbour row.
+// Time scheme (Table 1, reading A-40): the theta method on the spatial
+// operator A_s (convection + diffusion; b_s its explicit sources),
+//   (V/dt + theta A_s) x* = V/dt x^n + b_s - (1 - theta) A_s x^n,
+// theta = 1 backward Euler (A-11), 1/2 Crank-Nicolson, 0 forward Euler.
 static void assemble_transport(const Solver& S, int nc, int fi, double diffusivity, const double* U,
                                const double* phi, LDU& M, std::vector<double>& bvec) {
   const Mesh& m = *S.m;
@@ -243,13 +248,8 @@ static void assemble_transport(const Solver& S, int nc, int fi, double diffusivi
   std::vector<double> G((size_t)3 * nc * N);
   grad(m, b, fi, nc, U, G.data());
   auto lambda = [&](int64_t f, double md) { return conv == 1 ? m.w[f] : (md >= 0 ? 1.0 : 0.0); };
-  // cell-wise accumulation in ascending face order (the time term, a
-  // per-cell constant, is added first to keep the order explicit)
-  for (int64_t c = 0; c < N; ++c) {
-    const double vdt = m.V[c] / dt;
-    M.diag[c] = vdt;
-    for (int k = 0; k < nc; ++k) bvec[(size_t)nc * c + k] = vdt * U[(size_t)nc * c + k];
-  }
+  // spatial part: cell-wise accumulation in ascending face order into
+  // M.diag (= diag of A_s) and bvec (= b_s); the time term and theta after
   for (int64_t f = 0; f < m.F; ++f) {
     const double md = phi[f];
     const double lam = lambda(f, md);
@@ -311,6 +311,24 @@ static void assemble_transport(const Solver& S, int nc, int fi, double diffusivi
       }
     }
   }
+  // time term and theta weighting: b = V/dt x^n + b_s - (1 - theta) (A_s x^n),
+  // diag = V/dt + theta diag_s, off-diagonals theta a_s
+  const double th = S.o.theta;
+  for (int64_t c = 0; c < N; ++c) {
+    const double vdt = m.V[c] / dt;
+    for (int k = 0; k < nc; ++k) {
+      double ax = M.diag[c] * U[(size_t)nc * c + k];
+      for (int64_t i = m.cptr[c]; i < m.cptr[c + 1]; ++i) {
+        const int64_t f = m.cface[i];
+        if (f >= m.F) continue;
+        if (m.owner[f] == c) ax += M.upper[f] * U[(size_t)nc * m.neigh[f] + k];
+        else ax += M.lower[f] * U[(size_t)nc * m.owner[f] + k];
+      }
+      bvec[(size_t)nc * c + k] = vdt * U[(size_t)nc * c + k] + bvec[(size_t)nc * c + k] - (1.0 - th) * ax;
+    }
+  }
+  for (int64_t c = 0; c < N; ++c) M.diag[c] = m.V[c] / dt + th * M.diag[c];
+  for (int64_t f = 0; f < m.F; ++f) { M.upper[f] *= th; M.lower[f] *= th; }
 }
 
 static void assemble_momentum(const Solver& S, const double* U, const double* phi, LDU& M,
@@ -381,6 +399,14 @@ static int piso_step(Solver& S, double* U, double* p, double* phi, Report& R) {
   BCs& b = *S.b;
   const int64_t N = m.N;
   std::memset(&R, 0, sizeof(R));
+  // 0. time-varying boundary values at the new time level t^{n+1} (A-41)
+  for (int fi = 0; fi < 2; ++fi)
+    for (size_t pt = 0; pt < m.pkind.size(); ++pt)
+      if (b.bc[fi][pt].nh >= 0 && b.bc[fi][pt].kind != BC_FIXED && b.bc[fi][pt].kind != BC_PARABOLIC) {
+        set_error(E_INVALID_ARG, "time-varying waveform on a patch that is not fixed-value / parabolic", (int64_t)pt);
+        return E_INVALID_ARG;
+      }
+  b.t_eval = S.t + S.o.dt;
   // 1. assemble O-5 from (U^n, phi^n, grad U^n)
   LDU M;
   std::vector<double> bvec;
@@ -545,7 +571,7 @@ int orc_ldu_apply(const void* mp, const double* diag, const double* lower, const
 }
 
 void* orc_solver_create(const void* mp, void* bp, const double* dopts, const int64_t* iopts) {
-  // dopts: nu, dt, rho, p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, U_tol, U_rel_tol
+  // dopts: nu, dt, rho, p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, U_tol, U_rel_tol, theta
   // iopts: n_corr, n_nonorth, convection, p_ref_cell, direct, p_maxit, U_maxit
   Solver* S = new Solver();
   S->m = (const Mesh*)mp;
@@ -553,7 +579,7 @@ void* orc_solver_create(const void* mp, void* bp, const double* dopts, const int
   Opts& o = S->o;
   o.nu = dopts[0]; o.dt = dopts[1]; o.rho = dopts[2]; o.p_ref_value = dopts[3];
   o.p_tol = dopts[4]; o.p_rel_tol = dopts[5]; o.p_rel_tol_final = dopts[6];
-  o.U_tol = dopts[7]; o.U_rel_tol = dopts[8];
+  o.U_tol = dopts[7]; o.U_rel_tol = dopts[8]; o.theta = dopts[9];
   o.n_corr = (int)iopts[0]; o.n_nonorth = (int)iopts[1]; o.convection = (int)iopts[2];
   o.p_ref_cell = iopts[3]; o.direct = (int)iopts[4]; o.p_maxit = (int)iopts[5]; o.U_maxit = (int)iopts[6];
   return S;
