@@ -214,6 +214,21 @@ typedef struct dfvm_bcs dfvm_bcs;
 dfvm_status dfvm_bcs_create(dfvm_mesh* m, dfvm_bcs** out);
 dfvm_status dfvm_bcs_set(dfvm_bcs* b, int32_t patch, char field, const dfvm_bc_desc* desc);
 dfvm_status dfvm_bcs_destroy(dfvm_bcs* b);
+/* Time-varying boundary value (Table 1 P:393 "time-varying inflow", P:401,
+ * P:582 "a pulsatile parabolic velocity profile"; reading A-41):
+ * the fixed-value or parabolic value of (patch, field) is multiplied by
+ *   g(t) = a[0] + sum_{k=1..n_harmonics} a[k] cos(2 pi k t/period) + b[k] sin(2 pi k t/period),
+ * evaluated on the host in fp64 at the time the values are used: t^{n+1} =
+ * t^n + dt in dfvm_piso_step (the solver's time starts at 0 and advances by
+ * dt per step), else the time of the last dfvm_bcs_set_time (initially 0).
+ * field 'U' or 'p'; a[n_harmonics + 1], b[n_harmonics + 1] (b[0] unused;
+ * b may be NULL = all zero) are copied.  n_harmonics in [0, 16], period > 0,
+ * else DFVM_E_INVALID_ARG; a step whose waveform patch is not fixed-value /
+ * parabolic fails with DFVM_E_INVALID_ARG. */
+dfvm_status dfvm_bcs_set_waveform(dfvm_bcs* b, int32_t patch, char field, double period, int32_t n_harmonics,
+                                  const double* a, const double* bcoef);
+/* evaluate every waveform at time t (device values updated on `stream`) */
+dfvm_status dfvm_bcs_set_time(dfvm_bcs* b, double t, dfvm_stream stream);
 
 /* ------------------------------------------------------------ operators
  * Asynchronous on `stream`; each performs the halo exchange of its input
@@ -251,7 +266,14 @@ typedef struct {
                                    2 the same AMG with its hierarchy stored and cycled in fp32 under
                                    an fp64 PCG (residual, dots and iterates stay fp64; = 1 for fp32
                                    solvers).  Out of range -> DFVM_E_ARG. */
+  int32_t time_scheme;          /* momentum / transport time scheme (Table 1; A-40, the
+                                   theta method on the spatial operator A_s:
+                                   (V/dt + theta A_s) x* = V/dt x^n + b_s - (1 - theta) A_s x^n):
+                                   DFVM_TIME_BACKWARD_EULER (0, theta 1, default), DFVM_TIME_CRANK_NICOLSON
+                                   (theta 1/2), DFVM_TIME_FORWARD_EULER (theta 0: diagonal predictor).
+                                   Out of range -> DFVM_E_INVALID_ARG. */
 } dfvm_piso_opts;
+enum { DFVM_TIME_BACKWARD_EULER = 0, DFVM_TIME_CRANK_NICOLSON = 1, DFVM_TIME_FORWARD_EULER = 2 };
 
 /* Krylov stopping rule (A-13): b = 0 -> x = 0, 0 iterations; else
  * stop when ||r||_2 <= max(tol ||b||_2, rel_tol ||r_0||_2), or at maxit; for

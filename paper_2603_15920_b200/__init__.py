@@ -41,6 +41,7 @@ SYMBOLS = [
     "dfvm_windkessel_state", "dfvm_windkessel_update", "dfvm_solver_destroy", "dfvm_kernel_launches",
     "dfvm_solver_set_timing", "dfvm_solver_get_timing", "dfvm_comm_create_local", "dfvm_solver_amg_levels",
     "dfvm_transport_step", "dfvm_momentum_apply_transpose", "dfvm_pressure_solve_adjoint", "dfvm_pressure_vjp",
+    "dfvm_bcs_set_waveform", "dfvm_bcs_set_time",
 ]
 
 
@@ -79,7 +80,8 @@ class PisoOpts(C.Structure):
                 ("n_nonorth", C.c_int32), ("convection", C.c_int32), ("p_ref_cell", C.c_int64),
                 ("p_ref_value", C.c_double), ("p_tol", C.c_double), ("p_rel_tol", C.c_double),
                 ("p_rel_tol_final", C.c_double), ("p_maxit", C.c_int32), ("U_tol", C.c_double),
-                ("U_rel_tol", C.c_double), ("U_maxit", C.c_int32), ("p_precond", C.c_int32)]
+                ("U_rel_tol", C.c_double), ("U_maxit", C.c_int32), ("p_precond", C.c_int32),
+                ("time_scheme", C.c_int32)]
 
 
 class SolveReport(C.Structure):
@@ -123,6 +125,8 @@ def lib():
         L.dfvm_bcs_create.argtypes = [vp, C.POINTER(vp)]
         L.dfvm_bcs_set.argtypes = [vp, i32, C.c_char, C.POINTER(BcDesc)]
         L.dfvm_bcs_destroy.argtypes = [vp]
+        L.dfvm_bcs_set_waveform.argtypes = [vp, i32, C.c_char, f64, i32, vp, vp]
+        L.dfvm_bcs_set_time.argtypes = [vp, f64, vp]
         L.dfvm_fvc_interpolate.argtypes = [vp, vp, vp, C.c_char, vp, vp]
         L.dfvm_fvc_grad.argtypes = [vp, vp, vp, C.c_char, vp, vp]
         L.dfvm_fvc_grad_faces.argtypes = [vp, vp, vp, vp]
@@ -367,6 +371,20 @@ class BCs:
         _check(lib().dfvm_bcs_set(self.h, patch, fld.encode(), C.byref(d)))
         return self
 
+    def set_waveform(self, patch, fld, period, a, b=None):
+        """Time-varying multiplier g(t) = a0 + sum_k a_k cos(2 pi k t/T) + b_k sin(2 pi k t/T)
+        of a fixed-value / parabolic patch value (dfvm_bcs_set_waveform; A-41)."""
+        a = np.ascontiguousarray(a, np.float64)
+        bb = np.zeros(len(a)) if b is None else np.ascontiguousarray(b, np.float64)
+        assert len(bb) == len(a)
+        _check(lib().dfvm_bcs_set_waveform(self.h, patch, fld.encode(), period, len(a) - 1,
+                                           a.ctypes.data, bb.ctypes.data))
+        return self
+
+    def set_time(self, t, stream=None):
+        _check(lib().dfvm_bcs_set_time(self.h, t, stream))
+        return self
+
 
 # ------------------------------------------------------------------ operators
 def interpolate(mesh, x, bcs, fld, out, stream=None):
@@ -410,12 +428,16 @@ class Solver:
 
     def __init__(self, mesh, bcs, nu, dt, rho=1.0, n_corr=2, n_nonorth=0, convection="upwind", p_ref_cell=0,
                  p_ref_value=0.0, p_tol=1e-14, p_rel_tol=0.0, p_rel_tol_final=0.0, p_maxit=50000, U_tol=1e-14,
-                 U_rel_tol=0.0, U_maxit=50000, p_precond="jacobi"):
+                 U_rel_tol=0.0, U_maxit=50000, p_precond="jacobi", theta=1.0):
         self.mesh, self.bcs = mesh, bcs
+        # time scheme (Table 1): theta 1 backward Euler, 0.5 Crank-Nicolson, 0 forward Euler
+        schemes = {1.0: 0, 0.5: 1, 0.0: 2}
+        if float(theta) not in schemes:
+            raise ValueError(f"theta must be 1, 0.5 or 0 (backward Euler, Crank-Nicolson, forward Euler), got {theta}")
         o = PisoOpts(nu, dt, rho, n_corr, n_nonorth, {"upwind": 0, "central": 1, "sou": 2, "quick": 3}[convection],
                      p_ref_cell,
                      p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, p_maxit, U_tol, U_rel_tol, U_maxit,
-                     {"jacobi": 0, "amg": 1, "amg32": 2}[p_precond])
+                     {"jacobi": 0, "amg": 1, "amg32": 2}[p_precond], schemes[float(theta)])
         h = C.c_void_p()
         _check(lib().dfvm_solver_create(mesh.h, bcs.h, C.byref(o), C.byref(h)))
         self.h = h.value

@@ -219,7 +219,66 @@ dfvm_status bcs_device(dfvm_bcs* b, int slot, cudaStream_t s) {
   }
   DFVM_CUDA(cudaMemcpy(b->d_kind[slot], b->h_kind[slot].data(), b->h_kind[slot].size(), cudaMemcpyHostToDevice));
   DFVM_CUDA(cudaMemcpy(b->d_val[slot], b->h_valT[slot].data(), nval * bytesT, cudaMemcpyHostToDevice));
+  // time-varying patches (A-41): steady base values + per-face wave index
+  b->wave_patches[slot].clear();
+  for (size_t p = 0; p < H.pkind.size(); ++p)
+    if (H.pkind[p] != DFVM_PATCH_EMPTY && b->wave[slot][p].nh >= 0) {
+      const int k = b->spec[slot][p].kind;
+      if (k != DFVM_BC_FIXED_VALUE && k != DFVM_BC_PARABOLIC) {
+        set_error(DFVM_E_INVALID_ARG, "time-varying waveform on patch '" + H.pname[p] +
+                  "' which is not fixed-value / parabolic", (int64_t)p);
+        return DFVM_E_INVALID_ARG;
+      }
+      b->wave_patches[slot].push_back((int)p);
+    }
+  if (!b->wave_patches[slot].empty()) {
+    if ((int)b->wave_patches[slot].size() > kMaxWaves) {
+      set_error(DFVM_E_INVALID_ARG, "more than 16 time-varying patches for one field");
+      return DFVM_E_INVALID_ARG;
+    }
+    std::vector<int8_t> wid(std::max<int64_t>(B, 1), -1);
+    for (int64_t i = 0; i < B; ++i) {
+      const int p = H.bpatch[P.lb_gid[i] - H.F];
+      for (size_t j = 0; j < b->wave_patches[slot].size(); ++j)
+        if (b->wave_patches[slot][j] == p) wid[i] = (int8_t)j;
+    }
+    if (!b->d_base[slot]) {
+      DFVM_CUDA(cudaMalloc(&b->d_base[slot], nval * bytesT));
+      DFVM_CUDA(cudaMalloc(&b->d_wid[slot], wid.size()));
+    }
+    DFVM_CUDA(cudaMemcpy(b->d_base[slot], b->h_valT[slot].data(), nval * bytesT, cudaMemcpyHostToDevice));
+    DFVM_CUDA(cudaMemcpy(b->d_wid[slot], wid.data(), wid.size(), cudaMemcpyHostToDevice));
+  }
   b->dirty[slot] = false;
+  if (!b->wave_patches[slot].empty()) count_launch();
+  return bcs_time(b, slot, b->t_eval, s);
+}
+
+// g(t) of a patch wave: a0 + sum_k a_k cos(2 pi k t/T) + b_k sin(2 pi k t/T), ascending k (A-41)
+static double wave_g(const dfvm_bcs::Wave& w, double t) {
+  double g = w.a[0];
+  for (int k = 1; k <= w.nh; ++k) {
+    const double x = 2.0 * M_PI * k * t / w.period;
+    g += w.a[k] * std::cos(x) + w.b[k] * std::sin(x);
+  }
+  return g;
+}
+
+dfvm_status bcs_time(dfvm_bcs* b, int slot, double t, cudaStream_t s) {
+  b->t_eval = t;
+  if (b->dirty[slot] || b->wave_patches[slot].empty()) return DFVM_OK;
+  const int nc = slot == 0 ? 3 : 1;
+  const int64_t B = b->m->part.n_lb;
+  if (b->m->precision == DFVM_F64) {
+    WaveG<double> g{};
+    for (size_t j = 0; j < b->wave_patches[slot].size(); ++j) g.g[j] = wave_g(b->wave[slot][b->wave_patches[slot][j]], t);
+    launch_bc_wave<double>((double*)b->d_val[slot], (const double*)b->d_base[slot], b->d_wid[slot], B, nc, g, s);
+  } else {
+    WaveG<float> g{};
+    for (size_t j = 0; j < b->wave_patches[slot].size(); ++j) g.g[j] = (float)wave_g(b->wave[slot][b->wave_patches[slot][j]], t);
+    launch_bc_wave<float>((float*)b->d_val[slot], (const float*)b->d_base[slot], b->d_wid[slot], B, nc, g, s);
+  }
+  DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
 }
 
@@ -493,6 +552,7 @@ dfvm_status dfvm_bcs_create(dfvm_mesh* m, dfvm_bcs** out) {
   for (int i = 0; i < 3; ++i) {
     b->spec[i].assign(m->H.pkind.size(), dfvm_bc_desc{});
     b->set[i].assign(m->H.pkind.size(), 0);
+    b->wave[i].assign(m->H.pkind.size(), dfvm_bcs::Wave{});
   }
   *out = b;
   return DFVM_OK;
@@ -520,11 +580,42 @@ dfvm_status dfvm_bcs_set(dfvm_bcs* b, int32_t patch, char field, const dfvm_bc_d
   return DFVM_OK;
 }
 
+dfvm_status dfvm_bcs_set_waveform(dfvm_bcs* b, int32_t patch, char field, double period, int32_t nh,
+                                  const double* a, const double* bc) {
+  CHECK_ARG(b && a, "NULL argument");
+  const int slot = field_slot(field);
+  if (slot < 0 || slot > 1 || patch < 0 || patch >= (int32_t)b->m->H.pkind.size() || nh < 0 || nh > 16 ||
+      !(period > 0)) {
+    set_error(DFVM_E_INVALID_ARG, "bad waveform (field 'U' or 'p', 0 <= n_harmonics <= 16, period > 0)", patch);
+    return DFVM_E_INVALID_ARG;
+  }
+  dfvm_bcs::Wave w;
+  w.nh = nh; w.period = period;
+  for (int k = 0; k <= nh; ++k) { w.a[k] = a[k]; w.b[k] = (k > 0 && bc) ? bc[k] : 0.0; }
+  b->wave[slot][patch] = w;
+  b->dirty[slot] = true;
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_bcs_set_time(dfvm_bcs* b, double t, dfvm_stream stream) {
+  CHECK_ARG(b, "NULL argument");
+  b->t_eval = t;
+  for (int slot = 0; slot < 2; ++slot)
+    if (!b->dirty[slot]) {
+      dfvm_status st = bcs_time(b, slot, t, (cudaStream_t)stream);
+      if (st) return st;
+      if (!b->wave_patches[slot].empty()) count_launch();
+    }
+  return DFVM_OK;
+}
+
 dfvm_status dfvm_bcs_destroy(dfvm_bcs* b) {
   if (!b) return DFVM_OK;
   for (int i = 0; i < 3; ++i) {
     if (b->d_kind[i]) cudaFree(b->d_kind[i]);
     if (b->d_val[i]) cudaFree(b->d_val[i]);
+    if (b->d_base[i]) cudaFree(b->d_base[i]);
+    if (b->d_wid[i]) cudaFree(b->d_wid[i]);
   }
   delete b;
   return DFVM_OK;

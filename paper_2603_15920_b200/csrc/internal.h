@@ -161,9 +161,21 @@ struct dfvm_bcs {
   std::vector<uint8_t> h_kind[3];
   std::vector<double> h_val[3];
   std::vector<char> h_valT[3];  // staging in mesh precision
+  // time-varying multipliers (A-41), per field slot and patch: nh < 0 = steady
+  struct Wave { int nh = -1; double period = 1, a[17] = {0}, b[17] = {0}; };
+  std::vector<Wave> wave[3];
+  double t_eval = 0;
+  void* d_base[3] = {nullptr, nullptr, nullptr};   // steady values (mesh precision) of wave slots
+  int8_t* d_wid[3] = {nullptr, nullptr, nullptr};  // per boundary face: patch-wave index or -1
+  std::vector<int> wave_patches[3];                // patches with a wave, in index order
 };
 
 namespace dfvm {
 int field_slot(char fld);  // 'U' 0, 'p' 1, 's' 2, else -1
 dfvm_status bcs_device(dfvm_bcs* b, int slot, cudaStream_t s);  // validate + upload
+dfvm_status bcs_time(dfvm_bcs* b, int slot, double t, cudaStream_t s);  // apply waveforms at time t
+constexpr int kMaxWaves = 16;
+template <class T> struct WaveG { T g[kMaxWaves]; };
+template <class T>
+void launch_bc_wave(T* val, const T* base, const int8_t* wid, int64_t B, int nc, const WaveG<T>& g, cudaStream_t s);
 }

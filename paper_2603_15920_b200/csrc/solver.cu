@@ -231,17 +231,22 @@ __device__ __forceinline__ void sell_apply(const DevMesh<T>& M, int s, int lane,
 template <class T, int NC>
 __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, const T* __restrict__ U,
     const T* __restrict__ phi, const T* __restrict__ gU, const T* __restrict__ gp, const uint8_t* __restrict__ bk,
-    const T* __restrict__ bv, T nu, T rdt, int conv, int kcorr, const V4<T>* __restrict__ fdO,
+    const T* __restrict__ bv, T nu, T rdt, T theta, int conv, int kcorr, const V4<T>* __restrict__ fdO,
     const V4<T>* __restrict__ fdN, T* __restrict__ udiag, T* __restrict__ bU, T* __restrict__ rhsU,
     T* __restrict__ ucoef, T* __restrict__ ucoefT) {
+  const bool explicit_part = theta != T(1);
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
     const T V = live ? M.vol[row] : T(0);
-    T diag = V * rdt;
-    T bb[NC];
+    T diag = T(0);           // diagonal of the spatial operator A_s
+    T bb[NC], xc[NC], ax[NC];  // b_s (explicit sources); x^n_c; sum_nb a_s x^n_nb (theta != 1)
 #pragma unroll
-    for (int k = 0; k < NC; ++k) bb[k] = live ? diag * U[NC * (int64_t)row + k] : T(0);
+    for (int k = 0; k < NC; ++k) {
+      bb[k] = T(0);
+      ax[k] = T(0);
+      xc[k] = live ? U[NC * (int64_t)row + k] : T(0);
+    }
     const int len = __ldg(&M.sl_len[s]);
     const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
     const int mbase = __ldg(&M.ms_ptr[s]) + lane;
@@ -259,9 +264,12 @@ __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, c
         T cf, cfT;   // this row's coefficient and the transposed one (the other row's, NEXT-3)
         if (own) { diag += lam * md + nd; cf = (T(1) - lam) * md - nd; cfT = -lam * md - nd; }
         else { diag += -(T(1) - lam) * md + nd; cf = -lam * md - nd; cfT = (T(1) - lam) * md - nd; }
-        ucoefT[mbase + 32 * mj] = cfT;
-        ucoef[mbase + 32 * (mj++)] = cf;
+        ucoefT[mbase + 32 * mj] = theta * cfT;
+        ucoef[mbase + 32 * (mj++)] = theta * cf;
         const int n = en.y;
+        if (explicit_part)
+#pragma unroll
+          for (int k = 0; k < NC; ++k) ax[k] += cf * U[NC * (int64_t)n + k];
         const int O = own ? row : n, N = own ? n : row;
         T cr[NC];
 #pragma unroll
@@ -318,11 +326,16 @@ __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, c
       }
     }
     if (live) {
-      udiag[row] = diag;
+      // theta method (Table 1, A-40): diag = V/dt + theta diag_s,
+      // b = V/dt x^n + b_s - (1 - theta) (A_s x^n)
+      const T vdt = V * rdt;
+      udiag[row] = vdt + theta * diag;
 #pragma unroll
       for (int k = 0; k < NC; ++k) {
-        bU[NC * (int64_t)row + k] = bb[k];
-        rhsU[NC * (int64_t)row + k] = gp ? bb[k] - V * gp[3 * (int64_t)row + k] : bb[k];
+        const T axk = diag * xc[k] + ax[k];
+        const T bk_ = vdt * xc[k] + bb[k] - (T(1) - theta) * axk;
+        bU[NC * (int64_t)row + k] = bk_;
+        rhsU[NC * (int64_t)row + k] = gp ? bk_ - V * gp[3 * (int64_t)row + k] : bk_;
       }
     }
   }
@@ -1152,6 +1165,7 @@ struct dfvm_solver {
   std::vector<WK> wk;
   bool wk_dirty = true;
   int n_launch = 0;
+  double t = 0;   // solver time t^n (advanced by dt per PISO step; time-varying BCs use t^n + dt, A-41)
   // live kernel timing (CUDA events on the launching stream): class 0 = the
   // PCG SpMV kernel, class 1 = one full PCG iteration (3 kernels)
   bool timing = false;
@@ -1162,6 +1176,11 @@ struct dfvm_solver {
 };
 
 namespace dfvm {
+
+// time scheme -> theta (Table 1, reading A-40)
+static double theta_of(const dfvm_piso_opts& o) {
+  return o.time_scheme == DFVM_TIME_CRANK_NICOLSON ? 0.5 : o.time_scheme == DFVM_TIME_FORWARD_EULER ? 0.0 : 1.0;
+}
 
 static bool solver_has_fixed_p(const dfvm_solver* S) {
   const HostMesh& H = S->m->H;
@@ -1495,7 +1514,7 @@ static dfvm_status assemble(dfvm_solver* S, SolverT<T>& X, const T* U, const T* 
   S->n_launch++;
   if ((s2 = halo_exchange(S->m, X.gU, 9, st))) return s2;
   k_transport_assemble<T, 3><<<gs, kThreads, 0, st>>>(M, U, phi, X.gU, X.gp, b->d_kind[0], (const T*)b->d_val[0],
-                                                      (T)S->o.nu, (T)(1.0 / S->o.dt), S->o.convection, S->kcorr,
+                                                      (T)S->o.nu, (T)(1.0 / S->o.dt), (T)theta_of(S->o), S->o.convection, S->kcorr,
                                                       X.fdO, X.fdN, X.udiag, X.bU, X.rhsU, X.ucoef, X.ucoefT);
   S->n_launch++;
   if ((s2 = halo_exchange(S->m, X.udiag, 1, st))) return s2;   // k_bi_t gathers s / diag
@@ -1514,6 +1533,9 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   S->n_launch = 0;
   std::memset(R, 0, sizeof(*R));
   if ((s2 = bcs_device(b, 0, st)) || (s2 = bcs_device(b, 1, st))) return s2;
+  // time-varying boundary values at the new time level t^{n+1} (A-41)
+  if ((s2 = bcs_time(b, 0, S->t + o.dt, st)) || (s2 = bcs_time(b, 1, S->t + o.dt, st))) return s2;
+  S->n_launch += (int)!b->wave_patches[0].empty() + (int)!b->wave_patches[1].empty();
   if ((s2 = sync_wk(S, X, st))) return s2;
   const int gs = grid_for_slices(M.n_slices), gf = grid_for((int64_t)M.F + M.B);
   const uint8_t* bkU = b->d_kind[0];
@@ -1613,6 +1635,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   }
   R->gpu_launches = S->n_launch;
   count_launch(S->n_launch);
+  S->t += o.dt;
   if (R->nonfinite) { set_error(DFVM_E_NONFINITE, "non-finite U or p after the PISO step"); return DFVM_E_NONFINITE; }
   return res;
 }
@@ -1639,7 +1662,7 @@ static dfvm_status transport_step_t(dfvm_solver* S, SolverT<T>& X, T* x, const T
   if ((e = halo_exchange(S->m, X.gp, 3, st))) return e;
   const int gs = grid_for_slices(M.n_slices), ge = grid_for(M.n_own);
   k_transport_assemble<T, 1><<<gs, kThreads, 0, st>>>(M, x, phi, X.gp, nullptr, b->d_kind[2], (const T*)b->d_val[2],
-                                                      (T)gamma, (T)(1.0 / S->o.dt), S->o.convection, S->kcorr,
+                                                      (T)gamma, (T)(1.0 / S->o.dt), (T)theta_of(S->o), S->o.convection, S->kcorr,
                                                       X.fdO, X.fdN, X.udiag, X.prhs0, X.prhs, X.ucoef, X.ucoefT);
   if ((e = halo_exchange(S->m, X.udiag, 1, st))) return e;
   k_pack3<T><<<ge, kThreads, 0, st>>>(M.n_own, X.prhs, X.bU);
@@ -1665,7 +1688,8 @@ dfvm_status dfvm_solver_create(dfvm_mesh* m, dfvm_bcs* b, const dfvm_piso_opts* 
   if (!m || !b || !opts || !out || b->m != m) { set_error(DFVM_E_INVALID_ARG, "NULL or mismatched argument"); return DFVM_E_INVALID_ARG; }
   if (!(opts->dt > 0) || !(opts->nu >= 0) || opts->n_corr < 1 || opts->n_corr > 8 || opts->n_nonorth < 0 ||
       (opts->n_corr * (opts->n_nonorth + 1)) > 16 || opts->p_maxit < 1 || opts->U_maxit < 1 || !(opts->rho > 0) ||
-      opts->p_precond < 0 || opts->p_precond > 2 || opts->convection < 0 || opts->convection > 3) {
+      opts->p_precond < 0 || opts->p_precond > 2 || opts->convection < 0 || opts->convection > 3 ||
+      opts->time_scheme < DFVM_TIME_BACKWARD_EULER || opts->time_scheme > DFVM_TIME_FORWARD_EULER) {
     set_error(DFVM_E_INVALID_ARG, "invalid PISO options");
     return DFVM_E_INVALID_ARG;
   }
