@@ -9,6 +9,7 @@
 // face within the bandwidth window).  No atomics: the per-cell sum runs over
 // the row's incidences in ascending face order (P:297-305 eq:aggregate
 // realised as a gather, reading A-20).
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "dev.cuh"
@@ -217,6 +218,177 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
   }
 }
 
+// ------------------------------------------------- grouped cell-gathers
+// G = 4 lanes share a row: a warp covers a quarter of a SELL-32 slice (8
+// rows), lane g of a row visits its incidences k = g, g + 4, ... in ascending
+// order and the 4 partial sums are combined by a fixed xor-shuffle tree,
+// (a0 + a1) + (a2 + a3), so every lane of the group holds the bitwise-same
+// total (deterministic; the per-row incidence order is the same in any
+// partition, so partitioned results stay bitwise those of one rank).  On
+// tets (4 incidences per row) every lane issues one face-record + neighbour
+// gather per row: one gather round trip per unit instead of a dependent
+// chain of batches, with few registers (full-wave grid by occupancy).  The
+// next unit's slice metadata and incidence record are prefetched while the
+// current gathers are in flight.
+constexpr int kG = 4;
+
+struct GroupCursor {   // the (slice, quarter) unit a warp works on
+  int u, len;
+  const int2* e;
+};
+template <class T>
+__device__ __forceinline__ GroupCursor group_unit(const DevMesh<T>& M, int u, int rl) {
+  GroupCursor c{u, 0, M.inc};
+  if (u < 4 * M.n_slices) {
+    const int s = u >> 2;
+    c.len = __ldg(&M.sl_len[s]);
+    c.e = M.inc + __ldg(&M.sl_ptr[s]) + rl;
+  }
+  return c;
+}
+
+template <class T>
+__device__ __forceinline__ T group_sum(T v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
+}
+
+template <class T, int NC, bool FACEVALS>
+__global__ void __launch_bounds__(kThreads) k_grad_g(DevMesh<T> M, const T* __restrict__ x,
+                                                     const uint8_t* __restrict__ bkind, const T* __restrict__ bval,
+                                                     const T* __restrict__ fv, T* __restrict__ G) {
+  const int lane = threadIdx.x & 31, g = lane & (kG - 1);
+  const int nw = (gridDim.x * blockDim.x) >> 5, n_units = 4 * M.n_slices;
+  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  GroupCursor cur = group_unit(M, u, (u & 3) * 8 + (lane >> 2));
+  int2 en = (g < cur.len) ? __ldg(&cur.e[g * 32]) : make_int2(0, -2);
+  for (; u < n_units; u += nw) {
+    const int rl = (u & 3) * 8 + (lane >> 2);
+    const int row = (u >> 2) * 32 + rl;
+    const bool live = row < M.n_own;
+    // prefetch the next unit's metadata
+    const int un = u + nw;
+    GroupCursor nxt = group_unit(M, un, (un & 3) * 8 + (lane >> 2));
+    T xc[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) xc[k] = (!FACEVALS && live) ? x[(int64_t)row * NC + k] : T(0);
+    T acc[NC][3];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) acc[k][0] = acc[k][1] = acc[k][2] = T(0);
+    const T Vc = live ? M.vol[row] : T(1);
+    for (int j = g; j < cur.len; j += kG) {
+      if (j != g) en = __ldg(&cur.e[j * 32]);
+      V4<T> gg = V4<T>{T(0), T(0), T(0), T(0)};
+      T v[NC];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) v[k] = T(0);
+      if (en.y >= 0) {
+        const int f = en.x >= 0 ? en.x : ~en.x;
+        gg = ld4(&M.fgeo[f]);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) v[k] = FACEVALS ? fv[(int64_t)f * NC + k] : x[(int64_t)en.y * NC + k];
+      } else if (en.y == -1) {
+        const int b = en.x;
+        gg = ld4(&M.bgeo[b]);
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+          v[k] = FACEVALS ? fv[((int64_t)M.F + b) * NC + k] : (bkind[b] ? xc[k] : bval[(int64_t)b * NC + k]);
+      }
+      if (en.y >= 0) {
+        const bool own = en.x >= 0;
+        const T sg = own ? T(1) : T(-1);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          T pf;
+          if (FACEVALS) {
+            pf = v[k];
+          } else {
+            const T xO = own ? xc[k] : v[k], xN = own ? v[k] : xc[k];
+            pf = gg.w * xO + (T(1) - gg.w) * xN;
+          }
+          acc[k][0] += sg * pf * gg.x; acc[k][1] += sg * pf * gg.y; acc[k][2] += sg * pf * gg.z;
+        }
+      } else if (en.y == -1) {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) { acc[k][0] += v[k] * gg.x; acc[k][1] += v[k] * gg.y; acc[k][2] += v[k] * gg.z; }
+      }
+    }
+    // the next unit's first incidence record is in flight during the reduction and the writes
+    en = (g < nxt.len) ? __ldg(&nxt.e[g * 32]) : make_int2(0, -2);
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+#pragma unroll
+      for (int l = 0; l < 3; ++l) acc[k][l] = group_sum(acc[k][l]);
+    if (live) {
+#pragma unroll
+      for (int j = 0; j < 3 * NC; ++j)     // static register indexing; lane g writes entries j = g mod 4
+        if ((j & (kG - 1)) == g) G[(int64_t)row * 3 * NC + j] = acc[j / 3][j % 3] / Vc;
+    }
+    cur = nxt;
+  }
+}
+
+// y_c (over-relaxed Laplacian, as k_lap) with 4 lanes per row
+template <class T, bool GAMMA>
+__global__ void __launch_bounds__(kThreads) k_lap_g(DevMesh<T> M, const T* __restrict__ gamma, const T* __restrict__ x,
+                                                    const T* __restrict__ G, const uint8_t* __restrict__ bkind,
+                                                    const T* __restrict__ bval, T* __restrict__ y) {
+  const int lane = threadIdx.x & 31, g = lane & (kG - 1);
+  const int nw = (gridDim.x * blockDim.x) >> 5, n_units = 4 * M.n_slices;
+  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  GroupCursor cur = group_unit(M, u, (u & 3) * 8 + (lane >> 2));
+  int2 en = (g < cur.len) ? __ldg(&cur.e[g * 32]) : make_int2(0, -2);
+  for (; u < n_units; u += nw) {
+    const int rl = (u & 3) * 8 + (lane >> 2);
+    const int row = (u >> 2) * 32 + rl;
+    const bool live = row < M.n_own;
+    const int un = u + nw;
+    GroupCursor nxt = group_unit(M, un, (un & 3) * 8 + (lane >> 2));
+    const T xc = live ? x[row] : T(0);
+    const T gc = (GAMMA && live) ? gamma[row] : T(1);
+    T Gc[3] = {T(0), T(0), T(0)};
+    if (live) { Gc[0] = G[3 * (int64_t)row]; Gc[1] = G[3 * (int64_t)row + 1]; Gc[2] = G[3 * (int64_t)row + 2]; }
+    T acc = T(0);
+    for (int j = g; j < cur.len; j += kG) {
+      if (j != g) en = __ldg(&cur.e[j * 32]);
+      if (en.y >= 0) {
+        const int f = en.x >= 0 ? en.x : ~en.x;
+        const int n = en.y;
+        const T w = __ldg(&M.fw[f]);
+        const V4<T> c = ld4(&M.fcor[f]);
+        const T xn = x[n];
+        const T Gn0 = G[3 * (int64_t)n], Gn1 = G[3 * (int64_t)n + 1], Gn2 = G[3 * (int64_t)n + 2];
+        const T gn = GAMMA ? gamma[n] : T(1);
+        const bool own = en.x >= 0;
+        const T wO = w, wN = T(1) - w;
+        const T xO = own ? xc : xn, xN = own ? xn : xc;
+        const T GO0 = own ? Gc[0] : Gn0, GO1 = own ? Gc[1] : Gn1, GO2 = own ? Gc[2] : Gn2;
+        const T GN0 = own ? Gn0 : Gc[0], GN1 = own ? Gn1 : Gc[1], GN2 = own ? Gn2 : Gc[2];
+        T gf = T(1);
+        if (GAMMA) gf = wO * (own ? gc : gn) + wN * (own ? gn : gc);
+        const T corr = c.x * (wO * GO0 + wN * GN0) + c.y * (wO * GO1 + wN * GN1) + c.z * (wO * GO2 + wN * GN2);
+        const T q = gf * (c.w * (xN - xO) + corr);
+        acc += own ? q : -q;
+      } else if (en.y == -1) {
+        const int b = en.x;
+        if (bkind[b] == 0) acc += gc * ld4(&M.bgeo[b]).w * (bval[b] - xc);
+      }
+    }
+    en = (g < nxt.len) ? __ldg(&nxt.e[g * 32]) : make_int2(0, -2);
+    acc = group_sum(acc);
+    if (live && g == 0) y[row] = acc;
+    cur = nxt;
+  }
+}
+
+// Operator variant: 1 = grouped (default), 0 = one thread per row (A/B knob
+// DFVM_OPS_GROUP, read per launch).
+static int ops_group() {
+  const char* e = getenv("DFVM_OPS_GROUP");
+  return e ? atoi(e) : 1;
+}
+
 // ------------------------------------------------------------ divergence
 // D_c = sum_f s_cf F_f + sum_b F_b (not divided by V)
 template <class T>
@@ -355,16 +527,26 @@ void launch_interpolate(const DevMesh<T>& M, const T* x, int nc, const uint8_t* 
 }
 template <class T>
 void launch_grad(const DevMesh<T>& M, const T* x, int nc, const uint8_t* bk, const T* bv, T* G, cudaStream_t s) {
-  const int g = grid_for_slices(M.n_slices);
-  if (nc == 1) k_grad<T, 1, false><<<g, kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
-  else k_grad<T, 3, false><<<g, kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
+  if (ops_group()) {
+    if (nc == 1) k_grad_g<T, 1, false><<<grid_slices(k_grad_g<T, 1, false>, 4 * M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
+    else k_grad_g<T, 3, false><<<grid_slices(k_grad_g<T, 3, false>, 4 * M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
+  } else {
+    const int g = grid_for_slices(M.n_slices);
+    if (nc == 1) k_grad<T, 1, false><<<g, kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
+    else k_grad<T, 3, false><<<g, kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
+  }
   count_launch();
 }
 template <class T>
 void launch_grad_faces(const DevMesh<T>& M, const T* fv, int nc, T* G, cudaStream_t s) {
-  const int g = grid_for_slices(M.n_slices);
-  if (nc == 1) k_grad<T, 1, true><<<g, kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
-  else k_grad<T, 3, true><<<g, kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
+  if (ops_group()) {
+    if (nc == 1) k_grad_g<T, 1, true><<<grid_slices(k_grad_g<T, 1, true>, 4 * M.n_slices), kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
+    else k_grad_g<T, 3, true><<<grid_slices(k_grad_g<T, 3, true>, 4 * M.n_slices), kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
+  } else {
+    const int g = grid_for_slices(M.n_slices);
+    if (nc == 1) k_grad<T, 1, true><<<g, kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
+    else k_grad<T, 3, true><<<g, kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
+  }
   count_launch();
 }
 template <class T>
@@ -375,9 +557,14 @@ void launch_div(const DevMesh<T>& M, const T* flux, T* out, cudaStream_t s) {
 template <class T>
 void launch_laplacian(const DevMesh<T>& M, const T* gamma, const T* x, const T* G, const uint8_t* bk, const T* bv,
                       T* y, cudaStream_t s) {
-  const int g = grid_for_slices(M.n_slices);
-  if (gamma) k_lap<T, true><<<g, kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
-  else k_lap<T, false><<<g, kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+  if (ops_group()) {
+    if (gamma) k_lap_g<T, true><<<grid_slices(k_lap_g<T, true>, 4 * M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+    else k_lap_g<T, false><<<grid_slices(k_lap_g<T, false>, 4 * M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+  } else {
+    const int g = grid_for_slices(M.n_slices);
+    if (gamma) k_lap<T, true><<<g, kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+    else k_lap<T, false><<<g, kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+  }
   count_launch();
 }
 
@@ -397,6 +584,24 @@ INST(float)
 }  // namespace dfvm
 
 namespace dfvm {
+// time-varying boundary values (A-41): val[b] = base[b] * g[wave of b]
+template <class T>
+__global__ void k_bc_wave(T* __restrict__ val, const T* __restrict__ base, const int8_t* __restrict__ wid, int64_t B,
+                          int nc, WaveG<T> g) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
+    const int w = wid[i];
+    if (w >= 0)
+      for (int k = 0; k < nc; ++k) val[i * nc + k] = base[i * nc + k] * g.g[w];
+  }
+}
+template <class T>
+void launch_bc_wave(T* val, const T* base, const int8_t* wid, int64_t B, int nc, const WaveG<T>& g, cudaStream_t s) {
+  if (B <= 0) return;
+  k_bc_wave<T><<<grid_for(B), kThreads, 0, s>>>(val, base, wid, B, nc, g);   // counted by the caller
+}
+template void launch_bc_wave<double>(double*, const double*, const int8_t*, int64_t, int, const WaveG<double>&, cudaStream_t);
+template void launch_bc_wave<float>(float*, const float*, const int8_t*, int64_t, int, const WaveG<float>&, cudaStream_t);
+
 // halo pack: buf[i][k] = x[idx[i]][k]  (send list of owned interface cells)
 template <class T>
 __global__ void k_pack(T* __restrict__ buf, const T* __restrict__ x, const int32_t* __restrict__ idx, int64_t n, int nc) {
