@@ -353,7 +353,7 @@ def main():
     }
     kname, (kms, kn, alg) = max(cands.items(), key=lambda kv: kv[1][0])
     launch_ms = kms / max(kn, 1)
-    achieved = alg / (launch_ms / 1000.0) / 1e9 if kn else None
+    achieved = alg / (launch_ms / 1000.0) / 1e9 if (kn and kms > 0) else None
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
@@ -368,7 +368,7 @@ def main():
             "alg_bytes_per_launch": alg, "launch_ms": launch_ms, "launches": kn,
             "share_of_step": (kms / ms) if ms else None,
             "candidates": {k.split()[0]: {"ms_total": v[0], "launches": v[1], "alg_bytes": v[2],
-                                          "GBps": (v[2] * v[1] / (v[0] / 1000.0) / 1e9) if v[1] else None}
+                                          "GBps": (v[2] * v[1] / (v[0] / 1000.0) / 1e9) if (v[1] and v[0] > 0) else None}
                            for k, v in cands.items()},
             "pcg_iteration_ms": tim["cg_iter_ms"] / max(tim["cg_iter_n"], 1),
             "pcg_share_of_step": tim["cg_iter_ms"] / ms if ms else None, "amg_levels": lv}

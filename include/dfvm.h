@@ -167,6 +167,28 @@ dfvm_status dfvm_mesh_export_geometry(const dfvm_mesh* m, double* Sf, double* xf
                                       double* w, double* delta, double* k, double* delta_b);
 dfvm_status dfvm_mesh_destroy(dfvm_mesh* m);
 
+/* ---- OpenFOAM ASCII polyMesh reader (P:431-432
+ * "reads OpenFOAM polyMesh files directly", Table 1).
+ * dir: a case directory, its constant/polyMesh, or the polyMesh directory;
+ * files points, faces, owner, neighbour, boundary in ASCII format (FoamFile
+ * header `format ascii`; binary or gzip files -> DFVM_E_INVALID_ARG naming
+ * the file, as are parse errors and cyclic / processor / wedge patches).
+ * Patch type wall -> DFVM_PATCH_WALL, empty -> DFVM_PATCH_EMPTY, anything
+ * else -> DFVM_PATCH_GENERIC.  The reader only parses: mesh invariants are
+ * checked by dfvm_mesh_create.  dfvm_polymesh_arrays returns pointers owned
+ * by the reader object (valid until dfvm_polymesh_destroy), laid out exactly
+ * as dfvm_mesh_create takes them; n_cells = 1 + the largest owner /
+ * neighbour label.  Host only. */
+typedef struct dfvm_polymesh dfvm_polymesh;
+dfvm_status dfvm_polymesh_read(const char* dir, dfvm_polymesh** out);
+dfvm_status dfvm_polymesh_sizes(const dfvm_polymesh* m, int64_t* n_points, int64_t* n_faces,
+                                int64_t* n_face_points, int64_t* n_internal_faces, int32_t* n_patches,
+                                int64_t* n_cells);
+dfvm_status dfvm_polymesh_arrays(const dfvm_polymesh* m, const double** points, const int64_t** face_offsets,
+                                 const int32_t** face_points, const int32_t** owner, const int32_t** neighbour,
+                                 const dfvm_patch_desc** patches);
+dfvm_status dfvm_polymesh_destroy(dfvm_polymesh* m);
+
 /* ---------------------------------------------------------------- fields
  * Cell fields: [n_owned + n_ghost][n_comp] in internal (RCM) order.
  * Face fields: [n_local_internal + n_local_boundary + n_local_empty][n_comp]

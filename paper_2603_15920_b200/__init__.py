@@ -41,7 +41,8 @@ SYMBOLS = [
     "dfvm_windkessel_state", "dfvm_windkessel_update", "dfvm_solver_destroy", "dfvm_kernel_launches",
     "dfvm_solver_set_timing", "dfvm_solver_get_timing", "dfvm_comm_create_local", "dfvm_solver_amg_levels",
     "dfvm_transport_step", "dfvm_momentum_apply_transpose", "dfvm_pressure_solve_adjoint", "dfvm_pressure_vjp",
-    "dfvm_bcs_set_waveform", "dfvm_bcs_set_time",
+    "dfvm_bcs_set_waveform", "dfvm_bcs_set_time", "dfvm_polymesh_read", "dfvm_polymesh_sizes",
+    "dfvm_polymesh_arrays", "dfvm_polymesh_destroy",
 ]
 
 
@@ -125,6 +126,10 @@ def lib():
         L.dfvm_bcs_create.argtypes = [vp, C.POINTER(vp)]
         L.dfvm_bcs_set.argtypes = [vp, i32, C.c_char, C.POINTER(BcDesc)]
         L.dfvm_bcs_destroy.argtypes = [vp]
+        L.dfvm_polymesh_read.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.dfvm_polymesh_sizes.argtypes = [vp] + [C.POINTER(i64)] * 4 + [C.POINTER(i32), C.POINTER(i64)]
+        L.dfvm_polymesh_arrays.argtypes = [vp] + [C.POINTER(vp)] * 6
+        L.dfvm_polymesh_destroy.argtypes = [vp]
         L.dfvm_bcs_set_waveform.argtypes = [vp, i32, C.c_char, f64, i32, vp, vp]
         L.dfvm_bcs_set_time.argtypes = [vp, f64, vp]
         L.dfvm_fvc_interpolate.argtypes = [vp, vp, vp, C.c_char, vp, vp]
@@ -218,6 +223,69 @@ class Comm:
         if getattr(self, "h", None):
             lib().dfvm_comm_destroy(self.h)
             self.h = None
+
+
+class Patch:
+    def __init__(self, name, kind, start, n):
+        self.name, self.kind, self.start, self.n = name, kind, start, n
+
+    def __repr__(self):
+        return f"Patch({self.name!r}, kind={self.kind}, start={self.start}, n={self.n})"
+
+
+class PolyMesh:
+    """Arrays of an OpenFOAM ASCII polyMesh read by dfvm_polymesh_read (NEXT-4;
+    P:431-432), in the layout Mesh() / dfvm_mesh_create take (copied out of
+    the reader object)."""
+
+    def __init__(self, path):
+        L = lib()
+        h = C.c_void_p()
+        _check(L.dfvm_polymesh_read(os.fspath(path).encode(), C.byref(h)))
+        try:
+            n = [C.c_int64() for _ in range(4)]
+            npat, nc = C.c_int32(), C.c_int64()
+            _check(L.dfvm_polymesh_sizes(h, *[C.byref(x) for x in n], C.byref(npat), C.byref(nc)))
+            n_p, n_f, n_fp, F = (x.value for x in n)
+            ptr = [C.c_void_p() for _ in range(6)]
+            _check(L.dfvm_polymesh_arrays(h, *[C.byref(x) for x in ptr]))
+
+            def arr(p, count, ct, dt):
+                if count == 0:
+                    return np.zeros(0, dt)
+                return np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), (count,)).astype(dt, copy=True)
+
+            self.points = arr(ptr[0].value, 3 * n_p, C.c_double, np.float64).reshape(n_p, 3)
+            self.face_offsets = arr(ptr[1].value, n_f + 1, C.c_int64, np.int64)
+            self.face_points = arr(ptr[2].value, n_fp, C.c_int32, np.int32)
+            self.owner = arr(ptr[3].value, n_f, C.c_int32, np.int32)
+            self.neighbour = arr(ptr[4].value, F, C.c_int32, np.int32)
+            pd = C.cast(ptr[5].value, C.POINTER(PatchDesc))
+            self.patches = [Patch(pd[i].name.decode(), pd[i].kind, pd[i].start_face, pd[i].n_faces)
+                            for i in range(npat.value)]
+            self.n_cells = nc.value
+            self.meta = dict(kind="polyMesh", path=os.fspath(path))
+        finally:
+            L.dfvm_polymesh_destroy(h)
+
+    @property
+    def n_faces(self):
+        return len(self.owner)
+
+    @property
+    def n_internal(self):
+        return len(self.neighbour)
+
+    def patch(self, name):
+        for i, p in enumerate(self.patches):
+            if p.name == name:
+                return i
+        raise KeyError(name)
+
+
+def read_polymesh(path):
+    """OpenFOAM ASCII polyMesh (case dir, constant/polyMesh or the polyMesh dir) -> PolyMesh."""
+    return PolyMesh(path)
 
 
 class Mesh:

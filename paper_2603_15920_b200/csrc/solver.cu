@@ -1276,16 +1276,16 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
   int it_before = 0;
   for (int it0 = 0;; it0 += kChunk) {
     for (int k = 0; k < kChunk; ++k) {
-      if (S->timing) cudaEventRecord(S->ev[4 * k], st);
+      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k], st, cudaEventRecordExternal);
       k_cg_p<T><<<gp, kThreads, 0, st>>>(M.n_own, X.kr, X.pdiag, X.kp, x, X.d_ctl);
       if ((e = halo_exchange(m, X.kp, 1, st))) return e;
-      if (S->timing) cudaEventRecord(S->ev[4 * k + 1], st);
+      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 1], st, cudaEventRecordExternal);
       k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red);
-      if (S->timing) cudaEventRecord(S->ev[4 * k + 2], st);
+      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 2], st, cudaEventRecordExternal);
       if ((e = fin(S, X, CTL_CG_SPMV, 1, st))) return e;
       k_cg_r<T><<<gr, kThreads, 0, st>>>(M.n_own, X.kq, X.pdiag, X.kr, X.partials, X.ticket, X.d_ctl, red);
       if ((e = fin(S, X, CTL_CG_R, 2, st))) return e;
-      if (S->timing) cudaEventRecord(S->ev[4 * k + 3], st);
+      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 3], st, cudaEventRecordExternal);
       S->n_launch += 3;
     }
     DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
@@ -1357,12 +1357,12 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   auto enqueue_chunk = [&](int* nl) -> dfvm_status {
     dfvm_status e2;
     for (int k = 0; k < kChunk; ++k) {
-      if (S->timing) cudaEventRecord(S->ev[4 * k], st);
+      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k], st, cudaEventRecordExternal);
       k_cg_p2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kz, X.kp, x, X.d_ctl);
       if ((e2 = halo_exchange(m, X.kp, 1, st))) return e2;
-      if (S->timing) cudaEventRecord(S->ev[4 * k + 1], st);
+      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 1], st, cudaEventRecordExternal);
       k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red);
-      if (S->timing) cudaEventRecord(S->ev[4 * k + 2], st);
+      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 2], st, cudaEventRecordExternal);
       if ((e2 = fin(S, X, CTL_CG_SPMV, 1, st))) return e2;
       k_cg_r2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, X.partials, X.ticket, X.d_ctl, red);
       if ((e2 = fin(S, X, CTL_CG_R2, 1, st))) return e2;
@@ -1370,7 +1370,7 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
         return e2;
       k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ);
       if ((e2 = fin(S, X, CTL_CG_RZ, 1, st))) return e2;
-      if (S->timing) cudaEventRecord(S->ev[4 * k + 3], st);
+      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 3], st, cudaEventRecordExternal);
       *nl += 4;
     }
     return DFVM_OK;

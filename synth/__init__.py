@@ -457,3 +457,49 @@ def cylinder_poly(target_cells=1.0e6, seed=3, scramble=13, jitter=0.25, dz=0.01)
                          [PATCH_GENERIC, PATCH_GENERIC, PATCH_GENERIC, PATCH_WALL, PATCH_EMPTY], rules, 4, scramble)
     m.meta = dict(kind="cylinder_poly", h=h, dz=dz, n_theta=nth, n_ring=nring)
     return m
+
+
+# ----------------------------------------------------------------- polyMesh I/O
+def write_polymesh(raw: RawMesh, case_dir, note=""):
+    """Write `raw` as an OpenFOAM ASCII polyMesh under case_dir/constant/polyMesh
+    (input tooling for the NEXT-4 reader tests: a plain text dump of the
+    arrays, points with 17 significant digits so they round-trip exactly)."""
+    d = os.path.join(case_dir, "constant", "polyMesh")
+    os.makedirs(d, exist_ok=True)
+
+    def header(f, cls, obj):
+        f.write("/*--------------------------------*- C++ -*----------------------------------*\\\n"
+                "  synthetic mesh (synth.write_polymesh)\n"
+                "\\*---------------------------------------------------------------------------*/\n")
+        f.write(f"FoamFile\n{{\n    version     2.0;\n    format      ascii;\n    class       {cls};\n")
+        if note:
+            f.write(f'    note        "{note}";\n')
+        f.write(f'    location    "constant/polyMesh";\n    object      {obj};\n}}\n'
+                "// * * * * * * * * * * * * * * * * * * * * * * * * * * * * * * * * * * * * * //\n\n")
+
+    with open(os.path.join(d, "points"), "w") as f:
+        header(f, "vectorField", "points")
+        f.write(f"{len(raw.points)}\n(\n")
+        f.write("".join(f"({x!r} {y!r} {z!r})\n" for x, y, z in np.asarray(raw.points, np.float64).tolist()))
+        f.write(")\n")
+    with open(os.path.join(d, "faces"), "w") as f:
+        header(f, "faceList", "faces")
+        fo, fp = raw.face_offsets, raw.face_points
+        f.write(f"{raw.n_faces}\n(\n")
+        f.write("".join(f"{fo[i + 1] - fo[i]}({' '.join(map(str, fp[fo[i]:fo[i + 1]].tolist()))})\n"
+                        for i in range(raw.n_faces)))
+        f.write(")\n")
+    for name, arr in (("owner", raw.owner), ("neighbour", raw.neighbour)):
+        with open(os.path.join(d, name), "w") as f:
+            header(f, "labelList", name)
+            f.write(f"{len(arr)}\n(\n" + "".join(f"{v}\n" for v in np.asarray(arr).tolist()) + ")\n")
+    kinds = {PATCH_GENERIC: "patch", PATCH_WALL: "wall", PATCH_EMPTY: "empty"}
+    with open(os.path.join(d, "boundary"), "w") as f:
+        header(f, "polyBoundaryMesh", "boundary")
+        f.write(f"{len(raw.patches)}\n(\n")
+        for p in raw.patches:
+            f.write(f"    {p.name}\n    {{\n        type            {kinds[p.kind]};\n"
+                    f"        inGroups        List<word> 1({kinds[p.kind]});\n"
+                    f"        nFaces          {p.n};\n        startFace       {p.start};\n    }}\n")
+        f.write(")\n")
+    return d
