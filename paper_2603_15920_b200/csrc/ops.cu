@@ -113,11 +113,10 @@ __global__ void k_interp(DevMesh<T> M, const T* __restrict__ x, const uint8_t* _
 // ------------------------------------------------------------ Gauss grad
 // G_c = (1/V_c) [sum_f s_cf phi_f S_f + sum_b phi_b S_b] (eq:gauss_green
 // P:207-213), G[c][k][l] = d phi^k / d x^l.
-template <class T, int NC, bool FACEVALS>
-__global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __restrict__ x,
+template <class T, int NC, bool FACEVALS, int KB, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_grad(DevMesh<T> M, const T* __restrict__ x,
                                                    const uint8_t* __restrict__ bkind, const T* __restrict__ bval,
-                                                   const T* __restrict__ fv, T* __restrict__ G) {
-  constexpr int KB = NC == 1 ? kB : 2;     // batch depth: register budget of the 3-component case
+                                                   const T* __restrict__ fv, T* __restrict__ G, bool ld3_on) {
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   // software pipeline over the warp's slices: the next slice's metadata and
@@ -164,7 +163,11 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
           const int f = en[u].x >= 0 ? en[u].x : ~en[u].x;
           g[u] = ld4(&M.fgeo[f]);
 #pragma unroll
-          for (int k = 0; k < NC; ++k) v[u][k] = FACEVALS ? fv[(int64_t)f * NC + k] : x[(int64_t)en[u].y * NC + k];
+          if (NC == 3 && !FACEVALS && ld3_on)
+            ld3(&x[(int64_t)en[u].y * NC], v[u][0], v[u][NC > 1 ? 1 : 0], v[u][NC > 2 ? 2 : 0]);
+          else
+#pragma unroll
+            for (int k = 0; k < NC; ++k) v[u][k] = FACEVALS ? fv[(int64_t)f * NC + k] : x[(int64_t)en[u].y * NC + k];
         } else if (en[u].y == -1) {
           const int b = en[u].x;
           g[u] = ld4(&M.bgeo[b]);
@@ -218,177 +221,6 @@ __global__ void __launch_bounds__(kThreads) k_grad(DevMesh<T> M, const T* __rest
   }
 }
 
-// ------------------------------------------------- grouped cell-gathers
-// G = 4 lanes share a row: a warp covers a quarter of a SELL-32 slice (8
-// rows), lane g of a row visits its incidences k = g, g + 4, ... in ascending
-// order and the 4 partial sums are combined by a fixed xor-shuffle tree,
-// (a0 + a1) + (a2 + a3), so every lane of the group holds the bitwise-same
-// total (deterministic; the per-row incidence order is the same in any
-// partition, so partitioned results stay bitwise those of one rank).  On
-// tets (4 incidences per row) every lane issues one face-record + neighbour
-// gather per row: one gather round trip per unit instead of a dependent
-// chain of batches, with few registers (full-wave grid by occupancy).  The
-// next unit's slice metadata and incidence record are prefetched while the
-// current gathers are in flight.
-constexpr int kG = 4;
-
-struct GroupCursor {   // the (slice, quarter) unit a warp works on
-  int u, len;
-  const int2* e;
-};
-template <class T>
-__device__ __forceinline__ GroupCursor group_unit(const DevMesh<T>& M, int u, int rl) {
-  GroupCursor c{u, 0, M.inc};
-  if (u < 4 * M.n_slices) {
-    const int s = u >> 2;
-    c.len = __ldg(&M.sl_len[s]);
-    c.e = M.inc + __ldg(&M.sl_ptr[s]) + rl;
-  }
-  return c;
-}
-
-template <class T>
-__device__ __forceinline__ T group_sum(T v) {
-  v += __shfl_xor_sync(0xffffffffu, v, 1);
-  v += __shfl_xor_sync(0xffffffffu, v, 2);
-  return v;
-}
-
-template <class T, int NC, bool FACEVALS>
-__global__ void __launch_bounds__(kThreads) k_grad_g(DevMesh<T> M, const T* __restrict__ x,
-                                                     const uint8_t* __restrict__ bkind, const T* __restrict__ bval,
-                                                     const T* __restrict__ fv, T* __restrict__ G) {
-  const int lane = threadIdx.x & 31, g = lane & (kG - 1);
-  const int nw = (gridDim.x * blockDim.x) >> 5, n_units = 4 * M.n_slices;
-  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  GroupCursor cur = group_unit(M, u, (u & 3) * 8 + (lane >> 2));
-  int2 en = (g < cur.len) ? __ldg(&cur.e[g * 32]) : make_int2(0, -2);
-  for (; u < n_units; u += nw) {
-    const int rl = (u & 3) * 8 + (lane >> 2);
-    const int row = (u >> 2) * 32 + rl;
-    const bool live = row < M.n_own;
-    // prefetch the next unit's metadata
-    const int un = u + nw;
-    GroupCursor nxt = group_unit(M, un, (un & 3) * 8 + (lane >> 2));
-    T xc[NC];
-#pragma unroll
-    for (int k = 0; k < NC; ++k) xc[k] = (!FACEVALS && live) ? x[(int64_t)row * NC + k] : T(0);
-    T acc[NC][3];
-#pragma unroll
-    for (int k = 0; k < NC; ++k) acc[k][0] = acc[k][1] = acc[k][2] = T(0);
-    const T Vc = live ? M.vol[row] : T(1);
-    for (int j = g; j < cur.len; j += kG) {
-      if (j != g) en = __ldg(&cur.e[j * 32]);
-      V4<T> gg = V4<T>{T(0), T(0), T(0), T(0)};
-      T v[NC];
-#pragma unroll
-      for (int k = 0; k < NC; ++k) v[k] = T(0);
-      if (en.y >= 0) {
-        const int f = en.x >= 0 ? en.x : ~en.x;
-        gg = ld4(&M.fgeo[f]);
-#pragma unroll
-        for (int k = 0; k < NC; ++k) v[k] = FACEVALS ? fv[(int64_t)f * NC + k] : x[(int64_t)en.y * NC + k];
-      } else if (en.y == -1) {
-        const int b = en.x;
-        gg = ld4(&M.bgeo[b]);
-#pragma unroll
-        for (int k = 0; k < NC; ++k)
-          v[k] = FACEVALS ? fv[((int64_t)M.F + b) * NC + k] : (bkind[b] ? xc[k] : bval[(int64_t)b * NC + k]);
-      }
-      if (en.y >= 0) {
-        const bool own = en.x >= 0;
-        const T sg = own ? T(1) : T(-1);
-#pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          T pf;
-          if (FACEVALS) {
-            pf = v[k];
-          } else {
-            const T xO = own ? xc[k] : v[k], xN = own ? v[k] : xc[k];
-            pf = gg.w * xO + (T(1) - gg.w) * xN;
-          }
-          acc[k][0] += sg * pf * gg.x; acc[k][1] += sg * pf * gg.y; acc[k][2] += sg * pf * gg.z;
-        }
-      } else if (en.y == -1) {
-#pragma unroll
-        for (int k = 0; k < NC; ++k) { acc[k][0] += v[k] * gg.x; acc[k][1] += v[k] * gg.y; acc[k][2] += v[k] * gg.z; }
-      }
-    }
-    // the next unit's first incidence record is in flight during the reduction and the writes
-    en = (g < nxt.len) ? __ldg(&nxt.e[g * 32]) : make_int2(0, -2);
-#pragma unroll
-    for (int k = 0; k < NC; ++k)
-#pragma unroll
-      for (int l = 0; l < 3; ++l) acc[k][l] = group_sum(acc[k][l]);
-    if (live) {
-#pragma unroll
-      for (int j = 0; j < 3 * NC; ++j)     // static register indexing; lane g writes entries j = g mod 4
-        if ((j & (kG - 1)) == g) G[(int64_t)row * 3 * NC + j] = acc[j / 3][j % 3] / Vc;
-    }
-    cur = nxt;
-  }
-}
-
-// y_c (over-relaxed Laplacian, as k_lap) with 4 lanes per row
-template <class T, bool GAMMA>
-__global__ void __launch_bounds__(kThreads) k_lap_g(DevMesh<T> M, const T* __restrict__ gamma, const T* __restrict__ x,
-                                                    const T* __restrict__ G, const uint8_t* __restrict__ bkind,
-                                                    const T* __restrict__ bval, T* __restrict__ y) {
-  const int lane = threadIdx.x & 31, g = lane & (kG - 1);
-  const int nw = (gridDim.x * blockDim.x) >> 5, n_units = 4 * M.n_slices;
-  int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  GroupCursor cur = group_unit(M, u, (u & 3) * 8 + (lane >> 2));
-  int2 en = (g < cur.len) ? __ldg(&cur.e[g * 32]) : make_int2(0, -2);
-  for (; u < n_units; u += nw) {
-    const int rl = (u & 3) * 8 + (lane >> 2);
-    const int row = (u >> 2) * 32 + rl;
-    const bool live = row < M.n_own;
-    const int un = u + nw;
-    GroupCursor nxt = group_unit(M, un, (un & 3) * 8 + (lane >> 2));
-    const T xc = live ? x[row] : T(0);
-    const T gc = (GAMMA && live) ? gamma[row] : T(1);
-    T Gc[3] = {T(0), T(0), T(0)};
-    if (live) { Gc[0] = G[3 * (int64_t)row]; Gc[1] = G[3 * (int64_t)row + 1]; Gc[2] = G[3 * (int64_t)row + 2]; }
-    T acc = T(0);
-    for (int j = g; j < cur.len; j += kG) {
-      if (j != g) en = __ldg(&cur.e[j * 32]);
-      if (en.y >= 0) {
-        const int f = en.x >= 0 ? en.x : ~en.x;
-        const int n = en.y;
-        const T w = __ldg(&M.fw[f]);
-        const V4<T> c = ld4(&M.fcor[f]);
-        const T xn = x[n];
-        const T Gn0 = G[3 * (int64_t)n], Gn1 = G[3 * (int64_t)n + 1], Gn2 = G[3 * (int64_t)n + 2];
-        const T gn = GAMMA ? gamma[n] : T(1);
-        const bool own = en.x >= 0;
-        const T wO = w, wN = T(1) - w;
-        const T xO = own ? xc : xn, xN = own ? xn : xc;
-        const T GO0 = own ? Gc[0] : Gn0, GO1 = own ? Gc[1] : Gn1, GO2 = own ? Gc[2] : Gn2;
-        const T GN0 = own ? Gn0 : Gc[0], GN1 = own ? Gn1 : Gc[1], GN2 = own ? Gn2 : Gc[2];
-        T gf = T(1);
-        if (GAMMA) gf = wO * (own ? gc : gn) + wN * (own ? gn : gc);
-        const T corr = c.x * (wO * GO0 + wN * GN0) + c.y * (wO * GO1 + wN * GN1) + c.z * (wO * GO2 + wN * GN2);
-        const T q = gf * (c.w * (xN - xO) + corr);
-        acc += own ? q : -q;
-      } else if (en.y == -1) {
-        const int b = en.x;
-        if (bkind[b] == 0) acc += gc * ld4(&M.bgeo[b]).w * (bval[b] - xc);
-      }
-    }
-    en = (g < nxt.len) ? __ldg(&nxt.e[g * 32]) : make_int2(0, -2);
-    acc = group_sum(acc);
-    if (live && g == 0) y[row] = acc;
-    cur = nxt;
-  }
-}
-
-// Operator variant: 1 = grouped (default), 0 = one thread per row (A/B knob
-// DFVM_OPS_GROUP, read per launch).
-static int ops_group() {
-  const char* e = getenv("DFVM_OPS_GROUP");
-  return e ? atoi(e) : 1;
-}
-
 // ------------------------------------------------------------ divergence
 // D_c = sum_f s_cf F_f + sum_b F_b (not divided by V)
 template <class T>
@@ -427,11 +259,10 @@ __global__ void __launch_bounds__(kThreads) k_div(DevMesh<T> M, const T* __restr
 // ------------------------------------------------------------ Laplacian
 // y_c = sum_f s_cf gamma_f [delta_f (x_N - x_O) + k_f . (w G_O + (1-w) G_N)]
 //     + sum_{b fixed} gamma_c delta_b (x_b - x_c)   (eq:nonortho_flux P:240-250)
-template <class T, bool GAMMA>
-__global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restrict__ gamma, const T* __restrict__ x,
+template <class T, bool GAMMA, int KB, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_lap(DevMesh<T> M, const T* __restrict__ gamma, const T* __restrict__ x,
                                                   const T* __restrict__ G, const uint8_t* __restrict__ bkind,
-                                                  const T* __restrict__ bval, T* __restrict__ y) {
-  constexpr int KB = 2;                    // batch depth (9 gathered values per incidence)
+                                                  const T* __restrict__ bval, T* __restrict__ y, bool ld3_on) {
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   // software pipeline over the warp's slices (as in k_grad)
@@ -478,7 +309,8 @@ __global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restr
           w[u] = __ldg(&M.fw[f]);
           c[u] = ld4(&M.fcor[f]);
           xn[u] = x[n];
-          Gn[u][0] = G[3 * (int64_t)n]; Gn[u][1] = G[3 * (int64_t)n + 1]; Gn[u][2] = G[3 * (int64_t)n + 2];
+          if (ld3_on) ld3(&G[3 * (int64_t)n], Gn[u][0], Gn[u][1], Gn[u][2]);
+          else { Gn[u][0] = G[3 * (int64_t)n]; Gn[u][1] = G[3 * (int64_t)n + 1]; Gn[u][2] = G[3 * (int64_t)n + 2]; }
           if (GAMMA) gn[u] = gamma[n];
         } else if (en[u].y == -1) {
           const int b = en[u].x;
@@ -518,6 +350,12 @@ __global__ void __launch_bounds__(kThreads) k_lap(DevMesh<T> M, const T* __restr
 }
 
 // ------------------------------------------------------------ launchers
+// A/B knob of the 3-vector gathers (DFVM_LD3=0: three 64-bit loads)
+static bool ld3_env() {
+  const char* e = getenv("DFVM_LD3");
+  return !(e && e[0] == '0');
+}
+
 template <class T>
 void launch_interpolate(const DevMesh<T>& M, const T* x, int nc, const uint8_t* bk, const T* bv, T* xf, cudaStream_t s) {
   const int g = grid_for((int64_t)M.F + M.B + M.E);
@@ -525,28 +363,40 @@ void launch_interpolate(const DevMesh<T>& M, const T* x, int nc, const uint8_t* 
   else k_interp<T, 3><<<g, kThreads, 0, s>>>(M, x, bk, bv, xf);
   count_launch();
 }
+// Batch depth KB and minimum resident blocks MINB (register cap) per kernel:
+// variant table (DFVM_OPS_VARIANT, A/B knob) {KB, MINB} of the scalar
+// gradient, the vector gradient and the Laplacian.  Grids are one full wave
+// of resident blocks (occupancy API), never a partial second wave.
+static int ops_variant() {
+  const char* e = getenv("DFVM_OPS_VARIANT");
+  const int v = e ? atoi(e) : 0;
+  return v < 0 || v > 4 ? 0 : v;
+}
+template <class T, int NC, bool FV, int KB, int MINB>
+static void grad_v(const DevMesh<T>& M, const T* x, const uint8_t* bk, const T* bv, const T* fv, T* G, cudaStream_t s) {
+  auto fn = k_grad<T, NC, FV, KB, MINB>;
+  fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, fv, G, !FV && ld3_env());
+}
+template <class T, int NC, bool FV>
+static void grad_any(const DevMesh<T>& M, const T* x, const uint8_t* bk, const T* bv, const T* fv, T* G, cudaStream_t s) {
+  switch (ops_variant()) {
+    case 1: grad_v<T, NC, FV, NC == 1 ? 4 : 2, 3>(M, x, bk, bv, fv, G, s); break;
+    case 2: grad_v<T, NC, FV, NC == 1 ? 4 : 2, 4>(M, x, bk, bv, fv, G, s); break;
+    case 3: grad_v<T, NC, FV, NC == 1 ? 2 : 1, 4>(M, x, bk, bv, fv, G, s); break;
+    case 4: grad_v<T, NC, FV, NC == 1 ? 8 : 4, 2>(M, x, bk, bv, fv, G, s); break;
+    default: grad_v<T, NC, FV, NC == 1 ? 4 : 2, 1>(M, x, bk, bv, fv, G, s);
+  }
+}
 template <class T>
 void launch_grad(const DevMesh<T>& M, const T* x, int nc, const uint8_t* bk, const T* bv, T* G, cudaStream_t s) {
-  if (ops_group()) {
-    if (nc == 1) k_grad_g<T, 1, false><<<grid_slices(k_grad_g<T, 1, false>, 4 * M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
-    else k_grad_g<T, 3, false><<<grid_slices(k_grad_g<T, 3, false>, 4 * M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
-  } else {
-    const int g = grid_for_slices(M.n_slices);
-    if (nc == 1) k_grad<T, 1, false><<<g, kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
-    else k_grad<T, 3, false><<<g, kThreads, 0, s>>>(M, x, bk, bv, nullptr, G);
-  }
+  if (nc == 1) grad_any<T, 1, false>(M, x, bk, bv, nullptr, G, s);
+  else grad_any<T, 3, false>(M, x, bk, bv, nullptr, G, s);
   count_launch();
 }
 template <class T>
 void launch_grad_faces(const DevMesh<T>& M, const T* fv, int nc, T* G, cudaStream_t s) {
-  if (ops_group()) {
-    if (nc == 1) k_grad_g<T, 1, true><<<grid_slices(k_grad_g<T, 1, true>, 4 * M.n_slices), kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
-    else k_grad_g<T, 3, true><<<grid_slices(k_grad_g<T, 3, true>, 4 * M.n_slices), kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
-  } else {
-    const int g = grid_for_slices(M.n_slices);
-    if (nc == 1) k_grad<T, 1, true><<<g, kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
-    else k_grad<T, 3, true><<<g, kThreads, 0, s>>>(M, nullptr, nullptr, nullptr, fv, G);
-  }
+  if (nc == 1) grad_any<T, 1, true>(M, nullptr, nullptr, nullptr, fv, G, s);
+  else grad_any<T, 3, true>(M, nullptr, nullptr, nullptr, fv, G, s);
   count_launch();
 }
 template <class T>
@@ -554,17 +404,28 @@ void launch_div(const DevMesh<T>& M, const T* flux, T* out, cudaStream_t s) {
   k_div<T><<<grid_for_slices(M.n_slices), kThreads, 0, s>>>(M, flux, out);
   count_launch();
 }
+template <class T, bool GA, int KB, int MINB>
+static void lap_v(const DevMesh<T>& M, const T* gamma, const T* x, const T* G, const uint8_t* bk, const T* bv, T* y,
+                  cudaStream_t s) {
+  auto fn = k_lap<T, GA, KB, MINB>;
+  fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y, ld3_env());
+}
+template <class T, bool GA>
+static void lap_any(const DevMesh<T>& M, const T* gamma, const T* x, const T* G, const uint8_t* bk, const T* bv, T* y,
+                    cudaStream_t s) {
+  switch (ops_variant()) {
+    case 1: lap_v<T, GA, 2, 3>(M, gamma, x, G, bk, bv, y, s); break;
+    case 2: lap_v<T, GA, 2, 4>(M, gamma, x, G, bk, bv, y, s); break;
+    case 3: lap_v<T, GA, 1, 4>(M, gamma, x, G, bk, bv, y, s); break;
+    case 4: lap_v<T, GA, 4, 2>(M, gamma, x, G, bk, bv, y, s); break;
+    default: lap_v<T, GA, 2, 1>(M, gamma, x, G, bk, bv, y, s);
+  }
+}
 template <class T>
 void launch_laplacian(const DevMesh<T>& M, const T* gamma, const T* x, const T* G, const uint8_t* bk, const T* bv,
                       T* y, cudaStream_t s) {
-  if (ops_group()) {
-    if (gamma) k_lap_g<T, true><<<grid_slices(k_lap_g<T, true>, 4 * M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
-    else k_lap_g<T, false><<<grid_slices(k_lap_g<T, false>, 4 * M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
-  } else {
-    const int g = grid_for_slices(M.n_slices);
-    if (gamma) k_lap<T, true><<<g, kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
-    else k_lap<T, false><<<g, kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
-  }
+  if (gamma) lap_any<T, true>(M, gamma, x, G, bk, bv, y, s);
+  else lap_any<T, false>(M, gamma, x, G, bk, bv, y, s);
   count_launch();
 }
 

@@ -30,7 +30,7 @@ torch.cuda.set_stream(stream)
 import ctypes as C  # noqa: E402
 sp = C.c_void_p(stream.cuda_stream)
 keys = ["DFVM_AMG_COARSE", "DFVM_AMG_SWEEPS", "DFVM_AMG_CYCLE", "DFVM_AMG_WMAX", "DFVM_AMG_OMEGA",
-        "DFVM_AMG_TAIL", "DFVM_AMG_DIRECT"]
+        "DFVM_AMG_TAIL", "DFVM_AMG_DIRECT", "DFVM_AMG_SIGMA", "DFVM_AMG_GROUP", "DFVM_GRAPHS"]
 for line in open(cfgfile):
     parts = line.split()
     if not parts or parts[0].startswith("#"):
