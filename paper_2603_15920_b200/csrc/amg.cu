@@ -57,15 +57,18 @@ constexpr int kMaxLevels = 16;
 //   DFVM_AMG_OMEGA   coarse-correction scale (symmetric over-correction,
 //                    < 2 keeps M SPD with adjoint smoothers)   default 1.8
 //   DFVM_AMG_SIGMA   1: renumber aggregates by row length within windows of
-//                    256 (less SELL padding); 0: creation order      default 1
+//                    256 (less SELL padding); 0: creation order      default 0
 //   DFVM_AMG_GROUP   1: 4/8 lanes per row on long or few coarse rows; 0: one
-//                    thread per row                                  default 1
+//                    thread per row                                  default 0
+//                    (C5 amg32: 378 ms/step with both 0 against 423 ms with
+//                    both 1: sigma costs 0.5 PCG iterations per solve and
+//                    the grouped kernels are slower than one thread per row)
 //   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
 //                    exactly with a dense inverse (Gauss-Jordan once per
 //                    matrix update, one block), larger ones with
 //                    DFVM_AMG_SWEEPS l1-Jacobi sweeps (0: always sweeps)  default 512
 struct AmgParams {
-  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, sigma = 1, group = 1;
+  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, sigma = 0, group = 0;
   bool wcycle = true;
   double omega = 1.8;
   AmgParams() {

@@ -116,8 +116,9 @@ __global__ void k_interp(DevMesh<T> M, const T* __restrict__ x, const uint8_t* _
 template <class T, int NC, bool FACEVALS, int KB, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_grad(DevMesh<T> M, const T* __restrict__ x,
                                                    const uint8_t* __restrict__ bkind, const T* __restrict__ bval,
-                                                   const T* __restrict__ fv, T* __restrict__ G, bool ld3_on) {
-  const int lane = threadIdx.x & 31;
+                                                   const T* __restrict__ fv, T* __restrict__ G) {
+  __shared__ T sh_out[kWarpsPerBlock][32 * 3 * NC];   // staged outputs of the warp's 32 rows
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   // software pipeline over the warp's slices: the next slice's metadata and
   // first incidence batch are in flight while this slice's face records load
@@ -143,7 +144,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_grad(DevMesh<T> M, const T* 
     const bool live = row < M.n_own;
     T xc[NC];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) xc[k] = (!FACEVALS && live) ? x[(int64_t)row * NC + k] : T(0);
+    for (int k = 0; k < NC; ++k) xc[k] = T(0);
+    if (!FACEVALS && live) {
+      if (NC == 3) ld3(&x[(int64_t)row * NC], xc[0], xc[NC > 1 ? 1 : 0], xc[NC > 2 ? 2 : 0]);
+      else xc[0] = x[row];
+    }
     T acc[NC][3];
 #pragma unroll
     for (int k = 0; k < NC; ++k) acc[k][0] = acc[k][1] = acc[k][2] = T(0);
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_grad(DevMesh<T> M, const T* 
           const int f = en[u].x >= 0 ? en[u].x : ~en[u].x;
           g[u] = ld4(&M.fgeo[f]);
 #pragma unroll
-          if (NC == 3 && !FACEVALS && ld3_on)
+          if (NC == 3 && !FACEVALS)          // 3-vector gather in two loads (grad_U 0.456 -> 0.477)
             ld3(&x[(int64_t)en[u].y * NC], v[u][0], v[u][NC > 1 ? 1 : 0], v[u][NC > 2 ? 2 : 0]);
           else
 #pragma unroll
@@ -207,13 +212,23 @@ __global__ void __launch_bounds__(kThreads, MINB) k_grad(DevMesh<T> M, const T* 
     if (len == 0)
 #pragma unroll
       for (int u = 0; u < KB; ++u) en_n[u] = (u < len_n) ? __ldg(&e_n[u * 32]) : make_int2(0, -2);
+    // the warp's 32 rows x 3NC outputs are contiguous: stage them in shared
+    // memory and store them coalesced (3NC full-line stores instead of 3NC
+    // stride-3NC ones)
     if (live) {
       const T V = M.vol[row];
 #pragma unroll
       for (int k = 0; k < NC; ++k)
 #pragma unroll
-        for (int l = 0; l < 3; ++l) G[(int64_t)row * 3 * NC + 3 * k + l] = acc[k][l] / V;
+        for (int l = 0; l < 3; ++l) sh_out[wib][lane * 3 * NC + 3 * k + l] = acc[k][l] / V;
     }
+    __syncwarp();
+    {
+      const int nlive = min(32, M.n_own - s * 32);
+      T* gout = G + (int64_t)s * 32 * 3 * NC;
+      for (int i = lane; i < nlive * 3 * NC; i += 32) gout[i] = sh_out[wib][i];
+    }
+    __syncwarp();
 #pragma unroll
     for (int u = 0; u < KB; ++u) en[u] = en_n[u];
     len = len_n;
@@ -262,7 +277,7 @@ __global__ void __launch_bounds__(kThreads) k_div(DevMesh<T> M, const T* __restr
 template <class T, bool GAMMA, int KB, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_lap(DevMesh<T> M, const T* __restrict__ gamma, const T* __restrict__ x,
                                                   const T* __restrict__ G, const uint8_t* __restrict__ bkind,
-                                                  const T* __restrict__ bval, T* __restrict__ y, bool ld3_on) {
+                                                  const T* __restrict__ bval, T* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   // software pipeline over the warp's slices (as in k_grad)
@@ -309,8 +324,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_lap(DevMesh<T> M, const T* _
           w[u] = __ldg(&M.fw[f]);
           c[u] = ld4(&M.fcor[f]);
           xn[u] = x[n];
-          if (ld3_on) ld3(&G[3 * (int64_t)n], Gn[u][0], Gn[u][1], Gn[u][2]);
-          else { Gn[u][0] = G[3 * (int64_t)n]; Gn[u][1] = G[3 * (int64_t)n + 1]; Gn[u][2] = G[3 * (int64_t)n + 2]; }
+          Gn[u][0] = G[3 * (int64_t)n]; Gn[u][1] = G[3 * (int64_t)n + 1]; Gn[u][2] = G[3 * (int64_t)n + 2];
           if (GAMMA) gn[u] = gamma[n];
         } else if (en[u].y == -1) {
           const int b = en[u].x;
@@ -350,12 +364,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_lap(DevMesh<T> M, const T* _
 }
 
 // ------------------------------------------------------------ launchers
-// A/B knob of the 3-vector gathers (DFVM_LD3=0: three 64-bit loads)
-static bool ld3_env() {
-  const char* e = getenv("DFVM_LD3");
-  return !(e && e[0] == '0');
-}
-
 template <class T>
 void launch_interpolate(const DevMesh<T>& M, const T* x, int nc, const uint8_t* bk, const T* bv, T* xf, cudaStream_t s) {
   const int g = grid_for((int64_t)M.F + M.B + M.E);
@@ -363,29 +371,15 @@ void launch_interpolate(const DevMesh<T>& M, const T* x, int nc, const uint8_t* 
   else k_interp<T, 3><<<g, kThreads, 0, s>>>(M, x, bk, bv, xf);
   count_launch();
 }
-// Batch depth KB and minimum resident blocks MINB (register cap) per kernel:
-// variant table (DFVM_OPS_VARIANT, A/B knob) {KB, MINB} of the scalar
-// gradient, the vector gradient and the Laplacian.  Grids are one full wave
-// of resident blocks (occupancy API), never a partial second wave.
-static int ops_variant() {
-  const char* e = getenv("DFVM_OPS_VARIANT");
-  const int v = e ? atoi(e) : 0;
-  return v < 0 || v > 4 ? 0 : v;
-}
-template <class T, int NC, bool FV, int KB, int MINB>
-static void grad_v(const DevMesh<T>& M, const T* x, const uint8_t* bk, const T* bv, const T* fv, T* G, cudaStream_t s) {
-  auto fn = k_grad<T, NC, FV, KB, MINB>;
-  fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, fv, G, !FV && ld3_env());
-}
+// Batch depth KB and minimum resident blocks MINB (register cap 64), measured
+// on C5 (sweep of 5 {KB, MINB} variants, profiles/r01_ops_variants_c5.json):
+// shallow batches at 4 resident blocks per SM beat deeper batches at lower
+// occupancy (grad_s 0.62 -> 0.78, lap 0.45 -> 0.64 of the HBM peak).  Grids
+// are one full wave of resident blocks (occupancy API).
 template <class T, int NC, bool FV>
 static void grad_any(const DevMesh<T>& M, const T* x, const uint8_t* bk, const T* bv, const T* fv, T* G, cudaStream_t s) {
-  switch (ops_variant()) {
-    case 1: grad_v<T, NC, FV, NC == 1 ? 4 : 2, 3>(M, x, bk, bv, fv, G, s); break;
-    case 2: grad_v<T, NC, FV, NC == 1 ? 4 : 2, 4>(M, x, bk, bv, fv, G, s); break;
-    case 3: grad_v<T, NC, FV, NC == 1 ? 2 : 1, 4>(M, x, bk, bv, fv, G, s); break;
-    case 4: grad_v<T, NC, FV, NC == 1 ? 8 : 4, 2>(M, x, bk, bv, fv, G, s); break;
-    default: grad_v<T, NC, FV, NC == 1 ? 4 : 2, 1>(M, x, bk, bv, fv, G, s);
-  }
+  auto fn = k_grad<T, NC, FV, NC == 1 ? 2 : 1, 4>;
+  fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, fv, G);
 }
 template <class T>
 void launch_grad(const DevMesh<T>& M, const T* x, int nc, const uint8_t* bk, const T* bv, T* G, cudaStream_t s) {
@@ -404,22 +398,11 @@ void launch_div(const DevMesh<T>& M, const T* flux, T* out, cudaStream_t s) {
   k_div<T><<<grid_for_slices(M.n_slices), kThreads, 0, s>>>(M, flux, out);
   count_launch();
 }
-template <class T, bool GA, int KB, int MINB>
-static void lap_v(const DevMesh<T>& M, const T* gamma, const T* x, const T* G, const uint8_t* bk, const T* bv, T* y,
-                  cudaStream_t s) {
-  auto fn = k_lap<T, GA, KB, MINB>;
-  fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y, ld3_env());
-}
 template <class T, bool GA>
 static void lap_any(const DevMesh<T>& M, const T* gamma, const T* x, const T* G, const uint8_t* bk, const T* bv, T* y,
                     cudaStream_t s) {
-  switch (ops_variant()) {
-    case 1: lap_v<T, GA, 2, 3>(M, gamma, x, G, bk, bv, y, s); break;
-    case 2: lap_v<T, GA, 2, 4>(M, gamma, x, G, bk, bv, y, s); break;
-    case 3: lap_v<T, GA, 1, 4>(M, gamma, x, G, bk, bv, y, s); break;
-    case 4: lap_v<T, GA, 4, 2>(M, gamma, x, G, bk, bv, y, s); break;
-    default: lap_v<T, GA, 2, 1>(M, gamma, x, G, bk, bv, y, s);
-  }
+  auto fn = k_lap<T, GA, 1, 4>;
+  fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
 }
 template <class T>
 void launch_laplacian(const DevMesh<T>& M, const T* gamma, const T* x, const T* G, const uint8_t* bk, const T* bv,

@@ -959,8 +959,8 @@ __global__ void __launch_bounds__(kThreads) k_bi_v(DevMesh<T> M, const T* __rest
 
 // s = r - alpha v (own row and, on the fly, every neighbour); t = A (s / diag);
 // partials (t, s), (t, t), (s, s) -> half-step check, omega
-template <class T>
-__global__ void __launch_bounds__(kThreads) k_bi_t(DevMesh<T> M, const T* __restrict__ dinv,
+template <class T, int KBT, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_bi_t(DevMesh<T> M, const T* __restrict__ dinv,
     const T* __restrict__ coef, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ tv,
     double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   if (all_done(ctl)) return;
@@ -982,19 +982,19 @@ __global__ void __launch_bounds__(kThreads) k_bi_t(DevMesh<T> M, const T* __rest
     const int len = __ldg(&M.ms_len[s]);
     const int base = __ldg(&M.ms_ptr[s]) + lane;
     int j = 0;
-    for (; j + 4 <= len; j += 4) {
-      T c[4], dn[4], rn[4][3], vn[4][3];
-      int nn[4];
+    for (; j + KBT <= len; j += KBT) {
+      T c[KBT], dn[KBT], rn[KBT][3], vn[KBT][3];
+      int nn[KBT];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) { c[u] = __ldg(&coef[base + 32 * (j + u)]); nn[u] = __ldg(&M.mnb[base + 32 * (j + u)]); }
+      for (int u = 0; u < KBT; ++u) { c[u] = __ldg(&coef[base + 32 * (j + u)]); nn[u] = __ldg(&M.mnb[base + 32 * (j + u)]); }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < KBT; ++u) {
         dn[u] = dinv[nn[u]];
 #pragma unroll
         for (int k = 0; k < 3; ++k) { rn[u][k] = r[3 * (int64_t)nn[u] + k]; vn[u][k] = v[3 * (int64_t)nn[u] + k]; }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < KBT; ++u)
 #pragma unroll
         for (int k = 0; k < 3; ++k) acc[k] += c[u] * ((rn[u][k] - al[k] * vn[u][k]) * dn[u]);
     }
@@ -1455,7 +1455,8 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   DevMesh<T>& M = *X.M;
   dfvm_mesh* m = S->m;
   const Red red{m->part.P, X.red_local};
-  const int gs = grid_slices(k_bi_v<T>, M.n_slices), gt = grid_slices(k_bi_t<T>, M.n_slices);
+  // k_bi_t: batch 4 at >= 3 blocks/SM (batch 2 at 4 blocks/SM measured equal on C5)
+  const int gs = grid_slices(k_bi_v<T>, M.n_slices), gt = grid_slices(k_bi_t<T, 4, 3>, M.n_slices);
   const int ge = grid_for(M.n_own);
   KCtl init[3] = {};
   for (int k = 0; k < 3; ++k) { init[k].tol = tol; init[k].rel_tol = rel_tol; init[k].maxit = maxit; }
@@ -1475,7 +1476,7 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
                                          X.d_ctl, red);
       if ((e = fin(S, X, CTL_BI_V, 3, st))) return e;
       if ((e = halo_exchange(m, X.kr, 3, st)) || (e = halo_exchange(m, X.kv, 3, st))) return e;
-      k_bi_t<T><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket, X.d_ctl, red);
+      k_bi_t<T, 4, 3><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket, X.d_ctl, red);
       if ((e = fin(S, X, CTL_BI_T, 9, st))) return e;
       k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.kp, X.kv, X.kt, X.krh, x, X.kr, X.partials, X.ticket,
                                          X.d_ctl, red);

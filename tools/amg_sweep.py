@@ -35,7 +35,7 @@ for line in open(cfgfile):
     parts = line.split()
     if not parts or parts[0].startswith("#"):
         continue
-    for k in keys:
+    for k in [k for k in os.environ if k.startswith("DFVM_")]:
         os.environ.pop(k, None)
     for kv in parts[1:]:
         k, v = kv.split("=")
