@@ -862,10 +862,10 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   AmgLevelDev<P>& C = A->L[1];
   k_amg_pre<P, T, P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.il1, F.x, done);
   if ((e = halo_exchange_p(A->m, F.x, 1, f64, s))) return e;
-  if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+  if (ev) record_event(ev[0], s);
   k_amg_resid<P, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.x, r, F.r,
                                                        done);
-  if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
+  if (ev) record_event(ev[1], s);
   k_amg_restrict<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
   *nl += 3;
   cycle_coarse(A, 1, C.b, C.x, done, s, nl);
@@ -878,10 +878,10 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   }
   k_amg_prolong<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, F.x, F.t, (P)A->prm.omega, done);
   if ((e = halo_exchange_p(A->m, F.t, 1, f64, s))) return e;
-  if (ev) cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal);
+  if (ev) record_event(ev[2], s);
   k_amg_smooth<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1,
                                                            F.t, r, z, done);
-  if (ev) cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal);
+  if (ev) record_event(ev[3], s);
   *nl += 2;
   return DFVM_OK;
 }

@@ -48,6 +48,17 @@ template <class K> inline int grid_rows(K fn, int64_t n) {
   return (int)(need < 1 ? 1 : (need > cap ? cap : need));
 }
 
+// Timing event on a stream that may be capturing into a CUDA graph: inside a
+// capture the record must be an external event node (else it is only a
+// capture dependency and never fires on replay); outside a capture a plain
+// record (the external flag is an error there).
+inline cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal)
+                                             : cudaEventRecord(ev, s);
+}
+
 template <class T> __device__ __forceinline__ V4<T> ld4(const V4<T>* p);
 // fp64 records (32 B, 32-B aligned) in ONE 256-bit load (sm_100: LDG.E.ENL2.256):
 // a gathered face record costs one L1 request instead of two 128-bit ones —

@@ -1276,16 +1276,16 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
   int it_before = 0;
   for (int it0 = 0;; it0 += kChunk) {
     for (int k = 0; k < kChunk; ++k) {
-      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k], st, cudaEventRecordExternal);
+      if (S->timing) record_event(S->ev[4 * k], st);
       k_cg_p<T><<<gp, kThreads, 0, st>>>(M.n_own, X.kr, X.pdiag, X.kp, x, X.d_ctl);
       if ((e = halo_exchange(m, X.kp, 1, st))) return e;
-      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 1], st, cudaEventRecordExternal);
+      if (S->timing) record_event(S->ev[4 * k + 1], st);
       k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red);
-      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 2], st, cudaEventRecordExternal);
+      if (S->timing) record_event(S->ev[4 * k + 2], st);
       if ((e = fin(S, X, CTL_CG_SPMV, 1, st))) return e;
       k_cg_r<T><<<gr, kThreads, 0, st>>>(M.n_own, X.kq, X.pdiag, X.kr, X.partials, X.ticket, X.d_ctl, red);
       if ((e = fin(S, X, CTL_CG_R, 2, st))) return e;
-      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 3], st, cudaEventRecordExternal);
+      if (S->timing) record_event(S->ev[4 * k + 3], st);
       S->n_launch += 3;
     }
     DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
@@ -1357,12 +1357,12 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   auto enqueue_chunk = [&](int* nl) -> dfvm_status {
     dfvm_status e2;
     for (int k = 0; k < kChunk; ++k) {
-      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k], st, cudaEventRecordExternal);
+      if (S->timing) record_event(S->ev[4 * k], st);
       k_cg_p2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kz, X.kp, x, X.d_ctl);
       if ((e2 = halo_exchange(m, X.kp, 1, st))) return e2;
-      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 1], st, cudaEventRecordExternal);
+      if (S->timing) record_event(S->ev[4 * k + 1], st);
       k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red);
-      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 2], st, cudaEventRecordExternal);
+      if (S->timing) record_event(S->ev[4 * k + 2], st);
       if ((e2 = fin(S, X, CTL_CG_SPMV, 1, st))) return e2;
       k_cg_r2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, X.partials, X.ticket, X.d_ctl, red);
       if ((e2 = fin(S, X, CTL_CG_R2, 1, st))) return e2;
@@ -1370,7 +1370,7 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
         return e2;
       k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ);
       if ((e2 = fin(S, X, CTL_CG_RZ, 1, st))) return e2;
-      if (S->timing) cudaEventRecordWithFlags(S->ev[4 * k + 3], st, cudaEventRecordExternal);
+      if (S->timing) record_event(S->ev[4 * k + 3], st);
       *nl += 4;
     }
     return DFVM_OK;
@@ -1457,6 +1457,8 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   const Red red{m->part.P, X.red_local};
   // k_bi_t: batch 4 at >= 3 blocks/SM (batch 2 at 4 blocks/SM measured equal on C5)
   const int gs = grid_slices(k_bi_v<T>, M.n_slices), gt = grid_slices(k_bi_t<T, 4, 3>, M.n_slices);
+  // (measured on C5: flat [3n] p/x updates and shared-staged own rows in v/t
+  // were 26 ms/step slower than these one-thread-per-row kernels)
   const int ge = grid_for(M.n_own);
   KCtl init[3] = {};
   for (int k = 0; k < 3; ++k) { init[k].tol = tol; init[k].rel_tol = rel_tol; init[k].maxit = maxit; }
@@ -1551,7 +1553,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   if ((s2 = assemble(S, X, U, phi, st))) return s2;
   // 2. predictor
   dfvm_status res = run_bicgstab(S, X, X.rhsU, U, o.U_tol, o.U_rel_tol, o.U_maxit, R->U, st);
-  if (res == DFVM_E_BREAKDOWN) return res;
+  if (res != DFVM_OK && res != DFVM_E_NOT_CONVERGED) return res;   // breakdown, CUDA / NCCL errors
   const int n_wk = (int)S->wk.size();
   int np = 0;
   for (int corr = 1; corr <= o.n_corr; ++corr) {
@@ -1600,7 +1602,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
       s2 = run_cg(S, X, rhs, p, o.p_tol, final_corr ? o.p_rel_tol_final : o.p_rel_tol, o.p_maxit, &sr, st);
       if (np < 16) R->p[np] = sr;
       np++;
-      if (s2 == DFVM_E_BREAKDOWN) return s2;
+      if (s2 != DFVM_OK && s2 != DFVM_E_NOT_CONVERGED) return s2;   // breakdown, CUDA / NCCL errors
       if (s2 == DFVM_E_NOT_CONVERGED) res = s2;
       if (io == o.n_nonorth) {
         if ((s2 = halo_exchange(S->m, p, 1, st))) return s2;

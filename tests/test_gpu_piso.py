@@ -330,3 +330,30 @@ def test_graph_replay_bitwise(precond):
     assert out[0][3] == out[1][3]
     for a, b in zip(out[0][:3], out[1][:3]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("graphs", ["1", "0"])
+def test_live_timing_does_not_change_the_step(graphs, monkeypatch):
+    # live kernel timing (bench.py's roofline) records events inside captured
+    # graphs or directly on the stream; the fields, iteration counts and the
+    # status must be those of an untimed step, and the timers must count
+    import ctypes
+    import torch
+    monkeypatch.setenv("DFVM_GRAPHS", graphs)
+    raw, mo, mg, bo, bg, kw = pipe_case(n=8, m_r=4, n_z=40)
+    U0, p0, phi0 = initial_state(mo)
+    s = torch.cuda.Stream()
+    sp = ctypes.c_void_p(s.cuda_stream)
+    out = []
+    for timing in (False, True):
+        Sg = dfvm.Solver(mg, bg, p_precond="amg32", **kw, **TIGHT)
+        Sg.set_timing(timing)
+        Ug, pg, phig = mg.field("cells", 3, U0, sp), mg.field("cells", 1, p0, sp), mg.field("flux", 1, phi0, sp)
+        reps = [Sg.step(Ug, pg, phig, sp) for _ in range(2)]
+        out.append((Ug.get(sp), pg.get(sp), phig.get(sp), [r["it"] for rep in reps for r in rep["p"]]))
+        if timing:
+            tim = Sg.timing()
+            assert tim["spmv_n"] > 0 and tim["spmv_ms"] > 0 and tim["amg_pre_n"] > 0
+    assert out[0][3] == out[1][3] and min(out[0][3]) > 0
+    for a, b in zip(out[0][:3], out[1][:3]):
+        assert np.array_equal(a, b)
