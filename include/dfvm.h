@@ -294,6 +294,10 @@ typedef struct {
                                    DFVM_TIME_BACKWARD_EULER (0, theta 1, default), DFVM_TIME_CRANK_NICOLSON
                                    (theta 1/2), DFVM_TIME_FORWARD_EULER (theta 0: diagonal predictor).
                                    Out of range -> DFVM_E_INVALID_ARG. */
+  int32_t ddt_corr;             /* 1: add OpenFOAM's Euler ddtCorr Rhie-Chow term to phiHbyA on internal faces
+                                   (A-42): rAU_f c_f (phi^n - U^n_f . S_f) / dt with
+                                   c_f = 1 - min(|phi^n - U^n_f . S_f| / (|phi^n| + 1e-15), 1);
+                                   0 (default): the paper's form without it (A-9) */
 } dfvm_piso_opts;
 enum { DFVM_TIME_BACKWARD_EULER = 0, DFVM_TIME_CRANK_NICOLSON = 1, DFVM_TIME_FORWARD_EULER = 2 };
 

@@ -259,7 +259,7 @@ class Solver:
     def __init__(self, mesh, bcs, nu, dt, rho=1.0, n_corr=2, n_nonorth=0, convection="upwind",
                  p_ref_cell=0, p_ref_value=0.0, direct=False, p_tol=1e-14, p_rel_tol=0.0,
                  p_rel_tol_final=0.0, p_maxit=50000, U_tol=1e-14, U_rel_tol=0.0, U_maxit=50000, p_precond=None,
-                 theta=1.0):
+                 theta=1.0, ddt_corr=False):
         # p_precond is accepted for recipe compatibility and ignored: the oracle
         # always uses Jacobi CG (or dense LU); the converged pressure does not
         # depend on the preconditioner (A-14)
@@ -269,7 +269,7 @@ class Solver:
         d = np.array([nu, dt, rho, p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, U_tol, U_rel_tol, theta],
                      np.float64)
         i = np.array([n_corr, n_nonorth, {"upwind": 0, "central": 1, "sou": 2, "quick": 3}[convection], p_ref_cell,
-                      1 if direct else 0, p_maxit, U_maxit], np.int64)
+                      1 if direct else 0, p_maxit, U_maxit, 1 if ddt_corr else 0], np.int64)
         self.h = lib().orc_solver_create(mesh.h, bcs.h, _p(d), _p(i))
 
     def __del__(self):

@@ -186,6 +186,7 @@ struct Opts {
   double nu, dt, rho;
   double theta;                       // time scheme (Table 1): 1 backward Euler, 0.5 Crank-Nicolson, 0 forward Euler
   int n_corr, n_nonorth, convection;  // convection 0 upwind, 1 central
+  int ddt_corr;                       // OpenFOAM ddtCorr Rhie-Chow term in phiHbyA (reading A-42), 0 off
   int64_t p_ref_cell;
   double p_ref_value;
   int direct;
@@ -407,6 +408,8 @@ static int piso_step(Solver& S, double* U, double* p, double* phi, Report& R) {
         return E_INVALID_ARG;
       }
   b.t_eval = S.t + S.o.dt;
+  // start-of-step state for the optional ddtCorr term (A-42)
+  const std::vector<double> Un(U, U + 3 * N), phin(phi, phi + m.NF);
   // 1. assemble O-5 from (U^n, phi^n, grad U^n)
   LDU M;
   std::vector<double> bvec;
@@ -454,6 +457,21 @@ static int piso_step(Solver& S, double* U, double* p, double* phi, Report& R) {
     for (int64_t f = 0; f < m.NF; ++f) {
       if (f >= m.F && m.is_empty_face(f)) { phiHbyA[f] = 0; continue; }
       phiHbyA[f] = fv[3 * f] * m.Sf[3 * f] + fv[3 * f + 1] * m.Sf[3 * f + 1] + fv[3 * f + 2] * m.Sf[3 * f + 2];
+    }
+    // 3.3' optional ddtCorr (A-42, OpenFOAM's Euler ddtCorr): on internal faces
+    //   phiHbyA += rAU_f c_f (phi^n - U^n_f . S) / dt,
+    //   c_f = 1 - min(|phi^n - U^n_f . S| / (|phi^n| + 1e-15), 1)
+    if (S.o.ddt_corr) {
+      for (int64_t f = 0; f < m.F; ++f) {
+        const int64_t O = m.owner[f], Nn = m.neigh[f];
+        const double w = m.w[f];
+        double uS = 0;
+        for (int l = 0; l < 3; ++l) uS += (w * Un[3 * O + l] + (1.0 - w) * Un[3 * Nn + l]) * m.Sf[3 * f + l];
+        const double d = phin[f] - uS;
+        const double c = 1.0 - std::min(std::fabs(d) / (std::fabs(phin[f]) + 1e-15), 1.0);
+        const double rf = w * rAU[O] + (1.0 - w) * rAU[Nn];
+        phiHbyA[f] += rf * c * d / S.o.dt;
+      }
     }
     // 3.4 pressure coefficients
     LDU A;
@@ -572,7 +590,7 @@ int orc_ldu_apply(const void* mp, const double* diag, const double* lower, const
 
 void* orc_solver_create(const void* mp, void* bp, const double* dopts, const int64_t* iopts) {
   // dopts: nu, dt, rho, p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, U_tol, U_rel_tol, theta
-  // iopts: n_corr, n_nonorth, convection, p_ref_cell, direct, p_maxit, U_maxit
+  // iopts: n_corr, n_nonorth, convection, p_ref_cell, direct, p_maxit, U_maxit, ddt_corr
   Solver* S = new Solver();
   S->m = (const Mesh*)mp;
   S->b = (BCs*)bp;
@@ -582,6 +600,7 @@ void* orc_solver_create(const void* mp, void* bp, const double* dopts, const int
   o.U_tol = dopts[7]; o.U_rel_tol = dopts[8]; o.theta = dopts[9];
   o.n_corr = (int)iopts[0]; o.n_nonorth = (int)iopts[1]; o.convection = (int)iopts[2];
   o.p_ref_cell = iopts[3]; o.direct = (int)iopts[4]; o.p_maxit = (int)iopts[5]; o.U_maxit = (int)iopts[6];
+  o.ddt_corr = (int)iopts[7];
   return S;
 }
 void orc_solver_destroy(void* s) { delete (Solver*)s; }

@@ -82,7 +82,7 @@ class PisoOpts(C.Structure):
                 ("p_ref_value", C.c_double), ("p_tol", C.c_double), ("p_rel_tol", C.c_double),
                 ("p_rel_tol_final", C.c_double), ("p_maxit", C.c_int32), ("U_tol", C.c_double),
                 ("U_rel_tol", C.c_double), ("U_maxit", C.c_int32), ("p_precond", C.c_int32),
-                ("time_scheme", C.c_int32)]
+                ("time_scheme", C.c_int32), ("ddt_corr", C.c_int32)]
 
 
 class SolveReport(C.Structure):
@@ -496,7 +496,7 @@ class Solver:
 
     def __init__(self, mesh, bcs, nu, dt, rho=1.0, n_corr=2, n_nonorth=0, convection="upwind", p_ref_cell=0,
                  p_ref_value=0.0, p_tol=1e-14, p_rel_tol=0.0, p_rel_tol_final=0.0, p_maxit=50000, U_tol=1e-14,
-                 U_rel_tol=0.0, U_maxit=50000, p_precond="jacobi", theta=1.0):
+                 U_rel_tol=0.0, U_maxit=50000, p_precond="jacobi", theta=1.0, ddt_corr=False):
         self.mesh, self.bcs = mesh, bcs
         # time scheme (Table 1): theta 1 backward Euler, 0.5 Crank-Nicolson, 0 forward Euler
         schemes = {1.0: 0, 0.5: 1, 0.0: 2}
@@ -505,7 +505,7 @@ class Solver:
         o = PisoOpts(nu, dt, rho, n_corr, n_nonorth, {"upwind": 0, "central": 1, "sou": 2, "quick": 3}[convection],
                      p_ref_cell,
                      p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, p_maxit, U_tol, U_rel_tol, U_maxit,
-                     {"jacobi": 0, "amg": 1, "amg32": 2}[p_precond], schemes[float(theta)])
+                     {"jacobi": 0, "amg": 1, "amg32": 2}[p_precond], schemes[float(theta)], 1 if ddt_corr else 0)
         h = C.c_void_p()
         _check(lib().dfvm_solver_create(mesh.h, bcs.h, C.byref(o), C.byref(h)))
         self.h = h.value

@@ -377,9 +377,12 @@ __global__ void __launch_bounds__(kThreads) k_HbyA(DevMesh<T> M, const T* __rest
 }
 
 // phiHbyA_f = interp(HbyA) . S_f; boundary: U_b . S_b (fixed U) or HbyA_O . S_b
+// Optional ddtCorr (A-42, OpenFOAM's Euler ddtCorr) on internal faces:
+// phiHbyA += rAU_f c_f (phi^n - U^n_f . S) / dt, c_f = 1 - min(|d| / (|phi^n| + 1e-15), 1)
 template <class T>
 __global__ void k_phiHbyA(DevMesh<T> M, const T* __restrict__ HbyA, const uint8_t* __restrict__ bk,
-                          const T* __restrict__ bv, T* __restrict__ out) {
+                          const T* __restrict__ bv, T* __restrict__ out, const T* __restrict__ Uold,
+                          const T* __restrict__ phiold, const T* __restrict__ rAU, T rdt) {
   const int64_t total = (int64_t)M.F + M.B;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < M.F) {
@@ -387,8 +390,20 @@ __global__ void k_phiHbyA(DevMesh<T> M, const T* __restrict__ HbyA, const uint8_
       const V4<T> g = ld4(&M.fgeo[i]);
       const T* a = HbyA + 3 * (int64_t)c.x;
       const T* b = HbyA + 3 * (int64_t)c.y;
-      out[i] = (g.w * a[0] + (T(1) - g.w) * b[0]) * g.x + (g.w * a[1] + (T(1) - g.w) * b[1]) * g.y +
-               (g.w * a[2] + (T(1) - g.w) * b[2]) * g.z;
+      T v = (g.w * a[0] + (T(1) - g.w) * b[0]) * g.x + (g.w * a[1] + (T(1) - g.w) * b[1]) * g.y +
+            (g.w * a[2] + (T(1) - g.w) * b[2]) * g.z;
+      if (Uold) {
+        const T* uo = Uold + 3 * (int64_t)c.x;
+        const T* un = Uold + 3 * (int64_t)c.y;
+        const T uS = (g.w * uo[0] + (T(1) - g.w) * un[0]) * g.x + (g.w * uo[1] + (T(1) - g.w) * un[1]) * g.y +
+                     (g.w * uo[2] + (T(1) - g.w) * un[2]) * g.z;
+        const T ph = phiold[i];
+        const T d = ph - uS;
+        const T cc = T(1) - fmin(fabs(d) / (fabs(ph) + T(1e-15)), T(1));
+        const T rf = g.w * rAU[c.x] + (T(1) - g.w) * rAU[c.y];
+        v += rf * cc * d * rdt;
+      }
+      out[i] = v;
     } else {
       const int b = (int)(i - M.F);
       const V4<T> g = ld4(&M.bgeo[b]);
@@ -1089,6 +1104,8 @@ struct SolverT : SolverBase {
   struct ChunkGraph { const void* x; const void* b; bool timing; cudaGraphExec_t exec; int launches; };
   std::vector<ChunkGraph> graphs;
   bool graphs_off = false;
+  T* Uold = nullptr;     // start-of-step U and phi (ddtCorr, A-42; allocated on first use)
+  T* phiold = nullptr;
   ~SolverT() override {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (amg) amg_destroy<T>(amg);
@@ -1551,6 +1568,11 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   S->n_launch++;
   // 1. momentum assembly from (U^n, phi^n, grad U^n)
   if ((s2 = assemble(S, X, U, phi, st))) return s2;
+  if (o.ddt_corr) {   // start-of-step U (with ghosts, exchanged by assemble) and phi for ddtCorr (A-42)
+    if (!X.Uold && ((s2 = X.al(&X.Uold, 3 * (size_t)M.n_cells)) || (s2 = X.al(&X.phiold, (size_t)M.F + 1)))) return s2;
+    DFVM_CUDA(cudaMemcpyAsync(X.Uold, U, 3 * (size_t)M.n_cells * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    DFVM_CUDA(cudaMemcpyAsync(X.phiold, phi, (size_t)M.F * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  }
   // 2. predictor
   dfvm_status res = run_bicgstab(S, X, X.rhsU, U, o.U_tol, o.U_rel_tol, o.U_maxit, R->U, st);
   if (res != DFVM_OK && res != DFVM_E_NOT_CONVERGED) return res;   // breakdown, CUDA / NCCL errors
@@ -1575,7 +1597,8 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
     S->n_launch++;
     if ((s2 = halo_exchange(S->m, X.HbyA, 3, st)) || (s2 = halo_exchange(S->m, X.rAU, 1, st))) return s2;
     // 3.3 phiHbyA
-    k_phiHbyA<T><<<gf, kThreads, 0, st>>>(M, X.HbyA, bkU, bvU, X.phiHbyA);
+    k_phiHbyA<T><<<gf, kThreads, 0, st>>>(M, X.HbyA, bkU, bvU, X.phiHbyA, o.ddt_corr ? X.Uold : nullptr, X.phiold,
+                                          X.rAU, (T)(1.0 / o.dt));
     // 3.4 pressure coefficients
     k_pcoef<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
                                         (T)o.p_ref_value, X.pcoef, X.pdiag, X.prhs0);
@@ -1692,7 +1715,7 @@ dfvm_status dfvm_solver_create(dfvm_mesh* m, dfvm_bcs* b, const dfvm_piso_opts* 
   if (!(opts->dt > 0) || !(opts->nu >= 0) || opts->n_corr < 1 || opts->n_corr > 8 || opts->n_nonorth < 0 ||
       (opts->n_corr * (opts->n_nonorth + 1)) > 16 || opts->p_maxit < 1 || opts->U_maxit < 1 || !(opts->rho > 0) ||
       opts->p_precond < 0 || opts->p_precond > 2 || opts->convection < 0 || opts->convection > 3 ||
-      opts->time_scheme < DFVM_TIME_BACKWARD_EULER || opts->time_scheme > DFVM_TIME_FORWARD_EULER) {
+      opts->time_scheme < DFVM_TIME_BACKWARD_EULER || opts->time_scheme > DFVM_TIME_FORWARD_EULER || opts->ddt_corr < 0 || opts->ddt_corr > 1) {
     set_error(DFVM_E_INVALID_ARG, "invalid PISO options");
     return DFVM_E_INVALID_ARG;
   }

@@ -144,3 +144,35 @@ def test_polymesh_case_on_gpu(tmp_path):
     o, g, _, _, _ = run_both(raw, mo, mg, bo, bg, kw, steps=3)
     for a, b in zip(g, o):
         assert rel_l2(a, b) <= 1e-8
+
+
+@pytest.mark.parametrize("theta", [0.5, 0.0])
+def test_f32_theta_waveform_close_to_oracle(theta):
+    # the fp32 library path of NEXT-4 (theta assembly, k_bc_wave in float)
+    raw, mo, mg, bo, bg, kw = cavity_case(precision="f32")
+    wave = (0.02, [1.0, 0.3], [0.0, 0.2])
+    bo.set_waveform(raw.patch("movingWall"), "U", *wave)
+    bg.set_waveform(raw.patch("movingWall"), "U", *wave)
+    kw = dict(kw, theta=theta, dt=0.0005 if theta == 0.0 else kw["dt"])
+    Sg = dfvm.Solver(mg, bg, **kw, p_tol=1e-6, U_tol=1e-6)
+    Ug, pg, phig = mg.field("cells", 3), mg.field("cells", 1), mg.field("flux", 1)
+    So = oracle.Solver(mo, bo, direct=True, **kw)
+    U, p, phi = np.zeros((mo.N, 3)), np.zeros(mo.N), np.zeros(mo.NF)
+    for _ in range(5):
+        Sg.step(Ug, pg, phig)
+        So.step(U, p, phi)
+    assert rel_l2(Ug.get(), U) <= 1e-4 and rel_l2(pg.get(), p) <= 1e-3
+
+
+@pytest.mark.parametrize("case", ["cavity", "pipe"])
+def test_ddtcorr_steps(case):
+    # OpenFOAM's Euler ddtCorr Rhie-Chow term (A-42) against the oracle
+    if case == "cavity":
+        raw, mo, mg, bo, bg, kw = cavity_case()
+    else:
+        raw, mo, mg, bo, bg, kw = pipe_case()
+        kw = dict(kw, p_precond="amg32")
+    kw = dict(kw, ddt_corr=True)
+    o, g, _, _, _ = run_both(raw, mo, mg, bo, bg, kw, steps=4)
+    for a, b in zip(g, o):
+        assert rel_l2(a, b) <= 1e-8

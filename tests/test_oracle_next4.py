@@ -141,3 +141,48 @@ def test_waveform_rejected_on_zero_gradient_patch():
     with pytest.raises(oracle.OracleError) as e:
         S.step(U, p, phi)
     assert e.value.status == "INVALID_ARG"
+
+
+# ---------------------------------------------------------------- ddtCorr (A-42)
+def _cavity(ddt_corr):
+    import cases
+    case = cases.c1(scramble=11)
+    mo = oracle.Mesh(case.raw)
+    b = case.apply_bcs(oracle.BCs(mo))
+    return mo, oracle.Solver(mo, b, **dict(case.solver, ddt_corr=ddt_corr))
+
+
+def test_ddtcorr_vanishes_on_a_consistent_start():
+    # phi^n = interp(U^n).S on every internal face (the cavity from rest) ->
+    # d = 0, the term is exactly zero: step 1 bitwise equal; later steps differ
+    runs = []
+    for flag in (False, True):
+        mo, S = _cavity(flag)
+        U, p, phi = np.zeros((mo.N, 3)), np.zeros(mo.N), np.zeros(mo.NF)
+        S.step(U, p, phi)
+        first = (U.copy(), p.copy(), phi.copy())
+        S.step(U, p, phi)
+        runs.append((first, (U, p, phi)))
+    for x, y in zip(runs[0][0], runs[1][0]):
+        assert np.array_equal(x, y)
+    assert not np.array_equal(runs[0][1][2], runs[1][1][2])
+    # a small correction: the two fluxes agree to O(dt) of the flux scale
+    assert np.abs(runs[0][1][2] - runs[1][1][2]).max() <= 0.05 * np.abs(runs[0][1][2]).max()
+
+
+def test_ddtcorr_keeps_uniform_flow_fixed_point():
+    raw = synth.box(6, 5, 4, 1.0, 1.0, 1.0, split=5, jitter=0.15, scramble=9)
+    m = oracle.Mesh(raw)
+    b = oracle.BCs(m)
+    u = np.array([0.7, -0.3, 0.2])
+    xmin = raw.patch("xmin")
+    for i, pt in enumerate(raw.patches):
+        b.set(i, "U", oracle.BC_FIXED, tuple(u))
+        b.set(i, "p", oracle.BC_FIXED if i == xmin else oracle.BC_ZEROGRAD, (0.0, 0.0, 0.0))
+    S = oracle.Solver(m, b, nu=0.01, dt=0.01, n_corr=2, n_nonorth=1, ddt_corr=True, U_tol=1e-15, p_tol=1e-15)
+    U = np.tile(u, (m.N, 1))
+    p = np.zeros(m.N)
+    phi = m.Sf @ u
+    for _ in range(3):
+        S.step(U, p, phi)
+    assert np.abs(U - u).max() <= 1e-11 and np.abs(phi - m.Sf @ u).max() <= 1e-11 * np.abs(m.Sf).max()
