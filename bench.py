@@ -222,6 +222,9 @@ def main():
             run_reference(args)
         return
 
+    if world > 1 and "OMP_NUM_THREADS" not in os.environ:
+        # every rank runs the host mesh pipeline (OpenMP) at the same time: share the cores
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or world) // world))
     import torch
     import paper_2603_15920_b200 as dfvm
     import cases
