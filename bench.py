@@ -92,8 +92,9 @@ def oracle_sample(config, precision, steps=1, warmup=0):
     (2-8 s of CPU work per step; the GPU bench's cpu_baseline times 3 steps
     after one warm-up, ~10-30 s), pressure CG capped at 200 iterations per
     solve.  (The oracle visits faces in the generator's scrambled order, so
-    larger samples leave the host caches and slow down superlinearly.)  `warmup` untimed steps, then `steps` timed ones; the mesh and the
-    solver are built once."""
+    larger samples leave the host caches and slow down superlinearly.)
+    `warmup` untimed steps, then `steps` timed ones; the mesh and the solver
+    are built once."""
     import cases
     import oracle
     if config == "c5":
