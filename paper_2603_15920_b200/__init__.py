@@ -221,7 +221,10 @@ class Comm:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().dfvm_comm_destroy(self.h)
+            try:
+                lib().dfvm_comm_destroy(self.h)
+            except (TypeError, AttributeError):   # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
 
@@ -323,7 +326,10 @@ class Mesh:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().dfvm_mesh_destroy(self.h)
+            try:
+                lib().dfvm_mesh_destroy(self.h)
+            except (TypeError, AttributeError):   # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     def export_maps(self):
@@ -377,7 +383,10 @@ class Field:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().dfvm_field_destroy(self.h)
+            try:
+                lib().dfvm_field_destroy(self.h)
+            except (TypeError, AttributeError):   # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     @property
@@ -428,7 +437,10 @@ class BCs:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().dfvm_bcs_destroy(self.h)
+            try:
+                lib().dfvm_bcs_destroy(self.h)
+            except (TypeError, AttributeError):   # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     def set(self, patch, fld, kind, value=(0.0, 0.0, 0.0), u_max=0.0, center=(0.0, 0.0, 0.0), radius=1.0):
@@ -512,7 +524,10 @@ class Solver:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().dfvm_solver_destroy(self.h)
+            try:
+                lib().dfvm_solver_destroy(self.h)
+            except (TypeError, AttributeError):   # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     def windkessel_set(self, patch, Rp, Cc, Rd, pc0=0.0, scheme=0):

@@ -921,8 +921,8 @@ __global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ v, 
 }
 
 // v = A (p / diag); partial (rh, v) -> alpha   (dinv = 1 / diag)
-template <class T>
-__global__ void __launch_bounds__(kThreads) k_bi_v(DevMesh<T> M, const T* __restrict__ diag,
+template <class T, int KBV, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_bi_v(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ dinv, const T* __restrict__ coef, const T* __restrict__ p, const T* __restrict__ rh,
     T* __restrict__ v, double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   if (all_done(ctl)) return;
@@ -937,19 +937,19 @@ __global__ void __launch_bounds__(kThreads) k_bi_v(DevMesh<T> M, const T* __rest
     const int len = __ldg(&M.ms_len[s]);
     const int base = __ldg(&M.ms_ptr[s]) + lane;
     int j = 0;
-    for (; j + 4 <= len; j += 4) {
-      T c[4], dn[4], pn[4][3];
-      int nn[4];
+    for (; j + KBV <= len; j += KBV) {
+      T c[KBV], dn[KBV], pn[KBV][3];
+      int nn[KBV];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) { c[u] = __ldg(&coef[base + 32 * (j + u)]); nn[u] = __ldg(&M.mnb[base + 32 * (j + u)]); }
+      for (int u = 0; u < KBV; ++u) { c[u] = __ldg(&coef[base + 32 * (j + u)]); nn[u] = __ldg(&M.mnb[base + 32 * (j + u)]); }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < KBV; ++u) {
         dn[u] = dinv[nn[u]];
 #pragma unroll
         for (int k = 0; k < 3; ++k) pn[u][k] = p[3 * (int64_t)nn[u] + k];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < KBV; ++u)
 #pragma unroll
         for (int k = 0; k < 3; ++k) acc[k] += c[u] * (pn[u][k] * dn[u]);
     }
@@ -1473,7 +1473,9 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   dfvm_mesh* m = S->m;
   const Red red{m->part.P, X.red_local};
   // k_bi_t: batch 4 at >= 3 blocks/SM (batch 2 at 4 blocks/SM measured equal on C5)
-  const int gs = grid_slices(k_bi_v<T>, M.n_slices), gt = grid_slices(k_bi_t<T, 4, 3>, M.n_slices);
+  // batch depth / min blocks per SM: measured on C5 against batch 2 and 1
+  // with two-load 3-vector gathers (profiles/r01_bicgstab_variants_c5.txt)
+  const int gs = grid_slices(k_bi_v<T, 4, 6>, M.n_slices), gt = grid_slices(k_bi_t<T, 4, 3>, M.n_slices);
   // (measured on C5: flat [3n] p/x updates and shared-staged own rows in v/t
   // were 26 ms/step slower than these one-thread-per-row kernels)
   const int ge = grid_for(M.n_own);
@@ -1491,8 +1493,8 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
     for (int k = 0; k < kChunk; ++k) {
       k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.kp, X.d_ctl);
       if ((e = halo_exchange(m, X.kp, 3, st))) return e;
-      k_bi_v<T><<<gs, kThreads, 0, st>>>(M, X.udiag, X.udinv, X.ucoef, X.kp, X.krh, X.kv, X.partials, X.ticket,
-                                         X.d_ctl, red);
+      k_bi_v<T, 4, 6><<<gs, kThreads, 0, st>>>(M, X.udiag, X.udinv, X.ucoef, X.kp, X.krh, X.kv, X.partials, X.ticket,
+                                               X.d_ctl, red);
       if ((e = fin(S, X, CTL_BI_V, 3, st))) return e;
       if ((e = halo_exchange(m, X.kr, 3, st)) || (e = halo_exchange(m, X.kv, 3, st))) return e;
       k_bi_t<T, 4, 3><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket, X.d_ctl, red);
