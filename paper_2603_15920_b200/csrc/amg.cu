@@ -237,6 +237,10 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     int nc = 0;
     std::vector<int> agg = aggregate(F, nc);
     if (nc >= F.n * 0.85) break;           // coarsening stalled
+    // no degenerate tiny level: C5 with DFVM_AMG_COARSE=128 grew an 8-row
+    // level under the 144-row one and the PCG needed 1702 iterations per
+    // solve; the current level becomes the coarsest (solved exactly)
+    if (nc < 32) break;
     if (A->prm.sigma) {   // SELL-32-sigma: renumber the aggregates so that, within windows of 256
         // (8 slices, locality kept), rows are sorted by length: less padding
         // in the coarse SELL (35 % -> a few % on the C5 level 1)
