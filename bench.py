@@ -7,7 +7,7 @@ momentum assembly + BiCGStab predictor, n_corr correctors with Windkessel,
 H/rAU/HbyA, phiHbyA, pressure coefficients, PCG pressure solves, Rhie-Chow
 flux correction, velocity correction, continuity) on the configured mesh.
 
-    python bench.py [--gpus N --steps K --warmup W --config c5|c2|c1 --precision f64|f32]
+    python bench.py [--gpus N --steps K --warmup W --config c5|c4|c3|c2|c1 --precision f64|f32]
     python bench.py --impl reference ...   # the CPU oracle arm (bounded sample)
 
 value   = cells x steps / device seconds (max over ranks), whole job.
@@ -103,6 +103,9 @@ def oracle_sample(config, precision, steps=1, warmup=0):
     elif config == "c4":
         case = cases.c4(target_cells=1.0e6)
         sample = "PISO steps of the C4 H-tree generator at ~1e6 tets, C4 physics + 8 RCR outlets, CG capped at 200 it/solve"
+    elif config == "c3":
+        case = cases.c3(target_cells=1.0e5)
+        sample = "PISO steps of the C3 polygon-dual cylinder generator at ~1e5 cells, C3 physics, CG capped at 200 it/solve"
     elif config == "c2":
         case = cases.c2()
         sample = "PISO steps of C2 (199,680 tets), CG capped at 200 it/solve"
@@ -208,7 +211,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dfvm", choices=["dfvm", "reference"])
-    ap.add_argument("--config", default="c5", choices=["c5", "c4", "c2", "c1"])
+    ap.add_argument("--config", default="c5", choices=["c5", "c4", "c3", "c2", "c1"])
     ap.add_argument("--nz", type=int, default=None, help="override C5 axial layers (814 = 50.0M cells)")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--precond", default="amg32", choices=["jacobi", "amg", "amg32"],
