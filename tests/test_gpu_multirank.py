@@ -190,3 +190,44 @@ def test_adjoint_pieces_partitioned_equal_single(P):
         outs[r][0].get(sp[r], out=y)
         outs[r][1].get(sp[r], out=g)
     assert np.array_equal(y, ref_y) and np.array_equal(g[:, 0], ref_g)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_next4_partitioned_matches_single(P):
+    # NEXT-4 on a partitioned mesh: Crank-Nicolson (explicit part gathers ghost
+    # U), a pulsatile inlet waveform (per-rank boundary faces) and ddtCorr
+    # (start-of-step U with ghosts) equal the single-rank step
+    raw = _pipe()
+    mo = oracle.Mesh(raw)
+    U0 = np.zeros((raw.n_cells, 3))
+    U0[:, 2] = 2.0 * (1 - 4 * (mo.xc[:, 0] ** 2 + mo.xc[:, 1] ** 2))
+    U0 += 0.01 * synth.cell_field(21, raw.n_cells, 3)
+    phi0 = np.zeros(mo.NF)
+    kw = dict(nu=0.1, dt=0.005, n_corr=2, n_nonorth=1, convection="upwind", theta=0.5, ddt_corr=True, **TIGHT)
+    wave = (0.03, [1.0, 0.4], [0.0, 0.3])
+
+    def setup(m):
+        b = _bcs(m)
+        b.set_waveform(raw.patch("inlet"), "U", *wave)
+        S = dfvm.Solver(m, b, **kw)
+        return b, S, m.field("cells", 3, U0), m.field("cells", 1), m.field("flux", 1, phi0)
+    m1 = dfvm.Mesh(raw)
+    b1, S1, U1, p1, f1 = setup(m1)
+    for _ in range(3):
+        S1.step(U1, p1, f1)
+    refU, refp, refphi = U1.get(), p1.get(), f1.get()
+    comms = dfvm.Comm.local_group(P)
+    ms = [dfvm.Mesh(raw, n_parts=P, rank=r, comm=comms[r]) for r in range(P)]
+    st = [setup(m) for m in ms]
+    _, sp = _streams(P)
+
+    def work(r):
+        def f():
+            for _ in range(3):
+                st[r][1].step(st[r][2], st[r][3], st[r][4], stream=sp[r])
+        return f
+    _run_threads([work(r) for r in range(P)])
+    U = np.zeros((raw.n_cells, 3)); p = np.zeros((raw.n_cells, 1)); phi = np.zeros((mo.NF, 1))
+    for r in range(P):
+        st[r][2].get(sp[r], out=U); st[r][3].get(sp[r], out=p); st[r][4].get(sp[r], out=phi)
+    assert rel_l2(U, refU) <= 1e-10 and rel_l2(p[:, 0], refp) <= 1e-10 and rel_l2(phi[:, 0], refphi) <= 1e-10
