@@ -63,3 +63,26 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(dfvm.DfvmError) as ei:
         dfvm.Mesh(synth.cavity())
     assert ei.value.status == "CUDA"
+
+
+def test_missing_library_raises(monkeypatch, tmp_path):
+    """Without libdfvm.so the binding raises instead of running anything else:
+    there is no CPU or oracle fallback on the product path."""
+    monkeypatch.setattr(dfvm, "_LIB", None)
+    monkeypatch.setattr(dfvm, "LIB_PATH", str(tmp_path / "libdfvm.so"))
+    with pytest.raises(dfvm.DfvmError) as ei:
+        dfvm.lib()
+    assert "missing" in str(ei.value)
+
+
+def test_product_path_never_imports_oracle():
+    """The package and bench's timed arm share no code with oracle/: no module
+    of the package imports it, and the library does not link liboracle."""
+    pkg = os.path.join(ROOT, "paper_2603_15920_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
+                src = open(os.path.join(dirpath, f), errors="replace").read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", src, flags=re.M), f
+                assert "liboracle" not in src, f
+                assert "oracle/" not in src.replace("oracle/`", ""), f
