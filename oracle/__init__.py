@@ -8,6 +8,9 @@ SURVEY.md §8(c); it shares no code with the CUDA library and works in the
 caller's original numbering.
 
 Parity status of each function is listed in DESIGN.md ("Oracle pins").
+Parity unpinned: the Windkessel coupling inside PISO (reading A-19), the
+ddtCorr-free Rhie-Chow flux (A-9) on non-orthogonal tets and the optional
+ddtCorr term (A-42) -- checked only against invariants.
 """
 from __future__ import annotations
 

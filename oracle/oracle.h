@@ -12,6 +12,12 @@
 // ascending face index (internal faces, then boundary patches in patch
 // order); every cell accumulator receives its contributions in that order;
 // dot products run in ascending cell order.
+//
+// Parity unpinned: the Windkessel coupling inside the PISO
+// step (reading A-19), the ddtCorr-free Rhie-Chow face flux (A-9) on
+// non-orthogonal tets and the optional ddtCorr term (A-42) have no closed
+// form or printed example; they are checked only against invariants
+// (continuity, uniform-flow fixed point, zero ddtCorr on a consistent start).
 #pragma once
 #include <cstdint>
 #include <string>
