@@ -223,6 +223,20 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
 
+    # --gpus N without a torchrun environment: launch the N ranks ourselves
+    # (one process per GPU, NCCL over NVLink), exactly as the driver would
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus and args.impl != "reference":
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}"}), flush=True)
+        sys.exit(2)
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -239,6 +253,9 @@ def main():
     import cases
 
     torch.cuda.set_device(local)
+    # every library device buffer comes from torch's caching allocator
+    # (dfvm_set_allocator; north star "PyTorch only for device memory")
+    dfvm.use_torch_allocator()
     dist = None
     comm = None
     if world > 1:

@@ -71,6 +71,15 @@ def c2(scramble=12):
                 "O-grid pipe R=0.5 L=2.6, alternating 5-tet, N=199680, Re_D=10")
 
 
+def c2_small(n_z=8, scramble=12):
+    """The C2 recipe (same O-grid cross-section, physics and solver settings)
+    on a short pipe (n_z layers of L = 0.05 n_z): a test-sized case."""
+    raw = synth.pipe(16, 8, n_z, 0.5, 0.05 * n_z, True, scramble)
+    solver = dict(nu=0.1, dt=0.002, n_corr=2, n_nonorth=1, convection="upwind", p_ref_cell=0, **THROUGHPUT)
+    return Case(f"c2_small_pipe_tet_{raw.n_cells}", raw, _pipe_bcs(2.0, 0.5), solver, _poiseuille_ic(21, 2.0, 0.5),
+                f"C2 cross-section, n_z={n_z}, N={raw.n_cells}")
+
+
 def c5(n_z=814, scramble=15):
     raw = synth.pipe_c5(n_z=n_z, scramble=scramble)
     solver = dict(nu=0.01, dt=0.001, n_corr=2, n_nonorth=1, convection="upwind", p_ref_cell=0, **THROUGHPUT)

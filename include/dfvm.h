@@ -73,6 +73,26 @@ int64_t dfvm_last_error_index(void);
 /* library build/version string (also names the CUDA arch it was built for) */
 const char* dfvm_version(void);
 
+/* ------------------------------------------------------------- allocator
+ * §8(b) row b3 (north star: "PyTorch only for device memory"): every device
+ * buffer the library owns (mesh arrays, boundary values, library-owned
+ * fields, solver / AMG workspace, halo and staging buffers) comes from
+ * alloc(bytes, stream, ctx) and goes back through free_(ptr, bytes, stream,
+ * ctx); pass torch's caching allocator (torch.cuda.caching_allocator_alloc /
+ * _delete) to let PyTorch own the memory.  Default (both NULL):
+ * cudaMallocAsync / cudaFreeAsync on the stream.  `stream` is the caller's
+ * stream of the compute call that allocates lazily, or the legacy stream (0)
+ * for allocations made by *_create (which synchronise before returning);
+ * the library zero-fills new buffers on that stream.  Process-wide; may only
+ * be changed while no library allocation is live (else DFVM_E_INVALID_ARG,
+ * index = number of live allocations).  alloc returning NULL -> DFVM_E_OOM.
+ * The callbacks may be called from any thread that calls the library. */
+typedef void* (*dfvm_alloc_fn)(size_t bytes, dfvm_stream stream, void* ctx);
+typedef void (*dfvm_free_fn)(void* ptr, size_t bytes, dfvm_stream stream, void* ctx);
+dfvm_status dfvm_set_allocator(dfvm_alloc_fn alloc, dfvm_free_fn free_, void* ctx);
+/* bytes currently held by library allocations (all meshes / fields / solvers) */
+int64_t dfvm_live_device_bytes(void);
+
 /* ------------------------------------------------------------------ comm
  * Multi-GPU (§8(e)): one process per GPU.  Rank 0 calls dfvm_comm_unique_id,
  * the caller broadcasts the 128 bytes with torch.distributed, every rank
@@ -298,6 +318,11 @@ typedef struct {
                                    (A-42): rAU_f c_f (phi^n - U^n_f . S_f) / dt with
                                    c_f = 1 - min(|phi^n - U^n_f . S_f| / (|phi^n| + 1e-15), 1);
                                    0 (default): the paper's form without it (A-9) */
+  double cont_tol;              /* continuity check ("divergence check failure -> ContinuityViolation";
+                                   S:474 "max cell |sum mdot_f| <= 10 x pressure tolerance"): > 0 -> after the
+                                   step, max_c |D_c(phi)| > cont_tol returns DFVM_E_CONTINUITY (the step is
+                                   committed and the report filled, so the caller sees the offending value);
+                                   0 (default): reported only */
 } dfvm_piso_opts;
 enum { DFVM_TIME_BACKWARD_EULER = 0, DFVM_TIME_CRANK_NICOLSON = 1, DFVM_TIME_FORWARD_EULER = 2 };
 

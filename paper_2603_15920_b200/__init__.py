@@ -42,7 +42,7 @@ SYMBOLS = [
     "dfvm_solver_set_timing", "dfvm_solver_get_timing", "dfvm_comm_create_local", "dfvm_solver_amg_levels",
     "dfvm_transport_step", "dfvm_momentum_apply_transpose", "dfvm_pressure_solve_adjoint", "dfvm_pressure_vjp",
     "dfvm_bcs_set_waveform", "dfvm_bcs_set_time", "dfvm_polymesh_read", "dfvm_polymesh_sizes",
-    "dfvm_polymesh_arrays", "dfvm_polymesh_destroy",
+    "dfvm_polymesh_arrays", "dfvm_polymesh_destroy", "dfvm_set_allocator", "dfvm_live_device_bytes",
 ]
 
 
@@ -82,7 +82,7 @@ class PisoOpts(C.Structure):
                 ("p_ref_value", C.c_double), ("p_tol", C.c_double), ("p_rel_tol", C.c_double),
                 ("p_rel_tol_final", C.c_double), ("p_maxit", C.c_int32), ("U_tol", C.c_double),
                 ("U_rel_tol", C.c_double), ("U_maxit", C.c_int32), ("p_precond", C.c_int32),
-                ("time_scheme", C.c_int32), ("ddt_corr", C.c_int32)]
+                ("time_scheme", C.c_int32), ("ddt_corr", C.c_int32), ("cont_tol", C.c_double)]
 
 
 class SolveReport(C.Structure):
@@ -93,6 +93,12 @@ class StepReport(C.Structure):
     _fields_ = [("U", SolveReport * 3), ("p", SolveReport * 16), ("n_p", C.c_int32), ("cont_err_max", C.c_double),
                 ("cont_err_sum", C.c_double), ("n_outlets", C.c_int32), ("Q", C.c_double * 64),
                 ("p_o", C.c_double * 64), ("nonfinite", C.c_int32), ("gpu_launches", C.c_int32)]
+
+
+# dfvm_alloc_fn / dfvm_free_fn (include/dfvm.h, §8(b) b3)
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_ALLOCATOR = None   # keeps the ctypes callbacks alive while installed
 
 
 def lib():
@@ -157,6 +163,8 @@ def lib():
         L.dfvm_comm_create.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
         L.dfvm_comm_destroy.argtypes = [vp]
         L.dfvm_comm_create_local.argtypes = [C.c_int, vp, vp]
+        L.dfvm_set_allocator.argtypes = [ALLOC_FN, FREE_FN, vp]
+        L.dfvm_live_device_bytes.restype = i64
         _LIB = L
     return _LIB
 
@@ -185,6 +193,42 @@ def current_stream():
 
 def kernel_launches():
     return int(lib().dfvm_kernel_launches())
+
+
+def live_device_bytes():
+    """Bytes held by library-owned device allocations (dfvm_live_device_bytes)."""
+    return int(lib().dfvm_live_device_bytes())
+
+
+def set_allocator(alloc=None, free=None):
+    """dfvm_set_allocator: alloc(nbytes, stream) -> device pointer, free(ptr,
+    nbytes, stream); both None restores the default (cudaMallocAsync).  Only
+    while no library allocation is live."""
+    global _ALLOCATOR
+    if (alloc is None) != (free is None):
+        raise ValueError("set_allocator needs both callbacks or neither")
+    if alloc is None:
+        _check(lib().dfvm_set_allocator(C.cast(None, ALLOC_FN), C.cast(None, FREE_FN), None))
+        _ALLOCATOR = None
+        return
+    fa = ALLOC_FN(lambda n, s, ctx: alloc(n, s or 0) or None)
+    ff = FREE_FN(lambda p, n, s, ctx: free(p, n, s or 0))
+    _check(lib().dfvm_set_allocator(fa, ff, None))
+    _ALLOCATOR = (fa, ff)
+
+
+def use_torch_allocator():
+    """Route every library device allocation through PyTorch's caching
+    allocator (north star: "PyTorch only for device memory")."""
+    import torch
+
+    def alloc(n, stream):
+        return torch.cuda.caching_allocator_alloc(int(n), stream=int(stream))
+
+    def free(p, n, stream):
+        torch.cuda.caching_allocator_delete(int(p))
+
+    set_allocator(alloc, free)
 
 
 class Comm:
@@ -508,7 +552,7 @@ class Solver:
 
     def __init__(self, mesh, bcs, nu, dt, rho=1.0, n_corr=2, n_nonorth=0, convection="upwind", p_ref_cell=0,
                  p_ref_value=0.0, p_tol=1e-14, p_rel_tol=0.0, p_rel_tol_final=0.0, p_maxit=50000, U_tol=1e-14,
-                 U_rel_tol=0.0, U_maxit=50000, p_precond="jacobi", theta=1.0, ddt_corr=False):
+                 U_rel_tol=0.0, U_maxit=50000, p_precond="jacobi", theta=1.0, ddt_corr=False, cont_tol=0.0):
         self.mesh, self.bcs = mesh, bcs
         # time scheme (Table 1): theta 1 backward Euler, 0.5 Crank-Nicolson, 0 forward Euler
         schemes = {1.0: 0, 0.5: 1, 0.0: 2}
@@ -517,7 +561,8 @@ class Solver:
         o = PisoOpts(nu, dt, rho, n_corr, n_nonorth, {"upwind": 0, "central": 1, "sou": 2, "quick": 3}[convection],
                      p_ref_cell,
                      p_ref_value, p_tol, p_rel_tol, p_rel_tol_final, p_maxit, U_tol, U_rel_tol, U_maxit,
-                     {"jacobi": 0, "amg": 1, "amg32": 2}[p_precond], schemes[float(theta)], 1 if ddt_corr else 0)
+                     {"jacobi": 0, "amg": 1, "amg32": 2}[p_precond], schemes[float(theta)], 1 if ddt_corr else 0,
+                     cont_tol)
         h = C.c_void_p()
         _check(lib().dfvm_solver_create(mesh.h, bcs.h, C.byref(o), C.byref(h)))
         self.h = h.value

@@ -179,27 +179,22 @@ struct AmgH {
   P* ainv = nullptr;                // dense inverse of the coarsest matrix (column-major n x n), or NULL
   std::vector<void*> allocs;
   int64_t bytes = 0;
-  ~AmgH() { for (void* p : allocs) cudaFree(p); }
+  ~AmgH() { for (void* p : allocs) dev_free(p, nullptr); }
+  // legacy-stream allocations / uploads; amg_create synchronises once after
+  // the build, before the caller's stream uses any of them
   template <class U>
   dfvm_status up(U** d, const std::vector<U>& h) {
-    void* q = nullptr;
-    const size_t sz = std::max<size_t>(h.size(), 1) * sizeof(U);
-    DFVM_CUDA(cudaMalloc(&q, sz));
-    if (!h.empty()) DFVM_CUDA(cudaMemcpy(q, h.data(), h.size() * sizeof(U), cudaMemcpyHostToDevice));
-    allocs.push_back(q);
-    bytes += (int64_t)sz;
-    *d = (U*)q;
+    if (dfvm_status st = dev_alloc_n(d, h.size(), nullptr, false)) return st;
+    if (!h.empty()) DFVM_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(U), cudaMemcpyHostToDevice));
+    allocs.push_back((void*)*d);
+    bytes += (int64_t)(std::max<size_t>(h.size(), 1) * sizeof(U));
     return DFVM_OK;
   }
   template <class U>
   dfvm_status zalloc(U** d, size_t n) {
-    void* q = nullptr;
-    const size_t sz = std::max<size_t>(n, 1) * sizeof(U);
-    DFVM_CUDA(cudaMalloc(&q, sz));
-    DFVM_CUDA(cudaMemset(q, 0, sz));
-    allocs.push_back(q);
-    bytes += (int64_t)sz;
-    *d = (U*)q;
+    if (dfvm_status st = dev_alloc_n(d, n, nullptr, true)) return st;
+    allocs.push_back((void*)*d);
+    bytes += (int64_t)(std::max<size_t>(n, 1) * sizeof(U));
     return DFVM_OK;
   }
 };
@@ -376,6 +371,7 @@ dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** ou
     st = build<T, T>(m, M, A->same);
   }
   if (st) { delete A; return st; }
+  DFVM_CUDA(cudaStreamSynchronize(nullptr));   // pageable uploads + zero-fills done before the caller's stream runs
   *out = A;
   return DFVM_OK;
 }
@@ -808,10 +804,29 @@ template <class P>
 static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl) {
   AmgLevelDev<P>& F = A->L[l];
   if (l == A->nlev - 1) {
-    if (A->ainv) k_amg_dense<P, P, P><<<1, 1024, 0, s>>>(F.n, A->ainv, b, x, done);
-    else k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, x,
-                                                  A->prm.sweeps, done);
-    ++*nl;
+    if (A->ainv) {
+      k_amg_dense<P, P, P><<<1, 1024, 0, s>>>(F.n, A->ainv, b, x, done);
+      ++*nl;
+    } else if (F.n <= kCoarseMax) {
+      k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, x,
+                                               A->prm.sweeps, done);
+      ++*nl;
+    } else {
+      // coarsening stopped above the one-block capacity (stall, or the level
+      // cap): the same l1-Jacobi polynomial from zero, multi-block, ping-pong
+      // between x and t (an even sweep count ends in x)
+      const int g = grid_for(F.n);
+      k_amg_pre<P, P, P><<<g, kThreads, 0, s>>>(F.n, b, F.il1, x, done);
+      P* cur = x;
+      P* nxt = F.t;
+      const int sw = A->prm.sweeps + (A->prm.sweeps % 2 == 0 ? 1 : 0);   // odd: sw - 1 (even) smoothing steps
+      for (int it = 1; it < sw; ++it) {
+        k_amg_smooth<P, P, P><<<g, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, cur, b, nxt,
+                                                     done);
+        std::swap(cur, nxt);
+      }
+      *nl += sw;
+    }
     return;
   }
   AmgLevelDev<P>& C = A->L[l + 1];
@@ -854,8 +869,15 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   const bool f64 = std::is_same<P, double>::value;
   dfvm_status e;
   if (A->nlev == 1) {
-    if (A->m->part.P > 1) {   // single level with ghost columns: one l1-Jacobi step
+    if (A->m->part.P > 1 || F.n > kCoarseMax) {
+      // single level with ghost columns (or too large for the one-block
+      // solve): one l1-Jacobi step.  With several ranks the two level-0 halo
+      // exchanges of the multi-level cycle are still made, so every rank
+      // issues the same communication sequence whatever its level count
+      // (a rank whose block did not coarsen must not desynchronise the
+      // send / recv pairing of its peers).
       k_amg_pre<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.il1, z, done);
+      if ((e = halo_exchange_p(A->m, F.x, 1, f64, s)) || (e = halo_exchange_p(A->m, F.t, 1, f64, s))) return e;
     } else {
       k_amg_coarse<P, T, T><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, r, z,
                                                A->prm.sweeps, done);

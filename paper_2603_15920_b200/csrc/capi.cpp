@@ -43,8 +43,7 @@ static dfvm_status dalloc(dfvm_mesh* m, T** p, size_t count) {
   *p = nullptr;
   if (count == 0) count = 1;
   void* q = nullptr;
-  cudaError_t e = cudaMalloc(&q, count * sizeof(T));
-  if (e != cudaSuccess) return cuda_error(e, "cudaMalloc(mesh)");
+  if (dfvm_status st = dev_alloc(&q, count * sizeof(T), nullptr, false)) return st;   // legacy stream, before the uploads
   m->allocations.push_back(q);
   m->device_bytes += (int64_t)(count * sizeof(T));
   *p = (T*)q;
@@ -163,7 +162,6 @@ static dfvm_status upload_mesh(dfvm_mesh* m, DevMesh<T>& D) {
 }
 
 dfvm_status bcs_device(dfvm_bcs* b, int slot, cudaStream_t s) {
-  (void)s;
   dfvm_mesh* m = b->m;
   const HostMesh& H = m->H;
   const Part& P = m->part;
@@ -213,12 +211,17 @@ dfvm_status bcs_device(dfvm_bcs* b, int slot, cudaStream_t s) {
     if (bytesT == 8) std::memcpy(&b->h_valT[slot][8 * i], &b->h_val[slot][i], 8);
     else { float v = (float)b->h_val[slot][i]; std::memcpy(&b->h_valT[slot][4 * i], &v, 4); }
   }
+  // stream-ordered on the caller's stream: the kernels that read the values
+  // follow on the same stream (the host vectors are members: they outlive
+  // the copies)
+  dfvm_status st;
   if (!b->d_kind[slot]) {
-    DFVM_CUDA(cudaMalloc(&b->d_kind[slot], b->h_kind[slot].size()));
-    DFVM_CUDA(cudaMalloc(&b->d_val[slot], nval * bytesT));
+    if ((st = dev_alloc_n(&b->d_kind[slot], b->h_kind[slot].size(), s, false)) ||
+        (st = dev_alloc(&b->d_val[slot], nval * bytesT, s, false)))
+      return st;
   }
-  DFVM_CUDA(cudaMemcpy(b->d_kind[slot], b->h_kind[slot].data(), b->h_kind[slot].size(), cudaMemcpyHostToDevice));
-  DFVM_CUDA(cudaMemcpy(b->d_val[slot], b->h_valT[slot].data(), nval * bytesT, cudaMemcpyHostToDevice));
+  DFVM_CUDA(cudaMemcpyAsync(b->d_kind[slot], b->h_kind[slot].data(), b->h_kind[slot].size(), cudaMemcpyHostToDevice, s));
+  DFVM_CUDA(cudaMemcpyAsync(b->d_val[slot], b->h_valT[slot].data(), nval * bytesT, cudaMemcpyHostToDevice, s));
   // time-varying patches (A-41): steady base values + per-face wave index
   b->wave_patches[slot].clear();
   for (size_t p = 0; p < H.pkind.size(); ++p)
@@ -243,11 +246,13 @@ dfvm_status bcs_device(dfvm_bcs* b, int slot, cudaStream_t s) {
         if (b->wave_patches[slot][j] == p) wid[i] = (int8_t)j;
     }
     if (!b->d_base[slot]) {
-      DFVM_CUDA(cudaMalloc(&b->d_base[slot], nval * bytesT));
-      DFVM_CUDA(cudaMalloc(&b->d_wid[slot], wid.size()));
+      if ((st = dev_alloc(&b->d_base[slot], nval * bytesT, s, false)) ||
+          (st = dev_alloc_n(&b->d_wid[slot], wid.size(), s, false)))
+        return st;
     }
-    DFVM_CUDA(cudaMemcpy(b->d_base[slot], b->h_valT[slot].data(), nval * bytesT, cudaMemcpyHostToDevice));
-    DFVM_CUDA(cudaMemcpy(b->d_wid[slot], wid.data(), wid.size(), cudaMemcpyHostToDevice));
+    DFVM_CUDA(cudaMemcpyAsync(b->d_base[slot], b->h_valT[slot].data(), nval * bytesT, cudaMemcpyHostToDevice, s));
+    DFVM_CUDA(cudaMemcpyAsync(b->d_wid[slot], wid.data(), wid.size(), cudaMemcpyHostToDevice, s));
+    DFVM_CUDA(cudaStreamSynchronize(s));   // `wid` is a local vector
   }
   b->dirty[slot] = false;
   if (!b->wave_patches[slot].empty()) count_launch();
@@ -335,7 +340,7 @@ dfvm_status dfvm_mesh_create(const double* points, int64_t n_points, const int64
   if (!host_only) {
     st = o.precision == DFVM_F64 ? upload_mesh<double>(m.get(), m->d64) : upload_mesh<float>(m.get(), m->d32);
     if (st) {
-      for (void* p : m->allocations) cudaFree(p);
+      for (void* p : m->allocations) dev_free(p, nullptr);
       return st;
     }
     DFVM_CUDA(cudaDeviceSynchronize());
@@ -423,11 +428,12 @@ dfvm_status dfvm_mesh_destroy(dfvm_mesh* m) {
   if (!m) return DFVM_OK;
   if (m->host_only) { delete m; return DFVM_OK; }
   cudaSetDevice(m->device);
-  for (void* p : m->allocations) cudaFree(p);
-  if (m->d_send) cudaFree(m->d_send);
-  if (m->d_recv) cudaFree(m->d_recv);
-  if (m->d_send_idx) cudaFree(m->d_send_idx);
-  if (m->d_stage) cudaFree(m->d_stage);
+  cudaDeviceSynchronize();
+  for (void* p : m->allocations) dev_free(p, nullptr);
+  dev_free(m->d_send, nullptr);
+  dev_free(m->d_recv, nullptr);
+  dev_free(m->d_send_idx, nullptr);
+  dev_free(m->d_stage, nullptr);
   delete m;
   return DFVM_OK;
 }
@@ -448,8 +454,8 @@ dfvm_status dfvm_field_alloc(dfvm_mesh* m, int32_t loc, int32_t n_comp, dfvm_fie
   if (dfvm_status st = dfvm_field_bytes(m, loc, n_comp, &bytes)) return st;
   CHECK_ARG(out, "NULL out");
   void* p = nullptr;
-  DFVM_CUDA(cudaMalloc(&p, bytes));
-  DFVM_CUDA(cudaMemset(p, 0, bytes));
+  if (dfvm_status st = dev_alloc(&p, bytes, nullptr, true)) return st;
+  DFVM_CUDA(cudaStreamSynchronize(nullptr));   // zero-fill done before any use on a non-blocking stream
   dfvm_field* f = new dfvm_field();
   f->m = m; f->ptr = p; f->loc = loc; f->n_comp = n_comp; f->owned = true;
   *out = f;
@@ -474,7 +480,7 @@ dfvm_status dfvm_field_data(const dfvm_field* f, void** dev_ptr) {
 
 dfvm_status dfvm_field_destroy(dfvm_field* f) {
   if (!f) return DFVM_OK;
-  if (f->owned && f->ptr) cudaFree(f->ptr);
+  if (f->owned && f->ptr) { cudaDeviceSynchronize(); dev_free(f->ptr, nullptr); }
   delete f;
   return DFVM_OK;
 }
@@ -488,8 +494,9 @@ static int64_t global_count(const dfvm_field* f) {
 // spent ~1.3 s/step in import/export with it)
 static dfvm_status stage(dfvm_mesh* m, size_t bytes) {
   if (m->stage_bytes >= bytes) return DFVM_OK;
-  if (m->d_stage) { DFVM_CUDA(cudaDeviceSynchronize()); DFVM_CUDA(cudaFree(m->d_stage)); m->d_stage = nullptr; }
-  DFVM_CUDA(cudaMalloc(&m->d_stage, bytes));
+  if (m->d_stage) { DFVM_CUDA(cudaDeviceSynchronize()); dev_free(m->d_stage, nullptr); m->d_stage = nullptr; }
+  if (dfvm_status st = dev_alloc(&m->d_stage, bytes, nullptr, false)) return st;
+  DFVM_CUDA(cudaStreamSynchronize(nullptr));
   m->stage_bytes = bytes;
   return DFVM_OK;
 }
@@ -612,10 +619,10 @@ dfvm_status dfvm_bcs_set_time(dfvm_bcs* b, double t, dfvm_stream stream) {
 dfvm_status dfvm_bcs_destroy(dfvm_bcs* b) {
   if (!b) return DFVM_OK;
   for (int i = 0; i < 3; ++i) {
-    if (b->d_kind[i]) cudaFree(b->d_kind[i]);
-    if (b->d_val[i]) cudaFree(b->d_val[i]);
-    if (b->d_base[i]) cudaFree(b->d_base[i]);
-    if (b->d_wid[i]) cudaFree(b->d_wid[i]);
+    dev_free(b->d_kind[i], nullptr);
+    dev_free(b->d_val[i], nullptr);
+    dev_free(b->d_base[i], nullptr);
+    dev_free(b->d_wid[i], nullptr);
   }
   delete b;
   return DFVM_OK;
@@ -708,7 +715,7 @@ dfvm_status dfvm_fvm_laplacian_apply(dfvm_mesh* m, const dfvm_field* gamma, cons
   void* G = grad ? grad->ptr : nullptr;
   void* tmp = nullptr;
   if (!G) {
-    DFVM_CUDA(cudaMallocAsync(&tmp, (size_t)(m->part.n_own + m->part.n_ghost) * 3 * elem_bytes(m), s));
+    if ((st = dev_alloc(&tmp, (size_t)(m->part.n_own + m->part.n_ghost) * 3 * elem_bytes(m), s, false))) return st;
     G = tmp;
     DISPATCH(m, launch_grad<double>(m->d64, (const double*)x->ptr, 1, b->d_kind[slot], (const double*)b->d_val[slot], (double*)G, s),
                 launch_grad<float>(m->d32, (const float*)x->ptr, 1, b->d_kind[slot], (const float*)b->d_val[slot], (float*)G, s));
@@ -716,7 +723,7 @@ dfvm_status dfvm_fvm_laplacian_apply(dfvm_mesh* m, const dfvm_field* gamma, cons
   if ((st = halo_exchange(m, G, 3, s))) return st;
   DISPATCH(m, launch_laplacian<double>(m->d64, gamma ? (const double*)gamma->ptr : nullptr, (const double*)x->ptr, (const double*)G, b->d_kind[slot], (const double*)b->d_val[slot], (double*)y->ptr, s),
               launch_laplacian<float>(m->d32, gamma ? (const float*)gamma->ptr : nullptr, (const float*)x->ptr, (const float*)G, b->d_kind[slot], (const float*)b->d_val[slot], (float*)y->ptr, s));
-  if (tmp) DFVM_CUDA(cudaFreeAsync(tmp, s));
+  if (tmp) dev_free(tmp, s);
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
 }

@@ -112,10 +112,12 @@ static dfvm_status ensure_halo_buffers(dfvm_mesh* m) {
   if (m->d_send_idx || P.send_gid.empty()) return DFVM_OK;
   std::vector<int32_t> idx(P.send_gid.size());
   for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int32_t)(P.send_gid[i] - P.lo);
-  DFVM_CUDA(cudaMalloc(&m->d_send_idx, idx.size() * 4));
+  dfvm_status st;
+  if ((st = dev_alloc_n(&m->d_send_idx, idx.size(), nullptr, false))) return st;
   DFVM_CUDA(cudaMemcpy(m->d_send_idx, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice));
   m->halo_bytes = idx.size() * 9 * 8;   // up to 9 fp64 components
-  DFVM_CUDA(cudaMalloc(&m->d_send, m->halo_bytes));
+  if ((st = dev_alloc(&m->d_send, m->halo_bytes, nullptr, false))) return st;
+  DFVM_CUDA(cudaStreamSynchronize(nullptr));   // once: ordered before the caller's (non-blocking) stream uses them
   return DFVM_OK;
 }
 

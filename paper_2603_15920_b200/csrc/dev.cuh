@@ -2,6 +2,7 @@
 // warp-per-SELL-slice iteration, deterministic two-level reductions.
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <unordered_map>
 #include <cuda_runtime.h>
 
@@ -27,7 +28,10 @@ inline int grid_for(int64_t n) {
 // per kernel; a fixed function of (kernel, device), so the reduction
 // structure (and hence the bits) stays deterministic run to run.
 inline int occ_cap(const void* fn) {
+  // guarded: the in-process multi-rank path calls this from several host threads
+  static std::mutex mu;
   static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(fn);
   if (it != cache.end()) return it->second;
   int dev = 0, nsm = 148, b = 0;

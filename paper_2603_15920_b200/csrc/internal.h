@@ -39,6 +39,19 @@ dfvm_status cuda_error(cudaError_t e, const char* where);
 
 void count_launch(int n = 1);
 
+// device workspace (alloc.cpp): through the caller's allocator if one is set
+// (dfvm_set_allocator), else cudaMallocAsync; stream-ordered zero-fill
+dfvm_status dev_alloc(void** p, size_t bytes, cudaStream_t s, bool zero);
+void dev_free(void* p, cudaStream_t s);
+int64_t dev_live_bytes();
+template <class U>
+inline dfvm_status dev_alloc_n(U** p, size_t n, cudaStream_t s, bool zero) {
+  void* q = nullptr;
+  dfvm_status st = dev_alloc(&q, (n ? n : 1) * sizeof(U), s, zero);
+  *p = (U*)q;
+  return st;
+}
+
 // ------------------------------------------------------------ host mesh
 struct HostMesh {
   int64_t N = 0, F = 0, NF = 0;

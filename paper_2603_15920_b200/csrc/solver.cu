@@ -1107,20 +1107,23 @@ struct SolverT : SolverBase {
   T* Uold = nullptr;     // start-of-step U and phi (ddtCorr, A-42; allocated on first use)
   T* phiold = nullptr;
   ~SolverT() override {
+    cudaDeviceSynchronize();
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     if (amg) amg_destroy<T>(amg);
-    for (void* p : allocs) cudaFree(p);
+    for (void* p : allocs) dev_free(p, nullptr);
+    dev_free(d_wk, nullptr);
+    dev_free(d_wk_ptr, nullptr);
+    dev_free(d_wk_faces, nullptr);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (h_cont) cudaFreeHost(h_cont);
     if (h_wk) cudaFreeHost(h_wk);
   }
+  // zero-filled workspace on stream s (the legacy stream at create time,
+  // the caller's stream for lazy allocations inside a step)
   template <class U>
-  dfvm_status al(U** p, size_t n) {
-    void* q = nullptr;
-    DFVM_CUDA(cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(U)));
-    DFVM_CUDA(cudaMemset(q, 0, std::max<size_t>(n, 1) * sizeof(U)));
-    allocs.push_back(q);
-    *p = (U*)q;
+  dfvm_status al(U** p, size_t n, cudaStream_t s = nullptr) {
+    if (dfvm_status st = dev_alloc_n(p, n, s, true)) return st;
+    allocs.push_back((void*)*p);
     return DFVM_OK;
   }
   // face-to-cell displacements for the deferred-correction schemes (O-1 fp64
@@ -1143,6 +1146,7 @@ struct SolverT : SolverBase {
     if ((st = al(&fdO, o.size())) || (st = al(&fdN, n.size()))) return st;
     DFVM_CUDA(cudaMemcpy(fdO, o.data(), o.size() * sizeof(V4<T>), cudaMemcpyHostToDevice));
     DFVM_CUDA(cudaMemcpy(fdN, n.data(), n.size() * sizeof(V4<T>), cudaMemcpyHostToDevice));
+    DFVM_CUDA(cudaStreamSynchronize(nullptr));
     return DFVM_OK;
   }
   dfvm_status init(dfvm_mesh* mm, DevMesh<T>* MM) {
@@ -1161,6 +1165,7 @@ struct SolverT : SolverBase {
       return st;
     DFVM_CUDA(cudaMallocHost(&h_ctl, 4 * sizeof(KCtl)));
     DFVM_CUDA(cudaMallocHost(&h_cont, 4 * sizeof(double)));
+    DFVM_CUDA(cudaStreamSynchronize(nullptr));   // zero-fills complete before any use on the caller's stream
     return DFVM_OK;
   }
 };
@@ -1214,7 +1219,10 @@ static dfvm_status sync_wk(dfvm_solver* S, SolverT<T>& X, cudaStream_t st) {
   const Part& P = S->m->part;
   const HostMesh& H = S->m->H;
   const int n = (int)S->wk.size();
-  if (X.d_wk) { cudaFree(X.d_wk); cudaFree(X.d_wk_ptr); cudaFree(X.d_wk_faces); X.d_wk = nullptr; }
+  if (X.d_wk) {
+    dev_free(X.d_wk, st); dev_free(X.d_wk_ptr, st); dev_free(X.d_wk_faces, st);
+    X.d_wk = nullptr; X.d_wk_ptr = nullptr; X.d_wk_faces = nullptr;
+  }
   if (X.h_wk) { cudaFreeHost(X.h_wk); X.h_wk = nullptr; }
   if (n) {
     std::vector<int> ptr(n + 1, 0), faces;
@@ -1223,10 +1231,11 @@ static dfvm_status sync_wk(dfvm_solver* S, SolverT<T>& X, cudaStream_t st) {
         if (H.bpatch[P.lb_gid[b] - H.F] == S->wk[o].patch) faces.push_back((int)b);
       ptr[o + 1] = (int)faces.size();
     }
-    DFVM_CUDA(cudaMalloc(&X.d_wk, n * sizeof(WKDev)));
+    dfvm_status e;
+    if ((e = dev_alloc_n(&X.d_wk, n, st, false)) || (e = dev_alloc_n(&X.d_wk_ptr, n + 1, st, false)) ||
+        (e = dev_alloc_n(&X.d_wk_faces, faces.size(), st, false)))
+      return e;
     DFVM_CUDA(cudaMallocHost(&X.h_wk, n * sizeof(WKDev)));
-    DFVM_CUDA(cudaMalloc(&X.d_wk_ptr, (n + 1) * sizeof(int)));
-    DFVM_CUDA(cudaMalloc(&X.d_wk_faces, std::max<size_t>(faces.size(), 1) * sizeof(int)));
     for (int o = 0; o < n; ++o) {
       const auto& w = S->wk[o];
       X.h_wk[o] = WKDev{w.Rp, w.C, w.Rd, w.pc, w.pc, 0.0, 0.0, w.scheme, w.patch};
@@ -1571,7 +1580,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   // 1. momentum assembly from (U^n, phi^n, grad U^n)
   if ((s2 = assemble(S, X, U, phi, st))) return s2;
   if (o.ddt_corr) {   // start-of-step U (with ghosts, exchanged by assemble) and phi for ddtCorr (A-42)
-    if (!X.Uold && ((s2 = X.al(&X.Uold, 3 * (size_t)M.n_cells)) || (s2 = X.al(&X.phiold, (size_t)M.F + 1)))) return s2;
+    if (!X.Uold && ((s2 = X.al(&X.Uold, 3 * (size_t)M.n_cells, st)) || (s2 = X.al(&X.phiold, (size_t)M.F + 1, st)))) return s2;
     DFVM_CUDA(cudaMemcpyAsync(X.Uold, U, 3 * (size_t)M.n_cells * sizeof(T), cudaMemcpyDeviceToDevice, st));
     DFVM_CUDA(cudaMemcpyAsync(X.phiold, phi, (size_t)M.F * sizeof(T), cudaMemcpyDeviceToDevice, st));
   }
@@ -1665,6 +1674,11 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   count_launch(S->n_launch);
   S->t += o.dt;
   if (R->nonfinite) { set_error(DFVM_E_NONFINITE, "non-finite U or p after the PISO step"); return DFVM_E_NONFINITE; }
+  if (o.cont_tol > 0 && !(R->cont_err_max <= o.cont_tol)) {
+    set_error(DFVM_E_CONTINUITY, "continuity violated after the PISO step: max_c |sum_f s phi_f| = " +
+              std::to_string(R->cont_err_max) + " > cont_tol " + std::to_string(o.cont_tol));
+    return DFVM_E_CONTINUITY;
+  }
   return res;
 }
 
@@ -1717,7 +1731,8 @@ dfvm_status dfvm_solver_create(dfvm_mesh* m, dfvm_bcs* b, const dfvm_piso_opts* 
   if (!(opts->dt > 0) || !(opts->nu >= 0) || opts->n_corr < 1 || opts->n_corr > 8 || opts->n_nonorth < 0 ||
       (opts->n_corr * (opts->n_nonorth + 1)) > 16 || opts->p_maxit < 1 || opts->U_maxit < 1 || !(opts->rho > 0) ||
       opts->p_precond < 0 || opts->p_precond > 2 || opts->convection < 0 || opts->convection > 3 ||
-      opts->time_scheme < DFVM_TIME_BACKWARD_EULER || opts->time_scheme > DFVM_TIME_FORWARD_EULER || opts->ddt_corr < 0 || opts->ddt_corr > 1) {
+      opts->time_scheme < DFVM_TIME_BACKWARD_EULER || opts->time_scheme > DFVM_TIME_FORWARD_EULER || opts->ddt_corr < 0 || opts->ddt_corr > 1 ||
+      !(opts->cont_tol >= 0)) {
     set_error(DFVM_E_INVALID_ARG, "invalid PISO options");
     return DFVM_E_INVALID_ARG;
   }

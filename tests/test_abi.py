@@ -86,3 +86,28 @@ def test_product_path_never_imports_oracle():
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", src, flags=re.M), f
                 assert "liboracle" not in src, f
                 assert "oracle/" not in src.replace("oracle/`", ""), f
+
+
+def test_set_allocator_contract():
+    """§8(b) b3: dfvm_set_allocator takes both callbacks or neither, and may
+    be changed while no library allocation is live (true here: no GPU, so no
+    mesh / field was ever created)."""
+    assert dfvm.live_device_bytes() == 0
+    calls = []
+    dfvm.set_allocator(lambda n, s: calls.append(n) or 0, lambda p, n, s: None)
+    dfvm.set_allocator()
+    L = dfvm.lib()
+    st = L.dfvm_set_allocator(dfvm.ALLOC_FN(lambda n, s, c: None), dfvm.FREE_FN(0), None)
+    assert st == 1   # DFVM_E_INVALID_ARG: one callback without the other
+    assert calls == []   # installing never allocates
+
+
+def test_piso_opts_layout_matches_header():
+    """the binding's PisoOpts mirrors dfvm_piso_opts field for field (cont_tol last)"""
+    src = open(os.path.join(ROOT, "include", "dfvm.h")).read()
+    body = src[src.index("/* --------------------------------------------------------------- solver */"):]
+    body = body[:body.index("} dfvm_piso_opts;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = re.findall(r"(?:double|int32_t|int64_t)\s+([^;]+);", body)
+    flat = [n.strip() for grp in names for n in grp.split(",")]
+    assert flat == [f for f, _ in dfvm.PisoOpts._fields_]
