@@ -412,9 +412,34 @@ dfvm_status dfvm_solver_destroy(dfvm_solver* s);
  * SpMV.  set_timing resets the accumulators. */
 dfvm_status dfvm_solver_set_timing(dfvm_solver* s, int32_t on);
 dfvm_status dfvm_solver_get_timing(const dfvm_solver* s, double ms[4], int64_t count[4]);
-/* AMG hierarchy (built at the first AMG pressure solve): number of levels and
- * rows per level (sizes[] may be NULL; at most 16 levels). */
-dfvm_status dfvm_solver_amg_levels(const dfvm_solver* s, int32_t* n_levels, int64_t* sizes);
+/* AMG hierarchy (built at the first AMG pressure solve): number of levels,
+ * rows per level and real off-diagonal matrix entries per level (sizes[] and
+ * nnz[] may be NULL; at most 16 levels). */
+dfvm_status dfvm_solver_amg_levels(const dfvm_solver* s, int32_t* n_levels, int64_t* sizes, int64_t* nnz);
+
+/* Per-kernel live profile (north star "achieved HBM GB/s
+ * ... for every kernel").  dfvm_solver_profile(s, 1) clears the table and
+ * brackets every kernel launch of the following solver calls (piso_step,
+ * pressure_solve, transport_step) with CUDA events on the launching stream;
+ * AMG-PCG chunks are then captured and replayed as CUDA graphs one chunk at a
+ * time, so the events time the GPU, not the host enqueue.  Rows aggregate
+ * by (kernel, AMG level): launches, summed event time, summed algorithmic
+ * bytes (the per-launch formulas of DESIGN.md §6).  Launches of Krylov
+ * iterations the device skipped (solve already converged, the kernel exits
+ * on the done flag) are booked to the row "(no-op launches after
+ * convergence)" with zero bytes.  Profiling adds event nodes and disables the
+ * cached chunk graphs: time the step itself with profiling off.
+ * dfvm_solver_profile_get copies min(cap, n) rows and sets *n to the row
+ * count. */
+typedef struct {
+  char name[48];        /* __global__ kernel name, "k_grad (U)" / "k_grad (p)" for the Gauss gradients */
+  int32_t level;        /* AMG level the kernel runs on, -1 outside the AMG cycle */
+  int64_t launches;
+  double ms;            /* summed event-pair time */
+  double alg_bytes;     /* summed algorithmic bytes */
+} dfvm_kernel_stat;
+dfvm_status dfvm_solver_profile(dfvm_solver* s, int32_t on);
+dfvm_status dfvm_solver_profile_get(const dfvm_solver* s, dfvm_kernel_stat* out, int32_t cap, int32_t* n);
 
 /* Kernel launch counter (all kernels this process launched through the
  * library), for bench.py's gpu_launches claim. */

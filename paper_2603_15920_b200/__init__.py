@@ -43,6 +43,7 @@ SYMBOLS = [
     "dfvm_transport_step", "dfvm_momentum_apply_transpose", "dfvm_pressure_solve_adjoint", "dfvm_pressure_vjp",
     "dfvm_bcs_set_waveform", "dfvm_bcs_set_time", "dfvm_polymesh_read", "dfvm_polymesh_sizes",
     "dfvm_polymesh_arrays", "dfvm_polymesh_destroy", "dfvm_set_allocator", "dfvm_live_device_bytes",
+    "dfvm_solver_profile", "dfvm_solver_profile_get",
 ]
 
 
@@ -83,6 +84,11 @@ class PisoOpts(C.Structure):
                 ("p_rel_tol_final", C.c_double), ("p_maxit", C.c_int32), ("U_tol", C.c_double),
                 ("U_rel_tol", C.c_double), ("U_maxit", C.c_int32), ("p_precond", C.c_int32),
                 ("time_scheme", C.c_int32), ("ddt_corr", C.c_int32), ("cont_tol", C.c_double)]
+
+
+class KernelStat(C.Structure):
+    _fields_ = [("name", C.c_char * 48), ("level", C.c_int32), ("launches", C.c_int64), ("ms", C.c_double),
+                ("alg_bytes", C.c_double)]
 
 
 class SolveReport(C.Structure):
@@ -157,7 +163,9 @@ def lib():
         L.dfvm_windkessel_update.argtypes = [f64, f64, f64, f64, f64, f64, i32, C.POINTER(f64), C.POINTER(f64)]
         L.dfvm_solver_set_timing.argtypes = [vp, i32]
         L.dfvm_solver_get_timing.argtypes = [vp, vp, vp]
-        L.dfvm_solver_amg_levels.argtypes = [vp, vp, vp]
+        L.dfvm_solver_amg_levels.argtypes = [vp, vp, vp, vp]
+        L.dfvm_solver_profile.argtypes = [vp, i32]
+        L.dfvm_solver_profile_get.argtypes = [vp, vp, i32, C.POINTER(i32)]
         L.dfvm_transport_step.argtypes = [vp, vp, vp, f64, C.POINTER(SolveReport), vp]
         L.dfvm_comm_unique_id.argtypes = [vp]
         L.dfvm_comm_create.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
@@ -645,8 +653,24 @@ class Solver:
         return dict(spmv_ms=float(ms[0]), spmv_n=int(n[0]), cg_iter_ms=float(ms[1]), cg_iter_n=int(n[1]),
                     amg_pre_ms=float(ms[2]), amg_pre_n=int(n[2]), amg_post_ms=float(ms[3]), amg_post_n=int(n[3]))
 
-    def amg_levels(self):
+    def amg_levels(self, nnz=False):
         n = C.c_int32()
         sz = np.zeros(32, np.int64)
-        _check(lib().dfvm_solver_amg_levels(self.h, C.byref(n), _ptr(sz)))
+        nz = np.zeros(32, np.int64)
+        _check(lib().dfvm_solver_amg_levels(self.h, C.byref(n), _ptr(sz), _ptr(nz)))
+        if nnz:
+            return sz[:n.value].tolist(), nz[:n.value].tolist()
         return sz[:n.value].tolist()
+
+    def profile(self, on=True):
+        """dfvm_solver_profile: per-kernel event timing of the following calls (clears the table)."""
+        _check(lib().dfvm_solver_profile(self.h, 1 if on else 0))
+
+    def profile_table(self):
+        """rows {name, level, launches, ms, alg_bytes} of dfvm_solver_profile_get"""
+        n = C.c_int32()
+        _check(lib().dfvm_solver_profile_get(self.h, None, 0, C.byref(n)))
+        buf = (KernelStat * max(n.value, 1))()
+        _check(lib().dfvm_solver_profile_get(self.h, C.cast(buf, C.c_void_p), n.value, C.byref(n)))
+        return [dict(name=b.name.decode(), level=b.level, launches=b.launches, ms=b.ms, alg_bytes=b.alg_bytes)
+                for b in buf[:n.value]]

@@ -9,19 +9,26 @@
 //  * hierarchy (host, once per mesh, topology only): greedy aggregation of
 //    the owned rows in RCM order (root + its unaggregated neighbours; leftovers
 //    join a neighbouring aggregate; isolated rows become singletons), until
-//    <= 2048 rows.  Coarse levels are rank-local (couplings to ghost rows are
+//    <= 256 rows (DFVM_AMG_COARSE).  Coarse levels are rank-local (couplings to ghost rows are
 //    dropped: the coarse operator is the Galerkin product of the owned block,
 //    still SPD).
 //  * values (device, whenever the pressure matrix changes): Galerkin
 //    A_c = P^T A P with piecewise-constant P, as fixed-order gather sums over
 //    precomputed contribution lists (no atomics); l1-Jacobi diagonals
 //    d1_i = a_ii + sum_j |a_ij|.
-//  * V(1,1) cycle: pre-smooth x = D1^-1 b, residual, restriction (sum over
-//    aggregate members), coarse correction, prolongation x += x_c[agg],
-//    post-smooth x += D1^-1 (b - A x); coarsest level: 24 l1-Jacobi sweeps in
-//    one block (shared memory).  Pre/post smoothers are adjoint and the
-//    coarse solve is a fixed symmetric polynomial, so M^-1 is SPD and CG
-//    stays CG.  The converged pressure is preconditioner independent (A-14).
+//  * cycle (defaults measured on the C5 pipe): l1-Jacobi
+//    pre-smoothing from zero x0 = D1^-1 b, residual, restriction (sum over
+//    the aggregate's members), coarse correction scaled by omega = 1.9,
+//    prolongation x = x0 + omega x_c[agg], l1-Jacobi post-smoothing (the
+//    adjoint of the pre-smoother); a W-cycle (two coarse visits, the second
+//    on the residual of the first) on levels <= 4 and a V-cycle below;
+//    coarsening stops at <= 256 rows (never below 32), and the coarsest level
+//    (<= 512 rows) is solved exactly with its dense inverse (Gauss-Jordan
+//    once per matrix update); a larger coarsest level (coarsening stalled)
+//    gets `sweeps` l1-Jacobi sweeps (one block up to 2048 rows, multi-block
+//    above).  Adjoint smoothers, a symmetric coarse solve and the W-cycle's
+//    2B - BAB keep M^-1 SPD, so CG stays CG.  The converged pressure is
+//    preconditioner independent (A-14).
 //  * precision: the hierarchy's type P is the solver's T ("amg"), or fp32
 //    under an fp64 solver ("amg32": matrix copies, smoother and every level
 //    vector in fp32; the PCG itself — residual, dots, x, p — stays fp64).
@@ -36,6 +43,7 @@
 
 #include "amg.h"
 #include "dev.cuh"
+#include "prof.h"
 
 namespace dfvm {
 
@@ -58,23 +66,22 @@ constexpr int kMaxLevels = 16;
 //                    < 2 keeps M SPD with adjoint smoothers)   default 1.9
 //   DFVM_AMG_SIGMA   1: renumber aggregates by row length within windows of
 //                    256 (less SELL padding); 0: creation order      default 0
-//   DFVM_AMG_GROUP   1: 4/8 lanes per row on long or few coarse rows; 0: one
-//                    thread per row                                  default 0
-//                    (C5 amg32: 378 ms/step with both 0 against 423 ms with
-//                    both 1: sigma costs 0.5 PCG iterations per solve and
-//                    the grouped kernels are slower than one thread per row)
+//                    (C5 amg32, round 1: 378 ms/step without sigma against
+//                    423 ms with sigma and 4/8-lane grouped coarse kernels,
+//                    since removed: sigma costs 0.5 PCG iterations per
+//                    solve and the grouped kernels were slower than one
+//                    thread per row)
 //   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
 //                    exactly with a dense inverse (Gauss-Jordan once per
 //                    matrix update, one block), larger ones with
 //                    DFVM_AMG_SWEEPS l1-Jacobi sweeps (0: always sweeps)  default 512
 struct AmgParams {
-  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, sigma = 0, group = 0;
+  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, sigma = 0;
   bool wcycle = true;
   double omega = 1.9;   // C5 amg32: 362 ms, 11.6 it/solve (1.8: 369 ms, 12.2; 1.7: 380 ms)
   AmgParams() {
     if (const char* e = getenv("DFVM_AMG_DIRECT")) direct = std::max(0, std::min(kDirectMax, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_SIGMA")) sigma = atoi(e);
-    if (const char* e = getenv("DFVM_AMG_GROUP")) group = atoi(e);
     if (const char* e = getenv("DFVM_AMG_OMEGA")) omega = atof(e);
     if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kCoarseMax, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_SWEEPS")) sweeps = std::max(1, atoi(e));
@@ -152,8 +159,8 @@ std::vector<int> aggregate(const HostLevel& L, int& nagg) {
 template <class P>
 struct AmgLevelDev {
   int n = 0, n_slices = 0;
-  int G = 1;                 // lanes per row in the coarse-level kernels (1, 4 or 8)
-  int64_t n_sell = 0;
+  int64_t n_sell = 0;        // SELL slots (incl. padding)
+  int64_t nnz = 0;           // real off-diagonal entries (algorithmic bytes)
   const int *ms_ptr = nullptr, *ms_len = nullptr, *mnb = nullptr;
   const P* coef = nullptr;   // level 0: the solver's pcoef (P == T) or coef_own (fp32 copy)
   const P* diag = nullptr;   // level 0: the solver's pdiag (P == T) or diag_own
@@ -175,6 +182,7 @@ struct AmgH {
   dfvm_mesh* m = nullptr;
   int nlev = 0;
   AmgParams prm;
+  Prof* prof = nullptr;             // per-kernel profile of the caller (may be null)
   AmgLevelDev<P> L[kMaxLevels];
   P* ainv = nullptr;                // dense inverse of the coarsest matrix (column-major n x n), or NULL
   std::vector<void*> allocs;
@@ -216,7 +224,7 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
   sell_to_csr(H[0], M.n_own);
   // device view of level 0 (the mesh's matrix layout; coef / diag bound per update)
   AmgLevelDev<P>& L0 = A->L[0];
-  L0.n = M.n_own; L0.n_slices = M.n_slices; L0.n_sell = M.n_minc;
+  L0.n = M.n_own; L0.n_slices = M.n_slices; L0.n_sell = M.n_minc; L0.nnz = M.nnz;
   L0.ms_ptr = M.ms_ptr; L0.ms_len = M.ms_len; L0.mnb = M.mnb;
   dfvm_status st;
   if ((st = A->zalloc(&L0.il1, M.n_own)) || (st = A->zalloc(&L0.x, M.n_cells)) || (st = A->zalloc(&L0.r, M.n_own)) ||
@@ -330,10 +338,7 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     // upload
     AmgLevelDev<P>& D = A->L[lev + 1];
     D.n = nc; D.n_slices = S; D.n_sell = C.ms_ptr[S];
-    {   // grouped kernels where rows are long or few (latency-bound otherwise)
-      const double avg = (double)ccol.size() / std::max(1, nc);
-      D.G = !A->prm.group ? 1 : (avg >= 12.0 || nc < 50000) ? 8 : (avg >= 6.0 ? 4 : 1);
-    }
+    D.nnz = (int64_t)ccol.size();
     int *p0, *p1, *p2;
     if ((st = A->up(&p0, C.ms_ptr)) || (st = A->up(&p1, C.ms_len)) || (st = A->up(&p2, C.mnb)) ||
         (st = A->up(&D.gal_ptr, gal_ptr)) || (st = A->up(&D.gal_idx, gal_idx)) || (st = A->up(&D.dg_ptr, dg_ptr)) ||
@@ -580,87 +585,6 @@ __global__ void k_amg_prolong_smooth(int n, const int* __restrict__ ms_ptr, cons
     out[i] = prolong_smooth_row(i, ms_ptr, ms_len, mnb, coef, diag, il1, agg, xc, w, x0, b);
 }
 
-// Grouped coarse-level kernels: G consecutive lanes share a row, lane g sums
-// the row's entries j = g, g + G, ..., and a shuffle tree within the group
-// adds the partials (fixed order: deterministic).  A warp takes 32 / G rows
-// per step and every lane joins the shuffles (rows past n add zeros).
-template <int G, class T>
-__device__ __forceinline__ T group_sum(T v) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-#define GROUP_LOOP(n)                                                                              \
-  const int lane = threadIdx.x & 31, sub = lane % G;                                               \
-  const int64_t nwg = ((int64_t)gridDim.x * blockDim.x) >> 5;                                      \
-  for (int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; c * (32 / G) < (n); c += nwg)
-
-template <class T, int G>
-__global__ void k_amg_pre_resid_g(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                                  const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
-                                  const T* __restrict__ il1, const T* __restrict__ b, T* __restrict__ x0,
-                                  T* __restrict__ r, const int* done) {
-  if (*done) return;
-  GROUP_LOOP(n) {
-    const int row = (int)(c * (32 / G) + lane / G);
-    T part = T(0);
-    if (row < n) {
-      const int base = ms_ptr[row >> 5] + (row & 31), len = ms_len[row >> 5];
-      for (int j = sub; j < len; j += G) {
-        const int cc = __ldg(&mnb[base + 32 * j]);
-        part += __ldg(&coef[base + 32 * j]) * (b[cc] * il1[cc]);
-      }
-    }
-    const T sum = group_sum<G>(part);
-    if (row < n && sub == 0) {
-      const T bi = b[row], xi = bi * il1[row];
-      x0[row] = xi;
-      r[row] = bi - (diag[row] * xi + sum);
-    }
-  }
-}
-template <class T, int G>
-__global__ void k_amg_prolong_smooth_g(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                                       const int* __restrict__ mnb, const T* __restrict__ coef,
-                                       const T* __restrict__ diag, const T* __restrict__ il1,
-                                       const int* __restrict__ agg, const T* __restrict__ xc, T w,
-                                       const T* __restrict__ x0, const T* __restrict__ b, T* __restrict__ out,
-                                       const int* done) {
-  if (*done) return;
-  GROUP_LOOP(n) {
-    const int row = (int)(c * (32 / G) + lane / G);
-    T part = T(0);
-    if (row < n) {
-      const int base = ms_ptr[row >> 5] + (row & 31), len = ms_len[row >> 5];
-      for (int j = sub; j < len; j += G) {
-        const int cc = __ldg(&mnb[base + 32 * j]);
-        part += __ldg(&coef[base + 32 * j]) * (x0[cc] + w * xc[agg[cc]]);
-      }
-    }
-    const T sum = group_sum<G>(part);
-    if (row < n && sub == 0) {
-      const T ti = x0[row] + w * xc[agg[row]];
-      out[row] = ti + (b[row] - (diag[row] * ti + sum)) * il1[row];
-    }
-  }
-}
-template <class T, int G>
-__global__ void k_amg_resid_g(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                              const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
-                              const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ r, const int* done) {
-  if (*done) return;
-  GROUP_LOOP(n) {
-    const int row = (int)(c * (32 / G) + lane / G);
-    T part = T(0);
-    if (row < n) {
-      const int base = ms_ptr[row >> 5] + (row & 31), len = ms_len[row >> 5];
-      for (int j = sub; j < len; j += G) part += __ldg(&coef[base + 32 * j]) * x[__ldg(&mnb[base + 32 * j])];
-    }
-    const T sum = group_sum<G>(part);
-    if (row < n && sub == 0) r[row] = b[row] - (diag[row] * x[row] + sum);
-  }
-}
-#undef GROUP_LOOP
 
 // x += e
 template <class T>
@@ -758,30 +682,43 @@ __global__ void __launch_bounds__(1024) k_amg_dense(int n, const P* __restrict__
 }
 
 // ------------------------------------------------------------ host drivers
+// Algorithmic bytes per launch: n rows, Z real off-diagonal
+// entries (column 4 B + coefficient pb), vb bytes of the PCG vectors (T),
+// pb of the hierarchy (P); gathered values counted once; 4 B/row of SELL
+// row metadata on the matrix kernels.
 template <class P, class T>
 static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream_t s, int* nl) {
   AmgLevelDev<P>& L0 = A->L[0];
+  Prof* pr = A->prof;
+  const double pb = sizeof(P), vb = sizeof(T);
   if (std::is_same<P, T>::value) {
     L0.coef = (const P*)pcoef; L0.diag = (const P*)pdiag;
   } else {
-    k_amg_cvt<P, T><<<grid_for(L0.n_sell), kThreads, 0, s>>>(L0.n_sell, pcoef, L0.coef_own);
-    k_amg_cvt<P, T><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, pdiag, L0.diag_own);
+    PLAUNCH(pr, "k_amg_cvt", 0, (vb + pb) * (double)L0.n_sell, s,
+            (k_amg_cvt<P, T><<<grid_for(L0.n_sell), kThreads, 0, s>>>(L0.n_sell, pcoef, L0.coef_own)));
+    PLAUNCH(pr, "k_amg_cvt", 0, (vb + pb) * (double)L0.n, s,
+            (k_amg_cvt<P, T><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, pdiag, L0.diag_own)));
     *nl += 2;
   }
-  k_il1<P><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, L0.ms_ptr, L0.ms_len, L0.coef, L0.diag, L0.il1);
+  PLAUNCH(pr, "k_il1", 0, (4 + pb) * (double)L0.nnz + (4 + 2 * pb) * L0.n, s,
+          (k_il1<P><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, L0.ms_ptr, L0.ms_len, L0.coef, L0.diag, L0.il1)));
   ++*nl;
   for (int l = 1; l < A->nlev; ++l) {
     AmgLevelDev<P>& F = A->L[l - 1];
     AmgLevelDev<P>& C = A->L[l];
-    k_gal_off<P><<<grid_for(C.n_sell), kThreads, 0, s>>>(C.n_sell, C.gal_ptr, C.gal_idx, F.coef, C.coef_own);
-    k_gal_diag<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, C.dg_ptr, C.dg_idx, F.diag, F.coef,
-                                                      C.diag_own);
-    k_il1<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.coef, C.diag, C.il1);
+    PLAUNCH(pr, "k_gal_off", l, (8 + pb) * (double)C.nnz + (4 + pb) * (double)F.nnz, s,
+            (k_gal_off<P><<<grid_for(C.n_sell), kThreads, 0, s>>>(C.n_sell, C.gal_ptr, C.gal_idx, F.coef, C.coef_own)));
+    PLAUNCH(pr, "k_gal_diag", l, (8 + pb) * (double)C.n + (4 + pb) * (double)F.n, s,
+            (k_gal_diag<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, C.dg_ptr, C.dg_idx, F.diag, F.coef,
+                                                               C.diag_own)));
+    PLAUNCH(pr, "k_il1", l, (4 + pb) * (double)C.nnz + (4 + 2 * pb) * C.n, s,
+            (k_il1<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.coef, C.diag, C.il1)));
     *nl += 3;
   }
   if (A->ainv) {
     const AmgLevelDev<P>& C = A->L[A->nlev - 1];
-    k_amg_dense_inv<P><<<1, 1024, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, A->ainv);
+    PLAUNCH(pr, "k_amg_dense_inv", A->nlev - 1, 2 * pb * (double)C.n * C.n, s,
+            (k_amg_dense_inv<P><<<1, 1024, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, A->ainv)));
     ++*nl;
   }
   DFVM_CUDA(cudaGetLastError());
@@ -789,8 +726,44 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
 }
 
 template <class T>
-dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s, int* nl) {
-  return A->same ? update<T, T>(A->same, pcoef, pdiag, s, nl) : update<float, T>(A->lo, pcoef, pdiag, s, nl);
+dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s, int* nl, Prof* prof) {
+  if (A->same) { A->same->prof = prof; return update<T, T>(A->same, pcoef, pdiag, s, nl); }
+  A->lo->prof = prof;
+  return update<float, T>(A->lo, pcoef, pdiag, s, nl);
+}
+
+// Coarsest level l: exact dense solve, or l1-Jacobi sweeps from zero.
+template <class P>
+static void coarsest(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl) {
+  AmgLevelDev<P>& F = A->L[l];
+  Prof* pr = A->prof;
+  const double pb = sizeof(P), n = F.n;
+  if (A->ainv) {
+    PLAUNCH(pr, "k_amg_dense", l, pb * n * n + 2 * pb * n, s,
+            (k_amg_dense<P, P, P><<<1, 1024, 0, s>>>(F.n, A->ainv, b, x, done)));
+    ++*nl;
+  } else if (F.n <= kCoarseMax) {
+    PLAUNCH(pr, "k_amg_coarse", l, (4 + pb) * (double)F.nnz + 4 * pb * n, s,
+            (k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, x,
+                                                     A->prm.sweeps, done)));
+    ++*nl;
+  } else {
+    // coarsening stopped above the one-block capacity (stall, or the level
+    // cap): the same l1-Jacobi polynomial from zero, multi-block, ping-pong
+    // between x and t (an odd sweep count ends in x)
+    const int g = grid_for(F.n);
+    PLAUNCH(pr, "k_amg_pre", l, 3 * pb * n, s, (k_amg_pre<P, P, P><<<g, kThreads, 0, s>>>(F.n, b, F.il1, x, done)));
+    P* cur = x;
+    P* nxt = F.t;
+    const int sw = A->prm.sweeps + (A->prm.sweeps % 2 == 0 ? 1 : 0);
+    for (int it = 1; it < sw; ++it) {
+      PLAUNCH(pr, "k_amg_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
+              (k_amg_smooth<P, P, P><<<g, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, cur,
+                                                            b, nxt, done)));
+      std::swap(cur, nxt);
+    }
+    *nl += sw;
+  }
 }
 
 // Coarse level l >= 1 (no ghost columns): x = M_l^-1 b from a zero guess with
@@ -798,63 +771,35 @@ dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s
 // restriction, coarse correction (twice for the W-cycle: the second visit
 // solves for the residual of the first), prolongation + post-smooth.  Each
 // level's operator is symmetric (adjoint pre/post Jacobi, symmetric coarse
-// polynomial, two successive symmetric corrections 2B - BAB), so the
+// solve, two successive symmetric corrections 2B - BAB), so the
 // preconditioner stays SPD.
 template <class P>
 static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl) {
+  if (l == A->nlev - 1) { coarsest(A, l, b, x, done, s, nl); return; }
   AmgLevelDev<P>& F = A->L[l];
-  if (l == A->nlev - 1) {
-    if (A->ainv) {
-      k_amg_dense<P, P, P><<<1, 1024, 0, s>>>(F.n, A->ainv, b, x, done);
-      ++*nl;
-    } else if (F.n <= kCoarseMax) {
-      k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, x,
-                                               A->prm.sweeps, done);
-      ++*nl;
-    } else {
-      // coarsening stopped above the one-block capacity (stall, or the level
-      // cap): the same l1-Jacobi polynomial from zero, multi-block, ping-pong
-      // between x and t (an even sweep count ends in x)
-      const int g = grid_for(F.n);
-      k_amg_pre<P, P, P><<<g, kThreads, 0, s>>>(F.n, b, F.il1, x, done);
-      P* cur = x;
-      P* nxt = F.t;
-      const int sw = A->prm.sweeps + (A->prm.sweeps % 2 == 0 ? 1 : 0);   // odd: sw - 1 (even) smoothing steps
-      for (int it = 1; it < sw; ++it) {
-        k_amg_smooth<P, P, P><<<g, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, cur, b, nxt,
-                                                     done);
-        std::swap(cur, nxt);
-      }
-      *nl += sw;
-    }
-    return;
-  }
   AmgLevelDev<P>& C = A->L[l + 1];
+  Prof* pr = A->prof;
   const P w = (P)A->prm.omega;
-  const int gF = grid_for((int64_t)F.n * F.G), gC = grid_for((int64_t)C.n * C.G);
-  switch (F.G) {
-    case 8: k_amg_pre_resid_g<P, 8><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, F.t, F.r, done); break;
-    case 4: k_amg_pre_resid_g<P, 4><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, F.t, F.r, done); break;
-    default: k_amg_pre_resid<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, F.t, F.r, done);
-  }
-  k_amg_restrict<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
+  const double pb = sizeof(P), n = F.n, nc = C.n;
+  const int gF = grid_for(F.n), gC = grid_for(C.n);
+  PLAUNCH(pr, "k_amg_pre_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
+          (k_amg_pre_resid<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, F.t,
+                                                      F.r, done)));
+  PLAUNCH(pr, "k_amg_restrict", l, (4 + pb) * (n + nc), s,
+          (k_amg_restrict<P><<<gC, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
   *nl += 2;
   cycle_coarse(A, l + 1, C.b, C.x, done, s, nl);
   if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax) {
-    switch (C.G) {
-      case 8: k_amg_resid_g<P, 8><<<gC, kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b, C.r2, done); break;
-      case 4: k_amg_resid_g<P, 4><<<gC, kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b, C.r2, done); break;
-      default: k_amg_resid<P, P><<<gC, kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b, C.r2, done);
-    }
+    PLAUNCH(pr, "k_amg_resid", l + 1, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
+            (k_amg_resid<P, P><<<gC, kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b, C.r2,
+                                                       done)));
     cycle_coarse(A, l + 1, C.r2, C.e, done, s, nl);
-    k_amg_add<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done);
+    PLAUNCH(pr, "k_amg_add", l + 1, 3 * pb * nc, s, (k_amg_add<P><<<gC, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
     *nl += 2;
   }
-  switch (F.G) {
-    case 8: k_amg_prolong_smooth_g<P, 8><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.agg, C.x, w, F.t, b, x, done); break;
-    case 4: k_amg_prolong_smooth_g<P, 4><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.agg, C.x, w, F.t, b, x, done); break;
-    default: k_amg_prolong_smooth<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.agg, C.x, w, F.t, b, x, done);
-  }
+  PLAUNCH(pr, "k_amg_prolong_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + (4 + 5 * pb) * n + pb * nc, s,
+          (k_amg_prolong_smooth<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1,
+                                                           F.agg, C.x, w, F.t, b, x, done)));
   ++*nl;
 }
 
@@ -866,7 +811,9 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
 template <class P, class T>
 static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl, cudaEvent_t* ev) {
   AmgLevelDev<P>& F = A->L[0];
+  Prof* pr = A->prof;
   const bool f64 = std::is_same<P, double>::value;
+  const double pb = sizeof(P), vb = sizeof(T), n = F.n;
   dfvm_status e;
   if (A->nlev == 1) {
     if (A->m->part.P > 1 || F.n > kCoarseMax) {
@@ -876,37 +823,47 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
       // issues the same communication sequence whatever its level count
       // (a rank whose block did not coarsen must not desynchronise the
       // send / recv pairing of its peers).
-      k_amg_pre<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.il1, z, done);
+      PLAUNCH(pr, "k_amg_pre", 0, (2 * vb + pb) * n, s,
+              (k_amg_pre<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.il1, z, done)));
       if ((e = halo_exchange_p(A->m, F.x, 1, f64, s)) || (e = halo_exchange_p(A->m, F.t, 1, f64, s))) return e;
     } else {
-      k_amg_coarse<P, T, T><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, r, z,
-                                               A->prm.sweeps, done);
+      PLAUNCH(pr, "k_amg_coarse", 0, (4 + pb) * (double)F.nnz + 4 * pb * n, s,
+              (k_amg_coarse<P, T, T><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, r, z,
+                                                       A->prm.sweeps, done)));
     }
     ++*nl;
     return DFVM_OK;
   }
   AmgLevelDev<P>& C = A->L[1];
-  k_amg_pre<P, T, P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, r, F.il1, F.x, done);
+  const double nc = C.n;
+  const int g0 = grid_for(F.n), g1 = grid_for(C.n);
+  PLAUNCH(pr, "k_amg_pre", 0, (vb + 2 * pb) * n, s,
+          (k_amg_pre<P, T, P><<<g0, kThreads, 0, s>>>(F.n, r, F.il1, F.x, done)));
   if ((e = halo_exchange_p(A->m, F.x, 1, f64, s))) return e;
   if (ev) record_event(ev[0], s);
-  k_amg_resid<P, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.x, r, F.r,
-                                                       done);
+  PLAUNCH(pr, "k_amg_resid", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + vb) * n, s,
+          (k_amg_resid<P, T><<<g0, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.x, r, F.r,
+                                                     done)));
   if (ev) record_event(ev[1], s);
-  k_amg_restrict<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done);
+  PLAUNCH(pr, "k_amg_restrict", 0, (4 + pb) * (n + nc), s,
+          (k_amg_restrict<P><<<g1, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
   *nl += 3;
   cycle_coarse(A, 1, C.b, C.x, done, s, nl);
   if (A->prm.wcycle && 1 < A->nlev - 1 && 1 <= A->prm.wmax) {
-    k_amg_resid<P, P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b,
-                                                         C.r2, done);
+    PLAUNCH(pr, "k_amg_resid", 1, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
+            (k_amg_resid<P, P><<<g1, kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b,
+                                                       C.r2, done)));
     cycle_coarse(A, 1, C.r2, C.e, done, s, nl);
-    k_amg_add<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done);
+    PLAUNCH(pr, "k_amg_add", 1, 3 * pb * nc, s, (k_amg_add<P><<<g1, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
     *nl += 2;
   }
-  k_amg_prolong<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.agg, C.x, F.x, F.t, (P)A->prm.omega, done);
+  PLAUNCH(pr, "k_amg_prolong", 0, (4 + 2 * pb) * n + pb * nc, s,
+          (k_amg_prolong<P><<<g0, kThreads, 0, s>>>(F.n, F.agg, C.x, F.x, F.t, (P)A->prm.omega, done)));
   if ((e = halo_exchange_p(A->m, F.t, 1, f64, s))) return e;
   if (ev) record_event(ev[2], s);
-  k_amg_smooth<P, T, T><<<grid_for(F.n), kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1,
-                                                           F.t, r, z, done);
+  PLAUNCH(pr, "k_amg_smooth", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + 2 * vb) * n, s,
+          (k_amg_smooth<P, T, T><<<g0, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.t, r,
+                                                         z, done)));
   if (ev) record_event(ev[3], s);
   *nl += 2;
   return DFVM_OK;
@@ -914,19 +871,30 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
 
 // z = M^-1 r; skipped on the device when *done is set
 template <class T>
-dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl, cudaEvent_t* ev) {
-  dfvm_status e = A->same ? cycle0<T, T>(A->same, r, z, done, s, nl, ev) : cycle0<float, T>(A->lo, r, z, done, s, nl, ev);
+dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl, cudaEvent_t* ev,
+                      Prof* prof) {
+  dfvm_status e;
+  if (A->same) { A->same->prof = prof; e = cycle0<T, T>(A->same, r, z, done, s, nl, ev); }
+  else { A->lo->prof = prof; e = cycle0<float, T>(A->lo, r, z, done, s, nl, ev); }
   if (e) return e;
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
+}
+
+template <class T>
+int amg_level_nnz(const Amg<T>* A, int64_t* nnz) {
+  if (A->same) { for (int l = 0; l < A->same->nlev; ++l) nnz[l] = A->same->L[l].nnz; return A->same->nlev; }
+  for (int l = 0; l < A->lo->nlev; ++l) nnz[l] = A->lo->L[l].nnz;
+  return A->lo->nlev;
 }
 
 #define INST(T)                                                                           \
   template dfvm_status amg_create<T>(dfvm_mesh*, const DevMesh<T>&, bool, Amg<T>**);      \
   template void amg_destroy<T>(Amg<T>*);                                                  \
   template int amg_levels<T>(const Amg<T>*, int*);                                        \
-  template dfvm_status amg_update<T>(Amg<T>*, const T*, const T*, cudaStream_t, int*);    \
-  template dfvm_status amg_apply<T>(Amg<T>*, const T*, T*, const int*, cudaStream_t, int*, cudaEvent_t*);
+  template dfvm_status amg_update<T>(Amg<T>*, const T*, const T*, cudaStream_t, int*, Prof*); \
+  template dfvm_status amg_apply<T>(Amg<T>*, const T*, T*, const int*, cudaStream_t, int*, cudaEvent_t*, Prof*); \
+  template int amg_level_nnz<T>(const Amg<T>*, int64_t*);
 INST(double)
 INST(float)
 

@@ -119,6 +119,7 @@ static dfvm_status upload_mesh(dfvm_mesh* m, DevMesh<T>& D) {
     }
   D.n_inc = (int64_t)inc.size();
   D.n_minc = (int64_t)mnb.size();
+  D.nnz = mcnt[n_own];
   if (m->h_ms_ptr.empty()) { m->h_ms_ptr = ms_ptr; m->h_ms_len = ms_len; m->h_mnb = mnb; }   // AMG setup
   // face records
   std::vector<V4<T>> fgeo(F_l), fcor(F_l), bgeo(P.n_lb);

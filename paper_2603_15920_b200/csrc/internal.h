@@ -116,6 +116,7 @@ struct DevMesh {
   int* ms_len = nullptr;
   int* mnb = nullptr;
   int64_t n_inc = 0, n_minc = 0;
+  int64_t nnz = 0;         // real matrix entries of the owned rows (= 2F at P = 1; algorithmic bytes)
 };
 
 struct Comm;

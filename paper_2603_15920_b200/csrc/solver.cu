@@ -20,6 +20,7 @@
 #include "dev.cuh"
 #include "amg.h"
 #include "launch.h"
+#include "prof.h"
 
 namespace dfvm {
 
@@ -1194,6 +1195,9 @@ struct dfvm_solver {
   std::vector<cudaEvent_t> ev;
   double t_ms[4] = {0, 0, 0, 0};
   int64_t t_n[4] = {0, 0, 0, 0};
+  // per-kernel profile (dfvm_solver_profile; prof.h)
+  Prof prof;
+  Prof* pr() { return prof.on ? &prof : nullptr; }
   ~dfvm_solver() { for (auto e : ev) cudaEventDestroy(e); }
 };
 
@@ -1264,7 +1268,7 @@ template <class T>
 static dfvm_status fin(dfvm_solver* S, SolverT<T>& X, int kind, int nv, cudaStream_t st) {
   if (S->m->part.P == 1) return DFVM_OK;
   if (dfvm_status e = allgather_f64(S->m, X.red_local, X.red_all, nv, st)) return e;
-  k_finalize<<<1, 1, 0, st>>>(kind, nv, X.red_all, S->m->part.P, X.d_ctl);
+  PLAUNCH(S->pr(), "k_finalize", -1, 0, st, (k_finalize<<<1, 1, 0, st>>>(kind, nv, X.red_all, S->m->part.P, X.d_ctl)));
   S->n_launch++;
   return DFVM_OK;
 }
@@ -1283,13 +1287,16 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
   const Red red{m->part.P, X.red_local};
   const int gs = grid_slices(k_cg_spmv<T>, M.n_slices), ge = grid_for(M.n_own);
   const int gp = grid_rows(k_cg_p<T>, M.n_own), gr = grid_rows(k_cg_r<T>, M.n_own);
+  Prof* pr = S->pr();
+  const double v = sizeof(T), N = M.n_own, Z = (double)M.nnz;
   KCtl init{};
   init.tol = tol; init.rel_tol = rel_tol; init.maxit = maxit;
   DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, &init, sizeof(KCtl), cudaMemcpyHostToDevice, st));
   dfvm_status e;
   if ((e = halo_exchange(m, x, 1, st))) return e;
-  k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr,
-                                                                          X.partials, X.ticket, X.d_ctl, red);
+  PLAUNCH(pr, "k_cg_init", -1, 4 * N + Z * (4 + v) + 4 * v * N, st,
+          (k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr,
+                                                                                   X.partials, X.ticket, X.d_ctl, red)));
   S->n_launch++;
   if ((e = fin(S, X, CTL_CG_INIT, 3, st))) return e;
   if (S->timing && S->ev.size() < 4 * kChunk) {
@@ -1299,23 +1306,27 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
       S->ev.push_back(ev);
     }
   }
-  int it_before = 0;
+  int it_before = 0, it_prof = 0;
   for (int it0 = 0;; it0 += kChunk) {
     for (int k = 0; k < kChunk; ++k) {
+      if (pr) { pr->iter = k; pr->post = 0; }
       if (S->timing) record_event(S->ev[4 * k], st);
-      k_cg_p<T><<<gp, kThreads, 0, st>>>(M.n_own, X.kr, X.pdiag, X.kp, x, X.d_ctl);
+      PLAUNCH(pr, "k_cg_p", -1, 6 * v * N, st, (k_cg_p<T><<<gp, kThreads, 0, st>>>(M.n_own, X.kr, X.pdiag, X.kp, x, X.d_ctl)));
       if ((e = halo_exchange(m, X.kp, 1, st))) return e;
       if (S->timing) record_event(S->ev[4 * k + 1], st);
-      k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red);
+      PLAUNCH(pr, "k_cg_spmv", -1, 4 * N + Z * (4 + v) + 3 * v * N, st,
+              (k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red)));
       if (S->timing) record_event(S->ev[4 * k + 2], st);
       if ((e = fin(S, X, CTL_CG_SPMV, 1, st))) return e;
-      k_cg_r<T><<<gr, kThreads, 0, st>>>(M.n_own, X.kq, X.pdiag, X.kr, X.partials, X.ticket, X.d_ctl, red);
+      PLAUNCH(pr, "k_cg_r", -1, 4 * v * N, st,
+              (k_cg_r<T><<<gr, kThreads, 0, st>>>(M.n_own, X.kq, X.pdiag, X.kr, X.partials, X.ticket, X.d_ctl, red)));
       if ((e = fin(S, X, CTL_CG_R, 2, st))) return e;
       if (S->timing) record_event(S->ev[4 * k + 3], st);
       S->n_launch += 3;
     }
     DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
     DFVM_CUDA(cudaStreamSynchronize(st));
+    if (pr) { pr->harvest(X.h_ctl->it - it_prof, false); it_prof = X.h_ctl->it; pr->iter = -1; }
     if (S->timing) {
       // only iterations that actually ran (the rest exited on the done flag)
       const int ran = X.h_ctl->it - it_before;
@@ -1333,7 +1344,7 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
   DFVM_CUDA(cudaGetLastError());
   const KCtl& c = *X.h_ctl;
   if (c.half) {   // deferred x update of the last iteration
-    k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl);
+    PLAUNCH(pr, "k_cg_final", -1, 3 * v * N, st, (k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl)));
     S->n_launch++;
   }
   if (c.zero_x) DFVM_CUDA(cudaMemsetAsync(x, 0, (size_t)M.n_own * sizeof(T), st));
@@ -1353,8 +1364,10 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   dfvm_mesh* m = S->m;
   dfvm_status e;
   if (!X.amg && (e = amg_create<T>(m, M, S->o.p_precond == 2, &X.amg))) return e;
+  Prof* pr = S->pr();
+  const double v = sizeof(T), N = M.n_own, Z = (double)M.nnz;
   if (X.amg_dirty) {
-    if ((e = amg_update<T>(X.amg, X.pcoef, X.pdiag, st, &S->n_launch))) return e;
+    if ((e = amg_update<T>(X.amg, X.pcoef, X.pdiag, st, &S->n_launch, pr))) return e;
     X.amg_dirty = false;
   }
   const Red red{m->part.P, X.red_local};
@@ -1364,12 +1377,14 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   init.tol = tol; init.rel_tol = rel_tol; init.maxit = maxit;
   DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, &init, sizeof(KCtl), cudaMemcpyHostToDevice, st));
   if ((e = halo_exchange(m, x, 1, st))) return e;
-  k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr,
-                                                                          X.partials, X.ticket, X.d_ctl, red);
+  PLAUNCH(pr, "k_cg_init", -1, 4 * N + Z * (4 + v) + 4 * v * N, st,
+          (k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr,
+                                                                                   X.partials, X.ticket, X.d_ctl, red)));
   S->n_launch++;
   if ((e = fin(S, X, CTL_CG_INIT, 3, st))) return e;
-  if ((e = amg_apply<T>(X.amg, X.kr, X.kz, done, st, &S->n_launch, nullptr))) return e;
-  k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ0);
+  if ((e = amg_apply<T>(X.amg, X.kr, X.kz, done, st, &S->n_launch, nullptr, pr))) return e;
+  PLAUNCH(pr, "k_cg_dot", -1, 2 * v * N, st,
+          (k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ0)));
   S->n_launch++;
   if ((e = fin(S, X, CTL_CG_RZ0, 1, st))) return e;
   if (S->timing && S->ev.size() < 8 * kChunk) {
@@ -1383,18 +1398,23 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   auto enqueue_chunk = [&](int* nl) -> dfvm_status {
     dfvm_status e2;
     for (int k = 0; k < kChunk; ++k) {
+      if (pr) { pr->iter = k; pr->post = 0; }
       if (S->timing) record_event(S->ev[4 * k], st);
-      k_cg_p2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kz, X.kp, x, X.d_ctl);
+      PLAUNCH(pr, "k_cg_p2", -1, 5 * v * N, st, (k_cg_p2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kz, X.kp, x, X.d_ctl)));
       if ((e2 = halo_exchange(m, X.kp, 1, st))) return e2;
       if (S->timing) record_event(S->ev[4 * k + 1], st);
-      k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red);
+      PLAUNCH(pr, "k_cg_spmv", -1, 4 * N + Z * (4 + v) + 3 * v * N, st,
+              (k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red)));
       if (S->timing) record_event(S->ev[4 * k + 2], st);
       if ((e2 = fin(S, X, CTL_CG_SPMV, 1, st))) return e2;
-      k_cg_r2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, X.partials, X.ticket, X.d_ctl, red);
+      PLAUNCH(pr, "k_cg_r2", -1, 3 * v * N, st,
+              (k_cg_r2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, X.partials, X.ticket, X.d_ctl, red)));
       if ((e2 = fin(S, X, CTL_CG_R2, 1, st))) return e2;
-      if ((e2 = amg_apply<T>(X.amg, X.kr, X.kz, done, st, nl, S->timing ? &S->ev[4 * kChunk + 4 * k] : nullptr)))
+      if (pr) pr->post = 1;
+      if ((e2 = amg_apply<T>(X.amg, X.kr, X.kz, done, st, nl, S->timing ? &S->ev[4 * kChunk + 4 * k] : nullptr, pr)))
         return e2;
-      k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ);
+      PLAUNCH(pr, "k_cg_dot", -1, 2 * v * N, st,
+              (k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ)));
       if ((e2 = fin(S, X, CTL_CG_RZ, 1, st))) return e2;
       if (S->timing) record_event(S->ev[4 * k + 3], st);
       *nl += 4;
@@ -1406,7 +1426,7 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   // levels).  Captured on first use for this (x, b, timing); DFVM_GRAPHS=0
   // disables.
   typename SolverT<T>::ChunkGraph* graph = nullptr;
-  if (m->part.P == 1 && !X.graphs_off && st != nullptr) {   // (the legacy default stream cannot be captured)
+  if (m->part.P == 1 && !X.graphs_off && st != nullptr && !pr) {   // (the legacy default stream cannot be captured)
     const char* genv = getenv("DFVM_GRAPHS");
     if (genv && genv[0] == '0') X.graphs_off = true;
     for (auto& g : X.graphs)
@@ -1429,16 +1449,34 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
       }
     }
   }
-  int it_before = 0;
+  int it_before = 0, it_prof = 0;
+  const bool prof_graph = pr && m->part.P == 1 && st != nullptr;
   for (;;) {
     if (graph) {
       DFVM_CUDA(cudaGraphLaunch(graph->exec, st));
       S->n_launch += graph->launches;
+    } else if (prof_graph) {
+      // profile mode: this chunk captured afresh with its event pairs as
+      // graph nodes and replayed once (no host gap inside an event pair)
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t gx = nullptr;
+      int nl = 0;
+      DFVM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      const dfvm_status ce = enqueue_chunk(&nl);
+      DFVM_CUDA(cudaStreamEndCapture(st, &g));
+      if (ce) { cudaGraphDestroy(g); return ce; }
+      DFVM_CUDA(cudaGraphInstantiate(&gx, g, 0));
+      cudaGraphDestroy(g);
+      DFVM_CUDA(cudaGraphLaunch(gx, st));
+      DFVM_CUDA(cudaStreamSynchronize(st));
+      cudaGraphExecDestroy(gx);
+      S->n_launch += nl;
     } else if ((e = enqueue_chunk(&S->n_launch))) {
       return e;
     }
     DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
     DFVM_CUDA(cudaStreamSynchronize(st));
+    if (pr) { pr->harvest(X.h_ctl->it - it_prof, X.h_ctl->done != 0); it_prof = X.h_ctl->it; pr->iter = -1; pr->post = 0; }
     if (S->timing) {
       const int ran = X.h_ctl->it - it_before;
       for (int k = 0; k < kChunk && k < ran; ++k) {
@@ -1464,7 +1502,7 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   cudaGetLastError();   // clear a possible not-ready status of an unrecorded timing event
   const KCtl& c = *X.h_ctl;
   if (c.half) {
-    k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl);
+    PLAUNCH(pr, "k_cg_final", -1, 3 * v * N, st, (k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl)));
     S->n_launch++;
   }
   if (c.zero_x) DFVM_CUDA(cudaMemsetAsync(x, 0, (size_t)M.n_own * sizeof(T), st));
@@ -1488,33 +1526,50 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   // (measured on C5: flat [3n] p/x updates and shared-staged own rows in v/t
   // were 26 ms/step slower than these one-thread-per-row kernels)
   const int ge = grid_for(M.n_own);
+  Prof* pr = S->pr();
+  const double v = sizeof(T), N = M.n_own, Z = (double)M.nnz;
   KCtl init[3] = {};
   for (int k = 0; k < 3; ++k) { init[k].tol = tol; init[k].rel_tol = rel_tol; init[k].maxit = maxit; }
   DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, init, 3 * sizeof(KCtl), cudaMemcpyHostToDevice, st));
   dfvm_status e;
-  k_recip<T><<<grid_for(M.n_cells), kThreads, 0, st>>>(M.n_cells, X.udiag, X.udinv);
+  PLAUNCH(pr, "k_recip", -1, 2 * v * M.n_cells, st,
+          (k_recip<T><<<grid_for(M.n_cells), kThreads, 0, st>>>(M.n_cells, X.udiag, X.udinv)));
   S->n_launch++;
-  k_bi_init<T><<<grid_slices(k_bi_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr, X.krh,
-                                                                          X.kp, X.kv, X.partials, X.ticket, X.d_ctl, red);
+  PLAUNCH(pr, "k_bi_init", -1, 4 * N + Z * (4 + v) + 19 * v * N, st,
+          (k_bi_init<T><<<grid_slices(k_bi_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr,
+                                                                                   X.krh, X.kp, X.kv, X.partials,
+                                                                                   X.ticket, X.d_ctl, red)));
   S->n_launch++;
   if ((e = fin(S, X, CTL_BI_INIT, 6, st))) return e;
+  int it_prof = 0;
   for (;;) {
     for (int k = 0; k < kChunk; ++k) {
-      k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.kp, X.d_ctl);
+      if (pr) pr->iter = k;
+      PLAUNCH(pr, "k_bi_p", -1, 12 * v * N, st, (k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.kp, X.d_ctl)));
       if ((e = halo_exchange(m, X.kp, 3, st))) return e;
-      k_bi_v<T, 4, 6><<<gs, kThreads, 0, st>>>(M, X.udiag, X.udinv, X.ucoef, X.kp, X.krh, X.kv, X.partials, X.ticket,
-                                               X.d_ctl, red);
+      PLAUNCH(pr, "k_bi_v", -1, 4 * N + Z * (4 + v) + 11 * v * N, st,
+              (k_bi_v<T, 4, 6><<<gs, kThreads, 0, st>>>(M, X.udiag, X.udinv, X.ucoef, X.kp, X.krh, X.kv, X.partials,
+                                                        X.ticket, X.d_ctl, red)));
       if ((e = fin(S, X, CTL_BI_V, 3, st))) return e;
       if ((e = halo_exchange(m, X.kr, 3, st)) || (e = halo_exchange(m, X.kv, 3, st))) return e;
-      k_bi_t<T, 4, 3><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket, X.d_ctl, red);
+      PLAUNCH(pr, "k_bi_t", -1, 4 * N + Z * (4 + v) + 10 * v * N, st,
+              (k_bi_t<T, 4, 3><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket,
+                                                        X.d_ctl, red)));
       if ((e = fin(S, X, CTL_BI_T, 9, st))) return e;
-      k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.kp, X.kv, X.kt, X.krh, x, X.kr, X.partials, X.ticket,
-                                         X.d_ctl, red);
+      PLAUNCH(pr, "k_bi_x", -1, 25 * v * N, st,
+              (k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.kp, X.kv, X.kt, X.krh, x, X.kr, X.partials,
+                                                  X.ticket, X.d_ctl, red)));
       if ((e = fin(S, X, CTL_BI_X, 6, st))) return e;
       S->n_launch += 4;
     }
     DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, 3 * sizeof(KCtl), cudaMemcpyDeviceToHost, st));
     DFVM_CUDA(cudaStreamSynchronize(st));
+    if (pr) {
+      const int itm = std::max(X.h_ctl[0].it, std::max(X.h_ctl[1].it, X.h_ctl[2].it));
+      pr->harvest(itm - it_prof, false);
+      it_prof = itm;
+      pr->iter = -1;
+    }
     if (X.h_ctl[0].done && X.h_ctl[1].done && X.h_ctl[2].done) break;
   }
   DFVM_CUDA(cudaGetLastError());
@@ -1541,12 +1596,17 @@ static dfvm_status assemble(dfvm_solver* S, SolverT<T>& X, const T* U, const T* 
   if ((s2 = bcs_device(b, 0, st)) || (s2 = bcs_device(b, 1, st))) return s2;
   if ((s2 = halo_exchange(S->m, (void*)U, 3, st))) return s2;
   const int gs = grid_for_slices(M.n_slices);
-  launch_grad<T>(M, U, 3, b->d_kind[0], (const T*)b->d_val[0], X.gU, st);
+  Prof* pr = S->pr();
+  const double v = sizeof(T), N = M.n_own, F = M.F, Bf = M.B;
+  PLAUNCH(pr, "k_grad (U)", -1, 13 * v * N + (16 + 4 * v) * F + (9 + 7 * v) * Bf, st,
+          launch_grad<T>(M, U, 3, b->d_kind[0], (const T*)b->d_val[0], X.gU, st));
   S->n_launch++;
   if ((s2 = halo_exchange(S->m, X.gU, 9, st))) return s2;
-  k_transport_assemble<T, 3><<<gs, kThreads, 0, st>>>(M, U, phi, X.gU, X.gp, b->d_kind[0], (const T*)b->d_val[0],
-                                                      (T)S->o.nu, (T)(1.0 / S->o.dt), (T)theta_of(S->o), S->o.convection, S->kcorr,
-                                                      X.fdO, X.fdN, X.udiag, X.bU, X.rhsU, X.ucoef, X.ucoefT);
+  PLAUNCH(pr, "k_transport_assemble", -1, 23 * v * N + (16 + 10 * v) * F + (9 + 8 * v) * Bf, st,
+          (k_transport_assemble<T, 3><<<gs, kThreads, 0, st>>>(M, U, phi, X.gU, X.gp, b->d_kind[0],
+                                                               (const T*)b->d_val[0], (T)S->o.nu, (T)(1.0 / S->o.dt),
+                                                               (T)theta_of(S->o), S->o.convection, S->kcorr, X.fdO,
+                                                               X.fdN, X.udiag, X.bU, X.rhsU, X.ucoef, X.ucoefT)));
   S->n_launch++;
   if ((s2 = halo_exchange(S->m, X.udiag, 1, st))) return s2;   // k_bi_t gathers s / diag
   X.assembled = true;
@@ -1573,9 +1633,12 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   const T* bvU = (const T*)b->d_val[0];
   const uint8_t* bkp = b->d_kind[1];
   T* bvp = (T*)b->d_val[1];
+  Prof* pr = S->pr();
+  const double v = sizeof(T), N = M.n_own, F = M.F, Bf = M.B, Z = (double)M.nnz;
+  const double grad_s_bytes = 5 * v * N + (16 + 4 * v) * F + (9 + 5 * v) * Bf;
   // grad p^n (predictor source)
   if ((s2 = halo_exchange(S->m, p, 1, st))) return s2;
-  launch_grad<T>(M, p, 1, bkp, bvp, X.gp, st);
+  PLAUNCH(pr, "k_grad (p)", -1, grad_s_bytes, st, launch_grad<T>(M, p, 1, bkp, bvp, X.gp, st));
   S->n_launch++;
   // 1. momentum assembly from (U^n, phi^n, grad U^n)
   if ((s2 = assemble(S, X, U, phi, st))) return s2;
@@ -1592,8 +1655,9 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   for (int corr = 1; corr <= o.n_corr; ++corr) {
     // 3.1 Windkessel
     if (n_wk) {
-      k_windkessel<T><<<n_wk, kThreads, 0, st>>>(M, phi, X.d_wk, X.d_wk_ptr, X.d_wk_faces, o.dt, o.rho, bvp,
-                                                 Red{S->m->part.P, X.red_local});
+      PLAUNCH(pr, "k_windkessel", -1, 0, st,
+              (k_windkessel<T><<<n_wk, kThreads, 0, st>>>(M, phi, X.d_wk, X.d_wk_ptr, X.d_wk_faces, o.dt, o.rho, bvp,
+                                                          Red{S->m->part.P, X.red_local})));
       S->n_launch++;
       if (S->m->part.P > 1) {
         if ((s2 = allgather_f64(S->m, X.red_local, X.red_all, n_wk, st))) return s2;
@@ -1604,15 +1668,19 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
     }
     // 3.2 rAU, HbyA
     if ((s2 = halo_exchange(S->m, U, 3, st))) return s2;
-    k_HbyA<T><<<gs, kThreads, 0, st>>>(M, X.bU, X.udiag, X.ucoef, U, X.rAU, X.HbyA);
+    PLAUNCH(pr, "k_HbyA", -1, 4 * N + Z * (4 + v) + 12 * v * N, st,
+            (k_HbyA<T><<<gs, kThreads, 0, st>>>(M, X.bU, X.udiag, X.ucoef, U, X.rAU, X.HbyA)));
     S->n_launch++;
     if ((s2 = halo_exchange(S->m, X.HbyA, 3, st)) || (s2 = halo_exchange(S->m, X.rAU, 1, st))) return s2;
     // 3.3 phiHbyA
-    k_phiHbyA<T><<<gf, kThreads, 0, st>>>(M, X.HbyA, bkU, bvU, X.phiHbyA, o.ddt_corr ? X.Uold : nullptr, X.phiold,
-                                          X.rAU, (T)(1.0 / o.dt));
+    PLAUNCH(pr, "k_phiHbyA", -1,
+            3 * v * N + (8 + 5 * v) * F + (5 + 8 * v) * Bf + (o.ddt_corr ? 4 * v * N + v * F : 0.0), st,
+            (k_phiHbyA<T><<<gf, kThreads, 0, st>>>(M, X.HbyA, bkU, bvU, X.phiHbyA, o.ddt_corr ? X.Uold : nullptr,
+                                                   X.phiold, X.rAU, (T)(1.0 / o.dt))));
     // 3.4 pressure coefficients
-    k_pcoef<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
-                                        (T)o.p_ref_value, X.pcoef, X.pdiag, X.prhs0);
+    PLAUNCH(pr, "k_pcoef", -1, 3 * v * N + (16 + 5 * v) * F + (9 + 3 * v) * Bf, st,
+            (k_pcoef<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
+                                                 (T)o.p_ref_value, X.pcoef, X.pdiag, X.prhs0)));
     X.amg_dirty = true;
     S->n_launch += 2;
     // 3.5 non-orthogonal loop
@@ -1623,11 +1691,12 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
         // previous solve (io > 0) or after a Windkessel update of p_b
         if (io > 0 || n_wk > 0) {
           if ((s2 = halo_exchange(S->m, p, 1, st))) return s2;
-          launch_grad<T>(M, p, 1, bkp, bvp, X.gp, st);
+          PLAUNCH(pr, "k_grad (p)", -1, grad_s_bytes, st, launch_grad<T>(M, p, 1, bkp, bvp, X.gp, st));
           S->n_launch++;
         }
         if ((s2 = halo_exchange(S->m, X.gp, 3, st))) return s2;
-        k_prhs<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.gp, X.prhs0, X.prhs);
+        PLAUNCH(pr, "k_prhs", -1, 6 * v * N + (16 + 5 * v) * F, st,
+                (k_prhs<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.gp, X.prhs0, X.prhs)));
         S->n_launch++;
         rhs = X.prhs;
       }
@@ -1640,18 +1709,21 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
       if (s2 == DFVM_E_NOT_CONVERGED) res = s2;
       if (io == o.n_nonorth) {
         if ((s2 = halo_exchange(S->m, p, 1, st))) return s2;
-        k_fluxcorr<T><<<gf, kThreads, 0, st>>>(M, X.phiHbyA, p, X.rAU, X.gp, bkp, bvp, S->kcorr, phi);
+        PLAUNCH(pr, "k_fluxcorr", -1, 5 * v * N + (8 + 7 * v) * F + (5 + 4 * v) * Bf, st,
+                (k_fluxcorr<T><<<gf, kThreads, 0, st>>>(M, X.phiHbyA, p, X.rAU, X.gp, bkp, bvp, S->kcorr, phi)));
         S->n_launch++;
       }
     }
     // 3.6 velocity correction (also refreshes grad p)
-    k_Ucorr<T><<<gs, kThreads, 0, st>>>(M, p, bkp, bvp, X.HbyA, X.rAU, U, X.gp);
+    PLAUNCH(pr, "k_Ucorr", -1, 12 * v * N + (16 + 4 * v) * F + (9 + 4 * v) * Bf, st,
+            (k_Ucorr<T><<<gs, kThreads, 0, st>>>(M, p, bkp, bvp, X.HbyA, X.rAU, U, X.gp)));
     S->n_launch++;
   }
   R->n_p = np;
   // 4. continuity + non-finite + Windkessel commit
-  k_continuity<T><<<gs, kThreads, 0, st>>>(M, phi, U, p, X.partials, X.ticket, X.d_cont, X.d_wk, n_wk,
-                                           Red{S->m->part.P, X.red_local});
+  PLAUNCH(pr, "k_continuity", -1, 4 * v * N + (16 + v) * F + (8 + v) * Bf, st,
+          (k_continuity<T><<<gs, kThreads, 0, st>>>(M, phi, U, p, X.partials, X.ticket, X.d_cont, X.d_wk, n_wk,
+                                                    Red{S->m->part.P, X.red_local})));
   S->n_launch++;
   if (S->m->part.P > 1) {
     if ((s2 = allgather_f64(S->m, X.red_local, X.red_all, 3, st))) return s2;
@@ -1662,6 +1734,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   if (n_wk) DFVM_CUDA(cudaMemcpyAsync(X.h_wk, X.d_wk, n_wk * sizeof(WKDev), cudaMemcpyDeviceToHost, st));
   DFVM_CUDA(cudaStreamSynchronize(st));
   DFVM_CUDA(cudaGetLastError());
+  if (pr) pr->harvest();
   R->cont_err_max = X.h_cont[0];
   R->cont_err_sum = X.h_cont[1];
   R->nonfinite = X.h_cont[2] > 0;
@@ -1767,19 +1840,43 @@ dfvm_status dfvm_solver_set_timing(dfvm_solver* s, int32_t on) {
   return DFVM_OK;
 }
 
-dfvm_status dfvm_solver_amg_levels(const dfvm_solver* s, int32_t* n_levels, int64_t* sizes) {
+dfvm_status dfvm_solver_amg_levels(const dfvm_solver* s, int32_t* n_levels, int64_t* sizes, int64_t* nnz) {
   if (!s || !n_levels) { set_error(DFVM_E_INVALID_ARG, "NULL argument"); return DFVM_E_INVALID_ARG; }
   int lv[32] = {0};
+  int64_t nz[32] = {0};
   int n = 0;
   if (s->m->precision == DFVM_F64) {
     auto* X = static_cast<SolverT<double>*>(s->impl.get());
-    if (X->amg) n = amg_levels<double>(X->amg, lv);
+    if (X->amg) { n = amg_levels<double>(X->amg, lv); amg_level_nnz<double>(X->amg, nz); }
   } else {
     auto* X = static_cast<SolverT<float>*>(s->impl.get());
-    if (X->amg) n = amg_levels<float>(X->amg, lv);
+    if (X->amg) { n = amg_levels<float>(X->amg, lv); amg_level_nnz<float>(X->amg, nz); }
   }
   *n_levels = n;
   if (sizes) for (int i = 0; i < n; ++i) sizes[i] = lv[i];
+  if (nnz) for (int i = 0; i < n; ++i) nnz[i] = nz[i];
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_solver_profile(dfvm_solver* s, int32_t on) {
+  if (!s) { set_error(DFVM_E_INVALID_ARG, "NULL solver"); return DFVM_E_INVALID_ARG; }
+  s->prof.clear();
+  s->prof.on = on != 0;
+  return DFVM_OK;
+}
+
+dfvm_status dfvm_solver_profile_get(const dfvm_solver* s, dfvm_kernel_stat* out, int32_t cap, int32_t* n) {
+  if (!s || !n || (cap > 0 && !out)) { set_error(DFVM_E_INVALID_ARG, "NULL argument"); return DFVM_E_INVALID_ARG; }
+  const auto& st = s->prof.stats;
+  *n = (int32_t)st.size();
+  for (int32_t i = 0; i < cap && i < (int32_t)st.size(); ++i) {
+    std::memset(&out[i], 0, sizeof(out[i]));
+    std::strncpy(out[i].name, st[i].name, sizeof(out[i].name) - 1);
+    out[i].level = st[i].lvl;
+    out[i].launches = st[i].n;
+    out[i].ms = st[i].ms;
+    out[i].alg_bytes = st[i].bytes;
+  }
   return DFVM_OK;
 }
 
