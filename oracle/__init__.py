@@ -92,6 +92,9 @@ def lib():
         L.orc_renumber_maps.argtypes = [vp] * 10
         L.orc_renumber_part_sizes.argtypes = [vp, i32, vp]
         L.orc_renumber_part.argtypes = [vp, i32, vp, vp, vp, vp]
+        L.orc_laplacian_parts.argtypes = [vp, vp, i32, vp, vp, vp, vp]
+        L.orc_pressure_rhs.argtypes = [vp] * 5
+        L.orc_flux_correct.argtypes = [vp] * 5
         _LIB = L
     return _LIB
 
@@ -327,6 +330,21 @@ class Solver:
         st = lib().orc_pressure_adjoint(self.h, _p(rAU), _p(g), _p(lam), tol, maxit, 2 if direct else 0, _p(rep))
         return lam, dict(it=int(rep[0]), res0=rep[1], res=rep[2], converged=bool(rep[3]), status=STATUS[st])
 
+    def pressure_rhs(self, rAU, phiHbyA, p):
+        """O-6 step 3.5 right-hand side (A-9 reading): -D(phiHbyA) + sum_b c_b p_b
+        + sum_f s rAU_f k_f . (grad p)_f with the Gauss gradient of p."""
+        out = np.empty(self.mesh.N)
+        rAU, phiHbyA, p = _f64(rAU), _f64(phiHbyA), _f64(p)
+        _check(lib().orc_pressure_rhs(self.h, _p(rAU), _p(phiHbyA), _p(p), _p(out)))
+        return out
+
+    def flux_correct(self, rAU, phiHbyA, p):
+        """Rhie-Chow corrected flux (A-9): phiHbyA - c_f (p_N - p_O) - rAU_f k_f . (grad p)_f."""
+        out = np.empty(self.mesh.NF)
+        rAU, phiHbyA, p = _f64(rAU), _f64(phiHbyA), _f64(p)
+        _check(lib().orc_flux_correct(self.h, _p(rAU), _p(phiHbyA), _p(p), _p(out)))
+        return out
+
     def pressure_vjp(self, rAU, p, lam):
         """dL/drAU through the converged solve A(rAU) p = rhs, given lambda = A^-T dL/dp."""
         out = np.empty(self.mesh.N)
@@ -375,6 +393,15 @@ class Renumbering:
             sd = np.empty(ps[1], np.int32); sp = np.empty(ps[1], np.int32)
             L.orc_renumber_part(self.h, p, _p(g), _p(gp), _p(sd), _p(sp))
             self.parts.append(dict(ghost=g, ghost_peer=gp, send=sd, send_peer=sp))
+
+    def laplacian_parts(self, mesh, bcs, fld, x, gamma=None):
+        """O-10: the Laplacian applied part by part from owned + ghost data only
+        (ghosts filled from the owners' send lists); original numbering."""
+        y = np.empty(mesh.N)
+        x = _f64(x)
+        g = None if gamma is None else _f64(gamma)
+        _check(lib().orc_laplacian_parts(mesh.h, bcs.h, {"U": 0, "p": 1, "s": 2}[fld], self.h, _p(g), _p(x), _p(y)))
+        return y
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -386,6 +386,68 @@ static void pressure_matrix(const Solver& S, const double* rAU, LDU& A, std::vec
   }
 }
 
+// Pressure right-hand side of one non-orthogonal corrector (eq:pressure_poisson
+// RHS P:337-339 times -1; the explicit
+// non-orthogonal part in the A-9 reading):
+//   rhs_c = -D_c(phiHbyA) + sum_{b fixed p} c_b p_b
+//           + sum_{f in c} s_cf rAU_f k_f . (grad p)_f,
+// rAU_f = w rAU_O + (1 - w) rAU_N, (grad p)_f = w G_O + (1 - w) G_N (A-2),
+// G the Gauss gradient of the current p (passed in).  Faces of the cell in
+// ascending index.
+static void pressure_rhs(const Solver& S, const double* rAU, const double* Dphi, const std::vector<double>& cb,
+                         const double* p, const double* Gp, double* rhs) {
+  const Mesh& m = *S.m;
+  const BCs& b = *S.b;
+  for (int64_t c = 0; c < m.N; ++c) {
+    double acc = -Dphi[c];
+    for (int64_t i = m.cptr[c]; i < m.cptr[c + 1]; ++i) {
+      const int64_t f = m.cface[i];
+      if (f < m.F) {
+        const int64_t O = m.owner[f], Nn = m.neigh[f];
+        const double w = m.w[f];
+        const double rf = w * rAU[O] + (1.0 - w) * rAU[Nn];
+        double kg = 0;
+        for (int l = 0; l < 3; ++l) kg += m.kf[3 * f + l] * (w * Gp[3 * O + l] + (1.0 - w) * Gp[3 * Nn + l]);
+        acc += ((O == c) ? 1.0 : -1.0) * rf * kg;
+      } else if (cb[f - m.F] != 0.0) {
+        double pb;
+        boundary_value(m, b, 1, 1, p, f, &pb);
+        acc += cb[f - m.F] * pb;
+      }
+    }
+    rhs[c] = acc;
+  }
+}
+
+// Rhie-Chow flux correction (the A-9 form, no ddtCorr):
+//   phi_f = phiHbyA_f - c_f (p_N - p_O) - rAU_f k_f . (grad p)_f,
+//   phi_b = phiHbyA_b - c_b (p_b - p_O) on fixed-value p, phiHbyA_b otherwise,
+// with the same (grad p)_f as the right-hand side it corrects (so the
+// converged flux satisfies sum_f s_cf phi_f = 0 cell by cell).
+static void flux_correct(const Solver& S, const double* rAU, const double* phiHbyA, const std::vector<double>& cf,
+                         const std::vector<double>& cb, const double* p, const double* Gp, double* phi) {
+  const Mesh& m = *S.m;
+  const BCs& b = *S.b;
+  for (int64_t f = 0; f < m.F; ++f) {
+    const int64_t O = m.owner[f], Nn = m.neigh[f];
+    const double w = m.w[f];
+    const double rf = w * rAU[O] + (1.0 - w) * rAU[Nn];
+    double kg = 0;
+    for (int l = 0; l < 3; ++l) kg += m.kf[3 * f + l] * (w * Gp[3 * O + l] + (1.0 - w) * Gp[3 * Nn + l]);
+    phi[f] = phiHbyA[f] - cf[f] * (p[Nn] - p[O]) - rf * kg;
+  }
+  for (int64_t f = m.F; f < m.NF; ++f) {
+    if (m.is_empty_face(f)) { phi[f] = 0; continue; }
+    if (cb[f - m.F] != 0.0) {
+      double pb;
+      boundary_value(m, b, 1, 1, p, f, &pb);
+      phi[f] = phiHbyA[f] - cb[f - m.F] * (pb - p[m.owner[f]]);
+    } else {
+      phi[f] = phiHbyA[f];
+    }
+  }
+}
+
 // Gauge (A-12, OpenFOAM setReference): A_rr doubled and b_r += A_rr p_ref.
 static void apply_reference(const Solver& S, LDU& A, double* rhs) {
   const int64_t r = S.o.p_ref_cell;
@@ -482,25 +544,7 @@ static int piso_step(Solver& S, double* U, double* p, double* phi, Report& R) {
     // 3.5 non-orthogonal loop
     for (int io = 0; io <= S.o.n_nonorth; ++io) {
       grad(m, b, 1, 1, p, Gp.data());
-      for (int64_t c = 0; c < N; ++c) {
-        double acc = -Dphi[c];
-        for (int64_t i = m.cptr[c]; i < m.cptr[c + 1]; ++i) {
-          const int64_t f = m.cface[i];
-          if (f < m.F) {
-            const int64_t O = m.owner[f], Nn = m.neigh[f];
-            const double w = m.w[f];
-            const double rf = w * rAU[O] + (1.0 - w) * rAU[Nn];
-            double kg = 0;
-            for (int l = 0; l < 3; ++l) kg += m.kf[3 * f + l] * (w * Gp[3 * O + l] + (1.0 - w) * Gp[3 * Nn + l]);
-            acc += ((O == c) ? 1.0 : -1.0) * rf * kg;
-          } else if (cb[f - m.F] != 0.0) {
-            double pb;
-            boundary_value(m, b, 1, 1, p, f, &pb);
-            acc += cb[f - m.F] * pb;
-          }
-        }
-        rhs[c] = acc;
-      }
+      pressure_rhs(S, rAU.data(), Dphi.data(), cb, p, Gp.data(), rhs.data());
       LDU Ar = A;
       if (!fixed_p) apply_reference(S, Ar, rhs.data());
       const bool final_corr = corr == S.o.n_corr && io == S.o.n_nonorth;
@@ -508,27 +552,7 @@ static int piso_step(Solver& S, double* U, double* p, double* phi, Report& R) {
                              final_corr ? S.o.p_rel_tol_final : S.o.p_rel_tol, S.o.p_maxit);
       if (np < 16) R.p[np] = sr;
       np++;
-      if (io == S.o.n_nonorth) {
-        // flux correction (Rhie-Chow; A-9 form)
-        for (int64_t f = 0; f < m.F; ++f) {
-          const int64_t O = m.owner[f], Nn = m.neigh[f];
-          const double w = m.w[f];
-          const double rf = w * rAU[O] + (1.0 - w) * rAU[Nn];
-          double kg = 0;
-          for (int l = 0; l < 3; ++l) kg += m.kf[3 * f + l] * (w * Gp[3 * O + l] + (1.0 - w) * Gp[3 * Nn + l]);
-          phi[f] = phiHbyA[f] - cf[f] * (p[Nn] - p[O]) - rf * kg;
-        }
-        for (int64_t f = m.F; f < m.NF; ++f) {
-          if (m.is_empty_face(f)) { phi[f] = 0; continue; }
-          if (cb[f - m.F] != 0.0) {
-            double pb;
-            boundary_value(m, b, 1, 1, p, f, &pb);
-            phi[f] = phiHbyA[f] - cb[f - m.F] * (pb - p[m.owner[f]]);
-          } else {
-            phi[f] = phiHbyA[f];
-          }
-        }
-      }
+      if (io == S.o.n_nonorth) flux_correct(S, rAU.data(), phiHbyA.data(), cf, cb, p, Gp.data(), phi);
     }
     // 3.6 velocity correction (eq:velocity_correction P:344-346)
     grad(m, b, 1, 1, p, Gp.data());
@@ -604,6 +628,32 @@ void* orc_solver_create(const void* mp, void* bp, const double* dopts, const int
   return S;
 }
 void orc_solver_destroy(void* s) { delete (Solver*)s; }
+
+// O-6 step 3.5 pieces on the solver's mesh / p boundary conditions (pins of
+// the A-9 reading): rhs of the pressure equation from (rAU, phiHbyA, p), and
+// the corrected flux phi from (rAU, phiHbyA, p); (grad p) is the Gauss
+// gradient of the given p in both, as in the step.
+int orc_pressure_rhs(void* sp, const double* rAU, const double* phiHbyA, const double* p, double* rhs) {
+  Solver& S = *(Solver*)sp;
+  const Mesh& m = *S.m;
+  LDU A;
+  std::vector<double> cf, cb, Dphi(m.N), Gp(3 * m.N);
+  pressure_matrix(S, rAU, A, cf, cb);
+  div(m, phiHbyA, Dphi.data());
+  grad(m, *S.b, 1, 1, p, Gp.data());
+  pressure_rhs(S, rAU, Dphi.data(), cb, p, Gp.data(), rhs);
+  return OK;
+}
+int orc_flux_correct(void* sp, const double* rAU, const double* phiHbyA, const double* p, double* phi) {
+  Solver& S = *(Solver*)sp;
+  const Mesh& m = *S.m;
+  LDU A;
+  std::vector<double> cf, cb, Gp(3 * m.N);
+  pressure_matrix(S, rAU, A, cf, cb);
+  grad(m, *S.b, 1, 1, p, Gp.data());
+  flux_correct(S, rAU, phiHbyA, cf, cb, p, Gp.data(), phi);
+  return OK;
+}
 
 int orc_windkessel_set(void* sp, int32_t patch, double Rp, double Cc, double Rd, double pc0, int scheme) {
   Solver* S = (Solver*)sp;

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstring>
 #include <deque>
+#include <string>
 #include <tuple>
 
 namespace orc {
@@ -195,6 +196,150 @@ static Renum* renumber(const Mesh& m, int P, int use_rcm) {
   return R;
 }
 
+// ------------------------------------------------------------------ O-10
+// Partition emulation (the oracle-side check of the
+// O-9 partition and halo lists): every part holds only its owned cells
+// (ascending new id) and its ghost slice (ghost[p], ordered by (peer, new
+// id)); ghost values arrive by an explicit copy from the owning part's send
+// list to this part.  Per part, the Gauss gradient of the owned cells and
+// then the Laplacian of the owned cells are computed from local data only,
+// with the global operators' arithmetic (faces of a cell in ascending
+// original index, the same expressions), so the scattered result must equal
+// the global apply bit for bit.  A neighbour value that is neither owned nor
+// in the ghost slice, or a send list that does not match the receiver's
+// ghost slice, is an error (the halo lists are incomplete or misordered).
+namespace {
+struct PartData {
+  int64_t lo = 0, hi = 0;
+  std::vector<int32_t> g2l;            // new id -> local index (-1: not local)
+  std::vector<double> x, gamma, G;     // local vectors [n_own + n_ghost] (G: x3)
+};
+
+// copy the ghost slices of every part from the owners' send lists; nc
+// components of the vector selected by `sel`
+static int exchange(const Renum& R, std::vector<PartData>& D, int nc, std::vector<double> PartData::*sel) {
+  const int P = R.P;
+  for (int p = 0; p < P; ++p) {
+    const int64_t n_own = D[p].hi - D[p].lo;
+    size_t gi = 0;
+    for (int q = 0; q < P; ++q) {
+      if (q == p) continue;
+      // q's send list to p, in order
+      std::vector<int32_t> sl;
+      for (size_t i = 0; i < R.send[q].size(); ++i)
+        if (R.send_peer[q][i] == p) sl.push_back(R.send[q][i]);
+      for (size_t i = 0; i < sl.size(); ++i, ++gi) {
+        if (gi >= R.ghost[p].size() || R.ghost_peer[p][gi] != q || R.ghost[p][gi] != sl[i]) {
+          set_error(E_MESH_CONSISTENCY, "O-10: send list of part " + std::to_string(q) + " does not match the ghost slice of part " +
+                    std::to_string(p), sl[i]);
+          return E_MESH_CONSISTENCY;
+        }
+        const int32_t src = D[q].g2l[sl[i]];
+        for (int k = 0; k < nc; ++k) (D[p].*sel)[(size_t)nc * (n_own + gi) + k] = (D[q].*sel)[(size_t)nc * src + k];
+      }
+    }
+    if (gi != R.ghost[p].size()) {
+      set_error(E_MESH_CONSISTENCY, "O-10: ghost slice of part " + std::to_string(p) + " has cells no peer sends", p);
+      return E_MESH_CONSISTENCY;
+    }
+  }
+  return OK;
+}
+}  // namespace
+
+static int laplacian_parts(const Mesh& m, const BCs& b, int fi, const Renum& R, const double* gamma, const double* x,
+                           double* y) {
+  const int P = R.P;
+  const int64_t N = m.N;
+  std::vector<int32_t> old_of_new(N);
+  for (int64_t c = 0; c < N; ++c) old_of_new[R.new_of_old[c]] = (int32_t)c;
+  std::vector<PartData> D(P);
+  for (int p = 0; p < P; ++p) {
+    PartData& d = D[p];
+    d.lo = (int64_t)p * N / P; d.hi = (int64_t)(p + 1) * N / P;
+    const int64_t n_own = d.hi - d.lo, n_loc = n_own + (int64_t)R.ghost[p].size();
+    d.g2l.assign(N, -1);
+    for (int64_t k = 0; k < n_own; ++k) d.g2l[d.lo + k] = (int32_t)k;
+    for (size_t i = 0; i < R.ghost[p].size(); ++i) d.g2l[R.ghost[p][i]] = (int32_t)(n_own + i);
+    d.x.assign(n_loc, 0); d.gamma.assign(n_loc, 1.0); d.G.assign(3 * n_loc, 0);
+    for (int64_t k = 0; k < n_own; ++k) {          // the initial distribution of the owned values
+      d.x[k] = x[old_of_new[d.lo + k]];
+      if (gamma) d.gamma[k] = gamma[old_of_new[d.lo + k]];
+    }
+  }
+  int st;
+  if ((st = exchange(R, D, 1, &PartData::x))) return st;
+  if (gamma && (st = exchange(R, D, 1, &PartData::gamma))) return st;
+  auto local = [&](const PartData& d, int64_t old_id, int p) -> int64_t {
+    const int32_t l = d.g2l[R.new_of_old[old_id]];
+    if (l < 0) set_error(E_MESH_CONSISTENCY, "O-10: part " + std::to_string(p) + " reads a cell it neither owns nor ghosts", old_id);
+    return l;
+  };
+  // boundary value of a scalar field on face f of owned cell with local value xO
+  auto bval = [&](int64_t f, double xO) {
+    const BC& bc = b.bc[fi][m.face_patch[f - m.F]];
+    if (bc.kind == BC_FIXED || bc.kind == BC_PARABOLIC || bc.kind == BC_WINDKESSEL) {
+      double v;
+      boundary_value(m, b, fi, 1, nullptr, f, &v);
+      return v;
+    }
+    return xO;
+  };
+  // phase 1: Gauss gradient of the owned cells (grad() = interpolate + grad_from_faces)
+  for (int p = 0; p < P; ++p) {
+    PartData& d = D[p];
+    for (int64_t k = 0; k < d.hi - d.lo; ++k) {
+      const int64_t c = old_of_new[d.lo + k];
+      double acc[3] = {0, 0, 0};
+      for (int64_t i = m.cptr[c]; i < m.cptr[c + 1]; ++i) {
+        const int64_t f = m.cface[i];
+        if (f >= m.F && m.is_empty_face(f)) continue;
+        double fv;
+        if (f < m.F) {
+          const int64_t lO = local(d, m.owner[f], p), lN = local(d, m.neigh[f], p);
+          if (lO < 0 || lN < 0) return E_MESH_CONSISTENCY;
+          fv = m.w[f] * d.x[lO] + (1.0 - m.w[f]) * d.x[lN];
+        } else {
+          fv = bval(f, d.x[k]);
+        }
+        const double s = (m.owner[f] == c) ? 1.0 : -1.0;
+        for (int l = 0; l < 3; ++l) acc[l] += s * fv * m.Sf[3 * f + l];
+      }
+      for (int l = 0; l < 3; ++l) d.G[3 * k + l] = acc[l] / m.V[c];
+    }
+  }
+  if ((st = exchange(R, D, 3, &PartData::G))) return st;
+  // phase 2: Laplacian of the owned cells (laplacian() with the gradient given)
+  for (int p = 0; p < P; ++p) {
+    PartData& d = D[p];
+    for (int64_t k = 0; k < d.hi - d.lo; ++k) {
+      const int64_t c = old_of_new[d.lo + k];
+      double acc = 0;
+      for (int64_t i = m.cptr[c]; i < m.cptr[c + 1]; ++i) {
+        const int64_t f = m.cface[i];
+        if (f < m.F) {
+          const int64_t lO = local(d, m.owner[f], p), lN = local(d, m.neigh[f], p);
+          if (lO < 0 || lN < 0) return E_MESH_CONSISTENCY;
+          const double s = (m.owner[f] == c) ? 1.0 : -1.0;
+          const double w = m.w[f];
+          const double gf = gamma ? w * d.gamma[lO] + (1.0 - w) * d.gamma[lN] : 1.0;
+          double corr = 0;
+          for (int l = 0; l < 3; ++l) corr += m.kf[3 * f + l] * (w * d.G[3 * lO + l] + (1.0 - w) * d.G[3 * lN + l]);
+          acc += s * (gf * (m.delta[f] * (d.x[lN] - d.x[lO]) + corr));
+        } else {
+          const int pt = m.face_patch[f - m.F];
+          if (m.pkind[pt] == PK_EMPTY || !is_fixed(b, fi, pt)) continue;
+          const double xb = bval(f, d.x[k]);
+          const double gO = gamma ? d.gamma[k] : 1.0;
+          acc += gO * m.delta_b[f - m.F] * (xb - d.x[k]);
+        }
+      }
+      y[c] = acc;
+    }
+  }
+  return OK;
+}
+
 }  // namespace orc
 
 using namespace orc;
@@ -229,6 +374,11 @@ void orc_renumber_maps(const void* rp, int32_t* cell_new_of_old, int32_t* face_n
 void orc_renumber_part_sizes(const void* rp, int p, int64_t* out) {
   const Renum* R = (const Renum*)rp;
   out[0] = (int64_t)R->ghost[p].size(); out[1] = (int64_t)R->send[p].size();
+}
+// O-10: y (original numbering) = Laplacian of x applied part by part (see above)
+int orc_laplacian_parts(const void* mp, const void* bp, int fi, const void* rp, const double* gamma, const double* x,
+                        double* y) {
+  return laplacian_parts(*(const Mesh*)mp, *(const BCs*)bp, fi, *(const Renum*)rp, gamma, x, y);
 }
 void orc_renumber_part(const void* rp, int p, int32_t* ghost, int32_t* ghost_peer, int32_t* send,
                        int32_t* send_peer) {
