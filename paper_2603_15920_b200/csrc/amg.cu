@@ -44,6 +44,7 @@
 #include "amg.h"
 #include "dev.cuh"
 #include "prof.h"
+#include "krylov.cuh"
 
 namespace dfvm {
 
@@ -71,12 +72,21 @@ constexpr int kMaxLevels = 16;
 //                    since removed: sigma costs 0.5 PCG iterations per
 //                    solve and the grouped kernels were slower than one
 //                    thread per row)
+//   DFVM_AMG_TAIL    coarse levels with <= this many rows (all of them,
+//                    from the first such level down) run as ONE kernel per
+//                    visit of the level above: a thread-block cluster that
+//                    walks the whole sub-cycle with cluster barriers
+//                    (k_amg_tail; bitwise identical to the launched
+//                    kernels); 0: launched kernels            default 100000
+//   DFVM_AMG_TAIL_CLUSTER  CTAs of the tail cluster (16: non-portable size)
+//                                                             default 16
 //   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
 //                    exactly with a dense inverse (Gauss-Jordan once per
 //                    matrix update, one block), larger ones with
 //                    DFVM_AMG_SWEEPS l1-Jacobi sweeps (0: always sweeps)  default 512
 struct AmgParams {
   int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, sigma = 0;
+  int tail = 100000, tail_cluster = 16;
   bool wcycle = true;
   double omega = 1.9;   // C5 amg32: 362 ms, 11.6 it/solve (1.8: 369 ms, 12.2; 1.7: 380 ms)
   AmgParams() {
@@ -87,6 +97,8 @@ struct AmgParams {
     if (const char* e = getenv("DFVM_AMG_SWEEPS")) sweeps = std::max(1, atoi(e));
     if (const char* e = getenv("DFVM_AMG_CYCLE")) wcycle = (e[0] == 'W' || e[0] == 'w');
     if (const char* e = getenv("DFVM_AMG_WMAX")) wmax = std::max(0, atoi(e));
+    if (const char* e = getenv("DFVM_AMG_TAIL")) tail = std::max(0, atoi(e));
+    if (const char* e = getenv("DFVM_AMG_TAIL_CLUSTER")) tail_cluster = std::max(1, std::min(16, atoi(e)));
   }
 };
 
@@ -176,6 +188,25 @@ struct AmgLevelDev {
   P *e = nullptr, *r2 = nullptr;                  // W-cycle: second-visit solution / rhs
 };
 
+// device view of the levels for the cluster tail (k_amg_tail), in device
+// memory (one copy per hierarchy, written at build time)
+template <class P>
+struct TailLevel {
+  int n;
+  const int *ms_ptr, *ms_len, *mnb;
+  const P *coef, *diag, *il1;
+  const int* agg;               // fine row -> coarse row (this level -> next)
+  const int *mem_ptr, *mem;     // this level's aggregates: member rows of the finer level
+  P *x, *b, *r, *t, *e, *r2;
+};
+template <class P>
+struct TailArgs {
+  int nlev, wmax, wcycle, sweeps;
+  P omega;
+  const P* ainv;
+  TailLevel<P> L[kMaxLevels];
+};
+
 // hierarchy stored and cycled in type P
 template <class P>
 struct AmgH {
@@ -183,6 +214,9 @@ struct AmgH {
   int nlev = 0;
   AmgParams prm;
   Prof* prof = nullptr;             // per-kernel profile of the caller (may be null)
+  int tail_l0 = -1;                 // first level run by the cluster tail (-1: none)
+  int tail_cs = 16;                 // CTAs of the tail cluster
+  TailArgs<P>* d_tail = nullptr;
   AmgLevelDev<P> L[kMaxLevels];
   P* ainv = nullptr;                // dense inverse of the coarsest matrix (column-major n x n), or NULL
   std::vector<void*> allocs;
@@ -361,6 +395,27 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
               100.0 * (1.0 - (double)H[k].rp[H[k].n] / std::max<double>(1.0, (double)H[k].ms_ptr.back())));
   const int nc = A->L[lev].n;
   if (lev > 0 && nc <= A->prm.direct && (st = A->zalloc(&A->ainv, (size_t)nc * nc))) return st;
+  // cluster tail: from the first level >= 1 with <= prm.tail rows down (one
+  // rank only: coarse levels are rank-local, so it would also hold at P > 1,
+  // but the tail is kept to the single-rank path it is tested on)
+  A->tail_l0 = -1;
+  if (A->prm.tail > 0 && m->part.P == 1)
+    for (int l = 1; l < A->nlev; ++l)
+      if (A->L[l].n <= A->prm.tail) { A->tail_l0 = l; break; }
+  if (A->tail_l0 >= 0) {
+    TailArgs<P> h{};
+    h.nlev = A->nlev; h.wmax = A->prm.wmax; h.wcycle = A->prm.wcycle ? 1 : 0; h.sweeps = A->prm.sweeps;
+    h.omega = (P)A->prm.omega; h.ainv = A->ainv;
+    for (int l = 0; l < A->nlev; ++l) {
+      const AmgLevelDev<P>& D = A->L[l];
+      // level 0 of an amg32 hierarchy binds coef / diag per update: the tail never reads level 0
+      h.L[l] = TailLevel<P>{D.n, D.ms_ptr, D.ms_len, D.mnb, D.coef, D.diag, D.il1, D.agg, D.mem_ptr, D.mem,
+                            D.x, D.b, D.r, D.t, D.e, D.r2};
+    }
+    std::vector<TailArgs<P>> hv(1, h);
+    if ((st = A->up(&A->d_tail, hv))) return st;
+    A->tail_cs = A->prm.tail_cluster;
+  }
   return DFVM_OK;
 }
 
@@ -434,13 +489,20 @@ __global__ void k_il1(int n, const int* __restrict__ ms_ptr, const int* __restri
   }
 }
 
-template <class T>
+// Loads of vectors a kernel may itself have written earlier (the cluster
+// tail re-reads level vectors across phases: plain loads after the cluster
+// barrier, which flushes L1; never the non-coherent path).  LdDef is the
+// launched kernels' plain dereference.
+struct LdDef { template <class U> __device__ __forceinline__ static U ld(const U* p) { return *p; } };
+struct LdCoh { template <class U> __device__ __forceinline__ static U ld(const U* p) { return __ldcg(p); } };
+
+template <class T, class LD = LdDef>
 __device__ __forceinline__ T row_apply(int r, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
                                        const int* __restrict__ mnb, const T* __restrict__ coef,
-                                       const T* __restrict__ diag, const T* __restrict__ x) {
+                                       const T* __restrict__ diag, const T* x) {
   const int s = r >> 5, lane = r & 31;
   const int len = ms_len[s], base = ms_ptr[s] + lane;
-  T acc = diag[r] * x[r];
+  T acc = diag[r] * LD::ld(&x[r]);
   int j = 0;
   for (; j + 4 <= len; j += 4) {
     T a[4];
@@ -449,11 +511,11 @@ __device__ __forceinline__ T row_apply(int r, const int* __restrict__ ms_ptr, co
     for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&mnb[base + 32 * (j + u)]); }
     T v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = x[c[u]];
+    for (int u = 0; u < 4; ++u) v[u] = LD::ld(&x[c[u]]);
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
   }
-  for (; j < len; ++j) acc += __ldg(&coef[base + 32 * j]) * x[__ldg(&mnb[base + 32 * j])];
+  for (; j < len; ++j) acc += __ldg(&coef[base + 32 * j]) * LD::ld(&x[__ldg(&mnb[base + 32 * j])]);
   return acc;
 }
 
@@ -461,14 +523,14 @@ __device__ __forceinline__ T row_apply(int r, const int* __restrict__ ms_ptr, co
 // r_i = b_i - (A x0)_i with x0 of the neighbours formed on the fly.  Loads in
 // batches of 4 entries (columns + coefficients, then the gathered b and 1/d1),
 // accumulation in entry order.
-template <class T>
+template <class T, class LD = LdDef>
 __device__ __forceinline__ void pre_resid_row(int i, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
                                               const int* __restrict__ mnb, const T* __restrict__ coef,
                                               const T* __restrict__ diag, const T* __restrict__ il1,
-                                              const T* __restrict__ b, T& x0, T& r) {
+                                              const T* b, T& x0, T& r) {
   const int s = i >> 5, lane = i & 31;
   const int len = ms_len[s], base = ms_ptr[s] + lane;
-  const T bi = b[i];
+  const T bi = LD::ld(&b[i]);
   const T xi = bi * il1[i];
   T acc = diag[i] * xi;
   int j = 0;
@@ -478,28 +540,28 @@ __device__ __forceinline__ void pre_resid_row(int i, const int* __restrict__ ms_
 #pragma unroll
     for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&mnb[base + 32 * (j + u)]); }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = b[c[u]] * il1[c[u]];
+    for (int u = 0; u < 4; ++u) v[u] = LD::ld(&b[c[u]]) * il1[c[u]];
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
   }
   for (; j < len; ++j) {
     const int c = __ldg(&mnb[base + 32 * j]);
-    acc += __ldg(&coef[base + 32 * j]) * (b[c] * il1[c]);
+    acc += __ldg(&coef[base + 32 * j]) * (LD::ld(&b[c]) * il1[c]);
   }
   x0 = xi;
   r = bi - acc;
 }
 // One row of the fused prolongation + post-smooth: t = x0 + w x_c[agg] (on
 // the fly for the row and its neighbours), returns t_i + (b - A t)_i / d1_i.
-template <class T>
+template <class T, class LD = LdDef>
 __device__ __forceinline__ T prolong_smooth_row(int i, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
                                                 const int* __restrict__ mnb, const T* __restrict__ coef,
                                                 const T* __restrict__ diag, const T* __restrict__ il1,
-                                                const int* __restrict__ agg, const T* __restrict__ xc, T w,
-                                                const T* __restrict__ x0, const T* __restrict__ b) {
+                                                const int* __restrict__ agg, const T* xc, T w,
+                                                const T* x0, const T* b) {
   const int s = i >> 5, lane = i & 31;
   const int len = ms_len[s], base = ms_ptr[s] + lane;
-  const T ti = x0[i] + w * xc[agg[i]];
+  const T ti = LD::ld(&x0[i]) + w * LD::ld(&xc[agg[i]]);
   T acc = diag[i] * ti;
   int j = 0;
   for (; j + 4 <= len; j += 4) {
@@ -508,17 +570,17 @@ __device__ __forceinline__ T prolong_smooth_row(int i, const int* __restrict__ m
 #pragma unroll
     for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&mnb[base + 32 * (j + u)]); }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { g[u] = agg[c[u]]; v[u] = x0[c[u]]; }
+    for (int u = 0; u < 4; ++u) { g[u] = agg[c[u]]; v[u] = LD::ld(&x0[c[u]]); }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = v[u] + w * xc[g[u]];
+    for (int u = 0; u < 4; ++u) v[u] = v[u] + w * LD::ld(&xc[g[u]]);
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
   }
   for (; j < len; ++j) {
     const int c = __ldg(&mnb[base + 32 * j]);
-    acc += __ldg(&coef[base + 32 * j]) * (x0[c] + w * xc[agg[c]]);
+    acc += __ldg(&coef[base + 32 * j]) * (LD::ld(&x0[c]) + w * LD::ld(&xc[agg[c]]));
   }
-  return ti + (b[i] - acc) * il1[i];
+  return ti + (LD::ld(&b[i]) - acc) * il1[i];
 }
 
 // x = b / d1 (pre-smoothing from a zero guess); b in the caller's type TB
@@ -602,6 +664,25 @@ __global__ void k_amg_smooth(int n, const int* __restrict__ ms_ptr, const int* _
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = (TO)(x[i] + ((P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x)) * il1[i]);
 }
+// level-0 post-smoother with the PCG's r.z folded in: z = t + (r - A t) / d1
+// and the deterministic grid sum of r_i z_i (fp64) driving control step `kind`
+template <class P, class T>
+__global__ void __launch_bounds__(kThreads) k_amg_smooth_dot(int n, const int* __restrict__ ms_ptr,
+    const int* __restrict__ ms_len, const int* __restrict__ mnb, const P* __restrict__ coef, const P* __restrict__ diag,
+    const P* __restrict__ il1, const P* __restrict__ x, const T* __restrict__ b, T* __restrict__ out, const int* done,
+    double* partials, unsigned* ticket, KCtl* ctl, Red red, int kind) {
+  if (*done) return;
+  double v[1] = {0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const T bi = b[i];
+    const T zi = (T)(x[i] + ((P)bi - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x)) * il1[i]);
+    out[i] = zi;
+    v[0] += (double)bi * (double)zi;
+  }
+  double t[1];
+  if (grid_sum<1>(v, partials, ticket, t)) red_finish<1>(red, kind, ctl, t);
+}
+
 // coarsest level: `sweeps` l1-Jacobi sweeps from zero, one block, in shared memory
 template <class P, class TB, class TO>
 __global__ void __launch_bounds__(1024) k_amg_coarse(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
@@ -679,6 +760,131 @@ __global__ void __launch_bounds__(1024) k_amg_dense(int n, const P* __restrict__
                                                     TO* __restrict__ x, const int* done) {
   if (*done) return;
   dense_solve_block<P, TB, TO>(n, Ai, b, x);
+}
+
+// ------------------------------------------------------------ cluster tail
+// The coarse levels below a few 1e5 rows are latency-bound: each launched
+// kernel moves well under a megabyte.  k_amg_tail runs the
+// whole coarse correction of level l0 (its first visit, and for the W-cycle
+// the residual, the second visit and the add) as ONE launch of one
+// thread-block cluster: every phase of the recursion (pre-smooth+residual,
+// restriction, dense coarsest solve, prolongation+post-smooth, W residual /
+// add) is a cluster-strided loop over the level's rows followed by a cluster
+// barrier (barrier.cluster arrive.release / wait.acquire; it also
+// invalidates L1, so the next phase's plain loads see the other CTAs'
+// writes).  The per-row arithmetic is the launched kernels' row functions,
+// so the result is bitwise that of the launched cycle.
+constexpr int kTailThreads = 512;
+
+__device__ __forceinline__ void tail_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <class P>
+__device__ void tail_cycle(const TailArgs<P>& A, int l, const P* b, P* x, int gt, int gs) {
+  const TailLevel<P>& F = A.L[l];
+  if (l == A.nlev - 1) {
+    if (A.ainv) {
+      // = dense_solve_block, rows over the cluster's warps
+      const int lane = gt & 31;
+      for (int i = gt >> 5; i < F.n; i += gs >> 5) {
+        P acc = P(0);
+        for (int j = lane; j < F.n; j += 32) acc += A.ainv[(size_t)i * F.n + j] * LdCoh::ld(&b[j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) x[i] = acc;
+      }
+      tail_sync();
+    } else {
+      // = k_amg_coarse: sweeps l1-Jacobi steps from zero, ping-pong x / t
+      // (start buffer chosen so the last step lands in x)
+      P* cur = ((A.sweeps - 1) % 2 == 0) ? x : F.t;
+      P* nxt = cur == x ? F.t : x;
+      for (int i = gt; i < F.n; i += gs) cur[i] = LdCoh::ld(&b[i]) * F.il1[i];
+      tail_sync();
+      for (int it = 1; it < A.sweeps; ++it) {
+        for (int i = gt; i < F.n; i += gs)
+          nxt[i] = LdCoh::ld(&cur[i]) +
+                   (LdCoh::ld(&b[i]) - row_apply<P, LdCoh>(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, cur)) * F.il1[i];
+        tail_sync();
+        P* tmp = cur; cur = nxt; nxt = tmp;
+      }
+    }
+    return;
+  }
+  const TailLevel<P>& C = A.L[l + 1];
+  for (int i = gt; i < F.n; i += gs) {
+    P xv, rv;
+    pre_resid_row<P, LdCoh>(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, xv, rv);
+    F.t[i] = xv;
+    F.r[i] = rv;
+  }
+  tail_sync();
+  for (int I = gt; I < C.n; I += gs) {
+    P sum = P(0);
+    for (int k = C.mem_ptr[I]; k < C.mem_ptr[I + 1]; ++k) sum += LdCoh::ld(&F.r[C.mem[k]]);
+    C.b[I] = sum;
+  }
+  tail_sync();
+  tail_cycle(A, l + 1, C.b, C.x, gt, gs);
+  if (A.wcycle && l + 1 < A.nlev - 1 && l + 1 <= A.wmax) {
+    for (int I = gt; I < C.n; I += gs)
+      C.r2[I] = LdCoh::ld(&C.b[I]) - row_apply<P, LdCoh>(I, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x);
+    tail_sync();
+    tail_cycle(A, l + 1, C.r2, C.e, gt, gs);
+    for (int I = gt; I < C.n; I += gs) C.x[I] = LdCoh::ld(&C.x[I]) + LdCoh::ld(&C.e[I]);
+    tail_sync();
+  }
+  for (int i = gt; i < F.n; i += gs)
+    x[i] = prolong_smooth_row<P, LdCoh>(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.agg, C.x, A.omega,
+                                        F.t, b);
+  tail_sync();
+}
+
+// the coarse correction of level l0 (its rhs L[l0].b restricted by the caller)
+template <class P>
+__global__ void __launch_bounds__(kTailThreads) k_amg_tail(const TailArgs<P>* __restrict__ Ap, int l0, const int* done) {
+  if (*done) return;     // uniform over the cluster (nothing in here writes done)
+  const TailArgs<P>& A = *Ap;
+  const int gs = gridDim.x * blockDim.x;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const TailLevel<P>& C = A.L[l0];
+  tail_cycle(A, l0, C.b, C.x, gt, gs);
+  if (A.wcycle && l0 < A.nlev - 1 && l0 <= A.wmax) {
+    for (int I = gt; I < C.n; I += gs)
+      C.r2[I] = LdCoh::ld(&C.b[I]) - row_apply<P, LdCoh>(I, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x);
+    tail_sync();
+    tail_cycle(A, l0, C.r2, C.e, gt, gs);
+    for (int I = gt; I < C.n; I += gs) C.x[I] = LdCoh::ld(&C.x[I]) + LdCoh::ld(&C.e[I]);
+  }
+}
+
+// launch of the tail as one cluster of A->tail_cs CTAs (falls back to the
+// portable size 8 if the non-portable 16 is refused)
+template <class P>
+static dfvm_status launch_tail(AmgH<P>* A, const int* done, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_amg_tail<P>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr_set = true;
+  }
+  for (;;) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)A->tail_cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)A->tail_cs);
+    cfg.blockDim = dim3(kTailThreads);
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_amg_tail<P>, (const TailArgs<P>*)A->d_tail, A->tail_l0, done);
+    if (e == cudaSuccess) return DFVM_OK;
+    cudaGetLastError();
+    if (A->tail_cs > 8) { A->tail_cs = 8; continue; }
+    return cuda_error(e, "cudaLaunchKernelEx(k_amg_tail)");
+  }
 }
 
 // ------------------------------------------------------------ host drivers
@@ -766,6 +972,38 @@ static void coarsest(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaS
   }
 }
 
+// algorithmic bytes of one tail launch: every matrix / vector pass the
+// launched kernels of the same sub-cycle would make (row metadata 4 B/row,
+// entries 4 + pb B, the vectors each pass touches), summed over the
+// recursion
+template <class P>
+static double tail_pass_bytes(const AmgH<P>* A, int l, bool& ok) {
+  const double pb = sizeof(P);
+  const AmgLevelDev<P>& F = A->L[l];
+  if (l == A->nlev - 1)
+    return A->ainv ? pb * (double)F.n * F.n + 2 * pb * F.n
+                   : A->prm.sweeps * ((4 + pb) * (double)F.nnz + 4 * pb * F.n);
+  const AmgLevelDev<P>& C = A->L[l + 1];
+  double b = 4 * (double)F.n + (4 + pb) * (double)F.nnz + 5 * pb * F.n;            // pre_resid
+  b += (4 + pb) * ((double)F.n + C.n);                                               // restrict
+  b += tail_pass_bytes(A, l + 1, ok);
+  if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax)
+    b += 4 * (double)C.n + (4 + pb) * (double)C.nnz + 4 * pb * C.n + tail_pass_bytes(A, l + 1, ok) + 3 * pb * C.n;
+  b += 4 * (double)F.n + (4 + pb) * (double)F.nnz + (4 + 5 * pb) * F.n + pb * C.n;  // prolong_smooth
+  return b;
+}
+template <class P>
+static double tail_bytes(const AmgH<P>* A) {
+  bool ok = true;
+  const int l = A->tail_l0;
+  const double pb = sizeof(P);
+  const AmgLevelDev<P>& C = A->L[l];
+  double b = tail_pass_bytes(A, l, ok);
+  if (A->prm.wcycle && l < A->nlev - 1 && l <= A->prm.wmax)
+    b += 4 * (double)C.n + (4 + pb) * (double)C.nnz + 4 * pb * C.n + tail_pass_bytes(A, l, ok) + 3 * pb * C.n;
+  return b;
+}
+
 // Coarse level l >= 1 (no ghost columns): x = M_l^-1 b from a zero guess with
 // the fused kernels (launches dominate there): pre-smooth + residual,
 // restriction, coarse correction (twice for the W-cycle: the second visit
@@ -788,6 +1026,10 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
   PLAUNCH(pr, "k_amg_restrict", l, (4 + pb) * (n + nc), s,
           (k_amg_restrict<P><<<gC, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
   *nl += 2;
+  if (l + 1 == A->tail_l0) {
+    PLAUNCH(pr, "k_amg_tail", l + 1, tail_bytes(A), s, launch_tail(A, done, s));
+    ++*nl;
+  } else {
   cycle_coarse(A, l + 1, C.b, C.x, done, s, nl);
   if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax) {
     PLAUNCH(pr, "k_amg_resid", l + 1, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
@@ -796,6 +1038,7 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
     cycle_coarse(A, l + 1, C.r2, C.e, done, s, nl);
     PLAUNCH(pr, "k_amg_add", l + 1, 3 * pb * nc, s, (k_amg_add<P><<<gC, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
     *nl += 2;
+  }
   }
   PLAUNCH(pr, "k_amg_prolong_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + (4 + 5 * pb) * n + pb * nc, s,
           (k_amg_prolong_smooth<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1,
@@ -809,7 +1052,9 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
 // re-gather b/d1 (x0/agg/xc) per neighbour and ran 20 % slower per iteration
 // at 50 M rows), and must with several ranks (x0 and t need a halo exchange).
 template <class P, class T>
-static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl, cudaEvent_t* ev) {
+static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl, cudaEvent_t* ev,
+                          const KDot* dot, bool pre_done, bool* dot_done) {
+  if (dot_done) *dot_done = false;
   AmgLevelDev<P>& F = A->L[0];
   Prof* pr = A->prof;
   const bool f64 = std::is_same<P, double>::value;
@@ -837,8 +1082,11 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   AmgLevelDev<P>& C = A->L[1];
   const double nc = C.n;
   const int g0 = grid_for(F.n), g1 = grid_for(C.n);
-  PLAUNCH(pr, "k_amg_pre", 0, (vb + 2 * pb) * n, s,
-          (k_amg_pre<P, T, P><<<g0, kThreads, 0, s>>>(F.n, r, F.il1, F.x, done)));
+  if (!pre_done) {
+    PLAUNCH(pr, "k_amg_pre", 0, (vb + 2 * pb) * n, s,
+            (k_amg_pre<P, T, P><<<g0, kThreads, 0, s>>>(F.n, r, F.il1, F.x, done)));
+    ++*nl;
+  }
   if ((e = halo_exchange_p(A->m, F.x, 1, f64, s))) return e;
   if (ev) record_event(ev[0], s);
   PLAUNCH(pr, "k_amg_resid", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + vb) * n, s,
@@ -847,7 +1095,11 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   if (ev) record_event(ev[1], s);
   PLAUNCH(pr, "k_amg_restrict", 0, (4 + pb) * (n + nc), s,
           (k_amg_restrict<P><<<g1, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
-  *nl += 3;
+  *nl += 2;
+  if (A->tail_l0 == 1) {
+    PLAUNCH(pr, "k_amg_tail", 1, tail_bytes(A), s, launch_tail(A, done, s));
+    ++*nl;
+  } else {
   cycle_coarse(A, 1, C.b, C.x, done, s, nl);
   if (A->prm.wcycle && 1 < A->nlev - 1 && 1 <= A->prm.wmax) {
     PLAUNCH(pr, "k_amg_resid", 1, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
@@ -857,13 +1109,22 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
     PLAUNCH(pr, "k_amg_add", 1, 3 * pb * nc, s, (k_amg_add<P><<<g1, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
     *nl += 2;
   }
+  }
   PLAUNCH(pr, "k_amg_prolong", 0, (4 + 2 * pb) * n + pb * nc, s,
           (k_amg_prolong<P><<<g0, kThreads, 0, s>>>(F.n, F.agg, C.x, F.x, F.t, (P)A->prm.omega, done)));
   if ((e = halo_exchange_p(A->m, F.t, 1, f64, s))) return e;
   if (ev) record_event(ev[2], s);
-  PLAUNCH(pr, "k_amg_smooth", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + 2 * vb) * n, s,
-          (k_amg_smooth<P, T, T><<<g0, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.t, r,
-                                                         z, done)));
+  if (dot) {
+    PLAUNCH(pr, "k_amg_smooth_dot", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + 2 * vb) * n, s,
+            (k_amg_smooth_dot<P, T><<<g0, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1,
+                                                            F.t, r, z, done, dot->partials, dot->ticket, dot->ctl,
+                                                            dot->red, dot->kind)));
+    if (dot_done) *dot_done = true;
+  } else {
+    PLAUNCH(pr, "k_amg_smooth", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + 2 * vb) * n, s,
+            (k_amg_smooth<P, T, T><<<g0, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.t,
+                                                           r, z, done)));
+  }
   if (ev) record_event(ev[3], s);
   *nl += 2;
   return DFVM_OK;
@@ -872,13 +1133,20 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
 // z = M^-1 r; skipped on the device when *done is set
 template <class T>
 dfvm_status amg_apply(Amg<T>* A, const T* r, T* z, const int* done, cudaStream_t s, int* nl, cudaEvent_t* ev,
-                      Prof* prof) {
+                      Prof* prof, const KDot* dot, bool pre_done, bool* dot_done) {
   dfvm_status e;
-  if (A->same) { A->same->prof = prof; e = cycle0<T, T>(A->same, r, z, done, s, nl, ev); }
-  else { A->lo->prof = prof; e = cycle0<float, T>(A->lo, r, z, done, s, nl, ev); }
+  if (A->same) { A->same->prof = prof; e = cycle0<T, T>(A->same, r, z, done, s, nl, ev, dot, pre_done, dot_done); }
+  else { A->lo->prof = prof; e = cycle0<float, T>(A->lo, r, z, done, s, nl, ev, dot, pre_done, dot_done); }
   if (e) return e;
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
+}
+
+template <class T>
+void amg_level0_pre(Amg<T>* A, void** x0, const void** il1, int* p_bytes) {
+  *x0 = nullptr; *il1 = nullptr; *p_bytes = 0;
+  if (A->same && A->same->nlev > 1) { *x0 = A->same->L[0].x; *il1 = A->same->L[0].il1; *p_bytes = sizeof(T); }
+  if (A->lo && A->lo->nlev > 1) { *x0 = A->lo->L[0].x; *il1 = A->lo->L[0].il1; *p_bytes = 4; }
 }
 
 template <class T>
@@ -893,7 +1161,9 @@ int amg_level_nnz(const Amg<T>* A, int64_t* nnz) {
   template void amg_destroy<T>(Amg<T>*);                                                  \
   template int amg_levels<T>(const Amg<T>*, int*);                                        \
   template dfvm_status amg_update<T>(Amg<T>*, const T*, const T*, cudaStream_t, int*, Prof*); \
-  template dfvm_status amg_apply<T>(Amg<T>*, const T*, T*, const int*, cudaStream_t, int*, cudaEvent_t*, Prof*); \
+  template dfvm_status amg_apply<T>(Amg<T>*, const T*, T*, const int*, cudaStream_t, int*, cudaEvent_t*, Prof*,     \
+                                    const KDot*, bool, bool*);                                                   \
+  template void amg_level0_pre<T>(Amg<T>*, void**, const void**, int*);                                          \
   template int amg_level_nnz<T>(const Amg<T>*, int64_t*);
 INST(double)
 INST(float)

@@ -2,6 +2,7 @@
 // warp-per-SELL-slice iteration, deterministic two-level reductions.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 #include <cuda_runtime.h>
@@ -14,13 +15,27 @@ constexpr int kThreads = 256;          // 8 warps per block
 constexpr int kWarpsPerBlock = kThreads / 32;
 constexpr int kMaxBlocks = 148 * 8;    // one full wave of 256-thread blocks on 148 SMs
 
+// Debug / coverage knob DFVM_MAX_BLOCKS=k (read once): caps every
+// grid-stride launch at k blocks, so small parity meshes exercise the
+// multi-slice-per-warp loops (and their next-slice prefetch) that only the
+// full-size meshes reach otherwise.  Unset (default): no cap beyond one wave.
+inline int grid_cap() {
+  static const int cap = [] {
+    const char* e = getenv("DFVM_MAX_BLOCKS");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : kMaxBlocks;
+  }();
+  return cap;
+}
 inline int grid_for_slices(int n_slices) {
   int b = (n_slices + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  return b < 1 ? 1 : (b > kMaxBlocks ? kMaxBlocks : b);
+  const int mx = kMaxBlocks < grid_cap() ? kMaxBlocks : grid_cap();
+  return b < 1 ? 1 : (b > mx ? mx : b);
 }
 inline int grid_for(int64_t n) {
   int64_t b = (n + kThreads - 1) / kThreads;
-  return (int)(b < 1 ? 1 : (b > kMaxBlocks ? kMaxBlocks : b));
+  const int mx = kMaxBlocks < grid_cap() ? kMaxBlocks : grid_cap();
+  return (int)(b < 1 ? 1 : (b > mx ? mx : b));
 }
 
 // Resident-block cap of a kernel: (blocks per SM from the occupancy API) x
@@ -38,7 +53,8 @@ inline int occ_cap(const void* fn) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, 0) != cudaSuccess || b < 1) b = 1;
-  const int cap = b * nsm < kMaxBlocks ? b * nsm : kMaxBlocks;
+  int cap = b * nsm < kMaxBlocks ? b * nsm : kMaxBlocks;
+  if (cap > grid_cap()) cap = grid_cap();
   cache[fn] = cap;
   return cap;
 }

@@ -128,6 +128,18 @@ def box(nx, ny, nz, lx=1.0, ly=1.0, lz=1.0, split=0, patch_mode=0, jitter=0.0,
     return m
 
 
+def sheared_box(nx=6, ny=5, nz=3, alpha=25.0, scramble=6) -> RawMesh:
+    """Hex box [0,1]^3 mapped by (x, y, z) -> (x, y + alpha x, z): every cell a
+    congruent parallelepiped, x- and y-faces at arctan(alpha) to their centroid
+    links (alpha = 25: 87.7 deg, beyond the 87.1 deg at which the over-relaxed
+    coefficient is clamped, A-4).  Data only: a point transform."""
+    m = box(nx, ny, nz, 1.0, 1.0, 1.0, split=0, scramble=scramble)
+    m.points = np.array(m.points, np.float64, copy=True)
+    m.points[:, 1] += alpha * m.points[:, 0]
+    m.meta = dict(m.meta, kind="sheared_box", alpha=alpha)
+    return m
+
+
 def cavity(n=20, scramble=11) -> RawMesh:
     """C1: OpenFOAM cavity tutorial mesh, 0.1 x 0.1 x 0.01 m, n x n x 1 hex
     (reading A-31): movingWall (top), fixedWalls, and

@@ -41,6 +41,7 @@ MESHES = {
     "cylinder_poly": lambda: synth.cylinder_poly(6e3, scramble=13),     # C3 family: polygon prisms, F/N ~ 3
     "square_tri": lambda: synth.square_tri(12, jitter=0.2),             # NEXT-1 domain: triangle prisms
     "htree_tet": lambda: synth.htree(target_cells=2e4, scramble=14),    # C4 family: voxel tree, 5-tet
+    "sheared_clamp": lambda: synth.sheared_box(6, 5, 3, 25.0),           # > 87 deg faces: A-4 clamp active
 }
 
 

@@ -135,6 +135,21 @@ def test_piso_partitioned_matches_single(P, wk, precond):
     for r in range(P):
         st[r][2].get(sp[r], out=U); st[r][3].get(sp[r], out=p); st[r][4].get(sp[r], out=phi)
     assert rel_l2(U, refU) <= 1e-10 and rel_l2(p[:, 0], refp) <= 1e-10 and rel_l2(phi[:, 0], refphi) <= 1e-10
+    # and the partitioned path against the oracle itself (SURVEY §8(c) converged-field bound)
+    bo = oracle.BCs(mo)
+    for pn, f, k, kw2 in PIPE_BCS:
+        bo.set(pn, f, k, **kw2)
+    if not wk:
+        bo.set("outlet", "p", oracle.BC_FIXED, 0.0)
+    So = oracle.Solver(mo, bo, **{k: v for k, v in kw.items() if k != "p_precond"})
+    if wk:
+        So.windkessel_set("outlet", *wkargs)
+    Uo, po, fo = U0.copy(), np.zeros(mo.N), phi0.copy()
+    for _ in range(3):
+        ro = So.step(Uo, po, fo)
+    assert rel_l2(U, Uo) <= 1e-8 and rel_l2(p[:, 0], po) <= 1e-8 and rel_l2(phi[:, 0], fo) <= 1e-8
+    if wk:
+        assert np.allclose(reps[0]["Q"], ro["Q"], rtol=1e-8) and np.allclose(reps[0]["p_o"], ro["p_o"], rtol=1e-8)
     # every rank took the same Krylov decisions and sees the same global reports
     for r in range(1, P):
         assert [x["it"] for x in reps[r]["p"]] == [x["it"] for x in reps[0]["p"]]

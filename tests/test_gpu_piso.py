@@ -357,3 +357,93 @@ def test_live_timing_does_not_change_the_step(graphs, monkeypatch):
     assert out[0][3] == out[1][3] and min(out[0][3]) > 0
     for a, b in zip(out[0][:3], out[1][:3]):
         assert np.array_equal(a, b)
+
+
+def test_profile_mode_does_not_change_the_step():
+    # dfvm_solver_profile brackets every launch with events (and captures each
+    # AMG-PCG chunk afresh): fields and iteration counts bitwise those of an
+    # unprofiled step; the table books bytes per kernel and AMG level
+    import ctypes
+    import torch
+    raw, mo, mg, bo, bg, kw = pipe_case(n=8, m_r=4, n_z=40)
+    U0, p0, phi0 = initial_state(mo)
+    s = torch.cuda.Stream()
+    sp = ctypes.c_void_p(s.cuda_stream)
+    out = []
+    for prof in (False, True):
+        Sg = dfvm.Solver(mg, bg, p_precond="amg32", **kw, **TIGHT)
+        Sg.profile(prof)
+        Ug, pg, phig = mg.field("cells", 3, U0, sp), mg.field("cells", 1, p0, sp), mg.field("flux", 1, phi0, sp)
+        reps = [Sg.step(Ug, pg, phig, sp) for _ in range(2)]
+        out.append((Ug.get(sp), pg.get(sp), phig.get(sp), [r["it"] for rep in reps for r in rep["p"]]))
+        if prof:
+            rows = {(r["name"], r["level"]): r for r in Sg.profile_table()}
+            assert rows[("k_cg_spmv", -1)]["launches"] == sum(out[-1][3])
+            assert rows[("k_amg_resid", 0)]["alg_bytes"] > 0 and rows[("k_bi_t", -1)]["ms"] > 0
+            assert any(k[0].startswith("k_amg_prolong_smooth") and k[1] >= 1 for k in rows)
+    assert out[0][3] == out[1][3]
+    for a, b in zip(out[0][:3], out[1][:3]):
+        assert np.array_equal(a, b)
+
+
+def test_c1_cavity_100_steps_trajectory():
+    # SURVEY §8(c) "Multi-step trajectories: C1 100 steps <= 1e-8" (Re = 10 is
+    # strongly damped): the whole t = 0.5 trajectory of the A-31 cavity, oracle
+    # and CUDA path at parity tolerance, compared every 10 steps, plus the
+    # printed regression values of the survey's independent prototype at t = 0.5
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cavity_c1.json")))
+    raw, mo, mg, bo, bg, kw = cavity_case(scramble=0)
+    So = oracle.Solver(mo, bo, **kw, **TIGHT)
+    Sg = dfvm.Solver(mg, bg, **kw, **TIGHT)
+    U, p, phi = np.zeros((mo.N, 3)), np.zeros(mo.N), np.zeros(mo.NF)
+    Ug, pg, phig = mg.field("cells", 3), mg.field("cells", 1), mg.field("flux", 1)
+    for n in range(1, 101):
+        So.step(U, p, phi)
+        r = Sg.step(Ug, pg, phig)
+        assert r["cont_err_max"] <= 1e-13
+        if n % 10 == 0:
+            assert rel_l2(Ug.get(), U) <= 1e-8 and rel_l2(pg.get(), p) <= 1e-8 and rel_l2(phig.get(), phi) <= 1e-8, n
+    Uh, ph = Ug.get(), pg.get()
+    t05 = g["step100"]
+    assert abs(np.abs(Uh[:, 0]).max() - t05["max_abs_Ux"]) <= 1e-9
+    assert abs(np.abs(Uh[:, 1]).max() - t05["max_abs_Uy"]) <= 1e-9
+    assert abs(ph.min() - t05["p_min"]) <= 5e-9 and abs(ph.max() - t05["p_max"]) <= 5e-9
+    assert abs(np.abs(Uh).sum() - t05["sum_abs_U"]) <= 1e-7
+
+
+@pytest.mark.parametrize("precond", ["amg", "amg32"])
+@pytest.mark.parametrize("size", ["pipe_big", "c5_nz6"])
+def test_amg_cluster_tail_bitwise(precond, size, monkeypatch):
+    # the coarse levels below DFVM_AMG_TAIL rows run as one thread-block
+    # cluster kernel per visit (k_amg_tail); it must reproduce the launched
+    # W-cycle bit for bit (same row arithmetic, same order), hence identical
+    # fields and iteration counts
+    import ctypes
+    import torch
+    import cases
+    if size == "pipe_big":
+        raw, mo, mg, bo, bg, kw = pipe_case(n=8, m_r=4, n_z=40)
+        U0, p0, phi0 = initial_state(mo)
+        mk = lambda: dfvm.Solver(mg, bg, p_precond=precond, **kw, **TIGHT)
+    else:
+        case = cases.c5(n_z=6)
+        mg = dfvm.Mesh(case.raw)
+        geo = mg.export_geometry()
+        U0, p0, phi0 = case.initial_state(geo["xc"], geo["xf"], geo["Sf"])
+        bg = case.apply_bcs(dfvm.BCs(mg))
+        mk = lambda: dfvm.Solver(mg, bg, **dict(case.solver, p_precond=precond))
+    s = torch.cuda.Stream()
+    sp = ctypes.c_void_p(s.cuda_stream)
+    out = []
+    for tail in ("0", "100000", "5000"):
+        monkeypatch.setenv("DFVM_AMG_TAIL", tail)
+        Sg = mk()
+        Ug, pg, phig = mg.field("cells", 3, U0, sp), mg.field("cells", 1, p0, sp), mg.field("flux", 1, phi0, sp)
+        reps = [Sg.step(Ug, pg, phig, sp) for _ in range(2)]
+        out.append((Ug.get(sp), pg.get(sp), phig.get(sp), [r["it"] for rep in reps for r in rep["p"]]))
+        assert len(Sg.amg_levels()) >= 3
+    for o in out[1:]:
+        assert o[3] == out[0][3]
+        for a, b in zip(out[0][:3], o[:3]):
+            assert np.array_equal(a, b)

@@ -161,3 +161,21 @@ def test_interpolation_weight_on_segment_matches_euclidean():
     d0 = np.linalg.norm(m.xf[:m.F] - m.xc[m.owner[:m.F]], axis=1)
     d1 = np.linalg.norm(m.xc[m.neighbour] - m.xf[:m.F], axis=1)
     assert np.allclose(m.w, d1 / (d0 + d1), atol=1e-15)
+
+
+def test_overrelaxed_clamp_on_extreme_faces():
+    """A-4: on faces beyond ~87.1 deg the over-relaxed denominator S^.d is
+    clamped at 0.05 |d|, delta = |S| / (0.05 |d|), and every clamped face is
+    counted.  Sheared lattice (x, y + 25 x, z), h = 1/6 in x: x-faces have
+    S = (A, 0, 0), A = h_y h_z, d = (h, 25 h, 0), S^.d = h < 0.05 |d| = 0.05 h sqrt(626)."""
+    raw = synth.sheared_box(6, 5, 3, 25.0, scramble=0)
+    m = oracle.Mesh(raw, "overrelaxed")
+    # x-faces (5*5*3) and y-faces (6*4*3, normal ~ (-25, 1, 0) against d = (0, h_y, 0))
+    # are clamped; the z-faces (6*5*2) are orthogonal
+    assert m.F == 75 + 72 + 60 and m.n_clamped == 75 + 72
+    hx, hy, hz = 1 / 6, 1 / 5, 1 / 3
+    d = m.xc[m.neighbour] - m.xc[m.owner[:m.F]]
+    xf = np.abs(d[:, 0]) > 0.5 * hx
+    A = hy * hz
+    assert np.allclose(m.delta[xf], A / (0.05 * hx * math.sqrt(626.0)), rtol=1e-13)
+    assert np.allclose(np.linalg.norm(m.Sf[:m.F][xf], axis=1), A, rtol=1e-13)
