@@ -321,7 +321,6 @@ def main():
     barrier()
     torch.cuda.synchronize()
     clocks = Clocks(local)
-    S.set_timing(True)
     l0 = dfvm.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -335,8 +334,6 @@ def main():
     barrier()
     clk = clocks.stop()
     launches = dfvm.kernel_launches() - l0
-    tim = S.timing()
-    S.set_timing(False)
     ms = max_over_ranks(e0.elapsed_time(e1))
     N = info["n_cells"]
     value = N * args.steps / (ms / 1000.0)
@@ -362,49 +359,14 @@ def main():
         e2e = {"value": N * args.steps / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e / args.steps}
 
-    # ---------------- roofline of the dominant kernel
-    # Candidates timed live inside the library (CUDA events on the launching
-    # stream): the PCG SpMV and, with AMG, the two level-0 V-cycle SpMV
-    # kernels (residual, post-smoother).  The one with the largest total time in the timed region is
-    # reported.  Algorithmic bytes per launch (N owned cells,
-    # F internal faces, 2F incidences of (column 4 B + coefficient vb), row
-    # metadata counted as 4 B/row, gathered values counted once):
+    # ---------------- roofline: the kernel with the largest live share of
+    # the step (from the per-kernel profile pass below)
     hbm, peak_src = peaks()
-    n_own, F_l = info["n_owned"], info["n_local_internal_faces"]
-    vb, ib = (8, 4) if args.precision == "f64" else (4, 4)
+    n_own = info["n_owned"]
     lv = S.amg_levels(nnz=True) if args.precond != "jacobi" else []
-    pb = 4 if args.precond == "amg32" else vb       # AMG hierarchy element bytes
-    cands = {
-        "k_cg_spmv (PCG SpMV + p.q partials)":
-            (tim["spmv_ms"], tim["spmv_n"], 4 * n_own + 2 * F_l * (ib + vb) + 3 * vb * n_own),          # diag, p, q
-        "k_amg_resid (AMG level-0 residual: r = b - A x)":
-            (tim["amg_pre_ms"], tim["amg_pre_n"],
-             4 * n_own + 2 * F_l * (ib + pb) + (3 * pb + vb) * n_own),                                # x, diag, r; b
-        "k_amg_smooth (AMG level-0 post-smoother: z = t + (b - A t)/d1)":
-            (tim["amg_post_ms"], tim["amg_post_n"],
-             4 * n_own + 2 * F_l * (ib + pb) + (3 * pb + 2 * vb) * n_own),                            # t, diag, d1; b, z
-    }
-    kname, (kms, kn, alg) = max(cands.items(), key=lambda kv: kv[1][0])
-    launch_ms = kms / max(kn, 1)
-    achieved = alg / (launch_ms / 1000.0) / 1e9 if (kn and kms > 0) else None
-    traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tfile):
-        try:
-            kk = kname.split()[0]
-            pc = f"_{args.precond}" if kk.startswith("k_amg") else ""
-            traffic = json.load(open(tfile)).get(f"{kk}_{args.config}_{args.precision}{pc}_{n_own}")
-        except Exception:
-            traffic = None
-    roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "peak_source": peak_src,
-            "unit": "GB/s", "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-            "alg_bytes_per_launch": alg, "launch_ms": launch_ms, "launches": kn,
-            "share_of_step": (kms / ms) if ms else None,
-            "candidates": {k.split()[0]: {"ms_total": v[0], "launches": v[1], "alg_bytes": v[2],
-                                          "GBps": (v[2] * v[1] / (v[0] / 1000.0) / 1e9) if (v[1] and v[0] > 0) else None}
-                           for k, v in cands.items()},
-            "pcg_iteration_ms": tim["cg_iter_ms"] / max(tim["cg_iter_n"], 1),
-            "pcg_share_of_step": tim["cg_iter_ms"] / ms if ms else None, "amg_levels": lv}
+    roof = {"bound": "hbm", "kernel": None, "achieved": None, "peak": hbm, "peak_source": peak_src, "unit": "GB/s",
+            "frac": None, "traffic": None, "amg_levels": lv}
 
     # ---------------- per-kernel profile: the same K steps replayed from the
     # same start state with every launch bracketed by CUDA events on the
@@ -435,7 +397,16 @@ def main():
                           "alg_bytes_per_launch": per, "GBps": gbs, "frac": (gbs / hbm) if gbs else None})
         big = [t for t in table if t["alg_bytes_per_launch"] > 0]
         dom = big[0] if big else None
+        cyc = {"k_cg_init", "k_cg_p2", "k_cg_spmv", "k_cg_r2x", "k_cg_r2", "k_cg_dot", "k_cg_final", "k_cg_p", "k_cg_r",
+               "k_amg_pre", "k_amg_resid", "k_amg_restrict", "k_amg_prolong", "k_amg_smooth", "k_amg_smooth_dot",
+               "k_amg_pre_resid", "k_amg_prolong_smooth", "k_amg_add", "k_amg_dense", "k_amg_coarse", "k_amg_tail"}
+        n_it = sum(r["launches"] for r in rows if r["name"] == "k_cg_spmv")
+        pcg_ms = sum(r["ms"] for r in rows if r["name"] in cyc)
         kern = {"profiled_ms_per_step": ms_prof / args.steps, "kernel_ms_per_step": tot / args.steps,
+                "pcg_ms_per_iteration": pcg_ms / n_it if n_it else None,
+                "pcg_iteration_note": "all PCG + AMG-cycle kernel time of the solves (incl. each solve's initial "
+                                      "residual and preconditioner application) / PCG iterations",
+                "pcg_share_of_step": pcg_ms / ms_prof if ms_prof else None,
                 "coverage": tot / ms_prof if ms_prof else None,
                 "coverage_rows_ge_2pct": sum(t["share"] for t in table if t["share"] and t["share"] >= 0.02),
                 "rows": table}
@@ -447,14 +418,13 @@ def main():
                     traffic = json.load(open(tfile)).get(f"{kk}_{args.config}_{args.precision}_{args.precond}_{n_own}")
                 except Exception:
                     traffic = None
-            roof_timed = roof
             roof = {"bound": "hbm", "kernel": kk, "achieved": dom["GBps"], "peak": hbm, "peak_source": peak_src,
                     "unit": "GB/s", "frac": dom["frac"], "traffic": traffic,
                     "alg_bytes_per_launch": dom["alg_bytes_per_launch"],
                     "launch_ms": dom["ms_per_step"] / dom["launches_per_step"] if dom["launches_per_step"] else None,
                     "launches_per_step": dom["launches_per_step"], "share_of_step": dom["share"],
                     "source": "largest live share of the profiled replay of the timed steps (kernels.rows)",
-                    "timed_region": roof_timed}
+                    "amg_levels": lv}
 
     ops = None if args.no_operators else operator_bench(dfvm, torch, mesh, case, info, stream, sp, hbm, args,
                                                          max_over_ranks, barrier)

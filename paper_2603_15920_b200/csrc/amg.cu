@@ -77,7 +77,11 @@ constexpr int kMaxLevels = 16;
 //                    visit of the level above: a thread-block cluster that
 //                    walks the whole sub-cycle with cluster barriers
 //                    (k_amg_tail; bitwise identical to the launched
-//                    kernels); 0: launched kernels            default 100000
+//                    kernels); 0: launched kernels            default 0
+//                    (C5, round 2: a tail from the 78,802-row level 3 took
+//                    0.67 ms per visit against ~0.2 ms launched — 16 SMs
+//                    cannot hide the gather latency of 5e4+ rows; only
+//                    levels of a few thousand rows gain)
 //   DFVM_AMG_TAIL_CLUSTER  CTAs of the tail cluster (16: non-portable size)
 //                                                             default 16
 //   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
@@ -86,7 +90,7 @@ constexpr int kMaxLevels = 16;
 //                    DFVM_AMG_SWEEPS l1-Jacobi sweeps (0: always sweeps)  default 512
 struct AmgParams {
   int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, sigma = 0;
-  int tail = 100000, tail_cluster = 16;
+  int tail = 0, tail_cluster = 16;
   bool wcycle = true;
   double omega = 1.9;   // C5 amg32: 362 ms, 11.6 it/solve (1.8: 369 ms, 12.2; 1.7: 380 ms)
   AmgParams() {

@@ -968,15 +968,23 @@ struct SolverT : SolverBase {
   int* d_wk_ptr = nullptr;
   int* d_wk_faces = nullptr;
   bool assembled = false;
-  // CUDA graphs of the AMG-PCG chunk (one per (x, b, timing) in use)
-  struct ChunkGraph { const void* x; const void* b; bool timing; cudaGraphExec_t exec; int launches; };
-  std::vector<ChunkGraph> graphs;
-  bool graphs_off = false;
+  // device-resident Krylov solves: one CUDA graph per (solver kind, x, b):
+  // prologue, a conditional WHILE node whose body is one iteration (the last
+  // body kernel sets the condition from the control block), epilogue
+  struct LoopGraph { int kind; const void* x; const void* b; cudaGraphExec_t exec; int nl_fixed, nl_body; };
+  std::vector<LoopGraph> loops;
+  bool loops_off = false;
+  // reports of device-resident solves, read back at the next stream sync
+  static constexpr int kSlots = 48;
+  KCtl* h_slots = nullptr;           // pinned [kSlots][3]
+  struct Pending { int slot, nctl; dfvm_solve_report* rep; int nl_fixed, nl_body; };
+  std::vector<Pending> pending;
   T* Uold = nullptr;     // start-of-step U and phi (ddtCorr, A-42; allocated on first use)
   T* phiold = nullptr;
   ~SolverT() override {
     cudaDeviceSynchronize();
-    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    for (auto& g : loops) cudaGraphExecDestroy(g.exec);
+    if (h_slots) cudaFreeHost(h_slots);
     if (amg) amg_destroy<T>(amg);
     for (void* p : allocs) dev_free(p, nullptr);
     dev_free(d_wk, nullptr);
@@ -1032,6 +1040,7 @@ struct SolverT : SolverBase {
         (st = al(&d_cont, 8)) || (st = al(&red_local, 128)) || (st = al(&red_all, (size_t)128 * mm->part.P)))
       return st;
     DFVM_CUDA(cudaMallocHost(&h_ctl, 4 * sizeof(KCtl)));
+    DFVM_CUDA(cudaMallocHost(&h_slots, (size_t)kSlots * 3 * sizeof(KCtl)));
     DFVM_CUDA(cudaMallocHost(&h_cont, 4 * sizeof(double)));
     DFVM_CUDA(cudaStreamSynchronize(nullptr));   // zero-fills complete before any use on the caller's stream
     return DFVM_OK;
@@ -1140,11 +1149,195 @@ static dfvm_status fin(dfvm_solver* S, SolverT<T>& X, int kind, int nv, cudaStre
   return DFVM_OK;
 }
 
+// ---------------------------------------------------------------- solves
+// Each Krylov solve is a prologue (initial residual, first preconditioner
+// application), an iteration body and an epilogue (the deferred last x
+// update, x = 0 for b = 0).  Two drivers run them:
+//  * device-resident (one rank, a non-legacy stream, no profiling): the solve
+//    is ONE CUDA graph — prologue, a conditional WHILE node whose body is one
+//    iteration ending in k_loop_cond (continue while the control block is not
+//    done), epilogue — captured on first use per (kind, x, b) and replayed;
+//    no host synchronisation and no launch after convergence.  The control
+//    block is copied to a pinned report slot and read at the next stream
+//    synchronisation (the end of the step, or of the standalone call);
+//  * host-chunked (several ranks with host-side transports, the legacy
+//    stream, profiling, DFVM_GRAPHS=0): kChunk iterations enqueued per host
+//    round trip, every kernel exiting early on the done flag.
+enum LoopKind { LOOP_CG = 0, LOOP_CG_AMG = 1, LOOP_BICGSTAB = 2 };
+
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const KCtl* ctl, int nc) {
+  int go = 0;
+  for (int k = 0; k < nc; ++k) go |= !ctl[k].done;
+  cudaGraphSetConditional(h, go ? 1u : 0u);
+}
+
+template <class T>
+__global__ void k_zero_if(int n, int nc, T* __restrict__ x, const KCtl* ctl) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int k = 0; k < nc; ++k)
+      if (ctl[k].zero_x) x[(int64_t)nc * i + k] = T(0);
+}
+
+template <class T>
+static bool use_device_loops(dfvm_solver* S, SolverT<T>& X, cudaStream_t st) {
+  if (X.loops_off) return false;
+  const char* g = getenv("DFVM_GRAPHS");
+  if (g && g[0] == '0') { X.loops_off = true; return false; }
+  return S->m->part.P == 1 && st != nullptr && !S->pr() && !S->timing;
+}
+
+template <class T, class Pro, class Body, class Epi>
+static dfvm_status device_loop(dfvm_solver* S, SolverT<T>& X, int kind, const void* x, const void* b, int nctl,
+                               dfvm_solve_report* rep, cudaStream_t st, Pro pro, Body body, Epi epi) {
+  typename SolverT<T>::LoopGraph* L = nullptr;
+  for (auto& g : X.loops)
+    if (g.kind == kind && g.x == x && g.b == b) L = &g;
+  if (!L) {
+    cudaGraph_t g = nullptr, bg = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    cudaGraphConditionalHandle h;
+    int nl = 0, nb = 0;
+    DFVM_CUDA(cudaGraphCreate(&g, 0));
+    DFVM_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    DFVM_CUDA(cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    dfvm_status ce = pro(&nl);
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    cudaGraph_t cg = nullptr;
+    cudaGraphNode_t cn = nullptr;
+    cudaError_t err = cudaStreamGetCaptureInfo(st, &cs, nullptr, &cg, &deps, &nd);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    if (err == cudaSuccess) err = cudaGraphAddNode(&cn, g, deps, nd, &cp);
+    if (err == cudaSuccess) err = cudaStreamUpdateCaptureDependencies(st, &cn, 1, cudaStreamSetCaptureDependencies);
+    if (err == cudaSuccess && !ce) ce = epi(&nl);
+    cudaError_t e2 = cudaStreamEndCapture(st, &g);
+    if (err == cudaSuccess) err = e2;
+    if (err == cudaSuccess && !ce) {
+      bg = cp.conditional.phGraph_out[0];
+      err = cudaStreamBeginCaptureToGraph(st, bg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+      if (err == cudaSuccess) {
+        ce = body(&nb);
+        k_loop_cond<<<1, 1, 0, st>>>(h, X.d_ctl, nctl);
+        ++nb;
+        e2 = cudaStreamEndCapture(st, &bg);
+        if (err == cudaSuccess) err = e2;
+      }
+    }
+    if (err == cudaSuccess && !ce) err = cudaGraphInstantiate(&ex, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (ce) return ce;
+    if (err != cudaSuccess) return cuda_error(err, "device-resident Krylov graph");
+    X.loops.push_back({kind, x, b, ex, nl, nb});
+    L = &X.loops.back();
+  }
+  DFVM_CUDA(cudaGraphLaunch(L->exec, st));
+  const int slot = (int)X.pending.size();
+  if (slot >= SolverT<T>::kSlots) { set_error(DFVM_E_INVALID_ARG, "too many pending solves"); return DFVM_E_INVALID_ARG; }
+  DFVM_CUDA(cudaMemcpyAsync(X.h_slots + 3 * slot, X.d_ctl, nctl * sizeof(KCtl), cudaMemcpyDeviceToHost, st));
+  X.pending.push_back({slot, nctl, rep, L->nl_fixed, L->nl_body});
+  return DFVM_OK;
+}
+
+static dfvm_status solve_status(const KCtl* c, int nctl) {
+  dfvm_status res = DFVM_OK;
+  for (int k = 0; k < nctl; ++k) {
+    if (c[k].status == DFVM_E_BREAKDOWN) res = DFVM_E_BREAKDOWN;
+    else if (!c[k].converged && res == DFVM_OK) res = DFVM_E_NOT_CONVERGED;
+  }
+  return res;
+}
+
+// after a stream synchronisation: reports, launch counts and the worst status
+// of the device-resident solves enqueued since the last one
+template <class T>
+static dfvm_status resolve_pending(dfvm_solver* S, SolverT<T>& X) {
+  dfvm_status res = DFVM_OK;
+  for (const auto& p : X.pending) {
+    const KCtl* c = X.h_slots + 3 * p.slot;
+    int iters = 0;
+    for (int k = 0; k < p.nctl; ++k) {
+      if (p.rep) fill_report(c[k], &p.rep[k]);
+      iters = std::max(iters, c[k].it);
+    }
+    S->n_launch += p.nl_fixed + (iters + 1) * p.nl_body;
+    const dfvm_status st = solve_status(c, p.nctl);
+    if (st == DFVM_E_BREAKDOWN || (st == DFVM_E_NOT_CONVERGED && res == DFVM_OK)) res = st;
+  }
+  X.pending.clear();
+  return res;
+}
+
+// host-chunked driver: prologue, then chunks of kChunk iterations with one
+// control-block read-back each, then the epilogue
+struct NoHarvest { void operator()(int, bool) const {} };
+
+template <class T, class Pro, class Body, class Epi, class Harvest = NoHarvest>
+static dfvm_status chunk_loop(dfvm_solver* S, SolverT<T>& X, int nctl, dfvm_solve_report* rep, cudaStream_t st,
+                              Pro pro, Body body, Epi epi, Harvest harvest = Harvest()) {
+  Prof* pr = S->pr();
+  dfvm_status e;
+  if ((e = pro(&S->n_launch))) return e;
+  int it_prof = 0;
+  const bool prof_graph = pr && S->m->part.P == 1 && st != nullptr;
+  auto iters = [&]() { int i = 0; for (int k = 0; k < nctl; ++k) i = std::max(i, X.h_ctl[k].it); return i; };
+  auto all_done = [&]() { for (int k = 0; k < nctl; ++k) if (!X.h_ctl[k].done) return false; return true; };
+  for (;;) {
+    auto chunk = [&](int* nl) -> dfvm_status {
+      for (int k = 0; k < kChunk; ++k) {
+        if (pr) { pr->iter = k; pr->post = 0; }
+        dfvm_status e3 = body(nl);
+        if (e3) return e3;
+      }
+      return DFVM_OK;
+    };
+    if (prof_graph) {
+      // profile mode: this chunk captured afresh with its event pairs as
+      // graph nodes and replayed once (no host gap inside an event pair)
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t gx = nullptr;
+      int nl = 0;
+      DFVM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      const dfvm_status ce = chunk(&nl);
+      DFVM_CUDA(cudaStreamEndCapture(st, &g));
+      if (ce) { cudaGraphDestroy(g); return ce; }
+      DFVM_CUDA(cudaGraphInstantiate(&gx, g, 0));
+      cudaGraphDestroy(g);
+      DFVM_CUDA(cudaGraphLaunch(gx, st));
+      DFVM_CUDA(cudaStreamSynchronize(st));
+      cudaGraphExecDestroy(gx);
+      S->n_launch += nl;
+    } else if ((e = chunk(&S->n_launch))) {
+      return e;
+    }
+    DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, nctl * sizeof(KCtl), cudaMemcpyDeviceToHost, st));
+    DFVM_CUDA(cudaStreamSynchronize(st));
+    harvest(iters() - it_prof, all_done());
+    if (pr) {
+      pr->harvest(iters() - it_prof, nctl == 1 && X.h_ctl[0].done != 0);
+      pr->iter = -1; pr->post = 0;
+    }
+    it_prof = iters();
+    if (all_done()) break;
+  }
+  DFVM_CUDA(cudaGetLastError());
+  if ((e = epi(&S->n_launch))) return e;
+  for (int k = 0; k < nctl; ++k)
+    if (rep) fill_report(X.h_ctl[k], &rep[k]);
+  return solve_status(X.h_ctl, nctl);
+}
+
 template <class T>
 static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol,
                               int maxit, dfvm_solve_report* rep, cudaStream_t st);
 
-// Jacobi PCG on (pdiag, pcoef): x warm start, b rhs
+// Jacobi PCG on (pdiag, pcoef): x warm start, b rhs.  The x update of
+// iteration k is deferred into the p update of iteration k+1 (x is never read
+// inside the loop); k_cg_final applies the last pending one.
 template <class T>
 static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol, int maxit,
                           dfvm_solve_report* rep, cudaStream_t st) {
@@ -1159,71 +1352,68 @@ static dfvm_status run_cg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, doubl
   KCtl init{};
   init.tol = tol; init.rel_tol = rel_tol; init.maxit = maxit;
   DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, &init, sizeof(KCtl), cudaMemcpyHostToDevice, st));
-  dfvm_status e;
-  if ((e = halo_exchange(m, x, 1, st))) return e;
-  PLAUNCH(pr, "k_cg_init", -1, 4 * N + Z * (4 + v) + 4 * v * N, st,
-          (k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr,
-                                                                                   X.partials, X.ticket, X.d_ctl, red)));
-  S->n_launch++;
-  if ((e = fin(S, X, CTL_CG_INIT, 3, st))) return e;
-  if (S->timing && S->ev.size() < 4 * kChunk) {
+  if (S->timing && S->ev.size() < 4 * kChunk)
     while (S->ev.size() < 4 * kChunk) {
       cudaEvent_t ev;
       DFVM_CUDA(cudaEventCreate(&ev));
       S->ev.push_back(ev);
     }
-  }
-  int it_before = 0, it_prof = 0;
-  for (int it0 = 0;; it0 += kChunk) {
-    for (int k = 0; k < kChunk; ++k) {
-      if (pr) { pr->iter = k; pr->post = 0; }
-      if (S->timing) record_event(S->ev[4 * k], st);
-      PLAUNCH(pr, "k_cg_p", -1, 6 * v * N, st, (k_cg_p<T><<<gp, kThreads, 0, st>>>(M.n_own, X.kr, X.pdiag, X.kp, x, X.d_ctl)));
-      if ((e = halo_exchange(m, X.kp, 1, st))) return e;
-      if (S->timing) record_event(S->ev[4 * k + 1], st);
-      PLAUNCH(pr, "k_cg_spmv", -1, 4 * N + Z * (4 + v) + 3 * v * N, st,
-              (k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red)));
-      if (S->timing) record_event(S->ev[4 * k + 2], st);
-      if ((e = fin(S, X, CTL_CG_SPMV, 1, st))) return e;
-      PLAUNCH(pr, "k_cg_r", -1, 4 * v * N, st,
-              (k_cg_r<T><<<gr, kThreads, 0, st>>>(M.n_own, X.kq, X.pdiag, X.kr, X.partials, X.ticket, X.d_ctl, red)));
-      if ((e = fin(S, X, CTL_CG_R, 2, st))) return e;
-      if (S->timing) record_event(S->ev[4 * k + 3], st);
-      S->n_launch += 3;
-    }
-    DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
-    DFVM_CUDA(cudaStreamSynchronize(st));
-    if (pr) { pr->harvest(X.h_ctl->it - it_prof, false); it_prof = X.h_ctl->it; pr->iter = -1; }
-    if (S->timing) {
-      // only iterations that actually ran (the rest exited on the done flag)
-      const int ran = X.h_ctl->it - it_before;
-      for (int k = 0; k < kChunk && k < ran; ++k) {
-        float a = 0, b2 = 0;
-        cudaEventElapsedTime(&a, S->ev[4 * k + 1], S->ev[4 * k + 2]);
-        cudaEventElapsedTime(&b2, S->ev[4 * k], S->ev[4 * k + 3]);
-        S->t_ms[0] += a; S->t_n[0]++;
-        S->t_ms[1] += b2; S->t_n[1]++;
-      }
-      it_before = X.h_ctl->it;
-    }
-    if (X.h_ctl->done) break;
-  }
-  DFVM_CUDA(cudaGetLastError());
-  const KCtl& c = *X.h_ctl;
-  if (c.half) {   // deferred x update of the last iteration
+  int k_ev = 0;
+  auto pro = [&](int* nl) -> dfvm_status {
+    dfvm_status e;
+    if ((e = halo_exchange(m, x, 1, st))) return e;
+    PLAUNCH(pr, "k_cg_init", -1, 4 * N + Z * (4 + v) + 4 * v * N, st,
+            (k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x,
+                                                                                     X.kr, X.partials, X.ticket,
+                                                                                     X.d_ctl, red)));
+    ++*nl;
+    return fin(S, X, CTL_CG_INIT, 3, st);
+  };
+  auto body = [&](int* nl) -> dfvm_status {
+    dfvm_status e;
+    const int k = k_ev++ % kChunk;
+    if (S->timing) record_event(S->ev[4 * k], st);
+    PLAUNCH(pr, "k_cg_p", -1, 6 * v * N, st, (k_cg_p<T><<<gp, kThreads, 0, st>>>(M.n_own, X.kr, X.pdiag, X.kp, x, X.d_ctl)));
+    if ((e = halo_exchange(m, X.kp, 1, st))) return e;
+    if (S->timing) record_event(S->ev[4 * k + 1], st);
+    PLAUNCH(pr, "k_cg_spmv", -1, 4 * N + Z * (4 + v) + 3 * v * N, st,
+            (k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red)));
+    if (S->timing) record_event(S->ev[4 * k + 2], st);
+    if ((e = fin(S, X, CTL_CG_SPMV, 1, st))) return e;
+    PLAUNCH(pr, "k_cg_r", -1, 4 * v * N, st,
+            (k_cg_r<T><<<gr, kThreads, 0, st>>>(M.n_own, X.kq, X.pdiag, X.kr, X.partials, X.ticket, X.d_ctl, red)));
+    if ((e = fin(S, X, CTL_CG_R, 2, st))) return e;
+    if (S->timing) record_event(S->ev[4 * k + 3], st);
+    *nl += 3;
+    return DFVM_OK;
+  };
+  auto epi = [&](int* nl) -> dfvm_status {
     PLAUNCH(pr, "k_cg_final", -1, 3 * v * N, st, (k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl)));
-    S->n_launch++;
-  }
-  if (c.zero_x) DFVM_CUDA(cudaMemsetAsync(x, 0, (size_t)M.n_own * sizeof(T), st));
-  if (rep) fill_report(c, rep);
-  return (dfvm_status)(c.status == DFVM_E_BREAKDOWN ? DFVM_E_BREAKDOWN : (c.converged ? DFVM_OK : DFVM_E_NOT_CONVERGED));
+    k_zero_if<T><<<ge, kThreads, 0, st>>>(M.n_own, 1, x, X.d_ctl);
+    *nl += 2;
+    return DFVM_OK;
+  };
+  if (use_device_loops(S, X, st)) return device_loop(S, X, LOOP_CG, x, b, 1, rep, st, pro, body, epi);
+  // live timing (dfvm_solver_set_timing): the SpMV and whole iterations of
+  // the iterations that ran in each chunk
+  auto harvest = [&](int ran, bool) {
+    if (!S->timing) return;
+    for (int k = 0; k < kChunk && k < ran; ++k) {
+      float a = 0, b2 = 0;
+      cudaEventElapsedTime(&a, S->ev[4 * k + 1], S->ev[4 * k + 2]);
+      cudaEventElapsedTime(&b2, S->ev[4 * k], S->ev[4 * k + 3]);
+      S->t_ms[0] += a; S->t_n[0]++;
+      S->t_ms[1] += b2; S->t_n[1]++;
+    }
+  };
+  return chunk_loop(S, X, 1, rep, st, pro, body, epi, harvest);
 }
 
-// PCG preconditioned by one AMG V(1,1) cycle (amg.cu).
-// Same stopping rule, same deferred x update; per iteration:
+// PCG preconditioned by one AMG cycle (amg.cu).  Same
+// stopping rule, same deferred x update; per iteration:
 //   p update (z + beta p) | halo(p) | SpMV + p.q -> alpha | r update + r.r ->
-//   check | z = M^-1 r | r.z -> beta.   The V-cycle kernels exit early on the
-//   done flag, so the chunked host loop costs nothing after convergence.
+//   check, fused with the level-0 pre-smoothing | z = M^-1 r, r.z folded into
+//   the level-0 post-smoother -> beta.
 template <class T>
 static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol,
                               int maxit, dfvm_solve_report* rep, cudaStream_t st) {
@@ -1243,168 +1433,113 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   KCtl init{};
   init.tol = tol; init.rel_tol = rel_tol; init.maxit = maxit;
   DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, &init, sizeof(KCtl), cudaMemcpyHostToDevice, st));
-  if ((e = halo_exchange(m, x, 1, st))) return e;
-  PLAUNCH(pr, "k_cg_init", -1, 4 * N + Z * (4 + v) + 4 * v * N, st,
-          (k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x, X.kr,
-                                                                                   X.partials, X.ticket, X.d_ctl, red)));
-  S->n_launch++;
-  if ((e = fin(S, X, CTL_CG_INIT, 3, st))) return e;
-  // r.z is folded into the level-0 post-smoother when the cycle has one
-  // (k_amg_smooth_dot), else a separate k_cg_dot
   const KDot dot0{X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ0}, dot1{X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ};
   void* x0f = nullptr;
   const void* il1f = nullptr;
   int pbf = 0;
   amg_level0_pre<T>(X.amg, &x0f, &il1f, &pbf);
-  bool dot_done = false;
-  if ((e = amg_apply<T>(X.amg, X.kr, X.kz, done, st, &S->n_launch, nullptr, pr, &dot0, false, &dot_done))) return e;
-  if (!dot_done) {
-    PLAUNCH(pr, "k_cg_dot", -1, 2 * v * N, st,
-            (k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ0)));
-    S->n_launch++;
-  }
-  if ((e = fin(S, X, CTL_CG_RZ0, 1, st))) return e;
-  if (S->timing && S->ev.size() < 8 * kChunk) {
+  if (S->timing && S->ev.size() < 8 * kChunk)
     while (S->ev.size() < 8 * kChunk) {
       cudaEvent_t ev;
       DFVM_CUDA(cudaEventCreate(&ev));
       S->ev.push_back(ev);
     }
-  }
-  // one chunk of kChunk iterations (every kernel exits early on the done flag)
-  auto enqueue_chunk = [&](int* nl) -> dfvm_status {
+  int k_ev = 0;
+  auto pro = [&](int* nl) -> dfvm_status {
     dfvm_status e2;
-    for (int k = 0; k < kChunk; ++k) {
-      if (pr) { pr->iter = k; pr->post = 0; }
-      if (S->timing) record_event(S->ev[4 * k], st);
-      PLAUNCH(pr, "k_cg_p2", -1, 5 * v * N, st, (k_cg_p2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kz, X.kp, x, X.d_ctl)));
-      if ((e2 = halo_exchange(m, X.kp, 1, st))) return e2;
-      if (S->timing) record_event(S->ev[4 * k + 1], st);
-      PLAUNCH(pr, "k_cg_spmv", -1, 4 * N + Z * (4 + v) + 3 * v * N, st,
-              (k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red)));
-      if (S->timing) record_event(S->ev[4 * k + 2], st);
-      if ((e2 = fin(S, X, CTL_CG_SPMV, 1, st))) return e2;
-      if (pbf == 4) {
-        PLAUNCH(pr, "k_cg_r2x", -1, 3 * v * N + 8 * N, st,
-                (k_cg_r2x<T, float><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, (const float*)il1f, (float*)x0f,
-                                                              X.partials, X.ticket, X.d_ctl, red)));
-      } else if (pbf == 8) {
-        PLAUNCH(pr, "k_cg_r2x", -1, 3 * v * N + 16 * N, st,
-                (k_cg_r2x<T, double><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, (const double*)il1f, (double*)x0f,
-                                                               X.partials, X.ticket, X.d_ctl, red)));
-      } else {
-        PLAUNCH(pr, "k_cg_r2", -1, 3 * v * N, st,
-                (k_cg_r2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, X.partials, X.ticket, X.d_ctl, red)));
-      }
-      if ((e2 = fin(S, X, CTL_CG_R2, 1, st))) return e2;
-      if (pr) pr->post = 1;
-      bool dd = false;
-      if ((e2 = amg_apply<T>(X.amg, X.kr, X.kz, done, st, nl, S->timing ? &S->ev[4 * kChunk + 4 * k] : nullptr, pr,
-                             &dot1, pbf != 0, &dd)))
-        return e2;
-      if (!dd) {
-        PLAUNCH(pr, "k_cg_dot", -1, 2 * v * N, st,
-                (k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ)));
-        ++*nl;
-      }
-      if ((e2 = fin(S, X, CTL_CG_RZ, 1, st))) return e2;
-      if (S->timing) record_event(S->ev[4 * k + 3], st);
-      *nl += 3;
+    if ((e2 = halo_exchange(m, x, 1, st))) return e2;
+    PLAUNCH(pr, "k_cg_init", -1, 4 * N + Z * (4 + v) + 4 * v * N, st,
+            (k_cg_init<T><<<grid_slices(k_cg_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.pdiag, X.pcoef, b, x,
+                                                                                     X.kr, X.partials, X.ticket,
+                                                                                     X.d_ctl, red)));
+    ++*nl;
+    if ((e2 = fin(S, X, CTL_CG_INIT, 3, st))) return e2;
+    // r.z is folded into the level-0 post-smoother when the cycle has one
+    // (k_amg_smooth_dot), else a separate k_cg_dot
+    bool dd = false;
+    if ((e2 = amg_apply<T>(X.amg, X.kr, X.kz, done, st, nl, nullptr, pr, &dot0, false, &dd))) return e2;
+    if (!dd) {
+      PLAUNCH(pr, "k_cg_dot", -1, 2 * v * N, st,
+              (k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ0)));
+      ++*nl;
     }
+    return fin(S, X, CTL_CG_RZ0, 1, st);
+  };
+  auto body = [&](int* nl) -> dfvm_status {
+    dfvm_status e2;
+    const int k = k_ev++ % kChunk;
+    if (S->timing) record_event(S->ev[4 * k], st);
+    PLAUNCH(pr, "k_cg_p2", -1, 5 * v * N, st, (k_cg_p2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kz, X.kp, x, X.d_ctl)));
+    if ((e2 = halo_exchange(m, X.kp, 1, st))) return e2;
+    if (S->timing) record_event(S->ev[4 * k + 1], st);
+    PLAUNCH(pr, "k_cg_spmv", -1, 4 * N + Z * (4 + v) + 3 * v * N, st,
+            (k_cg_spmv<T><<<gs, kThreads, 0, st>>>(M, X.pdiag, X.pcoef, X.kp, X.kq, X.partials, X.ticket, X.d_ctl, red)));
+    if (S->timing) record_event(S->ev[4 * k + 2], st);
+    if ((e2 = fin(S, X, CTL_CG_SPMV, 1, st))) return e2;
+    if (pbf == 4) {
+      PLAUNCH(pr, "k_cg_r2x", -1, 3 * v * N + 8 * N, st,
+              (k_cg_r2x<T, float><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, (const float*)il1f, (float*)x0f,
+                                                            X.partials, X.ticket, X.d_ctl, red)));
+    } else if (pbf == 8) {
+      PLAUNCH(pr, "k_cg_r2x", -1, 3 * v * N + 16 * N, st,
+              (k_cg_r2x<T, double><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, (const double*)il1f, (double*)x0f,
+                                                             X.partials, X.ticket, X.d_ctl, red)));
+    } else {
+      PLAUNCH(pr, "k_cg_r2", -1, 3 * v * N, st,
+              (k_cg_r2<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kq, X.kr, X.partials, X.ticket, X.d_ctl, red)));
+    }
+    if ((e2 = fin(S, X, CTL_CG_R2, 1, st))) return e2;
+    if (pr) pr->post = 1;
+    bool dd = false;
+    if ((e2 = amg_apply<T>(X.amg, X.kr, X.kz, done, st, nl, S->timing ? &S->ev[4 * kChunk + 4 * k] : nullptr, pr,
+                           &dot1, pbf != 0, &dd)))
+      return e2;
+    if (!dd) {
+      PLAUNCH(pr, "k_cg_dot", -1, 2 * v * N, st,
+              (k_cg_dot<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kz, X.partials, X.ticket, X.d_ctl, red, CTL_CG_RZ)));
+      ++*nl;
+    }
+    if ((e2 = fin(S, X, CTL_CG_RZ, 1, st))) return e2;
+    if (S->timing) record_event(S->ev[4 * k + 3], st);
+    *nl += 3;
     return DFVM_OK;
   };
-  // Unpartitioned meshes replay the chunk as a CUDA graph (~1300 launches per
-  // chunk with the W-cycle: host enqueue, not the GPU, bounded the deep AMG
-  // levels).  Captured on first use for this (x, b, timing); DFVM_GRAPHS=0
-  // disables.
-  typename SolverT<T>::ChunkGraph* graph = nullptr;
-  if (m->part.P == 1 && !X.graphs_off && st != nullptr && !pr) {   // (the legacy default stream cannot be captured)
-    const char* genv = getenv("DFVM_GRAPHS");
-    if (genv && genv[0] == '0') X.graphs_off = true;
-    for (auto& g : X.graphs)
-      if (g.x == x && g.b == b && g.timing == S->timing) graph = &g;
-    if (!graph && !X.graphs_off) {
-      cudaGraph_t g = nullptr;
-      cudaGraphExec_t ge2 = nullptr;
-      int nl = 0;
-      bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-      dfvm_status ce = ok ? enqueue_chunk(&nl) : DFVM_OK;
-      ok = (cudaStreamEndCapture(st, &g) == cudaSuccess) && ok && ce == DFVM_OK && g;
-      ok = ok && cudaGraphInstantiate(&ge2, g, 0) == cudaSuccess;
-      if (g) cudaGraphDestroy(g);
-      cudaGetLastError();
-      if (ok) {
-        X.graphs.push_back({x, b, S->timing, ge2, nl});
-        graph = &X.graphs.back();
-      } else {
-        X.graphs_off = true;   // capture unsupported here: enqueue directly from now on
-      }
-    }
-  }
-  int it_before = 0, it_prof = 0;
-  const bool prof_graph = pr && m->part.P == 1 && st != nullptr;
-  for (;;) {
-    if (graph) {
-      DFVM_CUDA(cudaGraphLaunch(graph->exec, st));
-      S->n_launch += graph->launches;
-    } else if (prof_graph) {
-      // profile mode: this chunk captured afresh with its event pairs as
-      // graph nodes and replayed once (no host gap inside an event pair)
-      cudaGraph_t g = nullptr;
-      cudaGraphExec_t gx = nullptr;
-      int nl = 0;
-      DFVM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      const dfvm_status ce = enqueue_chunk(&nl);
-      DFVM_CUDA(cudaStreamEndCapture(st, &g));
-      if (ce) { cudaGraphDestroy(g); return ce; }
-      DFVM_CUDA(cudaGraphInstantiate(&gx, g, 0));
-      cudaGraphDestroy(g);
-      DFVM_CUDA(cudaGraphLaunch(gx, st));
-      DFVM_CUDA(cudaStreamSynchronize(st));
-      cudaGraphExecDestroy(gx);
-      S->n_launch += nl;
-    } else if ((e = enqueue_chunk(&S->n_launch))) {
-      return e;
-    }
-    DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, sizeof(KCtl), cudaMemcpyDeviceToHost, st));
-    DFVM_CUDA(cudaStreamSynchronize(st));
-    if (pr) { pr->harvest(X.h_ctl->it - it_prof, X.h_ctl->done != 0); it_prof = X.h_ctl->it; pr->iter = -1; pr->post = 0; }
-    if (S->timing) {
-      const int ran = X.h_ctl->it - it_before;
-      for (int k = 0; k < kChunk && k < ran; ++k) {
-        float a = 0, b2 = 0, c2 = 0, d2 = 0;
-        cudaEventElapsedTime(&a, S->ev[4 * k + 1], S->ev[4 * k + 2]);
-        cudaEventElapsedTime(&b2, S->ev[4 * k], S->ev[4 * k + 3]);
-        S->t_ms[0] += a; S->t_n[0]++;
-        S->t_ms[1] += b2; S->t_n[1]++;
-        // level-0 AMG kernels (recorded only when the fused path ran; the
-        // last iteration of a solve skips its V-cycle on the done flag)
-        if (k + 1 < ran || !X.h_ctl->done) {
-          cudaEvent_t* ea = &S->ev[4 * kChunk + 4 * k];
-          if (cudaEventElapsedTime(&c2, ea[0], ea[1]) == cudaSuccess && cudaEventElapsedTime(&d2, ea[2], ea[3]) == cudaSuccess) {
-            S->t_ms[2] += c2; S->t_n[2]++;
-            S->t_ms[3] += d2; S->t_n[3]++;
-          }
+  auto epi = [&](int* nl) -> dfvm_status {
+    PLAUNCH(pr, "k_cg_final", -1, 3 * v * N, st, (k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl)));
+    k_zero_if<T><<<ge, kThreads, 0, st>>>(M.n_own, 1, x, X.d_ctl);
+    *nl += 2;
+    return DFVM_OK;
+  };
+  if (use_device_loops(S, X, st)) return device_loop(S, X, LOOP_CG_AMG, x, b, 1, rep, st, pro, body, epi);
+  // live timing: SpMV, whole iteration, and the level-0 AMG kernels (recorded
+  // only when the cycle ran: the last iteration of a solve skips it)
+  auto harvest = [&](int ran, bool all_done) {
+    if (!S->timing) return;
+    for (int k = 0; k < kChunk && k < ran; ++k) {
+      float a = 0, b2 = 0, c2 = 0, d2 = 0;
+      cudaEventElapsedTime(&a, S->ev[4 * k + 1], S->ev[4 * k + 2]);
+      cudaEventElapsedTime(&b2, S->ev[4 * k], S->ev[4 * k + 3]);
+      S->t_ms[0] += a; S->t_n[0]++;
+      S->t_ms[1] += b2; S->t_n[1]++;
+      if (k + 1 < ran || !all_done) {
+        cudaEvent_t* ea = &S->ev[4 * kChunk + 4 * k];
+        if (cudaEventElapsedTime(&c2, ea[0], ea[1]) == cudaSuccess && cudaEventElapsedTime(&d2, ea[2], ea[3]) == cudaSuccess) {
+          S->t_ms[2] += c2; S->t_n[2]++;
+          S->t_ms[3] += d2; S->t_n[3]++;
         }
       }
-      it_before = X.h_ctl->it;
     }
-    if (X.h_ctl->done) break;
-  }
-  cudaGetLastError();   // clear a possible not-ready status of an unrecorded timing event
-  const KCtl& c = *X.h_ctl;
-  if (c.half) {
-    PLAUNCH(pr, "k_cg_final", -1, 3 * v * N, st, (k_cg_final<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kp, x, X.d_ctl)));
-    S->n_launch++;
-  }
-  if (c.zero_x) DFVM_CUDA(cudaMemsetAsync(x, 0, (size_t)M.n_own * sizeof(T), st));
-  if (rep) fill_report(c, rep);
-  return (dfvm_status)(c.status == DFVM_E_BREAKDOWN ? DFVM_E_BREAKDOWN : (c.converged ? DFVM_OK : DFVM_E_NOT_CONVERGED));
+    cudaGetLastError();
+  };
+  return chunk_loop(S, X, 1, rep, st, pro, body, epi, harvest);
 }
 
 // 3-component BiCGStab on (udiag, ucoef): x = U (warm start), b = rhsU.
-// Ghosts: x and udiag are exchanged by the caller (assemble); p, r and v are
-// exchanged before the applies that gather them.
+// Right-preconditioned (Jacobi) van der Vorst BiCGStab, the three velocity
+// components advanced together over one coefficient stream; each component
+// keeps its own scalars and stops independently.  Ghosts: x and udiag are
+// exchanged by the caller (assemble); p, r and v are exchanged before the
+// applies that gather them.
 template <class T>
 static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol,
                                 int maxit, dfvm_solve_report* rep, cudaStream_t st) {
@@ -1423,61 +1558,44 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   KCtl init[3] = {};
   for (int k = 0; k < 3; ++k) { init[k].tol = tol; init[k].rel_tol = rel_tol; init[k].maxit = maxit; }
   DFVM_CUDA(cudaMemcpyAsync(X.d_ctl, init, 3 * sizeof(KCtl), cudaMemcpyHostToDevice, st));
-  dfvm_status e;
-  PLAUNCH(pr, "k_recip", -1, 2 * v * M.n_cells, st,
-          (k_recip<T><<<grid_for(M.n_cells), kThreads, 0, st>>>(M.n_cells, X.udiag, X.udinv)));
-  S->n_launch++;
-  PLAUNCH(pr, "k_bi_init", -1, 4 * N + Z * (4 + v) + 19 * v * N, st,
-          (k_bi_init<T><<<grid_slices(k_bi_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr,
-                                                                                   X.krh, X.kp, X.kv, X.partials,
-                                                                                   X.ticket, X.d_ctl, red)));
-  S->n_launch++;
-  if ((e = fin(S, X, CTL_BI_INIT, 6, st))) return e;
-  int it_prof = 0;
-  for (;;) {
-    for (int k = 0; k < kChunk; ++k) {
-      if (pr) pr->iter = k;
-      PLAUNCH(pr, "k_bi_p", -1, 12 * v * N, st, (k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.kp, X.d_ctl)));
-      if ((e = halo_exchange(m, X.kp, 3, st))) return e;
-      PLAUNCH(pr, "k_bi_v", -1, 4 * N + Z * (4 + v) + 11 * v * N, st,
-              (k_bi_v<T, 4, 6><<<gs, kThreads, 0, st>>>(M, X.udiag, X.udinv, X.ucoef, X.kp, X.krh, X.kv, X.partials,
-                                                        X.ticket, X.d_ctl, red)));
-      if ((e = fin(S, X, CTL_BI_V, 3, st))) return e;
-      if ((e = halo_exchange(m, X.kr, 3, st)) || (e = halo_exchange(m, X.kv, 3, st))) return e;
-      PLAUNCH(pr, "k_bi_t", -1, 4 * N + Z * (4 + v) + 10 * v * N, st,
-              (k_bi_t<T, 4, 3><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket,
-                                                        X.d_ctl, red)));
-      if ((e = fin(S, X, CTL_BI_T, 9, st))) return e;
-      PLAUNCH(pr, "k_bi_x", -1, 25 * v * N, st,
-              (k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.kp, X.kv, X.kt, X.krh, x, X.kr, X.partials,
-                                                  X.ticket, X.d_ctl, red)));
-      if ((e = fin(S, X, CTL_BI_X, 6, st))) return e;
-      S->n_launch += 4;
-    }
-    DFVM_CUDA(cudaMemcpyAsync(X.h_ctl, X.d_ctl, 3 * sizeof(KCtl), cudaMemcpyDeviceToHost, st));
-    DFVM_CUDA(cudaStreamSynchronize(st));
-    if (pr) {
-      const int itm = std::max(X.h_ctl[0].it, std::max(X.h_ctl[1].it, X.h_ctl[2].it));
-      pr->harvest(itm - it_prof, false);
-      it_prof = itm;
-      pr->iter = -1;
-    }
-    if (X.h_ctl[0].done && X.h_ctl[1].done && X.h_ctl[2].done) break;
-  }
-  DFVM_CUDA(cudaGetLastError());
-  dfvm_status res = DFVM_OK;
-  for (int k = 0; k < 3; ++k) {
-    const KCtl& c = X.h_ctl[k];
-    if (rep) fill_report(c, &rep[k]);
-    if (c.status == DFVM_E_BREAKDOWN) res = DFVM_E_BREAKDOWN;
-    else if (!c.converged && res == DFVM_OK) res = DFVM_E_NOT_CONVERGED;
-  }
-  // b = 0 components: x = 0
-  for (int k = 0; k < 3; ++k)
-    if (X.h_ctl[k].zero_x) {
-      DFVM_CUDA(cudaMemset2DAsync((char*)x + k * sizeof(T), 3 * sizeof(T), 0, sizeof(T), M.n_own, st));
-    }
-  return res;
+  auto pro = [&](int* nl) -> dfvm_status {
+    PLAUNCH(pr, "k_recip", -1, 2 * v * M.n_cells, st,
+            (k_recip<T><<<grid_for(M.n_cells), kThreads, 0, st>>>(M.n_cells, X.udiag, X.udinv)));
+    PLAUNCH(pr, "k_bi_init", -1, 4 * N + Z * (4 + v) + 19 * v * N, st,
+            (k_bi_init<T><<<grid_slices(k_bi_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr,
+                                                                                     X.krh, X.kp, X.kv, X.partials,
+                                                                                     X.ticket, X.d_ctl, red)));
+    *nl += 2;
+    return fin(S, X, CTL_BI_INIT, 6, st);
+  };
+  auto body = [&](int* nl) -> dfvm_status {
+    dfvm_status e;
+    PLAUNCH(pr, "k_bi_p", -1, 12 * v * N, st, (k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.kp, X.d_ctl)));
+    if ((e = halo_exchange(m, X.kp, 3, st))) return e;
+    PLAUNCH(pr, "k_bi_v", -1, 4 * N + Z * (4 + v) + 11 * v * N, st,
+            (k_bi_v<T, 4, 6><<<gs, kThreads, 0, st>>>(M, X.udiag, X.udinv, X.ucoef, X.kp, X.krh, X.kv, X.partials,
+                                                      X.ticket, X.d_ctl, red)));
+    if ((e = fin(S, X, CTL_BI_V, 3, st))) return e;
+    if ((e = halo_exchange(m, X.kr, 3, st)) || (e = halo_exchange(m, X.kv, 3, st))) return e;
+    PLAUNCH(pr, "k_bi_t", -1, 4 * N + Z * (4 + v) + 10 * v * N, st,
+            (k_bi_t<T, 4, 3><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket,
+                                                      X.d_ctl, red)));
+    if ((e = fin(S, X, CTL_BI_T, 9, st))) return e;
+    PLAUNCH(pr, "k_bi_x", -1, 25 * v * N, st,
+            (k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.kp, X.kv, X.kt, X.krh, x, X.kr, X.partials,
+                                                X.ticket, X.d_ctl, red)));
+    if ((e = fin(S, X, CTL_BI_X, 6, st))) return e;
+    *nl += 4;
+    return DFVM_OK;
+  };
+  auto epi = [&](int* nl) -> dfvm_status {
+    // b = 0 components: x = 0
+    k_zero_if<T><<<ge, kThreads, 0, st>>>(M.n_own, 3, x, X.d_ctl);
+    ++*nl;
+    return DFVM_OK;
+  };
+  if (use_device_loops(S, X, st)) return device_loop(S, X, LOOP_BICGSTAB, x, b, 3, rep, st, pro, body, epi);
+  return chunk_loop(S, X, 3, rep, st, pro, body, epi);
 }
 
 template <class T>
@@ -1514,6 +1632,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   const dfvm_piso_opts& o = S->o;
   dfvm_status s2;
   S->n_launch = 0;
+  X.pending.clear();
   std::memset(R, 0, sizeof(*R));
   if ((s2 = bcs_device(b, 0, st)) || (s2 = bcs_device(b, 1, st))) return s2;
   // time-varying boundary values at the new time level t^{n+1} (A-41)
@@ -1593,9 +1712,8 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
         rhs = X.prhs;
       }
       const bool final_corr = corr == o.n_corr && io == o.n_nonorth;
-      dfvm_solve_report sr{};
-      s2 = run_cg(S, X, rhs, p, o.p_tol, final_corr ? o.p_rel_tol_final : o.p_rel_tol, o.p_maxit, &sr, st);
-      if (np < 16) R->p[np] = sr;
+      s2 = run_cg(S, X, rhs, p, o.p_tol, final_corr ? o.p_rel_tol_final : o.p_rel_tol, o.p_maxit,
+                  np < 16 ? &R->p[np] : nullptr, st);
       np++;
       if (s2 != DFVM_OK && s2 != DFVM_E_NOT_CONVERGED) return s2;   // breakdown, CUDA / NCCL errors
       if (s2 == DFVM_E_NOT_CONVERGED) res = s2;
@@ -1627,6 +1745,16 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
   DFVM_CUDA(cudaStreamSynchronize(st));
   DFVM_CUDA(cudaGetLastError());
   if (pr) pr->harvest();
+  {   // device-resident solves of this step: reports and status
+    const dfvm_status ps = resolve_pending(S, X);
+    if (ps == DFVM_E_BREAKDOWN) {
+      R->gpu_launches = S->n_launch;
+      count_launch(S->n_launch);
+      set_error(DFVM_E_BREAKDOWN, "Krylov breakdown in the PISO step");
+      return DFVM_E_BREAKDOWN;
+    }
+    if (ps == DFVM_E_NOT_CONVERGED) res = ps;
+  }
   R->cont_err_max = X.h_cont[0];
   R->cont_err_sum = X.h_cont[1];
   R->nonfinite = X.h_cont[2] > 0;
@@ -1664,6 +1792,7 @@ static dfvm_status transport_step_t(dfvm_solver* S, SolverT<T>& X, T* x, const T
   dfvm_status e;
   if ((e = bcs_device(b, 2, st))) return e;
   S->n_launch = 0;
+  X.pending.clear();
   if ((e = halo_exchange(S->m, x, 1, st))) return e;
   launch_grad<T>(M, x, 1, b->d_kind[2], (const T*)b->d_val[2], X.gp, st);
   if ((e = halo_exchange(S->m, X.gp, 3, st))) return e;
@@ -1682,6 +1811,7 @@ static dfvm_status transport_step_t(dfvm_solver* S, SolverT<T>& X, T* x, const T
   S->n_launch++;
   DFVM_CUDA(cudaStreamSynchronize(st));
   DFVM_CUDA(cudaGetLastError());
+  if (!X.pending.empty()) res = resolve_pending(S, X);
   count_launch(S->n_launch);
   if (rep) *rep = r3[0];
   return res;
@@ -1896,9 +2026,11 @@ static dfvm_status pressure_solve_t(dfvm_solver* s, SolverT<T>& X, const T* rAU,
   if (add_ref) k_add_at<T><<<1, 1, 0, st>>>(X.prhs, X.prhs0, ref);
   count_launch(1 + add_ref);
   s->n_launch = 0;
+  X.pending.clear();
   dfvm_status r = run_cg(s, X, X.prhs, p, tol, rel_tol, maxit, rep, st);
-  count_launch(s->n_launch);
   DFVM_CUDA(cudaStreamSynchronize(st));
+  if (!X.pending.empty() && r == DFVM_OK) r = resolve_pending(s, X);
+  count_launch(s->n_launch);
   return r;
 }
 
