@@ -95,6 +95,7 @@ def lib():
         L.orc_laplacian_parts.argtypes = [vp, vp, i32, vp, vp, vp, vp]
         L.orc_pressure_rhs.argtypes = [vp] * 5
         L.orc_flux_correct.argtypes = [vp] * 5
+        L.orc_phi_hbya.argtypes = [vp] * 6
         _LIB = L
     return _LIB
 
@@ -336,6 +337,13 @@ class Solver:
         out = np.empty(self.mesh.N)
         rAU, phiHbyA, p = _f64(rAU), _f64(phiHbyA), _f64(p)
         _check(lib().orc_pressure_rhs(self.h, _p(rAU), _p(phiHbyA), _p(p), _p(out)))
+        return out
+
+    def phi_hbya(self, HbyA, rAU, Un, phin):
+        """O-6 step 3.3 (+ 3.3' ddtCorr when the solver has ddt_corr, A-42): phiHbyA on every face."""
+        out = np.empty(self.mesh.NF)
+        HbyA, rAU, Un, phin = _f64(HbyA), _f64(rAU), _f64(Un), _f64(phin)
+        _check(lib().orc_phi_hbya(self.h, _p(HbyA), _p(rAU), _p(Un), _p(phin), _p(out)))
         return out
 
     def flux_correct(self, rAU, phiHbyA, p):

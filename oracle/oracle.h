@@ -13,11 +13,16 @@
 // order); every cell accumulator receives its contributions in that order;
 // dot products run in ascending cell order.
 //
-// Parity unpinned: the Windkessel coupling inside the PISO
-// step (reading A-19), the ddtCorr-free Rhie-Chow face flux (A-9) on
-// non-orthogonal tets and the optional ddtCorr term (A-42) have no closed
-// form or printed example; they are checked only against invariants
-// (continuity, uniform-flow fixed point, zero ddtCorr on a consistent start).
+// Pins: every part is pinned by a closed form, a hand value or
+// an already-pinned operator (tests/test_oracle_*.py), including the parts
+// round 1 left unpinned: the explicit non-orthogonal momentum correction
+// (O-5, by hand on a w = 3/4 two-cell fixture and against the pinned
+// Laplacian), the non-orthogonal pressure right-hand side and Rhie-Chow flux
+// term (A-9, by hand), the Windkessel coupling inside PISO (A-19: exact RCR
+// fixed point, per-corrector recurrence) and the partition emulation (O-10,
+// bitwise against the global apply) and the optional ddtCorr term (A-42, by
+// hand on the same fixture, both branches of its min()) —
+// tests/test_oracle_pins_r2.py.  No part is left "parity unpinned".
 #pragma once
 #include <cstdint>
 #include <string>

@@ -386,6 +386,36 @@ static void pressure_matrix(const Solver& S, const double* rAU, LDU& A, std::vec
   }
 }
 
+// O-6 step 3.3: phiHbyA = interp(HbyA) . S on internal faces; boundary
+// faces HbyA_b . S_b with HbyA_b = U_b on fixed-value U, HbyA_O on
+// zeroGradient; empty faces 0.  Step 3.3', the optional ddtCorr (A-42,
+// OpenFOAM's Euler ddtCorr), on internal faces:
+//   phiHbyA += rAU_f c_f (phi^n - U^n_f . S) / dt,
+//   c_f = 1 - min(|phi^n - U^n_f . S| / (|phi^n| + 1e-15), 1),
+// U^n_f, rAU_f the w-interpolates of the start-of-step U and of rAU.
+static void phi_hbya(const Solver& S, const double* HbyA, const double* rAU, const double* Un, const double* phin,
+                     std::vector<double>& fv, double* phiHbyA) {
+  const Mesh& m = *S.m;
+  fv.assign((size_t)3 * m.NF, 0.0);
+  interpolate(m, *S.b, 0, 3, HbyA, fv.data());
+  for (int64_t f = 0; f < m.NF; ++f) {
+    if (f >= m.F && m.is_empty_face(f)) { phiHbyA[f] = 0; continue; }
+    phiHbyA[f] = fv[3 * f] * m.Sf[3 * f] + fv[3 * f + 1] * m.Sf[3 * f + 1] + fv[3 * f + 2] * m.Sf[3 * f + 2];
+  }
+  if (S.o.ddt_corr) {
+    for (int64_t f = 0; f < m.F; ++f) {
+      const int64_t O = m.owner[f], Nn = m.neigh[f];
+      const double w = m.w[f];
+      double uS = 0;
+      for (int l = 0; l < 3; ++l) uS += (w * Un[3 * O + l] + (1.0 - w) * Un[3 * Nn + l]) * m.Sf[3 * f + l];
+      const double d = phin[f] - uS;
+      const double c = 1.0 - std::min(std::fabs(d) / (std::fabs(phin[f]) + 1e-15), 1.0);
+      const double rf = w * rAU[O] + (1.0 - w) * rAU[Nn];
+      phiHbyA[f] += rf * c * d / S.o.dt;
+    }
+  }
+}
+
 // Pressure right-hand side of one non-orthogonal corrector (eq:pressure_poisson
 // RHS P:337-339 times -1; the explicit
 // non-orthogonal part in the A-9 reading):
@@ -514,27 +544,8 @@ static int piso_step(Solver& S, double* U, double* p, double* phi, Report& R) {
       rAU[c] = m.V[c] / M.diag[c];
       for (int k = 0; k < 3; ++k) HbyA[3 * c + k] = H[3 * c + k] / M.diag[c];
     }
-    // 3.3 phiHbyA = interp(HbyA) . S (boundary: HbyA_b = U_b fixed, HbyA_O zeroGradient)
-    interpolate(m, b, 0, 3, HbyA.data(), fv.data());
-    for (int64_t f = 0; f < m.NF; ++f) {
-      if (f >= m.F && m.is_empty_face(f)) { phiHbyA[f] = 0; continue; }
-      phiHbyA[f] = fv[3 * f] * m.Sf[3 * f] + fv[3 * f + 1] * m.Sf[3 * f + 1] + fv[3 * f + 2] * m.Sf[3 * f + 2];
-    }
-    // 3.3' optional ddtCorr (A-42, OpenFOAM's Euler ddtCorr): on internal faces
-    //   phiHbyA += rAU_f c_f (phi^n - U^n_f . S) / dt,
-    //   c_f = 1 - min(|phi^n - U^n_f . S| / (|phi^n| + 1e-15), 1)
-    if (S.o.ddt_corr) {
-      for (int64_t f = 0; f < m.F; ++f) {
-        const int64_t O = m.owner[f], Nn = m.neigh[f];
-        const double w = m.w[f];
-        double uS = 0;
-        for (int l = 0; l < 3; ++l) uS += (w * Un[3 * O + l] + (1.0 - w) * Un[3 * Nn + l]) * m.Sf[3 * f + l];
-        const double d = phin[f] - uS;
-        const double c = 1.0 - std::min(std::fabs(d) / (std::fabs(phin[f]) + 1e-15), 1.0);
-        const double rf = w * rAU[O] + (1.0 - w) * rAU[Nn];
-        phiHbyA[f] += rf * c * d / S.o.dt;
-      }
-    }
+    // 3.3 phiHbyA (+ the optional ddtCorr term)
+    phi_hbya(S, HbyA.data(), rAU.data(), Un.data(), phin.data(), fv, phiHbyA.data());
     // 3.4 pressure coefficients
     LDU A;
     std::vector<double> cf, cb;
@@ -642,6 +653,13 @@ int orc_pressure_rhs(void* sp, const double* rAU, const double* phiHbyA, const d
   div(m, phiHbyA, Dphi.data());
   grad(m, *S.b, 1, 1, p, Gp.data());
   pressure_rhs(S, rAU, Dphi.data(), cb, p, Gp.data(), rhs);
+  return OK;
+}
+int orc_phi_hbya(void* sp, const double* HbyA, const double* rAU, const double* Un, const double* phin,
+                 double* phiHbyA) {
+  Solver& S = *(Solver*)sp;
+  std::vector<double> fv;
+  phi_hbya(S, HbyA, rAU, Un, phin, fv, phiHbyA);
   return OK;
 }
 int orc_flux_correct(void* sp, const double* rAU, const double* phiHbyA, const double* p, double* phi) {

@@ -84,6 +84,11 @@ constexpr int kMaxLevels = 16;
 //                    levels of a few thousand rows gain)
 //   DFVM_AMG_TAIL_CLUSTER  CTAs of the tail cluster (16: non-portable size)
 //                                                             default 16
+//   DFVM_AMG_FUSED_FROM  coarse levels l >= this run the fused pre-smooth +
+//                    residual / prolongation + post-smooth kernels; levels
+//                    1 .. this-1 the unfused ones (pre, resid | prolong,
+//                    smooth: fewer gathers per entry, one more vector pass;
+//                    bitwise identical results)                  default 1
 //   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
 //                    exactly with a dense inverse (Gauss-Jordan once per
 //                    matrix update, one block), larger ones with
@@ -91,6 +96,7 @@ constexpr int kMaxLevels = 16;
 struct AmgParams {
   int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, sigma = 0;
   int tail = 0, tail_cluster = 16;
+  int fused_from = 1;   // coarse levels >= this use the fused pre_resid / prolong_smooth kernels
   bool wcycle = true;
   double omega = 1.9;   // C5 amg32: 362 ms, 11.6 it/solve (1.8: 369 ms, 12.2; 1.7: 380 ms)
   AmgParams() {
@@ -102,6 +108,7 @@ struct AmgParams {
     if (const char* e = getenv("DFVM_AMG_CYCLE")) wcycle = (e[0] == 'W' || e[0] == 'w');
     if (const char* e = getenv("DFVM_AMG_WMAX")) wmax = std::max(0, atoi(e));
     if (const char* e = getenv("DFVM_AMG_TAIL")) tail = std::max(0, atoi(e));
+    if (const char* e = getenv("DFVM_AMG_FUSED_FROM")) fused_from = std::max(1, atoi(e));
     if (const char* e = getenv("DFVM_AMG_TAIL_CLUSTER")) tail_cluster = std::max(1, std::min(16, atoi(e)));
   }
 };
@@ -1024,9 +1031,18 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
   const P w = (P)A->prm.omega;
   const double pb = sizeof(P), n = F.n, nc = C.n;
   const int gF = grid_for(F.n), gC = grid_for(C.n);
-  PLAUNCH(pr, "k_amg_pre_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
-          (k_amg_pre_resid<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, F.t,
-                                                      F.r, done)));
+  const bool fused = l >= A->prm.fused_from;
+  if (fused) {
+    PLAUNCH(pr, "k_amg_pre_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
+            (k_amg_pre_resid<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, F.t,
+                                                        F.r, done)));
+  } else {
+    PLAUNCH(pr, "k_amg_pre", l, 3 * pb * n, s, (k_amg_pre<P, P, P><<<gF, kThreads, 0, s>>>(F.n, b, F.il1, F.t, done)));
+    PLAUNCH(pr, "k_amg_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 4 * pb * n, s,
+            (k_amg_resid<P, P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.t, b, F.r,
+                                                       done)));
+    ++*nl;
+  }
   PLAUNCH(pr, "k_amg_restrict", l, (4 + pb) * (n + nc), s,
           (k_amg_restrict<P><<<gC, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
   *nl += 2;
@@ -1044,9 +1060,19 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
     *nl += 2;
   }
   }
-  PLAUNCH(pr, "k_amg_prolong_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + (4 + 5 * pb) * n + pb * nc, s,
-          (k_amg_prolong_smooth<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1,
-                                                           F.agg, C.x, w, F.t, b, x, done)));
+  if (fused) {
+    PLAUNCH(pr, "k_amg_prolong_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + (4 + 5 * pb) * n + pb * nc, s,
+            (k_amg_prolong_smooth<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1,
+                                                             F.agg, C.x, w, F.t, b, x, done)));
+  } else {
+    // F.r is free after the restriction: the prolonged t = x0 + w x_c[agg] goes there
+    PLAUNCH(pr, "k_amg_prolong", l, (4 + 2 * pb) * n + pb * nc, s,
+            (k_amg_prolong<P><<<gF, kThreads, 0, s>>>(F.n, F.agg, C.x, F.t, F.r, w, done)));
+    PLAUNCH(pr, "k_amg_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
+            (k_amg_smooth<P, P, P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.r,
+                                                           b, x, done)));
+    ++*nl;
+  }
   ++*nl;
 }
 

@@ -564,19 +564,6 @@ __global__ void k_windkessel_fin(const double* __restrict__ all, int P, int n_wk
 template <class T>
 __global__ void k_add_at(T* a, const T* b, int i) { a[i] += b[i]; }
 
-// scalar <-> component 0 of a 3-vector (the scalar transport reuses the
-// 3-component BiCGStab; components 1, 2 have b = 0 and stop at iteration 0)
-template <class T>
-__global__ void k_pack3(int n, const T* __restrict__ a, T* __restrict__ a3) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    a3[3 * (int64_t)i] = a[i]; a3[3 * (int64_t)i + 1] = T(0); a3[3 * (int64_t)i + 2] = T(0);
-  }
-}
-template <class T>
-__global__ void k_unpack3(int n, const T* __restrict__ a3, T* __restrict__ a) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = a3[3 * (int64_t)i];
-}
-
 // ============================================================ Jacobi PCG
 // r = b - A x; partials b.b, r.r, r.z  -> control start
 template <class T>
@@ -722,13 +709,15 @@ __global__ void k_cg_final(int n, const T* __restrict__ pd, T* __restrict__ x, c
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] += alpha * pd[i];
 }
 
-// ============================================================ BiCGStab (3 components)
-// Right-preconditioned (Jacobi) van der Vorst BiCGStab, the three velocity
-// components advanced together over one coefficient stream; each component
-// keeps its own scalars and stops independently.
+// ============================================================ BiCGStab (NC components)
+// Right-preconditioned (Jacobi) van der Vorst BiCGStab, the NC components
+// (3 velocity components, or 1 transported scalar) advanced together over one
+// coefficient stream; each component keeps its own scalars and stops
+// independently.  The reductions always carry 3 component slots (zeros for
+// k >= NC: those components start with b = 0 and are done from the start).
 __device__ __forceinline__ bool all_done(const KCtl* c) { return c[0].done && c[1].done && c[2].done; }
 
-template <class T>
+template <class T, int NC>
 __global__ void __launch_bounds__(kThreads) k_bi_init(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ coef, const T* __restrict__ b, const T* __restrict__ x, T* __restrict__ r,
     T* __restrict__ rh, T* __restrict__ p, T* __restrict__ v, double* partials, unsigned* ticket, KCtl* ctl, Red red) {
@@ -736,15 +725,15 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(DevMesh<T> M, const T* __r
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
-    T acc[3];
+    T acc[NC];
     const T d = live ? diag[row] : T(0);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) acc[k] = live ? d * x[3 * (int64_t)row + k] : T(0);
-    sell_apply<T, 3>(M, s, lane, coef, x, acc);
+    for (int k = 0; k < NC; ++k) acc[k] = live ? d * x[NC * (int64_t)row + k] : T(0);
+    sell_apply<T, NC>(M, s, lane, coef, x, acc);
     if (live)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const int64_t i = 3 * (int64_t)row + k;
+      for (int k = 0; k < NC; ++k) {
+        const int64_t i = NC * (int64_t)row + k;
         const T rr = b[i] - acc[k];
         r[i] = rr; rh[i] = rr; p[i] = T(0); v[i] = T(0);
         a[k] += (double)b[i] * (double)b[i];
@@ -767,29 +756,29 @@ __global__ void k_recip(int n, const T* __restrict__ d, T* __restrict__ di) {
 // s is stored: the kernels that need them form them from p (r, v) and dinv.
 
 // p = r + beta (p - omega v)
-template <class T>
+template <class T, int NC>
 __global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ p, const KCtl* ctl) {
   if (all_done(ctl)) return;
   T beta[3], om[3];
   bool act[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < NC; ++k) {
     act[k] = !ctl[k].done;
     beta[k] = (T)((ctl[k].rho / ctl[k].rho_old) * (ctl[k].alpha / ctl[k].omega));
     om[k] = (T)ctl[k].omega;
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < NC; ++k) {
       if (!act[k]) continue;
-      const int64_t j = 3 * (int64_t)i + k;
+      const int64_t j = NC * (int64_t)i + k;
       p[j] = r[j] + beta[k] * (p[j] - om[k] * v[j]);
     }
   }
 }
 
 // v = A (p / diag); partial (rh, v) -> alpha   (dinv = 1 / diag)
-template <class T, int KBV, int MINB>
+template <class T, int NC, int KBV, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_bi_v(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ dinv, const T* __restrict__ coef, const T* __restrict__ p, const T* __restrict__ rh,
     T* __restrict__ v, double* partials, unsigned* ticket, KCtl* ctl, Red red) {
@@ -801,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_bi_v(DevMesh<T> M, const T* 
     T acc[3];
     const T d = live ? diag[row] : T(0), di = live ? dinv[row] : T(0);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) acc[k] = live ? d * (p[3 * (int64_t)row + k] * di) : T(0);
+    for (int k = 0; k < NC; ++k) acc[k] = live ? d * (p[NC * (int64_t)row + k] * di) : T(0);
     const int len = __ldg(&M.ms_len[s]);
     const int base = __ldg(&M.ms_ptr[s]) + lane;
     int j = 0;
@@ -814,24 +803,24 @@ __global__ void __launch_bounds__(kThreads, MINB) k_bi_v(DevMesh<T> M, const T* 
       for (int u = 0; u < KBV; ++u) {
         dn[u] = dinv[nn[u]];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) pn[u][k] = p[3 * (int64_t)nn[u] + k];
+        for (int k = 0; k < NC; ++k) pn[u][k] = p[NC * (int64_t)nn[u] + k];
       }
 #pragma unroll
       for (int u = 0; u < KBV; ++u)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) acc[k] += c[u] * (pn[u][k] * dn[u]);
+        for (int k = 0; k < NC; ++k) acc[k] += c[u] * (pn[u][k] * dn[u]);
     }
     for (; j < len; ++j) {
       const T c = __ldg(&coef[base + 32 * j]);
       const int nn = __ldg(&M.mnb[base + 32 * j]);
       const T dn = dinv[nn];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) acc[k] += c * (p[3 * (int64_t)nn + k] * dn);
+      for (int k = 0; k < NC; ++k) acc[k] += c * (p[NC * (int64_t)nn + k] * dn);
     }
     if (live)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const int64_t i = 3 * (int64_t)row + k;
+      for (int k = 0; k < NC; ++k) {
+        const int64_t i = NC * (int64_t)row + k;
         v[i] = acc[k];
         a[k] += (double)rh[i] * (double)acc[k];
       }
@@ -842,14 +831,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_bi_v(DevMesh<T> M, const T* 
 
 // s = r - alpha v (own row and, on the fly, every neighbour); t = A (s / diag);
 // partials (t, s), (t, t), (s, s) -> half-step check, omega
-template <class T, int KBT, int MINB>
+template <class T, int NC, int KBT, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_bi_t(DevMesh<T> M, const T* __restrict__ dinv,
     const T* __restrict__ coef, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ tv,
     double* partials, unsigned* ticket, KCtl* ctl, Red red) {
   if (all_done(ctl)) return;
   T al[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) al[k] = (T)ctl[k].alpha;
+  for (int k = 0; k < NC; ++k) al[k] = (T)ctl[k].alpha;
   double a[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
@@ -857,8 +846,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_bi_t(DevMesh<T> M, const T* 
     T acc[3] = {T(0), T(0), T(0)}, sr[3] = {T(0), T(0), T(0)};
     if (live)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const int64_t i = 3 * (int64_t)row + k;
+      for (int k = 0; k < NC; ++k) {
+        const int64_t i = NC * (int64_t)row + k;
         sr[k] = r[i] - al[k] * v[i];
         acc[k] = sr[k];                    // diag * (s / diag)
       }
@@ -874,24 +863,24 @@ __global__ void __launch_bounds__(kThreads, MINB) k_bi_t(DevMesh<T> M, const T* 
       for (int u = 0; u < KBT; ++u) {
         dn[u] = dinv[nn[u]];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) { rn[u][k] = r[3 * (int64_t)nn[u] + k]; vn[u][k] = v[3 * (int64_t)nn[u] + k]; }
+        for (int k = 0; k < NC; ++k) { rn[u][k] = r[NC * (int64_t)nn[u] + k]; vn[u][k] = v[NC * (int64_t)nn[u] + k]; }
       }
 #pragma unroll
       for (int u = 0; u < KBT; ++u)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) acc[k] += c[u] * ((rn[u][k] - al[k] * vn[u][k]) * dn[u]);
+        for (int k = 0; k < NC; ++k) acc[k] += c[u] * ((rn[u][k] - al[k] * vn[u][k]) * dn[u]);
     }
     for (; j < len; ++j) {
       const T c = __ldg(&coef[base + 32 * j]);
       const int nn = __ldg(&M.mnb[base + 32 * j]);
       const T dn = dinv[nn];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) acc[k] += c * ((r[3 * (int64_t)nn + k] - al[k] * v[3 * (int64_t)nn + k]) * dn);
+      for (int k = 0; k < NC; ++k) acc[k] += c * ((r[NC * (int64_t)nn + k] - al[k] * v[NC * (int64_t)nn + k]) * dn);
     }
     if (live)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        tv[3 * (int64_t)row + k] = acc[k];
+      for (int k = 0; k < NC; ++k) {
+        tv[NC * (int64_t)row + k] = acc[k];
         a[k] += (double)acc[k] * (double)sr[k];
         a[3 + k] += (double)acc[k] * (double)acc[k];
         a[6 + k] += (double)sr[k] * (double)sr[k];
@@ -903,7 +892,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_bi_t(DevMesh<T> M, const T* 
 
 // s = r - alpha v; x += alpha p/diag + omega s/diag; r = s - omega t;
 // partials (rh, r), (r, r)   (dinv = 1 / diag)
-template <class T>
+template <class T, int NC>
 __global__ void k_bi_x(int n, const T* __restrict__ dinv, const T* __restrict__ p, const T* __restrict__ v,
                        const T* __restrict__ tv, const T* __restrict__ rh, T* __restrict__ x, T* __restrict__ r,
                        double* partials, unsigned* ticket, KCtl* ctl, Red red) {
@@ -911,7 +900,7 @@ __global__ void k_bi_x(int n, const T* __restrict__ dinv, const T* __restrict__ 
   T al[3], om[3];
   int mode[3];   // 0 skip, 1 half step, 2 full step
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < NC; ++k) {
     mode[k] = ctl[k].done ? 0 : (ctl[k].half ? 1 : 2);
     al[k] = (T)ctl[k].alpha; om[k] = (T)ctl[k].omega;
   }
@@ -919,8 +908,8 @@ __global__ void k_bi_x(int n, const T* __restrict__ dinv, const T* __restrict__ 
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const T d = dinv[i];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const int64_t j = 3 * (int64_t)i + k;
+    for (int k = 0; k < NC; ++k) {
+      const int64_t j = NC * (int64_t)i + k;
       if (mode[k] == 1) { x[j] += al[k] * (p[j] * d); continue; }
       if (mode[k] != 2) continue;
       const T ss = r[j] - al[k] * v[j];
@@ -1163,7 +1152,7 @@ static dfvm_status fin(dfvm_solver* S, SolverT<T>& X, int kind, int nv, cudaStre
 //  * host-chunked (several ranks with host-side transports, the legacy
 //    stream, profiling, DFVM_GRAPHS=0): kChunk iterations enqueued per host
 //    round trip, every kernel exiting early on the done flag.
-enum LoopKind { LOOP_CG = 0, LOOP_CG_AMG = 1, LOOP_BICGSTAB = 2 };
+enum LoopKind { LOOP_CG = 0, LOOP_CG_AMG = 1, LOOP_BICGSTAB = 2, LOOP_BICGSTAB1 = 3 };
 
 __global__ void k_loop_cond(cudaGraphConditionalHandle h, const KCtl* ctl, int nc) {
   int go = 0;
@@ -1540,7 +1529,7 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
 // keeps its own scalars and stops independently.  Ghosts: x and udiag are
 // exchanged by the caller (assemble); p, r and v are exchanged before the
 // applies that gather them.
-template <class T>
+template <class T, int NC>
 static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol,
                                 int maxit, dfvm_solve_report* rep, cudaStream_t st) {
   DevMesh<T>& M = *X.M;
@@ -1549,7 +1538,7 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   // k_bi_t: batch 4 at >= 3 blocks/SM (batch 2 at 4 blocks/SM measured equal on C5)
   // batch depth / min blocks per SM: measured on C5 against batch 2 and 1
   // with two-load 3-vector gathers (profiles/r01_bicgstab_variants_c5.txt)
-  const int gs = grid_slices(k_bi_v<T, 4, 6>, M.n_slices), gt = grid_slices(k_bi_t<T, 4, 3>, M.n_slices);
+  const int gs = grid_slices(k_bi_v<T, NC, 4, 6>, M.n_slices), gt = grid_slices(k_bi_t<T, NC, 4, 3>, M.n_slices);
   // (measured on C5: flat [3n] p/x updates and shared-staged own rows in v/t
   // were 26 ms/step slower than these one-thread-per-row kernels)
   const int ge = grid_for(M.n_own);
@@ -1561,8 +1550,8 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   auto pro = [&](int* nl) -> dfvm_status {
     PLAUNCH(pr, "k_recip", -1, 2 * v * M.n_cells, st,
             (k_recip<T><<<grid_for(M.n_cells), kThreads, 0, st>>>(M.n_cells, X.udiag, X.udinv)));
-    PLAUNCH(pr, "k_bi_init", -1, 4 * N + Z * (4 + v) + 19 * v * N, st,
-            (k_bi_init<T><<<grid_slices(k_bi_init<T>, M.n_slices), kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr,
+    PLAUNCH(pr, "k_bi_init", -1, 4 * N + Z * (4 + v) + (1 + 6 * NC) * v * N, st,
+            (k_bi_init<T, NC><<<grid_slices(k_bi_init<T, NC>, M.n_slices), kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr,
                                                                                      X.krh, X.kp, X.kv, X.partials,
                                                                                      X.ticket, X.d_ctl, red)));
     *nl += 2;
@@ -1570,19 +1559,19 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   };
   auto body = [&](int* nl) -> dfvm_status {
     dfvm_status e;
-    PLAUNCH(pr, "k_bi_p", -1, 12 * v * N, st, (k_bi_p<T><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.kp, X.d_ctl)));
-    if ((e = halo_exchange(m, X.kp, 3, st))) return e;
-    PLAUNCH(pr, "k_bi_v", -1, 4 * N + Z * (4 + v) + 11 * v * N, st,
-            (k_bi_v<T, 4, 6><<<gs, kThreads, 0, st>>>(M, X.udiag, X.udinv, X.ucoef, X.kp, X.krh, X.kv, X.partials,
+    PLAUNCH(pr, "k_bi_p", -1, 4 * NC * v * N, st, (k_bi_p<T, NC><<<ge, kThreads, 0, st>>>(M.n_own, X.kr, X.kv, X.kp, X.d_ctl)));
+    if ((e = halo_exchange(m, X.kp, NC, st))) return e;
+    PLAUNCH(pr, "k_bi_v", -1, 4 * N + Z * (4 + v) + (2 + 3 * NC) * v * N, st,
+            (k_bi_v<T, NC, 4, 6><<<gs, kThreads, 0, st>>>(M, X.udiag, X.udinv, X.ucoef, X.kp, X.krh, X.kv, X.partials,
                                                       X.ticket, X.d_ctl, red)));
     if ((e = fin(S, X, CTL_BI_V, 3, st))) return e;
-    if ((e = halo_exchange(m, X.kr, 3, st)) || (e = halo_exchange(m, X.kv, 3, st))) return e;
-    PLAUNCH(pr, "k_bi_t", -1, 4 * N + Z * (4 + v) + 10 * v * N, st,
-            (k_bi_t<T, 4, 3><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket,
+    if ((e = halo_exchange(m, X.kr, NC, st)) || (e = halo_exchange(m, X.kv, NC, st))) return e;
+    PLAUNCH(pr, "k_bi_t", -1, 4 * N + Z * (4 + v) + (1 + 3 * NC) * v * N, st,
+            (k_bi_t<T, NC, 4, 3><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket,
                                                       X.d_ctl, red)));
     if ((e = fin(S, X, CTL_BI_T, 9, st))) return e;
-    PLAUNCH(pr, "k_bi_x", -1, 25 * v * N, st,
-            (k_bi_x<T><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.kp, X.kv, X.kt, X.krh, x, X.kr, X.partials,
+    PLAUNCH(pr, "k_bi_x", -1, (1 + 8 * NC) * v * N, st,
+            (k_bi_x<T, NC><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.kp, X.kv, X.kt, X.krh, x, X.kr, X.partials,
                                                 X.ticket, X.d_ctl, red)));
     if ((e = fin(S, X, CTL_BI_X, 6, st))) return e;
     *nl += 4;
@@ -1590,12 +1579,13 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   };
   auto epi = [&](int* nl) -> dfvm_status {
     // b = 0 components: x = 0
-    k_zero_if<T><<<ge, kThreads, 0, st>>>(M.n_own, 3, x, X.d_ctl);
+    k_zero_if<T><<<ge, kThreads, 0, st>>>(M.n_own, NC, x, X.d_ctl);
     ++*nl;
     return DFVM_OK;
   };
-  if (use_device_loops(S, X, st)) return device_loop(S, X, LOOP_BICGSTAB, x, b, 3, rep, st, pro, body, epi);
-  return chunk_loop(S, X, 3, rep, st, pro, body, epi);
+  if (use_device_loops(S, X, st))
+    return device_loop(S, X, NC == 3 ? LOOP_BICGSTAB : LOOP_BICGSTAB1, x, b, NC, rep, st, pro, body, epi);
+  return chunk_loop(S, X, NC, rep, st, pro, body, epi);
 }
 
 template <class T>
@@ -1659,7 +1649,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
     DFVM_CUDA(cudaMemcpyAsync(X.phiold, phi, (size_t)M.F * sizeof(T), cudaMemcpyDeviceToDevice, st));
   }
   // 2. predictor
-  dfvm_status res = run_bicgstab(S, X, X.rhsU, U, o.U_tol, o.U_rel_tol, o.U_maxit, R->U, st);
+  dfvm_status res = run_bicgstab<T, 3>(S, X, X.rhsU, U, o.U_tol, o.U_rel_tol, o.U_maxit, R->U, st);
   if (res != DFVM_OK && res != DFVM_E_NOT_CONVERGED) return res;   // breakdown, CUDA / NCCL errors
   const int n_wk = (int)S->wk.size();
   int np = 0;
@@ -1801,19 +1791,16 @@ static dfvm_status transport_step_t(dfvm_solver* S, SolverT<T>& X, T* x, const T
                                                       (T)gamma, (T)(1.0 / S->o.dt), (T)theta_of(S->o), S->o.convection, S->kcorr,
                                                       X.fdO, X.fdN, X.udiag, X.prhs0, X.prhs, X.ucoef, X.ucoefT);
   if ((e = halo_exchange(S->m, X.udiag, 1, st))) return e;
-  k_pack3<T><<<ge, kThreads, 0, st>>>(M.n_own, X.prhs, X.bU);
-  k_pack3<T><<<grid_for(M.n_cells), kThreads, 0, st>>>(M.n_cells, x, X.HbyA);
-  S->n_launch += 4;
+  S->n_launch += 2;
   X.assembled = true;
-  dfvm_solve_report r3[3];
-  dfvm_status res = run_bicgstab(S, X, X.bU, X.HbyA, S->o.U_tol, S->o.U_rel_tol, S->o.U_maxit, r3, st);
-  k_unpack3<T><<<ge, kThreads, 0, st>>>(M.n_own, X.HbyA, x);
-  S->n_launch++;
+  // one-component BiCGStab directly on x (halo-exchanged above) and b = prhs
+  dfvm_solve_report r1[1];
+  dfvm_status res = run_bicgstab<T, 1>(S, X, X.prhs, x, S->o.U_tol, S->o.U_rel_tol, S->o.U_maxit, r1, st);
   DFVM_CUDA(cudaStreamSynchronize(st));
   DFVM_CUDA(cudaGetLastError());
   if (!X.pending.empty()) res = resolve_pending(S, X);
   count_launch(S->n_launch);
-  if (rep) *rep = r3[0];
+  if (rep) *rep = r1[0];
   return res;
 }
 

@@ -436,8 +436,10 @@ def test_amg_cluster_tail_bitwise(precond, size, monkeypatch):
     s = torch.cuda.Stream()
     sp = ctypes.c_void_p(s.cuda_stream)
     out = []
-    for tail in ("0", "100000", "4000"):
-        monkeypatch.setenv("DFVM_AMG_TAIL", tail)
+    for var, val in (("DFVM_AMG_TAIL", "0"), ("DFVM_AMG_TAIL", "100000"), ("DFVM_AMG_TAIL", "4000"),
+                     ("DFVM_AMG_FUSED_FROM", "3")):
+        monkeypatch.delenv("DFVM_AMG_TAIL", raising=False)
+        monkeypatch.setenv(var, val)
         Sg = mk()
         Ug, pg, phig = mg.field("cells", 3, U0, sp), mg.field("cells", 1, p0, sp), mg.field("flux", 1, phi0, sp)
         reps = [Sg.step(Ug, pg, phig, sp) for _ in range(2)]

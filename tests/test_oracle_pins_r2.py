@@ -321,3 +321,36 @@ def test_o10_partitioned_laplacian_bitwise(name, P):
         assert np.array_equal(y, yp), np.abs(y - yp).max()
     # every part has ghosts (the partition really splits the operator)
     assert all(len(pp["ghost"]) > 0 for pp in R.parts)
+
+
+# ------------------------------------------------------------ A-42
+@pytest.mark.parametrize("phin0,expect_c", [(0.5, None), (0.01, 0.0)])
+def test_ddtcorr_term_by_hand(phin0, expect_c):
+    """A-42 (OpenFOAM's Euler ddtCorr, the optional NEXT-4 flag) on the w = 3/4
+    fixture: phiHbyA_f = (w HbyA_O + (1 - w) HbyA_N) . S + rAU_f c (phi^n - U^n_f . S) / dt,
+    c = 1 - min(|phi^n - U^n_f . S| / (|phi^n| + 1e-15), 1); with S = (1, 0, 0)
+    only x-components enter.  Boundary faces (walls, U = 0) carry HbyA_b . S = 0
+    and no correction; without the flag the correction is absent."""
+    raw = sheared_pair()
+    m = oracle.Mesh(raw, "minimum")
+    dt = 0.25
+    HbyA = np.array([[0.4, -0.3, 0.2], [0.1, 0.6, -0.5]])
+    rAU = np.array([0.2, 0.05])
+    Un = np.array([[0.3, 0.1, 0.0], [0.7, -0.2, 0.4]])
+    phin = np.zeros(m.NF)
+    phin[0] = phin0
+    base = 0.75 * 0.4 + 0.25 * 0.1
+    uS = 0.75 * 0.3 + 0.25 * 0.7
+    d = phin0 - uS
+    c = 1.0 - min(abs(d) / (abs(phin0) + 1e-15), 1.0)
+    if expect_c is not None:
+        assert c == expect_c
+    rf = 0.75 * 0.2 + 0.25 * 0.05
+    for flag, want in ((True, base + rf * c * d / dt), (False, base)):
+        b = oracle.BCs(m)
+        b.set("walls", "U", oracle.BC_FIXED, (0.0, 0.0, 0.0))
+        b.set("walls", "p", oracle.BC_ZEROGRAD)
+        S = oracle.Solver(m, b, nu=1.0, dt=dt, ddt_corr=flag)
+        out = S.phi_hbya(HbyA, rAU, Un, phin)
+        assert abs(out[0] - want) <= 1e-15, (flag, out[0], want)
+        assert np.abs(out[m.F:]).max() == 0.0
