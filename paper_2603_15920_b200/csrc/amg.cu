@@ -18,7 +18,7 @@
 //    d1_i = a_ii + sum_j |a_ij|.
 //  * cycle (defaults measured on the C5 pipe): l1-Jacobi
 //    pre-smoothing from zero x0 = D1^-1 b, residual, restriction (sum over
-//    the aggregate's members), coarse correction scaled by omega = 1.9,
+//    the aggregate's members), coarse correction scaled by omega = 1.95,
 //    prolongation x = x0 + omega x_c[agg], l1-Jacobi post-smoothing (the
 //    adjoint of the pre-smoother); a W-cycle (two coarse visits, the second
 //    on the residual of the first) on levels <= 4 and a V-cycle below;
@@ -64,7 +64,7 @@ constexpr int kMaxLevels = 16;
 //                    (deeper levels use V-cycles: the W launch count
 //                    doubles per level, and deep levels are launch-bound)
 //   DFVM_AMG_OMEGA   coarse-correction scale (symmetric over-correction,
-//                    < 2 keeps M SPD with adjoint smoothers)   default 1.9
+//                    < 2 keeps M SPD with adjoint smoothers)   default 1.95
 //   DFVM_AMG_SIGMA   1: renumber aggregates by row length within windows of
 //                    256 (less SELL padding); 0: creation order      default 0
 //                    (C5 amg32, round 1: 378 ms/step without sigma against
@@ -88,7 +88,10 @@ constexpr int kMaxLevels = 16;
 //                    residual / prolongation + post-smooth kernels; levels
 //                    1 .. this-1 the unfused ones (pre, resid | prolong,
 //                    smooth: fewer gathers per entry, one more vector pass;
-//                    bitwise identical results)                  default 1
+//                    bitwise identical results)                  default 3
+//                    (C5 amg32: 340.3 ms/step against 349.6 ms with every
+//                    coarse level fused, 347.2 with level 1 unfused;
+//                    profiles/r02_amg_sweep_c5.jsonl)
 //   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
 //                    exactly with a dense inverse (Gauss-Jordan once per
 //                    matrix update, one block), larger ones with
@@ -96,9 +99,9 @@ constexpr int kMaxLevels = 16;
 struct AmgParams {
   int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, sigma = 0;
   int tail = 0, tail_cluster = 16;
-  int fused_from = 1;   // coarse levels >= this use the fused pre_resid / prolong_smooth kernels
+  int fused_from = 3;   // coarse levels >= this use the fused pre_resid / prolong_smooth kernels
   bool wcycle = true;
-  double omega = 1.9;   // C5 amg32: 362 ms, 11.6 it/solve (1.8: 369 ms, 12.2; 1.7: 380 ms)
+  double omega = 1.95;  // C5 amg32 (round 2): 344.0 ms, 11.33 it/solve (1.9: 349.6 ms, 11.58; 1.8: 360.2 ms, 12.17)
   AmgParams() {
     if (const char* e = getenv("DFVM_AMG_DIRECT")) direct = std::max(0, std::min(kDirectMax, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_SIGMA")) sigma = atoi(e);

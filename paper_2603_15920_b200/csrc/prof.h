@@ -2,9 +2,13 @@
 // "kernels" table of bench.py; north star: "achieved HBM GB/s reported
 // against B200 peak for every kernel").
 //
-// In profile mode every kernel launch of the step is bracketed by two CUDA
-// events on the launching stream and tagged with its kernel name, AMG level
-// and algorithmic bytes.  Krylov kernels also carry their
+// In profile mode every kernel launch of the step is followed by a CUDA
+// event on the launching stream and tagged with its kernel name, AMG level
+// and algorithmic bytes; a launch's time is the interval from
+// the previous launch's event (or, at the start of a sequence, a fresh start
+// event) to its own, so the rows add up to the profiled time of the
+// sequences and each kernel carries its own launch gap (what a launch costs
+// the step, the point in the latency-bound AMG levels).  Krylov kernels also carry their
 // iteration index within the enqueued chunk; after the chunk's control-block
 // read-back the harvest attributes the launches of iterations the device
 // skipped (solve already converged: the kernel exits on the done flag) to a
@@ -30,14 +34,22 @@ struct Prof {
   std::vector<cudaEvent_t> pool;
   int iter = -1;                     // Krylov iteration within the current chunk (-1: not iterative)
   int post = 0;                      // 1: launched after the iteration's convergence check
+  cudaEvent_t last = nullptr;        // the previous launch's end event in the current sequence
 
   ~Prof() {
     for (auto e : pool) cudaEventDestroy(e);
-    for (auto& r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto& r : recs) cudaEventDestroy(r.b);
+    for (auto e : starts) cudaEventDestroy(e);
   }
+  // a new sequence (host synchronisation, start / end of a graph capture):
+  // the next launch starts from a fresh event
+  void cut() { last = nullptr; }
   void clear() {
+    last = nullptr;
     stats.clear();
-    for (auto& r : recs) { pool.push_back(r.a); pool.push_back(r.b); }
+    for (auto& r : recs) pool.push_back(r.b);
+    for (auto e : starts) pool.push_back(e);
+    starts.clear();
     recs.clear();
   }
   int stat_index(const char* name, int lvl) {
@@ -53,15 +65,19 @@ struct Prof {
     return e;
   }
   cudaEvent_t begin(cudaStream_t s) {
+    if (last) return last;
     cudaEvent_t a = get();
     record_event(a, s);
+    starts.push_back(a);
     return a;
   }
   void end(cudaEvent_t a, const char* name, int lvl, double bytes, cudaStream_t s) {
     cudaEvent_t b = get();
     record_event(b, s);
     recs.push_back(Rec{stat_index(name, lvl), bytes, iter, post, a, b});
+    last = b;
   }
+  std::vector<cudaEvent_t> starts;   // fresh start events of the sequences (returned at harvest)
   // after the stream has synchronised: `ran` iterations of the chunk did
   // work, the last one stopped after its check when `done_last`
   void harvest(int ran = 1 << 30, bool done_last = false) {
@@ -73,10 +89,12 @@ struct Prof {
       st.n++;
       st.ms += ms;
       if (!noop) st.bytes += r.bytes;
-      pool.push_back(r.a);
-      pool.push_back(r.b);
+      pool.push_back(r.b);            // every event is some record's end, or a sequence start
     }
+    for (auto e : starts) pool.push_back(e);
+    starts.clear();
     recs.clear();
+    last = nullptr;
     cudaGetLastError();
   }
 };

@@ -1290,9 +1290,11 @@ static dfvm_status chunk_loop(dfvm_solver* S, SolverT<T>& X, int nctl, dfvm_solv
       cudaGraph_t g = nullptr;
       cudaGraphExec_t gx = nullptr;
       int nl = 0;
+      pr->cut();
       DFVM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       const dfvm_status ce = chunk(&nl);
       DFVM_CUDA(cudaStreamEndCapture(st, &g));
+      pr->cut();
       if (ce) { cudaGraphDestroy(g); return ce; }
       DFVM_CUDA(cudaGraphInstantiate(&gx, g, 0));
       cudaGraphDestroy(g);
