@@ -65,25 +65,18 @@ constexpr int kMaxLevels = 16;
 //                    doubles per level, and deep levels are launch-bound)
 //   DFVM_AMG_OMEGA   coarse-correction scale (symmetric over-correction,
 //                    < 2 keeps M SPD with adjoint smoothers)   default 1.95
-//   DFVM_AMG_SIGMA   1: renumber aggregates by row length within windows of
-//                    256 (less SELL padding); 0: creation order      default 0
-//                    (C5 amg32, round 1: 378 ms/step without sigma against
-//                    423 ms with sigma and 4/8-lane grouped coarse kernels,
-//                    since removed: sigma costs 0.5 PCG iterations per
-//                    solve and the grouped kernels were slower than one
-//                    thread per row)
-//   DFVM_AMG_TAIL    coarse levels with <= this many rows (all of them,
-//                    from the first such level down) run as ONE kernel per
-//                    visit of the level above: a thread-block cluster that
-//                    walks the whole sub-cycle with cluster barriers
-//                    (k_amg_tail; bitwise identical to the launched
-//                    kernels); 0: launched kernels            default 0
-//                    (C5, round 2: a tail from the 78,802-row level 3 took
-//                    0.67 ms per visit against ~0.2 ms launched — 16 SMs
-//                    cannot hide the gather latency of 5e4+ rows; only
-//                    levels of a few thousand rows gain)
-//   DFVM_AMG_TAIL_CLUSTER  CTAs of the tail cluster (16: non-portable size)
-//                                                             default 16
+//   DFVM_AMG_PERM    1: coarse-level SELL storage sorted by row length
+//                    within windows of 256 slots (SELL-32-sigma: rows keep
+//                    their numbers, the hierarchy and results are unchanged,
+//                    padding shrinks); 0: natural order          default 1
+//                    (round 1 renumbered the aggregates themselves by
+//                    length instead: that changed the next aggregation
+//                    and cost 0.5 PCG iterations per solve — removed)
+//   (round 2 measured and removed a one-cluster "tail" kernel that walked
+//   all levels below a size bound with cluster barriers: 0.67 ms per
+//   level-3 visit on C5 against ~0.2 ms launched, and slower even from the
+//   3,330-row level 4 — 16 SMs cannot hide the gather latency; profiles/
+//   r02_bench_c5_tail_variants.txt)
 //   DFVM_AMG_FUSED_FROM  coarse levels l >= this run the fused pre-smooth +
 //                    residual / prolongation + post-smooth kernels; levels
 //                    1 .. this-1 the unfused ones (pre, resid | prolong,
@@ -97,25 +90,33 @@ constexpr int kMaxLevels = 16;
 //                    matrix update, one block), larger ones with
 //                    DFVM_AMG_SWEEPS l1-Jacobi sweeps (0: always sweeps)  default 512
 struct AmgParams {
-  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, sigma = 0;
-  int tail = 0, tail_cluster = 16;
+  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, perm = 1;
   int fused_from = 3;   // coarse levels >= this use the fused pre_resid / prolong_smooth kernels
   bool wcycle = true;
   double omega = 1.95;  // C5 amg32 (round 2): 344.0 ms, 11.33 it/solve (1.9: 349.6 ms, 11.58; 1.8: 360.2 ms, 12.17)
   AmgParams() {
     if (const char* e = getenv("DFVM_AMG_DIRECT")) direct = std::max(0, std::min(kDirectMax, atoi(e)));
-    if (const char* e = getenv("DFVM_AMG_SIGMA")) sigma = atoi(e);
+    if (const char* e = getenv("DFVM_AMG_PERM")) perm = atoi(e);
     if (const char* e = getenv("DFVM_AMG_OMEGA")) omega = atof(e);
     if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kCoarseMax, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_SWEEPS")) sweeps = std::max(1, atoi(e));
     if (const char* e = getenv("DFVM_AMG_CYCLE")) wcycle = (e[0] == 'W' || e[0] == 'w');
     if (const char* e = getenv("DFVM_AMG_WMAX")) wmax = std::max(0, atoi(e));
-    if (const char* e = getenv("DFVM_AMG_TAIL")) tail = std::max(0, atoi(e));
     if (const char* e = getenv("DFVM_AMG_FUSED_FROM")) fused_from = std::max(1, atoi(e));
-    if (const char* e = getenv("DFVM_AMG_TAIL_CLUSTER")) tail_cluster = std::max(1, std::min(16, atoi(e)));
   }
 };
 
+// A level's matrix in SELL-32 storage.  Slot q of slice q / 32 (lane q % 32)
+// holds row perm[q] (perm == NULL: row q).  The coarse levels sort the rows of
+// each window of 256 slots by length (SELL-32-sigma storage; the rows keep
+// their numbers, so the hierarchy and every result are unchanged): much
+// less padding than natural order on aggregation levels.
+struct SellView {
+  const int* ms_ptr;
+  const int* ms_len;
+  const int* mnb;
+  const int* perm;
+};
 // ------------------------------------------------------------ host setup
 namespace {
 
@@ -123,15 +124,17 @@ struct HostLevel {
   int n = 0;
   // SELL-32 of this level's matrix (level 0: the mesh's matrix layout)
   std::vector<int> ms_ptr, ms_len, mnb;
+  std::vector<int> perm, slot_of;   // SELL slot -> row and back (empty: identity)
   // CSR view of the real entries: (col, SELL position), owned cols only
   std::vector<int> rp, col, pos;
+  int slot(int r) const { return slot_of.empty() ? r : slot_of[r]; }
 };
 
 void sell_to_csr(HostLevel& L, int n_owned_cols) {
   const int n = L.n;
   L.rp.assign(n + 1, 0);
   for (int r = 0; r < n; ++r) {
-    const int s = r / 32, lane = r % 32;
+    const int q = L.slot(r), s = q / 32, lane = q % 32;
     for (int j = 0; j < L.ms_len[s]; ++j) {
       const int c = L.mnb[L.ms_ptr[s] + 32 * j + lane];
       if (c != r && c < n_owned_cols) L.rp[r + 1]++;
@@ -141,7 +144,7 @@ void sell_to_csr(HostLevel& L, int n_owned_cols) {
   L.col.assign(L.rp[n], 0);
   L.pos.assign(L.rp[n], 0);
   for (int r = 0; r < n; ++r) {
-    const int s = r / 32, lane = r % 32;
+    const int q = L.slot(r), s = q / 32, lane = q % 32;
     int k = L.rp[r];
     for (int j = 0; j < L.ms_len[s]; ++j) {
       const int p = L.ms_ptr[s] + 32 * j + lane;
@@ -188,6 +191,8 @@ struct AmgLevelDev {
   int64_t n_sell = 0;        // SELL slots (incl. padding)
   int64_t nnz = 0;           // real off-diagonal entries (algorithmic bytes)
   const int *ms_ptr = nullptr, *ms_len = nullptr, *mnb = nullptr;
+  const int* perm = nullptr;  // SELL slot -> row (coarse levels, SELL-32-sigma storage), NULL: identity
+  SellView sv() const { return SellView{ms_ptr, ms_len, mnb, perm}; }
   const P* coef = nullptr;   // level 0: the solver's pcoef (P == T) or coef_own (fp32 copy)
   const P* diag = nullptr;   // level 0: the solver's pdiag (P == T) or diag_own
   P* coef_own = nullptr;
@@ -202,25 +207,6 @@ struct AmgLevelDev {
   P *e = nullptr, *r2 = nullptr;                  // W-cycle: second-visit solution / rhs
 };
 
-// device view of the levels for the cluster tail (k_amg_tail), in device
-// memory (one copy per hierarchy, written at build time)
-template <class P>
-struct TailLevel {
-  int n;
-  const int *ms_ptr, *ms_len, *mnb;
-  const P *coef, *diag, *il1;
-  const int* agg;               // fine row -> coarse row (this level -> next)
-  const int *mem_ptr, *mem;     // this level's aggregates: member rows of the finer level
-  P *x, *b, *r, *t, *e, *r2;
-};
-template <class P>
-struct TailArgs {
-  int nlev, wmax, wcycle, sweeps;
-  P omega;
-  const P* ainv;
-  TailLevel<P> L[kMaxLevels];
-};
-
 // hierarchy stored and cycled in type P
 template <class P>
 struct AmgH {
@@ -228,9 +214,6 @@ struct AmgH {
   int nlev = 0;
   AmgParams prm;
   Prof* prof = nullptr;             // per-kernel profile of the caller (may be null)
-  int tail_l0 = -1;                 // first level run by the cluster tail (-1: none)
-  int tail_cs = 16;                 // CTAs of the tail cluster
-  TailArgs<P>* d_tail = nullptr;
   AmgLevelDev<P> L[kMaxLevels];
   P* ainv = nullptr;                // dense inverse of the coarsest matrix (column-major n x n), or NULL
   std::vector<void*> allocs;
@@ -292,33 +275,6 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     // level under the 144-row one and the PCG needed 1702 iterations per
     // solve; the current level becomes the coarsest (solved exactly)
     if (nc < 32) break;
-    if (A->prm.sigma) {   // SELL-32-sigma: renumber the aggregates so that, within windows of 256
-        // (8 slices, locality kept), rows are sorted by length: less padding
-        // in the coarse SELL (35 % -> a few % on the C5 level 1)
-      std::vector<std::vector<int>> members(nc);
-      for (int i = 0; i < F.n; ++i) members[agg[i]].push_back(i);
-      std::vector<int> len(nc), nb;
-      for (int I = 0; I < nc; ++I) {
-        nb.clear();
-        for (int i : members[I])
-          for (int k = F.rp[i]; k < F.rp[i + 1]; ++k) nb.push_back(agg[F.col[k]]);
-        std::sort(nb.begin(), nb.end());
-        int u = 0;
-        for (size_t k = 0; k < nb.size(); ++k)
-          if ((k == 0 || nb[k] != nb[k - 1]) && nb[k] != I) ++u;
-        len[I] = u;
-      }
-      std::vector<int> order(nc);
-      std::iota(order.begin(), order.end(), 0);
-      constexpr int kSigma = 256;
-      for (int w0 = 0; w0 < nc; w0 += kSigma) {
-        const int w1 = std::min(nc, w0 + kSigma);
-        std::stable_sort(order.begin() + w0, order.begin() + w1, [&](int a, int b) { return len[a] > len[b]; });
-      }
-      std::vector<int> newid(nc);
-      for (int k = 0; k < nc; ++k) newid[order[k]] = k;
-      for (int i = 0; i < F.n; ++i) agg[i] = newid[agg[i]];
-    }
     // members
     std::vector<int> mem_ptr(nc + 1, 0), mem(F.n);
     for (int i = 0; i < F.n; ++i) mem_ptr[agg[i] + 1]++;
@@ -356,13 +312,33 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
       crow_ptr[I + 1] = (int)ccol.size();
       dg_ptr[I + 1] = (int)dg_idx.size();
     }
-    // coarse SELL-32 layout
+    // coarse SELL-32 layout; with prm.perm the rows of each window of 256
+    // slots are stored by decreasing length (SELL-32-sigma storage: the rows
+    // keep their numbers, so aggregation below and every result are
+    // unchanged, only the padding shrinks)
     const int S = (nc + 31) / 32;
+    if (A->prm.perm) {
+      C.perm.resize(nc);
+      C.slot_of.resize(nc);
+      for (int I = 0; I < nc; ++I) C.perm[I] = I;
+      constexpr int kSigma = 256;
+      for (int w0 = 0; w0 < nc; w0 += kSigma) {
+        const int w1 = std::min(nc, w0 + kSigma);
+        std::stable_sort(C.perm.begin() + w0, C.perm.begin() + w1, [&](int a, int b) {
+          return crow_ptr[a + 1] - crow_ptr[a] > crow_ptr[b + 1] - crow_ptr[b];
+        });
+      }
+      for (int q = 0; q < nc; ++q) C.slot_of[C.perm[q]] = q;
+    }
+    auto row_at = [&](int q) { return C.perm.empty() ? q : C.perm[q]; };
     C.ms_ptr.assign(S + 1, 0);
     C.ms_len.assign(S, 0);
     for (int s = 0; s < S; ++s) {
       int w = 0;
-      for (int I = s * 32; I < std::min(nc, s * 32 + 32); ++I) w = std::max(w, crow_ptr[I + 1] - crow_ptr[I]);
+      for (int q = s * 32; q < std::min(nc, s * 32 + 32); ++q) {
+        const int I = row_at(q);
+        w = std::max(w, crow_ptr[I + 1] - crow_ptr[I]);
+      }
       C.ms_len[s] = w;
       C.ms_ptr[s + 1] = C.ms_ptr[s] + 32 * w;
     }
@@ -370,7 +346,7 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     std::vector<int> gal_ptr(C.ms_ptr[S] + 1, 0), gal_idx;
     std::vector<int> slot_entry(C.ms_ptr[S], -1);
     for (int I = 0; I < nc; ++I) {
-      const int s = I / 32, lane = I % 32;
+      const int q = C.slot(I), s = q / 32, lane = q % 32;
       for (int j = 0; j < C.ms_len[s]; ++j) {
         const int p = C.ms_ptr[s] + 32 * j + lane;
         const int e = crow_ptr[I] + j;
@@ -387,7 +363,9 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     AmgLevelDev<P>& D = A->L[lev + 1];
     D.n = nc; D.n_slices = S; D.n_sell = C.ms_ptr[S];
     D.nnz = (int64_t)ccol.size();
-    int *p0, *p1, *p2;
+    int *p0, *p1, *p2, *p3 = nullptr;
+    if (!C.perm.empty() && (st = A->up(&p3, C.perm))) return st;
+    D.perm = p3;
     if ((st = A->up(&p0, C.ms_ptr)) || (st = A->up(&p1, C.ms_len)) || (st = A->up(&p2, C.mnb)) ||
         (st = A->up(&D.gal_ptr, gal_ptr)) || (st = A->up(&D.gal_idx, gal_idx)) || (st = A->up(&D.dg_ptr, dg_ptr)) ||
         (st = A->up(&D.dg_idx, dg_idx)) || (st = A->up(&D.mem_ptr, mem_ptr)) || (st = A->up(&D.mem, mem)) ||
@@ -409,27 +387,6 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
               100.0 * (1.0 - (double)H[k].rp[H[k].n] / std::max<double>(1.0, (double)H[k].ms_ptr.back())));
   const int nc = A->L[lev].n;
   if (lev > 0 && nc <= A->prm.direct && (st = A->zalloc(&A->ainv, (size_t)nc * nc))) return st;
-  // cluster tail: from the first level >= 1 with <= prm.tail rows down (one
-  // rank only: coarse levels are rank-local, so it would also hold at P > 1,
-  // but the tail is kept to the single-rank path it is tested on)
-  A->tail_l0 = -1;
-  if (A->prm.tail > 0 && m->part.P == 1)
-    for (int l = 1; l < A->nlev; ++l)
-      if (A->L[l].n <= A->prm.tail) { A->tail_l0 = l; break; }
-  if (A->tail_l0 >= 0) {
-    TailArgs<P> h{};
-    h.nlev = A->nlev; h.wmax = A->prm.wmax; h.wcycle = A->prm.wcycle ? 1 : 0; h.sweeps = A->prm.sweeps;
-    h.omega = (P)A->prm.omega; h.ainv = A->ainv;
-    for (int l = 0; l < A->nlev; ++l) {
-      const AmgLevelDev<P>& D = A->L[l];
-      // level 0 of an amg32 hierarchy binds coef / diag per update: the tail never reads level 0
-      h.L[l] = TailLevel<P>{D.n, D.ms_ptr, D.ms_len, D.mnb, D.coef, D.diag, D.il1, D.agg, D.mem_ptr, D.mem,
-                            D.x, D.b, D.r, D.t, D.e, D.r2};
-    }
-    std::vector<TailArgs<P>> hv(1, h);
-    if ((st = A->up(&A->d_tail, hv))) return st;
-    A->tail_cs = A->prm.tail_cluster;
-  }
   return DFVM_OK;
 }
 
@@ -490,46 +447,39 @@ __global__ void k_gal_diag(int n, const int* __restrict__ mp, const int* __restr
   }
 }
 
+__device__ __forceinline__ int slot_row(const SellView& S, int q) { return S.perm ? __ldg(&S.perm[q]) : q; }
+
 // inverse l1 diagonal: 1 / (a_ii + sum_j |a_ij|) over the row's SELL entries
 // (stored inverted: the smoothers multiply, no fp64 division per gather)
 template <class T>
-__global__ void k_il1(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                      const T* __restrict__ coef, const T* __restrict__ diag, T* __restrict__ il1) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    const int s = r >> 5, lane = r & 31;
+__global__ void k_il1(int n, SellView S, const T* __restrict__ coef, const T* __restrict__ diag, T* __restrict__ il1) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int r = slot_row(S, q), sl = q >> 5, lane = q & 31;
     T a = diag[r];
-    for (int j = 0; j < ms_len[s]; ++j) a += fabs(coef[ms_ptr[s] + 32 * j + lane]);
+    for (int j = 0; j < S.ms_len[sl]; ++j) a += fabs(coef[S.ms_ptr[sl] + 32 * j + lane]);
     il1[r] = T(1) / a;
   }
 }
 
-// Loads of vectors a kernel may itself have written earlier (the cluster
-// tail re-reads level vectors across phases: plain loads after the cluster
-// barrier, which flushes L1; never the non-coherent path).  LdDef is the
-// launched kernels' plain dereference.
-struct LdDef { template <class U> __device__ __forceinline__ static U ld(const U* p) { return *p; } };
-struct LdCoh { template <class U> __device__ __forceinline__ static U ld(const U* p) { return __ldcg(p); } };
-
-template <class T, class LD = LdDef>
-__device__ __forceinline__ T row_apply(int r, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                                       const int* __restrict__ mnb, const T* __restrict__ coef,
-                                       const T* __restrict__ diag, const T* x) {
-  const int s = r >> 5, lane = r & 31;
-  const int len = ms_len[s], base = ms_ptr[s] + lane;
-  T acc = diag[r] * LD::ld(&x[r]);
+template <class T>
+__device__ __forceinline__ T row_apply(const SellView& S, int q, int r, const T* __restrict__ coef,
+                                       const T* __restrict__ diag, const T* __restrict__ x) {
+  const int sl = q >> 5, lane = q & 31;
+  const int len = S.ms_len[sl], base = S.ms_ptr[sl] + lane;
+  T acc = diag[r] * x[r];
   int j = 0;
   for (; j + 4 <= len; j += 4) {
     T a[4];
     int c[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&mnb[base + 32 * (j + u)]); }
+    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&S.mnb[base + 32 * (j + u)]); }
     T v[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = LD::ld(&x[c[u]]);
+    for (int u = 0; u < 4; ++u) v[u] = x[c[u]];
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
   }
-  for (; j < len; ++j) acc += __ldg(&coef[base + 32 * j]) * LD::ld(&x[__ldg(&mnb[base + 32 * j])]);
+  for (; j < len; ++j) acc += __ldg(&coef[base + 32 * j]) * x[__ldg(&S.mnb[base + 32 * j])];
   return acc;
 }
 
@@ -537,14 +487,13 @@ __device__ __forceinline__ T row_apply(int r, const int* __restrict__ ms_ptr, co
 // r_i = b_i - (A x0)_i with x0 of the neighbours formed on the fly.  Loads in
 // batches of 4 entries (columns + coefficients, then the gathered b and 1/d1),
 // accumulation in entry order.
-template <class T, class LD = LdDef>
-__device__ __forceinline__ void pre_resid_row(int i, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                                              const int* __restrict__ mnb, const T* __restrict__ coef,
+template <class T>
+__device__ __forceinline__ void pre_resid_row(const SellView& S, int q, int i, const T* __restrict__ coef,
                                               const T* __restrict__ diag, const T* __restrict__ il1,
-                                              const T* b, T& x0, T& r) {
-  const int s = i >> 5, lane = i & 31;
-  const int len = ms_len[s], base = ms_ptr[s] + lane;
-  const T bi = LD::ld(&b[i]);
+                                              const T* __restrict__ b, T& x0, T& r) {
+  const int sl = q >> 5, lane = q & 31;
+  const int len = S.ms_len[sl], base = S.ms_ptr[sl] + lane;
+  const T bi = b[i];
   const T xi = bi * il1[i];
   T acc = diag[i] * xi;
   int j = 0;
@@ -552,50 +501,51 @@ __device__ __forceinline__ void pre_resid_row(int i, const int* __restrict__ ms_
     T a[4], v[4];
     int c[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&mnb[base + 32 * (j + u)]); }
+    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&S.mnb[base + 32 * (j + u)]); }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = LD::ld(&b[c[u]]) * il1[c[u]];
+    for (int u = 0; u < 4; ++u) v[u] = b[c[u]] * il1[c[u]];
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
   }
   for (; j < len; ++j) {
-    const int c = __ldg(&mnb[base + 32 * j]);
-    acc += __ldg(&coef[base + 32 * j]) * (LD::ld(&b[c]) * il1[c]);
+    const int c = __ldg(&S.mnb[base + 32 * j]);
+    acc += __ldg(&coef[base + 32 * j]) * (b[c] * il1[c]);
   }
   x0 = xi;
   r = bi - acc;
 }
 // One row of the fused prolongation + post-smooth: t = x0 + w x_c[agg] (on
 // the fly for the row and its neighbours), returns t_i + (b - A t)_i / d1_i.
-template <class T, class LD = LdDef>
-__device__ __forceinline__ T prolong_smooth_row(int i, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                                                const int* __restrict__ mnb, const T* __restrict__ coef,
+template <class T>
+__device__ __forceinline__ T prolong_smooth_row(const SellView& S, int q, int i, const T* __restrict__ coef,
                                                 const T* __restrict__ diag, const T* __restrict__ il1,
-                                                const int* __restrict__ agg, const T* xc, T w,
-                                                const T* x0, const T* b) {
-  const int s = i >> 5, lane = i & 31;
-  const int len = ms_len[s], base = ms_ptr[s] + lane;
-  const T ti = LD::ld(&x0[i]) + w * LD::ld(&xc[agg[i]]);
+                                                const int* __restrict__ agg, const T* __restrict__ xc, T w,
+                                                const T* __restrict__ x0, const T* __restrict__ b) {
+  const int sl = q >> 5, lane = q & 31;
+  const int len = S.ms_len[sl], base = S.ms_ptr[sl] + lane;
+  const T ti = x0[i] + w * xc[agg[i]];
   T acc = diag[i] * ti;
   int j = 0;
   for (; j + 4 <= len; j += 4) {
     T a[4], v[4];
     int c[4], g[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&mnb[base + 32 * (j + u)]); }
+    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&S.mnb[base + 32 * (j + u)]); }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) { g[u] = agg[c[u]]; v[u] = LD::ld(&x0[c[u]]); }
+    for (int u = 0; u < 4; ++u) { g[u] = agg[c[u]]; v[u] = x0[c[u]]; }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = v[u] + w * LD::ld(&xc[g[u]]);
+    for (int u = 0; u < 4; ++u) v[u] = v[u] + w * xc[g[u]];
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
   }
   for (; j < len; ++j) {
-    const int c = __ldg(&mnb[base + 32 * j]);
-    acc += __ldg(&coef[base + 32 * j]) * (LD::ld(&x0[c]) + w * LD::ld(&xc[agg[c]]));
+    const int c = __ldg(&S.mnb[base + 32 * j]);
+    acc += __ldg(&coef[base + 32 * j]) * (x0[c] + w * xc[agg[c]]);
   }
-  return ti + (LD::ld(&b[i]) - acc) * il1[i];
+  return ti + (b[i] - acc) * il1[i];
 }
+
+#define AMG_SLOT_LOOP(n) for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < (n); q += gridDim.x * blockDim.x)
 
 // x = b / d1 (pre-smoothing from a zero guess); b in the caller's type TB
 template <class P, class TB, class TX>
@@ -607,12 +557,13 @@ __global__ void k_amg_pre(int n, const TB* __restrict__ b, const P* __restrict__
 }
 // r = b - A x
 template <class P, class TB>
-__global__ void k_amg_resid(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                            const int* __restrict__ mnb, const P* __restrict__ coef, const P* __restrict__ diag,
+__global__ void k_amg_resid(int n, SellView S, const P* __restrict__ coef, const P* __restrict__ diag,
                             const P* __restrict__ x, const TB* __restrict__ b, P* __restrict__ r, const int* done) {
   if (*done) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    r[i] = (P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x);
+  AMG_SLOT_LOOP(n) {
+    const int i = slot_row(S, q);
+    r[i] = (P)b[i] - row_apply(S, q, i, coef, diag, x);
+  }
 }
 // b_c[I] = sum over the aggregate's members of r_f
 template <class T>
@@ -635,14 +586,14 @@ __global__ void k_amg_prolong(int n, const int* __restrict__ agg, const T* __res
 // fused pre-smooth + residual (rows without ghost columns): x0 = b / d1 for
 // the row and, on the fly, for every neighbour; writes x0 and r = b - A x0
 template <class T>
-__global__ void k_amg_pre_resid(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                                const int* __restrict__ mnb, const T* __restrict__ coef, const T* __restrict__ diag,
+__global__ void k_amg_pre_resid(int n, SellView S, const T* __restrict__ coef, const T* __restrict__ diag,
                                 const T* __restrict__ il1, const T* __restrict__ b, T* __restrict__ x0,
                                 T* __restrict__ r, const int* done) {
   if (*done) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  AMG_SLOT_LOOP(n) {
+    const int i = slot_row(S, q);
     T xv, rv;
-    pre_resid_row(i, ms_ptr, ms_len, mnb, coef, diag, il1, b, xv, rv);
+    pre_resid_row(S, q, i, coef, diag, il1, b, xv, rv);
     x0[i] = xv;
     r[i] = rv;
   }
@@ -650,17 +601,16 @@ __global__ void k_amg_pre_resid(int n, const int* __restrict__ ms_ptr, const int
 // fused prolongation + post-smooth: t = x0 + w P x_c (on the fly for the row
 // and its neighbours), out = t + (b - A t) / d1
 template <class T>
-__global__ void k_amg_prolong_smooth(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                                     const int* __restrict__ mnb, const T* __restrict__ coef,
-                                     const T* __restrict__ diag, const T* __restrict__ il1,
-                                     const int* __restrict__ agg, const T* __restrict__ xc, T w,
-                                     const T* __restrict__ x0, const T* __restrict__ b, T* __restrict__ out,
+__global__ void k_amg_prolong_smooth(int n, SellView S, const T* __restrict__ coef, const T* __restrict__ diag,
+                                     const T* __restrict__ il1, const int* __restrict__ agg, const T* __restrict__ xc,
+                                     T w, const T* __restrict__ x0, const T* __restrict__ b, T* __restrict__ out,
                                      const int* done) {
   if (*done) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    out[i] = prolong_smooth_row(i, ms_ptr, ms_len, mnb, coef, diag, il1, agg, xc, w, x0, b);
+  AMG_SLOT_LOOP(n) {
+    const int i = slot_row(S, q);
+    out[i] = prolong_smooth_row(S, q, i, coef, diag, il1, agg, xc, w, x0, b);
+  }
 }
-
 
 // x += e
 template <class T>
@@ -670,26 +620,27 @@ __global__ void k_amg_add(int n, const T* __restrict__ e, T* __restrict__ x, con
 }
 // out = x + (b - A x) / d1   (b in TB, out in TO: level 0 reads / writes the PCG's type)
 template <class P, class TB, class TO>
-__global__ void k_amg_smooth(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                             const int* __restrict__ mnb, const P* __restrict__ coef, const P* __restrict__ diag,
+__global__ void k_amg_smooth(int n, SellView S, const P* __restrict__ coef, const P* __restrict__ diag,
                              const P* __restrict__ il1, const P* __restrict__ x, const TB* __restrict__ b,
                              TO* __restrict__ out, const int* done) {
   if (*done) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    out[i] = (TO)(x[i] + ((P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x)) * il1[i]);
+  AMG_SLOT_LOOP(n) {
+    const int i = slot_row(S, q);
+    out[i] = (TO)(x[i] + ((P)b[i] - row_apply(S, q, i, coef, diag, x)) * il1[i]);
+  }
 }
 // level-0 post-smoother with the PCG's r.z folded in: z = t + (r - A t) / d1
 // and the deterministic grid sum of r_i z_i (fp64) driving control step `kind`
 template <class P, class T>
-__global__ void __launch_bounds__(kThreads) k_amg_smooth_dot(int n, const int* __restrict__ ms_ptr,
-    const int* __restrict__ ms_len, const int* __restrict__ mnb, const P* __restrict__ coef, const P* __restrict__ diag,
-    const P* __restrict__ il1, const P* __restrict__ x, const T* __restrict__ b, T* __restrict__ out, const int* done,
-    double* partials, unsigned* ticket, KCtl* ctl, Red red, int kind) {
+__global__ void __launch_bounds__(kThreads) k_amg_smooth_dot(int n, SellView S, const P* __restrict__ coef,
+    const P* __restrict__ diag, const P* __restrict__ il1, const P* __restrict__ x, const T* __restrict__ b,
+    T* __restrict__ out, const int* done, double* partials, unsigned* ticket, KCtl* ctl, Red red, int kind) {
   if (*done) return;
   double v[1] = {0};
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  AMG_SLOT_LOOP(n) {
+    const int i = slot_row(S, q);
     const T bi = b[i];
-    const T zi = (T)(x[i] + ((P)bi - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, x)) * il1[i]);
+    const T zi = (T)(x[i] + ((P)bi - row_apply(S, q, i, coef, diag, x)) * il1[i]);
     out[i] = zi;
     v[0] += (double)bi * (double)zi;
   }
@@ -699,8 +650,7 @@ __global__ void __launch_bounds__(kThreads) k_amg_smooth_dot(int n, const int* _
 
 // coarsest level: `sweeps` l1-Jacobi sweeps from zero, one block, in shared memory
 template <class P, class TB, class TO>
-__global__ void __launch_bounds__(1024) k_amg_coarse(int n, const int* __restrict__ ms_ptr, const int* __restrict__ ms_len,
-                                                    const int* __restrict__ mnb, const P* __restrict__ coef,
+__global__ void __launch_bounds__(1024) k_amg_coarse(int n, SellView S, const P* __restrict__ coef,
                                                     const P* __restrict__ diag, const P* __restrict__ il1,
                                                     const TB* __restrict__ b, TO* __restrict__ xout, int sweeps,
                                                     const int* done) {
@@ -710,8 +660,10 @@ __global__ void __launch_bounds__(1024) k_amg_coarse(int n, const int* __restric
   __syncthreads();
   int cur = 0;
   for (int it = 1; it < sweeps; ++it) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-      xs[cur ^ 1][i] = xs[cur][i] + ((P)b[i] - row_apply(i, ms_ptr, ms_len, mnb, coef, diag, xs[cur])) * il1[i];
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+      const int i = slot_row(S, q);
+      xs[cur ^ 1][i] = xs[cur][i] + ((P)b[i] - row_apply(S, q, i, coef, diag, xs[cur])) * il1[i];
+    }
     __syncthreads();
     cur ^= 1;
   }
@@ -723,19 +675,18 @@ __global__ void __launch_bounds__(1024) k_amg_coarse(int n, const int* __restric
 // an SPD operator is SPD).  Step k: row k <- row k / a_kk (with a_kk <- 1 first),
 // row i <- row i - a_ik row k (with a_ik <- 0 first).
 template <class P>
-__global__ void __launch_bounds__(1024) k_amg_dense_inv(int n, const int* __restrict__ ms_ptr,
-                                                        const int* __restrict__ ms_len, const int* __restrict__ mnb,
-                                                        const P* __restrict__ coef, const P* __restrict__ diag,
-                                                        P* __restrict__ A) {
+__global__ void __launch_bounds__(1024) k_amg_dense_inv(int n, SellView S, const P* __restrict__ coef,
+                                                        const P* __restrict__ diag, P* __restrict__ A) {
   __shared__ P colk[kDirectMax], rowk[kDirectMax];
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) A[e] = P(0);
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {      // thread i owns row i
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {      // thread q owns slot q (row i)
+    const int i = slot_row(S, q);
     A[(size_t)i * n + i] = diag[i];
-    const int s = i >> 5, lane = i & 31;
-    for (int j = 0; j < ms_len[s]; ++j) {
-      const int p = ms_ptr[s] + 32 * j + lane;
-      A[(size_t)i * n + mnb[p]] += coef[p];
+    const int sl = q >> 5, lane = q & 31;
+    for (int j = 0; j < S.ms_len[sl]; ++j) {
+      const int p = S.ms_ptr[sl] + 32 * j + lane;
+      A[(size_t)i * n + S.mnb[p]] += coef[p];
     }
   }
   __syncthreads();
@@ -776,131 +727,6 @@ __global__ void __launch_bounds__(1024) k_amg_dense(int n, const P* __restrict__
   dense_solve_block<P, TB, TO>(n, Ai, b, x);
 }
 
-// ------------------------------------------------------------ cluster tail
-// The coarse levels below a few 1e5 rows are latency-bound: each launched
-// kernel moves well under a megabyte.  k_amg_tail runs the
-// whole coarse correction of level l0 (its first visit, and for the W-cycle
-// the residual, the second visit and the add) as ONE launch of one
-// thread-block cluster: every phase of the recursion (pre-smooth+residual,
-// restriction, dense coarsest solve, prolongation+post-smooth, W residual /
-// add) is a cluster-strided loop over the level's rows followed by a cluster
-// barrier (barrier.cluster arrive.release / wait.acquire; it also
-// invalidates L1, so the next phase's plain loads see the other CTAs'
-// writes).  The per-row arithmetic is the launched kernels' row functions,
-// so the result is bitwise that of the launched cycle.
-constexpr int kTailThreads = 512;
-
-__device__ __forceinline__ void tail_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-template <class P>
-__device__ void tail_cycle(const TailArgs<P>& A, int l, const P* b, P* x, int gt, int gs) {
-  const TailLevel<P>& F = A.L[l];
-  if (l == A.nlev - 1) {
-    if (A.ainv) {
-      // = dense_solve_block, rows over the cluster's warps
-      const int lane = gt & 31;
-      for (int i = gt >> 5; i < F.n; i += gs >> 5) {
-        P acc = P(0);
-        for (int j = lane; j < F.n; j += 32) acc += A.ainv[(size_t)i * F.n + j] * LdCoh::ld(&b[j]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) x[i] = acc;
-      }
-      tail_sync();
-    } else {
-      // = k_amg_coarse: sweeps l1-Jacobi steps from zero, ping-pong x / t
-      // (start buffer chosen so the last step lands in x)
-      P* cur = ((A.sweeps - 1) % 2 == 0) ? x : F.t;
-      P* nxt = cur == x ? F.t : x;
-      for (int i = gt; i < F.n; i += gs) cur[i] = LdCoh::ld(&b[i]) * F.il1[i];
-      tail_sync();
-      for (int it = 1; it < A.sweeps; ++it) {
-        for (int i = gt; i < F.n; i += gs)
-          nxt[i] = LdCoh::ld(&cur[i]) +
-                   (LdCoh::ld(&b[i]) - row_apply<P, LdCoh>(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, cur)) * F.il1[i];
-        tail_sync();
-        P* tmp = cur; cur = nxt; nxt = tmp;
-      }
-    }
-    return;
-  }
-  const TailLevel<P>& C = A.L[l + 1];
-  for (int i = gt; i < F.n; i += gs) {
-    P xv, rv;
-    pre_resid_row<P, LdCoh>(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, xv, rv);
-    F.t[i] = xv;
-    F.r[i] = rv;
-  }
-  tail_sync();
-  for (int I = gt; I < C.n; I += gs) {
-    P sum = P(0);
-    for (int k = C.mem_ptr[I]; k < C.mem_ptr[I + 1]; ++k) sum += LdCoh::ld(&F.r[C.mem[k]]);
-    C.b[I] = sum;
-  }
-  tail_sync();
-  tail_cycle(A, l + 1, C.b, C.x, gt, gs);
-  if (A.wcycle && l + 1 < A.nlev - 1 && l + 1 <= A.wmax) {
-    for (int I = gt; I < C.n; I += gs)
-      C.r2[I] = LdCoh::ld(&C.b[I]) - row_apply<P, LdCoh>(I, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x);
-    tail_sync();
-    tail_cycle(A, l + 1, C.r2, C.e, gt, gs);
-    for (int I = gt; I < C.n; I += gs) C.x[I] = LdCoh::ld(&C.x[I]) + LdCoh::ld(&C.e[I]);
-    tail_sync();
-  }
-  for (int i = gt; i < F.n; i += gs)
-    x[i] = prolong_smooth_row<P, LdCoh>(i, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.agg, C.x, A.omega,
-                                        F.t, b);
-  tail_sync();
-}
-
-// the coarse correction of level l0 (its rhs L[l0].b restricted by the caller)
-template <class P>
-__global__ void __launch_bounds__(kTailThreads) k_amg_tail(const TailArgs<P>* __restrict__ Ap, int l0, const int* done) {
-  if (*done) return;     // uniform over the cluster (nothing in here writes done)
-  const TailArgs<P>& A = *Ap;
-  const int gs = gridDim.x * blockDim.x;
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const TailLevel<P>& C = A.L[l0];
-  tail_cycle(A, l0, C.b, C.x, gt, gs);
-  if (A.wcycle && l0 < A.nlev - 1 && l0 <= A.wmax) {
-    for (int I = gt; I < C.n; I += gs)
-      C.r2[I] = LdCoh::ld(&C.b[I]) - row_apply<P, LdCoh>(I, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x);
-    tail_sync();
-    tail_cycle(A, l0, C.r2, C.e, gt, gs);
-    for (int I = gt; I < C.n; I += gs) C.x[I] = LdCoh::ld(&C.x[I]) + LdCoh::ld(&C.e[I]);
-  }
-}
-
-// launch of the tail as one cluster of A->tail_cs CTAs (falls back to the
-// portable size 8 if the non-portable 16 is refused)
-template <class P>
-static dfvm_status launch_tail(AmgH<P>* A, const int* done, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_amg_tail<P>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr_set = true;
-  }
-  for (;;) {
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)A->tail_cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3((unsigned)A->tail_cs);
-    cfg.blockDim = dim3(kTailThreads);
-    cfg.stream = s;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_amg_tail<P>, (const TailArgs<P>*)A->d_tail, A->tail_l0, done);
-    if (e == cudaSuccess) return DFVM_OK;
-    cudaGetLastError();
-    if (A->tail_cs > 8) { A->tail_cs = 8; continue; }
-    return cuda_error(e, "cudaLaunchKernelEx(k_amg_tail)");
-  }
-}
-
 // ------------------------------------------------------------ host drivers
 // Algorithmic bytes per launch: n rows, Z real off-diagonal
 // entries (column 4 B + coefficient pb), vb bytes of the PCG vectors (T),
@@ -921,7 +747,7 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
     *nl += 2;
   }
   PLAUNCH(pr, "k_il1", 0, (4 + pb) * (double)L0.nnz + (4 + 2 * pb) * L0.n, s,
-          (k_il1<P><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, L0.ms_ptr, L0.ms_len, L0.coef, L0.diag, L0.il1)));
+          (k_il1<P><<<grid_for(L0.n), kThreads, 0, s>>>(L0.n, L0.sv(), L0.coef, L0.diag, L0.il1)));
   ++*nl;
   for (int l = 1; l < A->nlev; ++l) {
     AmgLevelDev<P>& F = A->L[l - 1];
@@ -932,13 +758,13 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
             (k_gal_diag<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, C.dg_ptr, C.dg_idx, F.diag, F.coef,
                                                                C.diag_own)));
     PLAUNCH(pr, "k_il1", l, (4 + pb) * (double)C.nnz + (4 + 2 * pb) * C.n, s,
-            (k_il1<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.coef, C.diag, C.il1)));
+            (k_il1<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.il1)));
     *nl += 3;
   }
   if (A->ainv) {
     const AmgLevelDev<P>& C = A->L[A->nlev - 1];
     PLAUNCH(pr, "k_amg_dense_inv", A->nlev - 1, 2 * pb * (double)C.n * C.n, s,
-            (k_amg_dense_inv<P><<<1, 1024, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, A->ainv)));
+            (k_amg_dense_inv<P><<<1, 1024, 0, s>>>(C.n, C.sv(), C.coef, C.diag, A->ainv)));
     ++*nl;
   }
   DFVM_CUDA(cudaGetLastError());
@@ -964,7 +790,7 @@ static void coarsest(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaS
     ++*nl;
   } else if (F.n <= kCoarseMax) {
     PLAUNCH(pr, "k_amg_coarse", l, (4 + pb) * (double)F.nnz + 4 * pb * n, s,
-            (k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, x,
+            (k_amg_coarse<P, P, P><<<1, 1024, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, b, x,
                                                      A->prm.sweeps, done)));
     ++*nl;
   } else {
@@ -978,44 +804,12 @@ static void coarsest(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaS
     const int sw = A->prm.sweeps + (A->prm.sweeps % 2 == 0 ? 1 : 0);
     for (int it = 1; it < sw; ++it) {
       PLAUNCH(pr, "k_amg_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
-              (k_amg_smooth<P, P, P><<<g, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, cur,
+              (k_amg_smooth<P, P, P><<<g, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, cur,
                                                             b, nxt, done)));
       std::swap(cur, nxt);
     }
     *nl += sw;
   }
-}
-
-// algorithmic bytes of one tail launch: every matrix / vector pass the
-// launched kernels of the same sub-cycle would make (row metadata 4 B/row,
-// entries 4 + pb B, the vectors each pass touches), summed over the
-// recursion
-template <class P>
-static double tail_pass_bytes(const AmgH<P>* A, int l, bool& ok) {
-  const double pb = sizeof(P);
-  const AmgLevelDev<P>& F = A->L[l];
-  if (l == A->nlev - 1)
-    return A->ainv ? pb * (double)F.n * F.n + 2 * pb * F.n
-                   : A->prm.sweeps * ((4 + pb) * (double)F.nnz + 4 * pb * F.n);
-  const AmgLevelDev<P>& C = A->L[l + 1];
-  double b = 4 * (double)F.n + (4 + pb) * (double)F.nnz + 5 * pb * F.n;            // pre_resid
-  b += (4 + pb) * ((double)F.n + C.n);                                               // restrict
-  b += tail_pass_bytes(A, l + 1, ok);
-  if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax)
-    b += 4 * (double)C.n + (4 + pb) * (double)C.nnz + 4 * pb * C.n + tail_pass_bytes(A, l + 1, ok) + 3 * pb * C.n;
-  b += 4 * (double)F.n + (4 + pb) * (double)F.nnz + (4 + 5 * pb) * F.n + pb * C.n;  // prolong_smooth
-  return b;
-}
-template <class P>
-static double tail_bytes(const AmgH<P>* A) {
-  bool ok = true;
-  const int l = A->tail_l0;
-  const double pb = sizeof(P);
-  const AmgLevelDev<P>& C = A->L[l];
-  double b = tail_pass_bytes(A, l, ok);
-  if (A->prm.wcycle && l < A->nlev - 1 && l <= A->prm.wmax)
-    b += 4 * (double)C.n + (4 + pb) * (double)C.nnz + 4 * pb * C.n + tail_pass_bytes(A, l, ok) + 3 * pb * C.n;
-  return b;
 }
 
 // Coarse level l >= 1 (no ghost columns): x = M_l^-1 b from a zero guess with
@@ -1037,42 +831,37 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
   const bool fused = l >= A->prm.fused_from;
   if (fused) {
     PLAUNCH(pr, "k_amg_pre_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
-            (k_amg_pre_resid<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, b, F.t,
+            (k_amg_pre_resid<P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, b, F.t,
                                                         F.r, done)));
   } else {
     PLAUNCH(pr, "k_amg_pre", l, 3 * pb * n, s, (k_amg_pre<P, P, P><<<gF, kThreads, 0, s>>>(F.n, b, F.il1, F.t, done)));
     PLAUNCH(pr, "k_amg_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 4 * pb * n, s,
-            (k_amg_resid<P, P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.t, b, F.r,
+            (k_amg_resid<P, P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.t, b, F.r,
                                                        done)));
     ++*nl;
   }
   PLAUNCH(pr, "k_amg_restrict", l, (4 + pb) * (n + nc), s,
           (k_amg_restrict<P><<<gC, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
   *nl += 2;
-  if (l + 1 == A->tail_l0) {
-    PLAUNCH(pr, "k_amg_tail", l + 1, tail_bytes(A), s, launch_tail(A, done, s));
-    ++*nl;
-  } else {
   cycle_coarse(A, l + 1, C.b, C.x, done, s, nl);
   if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax) {
     PLAUNCH(pr, "k_amg_resid", l + 1, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
-            (k_amg_resid<P, P><<<gC, kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b, C.r2,
+            (k_amg_resid<P, P><<<gC, kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.x, C.b, C.r2,
                                                        done)));
     cycle_coarse(A, l + 1, C.r2, C.e, done, s, nl);
     PLAUNCH(pr, "k_amg_add", l + 1, 3 * pb * nc, s, (k_amg_add<P><<<gC, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
     *nl += 2;
   }
-  }
   if (fused) {
     PLAUNCH(pr, "k_amg_prolong_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + (4 + 5 * pb) * n + pb * nc, s,
-            (k_amg_prolong_smooth<P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1,
+            (k_amg_prolong_smooth<P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1,
                                                              F.agg, C.x, w, F.t, b, x, done)));
   } else {
     // F.r is free after the restriction: the prolonged t = x0 + w x_c[agg] goes there
     PLAUNCH(pr, "k_amg_prolong", l, (4 + 2 * pb) * n + pb * nc, s,
             (k_amg_prolong<P><<<gF, kThreads, 0, s>>>(F.n, F.agg, C.x, F.t, F.r, w, done)));
     PLAUNCH(pr, "k_amg_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
-            (k_amg_smooth<P, P, P><<<gF, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.r,
+            (k_amg_smooth<P, P, P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, F.r,
                                                            b, x, done)));
     ++*nl;
   }
@@ -1106,7 +895,7 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
       if ((e = halo_exchange_p(A->m, F.x, 1, f64, s)) || (e = halo_exchange_p(A->m, F.t, 1, f64, s))) return e;
     } else {
       PLAUNCH(pr, "k_amg_coarse", 0, (4 + pb) * (double)F.nnz + 4 * pb * n, s,
-              (k_amg_coarse<P, T, T><<<1, 1024, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, r, z,
+              (k_amg_coarse<P, T, T><<<1, 1024, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, r, z,
                                                        A->prm.sweeps, done)));
     }
     ++*nl;
@@ -1123,25 +912,20 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   if ((e = halo_exchange_p(A->m, F.x, 1, f64, s))) return e;
   if (ev) record_event(ev[0], s);
   PLAUNCH(pr, "k_amg_resid", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + vb) * n, s,
-          (k_amg_resid<P, T><<<g0, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.x, r, F.r,
+          (k_amg_resid<P, T><<<g0, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.x, r, F.r,
                                                      done)));
   if (ev) record_event(ev[1], s);
   PLAUNCH(pr, "k_amg_restrict", 0, (4 + pb) * (n + nc), s,
           (k_amg_restrict<P><<<g1, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
   *nl += 2;
-  if (A->tail_l0 == 1) {
-    PLAUNCH(pr, "k_amg_tail", 1, tail_bytes(A), s, launch_tail(A, done, s));
-    ++*nl;
-  } else {
   cycle_coarse(A, 1, C.b, C.x, done, s, nl);
   if (A->prm.wcycle && 1 < A->nlev - 1 && 1 <= A->prm.wmax) {
     PLAUNCH(pr, "k_amg_resid", 1, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
-            (k_amg_resid<P, P><<<g1, kThreads, 0, s>>>(C.n, C.ms_ptr, C.ms_len, C.mnb, C.coef, C.diag, C.x, C.b,
+            (k_amg_resid<P, P><<<g1, kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.x, C.b,
                                                        C.r2, done)));
     cycle_coarse(A, 1, C.r2, C.e, done, s, nl);
     PLAUNCH(pr, "k_amg_add", 1, 3 * pb * nc, s, (k_amg_add<P><<<g1, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
     *nl += 2;
-  }
   }
   PLAUNCH(pr, "k_amg_prolong", 0, (4 + 2 * pb) * n + pb * nc, s,
           (k_amg_prolong<P><<<g0, kThreads, 0, s>>>(F.n, F.agg, C.x, F.x, F.t, (P)A->prm.omega, done)));
@@ -1149,13 +933,13 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   if (ev) record_event(ev[2], s);
   if (dot) {
     PLAUNCH(pr, "k_amg_smooth_dot", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + 2 * vb) * n, s,
-            (k_amg_smooth_dot<P, T><<<g0, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1,
+            (k_amg_smooth_dot<P, T><<<g0, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1,
                                                             F.t, r, z, done, dot->partials, dot->ticket, dot->ctl,
                                                             dot->red, dot->kind)));
     if (dot_done) *dot_done = true;
   } else {
     PLAUNCH(pr, "k_amg_smooth", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + 2 * vb) * n, s,
-            (k_amg_smooth<P, T, T><<<g0, kThreads, 0, s>>>(F.n, F.ms_ptr, F.ms_len, F.mnb, F.coef, F.diag, F.il1, F.t,
+            (k_amg_smooth<P, T, T><<<g0, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, F.t,
                                                            r, z, done)));
   }
   if (ev) record_event(ev[3], s);

@@ -414,11 +414,12 @@ def test_c1_cavity_100_steps_trajectory():
 
 @pytest.mark.parametrize("precond", ["amg", "amg32"])
 @pytest.mark.parametrize("size", ["pipe_big", "c5_nz6"])
-def test_amg_cluster_tail_bitwise(precond, size, monkeypatch):
-    # the coarse levels below DFVM_AMG_TAIL rows run as one thread-block
-    # cluster kernel per visit (k_amg_tail); it must reproduce the launched
-    # W-cycle bit for bit (same row arithmetic, same order), hence identical
-    # fields and iteration counts
+def test_amg_storage_and_kernel_variants_bitwise(precond, size, monkeypatch):
+    # the coarse-level SELL storage order (DFVM_AMG_PERM: rows sorted by
+    # length within windows of 256 slots) and the fused / unfused coarse
+    # kernels (DFVM_AMG_FUSED_FROM) change the memory traffic only: same rows,
+    # same per-row arithmetic in the same order, hence bitwise equal fields
+    # and identical iteration counts
     import ctypes
     import torch
     import cases
@@ -436,10 +437,10 @@ def test_amg_cluster_tail_bitwise(precond, size, monkeypatch):
     s = torch.cuda.Stream()
     sp = ctypes.c_void_p(s.cuda_stream)
     out = []
-    for var, val in (("DFVM_AMG_TAIL", "0"), ("DFVM_AMG_TAIL", "100000"), ("DFVM_AMG_TAIL", "4000"),
-                     ("DFVM_AMG_FUSED_FROM", "3")):
-        monkeypatch.delenv("DFVM_AMG_TAIL", raising=False)
-        monkeypatch.setenv(var, val)
+    for env in ({"DFVM_AMG_PERM": "0", "DFVM_AMG_FUSED_FROM": "1"}, {"DFVM_AMG_PERM": "1", "DFVM_AMG_FUSED_FROM": "1"},
+                {"DFVM_AMG_PERM": "1", "DFVM_AMG_FUSED_FROM": "3"}, {"DFVM_AMG_PERM": "0", "DFVM_AMG_FUSED_FROM": "9"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         Sg = mk()
         Ug, pg, phig = mg.field("cells", 3, U0, sp), mg.field("cells", 1, p0, sp), mg.field("flux", 1, phi0, sp)
         reps = [Sg.step(Ug, pg, phig, sp) for _ in range(2)]
