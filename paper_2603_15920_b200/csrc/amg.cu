@@ -68,7 +68,12 @@ constexpr int kMaxLevels = 16;
 //   DFVM_AMG_PERM    1: coarse-level SELL storage sorted by row length
 //                    within windows of 256 slots (SELL-32-sigma: rows keep
 //                    their numbers, the hierarchy and results are unchanged,
-//                    padding shrinks); 0: natural order          default 1
+//                    padding shrinks); 0: natural order          default 0
+//                    (C5 round 2: padding 8.4 % on level 1, yet 347.2 ms/step
+//                    against 343.1 ms in natural order — the coarse
+//                    kernels are bound by their gathers, and the permuted
+//                    own-row accesses cost more than the padding saved;
+//                    profiles/r02_amg_sweep2_c5.jsonl)
 //                    (round 1 renumbered the aggregates themselves by
 //                    length instead: that changed the next aggregation
 //                    and cost 0.5 PCG iterations per solve — removed)
@@ -90,7 +95,7 @@ constexpr int kMaxLevels = 16;
 //                    matrix update, one block), larger ones with
 //                    DFVM_AMG_SWEEPS l1-Jacobi sweeps (0: always sweeps)  default 512
 struct AmgParams {
-  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, perm = 1;
+  int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, perm = 0;
   int fused_from = 3;   // coarse levels >= this use the fused pre_resid / prolong_smooth kernels
   bool wcycle = true;
   double omega = 1.95;  // C5 amg32 (round 2): 344.0 ms, 11.33 it/solve (1.9: 349.6 ms, 11.58; 1.8: 360.2 ms, 12.17)
