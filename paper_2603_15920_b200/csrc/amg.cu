@@ -49,6 +49,8 @@
 namespace dfvm {
 
 dfvm_status halo_exchange_p(dfvm_mesh* m, void* data, int nc, bool f64, cudaStream_t s);
+dfvm_status halo_exchange_lists(dfvm_mesh* m, HaloLists& L, void* data, int nc, bool f64, cudaStream_t s);
+dfvm_status allgather_f64(dfvm_mesh* m, const double* local, double* gathered, int n, cudaStream_t s);
 bool comm_is_local(const dfvm_comm* c);
 
 constexpr int kCoarseMax = 2048;     // shared-memory capacity of the one-block coarse solve
@@ -132,8 +134,31 @@ struct HostLevel {
   std::vector<int> perm, slot_of;   // SELL slot -> row and back (empty: identity)
   // CSR view of the real entries: (col, SELL position), owned cols only
   std::vector<int> rp, col, pos;
+  // several ranks: ghost rows [n, n + ng) (owner rank, owner-local index),
+  // the halo lists, and the CSR of the entries with ghost columns
+  int ng = 0;
+  std::vector<int> ghost_peer, ghost_key;
+  HaloLists halo;
+  std::vector<int> grp, gcol, gpos;
   int slot(int r) const { return slot_of.empty() ? r : slot_of[r]; }
 };
+
+// entries of owned rows with ghost columns (c >= n)
+void sell_to_ghost_csr(HostLevel& L) {
+  const int n = L.n;
+  L.grp.assign(n + 1, 0);
+  L.gcol.clear();
+  L.gpos.clear();
+  for (int r = 0; r < n; ++r) {
+    const int q = L.slot(r), s = q / 32, lane = q % 32;
+    for (int j = 0; j < L.ms_len[s]; ++j) {
+      const int p = L.ms_ptr[s] + 32 * j + lane;
+      const int c = L.mnb[p];
+      if (c >= n) { L.gcol.push_back(c); L.gpos.push_back(p); }
+    }
+    L.grp[r + 1] = (int)L.gcol.size();
+  }
+}
 
 void sell_to_csr(HostLevel& L, int n_owned_cols) {
   const int n = L.n;
@@ -210,6 +235,7 @@ struct AmgLevelDev {
   int* agg = nullptr;                             // on the FINE level: fine row -> coarse row
   P *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr;
   P *e = nullptr, *r2 = nullptr;                  // W-cycle: second-visit solution / rhs
+  int n_cells = 0;                                // owned + ghost rows (several ranks)
 };
 
 // hierarchy stored and cycled in type P
@@ -221,9 +247,23 @@ struct AmgH {
   Prof* prof = nullptr;             // per-kernel profile of the caller (may be null)
   AmgLevelDev<P> L[kMaxLevels];
   P* ainv = nullptr;                // dense inverse of the coarsest matrix (column-major n x n), or NULL
+  // several ranks: every level is distributed (owned aggregates of owned
+  // rows, ghost aggregates of the neighbours, a halo per level) and the
+  // coarsest level is solved globally: the ranks' coarsest rows, padded to
+  // n_cmax per rank, form one Np = P n_cmax system, all-gathered and
+  // inverted redundantly on every rank
+  bool dist = false;
+  HaloLists halos[kMaxLevels];
+  bool gdense = false;
+  int n_cmax = 0, Np = 0;
+  double *d_rows = nullptr, *d_all = nullptr, *d_rhs = nullptr, *d_rhs_all = nullptr;
+  int* d_gcol = nullptr;            // coarsest ghost row -> padded global column
   std::vector<void*> allocs;
   int64_t bytes = 0;
-  ~AmgH() { for (void* p : allocs) dev_free(p, nullptr); }
+  ~AmgH() {
+    for (void* p : allocs) dev_free(p, nullptr);
+    for (auto& h : halos) { dev_free(h.d_send, nullptr); dev_free(h.d_send_idx, nullptr); }
+  }
   // legacy-stream allocations / uploads; amg_create synchronises once after
   // the build, before the caller's stream uses any of them
   template <class U>
@@ -395,16 +435,254 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
   return DFVM_OK;
 }
 
+// ---- several ranks: a distributed hierarchy.
+// Aggregation stays rank-local (an aggregate never spans ranks), but every
+// coarse operator is the Galerkin product of the GLOBAL matrix: the
+// couplings through the interface become entries to ghost aggregates of the
+// neighbouring ranks, each level carries a halo, and the coarsest level is
+// solved globally.  So the preconditioner sees the whole domain at every
+// level (round 1's rank-local coarse levels — block Jacobi across ranks —
+// grew the PCG iterations from 13 to 71 per solve at P = 8 on a 12.5M-cell
+// C5 pipe, profiles/r02_scale_iters_c5nz204_rank_local_amg.jsonl).
+// Collective: all ranks build at the same time (host decisions are agreed
+// through all-gathers, so every rank makes the same number of levels and the
+// same halo / all-gather sequence in the cycle).
+static dfvm_status agree_all(dfvm_mesh* m, double v, std::vector<double>& out, cudaStream_t s) {
+  const int P = m->part.P;
+  double *dl = nullptr, *da = nullptr;
+  dfvm_status st;
+  if ((st = dev_alloc_n(&dl, 1, s, false)) || (st = dev_alloc_n(&da, (size_t)P, s, false))) return st;
+  DFVM_CUDA(cudaMemcpyAsync(dl, &v, 8, cudaMemcpyHostToDevice, s));
+  if ((st = allgather_f64(m, dl, da, 1, s))) return st;
+  out.assign(P, 0.0);
+  DFVM_CUDA(cudaMemcpyAsync(out.data(), da, 8 * (size_t)P, cudaMemcpyDeviceToHost, s));
+  DFVM_CUDA(cudaStreamSynchronize(s));
+  dev_free(dl, s);
+  dev_free(da, s);
+  return DFVM_OK;
+}
+
+template <class P, class T>
+static dfvm_status build_dist(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A, cudaStream_t s) {
+  A->m = m;
+  A->dist = true;
+  const Part& Pt = m->part;
+  const int NR = Pt.P;
+  const int64_t Ng = m->H.N;
+  std::vector<HostLevel> H(1);
+  HostLevel& H0 = H[0];
+  H0.n = M.n_own;
+  H0.ms_ptr = m->h_ms_ptr; H0.ms_len = m->h_ms_len; H0.mnb = m->h_mnb;
+  sell_to_csr(H0, M.n_own);
+  sell_to_ghost_csr(H0);
+  H0.ng = (int)Pt.n_ghost;
+  H0.ghost_peer.assign(Pt.ghost_peer.begin(), Pt.ghost_peer.end());
+  H0.ghost_key.resize(H0.ng);
+  for (int k = 0; k < H0.ng; ++k) {
+    const int q = Pt.ghost_peer[k];
+    H0.ghost_key[k] = (int)(Pt.ghost_gid[k] - (int64_t)q * Ng / NR);
+  }
+  H0.halo.n_own = H0.n;
+  H0.halo.peers = Pt.peers;
+  H0.halo.send_off = Pt.peer_send_off;
+  H0.halo.ghost_off = Pt.peer_ghost_off;
+  H0.halo.send_idx.resize(Pt.send_gid.size());
+  for (size_t i = 0; i < Pt.send_gid.size(); ++i) H0.halo.send_idx[i] = (int32_t)(Pt.send_gid[i] - Pt.lo);
+  H0.halo.ready = true;
+  A->halos[0] = H0.halo;
+  AmgLevelDev<P>& L0 = A->L[0];
+  L0.n = M.n_own; L0.n_slices = M.n_slices; L0.n_sell = M.n_minc; L0.nnz = M.nnz; L0.n_cells = M.n_cells;
+  L0.ms_ptr = M.ms_ptr; L0.ms_len = M.ms_len; L0.mnb = M.mnb;
+  dfvm_status st;
+  if ((st = A->zalloc(&L0.il1, M.n_own)) || (st = A->zalloc(&L0.x, M.n_cells)) || (st = A->zalloc(&L0.r, M.n_own)) ||
+      (st = A->zalloc(&L0.t, M.n_cells)))
+    return st;
+  if (!std::is_same<P, T>::value) {
+    if ((st = A->zalloc(&L0.coef_own, (size_t)M.n_minc)) || (st = A->zalloc(&L0.diag_own, M.n_own))) return st;
+    L0.coef = L0.coef_own; L0.diag = L0.diag_own;
+  }
+  // the global coarsest system holds NR * (rows per rank): stop each rank's
+  // coarsening near kDirectMax / NR rows (never below 32)
+  const int target = std::max(32, std::min(A->prm.coarse, kDirectMax / NR));
+  int lev = 0;
+  std::vector<double> votes;
+  int32_t* d_agg = nullptr;
+  while (lev + 1 < kMaxLevels) {
+    HostLevel& F = H[lev];
+    int nc = 0;
+    std::vector<int> agg = aggregate(F, nc);
+    const bool want = F.n > target && nc < F.n * 0.85 && nc >= 32;
+    if ((st = agree_all(m, want ? 1.0 : 0.0, votes, s))) return st;
+    bool all = true;
+    for (double v : votes) all = all && v > 0.5;
+    if (!all) break;
+    // owners' aggregate of every ghost row: one halo exchange of agg (int32 bits)
+    std::vector<int> agg_ext(F.n + F.ng, -1);
+    for (int i = 0; i < F.n; ++i) agg_ext[i] = agg[i];
+    if ((st = dev_alloc_n(&d_agg, (size_t)(F.n + F.ng), s, false))) return st;
+    DFVM_CUDA(cudaMemcpyAsync(d_agg, agg_ext.data(), 4 * (size_t)(F.n + F.ng), cudaMemcpyHostToDevice, s));
+    if ((st = halo_exchange_lists(m, A->halos[lev], d_agg, 1, false, s))) return st;
+    DFVM_CUDA(cudaMemcpyAsync(agg_ext.data(), d_agg, 4 * (size_t)(F.n + F.ng), cudaMemcpyDeviceToHost, s));
+    DFVM_CUDA(cudaStreamSynchronize(s));
+    dev_free(d_agg, s);
+    d_agg = nullptr;
+    // coarse ghosts: (owner, owner's aggregate) of every ghost column, sorted
+    std::vector<std::pair<int, int>> cg;
+    for (size_t k = 0; k < F.gcol.size(); ++k) {
+      const int c = F.gcol[k];
+      cg.push_back({F.ghost_peer[c - F.n], agg_ext[c]});
+    }
+    std::sort(cg.begin(), cg.end());
+    cg.erase(std::unique(cg.begin(), cg.end()), cg.end());
+    auto gidx = [&](int q, int key) {
+      return nc + (int)(std::lower_bound(cg.begin(), cg.end(), std::make_pair(q, key)) - cg.begin());
+    };
+    HostLevel C;
+    C.n = nc;
+    C.ng = (int)cg.size();
+    C.ghost_peer.resize(C.ng);
+    C.ghost_key.resize(C.ng);
+    for (int k = 0; k < C.ng; ++k) { C.ghost_peer[k] = cg[k].first; C.ghost_key[k] = cg[k].second; }
+    // coarse halo: to peer q the aggregates of the fine rows sent to q, from
+    // q the ghost aggregates owned by q (both ascending: the same list)
+    C.halo.n_own = nc;
+    C.halo.peers = F.halo.peers;
+    C.halo.send_off.assign(1, 0);
+    C.halo.ghost_off.assign(1, 0);
+    for (size_t pi = 0; pi < F.halo.peers.size(); ++pi) {
+      const int q = F.halo.peers[pi];
+      std::vector<int> snd;
+      for (int64_t k = F.halo.send_off[pi]; k < F.halo.send_off[pi + 1]; ++k) snd.push_back(agg[F.halo.send_idx[k]]);
+      std::sort(snd.begin(), snd.end());
+      snd.erase(std::unique(snd.begin(), snd.end()), snd.end());
+      for (int v : snd) C.halo.send_idx.push_back(v);
+      C.halo.send_off.push_back((int64_t)C.halo.send_idx.size());
+      int64_t gcount = 0;
+      for (int k = 0; k < C.ng; ++k) gcount += C.ghost_peer[k] == q;
+      C.halo.ghost_off.push_back(C.halo.ghost_off.back() + gcount);
+    }
+    C.halo.ready = true;
+    // members
+    std::vector<int> mem_ptr(nc + 1, 0), mem(F.n);
+    for (int i = 0; i < F.n; ++i) mem_ptr[agg[i] + 1]++;
+    for (int I = 0; I < nc; ++I) mem_ptr[I + 1] += mem_ptr[I];
+    {
+      std::vector<int> pp(mem_ptr.begin(), mem_ptr.end() - 1);
+      for (int i = 0; i < F.n; ++i) mem[pp[agg[i]]++] = i;
+    }
+    // coarse rows: owned columns agg[c], ghost columns their coarse ghost
+    std::vector<int> crow_ptr(nc + 1, 0), ccol, dg_ptr(nc + 1, 0), dg_idx;
+    std::vector<std::vector<int>> gal_lists;
+    std::vector<std::pair<int, int>> buf;
+    for (int I = 0; I < nc; ++I) {
+      buf.clear();
+      for (int q = mem_ptr[I]; q < mem_ptr[I + 1]; ++q) {
+        const int i = mem[q];
+        for (int k = F.rp[i]; k < F.rp[i + 1]; ++k) buf.push_back({agg[F.col[k]], F.pos[k]});
+        for (int k = F.grp[i]; k < F.grp[i + 1]; ++k)
+          buf.push_back({gidx(F.ghost_peer[F.gcol[k] - F.n], agg_ext[F.gcol[k]]), F.gpos[k]});
+      }
+      std::sort(buf.begin(), buf.end());
+      for (size_t k = 0; k < buf.size();) {
+        const int J = buf[k].first;
+        size_t e = k;
+        while (e < buf.size() && buf[e].first == J) ++e;
+        if (J == I) {
+          for (size_t u = k; u < e; ++u) dg_idx.push_back(buf[u].second);
+        } else {
+          ccol.push_back(J);
+          gal_lists.emplace_back();
+          for (size_t u = k; u < e; ++u) gal_lists.back().push_back(buf[u].second);
+        }
+        k = e;
+      }
+      crow_ptr[I + 1] = (int)ccol.size();
+      dg_ptr[I + 1] = (int)dg_idx.size();
+    }
+    const int S = (nc + 31) / 32;
+    C.ms_ptr.assign(S + 1, 0);
+    C.ms_len.assign(S, 0);
+    for (int sl = 0; sl < S; ++sl) {
+      int w = 0;
+      for (int I = sl * 32; I < std::min(nc, sl * 32 + 32); ++I) w = std::max(w, crow_ptr[I + 1] - crow_ptr[I]);
+      C.ms_len[sl] = w;
+      C.ms_ptr[sl + 1] = C.ms_ptr[sl] + 32 * w;
+    }
+    C.mnb.assign(C.ms_ptr[S], 0);
+    std::vector<int> gal_ptr(C.ms_ptr[S] + 1, 0), gal_idx, slot_entry(C.ms_ptr[S], -1);
+    for (int I = 0; I < nc; ++I) {
+      const int sl = I / 32, lane = I % 32;
+      for (int j = 0; j < C.ms_len[sl]; ++j) {
+        const int pp = C.ms_ptr[sl] + 32 * j + lane;
+        const int e = crow_ptr[I] + j;
+        if (e < crow_ptr[I + 1]) { C.mnb[pp] = ccol[e]; slot_entry[pp] = e; }
+        else C.mnb[pp] = I;
+      }
+    }
+    for (int pp = 0; pp < C.ms_ptr[S]; ++pp) {
+      if (slot_entry[pp] >= 0) for (int f : gal_lists[slot_entry[pp]]) gal_idx.push_back(f);
+      gal_ptr[pp + 1] = (int)gal_idx.size();
+    }
+    sell_to_csr(C, nc);
+    sell_to_ghost_csr(C);
+    AmgLevelDev<P>& D = A->L[lev + 1];
+    const int ncell = nc + C.ng;
+    D.n = nc; D.n_slices = S; D.n_sell = C.ms_ptr[S]; D.n_cells = ncell;
+    D.nnz = (int64_t)ccol.size();
+    int *p0, *p1, *p2;
+    if ((st = A->up(&p0, C.ms_ptr)) || (st = A->up(&p1, C.ms_len)) || (st = A->up(&p2, C.mnb)) ||
+        (st = A->up(&D.gal_ptr, gal_ptr)) || (st = A->up(&D.gal_idx, gal_idx)) || (st = A->up(&D.dg_ptr, dg_ptr)) ||
+        (st = A->up(&D.dg_idx, dg_idx)) || (st = A->up(&D.mem_ptr, mem_ptr)) || (st = A->up(&D.mem, mem)) ||
+        (st = A->up(&A->L[lev].agg, agg)) || (st = A->zalloc(&D.coef_own, (size_t)D.n_sell)) ||
+        (st = A->zalloc(&D.diag_own, nc)) || (st = A->zalloc(&D.il1, nc)) || (st = A->zalloc(&D.x, ncell)) ||
+        (st = A->zalloc(&D.b, nc)) || (st = A->zalloc(&D.r, ncell)) || (st = A->zalloc(&D.t, ncell)) ||
+        (st = A->zalloc(&D.e, ncell)) || (st = A->zalloc(&D.r2, nc)))
+      return st;
+    D.ms_ptr = p0; D.ms_len = p1; D.mnb = p2;
+    D.coef = D.coef_own; D.diag = D.diag_own;
+    A->halos[lev + 1] = C.halo;
+    H.push_back(std::move(C));
+    ++lev;
+  }
+  A->nlev = lev + 1;
+  // global coarsest: padded blocks of n_cmax rows per rank
+  const HostLevel& Cl = H[lev];
+  if ((st = agree_all(m, (double)Cl.n, votes, s))) return st;
+  int n_cmax = 0;
+  for (double v : votes) n_cmax = std::max(n_cmax, (int)v);
+  if (lev > 0 && (int64_t)n_cmax * NR <= kDirectMax) {
+    A->gdense = true;
+    A->n_cmax = n_cmax;
+    A->Np = n_cmax * NR;
+    std::vector<int> gcol(std::max(1, Cl.ng));
+    for (int k = 0; k < Cl.ng; ++k) gcol[k] = Cl.ghost_peer[k] * n_cmax + Cl.ghost_key[k];
+    if ((st = A->up(&A->d_gcol, gcol)) || (st = A->zalloc(&A->d_rows, (size_t)n_cmax * A->Np)) ||
+        (st = A->zalloc(&A->d_all, (size_t)A->Np * A->Np)) || (st = A->zalloc(&A->d_rhs, (size_t)n_cmax)) ||
+        (st = A->zalloc(&A->d_rhs_all, (size_t)A->Np)))
+      return st;
+  } else if (lev > 0 && A->L[lev].n <= A->prm.direct) {
+    // (rank-local coarsest, block Jacobi across ranks at that level only)
+    if ((st = A->zalloc(&A->ainv, (size_t)A->L[lev].n * A->L[lev].n))) return st;
+  }
+  if (getenv("DFVM_AMG_VERBOSE"))
+    for (int k = 0; k <= lev; ++k)
+      fprintf(stderr, "[amg r%d] level %d: rows %d + %d ghosts, entries %d + %d to ghosts%s\n", Pt.rank, k, H[k].n,
+              H[k].ng, H[k].rp[H[k].n], H[k].grp.empty() ? 0 : H[k].grp[H[k].n],
+              (k == lev && A->gdense) ? " (global coarsest)" : "");
+  return DFVM_OK;
+}
+
 template <class T>
-dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** out) {
+dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** out, cudaStream_t s) {
   Amg<T>* A = new Amg<T>();
   dfvm_status st;
+  const bool dist = m->part.P > 1;
   if (fp32 && !std::is_same<T, float>::value) {
     A->lo = new AmgH<float>();
-    st = build<float, T>(m, M, A->lo);
+    st = dist ? build_dist<float, T>(m, M, A->lo, s) : build<float, T>(m, M, A->lo);
   } else {
     A->same = new AmgH<T>();
-    st = build<T, T>(m, M, A->same);
+    st = dist ? build_dist<T, T>(m, M, A->same, s) : build<T, T>(m, M, A->same);
   }
   if (st) { delete A; return st; }
   DFVM_CUDA(cudaStreamSynchronize(nullptr));   // pageable uploads + zero-fills done before the caller's stream runs
@@ -691,7 +969,7 @@ __global__ void __launch_bounds__(1024) k_amg_dense_inv(int n, SellView S, const
     const int sl = q >> 5, lane = q & 31;
     for (int j = 0; j < S.ms_len[sl]; ++j) {
       const int p = S.ms_ptr[sl] + 32 * j + lane;
-      A[(size_t)i * n + S.mnb[p]] += coef[p];
+      if (S.mnb[p] < n) A[(size_t)i * n + S.mnb[p]] += coef[p];   // (ghost columns: dropped, rank-local block)
     }
   }
   __syncthreads();
@@ -730,6 +1008,69 @@ __global__ void __launch_bounds__(1024) k_amg_dense(int n, const P* __restrict__
                                                     TO* __restrict__ x, const int* done) {
   if (*done) return;
   dense_solve_block<P, TB, TO>(n, Ai, b, x);
+}
+
+// ---- global coarsest of a distributed hierarchy (several ranks)
+// The rank's owned coarsest rows in the padded global numbering (rank r's
+// row i -> r n_cmax + i; ghost columns through gcol); padding rows carry a
+// unit diagonal, so the padded Np x Np system stays SPD.  One block.
+template <class P>
+__global__ void __launch_bounds__(1024) k_dense_rows(int n, int n_cmax, int Np, int rank, SellView S,
+                                                     const P* __restrict__ coef, const P* __restrict__ diag,
+                                                     const int* __restrict__ gcol, double* __restrict__ rows) {
+  for (int e = threadIdx.x; e < n_cmax * Np; e += blockDim.x) rows[e] = 0.0;
+  __syncthreads();
+  const int off = rank * n_cmax;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {      // thread q owns slot q (row i): no write races
+    const int i = slot_row(S, q);
+    double* row = rows + (size_t)i * Np;
+    row[off + i] += (double)diag[i];
+    const int sl = q >> 5, lane = q & 31;
+    for (int j = 0; j < S.ms_len[sl]; ++j) {
+      const int p = S.ms_ptr[sl] + 32 * j + lane;
+      const int c = S.mnb[p];
+      row[c < n ? off + c : gcol[c - n]] += (double)coef[p];
+    }
+  }
+  for (int i = n + threadIdx.x; i < n_cmax; i += blockDim.x) rows[(size_t)i * Np + off + i] = 1.0;
+}
+// in-place Gauss-Jordan inverse of an SPD n x n matrix (fp64, one block)
+__global__ void __launch_bounds__(1024) k_gj_inverse(int n, double* __restrict__ A) {
+  __shared__ double colk[kDirectMax], rowk[kDirectMax];
+  for (int k = 0; k < n; ++k) {
+    const double piv = A[(size_t)k * n + k];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      colk[i] = A[(size_t)i * n + k];
+      rowk[i] = (i == k ? 1.0 : A[(size_t)k * n + i]) / piv;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      const double a = A[e];
+      A[e] = (i == k) ? rowk[j] : ((j == k ? 0.0 : a) - colk[i] * rowk[j]);
+    }
+    __syncthreads();
+  }
+}
+template <class P>
+__global__ void k_pack_rhs(int n, int n_cmax, const P* __restrict__ b, double* __restrict__ out, const int* done) {
+  if (*done) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_cmax; i += gridDim.x * blockDim.x)
+    out[i] = i < n ? (double)b[i] : 0.0;
+}
+// x_i = sum_j Ainv[off + i][j] rhs_j for the rank's owned rows (one warp per row)
+template <class P>
+__global__ void __launch_bounds__(1024) k_gsolve(int n, int Np, int off, const double* __restrict__ Ai,
+                                                 const double* __restrict__ rhs, P* __restrict__ x, const int* done) {
+  if (*done) return;
+  const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int i = threadIdx.x >> 5; i < n; i += nwarps) {
+    double acc = 0.0;
+    for (int j = lane; j < Np; j += 32) acc += Ai[(size_t)(off + i) * Np + j] * rhs[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) x[i] = (P)acc;
+  }
 }
 
 // ------------------------------------------------------------ host drivers
@@ -771,6 +1112,16 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
     PLAUNCH(pr, "k_amg_dense_inv", A->nlev - 1, 2 * pb * (double)C.n * C.n, s,
             (k_amg_dense_inv<P><<<1, 1024, 0, s>>>(C.n, C.sv(), C.coef, C.diag, A->ainv)));
     ++*nl;
+  }
+  if (A->gdense) {   // global coarsest: all-gather the ranks' rows, invert redundantly
+    const AmgLevelDev<P>& C = A->L[A->nlev - 1];
+    const double np = A->Np;
+    PLAUNCH(pr, "k_dense_rows", A->nlev - 1, 8.0 * A->n_cmax * np, s,
+            (k_dense_rows<P><<<1, 1024, 0, s>>>(C.n, A->n_cmax, A->Np, A->m->part.rank, C.sv(), C.coef, C.diag,
+                                                A->d_gcol, A->d_rows)));
+    if (dfvm_status e = allgather_f64(A->m, A->d_rows, A->d_all, A->n_cmax * A->Np, s)) return e;
+    PLAUNCH(pr, "k_gj_inverse", A->nlev - 1, 16.0 * np * np, s, (k_gj_inverse<<<1, 1024, 0, s>>>(A->Np, A->d_all)));
+    *nl += 2;
   }
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
@@ -873,6 +1224,82 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
   ++*nl;
 }
 
+template <class P>
+static dfvm_status coarse_correction(AmgH<P>* A, int l, const int* done, cudaStream_t s, int* nl);
+
+// Distributed hierarchy (several ranks): level l >= 1 with ghost aggregates.
+// Unfused kernels, a halo exchange before every kernel that gathers
+// neighbour values (t, the prolonged r, and the W-cycle's coarse x), the
+// coarsest level solved globally (all-gather of the padded right-hand sides,
+// every rank applies its rows of the redundant inverse).  Every rank issues
+// the same sequence of exchanges (the level count is agreed at build).
+template <class P>
+static dfvm_status cycle_dist(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl) {
+  AmgLevelDev<P>& F = A->L[l];
+  Prof* pr = A->prof;
+  const bool f64 = std::is_same<P, double>::value;
+  const double pb = sizeof(P), n = F.n;
+  dfvm_status e;
+  if (l == A->nlev - 1) {
+    if (A->gdense) {
+      PLAUNCH(pr, "k_pack_rhs", l, (pb + 8) * n, s,
+              (k_pack_rhs<P><<<1, 256, 0, s>>>(F.n, A->n_cmax, b, A->d_rhs, done)));
+      if ((e = allgather_f64(A->m, A->d_rhs, A->d_rhs_all, A->n_cmax, s))) return e;
+      PLAUNCH(pr, "k_gsolve", l, 8.0 * n * A->Np + 8.0 * A->Np + pb * n, s,
+              (k_gsolve<P><<<1, 1024, 0, s>>>(F.n, A->Np, A->m->part.rank * A->n_cmax, A->d_all, A->d_rhs_all, x,
+                                              done)));
+      *nl += 2;
+    } else {
+      coarsest(A, l, b, x, done, s, nl);
+    }
+    return DFVM_OK;
+  }
+  AmgLevelDev<P>& C = A->L[l + 1];
+  const P w = (P)A->prm.omega;
+  const double nc = C.n;
+  const int gF = grid_for(F.n), gC = grid_for(C.n);
+  PLAUNCH(pr, "k_amg_pre", l, 3 * pb * n, s, (k_amg_pre<P, P, P><<<gF, kThreads, 0, s>>>(F.n, b, F.il1, F.t, done)));
+  if ((e = halo_exchange_lists(A->m, A->halos[l], F.t, 1, f64, s))) return e;
+  PLAUNCH(pr, "k_amg_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 4 * pb * n, s,
+          (k_amg_resid<P, P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.t, b, F.r, done)));
+  PLAUNCH(pr, "k_amg_restrict", l, (4 + pb) * (n + nc), s,
+          (k_amg_restrict<P><<<gC, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
+  *nl += 3;
+  if ((e = coarse_correction(A, l + 1, done, s, nl))) return e;
+  PLAUNCH(pr, "k_amg_prolong", l, (4 + 2 * pb) * n + pb * nc, s,
+          (k_amg_prolong<P><<<gF, kThreads, 0, s>>>(F.n, F.agg, C.x, F.t, F.r, w, done)));
+  if ((e = halo_exchange_lists(A->m, A->halos[l], F.r, 1, f64, s))) return e;
+  PLAUNCH(pr, "k_amg_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
+          (k_amg_smooth<P, P, P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, F.r, b, x, done)));
+  *nl += 2;
+  return DFVM_OK;
+}
+
+// The coarse correction of level l (its rhs L[l].b already restricted):
+// x_l = M_l^-1 b_l, and for the W-cycle the second visit on the residual
+// r2 = b - A x, added.
+template <class P>
+static dfvm_status coarse_correction(AmgH<P>* A, int l, const int* done, cudaStream_t s, int* nl) {
+  AmgLevelDev<P>& C = A->L[l];
+  Prof* pr = A->prof;
+  const bool f64 = std::is_same<P, double>::value;
+  const double pb = sizeof(P), nc = C.n;
+  const int gC = grid_for(C.n);
+  dfvm_status e;
+  if (A->dist) { if ((e = cycle_dist(A, l, C.b, C.x, done, s, nl))) return e; }
+  else cycle_coarse(A, l, C.b, C.x, done, s, nl);
+  if (A->prm.wcycle && l < A->nlev - 1 && l <= A->prm.wmax) {
+    if (A->dist && (e = halo_exchange_lists(A->m, A->halos[l], C.x, 1, f64, s))) return e;
+    PLAUNCH(pr, "k_amg_resid", l, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
+            (k_amg_resid<P, P><<<gC, kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.x, C.b, C.r2, done)));
+    if (A->dist) { if ((e = cycle_dist(A, l, C.r2, C.e, done, s, nl))) return e; }
+    else cycle_coarse(A, l, C.r2, C.e, done, s, nl);
+    PLAUNCH(pr, "k_amg_add", l, 3 * pb * nc, s, (k_amg_add<P><<<gC, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
+    *nl += 2;
+  }
+  return DFVM_OK;
+}
+
 // Level 0: reads the PCG residual r (type T), writes z (type T); its own
 // vectors are in P and carry ghost slices (exchanged before each SpMV).
 // Level 0 uses the unfused kernels (measured on B200: the fused versions
@@ -923,15 +1350,7 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   PLAUNCH(pr, "k_amg_restrict", 0, (4 + pb) * (n + nc), s,
           (k_amg_restrict<P><<<g1, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
   *nl += 2;
-  cycle_coarse(A, 1, C.b, C.x, done, s, nl);
-  if (A->prm.wcycle && 1 < A->nlev - 1 && 1 <= A->prm.wmax) {
-    PLAUNCH(pr, "k_amg_resid", 1, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
-            (k_amg_resid<P, P><<<g1, kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.x, C.b,
-                                                       C.r2, done)));
-    cycle_coarse(A, 1, C.r2, C.e, done, s, nl);
-    PLAUNCH(pr, "k_amg_add", 1, 3 * pb * nc, s, (k_amg_add<P><<<g1, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
-    *nl += 2;
-  }
+  if ((e = coarse_correction(A, 1, done, s, nl))) return e;
   PLAUNCH(pr, "k_amg_prolong", 0, (4 + 2 * pb) * n + pb * nc, s,
           (k_amg_prolong<P><<<g0, kThreads, 0, s>>>(F.n, F.agg, C.x, F.x, F.t, (P)A->prm.omega, done)));
   if ((e = halo_exchange_p(A->m, F.t, 1, f64, s))) return e;
@@ -979,7 +1398,7 @@ int amg_level_nnz(const Amg<T>* A, int64_t* nnz) {
 }
 
 #define INST(T)                                                                           \
-  template dfvm_status amg_create<T>(dfvm_mesh*, const DevMesh<T>&, bool, Amg<T>**);      \
+  template dfvm_status amg_create<T>(dfvm_mesh*, const DevMesh<T>&, bool, Amg<T>**, cudaStream_t); \
   template void amg_destroy<T>(Amg<T>*);                                                  \
   template int amg_levels<T>(const Amg<T>*, int*);                                        \
   template dfvm_status amg_update<T>(Amg<T>*, const T*, const T*, cudaStream_t, int*, Prof*); \

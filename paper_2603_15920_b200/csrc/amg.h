@@ -12,7 +12,7 @@ struct Prof;
 template <class T> struct Amg;
 // hierarchy from the mesh topology (host, once per mesh); fp32: store and
 // cycle the hierarchy in fp32 under an fp64 solver ("amg32")
-template <class T> dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** out);
+template <class T> dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** out, cudaStream_t s);
 template <class T> void amg_destroy(Amg<T>* A);
 template <class T> int amg_levels(const Amg<T>* A, int* sizes);
 // Galerkin values + l1 diagonals for the current pressure matrix (pcoef, pdiag)

@@ -431,9 +431,8 @@ dfvm_status dfvm_mesh_destroy(dfvm_mesh* m) {
   cudaSetDevice(m->device);
   cudaDeviceSynchronize();
   for (void* p : m->allocations) dev_free(p, nullptr);
-  dev_free(m->d_send, nullptr);
-  dev_free(m->d_recv, nullptr);
-  dev_free(m->d_send_idx, nullptr);
+  dev_free(m->halo0.d_send, nullptr);
+  dev_free(m->halo0.d_send_idx, nullptr);
   dev_free(m->d_stage, nullptr);
   delete m;
   return DFVM_OK;

@@ -107,20 +107,6 @@ static dfvm_status nccl_error(ncclResult_t r, const char* where) {
 
 dfvm_status halo_exchange_p(dfvm_mesh* m, void* data, int nc, bool f64, cudaStream_t s);
 
-static dfvm_status ensure_halo_buffers(dfvm_mesh* m) {
-  const Part& P = m->part;
-  if (m->d_send_idx || P.send_gid.empty()) return DFVM_OK;
-  std::vector<int32_t> idx(P.send_gid.size());
-  for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int32_t)(P.send_gid[i] - P.lo);
-  dfvm_status st;
-  if ((st = dev_alloc_n(&m->d_send_idx, idx.size(), nullptr, false))) return st;
-  DFVM_CUDA(cudaMemcpy(m->d_send_idx, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice));
-  m->halo_bytes = idx.size() * 9 * 8;   // up to 9 fp64 components
-  if ((st = dev_alloc(&m->d_send, m->halo_bytes, nullptr, false))) return st;
-  DFVM_CUDA(cudaStreamSynchronize(nullptr));   // once: ordered before the caller's (non-blocking) stream uses them
-  return DFVM_OK;
-}
-
 // local transport: every rank publishes, all wait for everybody's data,
 // copy, then wait until every peer has consumed before the published
 // buffers may be overwritten by the next stream operation.
@@ -133,6 +119,71 @@ static dfvm_status local_finish(LocalGroup* G, int rank, cudaStream_t s) {
   return DFVM_OK;
 }
 
+// Halo of one partitioned vector space (level 0: the mesh's cells; AMG
+// coarse levels: their aggregates): owned rows [0, n_own), ghosts in
+// contiguous per-peer slices ordered by the owner's local index; the send
+// list to peer q (owned rows, ascending) is q's ghost slice for this rank in
+// the same order, so a receive lands directly in the slice (no unpack).
+dfvm_status halo_exchange_lists(dfvm_mesh* m, HaloLists& L, void* data, int nc, bool f64, cudaStream_t s) {
+  if (m->part.P == 1 || L.peers.empty()) return DFVM_OK;
+  if (!m->comm) { set_error(DFVM_E_NCCL, "multi-part mesh without communicator"); return DFVM_E_NCCL; }
+  const size_t eb = f64 ? 8 : 4;
+  const int64_t ns = L.send_off.back();
+  if (!L.d_send_idx && ns) {
+    dfvm_status st;
+    if ((st = dev_alloc_n(&L.d_send_idx, (size_t)ns, nullptr, false))) return st;
+    DFVM_CUDA(cudaMemcpy(L.d_send_idx, L.send_idx.data(), (size_t)ns * 4, cudaMemcpyHostToDevice));
+    L.buf_bytes = (size_t)ns * 9 * 8;   // up to 9 fp64 components
+    if ((st = dev_alloc(&L.d_send, L.buf_bytes, nullptr, false))) return st;
+    DFVM_CUDA(cudaStreamSynchronize(nullptr));   // once: ordered before the caller's (non-blocking) stream uses them
+  }
+  if (ns) {
+    if (f64) launch_pack<double>((double*)L.d_send, (const double*)data, L.d_send_idx, ns, nc, s);
+    else launch_pack<float>((float*)L.d_send, (const float*)data, L.d_send_idx, ns, nc, s);
+  }
+  dfvm_comm* C = m->comm;
+  if (C->backend == 0) {
+    const ncclDataType_t dt = f64 ? ncclFloat64 : ncclFloat32;
+    DFVM_NCCL(nccl().GroupStart());
+    for (size_t i = 0; i < L.peers.size(); ++i) {
+      const int q = L.peers[i];
+      const int64_t so = L.send_off[i], sn = L.send_off[i + 1] - so;
+      const int64_t go = L.ghost_off[i], gn = L.ghost_off[i + 1] - go;
+      DFVM_NCCL(nccl().Send((const char*)L.d_send + so * nc * eb, (size_t)(sn * nc), dt, q, C->nccl, s));
+      DFVM_NCCL(nccl().Recv((char*)data + (L.n_own + go) * nc * eb, (size_t)(gn * nc), dt, q, C->nccl, s));
+    }
+    DFVM_NCCL(nccl().GroupEnd());
+    return DFVM_OK;
+  }
+  LocalGroup* G = C->grp;
+  const int me = C->rank;
+  for (size_t i = 0; i < L.peers.size(); ++i)
+    G->box[(size_t)me * G->n + L.peers[i]] = (const char*)L.d_send + L.send_off[i] * nc * eb;
+  DFVM_CUDA(cudaEventRecord(G->posted[me], s));
+  G->barrier();
+  for (size_t i = 0; i < L.peers.size(); ++i) {
+    const int q = L.peers[i];
+    const int64_t go = L.ghost_off[i], gn = L.ghost_off[i + 1] - go;
+    DFVM_CUDA(cudaStreamWaitEvent(s, G->posted[q], 0));
+    DFVM_CUDA(cudaMemcpyAsync((char*)data + (L.n_own + go) * nc * eb, G->box[(size_t)q * G->n + me],
+                              (size_t)(gn * nc) * eb, cudaMemcpyDeviceToDevice, s));
+  }
+  return local_finish(G, me, s);
+}
+
+static void ensure_mesh_halo(dfvm_mesh* m) {
+  HaloLists& L = m->halo0;
+  if (L.ready) return;
+  const Part& P = m->part;
+  L.n_own = P.n_own;
+  L.peers = P.peers;
+  L.send_off = P.peer_send_off;
+  L.ghost_off = P.peer_ghost_off;
+  L.send_idx.resize(P.send_gid.size());
+  for (size_t i = 0; i < P.send_gid.size(); ++i) L.send_idx[i] = (int32_t)(P.send_gid[i] - P.lo);
+  L.ready = true;
+}
+
 dfvm_status halo_exchange(dfvm_mesh* m, void* data, int nc, cudaStream_t s) {
   return halo_exchange_p(m, data, nc, m->precision == DFVM_F64, s);
 }
@@ -140,44 +191,9 @@ dfvm_status halo_exchange(dfvm_mesh* m, void* data, int nc, cudaStream_t s) {
 // element type given explicitly (f64 or f32), e.g. the fp32 AMG hierarchy of
 // an fp64 solver; the send buffer is sized for 9 fp64 components
 dfvm_status halo_exchange_p(dfvm_mesh* m, void* data, int nc, bool f64, cudaStream_t s) {
-  const Part& P = m->part;
-  if (P.P == 1) return DFVM_OK;
-  if (!m->comm) { set_error(DFVM_E_NCCL, "multi-part mesh without communicator"); return DFVM_E_NCCL; }
-  if (dfvm_status st = ensure_halo_buffers(m)) return st;
-  const size_t eb = f64 ? 8 : 4;
-  const int64_t ns = (int64_t)P.send_gid.size();
-  if (ns) {
-    if (f64) launch_pack<double>((double*)m->d_send, (const double*)data, m->d_send_idx, ns, nc, s);
-    else launch_pack<float>((float*)m->d_send, (const float*)data, m->d_send_idx, ns, nc, s);
-  }
-  dfvm_comm* C = m->comm;
-  if (C->backend == 0) {
-    const ncclDataType_t dt = f64 ? ncclFloat64 : ncclFloat32;
-    DFVM_NCCL(nccl().GroupStart());
-    for (size_t i = 0; i < P.peers.size(); ++i) {
-      const int q = P.peers[i];
-      const int64_t so = P.peer_send_off[i], sn = P.peer_send_off[i + 1] - so;
-      const int64_t go = P.peer_ghost_off[i], gn = P.peer_ghost_off[i + 1] - go;
-      DFVM_NCCL(nccl().Send((const char*)m->d_send + so * nc * eb, (size_t)(sn * nc), dt, q, C->nccl, s));
-      DFVM_NCCL(nccl().Recv((char*)data + (P.n_own + go) * nc * eb, (size_t)(gn * nc), dt, q, C->nccl, s));
-    }
-    DFVM_NCCL(nccl().GroupEnd());
-    return DFVM_OK;
-  }
-  LocalGroup* G = C->grp;
-  const int me = C->rank;
-  for (size_t i = 0; i < P.peers.size(); ++i)
-    G->box[(size_t)me * G->n + P.peers[i]] = (const char*)m->d_send + P.peer_send_off[i] * nc * eb;
-  DFVM_CUDA(cudaEventRecord(G->posted[me], s));
-  G->barrier();
-  for (size_t i = 0; i < P.peers.size(); ++i) {
-    const int q = P.peers[i];
-    const int64_t go = P.peer_ghost_off[i], gn = P.peer_ghost_off[i + 1] - go;
-    DFVM_CUDA(cudaStreamWaitEvent(s, G->posted[q], 0));
-    DFVM_CUDA(cudaMemcpyAsync((char*)data + (P.n_own + go) * nc * eb, G->box[(size_t)q * G->n + me],
-                              (size_t)(gn * nc) * eb, cudaMemcpyDeviceToDevice, s));
-  }
-  return local_finish(G, me, s);
+  if (m->part.P == 1) return DFVM_OK;
+  ensure_mesh_halo(m);
+  return halo_exchange_lists(m, m->halo0, data, nc, f64, s);
 }
 
 bool comm_is_local(const dfvm_comm* c) { return c && c->backend == 1; }

@@ -121,6 +121,18 @@ struct DevMesh {
 
 struct Comm;
 
+// halo lists of one partitioned vector space (comm.cpp halo_exchange_lists)
+struct HaloLists {
+  bool ready = false;
+  int64_t n_own = 0;
+  std::vector<int32_t> peers;               // ascending
+  std::vector<int64_t> send_off, ghost_off; // per peer, [n_peers + 1]
+  std::vector<int32_t> send_idx;            // owned local rows, per peer ascending
+  int32_t* d_send_idx = nullptr;
+  void* d_send = nullptr;
+  size_t buf_bytes = 0;
+};
+
 }  // namespace dfvm
 
 // opaque ABI objects
@@ -141,9 +153,8 @@ struct dfvm_mesh {
   // lazily built device maps for device-side import/export
   int32_t* d_cell_orig = nullptr;   // [n_cells] original id of local cell
   int32_t* d_face_orig = nullptr;   // [n_faces_local] original face id, sign-flip flag in bit 31
-  // halo exchange buffers (P > 1)
-  void* d_send = nullptr; void* d_recv = nullptr; int32_t* d_send_idx = nullptr;
-  size_t halo_bytes = 0;
+  // halo of the cells (P > 1)
+  dfvm::HaloLists halo0;
   // persistent device staging buffer of host<->device field import/export
   // (grown on demand, guarded: one import/export at a time per mesh)
   void* d_stage = nullptr;

@@ -1411,7 +1411,7 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
   DevMesh<T>& M = *X.M;
   dfvm_mesh* m = S->m;
   dfvm_status e;
-  if (!X.amg && (e = amg_create<T>(m, M, S->o.p_precond == 2, &X.amg))) return e;
+  if (!X.amg && (e = amg_create<T>(m, M, S->o.p_precond == 2, &X.amg, st))) return e;
   Prof* pr = S->pr();
   const double v = sizeof(T), N = M.n_own, Z = (double)M.nnz;
   if (X.amg_dirty) {
