@@ -502,8 +502,9 @@ static dfvm_status build_dist(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A, cud
     L0.coef = L0.coef_own; L0.diag = L0.diag_own;
   }
   // the global coarsest system holds NR * (rows per rank): stop each rank's
-  // coarsening near kDirectMax / NR rows (never below 32)
-  const int target = std::max(32, std::min(A->prm.coarse, kDirectMax / NR));
+  // coarsening near 256 / NR rows (never below 32), so the redundant inverse
+  // of each update stays at Np <= ~256 (<= kDirectMax = 512 enforced below)
+  const int target = std::max(32, std::min(A->prm.coarse, 256 / NR));
   int lev = 0;
   std::vector<double> votes;
   int32_t* d_agg = nullptr;

@@ -1276,8 +1276,11 @@ static dfvm_status chunk_loop(dfvm_solver* S, SolverT<T>& X, int nctl, dfvm_solv
   auto iters = [&]() { int i = 0; for (int k = 0; k < nctl; ++k) i = std::max(i, X.h_ctl[k].it); return i; };
   auto all_done = [&]() { for (int k = 0; k < nctl; ++k) if (!X.h_ctl[k].done) return false; return true; };
   for (;;) {
+    // profile mode: one iteration per captured chunk, so no launch after
+    // convergence is timed (the device-resident loop makes none either)
+    const int nchunk = pr ? 1 : kChunk;
     auto chunk = [&](int* nl) -> dfvm_status {
-      for (int k = 0; k < kChunk; ++k) {
+      for (int k = 0; k < nchunk; ++k) {
         if (pr) { pr->iter = k; pr->post = 0; }
         dfvm_status e3 = body(nl);
         if (e3) return e3;
