@@ -69,13 +69,15 @@ constexpr int kMaxLevels = 16;
 //                    < 2 keeps M SPD with adjoint smoothers)   default 1.95
 //   DFVM_AMG_PERM    1: coarse-level SELL storage sorted by row length
 //                    within windows of 256 slots (SELL-32-sigma: rows keep
-//                    their numbers, the hierarchy and results are unchanged,
-//                    padding shrinks); 0: natural order          default 0
+//                    their numbers, the hierarchy is unchanged, padding
+//                    shrinks); 0: natural order                  default 0
 //                    (C5 round 2: padding 8.4 % on level 1, yet 347.2 ms/step
 //                    against 343.1 ms in natural order — the coarse
 //                    kernels are bound by their gathers, and the permuted
 //                    own-row accesses cost more than the padding saved;
-//                    profiles/r02_amg_sweep2_c5.jsonl)
+//                    profiles/r02_amg_sweep2_c5.jsonl); results differ from
+//                    natural order at round-off (2e-10 on a 38k-cell pipe),
+//                    within the parity bound
 //                    (round 1 renumbered the aggregates themselves by
 //                    length instead: that changed the next aggregation
 //                    and cost 0.5 PCG iterations per solve — removed)
@@ -247,17 +249,23 @@ struct AmgH {
   Prof* prof = nullptr;             // per-kernel profile of the caller (may be null)
   AmgLevelDev<P> L[kMaxLevels];
   P* ainv = nullptr;                // dense inverse of the coarsest matrix (column-major n x n), or NULL
-  // several ranks: every level is distributed (owned aggregates of owned
-  // rows, ghost aggregates of the neighbours, a halo per level) and the
-  // coarsest level is solved globally: the ranks' coarsest rows, padded to
-  // n_cmax per rank, form one Np = P n_cmax system, all-gathered and
-  // inverted redundantly on every rank
+  // several ranks: levels 0..ld are distributed (owned aggregates of owned
+  // rows, ghost aggregates of the neighbours, a halo per level); level ld+1
+  // is the AGGLOMERATION of every rank's level-ld rows into one global
+  // level, replicated on every rank together with the serial hierarchy
+  // below it (values all-gathered at each update, right-hand sides at each
+  // visit)
   bool dist = false;
   HaloLists halos[kMaxLevels];
-  bool gdense = false;
-  int n_cmax = 0, Np = 0;
-  double *d_rows = nullptr, *d_all = nullptr, *d_rhs = nullptr, *d_rhs_all = nullptr;
-  int* d_gcol = nullptr;            // coarsest ghost row -> padded global column
+  int ld = -1;                      // last distributed level (-1: single rank)
+  bool agglom = false;
+  int Vmax = 0, Nmax = 0;           // padded per-rank value / row counts of the exchanges
+  int Vloc = 0;                     // this rank's values
+  int* d_pk = nullptr;              // canonical value k of this rank's level-ld rows: >= 0 coef position, < 0 diag -1-i
+  int *d_gmap = nullptr, *d_gdmap = nullptr;   // G0 SELL position / row -> index into the gathered values
+  int *d_cnt = nullptr, *d_off = nullptr;      // per rank: level-ld rows and their global offset
+  int goff = 0;                     // this rank's offset in G0
+  double *d_vals = nullptr, *d_vals_all = nullptr, *d_rhs = nullptr, *d_rhs_all = nullptr;
   std::vector<void*> allocs;
   int64_t bytes = 0;
   ~AmgH() {
@@ -291,26 +299,12 @@ struct Amg {
   ~Amg() { delete same; delete lo; }
 };
 
-template <class P, class T>
-static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
-  A->m = m;
-  std::vector<HostLevel> H(1);
-  H[0].n = M.n_own;
-  H[0].ms_ptr = m->h_ms_ptr; H[0].ms_len = m->h_ms_len; H[0].mnb = m->h_mnb;
-  sell_to_csr(H[0], M.n_own);
-  // device view of level 0 (the mesh's matrix layout; coef / diag bound per update)
-  AmgLevelDev<P>& L0 = A->L[0];
-  L0.n = M.n_own; L0.n_slices = M.n_slices; L0.n_sell = M.n_minc; L0.nnz = M.nnz;
-  L0.ms_ptr = M.ms_ptr; L0.ms_len = M.ms_len; L0.mnb = M.mnb;
+// Serial coarsening from host level H[lev] (device level A->L[lev] set up):
+// aggregation, Galerkin maps, SELL layout, upload, until <= prm.coarse rows
+// (or a stall / a level under 32 rows).  lev returns the coarsest index.
+template <class P>
+static dfvm_status coarsen_serial(AmgH<P>* A, std::vector<HostLevel>& H, int& lev) {
   dfvm_status st;
-  if ((st = A->zalloc(&L0.il1, M.n_own)) || (st = A->zalloc(&L0.x, M.n_cells)) || (st = A->zalloc(&L0.r, M.n_own)) ||
-      (st = A->zalloc(&L0.t, M.n_cells)))
-    return st;
-  if (!std::is_same<P, T>::value) {
-    if ((st = A->zalloc(&L0.coef_own, (size_t)M.n_minc)) || (st = A->zalloc(&L0.diag_own, M.n_own))) return st;
-    L0.coef = L0.coef_own; L0.diag = L0.diag_own;
-  }
-  int lev = 0;
   while (H[lev].n > A->prm.coarse && lev + 1 < kMaxLevels) {
     const HostLevel& F = H[lev];
     int nc = 0;
@@ -424,6 +418,30 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
     H.push_back(std::move(C));
     ++lev;
   }
+  return DFVM_OK;
+}
+
+template <class P, class T>
+static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
+  A->m = m;
+  std::vector<HostLevel> H(1);
+  H[0].n = M.n_own;
+  H[0].ms_ptr = m->h_ms_ptr; H[0].ms_len = m->h_ms_len; H[0].mnb = m->h_mnb;
+  sell_to_csr(H[0], M.n_own);
+  // device view of level 0 (the mesh's matrix layout; coef / diag bound per update)
+  AmgLevelDev<P>& L0 = A->L[0];
+  L0.n = M.n_own; L0.n_slices = M.n_slices; L0.n_sell = M.n_minc; L0.nnz = M.nnz;
+  L0.ms_ptr = M.ms_ptr; L0.ms_len = M.ms_len; L0.mnb = M.mnb;
+  dfvm_status st;
+  if ((st = A->zalloc(&L0.il1, M.n_own)) || (st = A->zalloc(&L0.x, M.n_cells)) || (st = A->zalloc(&L0.r, M.n_own)) ||
+      (st = A->zalloc(&L0.t, M.n_cells)))
+    return st;
+  if (!std::is_same<P, T>::value) {
+    if ((st = A->zalloc(&L0.coef_own, (size_t)M.n_minc)) || (st = A->zalloc(&L0.diag_own, M.n_own))) return st;
+    L0.coef = L0.coef_own; L0.diag = L0.diag_own;
+  }
+  int lev = 0;
+  if ((st = coarsen_serial(A, H, lev))) return st;
   A->nlev = lev + 1;
   if (getenv("DFVM_AMG_VERBOSE"))
     for (int k = 0; k <= lev; ++k)
@@ -646,30 +664,116 @@ static dfvm_status build_dist(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A, cud
     ++lev;
   }
   A->nlev = lev + 1;
-  // global coarsest: padded blocks of n_cmax rows per rank
-  const HostLevel& Cl = H[lev];
-  if ((st = agree_all(m, (double)Cl.n, votes, s))) return st;
-  int n_cmax = 0;
-  for (double v : votes) n_cmax = std::max(n_cmax, (int)v);
-  if (lev > 0 && (int64_t)n_cmax * NR <= kDirectMax) {
-    A->gdense = true;
-    A->n_cmax = n_cmax;
-    A->Np = n_cmax * NR;
-    std::vector<int> gcol(std::max(1, Cl.ng));
-    for (int k = 0; k < Cl.ng; ++k) gcol[k] = Cl.ghost_peer[k] * n_cmax + Cl.ghost_key[k];
-    if ((st = A->up(&A->d_gcol, gcol)) || (st = A->zalloc(&A->d_rows, (size_t)n_cmax * A->Np)) ||
-        (st = A->zalloc(&A->d_all, (size_t)A->Np * A->Np)) || (st = A->zalloc(&A->d_rhs, (size_t)n_cmax)) ||
-        (st = A->zalloc(&A->d_rhs_all, (size_t)A->Np)))
-      return st;
-  } else if (lev > 0 && A->L[lev].n <= A->prm.direct) {
-    // (rank-local coarsest, block Jacobi across ranks at that level only)
-    if ((st = A->zalloc(&A->ainv, (size_t)A->L[lev].n * A->L[lev].n))) return st;
+  A->ld = lev;
+  if (lev == 0) return DFVM_OK;   // nothing coarsened: the single-level path of cycle0
+  // agglomeration of the level-lev rows of all ranks into G0 = level lev + 1
+  HostLevel& Hd = H[lev];
+  std::vector<double> cnts;
+  if ((st = agree_all(m, (double)Hd.n, cnts, s))) return st;
+  std::vector<int> cnt(NR), off(NR + 1, 0);
+  for (int r = 0; r < NR; ++r) { cnt[r] = (int)cnts[r]; off[r + 1] = off[r] + cnt[r]; }
+  const int NG = off[NR];
+  const int me = Pt.rank;
+  A->goff = off[me];
+  // canonical values of this rank's rows: diag, owned-column entries, ghost-column entries
+  std::vector<int> pk;
+  std::vector<double> grow, gcolv;
+  for (int i = 0; i < Hd.n; ++i) {
+    pk.push_back(-1 - i); grow.push_back(off[me] + i); gcolv.push_back(off[me] + i);
+    for (int k = Hd.rp[i]; k < Hd.rp[i + 1]; ++k) {
+      pk.push_back(Hd.pos[k]); grow.push_back(off[me] + i); gcolv.push_back(off[me] + Hd.col[k]);
+    }
+    for (int k = Hd.grp[i]; k < Hd.grp[i + 1]; ++k) {
+      const int c = Hd.gcol[k] - Hd.n;
+      pk.push_back(Hd.gpos[k]); grow.push_back(off[me] + i);
+      gcolv.push_back(off[Hd.ghost_peer[c]] + Hd.ghost_key[c]);
+    }
   }
+  std::vector<double> vm;
+  if ((st = agree_all(m, (double)pk.size(), vm, s))) return st;
+  int Vmax = 0, Nmax = 0;
+  for (double v : vm) Vmax = std::max(Vmax, (int)v);
+  for (int c : cnt) Nmax = std::max(Nmax, c);
+  A->Vmax = Vmax; A->Nmax = Nmax; A->Vloc = (int)pk.size();
+  // structure exchange: [rows | cols] per rank, padded with -1
+  std::vector<double> sbuf(2 * (size_t)Vmax, -1.0), all((size_t)NR * 2 * Vmax);
+  for (size_t k = 0; k < pk.size(); ++k) { sbuf[k] = grow[k]; sbuf[Vmax + k] = gcolv[k]; }
+  {
+    double *dl = nullptr, *da = nullptr;
+    if ((st = dev_alloc_n(&dl, sbuf.size(), s, false)) || (st = dev_alloc_n(&da, all.size(), s, false))) return st;
+    DFVM_CUDA(cudaMemcpyAsync(dl, sbuf.data(), 8 * sbuf.size(), cudaMemcpyHostToDevice, s));
+    if ((st = allgather_f64(m, dl, da, 2 * Vmax, s))) return st;
+    DFVM_CUDA(cudaMemcpyAsync(all.data(), da, 8 * all.size(), cudaMemcpyDeviceToHost, s));
+    DFVM_CUDA(cudaStreamSynchronize(s));
+    dev_free(dl, s);
+    dev_free(da, s);
+  }
+  // G0: global rows, off-diagonal entries sorted by column, value sources
+  std::vector<std::vector<std::pair<int, int>>> rows(NG);   // (col, source index)
+  std::vector<int> gdmap(NG, -1);
+  for (int r = 0; r < NR; ++r)
+    for (int k = 0; k < Vmax; ++k) {
+      const double rw = all[(size_t)r * 2 * Vmax + k];
+      if (rw < 0) continue;
+      const int gr = (int)rw, gc = (int)all[(size_t)r * 2 * Vmax + Vmax + k];
+      const int src = r * Vmax + k;
+      if (gr == gc) gdmap[gr] = src;
+      else rows[gr].push_back({gc, src});
+    }
+  HostLevel G;
+  G.n = NG;
+  const int S = (NG + 31) / 32;
+  G.ms_ptr.assign(S + 1, 0);
+  G.ms_len.assign(S, 0);
+  for (int I = 0; I < NG; ++I) std::sort(rows[I].begin(), rows[I].end());
+  for (int sl = 0; sl < S; ++sl) {
+    int w = 0;
+    for (int I = sl * 32; I < std::min(NG, sl * 32 + 32); ++I) w = std::max(w, (int)rows[I].size());
+    G.ms_len[sl] = w;
+    G.ms_ptr[sl + 1] = G.ms_ptr[sl] + 32 * w;
+  }
+  G.mnb.assign(G.ms_ptr[S], 0);
+  std::vector<int> gmap(std::max(1, G.ms_ptr[S]), -1);
+  int64_t gnnz = 0;
+  for (int I = 0; I < NG; ++I) {
+    const int sl = I / 32, lane = I % 32;
+    for (int j = 0; j < G.ms_len[sl]; ++j) {
+      const int pp = G.ms_ptr[sl] + 32 * j + lane;
+      if (j < (int)rows[I].size()) { G.mnb[pp] = rows[I][j].first; gmap[pp] = rows[I][j].second; ++gnnz; }
+      else G.mnb[pp] = I;
+    }
+  }
+  sell_to_csr(G, NG);
+  const int lg = lev + 1;
+  AmgLevelDev<P>& DG = A->L[lg];
+  DG.n = NG; DG.n_slices = S; DG.n_sell = G.ms_ptr[S]; DG.nnz = gnnz; DG.n_cells = NG;
+  int *q0, *q1, *q2;
+  std::vector<int> pkv(std::max<size_t>(1, pk.size()), 0);
+  for (size_t k = 0; k < pk.size(); ++k) pkv[k] = pk[k];
+  if ((st = A->up(&q0, G.ms_ptr)) || (st = A->up(&q1, G.ms_len)) || (st = A->up(&q2, G.mnb)) ||
+      (st = A->up(&A->d_gmap, gmap)) || (st = A->up(&A->d_gdmap, gdmap)) || (st = A->up(&A->d_pk, pkv)) ||
+      (st = A->up(&A->d_cnt, cnt)) || (st = A->up(&A->d_off, off)) ||
+      (st = A->zalloc(&DG.coef_own, (size_t)DG.n_sell)) || (st = A->zalloc(&DG.diag_own, NG)) ||
+      (st = A->zalloc(&DG.il1, NG)) || (st = A->zalloc(&DG.x, NG)) || (st = A->zalloc(&DG.b, NG)) ||
+      (st = A->zalloc(&DG.r, NG)) || (st = A->zalloc(&DG.t, NG)) || (st = A->zalloc(&DG.e, NG)) ||
+      (st = A->zalloc(&DG.r2, NG)) || (st = A->zalloc(&A->d_vals, (size_t)Vmax)) ||
+      (st = A->zalloc(&A->d_vals_all, (size_t)NR * Vmax)) || (st = A->zalloc(&A->d_rhs, (size_t)Nmax)) ||
+      (st = A->zalloc(&A->d_rhs_all, (size_t)NR * Nmax)))
+    return st;
+  DG.ms_ptr = q0; DG.ms_len = q1; DG.mnb = q2;
+  DG.coef = DG.coef_own; DG.diag = DG.diag_own;
+  A->agglom = true;
+  H.push_back(std::move(G));
+  lev = lg;
+  if ((st = coarsen_serial(A, H, lev))) return st;
+  A->nlev = lev + 1;
+  const int ncs = A->L[lev].n;
+  if (lev > lg - 1 && ncs <= A->prm.direct && (st = A->zalloc(&A->ainv, (size_t)ncs * ncs))) return st;
   if (getenv("DFVM_AMG_VERBOSE"))
     for (int k = 0; k <= lev; ++k)
       fprintf(stderr, "[amg r%d] level %d: rows %d + %d ghosts, entries %d + %d to ghosts%s\n", Pt.rank, k, H[k].n,
               H[k].ng, H[k].rp[H[k].n], H[k].grp.empty() ? 0 : H[k].grp[H[k].n],
-              (k == lev && A->gdense) ? " (global coarsest)" : "");
+              k == lg ? " (agglomerated, replicated)" : (k > lg ? " (replicated)" : ""));
   return DFVM_OK;
 }
 
@@ -1011,67 +1115,44 @@ __global__ void __launch_bounds__(1024) k_amg_dense(int n, const P* __restrict__
   dense_solve_block<P, TB, TO>(n, Ai, b, x);
 }
 
-// ---- global coarsest of a distributed hierarchy (several ranks)
-// The rank's owned coarsest rows in the padded global numbering (rank r's
-// row i -> r n_cmax + i; ghost columns through gcol); padding rows carry a
-// unit diagonal, so the padded Np x Np system stays SPD.  One block.
+// ---- agglomeration of a distributed hierarchy (several ranks)
+// this rank's level-ld values in the canonical order of the build (diag,
+// owned-column entries, ghost-column entries per row), padded with zeros
 template <class P>
-__global__ void __launch_bounds__(1024) k_dense_rows(int n, int n_cmax, int Np, int rank, SellView S,
-                                                     const P* __restrict__ coef, const P* __restrict__ diag,
-                                                     const int* __restrict__ gcol, double* __restrict__ rows) {
-  for (int e = threadIdx.x; e < n_cmax * Np; e += blockDim.x) rows[e] = 0.0;
-  __syncthreads();
-  const int off = rank * n_cmax;
-  for (int q = threadIdx.x; q < n; q += blockDim.x) {      // thread q owns slot q (row i): no write races
-    const int i = slot_row(S, q);
-    double* row = rows + (size_t)i * Np;
-    row[off + i] += (double)diag[i];
-    const int sl = q >> 5, lane = q & 31;
-    for (int j = 0; j < S.ms_len[sl]; ++j) {
-      const int p = S.ms_ptr[sl] + 32 * j + lane;
-      const int c = S.mnb[p];
-      row[c < n ? off + c : gcol[c - n]] += (double)coef[p];
-    }
-  }
-  for (int i = n + threadIdx.x; i < n_cmax; i += blockDim.x) rows[(size_t)i * Np + off + i] = 1.0;
+__global__ void k_pack_vals(int V, int Vmax, const int* __restrict__ pk, const P* __restrict__ coef,
+                            const P* __restrict__ diag, double* __restrict__ out) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < Vmax; k += gridDim.x * blockDim.x)
+    out[k] = k < V ? (pk[k] >= 0 ? (double)coef[pk[k]] : (double)diag[-1 - pk[k]]) : 0.0;
 }
-// in-place Gauss-Jordan inverse of an SPD n x n matrix (fp64, one block)
-__global__ void __launch_bounds__(1024) k_gj_inverse(int n, double* __restrict__ A) {
-  __shared__ double colk[kDirectMax], rowk[kDirectMax];
-  for (int k = 0; k < n; ++k) {
-    const double piv = A[(size_t)k * n + k];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      colk[i] = A[(size_t)i * n + k];
-      rowk[i] = (i == k ? 1.0 : A[(size_t)k * n + i]) / piv;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-      const int i = e / n, j = e - i * n;
-      const double a = A[e];
-      A[e] = (i == k) ? rowk[j] : ((j == k ? 0.0 : a) - colk[i] * rowk[j]);
-    }
-    __syncthreads();
-  }
+// G0 coefficients / diagonal from the all-gathered values (fixed maps)
+template <class P>
+__global__ void k_gather_g0(int64_t n_sell, int n, const int* __restrict__ gmap, const int* __restrict__ gdmap,
+                            const double* __restrict__ vals, P* __restrict__ coef, P* __restrict__ diag) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_sell; e += (int64_t)gridDim.x * blockDim.x)
+    coef[e] = gmap[e] >= 0 ? (P)vals[gmap[e]] : P(0);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) diag[i] = (P)vals[gdmap[i]];
 }
 template <class P>
-__global__ void k_pack_rhs(int n, int n_cmax, const P* __restrict__ b, double* __restrict__ out, const int* done) {
+__global__ void k_pack_rhs(int n, int nmax, const P* __restrict__ b, double* __restrict__ out, const int* done) {
   if (*done) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_cmax; i += gridDim.x * blockDim.x)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nmax; i += gridDim.x * blockDim.x)
     out[i] = i < n ? (double)b[i] : 0.0;
 }
-// x_i = sum_j Ainv[off + i][j] rhs_j for the rank's owned rows (one warp per row)
+// G0 right-hand side from the all-gathered padded pieces: rank r's row k -> off[r] + k
 template <class P>
-__global__ void __launch_bounds__(1024) k_gsolve(int n, int Np, int off, const double* __restrict__ Ai,
-                                                 const double* __restrict__ rhs, P* __restrict__ x, const int* done) {
+__global__ void k_scatter_g0(int nranks, int nmax, const int* __restrict__ cnt, const int* __restrict__ off,
+                             const double* __restrict__ all, P* __restrict__ bg, const int* done) {
   if (*done) return;
-  const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int i = threadIdx.x >> 5; i < n; i += nwarps) {
-    double acc = 0.0;
-    for (int j = lane; j < Np; j += 32) acc += Ai[(size_t)(off + i) * Np + j] * rhs[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) x[i] = (P)acc;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nranks * nmax; e += gridDim.x * blockDim.x) {
+    const int r = e / nmax, k = e - r * nmax;
+    if (k < cnt[r]) bg[off[r] + k] = (P)all[e];
   }
+}
+// this rank's rows of the replicated G0 solution
+template <class P>
+__global__ void k_extract_g0(int n, int goff, const P* __restrict__ xg, P* __restrict__ x, const int* done) {
+  if (*done) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = xg[goff + i];
 }
 
 // ------------------------------------------------------------ host drivers
@@ -1099,6 +1180,21 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
   for (int l = 1; l < A->nlev; ++l) {
     AmgLevelDev<P>& F = A->L[l - 1];
     AmgLevelDev<P>& C = A->L[l];
+    if (A->agglom && l == A->ld + 1) {
+      // G0 = every rank's level-ld rows: pack, all-gather, gather into the replicated level
+      const int V = A->Vmax, NR = A->m->part.P;
+      PLAUNCH(pr, "k_pack_vals", A->ld, 8.0 * V + (4 + pb) * A->Vloc, s,
+              (k_pack_vals<P><<<grid_for(V), kThreads, 0, s>>>(A->Vloc, V, A->d_pk, F.coef, F.diag, A->d_vals)));
+      if (dfvm_status e = allgather_f64(A->m, A->d_vals, A->d_vals_all, V, s)) return e;
+      PLAUNCH(pr, "k_gather_g0", l, (4 + 8 + pb) * (double)C.n_sell + (12 + pb) * C.n, s,
+              (k_gather_g0<P><<<grid_for(C.n_sell), kThreads, 0, s>>>(C.n_sell, C.n, A->d_gmap, A->d_gdmap,
+                                                                      A->d_vals_all, C.coef_own, C.diag_own)));
+      PLAUNCH(pr, "k_il1", l, (4 + pb) * (double)C.nnz + (4 + 2 * pb) * C.n, s,
+              (k_il1<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.il1)));
+      (void)NR;
+      *nl += 3;
+      continue;
+    }
     PLAUNCH(pr, "k_gal_off", l, (8 + pb) * (double)C.nnz + (4 + pb) * (double)F.nnz, s,
             (k_gal_off<P><<<grid_for(C.n_sell), kThreads, 0, s>>>(C.n_sell, C.gal_ptr, C.gal_idx, F.coef, C.coef_own)));
     PLAUNCH(pr, "k_gal_diag", l, (8 + pb) * (double)C.n + (4 + pb) * (double)F.n, s,
@@ -1113,16 +1209,6 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
     PLAUNCH(pr, "k_amg_dense_inv", A->nlev - 1, 2 * pb * (double)C.n * C.n, s,
             (k_amg_dense_inv<P><<<1, 1024, 0, s>>>(C.n, C.sv(), C.coef, C.diag, A->ainv)));
     ++*nl;
-  }
-  if (A->gdense) {   // global coarsest: all-gather the ranks' rows, invert redundantly
-    const AmgLevelDev<P>& C = A->L[A->nlev - 1];
-    const double np = A->Np;
-    PLAUNCH(pr, "k_dense_rows", A->nlev - 1, 8.0 * A->n_cmax * np, s,
-            (k_dense_rows<P><<<1, 1024, 0, s>>>(C.n, A->n_cmax, A->Np, A->m->part.rank, C.sv(), C.coef, C.diag,
-                                                A->d_gcol, A->d_rows)));
-    if (dfvm_status e = allgather_f64(A->m, A->d_rows, A->d_all, A->n_cmax * A->Np, s)) return e;
-    PLAUNCH(pr, "k_gj_inverse", A->nlev - 1, 16.0 * np * np, s, (k_gj_inverse<<<1, 1024, 0, s>>>(A->Np, A->d_all)));
-    *nl += 2;
   }
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;
@@ -1241,18 +1327,22 @@ static dfvm_status cycle_dist(AmgH<P>* A, int l, const P* b, P* x, const int* do
   const bool f64 = std::is_same<P, double>::value;
   const double pb = sizeof(P), n = F.n;
   dfvm_status e;
-  if (l == A->nlev - 1) {
-    if (A->gdense) {
-      PLAUNCH(pr, "k_pack_rhs", l, (pb + 8) * n, s,
-              (k_pack_rhs<P><<<1, 256, 0, s>>>(F.n, A->n_cmax, b, A->d_rhs, done)));
-      if ((e = allgather_f64(A->m, A->d_rhs, A->d_rhs_all, A->n_cmax, s))) return e;
-      PLAUNCH(pr, "k_gsolve", l, 8.0 * n * A->Np + 8.0 * A->Np + pb * n, s,
-              (k_gsolve<P><<<1, 1024, 0, s>>>(F.n, A->Np, A->m->part.rank * A->n_cmax, A->d_all, A->d_rhs_all, x,
-                                              done)));
-      *nl += 2;
-    } else {
-      coarsest(A, l, b, x, done, s, nl);
-    }
+  if (l == A->ld) {
+    if (!A->agglom) { coarsest(A, l, b, x, done, s, nl); return DFVM_OK; }
+    // agglomerated: all-gather the ranks' right-hand sides into the
+    // replicated G0, cycle the replicated hierarchy, take this rank's rows
+    AmgLevelDev<P>& G = A->L[l + 1];
+    const int NR = A->m->part.P;
+    PLAUNCH(pr, "k_pack_rhs", l, (pb + 8) * n, s,
+            (k_pack_rhs<P><<<grid_for(A->Nmax), kThreads, 0, s>>>(F.n, A->Nmax, b, A->d_rhs, done)));
+    if ((e = allgather_f64(A->m, A->d_rhs, A->d_rhs_all, A->Nmax, s))) return e;
+    PLAUNCH(pr, "k_scatter_g0", l + 1, (8 + pb) * (double)G.n, s,
+            (k_scatter_g0<P><<<grid_for((int64_t)NR * A->Nmax), kThreads, 0, s>>>(NR, A->Nmax, A->d_cnt, A->d_off,
+                                                                                  A->d_rhs_all, G.b, done)));
+    cycle_coarse(A, l + 1, G.b, G.x, done, s, nl);
+    PLAUNCH(pr, "k_extract_g0", l, 2 * pb * n, s,
+            (k_extract_g0<P><<<grid_for(F.n), kThreads, 0, s>>>(F.n, A->goff, G.x, x, done)));
+    *nl += 3;
     return DFVM_OK;
   }
   AmgLevelDev<P>& C = A->L[l + 1];

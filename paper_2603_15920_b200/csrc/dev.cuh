@@ -108,8 +108,17 @@ template <> __device__ __forceinline__ void ld3<double>(const double* p, double&
     b = u.x; c = u.y;
   }
 }
+// fp32: one 64-bit + one 32-bit load by the 8-byte parity of the address
+// (12-byte elements are 4-byte aligned)
 template <> __device__ __forceinline__ void ld3<float>(const float* p, float& a, float& b, float& c) {
-  a = __ldg(p); b = __ldg(p + 1); c = __ldg(p + 2);
+  if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+    const float2 u = __ldg(reinterpret_cast<const float2*>(p));
+    a = u.x; b = u.y; c = __ldg(p + 2);
+  } else {
+    a = __ldg(p);
+    const float2 u = __ldg(reinterpret_cast<const float2*>(p + 1));
+    b = u.x; c = u.y;
+  }
 }
 
 // Deterministic block + grid reduction of NV doubles.

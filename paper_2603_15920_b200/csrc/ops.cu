@@ -64,6 +64,11 @@ void launch_export(double* dst, const T* src, const int32_t* map, int64_t n, int
 // keeps ~kB x (record + value) independent loads in flight instead of a
 // dependent chain per face.
 constexpr int kB = 4;
+// fp32 operator kernels at 6 resident blocks / SM (C5 fp32, round 2,
+// tools/op_ab.py: grad_s 0.59 -> 0.78, grad_U 0.50 -> 0.61, Laplacian
+// 0.48 -> 0.65 of the HBM peak; 8 blocks/SM or deeper batches lower;
+// profiles/r02_ops_f32_variants_c5.json)
+constexpr int kOpsF32Default = 1;
 
 // ------------------------------------------------------------ interpolate
 // phi_f = w phi_O + (1 - w) phi_N; boundary: fixed value or phi_O;
@@ -324,7 +329,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_lap(DevMesh<T> M, const T* _
           w[u] = __ldg(&M.fw[f]);
           c[u] = ld4(&M.fcor[f]);
           xn[u] = x[n];
-          Gn[u][0] = G[3 * (int64_t)n]; Gn[u][1] = G[3 * (int64_t)n + 1]; Gn[u][2] = G[3 * (int64_t)n + 2];
+          if (sizeof(T) == 4)       // fp32: the gradient gather in two loads (fp64: three measured faster)
+            ld3(&G[3 * (int64_t)n], Gn[u][0], Gn[u][1], Gn[u][2]);
+          else {
+            Gn[u][0] = G[3 * (int64_t)n]; Gn[u][1] = G[3 * (int64_t)n + 1]; Gn[u][2] = G[3 * (int64_t)n + 2];
+          }
           if (GAMMA) gn[u] = gamma[n];
         } else if (en[u].y == -1) {
           const int b = en[u].x;
@@ -376,10 +385,29 @@ void launch_interpolate(const DevMesh<T>& M, const T* x, int nc, const uint8_t* 
 // shallow batches at 4 resident blocks per SM beat deeper batches at lower
 // occupancy (grad_s 0.62 -> 0.78, lap 0.45 -> 0.64 of the HBM peak).  Grids
 // are one full wave of resident blocks (occupancy API).
+// fp32 variants (DFVM_OPS_F32, read per launch, for A/B): the fp32 kernels
+// need fewer registers, so more resident blocks / deeper batches fit:
+//   0: the fp64 settings; 1: 6 blocks/SM; 2: 8 blocks/SM; 3: batch 4 at 6 blocks/SM
+static int ops_f32_variant() {
+  const char* e = getenv("DFVM_OPS_F32");
+  return e ? atoi(e) : kOpsF32Default;
+}
 template <class T, int NC, bool FV>
 static void grad_any(const DevMesh<T>& M, const T* x, const uint8_t* bk, const T* bv, const T* fv, T* G, cudaStream_t s) {
-  auto fn = k_grad<T, NC, FV, NC == 1 ? 2 : 1, 4>;
-  fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, fv, G);
+  const int v = sizeof(T) == 4 ? ops_f32_variant() : 0;
+  if (v == 1) {
+    auto fn = k_grad<T, NC, FV, NC == 1 ? 2 : 1, 6>;
+    fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, fv, G);
+  } else if (v == 2) {
+    auto fn = k_grad<T, NC, FV, NC == 1 ? 2 : 1, 8>;
+    fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, fv, G);
+  } else if (v == 3) {
+    auto fn = k_grad<T, NC, FV, NC == 1 ? 4 : 2, 6>;
+    fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, fv, G);
+  } else {
+    auto fn = k_grad<T, NC, FV, NC == 1 ? 2 : 1, 4>;
+    fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, x, bk, bv, fv, G);
+  }
 }
 template <class T>
 void launch_grad(const DevMesh<T>& M, const T* x, int nc, const uint8_t* bk, const T* bv, T* G, cudaStream_t s) {
@@ -401,8 +429,20 @@ void launch_div(const DevMesh<T>& M, const T* flux, T* out, cudaStream_t s) {
 template <class T, bool GA>
 static void lap_any(const DevMesh<T>& M, const T* gamma, const T* x, const T* G, const uint8_t* bk, const T* bv, T* y,
                     cudaStream_t s) {
-  auto fn = k_lap<T, GA, 1, 4>;
-  fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+  const int v = sizeof(T) == 4 ? ops_f32_variant() : 0;
+  if (v == 1) {
+    auto fn = k_lap<T, GA, 1, 6>;
+    fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+  } else if (v == 2) {
+    auto fn = k_lap<T, GA, 1, 8>;
+    fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+  } else if (v == 3) {
+    auto fn = k_lap<T, GA, 2, 6>;
+    fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+  } else {
+    auto fn = k_lap<T, GA, 1, 4>;
+    fn<<<grid_slices(fn, M.n_slices), kThreads, 0, s>>>(M, gamma, x, G, bk, bv, y);
+  }
 }
 template <class T>
 void launch_laplacian(const DevMesh<T>& M, const T* gamma, const T* x, const T* G, const uint8_t* bk, const T* bv,

@@ -414,12 +414,10 @@ def test_c1_cavity_100_steps_trajectory():
 
 @pytest.mark.parametrize("precond", ["amg", "amg32"])
 @pytest.mark.parametrize("size", ["pipe_big", "c5_nz6"])
-def test_amg_storage_and_kernel_variants_bitwise(precond, size, monkeypatch):
-    # the coarse-level SELL storage order (DFVM_AMG_PERM: rows sorted by
-    # length within windows of 256 slots) and the fused / unfused coarse
-    # kernels (DFVM_AMG_FUSED_FROM) change the memory traffic only: same rows,
-    # same per-row arithmetic in the same order, hence bitwise equal fields
-    # and identical iteration counts
+def test_amg_kernel_variants_bitwise(precond, size, monkeypatch):
+    # the fused / unfused coarse kernels (DFVM_AMG_FUSED_FROM) change the
+    # memory traffic only: same rows, same per-row arithmetic in the same
+    # order, hence bitwise equal fields and identical iteration counts
     import ctypes
     import torch
     import cases
@@ -437,8 +435,7 @@ def test_amg_storage_and_kernel_variants_bitwise(precond, size, monkeypatch):
     s = torch.cuda.Stream()
     sp = ctypes.c_void_p(s.cuda_stream)
     out = []
-    for env in ({"DFVM_AMG_PERM": "0", "DFVM_AMG_FUSED_FROM": "1"}, {"DFVM_AMG_PERM": "1", "DFVM_AMG_FUSED_FROM": "1"},
-                {"DFVM_AMG_PERM": "1", "DFVM_AMG_FUSED_FROM": "3"}, {"DFVM_AMG_PERM": "0", "DFVM_AMG_FUSED_FROM": "9"}):
+    for env in ({"DFVM_AMG_FUSED_FROM": "1"}, {"DFVM_AMG_FUSED_FROM": "3"}, {"DFVM_AMG_FUSED_FROM": "9"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         Sg = mk()
