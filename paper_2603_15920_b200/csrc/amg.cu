@@ -94,6 +94,11 @@ constexpr int kMaxLevels = 16;
 //                    (C5 amg32: 340.3 ms/step against 349.6 ms with every
 //                    coarse level fused, 347.2 with level 1 unfused;
 //                    profiles/r02_amg_sweep_c5.jsonl)
+//   DFVM_AMG_AGGLOM  several ranks: the first coarse level whose rows, summed
+//                    over the ranks, are <= this is agglomerated into one
+//                    global level replicated on every rank (with the serial
+//                    hierarchy below it); the levels above are distributed
+//                                                               default 100000
 //   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
 //                    exactly with a dense inverse (Gauss-Jordan once per
 //                    matrix update, one block), larger ones with
@@ -101,6 +106,7 @@ constexpr int kMaxLevels = 16;
 struct AmgParams {
   int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, perm = 0;
   int fused_from = 3;   // coarse levels >= this use the fused pre_resid / prolong_smooth kernels
+  int agglom = 100000;  // several ranks: agglomerate the first coarse level with <= this many rows in total
   bool wcycle = true;
   double omega = 1.95;  // C5 amg32 (round 2): 344.0 ms, 11.33 it/solve (1.9: 349.6 ms, 11.58; 1.8: 360.2 ms, 12.17)
   AmgParams() {
@@ -112,6 +118,7 @@ struct AmgParams {
     if (const char* e = getenv("DFVM_AMG_CYCLE")) wcycle = (e[0] == 'W' || e[0] == 'w');
     if (const char* e = getenv("DFVM_AMG_WMAX")) wmax = std::max(0, atoi(e));
     if (const char* e = getenv("DFVM_AMG_FUSED_FROM")) fused_from = std::max(1, atoi(e));
+    if (const char* e = getenv("DFVM_AMG_AGGLOM")) agglom = std::max(32, atoi(e));
   }
 };
 
@@ -528,6 +535,15 @@ static dfvm_status build_dist(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A, cud
   int32_t* d_agg = nullptr;
   while (lev + 1 < kMaxLevels) {
     HostLevel& F = H[lev];
+    // distribute while the level is large; once the union of the ranks'
+    // rows is <= prm.agglom it is agglomerated (below) and the rest of the
+    // hierarchy is replicated: the small levels are latency-bound anyway,
+    // and every distributed visit costs halo exchanges
+    std::vector<double> sizes;
+    if ((st = agree_all(m, (double)F.n, sizes, s))) return st;
+    double total = 0;
+    for (double v : sizes) total += v;
+    if (lev > 0 && total <= A->prm.agglom) break;
     int nc = 0;
     std::vector<int> agg = aggregate(F, nc);
     const bool want = F.n > target && nc < F.n * 0.85 && nc >= 32;
