@@ -34,6 +34,7 @@
 //    vector in fp32; the PCG itself — residual, dots, x, p — stays fp64).
 //    Level 0 reads the PCG residual in T and writes z = M^-1 r in T.
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -107,6 +108,7 @@ struct AmgParams {
   int coarse = 256, sweeps = 32, wmax = 4, direct = kDirectMax, perm = 0;
   int fused_from = 3;   // coarse levels >= this use the fused pre_resid / prolong_smooth kernels
   int agglom = 100000;  // several ranks: agglomerate the first coarse level with <= this many rows in total
+  int renum = 0;        // 1: aggregates renumbered by their first member (locality order)
   bool wcycle = true;
   double omega = 1.95;  // C5 amg32 (round 2): 344.0 ms, 11.33 it/solve (1.9: 349.6 ms, 11.58; 1.8: 360.2 ms, 12.17)
   AmgParams() {
@@ -119,6 +121,7 @@ struct AmgParams {
     if (const char* e = getenv("DFVM_AMG_WMAX")) wmax = std::max(0, atoi(e));
     if (const char* e = getenv("DFVM_AMG_FUSED_FROM")) fused_from = std::max(1, atoi(e));
     if (const char* e = getenv("DFVM_AMG_AGGLOM")) agglom = std::max(32, atoi(e));
+    if (const char* e = getenv("DFVM_AMG_RENUM")) renum = atoi(e);
   }
 };
 
@@ -222,6 +225,23 @@ std::vector<int> aggregate(const HostLevel& L, int& nagg) {
   return agg;
 }
 
+// Locality order of the aggregates: renumber by their smallest member row, so
+// the coarse rows follow the fine (RCM) order — pass-3 leftovers, created
+// last, land next to their members instead of at the end (coarse gathers
+// stay local).  A monotone map of the fine order: no change to which rows
+// are aggregated, but the next level's greedy aggregation sees a different
+// row order.
+void renumber_by_first_member(std::vector<int>& agg, int nc) {
+  std::vector<int> first(nc, INT32_MAX);
+  for (int i = 0; i < (int)agg.size(); ++i) first[agg[i]] = std::min(first[agg[i]], i);
+  std::vector<int> order(nc);
+  for (int I = 0; I < nc; ++I) order[I] = I;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return first[a] < first[b]; });
+  std::vector<int> newid(nc);
+  for (int k = 0; k < nc; ++k) newid[order[k]] = k;
+  for (auto& a : agg) a = newid[a];
+}
+
 }  // namespace
 
 template <class P>
@@ -266,6 +286,9 @@ struct AmgH {
   HaloLists halos[kMaxLevels];
   int ld = -1;                      // last distributed level (-1: single rank)
   bool agglom = false;
+  // depth of level l in the single-rank sense (the agglomerated level is the
+  // replicated copy of level ld, so the W-cycle depth rule skips it)
+  int depth(int l) const { return (agglom && l > ld) ? l - 1 : l; }
   int Vmax = 0, Nmax = 0;           // padded per-rank value / row counts of the exchanges
   int Vloc = 0;                     // this rank's values
   int* d_pk = nullptr;              // canonical value k of this rank's level-ld rows: >= 0 coef position, < 0 diag -1-i
@@ -316,6 +339,7 @@ static dfvm_status coarsen_serial(AmgH<P>* A, std::vector<HostLevel>& H, int& le
     const HostLevel& F = H[lev];
     int nc = 0;
     std::vector<int> agg = aggregate(F, nc);
+    if (A->prm.renum) renumber_by_first_member(agg, nc);
     if (nc >= F.n * 0.85) break;           // coarsening stalled
     // no degenerate tiny level: C5 with DFVM_AMG_COARSE=128 grew an 8-row
     // level under the 144-row one and the PCG needed 1702 iterations per
@@ -546,6 +570,7 @@ static dfvm_status build_dist(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A, cud
     if (lev > 0 && total <= A->prm.agglom) break;
     int nc = 0;
     std::vector<int> agg = aggregate(F, nc);
+    if (A->prm.renum) renumber_by_first_member(agg, nc);
     const bool want = F.n > target && nc < F.n * 0.85 && nc >= 32;
     if ((st = agree_all(m, want ? 1.0 : 0.0, votes, s))) return st;
     bool all = true;
@@ -1303,7 +1328,7 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
           (k_amg_restrict<P><<<gC, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
   *nl += 2;
   cycle_coarse(A, l + 1, C.b, C.x, done, s, nl);
-  if (A->prm.wcycle && l + 1 < A->nlev - 1 && l + 1 <= A->prm.wmax) {
+  if (A->prm.wcycle && l + 1 < A->nlev - 1 && A->depth(l + 1) <= A->prm.wmax) {
     PLAUNCH(pr, "k_amg_resid", l + 1, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
             (k_amg_resid<P, P><<<gC, kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.x, C.b, C.r2,
                                                        done)));
@@ -1395,7 +1420,7 @@ static dfvm_status coarse_correction(AmgH<P>* A, int l, const int* done, cudaStr
   dfvm_status e;
   if (A->dist) { if ((e = cycle_dist(A, l, C.b, C.x, done, s, nl))) return e; }
   else cycle_coarse(A, l, C.b, C.x, done, s, nl);
-  if (A->prm.wcycle && l < A->nlev - 1 && l <= A->prm.wmax) {
+  if (A->prm.wcycle && l < A->nlev - 1 && A->depth(l) <= A->prm.wmax) {
     if (A->dist && (e = halo_exchange_lists(A->m, A->halos[l], C.x, 1, f64, s))) return e;
     PLAUNCH(pr, "k_amg_resid", l, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
             (k_amg_resid<P, P><<<gC, kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.x, C.b, C.r2, done)));
