@@ -135,6 +135,7 @@ struct SellView {
   const int* ms_len;
   const int* mnb;
   const int* perm;
+  const unsigned char* rlen;   // per-slot row length (coarse levels), NULL: the slice length
 };
 // ------------------------------------------------------------ host setup
 namespace {
@@ -251,7 +252,9 @@ struct AmgLevelDev {
   int64_t nnz = 0;           // real off-diagonal entries (algorithmic bytes)
   const int *ms_ptr = nullptr, *ms_len = nullptr, *mnb = nullptr;
   const int* perm = nullptr;  // SELL slot -> row (coarse levels, SELL-32-sigma storage), NULL: identity
-  SellView sv() const { return SellView{ms_ptr, ms_len, mnb, perm}; }
+  const unsigned char* rlen = nullptr;   // per-slot row length (serial coarse levels), NULL: slice length
+  SellView sv() const { return SellView{ms_ptr, ms_len, mnb, perm, use_rlen ? rlen : nullptr}; }
+  bool use_rlen = false;
   const P* coef = nullptr;   // level 0: the solver's pcoef (P == T) or coef_own (fp32 copy)
   const P* diag = nullptr;   // level 0: the solver's pdiag (P == T) or diag_own
   P* coef_own = nullptr;
@@ -265,6 +268,8 @@ struct AmgLevelDev {
   P *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr;
   P *e = nullptr, *r2 = nullptr;                  // W-cycle: second-visit solution / rhs
   int n_cells = 0;                                // owned + ghost rows (several ranks)
+  int G = 1;                                      // lanes per row of this level's matrix kernels
+  int Gr = 1;                                     // lanes per row of the restriction INTO this level
 };
 
 // hierarchy stored and cycled in type P
@@ -434,18 +439,68 @@ static dfvm_status coarsen_serial(AmgH<P>* A, std::vector<HostLevel>& H, int& le
     D.n = nc; D.n_slices = S; D.n_sell = C.ms_ptr[S];
     D.nnz = (int64_t)ccol.size();
     int *p0, *p1, *p2, *p3 = nullptr;
-    if (!C.perm.empty() && (st = A->up(&p3, C.perm))) return st;
+    // perm == 2 (relabel): the coarse rows are RENUMBERED by their SELL slot
+    // on the device (row q lives in slot q, no indirection): columns, member
+    // lists, diagonal lists and the fine level's aggregate map are uploaded
+    // in slot order (the fine rows in the fine level's slot order).  The host
+    // levels keep the original numbering, so the aggregation below — hence
+    // the hierarchy and every per-row sum order — is that of natural order;
+    // only storage padding (and own-row contiguity) changes.
+    const bool relabel = A->prm.perm == 2 && !C.perm.empty();
+    std::vector<int> mnb_u, mem_ptr_u, mem_u, dg_ptr_u, dg_idx_u, agg_u;
+    const std::vector<int>* up_mnb = &C.mnb;
+    const std::vector<int>*up_mp = &mem_ptr, *up_mem = &mem, *up_dp = &dg_ptr, *up_di = &dg_idx, *up_agg = &agg;
+    if (relabel) {
+      const std::vector<int>& pf = F.slot_of;   // the fine level's relabelling (level 0: none)
+      auto PF = [&](int i) { return pf.empty() ? i : pf[i]; };
+      mnb_u.resize(C.mnb.size());
+      for (size_t k = 0; k < C.mnb.size(); ++k) mnb_u[k] = C.slot_of[C.mnb[k]];
+      mem_ptr_u.assign(nc + 1, 0); dg_ptr_u.assign(nc + 1, 0);
+      mem_u.reserve(mem.size()); dg_idx_u.reserve(dg_idx.size());
+      for (int q = 0; q < nc; ++q) {
+        const int I = C.perm[q];
+        for (int k = mem_ptr[I]; k < mem_ptr[I + 1]; ++k) mem_u.push_back(PF(mem[k]));
+        for (int k = dg_ptr[I]; k < dg_ptr[I + 1]; ++k) dg_idx_u.push_back(dg_idx[k]);
+        mem_ptr_u[q + 1] = (int)mem_u.size();
+        dg_ptr_u[q + 1] = (int)dg_idx_u.size();
+      }
+      agg_u.resize(agg.size());
+      for (int i = 0; i < (int)agg.size(); ++i) agg_u[PF(i)] = C.slot_of[agg[i]];
+      up_mnb = &mnb_u; up_mp = &mem_ptr_u; up_mem = &mem_u; up_dp = &dg_ptr_u; up_di = &dg_idx_u; up_agg = &agg_u;
+    } else if (!C.perm.empty() && (st = A->up(&p3, C.perm))) {
+      return st;
+    }
     D.perm = p3;
-    if ((st = A->up(&p0, C.ms_ptr)) || (st = A->up(&p1, C.ms_len)) || (st = A->up(&p2, C.mnb)) ||
-        (st = A->up(&D.gal_ptr, gal_ptr)) || (st = A->up(&D.gal_idx, gal_idx)) || (st = A->up(&D.dg_ptr, dg_ptr)) ||
-        (st = A->up(&D.dg_idx, dg_idx)) || (st = A->up(&D.mem_ptr, mem_ptr)) || (st = A->up(&D.mem, mem)) ||
-        (st = A->up(&A->L[lev].agg, agg)) || (st = A->zalloc(&D.coef_own, (size_t)D.n_sell)) ||
+    if ((st = A->up(&p0, C.ms_ptr)) || (st = A->up(&p1, C.ms_len)) || (st = A->up(&p2, *up_mnb)) ||
+        (st = A->up(&D.gal_ptr, gal_ptr)) || (st = A->up(&D.gal_idx, gal_idx)) || (st = A->up(&D.dg_ptr, *up_dp)) ||
+        (st = A->up(&D.dg_idx, *up_di)) || (st = A->up(&D.mem_ptr, *up_mp)) || (st = A->up(&D.mem, *up_mem)) ||
+        (st = A->up(&A->L[lev].agg, *up_agg)) || (st = A->zalloc(&D.coef_own, (size_t)D.n_sell)) ||
         (st = A->zalloc(&D.diag_own, nc)) || (st = A->zalloc(&D.il1, nc)) || (st = A->zalloc(&D.x, nc)) ||
         (st = A->zalloc(&D.b, nc)) || (st = A->zalloc(&D.r, nc)) || (st = A->zalloc(&D.t, nc)) ||
         (st = A->zalloc(&D.e, nc)) || (st = A->zalloc(&D.r2, nc)))
       return st;
     D.ms_ptr = p0; D.ms_len = p1; D.mnb = p2;
     D.coef = D.coef_own; D.diag = D.diag_own;
+    {
+      // per-slot row lengths: DFVM_AMG_RLEN=1 stops each lane at its own
+      // row (padding neither loaded nor gathered).  Default off: measured on
+      // C5 round 2 at 335.1 / 337.7 ms/step against 334.6 / 333.6 with every
+      // lane walking the slice length (profiles/r02_sweep_r2h.jsonl) — the
+      // coarse kernels are bound by their gathers' latency, not by the
+      // padding's bytes, and the divergent trip counts cost more
+      std::vector<unsigned char> rl(nc);
+      bool fits = true;
+      for (int q = 0; q < nc; ++q) {
+        const int I = row_at(q), l = crow_ptr[I + 1] - crow_ptr[I];
+        fits = fits && l < 256;
+        rl[q] = (unsigned char)std::min(l, 255);
+      }
+      const char* e = getenv("DFVM_AMG_RLEN");
+      D.use_rlen = e && atoi(e) == 1;
+      unsigned char* d_rl = nullptr;
+      if (fits && (st = A->up(&d_rl, rl))) return st;
+      D.rlen = fits ? d_rl : nullptr;
+    }
     H.push_back(std::move(C));
     ++lev;
   }
@@ -818,6 +873,31 @@ static dfvm_status build_dist(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A, cud
   return DFVM_OK;
 }
 
+// Lanes per row of each level's kernels: one thread per row
+// while the level alone fills the GPU (kGroupFill threads), else the
+// smallest power of two G <= 16 (32 for the restriction) that does, bounded
+// by the entries (members) per row — the deep levels are latency bound, and
+// G lanes cut a row's chain of dependent gathers by G.  Level 0 keeps one
+// thread per row.  DFVM_AMG_GROUP=0: one thread per row everywhere.
+constexpr int64_t kGroupFill = 148 * 2048;
+static int group_for(int64_t n, double per_row, int gmax) {
+  int G = 1;
+  while (G < gmax && n * G < kGroupFill && G < per_row) G *= 2;
+  return G;
+}
+template <class P>
+static void set_groups(AmgH<P>* A) {
+  const char* e = getenv("DFVM_AMG_GROUP");
+  const bool on = !(e && atoi(e) == 0);
+  for (int l = 0; l < A->nlev; ++l) {
+    AmgLevelDev<P>& L = A->L[l];
+    L.G = (on && l > 0) ? group_for(L.n, (double)L.nnz / std::max(1, L.n), 16) : 1;
+    L.Gr = (on && l > 0) ? group_for(L.n, (double)A->L[l - 1].n / std::max(1, L.n), 32) : 1;
+  }
+  if (getenv("DFVM_AMG_VERBOSE"))
+    for (int l = 0; l < A->nlev; ++l) fprintf(stderr, "[amg] level %d: %d lanes per row, %d per restricted row\n", l, A->L[l].G, A->L[l].Gr);
+}
+
 template <class T>
 dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** out, cudaStream_t s) {
   Amg<T>* A = new Amg<T>();
@@ -831,6 +911,7 @@ dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** ou
     st = dist ? build_dist<T, T>(m, M, A->same, s) : build<T, T>(m, M, A->same);
   }
   if (st) { delete A; return st; }
+  if (A->lo) set_groups(A->lo); else set_groups(A->same);
   DFVM_CUDA(cudaStreamSynchronize(nullptr));   // pageable uploads + zero-fills done before the caller's stream runs
   *out = A;
   return DFVM_OK;
@@ -850,6 +931,7 @@ int amg_levels(const Amg<T>* A, int* sizes) { return A->same ? levels(A->same, s
 // ------------------------------------------------------------ kernels
 template <class P, class T>
 __global__ void k_amg_cvt(int64_t n, const T* __restrict__ a, P* __restrict__ b) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = (P)a[i];
 }
@@ -857,6 +939,7 @@ __global__ void k_amg_cvt(int64_t n, const T* __restrict__ a, P* __restrict__ b)
 template <class T>
 __global__ void k_gal_off(int64_t n_sell, const int* __restrict__ gp, const int* __restrict__ gi,
                           const T* __restrict__ fcoef, T* __restrict__ ccoef) {
+  PDL_ENTRY();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_sell; e += (int64_t)gridDim.x * blockDim.x) {
     T s = T(0);
     for (int k = gp[e]; k < gp[e + 1]; ++k) s += fcoef[gi[k]];
@@ -868,6 +951,7 @@ template <class T>
 __global__ void k_gal_diag(int n, const int* __restrict__ mp, const int* __restrict__ mem,
                            const int* __restrict__ dp, const int* __restrict__ di, const T* __restrict__ fdiag,
                            const T* __restrict__ fcoef, T* __restrict__ cdiag) {
+  PDL_ENTRY();
   for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < n; I += gridDim.x * blockDim.x) {
     T s = T(0);
     for (int k = mp[I]; k < mp[I + 1]; ++k) s += fdiag[mem[k]];
@@ -882,6 +966,7 @@ __device__ __forceinline__ int slot_row(const SellView& S, int q) { return S.per
 // (stored inverted: the smoothers multiply, no fp64 division per gather)
 template <class T>
 __global__ void k_il1(int n, SellView S, const T* __restrict__ coef, const T* __restrict__ diag, T* __restrict__ il1) {
+  PDL_ENTRY();
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
     const int r = slot_row(S, q), sl = q >> 5, lane = q & 31;
     T a = diag[r];
@@ -890,172 +975,203 @@ __global__ void k_il1(int n, SellView S, const T* __restrict__ coef, const T* __
   }
 }
 
+// ---- SELL row sums with G lanes per row
+// Slot q's entries j = sub, sub + G, sub + 2G, ... are summed by lane `sub`
+// of the row's G-lane group, in batches of 4 entries: every column /
+// coefficient load of the batch first, then every gathered value, then the
+// FMAs in entry order; the last batch is predicated (no dependent load chain
+// for a leftover entry: one memory round trip per batch).  G = 1 keeps the
+// strict entry order of one thread per row.  G > 1 (small coarse levels,
+// which are latency bound: one thread per row walks 15 entries in 4
+// dependent rounds) splits the row over G lanes and combines the partials
+// with a shuffle tree (lane 0 of the group ends with the sum).
+template <int G, class T, class NB>
+__device__ __forceinline__ T row_part(const SellView& S, int q, int sub, bool live, const T* __restrict__ coef, T acc,
+                                      NB nb) {
+  const int sl = q >> 5, lane = q & 31;
+  // a lane stops at its own row's length (S.rlen): the padding slots of
+  // shorter rows in the slice are neither loaded nor gathered — SELL-32
+  // padding is 30-35 % on the aggregation levels, and a sector whose 8 lanes
+  // are all padding is never fetched (same sums: padding coefficients are 0)
+  const int len = live ? (S.rlen ? (int)__ldg(&S.rlen[q]) : __ldg(&S.ms_len[sl])) : 0;
+  const int base = live ? __ldg(&S.ms_ptr[sl]) + lane : 0;
+  if constexpr (G == 1) {
+    // one thread per row: whole batches, then the leftover entries one by one
+    // (measured on C5: a predicated last batch was 4 % slower on level 2)
+    int j = 0;
+    for (; j + 4 <= len; j += 4) {
+      T a[4], v[4];
+      int c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&S.mnb[base + 32 * (j + u)]); }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = nb(c[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
+    }
+    for (; j < len; ++j) acc += __ldg(&coef[base + 32 * j]) * nb(__ldg(&S.mnb[base + 32 * j]));
+    return acc;
+  }
+  for (int j = sub; j < len; j += 4 * G) {
+    T a[4], v[4];
+    int c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = j + u * G < len;
+      a[u] = ok ? __ldg(&coef[base + 32 * (j + u * G)]) : T(0);
+      c[u] = ok ? __ldg(&S.mnb[base + 32 * (j + u * G)]) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = c[u] >= 0 ? nb(c[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c[u] >= 0) acc += a[u] * v[u];
+  }
+  return acc;
+}
+template <int G, class T>
+__device__ __forceinline__ T group_sum(T v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, G);
+  return v;
+}
+// Grid-stride loop over the n rows with G consecutive threads per row.  The
+// trip count is rounded up to whole warps so every lane of a warp takes part
+// in the group shuffles; `live` marks the threads that own a real row, q_ is
+// the SELL slot, sub_ the lane within the row's group.
+#define AMG_GROUP_LOOP(n, G)                                                                               \
+  const int sub_ = (int)(threadIdx.x & ((G) - 1));                                                          \
+  const int64_t nt_ = (int64_t)(n) * (G), nt32_ = (nt_ + 31) & ~(int64_t)31;                                \
+  for (int64_t t_ = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t_ < nt32_; t_ += (int64_t)gridDim.x * blockDim.x) \
+    if (const bool live = t_ < nt_; true)                                                                   \
+      if (const int q_ = live ? (int)(t_ / (G)) : 0; true)
+
 template <class T>
 __device__ __forceinline__ T row_apply(const SellView& S, int q, int r, const T* __restrict__ coef,
                                        const T* __restrict__ diag, const T* __restrict__ x) {
-  const int sl = q >> 5, lane = q & 31;
-  const int len = S.ms_len[sl], base = S.ms_ptr[sl] + lane;
-  T acc = diag[r] * x[r];
-  int j = 0;
-  for (; j + 4 <= len; j += 4) {
-    T a[4];
-    int c[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&S.mnb[base + 32 * (j + u)]); }
-    T v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = x[c[u]];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
-  }
-  for (; j < len; ++j) acc += __ldg(&coef[base + 32 * j]) * x[__ldg(&S.mnb[base + 32 * j])];
-  return acc;
+  return row_part<1>(S, q, 0, true, coef, diag[r] * x[r], [&](int c) { return x[c]; });
 }
-
-// One row of the fused pre-smooth + residual: x0_i = b_i / d1_i and
-// r_i = b_i - (A x0)_i with x0 of the neighbours formed on the fly.  Loads in
-// batches of 4 entries (columns + coefficients, then the gathered b and 1/d1),
-// accumulation in entry order.
-template <class T>
-__device__ __forceinline__ void pre_resid_row(const SellView& S, int q, int i, const T* __restrict__ coef,
-                                              const T* __restrict__ diag, const T* __restrict__ il1,
-                                              const T* __restrict__ b, T& x0, T& r) {
-  const int sl = q >> 5, lane = q & 31;
-  const int len = S.ms_len[sl], base = S.ms_ptr[sl] + lane;
-  const T bi = b[i];
-  const T xi = bi * il1[i];
-  T acc = diag[i] * xi;
-  int j = 0;
-  for (; j + 4 <= len; j += 4) {
-    T a[4], v[4];
-    int c[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&S.mnb[base + 32 * (j + u)]); }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = b[c[u]] * il1[c[u]];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
-  }
-  for (; j < len; ++j) {
-    const int c = __ldg(&S.mnb[base + 32 * j]);
-    acc += __ldg(&coef[base + 32 * j]) * (b[c] * il1[c]);
-  }
-  x0 = xi;
-  r = bi - acc;
-}
-// One row of the fused prolongation + post-smooth: t = x0 + w x_c[agg] (on
-// the fly for the row and its neighbours), returns t_i + (b - A t)_i / d1_i.
-template <class T>
-__device__ __forceinline__ T prolong_smooth_row(const SellView& S, int q, int i, const T* __restrict__ coef,
-                                                const T* __restrict__ diag, const T* __restrict__ il1,
-                                                const int* __restrict__ agg, const T* __restrict__ xc, T w,
-                                                const T* __restrict__ x0, const T* __restrict__ b) {
-  const int sl = q >> 5, lane = q & 31;
-  const int len = S.ms_len[sl], base = S.ms_ptr[sl] + lane;
-  const T ti = x0[i] + w * xc[agg[i]];
-  T acc = diag[i] * ti;
-  int j = 0;
-  for (; j + 4 <= len; j += 4) {
-    T a[4], v[4];
-    int c[4], g[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { a[u] = __ldg(&coef[base + 32 * (j + u)]); c[u] = __ldg(&S.mnb[base + 32 * (j + u)]); }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { g[u] = agg[c[u]]; v[u] = x0[c[u]]; }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = v[u] + w * xc[g[u]];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc += a[u] * v[u];
-  }
-  for (; j < len; ++j) {
-    const int c = __ldg(&S.mnb[base + 32 * j]);
-    acc += __ldg(&coef[base + 32 * j]) * (x0[c] + w * xc[agg[c]]);
-  }
-  return ti + (b[i] - acc) * il1[i];
-}
-
-#define AMG_SLOT_LOOP(n) for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < (n); q += gridDim.x * blockDim.x)
 
 // x = b / d1 (pre-smoothing from a zero guess); b in the caller's type TB
 template <class P, class TB, class TX>
 __global__ void k_amg_pre(int n, const TB* __restrict__ b, const P* __restrict__ il1, TX* __restrict__ x,
                           const int* done) {
+  PDL_ENTRY();
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     x[i] = (TX)((P)b[i] * il1[i]);
 }
 // r = b - A x
-template <class P, class TB>
+template <int G, class P, class TB>
 __global__ void k_amg_resid(int n, SellView S, const P* __restrict__ coef, const P* __restrict__ diag,
                             const P* __restrict__ x, const TB* __restrict__ b, P* __restrict__ r, const int* done) {
+  PDL_ENTRY();
   if (*done) return;
-  AMG_SLOT_LOOP(n) {
-    const int i = slot_row(S, q);
-    r[i] = (P)b[i] - row_apply(S, q, i, coef, diag, x);
+  AMG_GROUP_LOOP(n, G) {
+    const int i = live ? slot_row(S, q_) : 0;
+    P acc = (live && sub_ == 0) ? diag[i] * x[i] : P(0);
+    acc = group_sum<G>(row_part<G>(S, q_, sub_, live, coef, acc, [&](int c) { return x[c]; }));
+    if (live && sub_ == 0) r[i] = (P)b[i] - acc;
   }
 }
-// b_c[I] = sum over the aggregate's members of r_f
-template <class T>
+// b_c[I] = sum over the aggregate's members of r_f (G lanes per coarse row:
+// deep levels have 17-24 members per aggregate)
+template <int G, class T>
 __global__ void k_amg_restrict(int nc, const int* __restrict__ mp, const int* __restrict__ mem,
                                const T* __restrict__ rf, T* __restrict__ bc, const int* done) {
+  PDL_ENTRY();
   if (*done) return;
-  for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
+  AMG_GROUP_LOOP(nc, G) {
+    const int k0 = live ? __ldg(&mp[q_]) : 0, k1 = live ? __ldg(&mp[q_ + 1]) : 0;
     T s = T(0);
-    for (int k = mp[I]; k < mp[I + 1]; ++k) s += rf[mem[k]];
-    bc[I] = s;
+    if (G == 1)
+      for (int k = k0; k < k1; ++k) s += rf[__ldg(&mem[k])];
+    else
+    for (int k = k0 + sub_; k < k1; k += 4 * G) {
+      int f[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) f[u] = k + u * G < k1 ? __ldg(&mem[k + u * G]) : -1;
+      T v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = f[u] >= 0 ? rf[f[u]] : T(0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (f[u] >= 0) s += v[u];
+    }
+    s = group_sum<G>(s);
+    if (live && sub_ == 0) bc[q_] = s;
   }
 }
 // t = x + w x_c[agg[i]]  (coarse correction, out of place: t feeds the smoother)
 template <class T>
 __global__ void k_amg_prolong(int n, const int* __restrict__ agg, const T* __restrict__ xc, const T* __restrict__ x,
                               T* __restrict__ t, T w, const int* done) {
+  PDL_ENTRY();
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = x[i] + w * xc[agg[i]];
 }
 // fused pre-smooth + residual (rows without ghost columns): x0 = b / d1 for
 // the row and, on the fly, for every neighbour; writes x0 and r = b - A x0
-template <class T>
+template <int G, class T>
 __global__ void k_amg_pre_resid(int n, SellView S, const T* __restrict__ coef, const T* __restrict__ diag,
                                 const T* __restrict__ il1, const T* __restrict__ b, T* __restrict__ x0,
                                 T* __restrict__ r, const int* done) {
+  PDL_ENTRY();
   if (*done) return;
-  AMG_SLOT_LOOP(n) {
-    const int i = slot_row(S, q);
-    T xv, rv;
-    pre_resid_row(S, q, i, coef, diag, il1, b, xv, rv);
-    x0[i] = xv;
-    r[i] = rv;
+  AMG_GROUP_LOOP(n, G) {
+    const int i = live ? slot_row(S, q_) : 0;
+    T bi = T(0), xi = T(0), acc = T(0);
+    if (live && sub_ == 0) { bi = b[i]; xi = bi * il1[i]; acc = diag[i] * xi; }
+    acc = group_sum<G>(row_part<G>(S, q_, sub_, live, coef, acc, [&](int c) { return b[c] * il1[c]; }));
+    if (live && sub_ == 0) { x0[i] = xi; r[i] = bi - acc; }
   }
 }
 // fused prolongation + post-smooth: t = x0 + w P x_c (on the fly for the row
-// and its neighbours), out = t + (b - A t) / d1
-template <class T>
+// and its neighbours), out = t + (b - A t) / d1; accum: out += that instead
+// (the W-cycle's second visit adds its correction in place)
+template <int G, class T>
 __global__ void k_amg_prolong_smooth(int n, SellView S, const T* __restrict__ coef, const T* __restrict__ diag,
                                      const T* __restrict__ il1, const int* __restrict__ agg, const T* __restrict__ xc,
                                      T w, const T* __restrict__ x0, const T* __restrict__ b, T* __restrict__ out,
-                                     const int* done) {
+                                     int accum, const int* done) {
+  PDL_ENTRY();
   if (*done) return;
-  AMG_SLOT_LOOP(n) {
-    const int i = slot_row(S, q);
-    out[i] = prolong_smooth_row(S, q, i, coef, diag, il1, agg, xc, w, x0, b);
+  AMG_GROUP_LOOP(n, G) {
+    const int i = live ? slot_row(S, q_) : 0;
+    T ti = T(0), acc = T(0);
+    if (live && sub_ == 0) { ti = x0[i] + w * xc[agg[i]]; acc = diag[i] * ti; }
+    acc = group_sum<G>(
+        row_part<G>(S, q_, sub_, live, coef, acc, [&](int c) { return x0[c] + w * xc[agg[c]]; }));
+    if (live && sub_ == 0) {
+      const T z = ti + (b[i] - acc) * il1[i];
+      out[i] = accum ? out[i] + z : z;
+    }
   }
 }
 
 // x += e
 template <class T>
 __global__ void k_amg_add(int n, const T* __restrict__ e, T* __restrict__ x, const int* done) {
+  PDL_ENTRY();
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] += e[i];
 }
-// out = x + (b - A x) / d1   (b in TB, out in TO: level 0 reads / writes the PCG's type)
-template <class P, class TB, class TO>
+// out = x + (b - A x) / d1   (b in TB, out in TO: level 0 reads / writes the
+// PCG's type); accum: out += that (W-cycle second visit, in place)
+template <int G, class P, class TB, class TO>
 __global__ void k_amg_smooth(int n, SellView S, const P* __restrict__ coef, const P* __restrict__ diag,
                              const P* __restrict__ il1, const P* __restrict__ x, const TB* __restrict__ b,
-                             TO* __restrict__ out, const int* done) {
+                             TO* __restrict__ out, int accum, const int* done) {
+  PDL_ENTRY();
   if (*done) return;
-  AMG_SLOT_LOOP(n) {
-    const int i = slot_row(S, q);
-    out[i] = (TO)(x[i] + ((P)b[i] - row_apply(S, q, i, coef, diag, x)) * il1[i]);
+  AMG_GROUP_LOOP(n, G) {
+    const int i = live ? slot_row(S, q_) : 0;
+    P acc = (live && sub_ == 0) ? diag[i] * x[i] : P(0);
+    acc = group_sum<G>(row_part<G>(S, q_, sub_, live, coef, acc, [&](int c) { return x[c]; }));
+    if (live && sub_ == 0) {
+      const TO z = (TO)(x[i] + ((P)b[i] - acc) * il1[i]);
+      out[i] = accum ? (TO)(out[i] + z) : z;
+    }
   }
 }
 // level-0 post-smoother with the PCG's r.z folded in: z = t + (r - A t) / d1
@@ -1064,9 +1180,10 @@ template <class P, class T>
 __global__ void __launch_bounds__(kThreads) k_amg_smooth_dot(int n, SellView S, const P* __restrict__ coef,
     const P* __restrict__ diag, const P* __restrict__ il1, const P* __restrict__ x, const T* __restrict__ b,
     T* __restrict__ out, const int* done, double* partials, unsigned* ticket, KCtl* ctl, Red red, int kind) {
+  PDL_ENTRY();
   if (*done) return;
   double v[1] = {0};
-  AMG_SLOT_LOOP(n) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
     const int i = slot_row(S, q);
     const T bi = b[i];
     const T zi = (T)(x[i] + ((P)bi - row_apply(S, q, i, coef, diag, x)) * il1[i]);
@@ -1083,6 +1200,7 @@ __global__ void __launch_bounds__(1024) k_amg_coarse(int n, SellView S, const P*
                                                     const P* __restrict__ diag, const P* __restrict__ il1,
                                                     const TB* __restrict__ b, TO* __restrict__ xout, int sweeps,
                                                     const int* done) {
+  PDL_ENTRY();
   if (*done) return;
   __shared__ P xs[2][kCoarseMax];
   for (int i = threadIdx.x; i < n; i += blockDim.x) xs[0][i] = (P)b[i] * il1[i];
@@ -1106,6 +1224,7 @@ __global__ void __launch_bounds__(1024) k_amg_coarse(int n, SellView S, const P*
 template <class P>
 __global__ void __launch_bounds__(1024) k_amg_dense_inv(int n, SellView S, const P* __restrict__ coef,
                                                         const P* __restrict__ diag, P* __restrict__ A) {
+  PDL_ENTRY();
   __shared__ P colk[kDirectMax], rowk[kDirectMax];
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) A[e] = P(0);
   __syncthreads();
@@ -1135,25 +1254,67 @@ __global__ void __launch_bounds__(1024) k_amg_dense_inv(int n, SellView S, const
   }
 }
 
-// coarsest solve with the dense inverse: x_i = sum_j Ainv_ij b_j (one block)
+// coarsest solve with the dense inverse: x_i = sum_j Ainv_ij b_j, one warp
+// per row (row-major Ainv: coalesced across the lanes, 4 loads in flight per
+// lane), shuffle tree; as many blocks as the rows need (was one block: a
+// 144-row solve took ~8 us).  accum: x += that (W-cycle second visit).
 template <class P, class TB, class TO>
-__device__ __forceinline__ void dense_solve_block(int n, const P* __restrict__ Ai, const TB* __restrict__ b,
-                                                  TO* __restrict__ x) {
-  // one warp per row (row-major Ainv: coalesced across the lanes), shuffle tree
-  const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int i = threadIdx.x >> 5; i < n; i += nwarps) {
+__global__ void __launch_bounds__(kThreads) k_amg_dense(int n, const P* __restrict__ Ai, const TB* __restrict__ b,
+                                                        TO* __restrict__ x, int accum, const int* done) {
+  PDL_ENTRY();
+  if (*done) return;
+  const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); i < n; i += nw) {
     P acc = P(0);
-    for (int j = lane; j < n; j += 32) acc += Ai[(size_t)i * n + j] * (P)b[j];
+    const P* row = Ai + (size_t)i * n;
+#pragma unroll 4
+    for (int j = lane; j < n; j += 32) acc += row[j] * (P)b[j];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) x[i] = (TO)acc;
+    if (lane == 0) x[i] = accum ? (TO)(x[i] + (TO)acc) : (TO)acc;
   }
 }
+
+// ---- host launchers for the group-templated kernels (G in {1,2,4,...,32})
+#define AMG_G_SWITCH(G, CALL)                      \
+  switch (G) {                                     \
+    case 2: { constexpr int kG = 2; CALL; } break;   \
+    case 4: { constexpr int kG = 4; CALL; } break;   \
+    case 8: { constexpr int kG = 8; CALL; } break;   \
+    case 16: { constexpr int kG = 16; CALL; } break; \
+    case 32: { constexpr int kG = 32; CALL; } break; \
+    default: { constexpr int kG = 1; CALL; } break;  \
+  }
+inline int grid_group(int64_t n, int G) { return grid_for(n * G); }
+
+template <class P, class TB>
+static void launch_resid(int G, int n, const SellView& S, const P* coef, const P* diag, const P* x, const TB* b, P* r,
+                         const int* done, cudaStream_t s) {
+  AMG_G_SWITCH(G, (k_amg_resid<kG, P, TB><<<grid_group(n, kG), kThreads, 0, s>>>(n, S, coef, diag, x, b, r, done)));
+}
+template <class P>
+static void launch_restrict(int G, int nc, const int* mp, const int* mem, const P* rf, P* bc, const int* done,
+                            cudaStream_t s) {
+  AMG_G_SWITCH(G, (k_amg_restrict<kG, P><<<grid_group(nc, kG), kThreads, 0, s>>>(nc, mp, mem, rf, bc, done)));
+}
+template <class P>
+static void launch_pre_resid(int G, int n, const SellView& S, const P* coef, const P* diag, const P* il1, const P* b,
+                             P* x0, P* r, const int* done, cudaStream_t s) {
+  AMG_G_SWITCH(G, (k_amg_pre_resid<kG, P><<<grid_group(n, kG), kThreads, 0, s>>>(n, S, coef, diag, il1, b, x0, r,
+                                                                                 done)));
+}
+template <class P>
+static void launch_prolong_smooth(int G, int n, const SellView& S, const P* coef, const P* diag, const P* il1,
+                                  const int* agg, const P* xc, P w, const P* x0, const P* b, P* out, int accum,
+                                  const int* done, cudaStream_t s) {
+  AMG_G_SWITCH(G, (k_amg_prolong_smooth<kG, P><<<grid_group(n, kG), kThreads, 0, s>>>(n, S, coef, diag, il1, agg, xc,
+                                                                                      w, x0, b, out, accum, done)));
+}
 template <class P, class TB, class TO>
-__global__ void __launch_bounds__(1024) k_amg_dense(int n, const P* __restrict__ Ai, const TB* __restrict__ b,
-                                                    TO* __restrict__ x, const int* done) {
-  if (*done) return;
-  dense_solve_block<P, TB, TO>(n, Ai, b, x);
+static void launch_smooth(int G, int n, const SellView& S, const P* coef, const P* diag, const P* il1, const P* x,
+                          const TB* b, TO* out, int accum, const int* done, cudaStream_t s) {
+  AMG_G_SWITCH(G, (k_amg_smooth<kG, P, TB, TO><<<grid_group(n, kG), kThreads, 0, s>>>(n, S, coef, diag, il1, x, b,
+                                                                                      out, accum, done)));
 }
 
 // ---- agglomeration of a distributed hierarchy (several ranks)
@@ -1162,6 +1323,7 @@ __global__ void __launch_bounds__(1024) k_amg_dense(int n, const P* __restrict__
 template <class P>
 __global__ void k_pack_vals(int V, int Vmax, const int* __restrict__ pk, const P* __restrict__ coef,
                             const P* __restrict__ diag, double* __restrict__ out) {
+  PDL_ENTRY();
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < Vmax; k += gridDim.x * blockDim.x)
     out[k] = k < V ? (pk[k] >= 0 ? (double)coef[pk[k]] : (double)diag[-1 - pk[k]]) : 0.0;
 }
@@ -1169,12 +1331,14 @@ __global__ void k_pack_vals(int V, int Vmax, const int* __restrict__ pk, const P
 template <class P>
 __global__ void k_gather_g0(int64_t n_sell, int n, const int* __restrict__ gmap, const int* __restrict__ gdmap,
                             const double* __restrict__ vals, P* __restrict__ coef, P* __restrict__ diag) {
+  PDL_ENTRY();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_sell; e += (int64_t)gridDim.x * blockDim.x)
     coef[e] = gmap[e] >= 0 ? (P)vals[gmap[e]] : P(0);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) diag[i] = (P)vals[gdmap[i]];
 }
 template <class P>
 __global__ void k_pack_rhs(int n, int nmax, const P* __restrict__ b, double* __restrict__ out, const int* done) {
+  PDL_ENTRY();
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nmax; i += gridDim.x * blockDim.x)
     out[i] = i < n ? (double)b[i] : 0.0;
@@ -1183,6 +1347,7 @@ __global__ void k_pack_rhs(int n, int nmax, const P* __restrict__ b, double* __r
 template <class P>
 __global__ void k_scatter_g0(int nranks, int nmax, const int* __restrict__ cnt, const int* __restrict__ off,
                              const double* __restrict__ all, P* __restrict__ bg, const int* done) {
+  PDL_ENTRY();
   if (*done) return;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nranks * nmax; e += gridDim.x * blockDim.x) {
     const int r = e / nmax, k = e - r * nmax;
@@ -1192,6 +1357,7 @@ __global__ void k_scatter_g0(int nranks, int nmax, const int* __restrict__ cnt, 
 // this rank's rows of the replicated G0 solution
 template <class P>
 __global__ void k_extract_g0(int n, int goff, const P* __restrict__ xg, P* __restrict__ x, const int* done) {
+  PDL_ENTRY();
   if (*done) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = xg[goff + i];
 }
@@ -1263,14 +1429,16 @@ dfvm_status amg_update(Amg<T>* A, const T* pcoef, const T* pdiag, cudaStream_t s
 }
 
 // Coarsest level l: exact dense solve, or l1-Jacobi sweeps from zero.
+// accum (dense solve only, see accum_ok): x += the solution.
 template <class P>
-static void coarsest(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl) {
+static void coarsest(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl, bool accum = false) {
   AmgLevelDev<P>& F = A->L[l];
   Prof* pr = A->prof;
   const double pb = sizeof(P), n = F.n;
   if (A->ainv) {
-    PLAUNCH(pr, "k_amg_dense", l, pb * n * n + 2 * pb * n, s,
-            (k_amg_dense<P, P, P><<<1, 1024, 0, s>>>(F.n, A->ainv, b, x, done)));
+    PLAUNCH(pr, "k_amg_dense", l, pb * n * n + (accum ? 3 : 2) * pb * n, s,
+            (k_amg_dense<P, P, P><<<grid_for((int64_t)F.n * 32), kThreads, 0, s>>>(F.n, A->ainv, b, x, accum ? 1 : 0,
+                                                                                    done)));
     ++*nl;
   } else if (F.n <= kCoarseMax) {
     PLAUNCH(pr, "k_amg_coarse", l, (4 + pb) * (double)F.nnz + 4 * pb * n, s,
@@ -1288,8 +1456,7 @@ static void coarsest(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaS
     const int sw = A->prm.sweeps + (A->prm.sweeps % 2 == 0 ? 1 : 0);
     for (int it = 1; it < sw; ++it) {
       PLAUNCH(pr, "k_amg_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
-              (k_amg_smooth<P, P, P><<<g, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, cur,
-                                                            b, nxt, done)));
+              launch_smooth<P, P, P>(F.G, F.n, F.sv(), F.coef, F.diag, F.il1, cur, b, nxt, 0, done, s));
       std::swap(cur, nxt);
     }
     *nl += sw;
@@ -1303,50 +1470,60 @@ static void coarsest(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaS
 // level's operator is symmetric (adjoint pre/post Jacobi, symmetric coarse
 // solve, two successive symmetric corrections 2B - BAB), so the
 // preconditioner stays SPD.
+// Can level l's cycle add its result into x in place (the last kernel of
+// the visit takes an accumulate flag)?  Every non-coarsest level (its
+// prolongation + post-smoother) and a dense coarsest solve can.
 template <class P>
-static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl) {
-  if (l == A->nlev - 1) { coarsest(A, l, b, x, done, s, nl); return; }
+static bool accum_ok(const AmgH<P>* A, int l) { return l < A->nlev - 1 || A->ainv != nullptr; }
+
+template <class P>
+static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaStream_t s, int* nl,
+                         bool accum = false) {
+  if (l == A->nlev - 1) { coarsest(A, l, b, x, done, s, nl, accum); return; }
   AmgLevelDev<P>& F = A->L[l];
   AmgLevelDev<P>& C = A->L[l + 1];
   Prof* pr = A->prof;
   const P w = (P)A->prm.omega;
   const double pb = sizeof(P), n = F.n, nc = C.n;
-  const int gF = grid_for(F.n), gC = grid_for(C.n);
+  const int gF = grid_for(F.n);
   const bool fused = l >= A->prm.fused_from;
   if (fused) {
     PLAUNCH(pr, "k_amg_pre_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
-            (k_amg_pre_resid<P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, b, F.t,
-                                                        F.r, done)));
+            launch_pre_resid<P>(F.G, F.n, F.sv(), F.coef, F.diag, F.il1, b, F.t, F.r, done, s));
   } else {
     PLAUNCH(pr, "k_amg_pre", l, 3 * pb * n, s, (k_amg_pre<P, P, P><<<gF, kThreads, 0, s>>>(F.n, b, F.il1, F.t, done)));
     PLAUNCH(pr, "k_amg_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 4 * pb * n, s,
-            (k_amg_resid<P, P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.t, b, F.r,
-                                                       done)));
+            launch_resid<P, P>(F.G, F.n, F.sv(), F.coef, F.diag, F.t, b, F.r, done, s));
     ++*nl;
   }
   PLAUNCH(pr, "k_amg_restrict", l, (4 + pb) * (n + nc), s,
-          (k_amg_restrict<P><<<gC, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
+          launch_restrict<P>(C.Gr, C.n, C.mem_ptr, C.mem, F.r, C.b, done, s));
   *nl += 2;
   cycle_coarse(A, l + 1, C.b, C.x, done, s, nl);
   if (A->prm.wcycle && l + 1 < A->nlev - 1 && A->depth(l + 1) <= A->prm.wmax) {
     PLAUNCH(pr, "k_amg_resid", l + 1, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
-            (k_amg_resid<P, P><<<gC, kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.x, C.b, C.r2,
-                                                       done)));
-    cycle_coarse(A, l + 1, C.r2, C.e, done, s, nl);
-    PLAUNCH(pr, "k_amg_add", l + 1, 3 * pb * nc, s, (k_amg_add<P><<<gC, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
-    *nl += 2;
+            launch_resid<P, P>(C.G, C.n, C.sv(), C.coef, C.diag, C.x, C.b, C.r2, done, s));
+    ++*nl;
+    if (accum_ok(A, l + 1)) {
+      cycle_coarse(A, l + 1, C.r2, C.x, done, s, nl, true);   // x_c += M^-1 r2 in place
+    } else {
+      cycle_coarse(A, l + 1, C.r2, C.e, done, s, nl);
+      PLAUNCH(pr, "k_amg_add", l + 1, 3 * pb * nc, s,
+              (k_amg_add<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.e, C.x, done)));
+      ++*nl;
+    }
   }
+  const double acc_b = accum ? pb * n : 0.0;
   if (fused) {
-    PLAUNCH(pr, "k_amg_prolong_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + (4 + 5 * pb) * n + pb * nc, s,
-            (k_amg_prolong_smooth<P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1,
-                                                             F.agg, C.x, w, F.t, b, x, done)));
+    PLAUNCH(pr, "k_amg_prolong_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + (4 + 5 * pb) * n + pb * nc + acc_b, s,
+            launch_prolong_smooth<P>(F.G, F.n, F.sv(), F.coef, F.diag, F.il1, F.agg, C.x, w, F.t, b, x,
+                                     accum ? 1 : 0, done, s));
   } else {
     // F.r is free after the restriction: the prolonged t = x0 + w x_c[agg] goes there
     PLAUNCH(pr, "k_amg_prolong", l, (4 + 2 * pb) * n + pb * nc, s,
             (k_amg_prolong<P><<<gF, kThreads, 0, s>>>(F.n, F.agg, C.x, F.t, F.r, w, done)));
-    PLAUNCH(pr, "k_amg_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
-            (k_amg_smooth<P, P, P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, F.r,
-                                                           b, x, done)));
+    PLAUNCH(pr, "k_amg_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n + acc_b, s,
+            launch_smooth<P, P, P>(F.G, F.n, F.sv(), F.coef, F.diag, F.il1, F.r, b, x, accum ? 1 : 0, done, s));
     ++*nl;
   }
   ++*nl;
@@ -1389,20 +1566,20 @@ static dfvm_status cycle_dist(AmgH<P>* A, int l, const P* b, P* x, const int* do
   AmgLevelDev<P>& C = A->L[l + 1];
   const P w = (P)A->prm.omega;
   const double nc = C.n;
-  const int gF = grid_for(F.n), gC = grid_for(C.n);
+  const int gF = grid_for(F.n);
   PLAUNCH(pr, "k_amg_pre", l, 3 * pb * n, s, (k_amg_pre<P, P, P><<<gF, kThreads, 0, s>>>(F.n, b, F.il1, F.t, done)));
   if ((e = halo_exchange_lists(A->m, A->halos[l], F.t, 1, f64, s))) return e;
   PLAUNCH(pr, "k_amg_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 4 * pb * n, s,
-          (k_amg_resid<P, P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.t, b, F.r, done)));
+          launch_resid<P, P>(F.G, F.n, F.sv(), F.coef, F.diag, F.t, b, F.r, done, s));
   PLAUNCH(pr, "k_amg_restrict", l, (4 + pb) * (n + nc), s,
-          (k_amg_restrict<P><<<gC, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
+          launch_restrict<P>(C.Gr, C.n, C.mem_ptr, C.mem, F.r, C.b, done, s));
   *nl += 3;
   if ((e = coarse_correction(A, l + 1, done, s, nl))) return e;
   PLAUNCH(pr, "k_amg_prolong", l, (4 + 2 * pb) * n + pb * nc, s,
           (k_amg_prolong<P><<<gF, kThreads, 0, s>>>(F.n, F.agg, C.x, F.t, F.r, w, done)));
   if ((e = halo_exchange_lists(A->m, A->halos[l], F.r, 1, f64, s))) return e;
   PLAUNCH(pr, "k_amg_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n, s,
-          (k_amg_smooth<P, P, P><<<gF, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, F.r, b, x, done)));
+          launch_smooth<P, P, P>(F.G, F.n, F.sv(), F.coef, F.diag, F.il1, F.r, b, x, 0, done, s));
   *nl += 2;
   return DFVM_OK;
 }
@@ -1423,11 +1600,16 @@ static dfvm_status coarse_correction(AmgH<P>* A, int l, const int* done, cudaStr
   if (A->prm.wcycle && l < A->nlev - 1 && A->depth(l) <= A->prm.wmax) {
     if (A->dist && (e = halo_exchange_lists(A->m, A->halos[l], C.x, 1, f64, s))) return e;
     PLAUNCH(pr, "k_amg_resid", l, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
-            (k_amg_resid<P, P><<<gC, kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.x, C.b, C.r2, done)));
-    if (A->dist) { if ((e = cycle_dist(A, l, C.r2, C.e, done, s, nl))) return e; }
-    else cycle_coarse(A, l, C.r2, C.e, done, s, nl);
-    PLAUNCH(pr, "k_amg_add", l, 3 * pb * nc, s, (k_amg_add<P><<<gC, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
-    *nl += 2;
+            launch_resid<P, P>(C.G, C.n, C.sv(), C.coef, C.diag, C.x, C.b, C.r2, done, s));
+    ++*nl;
+    if (!A->dist && accum_ok(A, l)) {
+      cycle_coarse(A, l, C.r2, C.x, done, s, nl, true);   // x_c += M^-1 r2 in place
+    } else {
+      if (A->dist) { if ((e = cycle_dist(A, l, C.r2, C.e, done, s, nl))) return e; }
+      else cycle_coarse(A, l, C.r2, C.e, done, s, nl);
+      PLAUNCH(pr, "k_amg_add", l, 3 * pb * nc, s, (k_amg_add<P><<<gC, kThreads, 0, s>>>(C.n, C.e, C.x, done)));
+      ++*nl;
+    }
   }
   return DFVM_OK;
 }
@@ -1467,7 +1649,7 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   }
   AmgLevelDev<P>& C = A->L[1];
   const double nc = C.n;
-  const int g0 = grid_for(F.n), g1 = grid_for(C.n);
+  const int g0 = grid_for(F.n);
   if (!pre_done) {
     PLAUNCH(pr, "k_amg_pre", 0, (vb + 2 * pb) * n, s,
             (k_amg_pre<P, T, P><<<g0, kThreads, 0, s>>>(F.n, r, F.il1, F.x, done)));
@@ -1476,11 +1658,10 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
   if ((e = halo_exchange_p(A->m, F.x, 1, f64, s))) return e;
   if (ev) record_event(ev[0], s);
   PLAUNCH(pr, "k_amg_resid", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + vb) * n, s,
-          (k_amg_resid<P, T><<<g0, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.x, r, F.r,
-                                                     done)));
+          launch_resid<P, T>(F.G, F.n, F.sv(), F.coef, F.diag, F.x, r, F.r, done, s));
   if (ev) record_event(ev[1], s);
   PLAUNCH(pr, "k_amg_restrict", 0, (4 + pb) * (n + nc), s,
-          (k_amg_restrict<P><<<g1, kThreads, 0, s>>>(C.n, C.mem_ptr, C.mem, F.r, C.b, done)));
+          launch_restrict<P>(C.Gr, C.n, C.mem_ptr, C.mem, F.r, C.b, done, s));
   *nl += 2;
   if ((e = coarse_correction(A, 1, done, s, nl))) return e;
   PLAUNCH(pr, "k_amg_prolong", 0, (4 + 2 * pb) * n + pb * nc, s,
@@ -1495,8 +1676,7 @@ static dfvm_status cycle0(AmgH<P>* A, const T* r, T* z, const int* done, cudaStr
     if (dot_done) *dot_done = true;
   } else {
     PLAUNCH(pr, "k_amg_smooth", 0, 4 * n + (4 + pb) * (double)F.nnz + (3 * pb + 2 * vb) * n, s,
-            (k_amg_smooth<P, T, T><<<g0, kThreads, 0, s>>>(F.n, F.sv(), F.coef, F.diag, F.il1, F.t,
-                                                           r, z, done)));
+            launch_smooth<P, T, T>(F.G, F.n, F.sv(), F.coef, F.diag, F.il1, F.t, r, z, 0, done, s));
   }
   if (ev) record_event(ev[3], s);
   *nl += 2;

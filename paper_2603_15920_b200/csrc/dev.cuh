@@ -11,6 +11,15 @@
 
 namespace dfvm {
 
+// Programmatic dependent launch: inside the captured Krylov
+// graphs the edges between consecutive kernel nodes are made programmatic
+// (solver.cu make_programmatic), so a kernel's blocks may become resident
+// while its predecessor is still running.  Every kernel therefore starts by
+// waiting for the completion and memory of the grids it depends on
+// (griddepcontrol.wait; a no-op for a kernel launched without a programmatic
+// dependency) — nothing is read or written before it.
+#define PDL_ENTRY() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 constexpr int kThreads = 256;          // 8 warps per block
 constexpr int kWarpsPerBlock = kThreads / 32;
 constexpr int kMaxBlocks = 148 * 8;    // one full wave of 256-thread blocks on 148 SMs

@@ -150,6 +150,7 @@ __device__ __forceinline__ void red_finish(const Red& red, int kind, KCtl* ctl, 
   for (int i = 0; i < NV; ++i) red.local[i] = t[i];
 }
 static __global__ void k_finalize(int kind, int nv, const double* __restrict__ all, int P, KCtl* ctl) {
+  PDL_ENTRY();
   // the reducing kernel exited early (and produced no totals) when the solve
   // was already done; init kernels always run
   if (kind == CTL_CG_SPMV || kind == CTL_CG_R || kind == CTL_CG_R2 || kind == CTL_CG_RZ0 || kind == CTL_CG_RZ) {

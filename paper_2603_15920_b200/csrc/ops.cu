@@ -21,6 +21,7 @@ namespace dfvm {
 template <class T>
 __global__ void k_import(T* __restrict__ dst, const double* __restrict__ src, const int32_t* __restrict__ map,
                          int64_t n, int nc, bool oriented) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t m = map[i];
     const bool neg = oriented && (m < 0);
@@ -34,6 +35,7 @@ __global__ void k_import(T* __restrict__ dst, const double* __restrict__ src, co
 template <class T>
 __global__ void k_export(double* __restrict__ dst, const T* __restrict__ src, const int32_t* __restrict__ map,
                          int64_t n, int nc, bool oriented) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int32_t m = map[i];
     const bool neg = oriented && (m < 0);
@@ -77,6 +79,7 @@ constexpr int kOpsF32Default = 1;
 template <class T, int NC>
 __global__ void k_interp(DevMesh<T> M, const T* __restrict__ x, const uint8_t* __restrict__ bkind,
                          const T* __restrict__ bval, T* __restrict__ xf) {
+  PDL_ENTRY();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = tid; i0 < M.F; i0 += kB * nt) {
     int2 c[kB];
@@ -122,6 +125,7 @@ template <class T, int NC, bool FACEVALS, int KB, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_grad(DevMesh<T> M, const T* __restrict__ x,
                                                    const uint8_t* __restrict__ bkind, const T* __restrict__ bval,
                                                    const T* __restrict__ fv, T* __restrict__ G) {
+  PDL_ENTRY();
   __shared__ T sh_out[kWarpsPerBlock][32 * 3 * NC];   // staged outputs of the warp's 32 rows
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -245,6 +249,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_grad(DevMesh<T> M, const T* 
 // D_c = sum_f s_cf F_f + sum_b F_b (not divided by V)
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_div(DevMesh<T> M, const T* __restrict__ flux, T* __restrict__ out) {
+  PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < M.n_slices; s += nw) {
@@ -283,6 +288,7 @@ template <class T, bool GAMMA, int KB, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_lap(DevMesh<T> M, const T* __restrict__ gamma, const T* __restrict__ x,
                                                   const T* __restrict__ G, const uint8_t* __restrict__ bkind,
                                                   const T* __restrict__ bval, T* __restrict__ y) {
+  PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   // software pipeline over the warp's slices (as in k_grad)
@@ -472,6 +478,7 @@ namespace dfvm {
 template <class T>
 __global__ void k_bc_wave(T* __restrict__ val, const T* __restrict__ base, const int8_t* __restrict__ wid, int64_t B,
                           int nc, WaveG<T> g) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
     const int w = wid[i];
     if (w >= 0)
@@ -489,6 +496,7 @@ template void launch_bc_wave<float>(float*, const float*, const int8_t*, int64_t
 // halo pack: buf[i][k] = x[idx[i]][k]  (send list of owned interface cells)
 template <class T>
 __global__ void k_pack(T* __restrict__ buf, const T* __restrict__ x, const int32_t* __restrict__ idx, int64_t n, int nc) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     for (int k = 0; k < nc; ++k) buf[i * nc + k] = x[(int64_t)idx[i] * nc + k];
 }

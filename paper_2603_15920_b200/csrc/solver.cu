@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, c
     const T* __restrict__ bv, T nu, T rdt, T theta, int conv, int kcorr, const V4<T>* __restrict__ fdO,
     const V4<T>* __restrict__ fdN, T* __restrict__ udiag, T* __restrict__ bU, T* __restrict__ rhsU,
     T* __restrict__ ucoef, T* __restrict__ ucoefT) {
+  PDL_ENTRY();
   const bool explicit_part = theta != T(1);
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, c
 template <class T, int NC>
 __global__ void __launch_bounds__(kThreads) k_apply(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ coef, const T* __restrict__ x, T* __restrict__ y) {
+  PDL_ENTRY();
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
@@ -212,6 +214,7 @@ __global__ void __launch_bounds__(kThreads) k_apply(DevMesh<T> M, const T* __res
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_HbyA(DevMesh<T> M, const T* __restrict__ bU, const T* __restrict__ udiag,
     const T* __restrict__ ucoef, const T* __restrict__ U, T* __restrict__ rAU, T* __restrict__ HbyA) {
+  PDL_ENTRY();
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
@@ -233,6 +236,7 @@ template <class T>
 __global__ void k_phiHbyA(DevMesh<T> M, const T* __restrict__ HbyA, const uint8_t* __restrict__ bk,
                           const T* __restrict__ bv, T* __restrict__ out, const T* __restrict__ Uold,
                           const T* __restrict__ phiold, const T* __restrict__ rAU, T rdt) {
+  PDL_ENTRY();
   const int64_t total = (int64_t)M.F + M.B;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < M.F) {
@@ -269,6 +273,7 @@ template <class T>
 __global__ void __launch_bounds__(kThreads) k_pcoef(DevMesh<T> M, const T* __restrict__ rAU,
     const T* __restrict__ phiHbyA, const uint8_t* __restrict__ bkp, const T* __restrict__ bvp, int ref_row,
     T p_ref, T* __restrict__ pcoef, T* __restrict__ pdiag, T* __restrict__ prhs0) {
+  PDL_ENTRY();
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
@@ -317,6 +322,7 @@ __global__ void __launch_bounds__(kThreads) k_pcoef(DevMesh<T> M, const T* __res
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_pvjp(DevMesh<T> M, const T* __restrict__ p, const T* __restrict__ lam,
     const uint8_t* __restrict__ bkp, const int32_t* __restrict__ corig, int ref_orig, T p_ref, T* __restrict__ grad) {
+  PDL_ENTRY();
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
@@ -353,6 +359,7 @@ __global__ void __launch_bounds__(kThreads) k_pvjp(DevMesh<T> M, const T* __rest
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_prhs(DevMesh<T> M, const T* __restrict__ rAU, const T* __restrict__ gp,
     const T* __restrict__ prhs0, T* __restrict__ prhs) {
+  PDL_ENTRY();
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
@@ -387,6 +394,7 @@ template <class T>
 __global__ void k_fluxcorr(DevMesh<T> M, const T* __restrict__ phiHbyA, const T* __restrict__ p,
                            const T* __restrict__ rAU, const T* __restrict__ gp, const uint8_t* __restrict__ bkp,
                            const T* __restrict__ bvp, int kcorr, T* __restrict__ phi) {
+  PDL_ENTRY();
   const int64_t total = (int64_t)M.F + M.B;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < M.F) {
@@ -422,6 +430,7 @@ template <class T>
 __global__ void __launch_bounds__(kThreads) k_Ucorr(DevMesh<T> M, const T* __restrict__ p,
     const uint8_t* __restrict__ bkp, const T* __restrict__ bvp, const T* __restrict__ HbyA,
     const T* __restrict__ rAU, T* __restrict__ U, T* __restrict__ gp) {
+  PDL_ENTRY();
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
@@ -464,6 +473,7 @@ template <class T>
 __global__ void __launch_bounds__(kThreads) k_continuity(DevMesh<T> M, const T* __restrict__ phi,
     const T* __restrict__ U, const T* __restrict__ p, double* partials, unsigned* ticket, double* out,
     WKDev* wk, int n_wk, Red red) {
+  PDL_ENTRY();
   double mx = 0, sm = 0, nf = 0;
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
@@ -508,6 +518,7 @@ __global__ void __launch_bounds__(kThreads) k_continuity(DevMesh<T> M, const T* 
 // cross-rank continuity: max / sum / non-finite over ranks, then the
 // Windkessel commit (every rank holds the same outlet states)
 __global__ void k_continuity_fin(const double* __restrict__ all, int P, double* out, WKDev* wk, int n_wk) {
+  PDL_ENTRY();
   double mx = 0, sm = 0, nf = 0;
   for (int r = 0; r < P; ++r) { mx = fmax(mx, all[3 * r]); sm += all[3 * r + 1]; nf += all[3 * r + 2]; }
   out[0] = mx; out[1] = sm; out[2] = nf > 0 ? 1.0 : 0.0;
@@ -529,6 +540,7 @@ __device__ __forceinline__ double wk_update(WKDev& W, double Q, double dt) {
 template <class T>
 __global__ void k_windkessel(DevMesh<T> M, const T* __restrict__ phi, WKDev* wk, const int* __restrict__ fptr,
                              const int* __restrict__ faces, double dt, double rho, T* __restrict__ bvp, Red red) {
+  PDL_ENTRY();
   const int o = blockIdx.x;
   double q = 0;
   for (int i = fptr[o] + threadIdx.x; i < fptr[o + 1]; i += blockDim.x) q += (double)phi[M.F + faces[i]];
@@ -550,6 +562,7 @@ template <class T>
 __global__ void k_windkessel_fin(const double* __restrict__ all, int P, int n_wk, WKDev* wk,
                                  const int* __restrict__ fptr, const int* __restrict__ faces, double dt, double rho,
                                  T* __restrict__ bvp) {
+  PDL_ENTRY();
   const int o = blockIdx.x;
   __shared__ double po_s;
   if (threadIdx.x == 0) {
@@ -562,7 +575,8 @@ __global__ void k_windkessel_fin(const double* __restrict__ all, int P, int n_wk
 }
 
 template <class T>
-__global__ void k_add_at(T* a, const T* b, int i) { a[i] += b[i]; }
+__global__ void k_add_at(T* a, const T* b, int i) {
+  PDL_ENTRY(); a[i] += b[i]; }
 
 // ============================================================ Jacobi PCG
 // r = b - A x; partials b.b, r.r, r.z  -> control start
@@ -570,6 +584,7 @@ template <class T>
 __global__ void __launch_bounds__(kThreads) k_cg_init(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ coef, const T* __restrict__ b, const T* __restrict__ x, T* __restrict__ r,
     double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+  PDL_ENTRY();
   double v[3] = {0, 0, 0};
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
@@ -598,6 +613,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_init(DevMesh<T> M, const T* __r
 template <class T>
 __global__ void k_cg_p(int n, const T* __restrict__ r, const T* __restrict__ diag, T* __restrict__ pd,
                        T* __restrict__ x, const KCtl* ctl) {
+  PDL_ENTRY();
   if (ctl->done) return;
   const T beta = (T)ctl->beta, alpha = (T)ctl->alpha;
   const bool first = ctl->it == 0;
@@ -615,6 +631,7 @@ template <class T>
 __global__ void __launch_bounds__(kThreads) k_cg_spmv(DevMesh<T> M, const T* __restrict__ diag,
     const T* __restrict__ coef, const T* __restrict__ pd, T* __restrict__ q, double* partials, unsigned* ticket,
     KCtl* ctl, Red red) {
+  PDL_ENTRY();
   if (ctl->done) return;
   double v[1] = {0};
   SLICE_LOOP(M) {
@@ -632,6 +649,7 @@ __global__ void __launch_bounds__(kThreads) k_cg_spmv(DevMesh<T> M, const T* __r
 template <class T>
 __global__ void k_cg_r(int n, const T* __restrict__ q, const T* __restrict__ diag, T* __restrict__ r,
                        double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+  PDL_ENTRY();
   if (ctl->done) return;
   const T alpha = (T)ctl->alpha;
   double v[2] = {0, 0};
@@ -648,6 +666,7 @@ __global__ void k_cg_r(int n, const T* __restrict__ q, const T* __restrict__ dia
 // ---- AMG-preconditioned variant: z = M^-1 r comes from amg_apply
 template <class T>
 __global__ void k_cg_p2(int n, const T* __restrict__ z, T* __restrict__ pd, T* __restrict__ x, const KCtl* ctl) {
+  PDL_ENTRY();
   if (ctl->done) return;
   const T beta = (T)ctl->beta, alpha = (T)ctl->alpha;
   const bool first = ctl->it == 0;
@@ -661,6 +680,7 @@ __global__ void k_cg_p2(int n, const T* __restrict__ z, T* __restrict__ pd, T* _
 template <class T>
 __global__ void k_cg_r2(int n, const T* __restrict__ q, T* __restrict__ r, double* partials, unsigned* ticket,
                         KCtl* ctl, Red red) {
+  PDL_ENTRY();
   if (ctl->done) return;
   const T alpha = (T)ctl->alpha;
   double v[1] = {0};
@@ -678,6 +698,7 @@ __global__ void k_cg_r2(int n, const T* __restrict__ q, T* __restrict__ r, doubl
 template <class T, class P>
 __global__ void k_cg_r2x(int n, const T* __restrict__ q, T* __restrict__ r, const P* __restrict__ il1,
                          P* __restrict__ x0, double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+  PDL_ENTRY();
   if (ctl->done) return;
   const T alpha = (T)ctl->alpha;
   double v[1] = {0};
@@ -693,6 +714,7 @@ __global__ void k_cg_r2x(int n, const T* __restrict__ q, T* __restrict__ r, cons
 template <class T>
 __global__ void k_cg_dot(int n, const T* __restrict__ a, const T* __restrict__ b, double* partials, unsigned* ticket,
                          KCtl* ctl, Red red, int kind) {
+  PDL_ENTRY();
   if (ctl->done) return;
   double v[1] = {0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -704,6 +726,7 @@ __global__ void k_cg_dot(int n, const T* __restrict__ a, const T* __restrict__ b
 // the deferred x update of the final iteration
 template <class T>
 __global__ void k_cg_final(int n, const T* __restrict__ pd, T* __restrict__ x, const KCtl* ctl) {
+  PDL_ENTRY();
   if (!ctl->half) return;
   const T alpha = (T)ctl->alpha;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] += alpha * pd[i];
@@ -717,10 +740,30 @@ __global__ void k_cg_final(int n, const T* __restrict__ pd, T* __restrict__ x, c
 // k >= NC: those components start with b = 0 and are done from the start).
 __device__ __forceinline__ bool all_done(const KCtl* c) { return c[0].done && c[1].done && c[2].done; }
 
+// Gather of an NC-vector: NC scalar loads (measured on C5: dev.cuh's
+// two-load ld3 made k_bi_t slower here, 0.53 against 0.64 of the roofline)
+template <class T, int NC>
+__device__ __forceinline__ void ldv(const T* __restrict__ p, int64_t i, T (&o)[3]) {
+#pragma unroll
+  for (int k = 0; k < NC; ++k) o[k] = p[NC * i + k];
+}
+
+// The BiCGStab vectors are kept SCALED by the Jacobi preconditioner
+// D^-1 = 1 / diag (round 2): r~ = D^-1 r, v~ = D^-1 v and y = D^-1 p
+// replace r, v, p, so the two matrix applies gather one (v: y) or two
+// (t: r~, v~) NC-vectors per neighbour and no 1/diag:
+//   p update    y = r~ + beta (y - omega v~)             (= D^-1 (r + beta (p - omega v)))
+//   v = A y,    v~ = D^-1 v,  alpha = rho / (rh, v)
+//   z = r~ - alpha v~ (= D^-1 s, formed on the fly), t = A z, s = D z
+//   x += alpha y + omega z,   r = s - omega t,  r~ = D^-1 r
+// The dot products use the unscaled r, v, s, t (the scalars of the
+// textbook recurrence); the shadow residual rh stays unscaled.
 template <class T, int NC>
 __global__ void __launch_bounds__(kThreads) k_bi_init(DevMesh<T> M, const T* __restrict__ diag,
-    const T* __restrict__ coef, const T* __restrict__ b, const T* __restrict__ x, T* __restrict__ r,
-    T* __restrict__ rh, T* __restrict__ p, T* __restrict__ v, double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+    const T* __restrict__ dinv, const T* __restrict__ coef, const T* __restrict__ b, const T* __restrict__ x,
+    T* __restrict__ rs, T* __restrict__ rh, T* __restrict__ y, T* __restrict__ vs, double* partials, unsigned* ticket,
+    KCtl* ctl, Red red) {
+  PDL_ENTRY();
   double a[6] = {0, 0, 0, 0, 0, 0};
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
@@ -730,15 +773,17 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(DevMesh<T> M, const T* __r
 #pragma unroll
     for (int k = 0; k < NC; ++k) acc[k] = live ? d * x[NC * (int64_t)row + k] : T(0);
     sell_apply<T, NC>(M, s, lane, coef, x, acc);
-    if (live)
+    if (live) {
+      const T di = dinv[row];
 #pragma unroll
       for (int k = 0; k < NC; ++k) {
         const int64_t i = NC * (int64_t)row + k;
         const T rr = b[i] - acc[k];
-        r[i] = rr; rh[i] = rr; p[i] = T(0); v[i] = T(0);
+        rs[i] = rr * di; rh[i] = rr; y[i] = T(0); vs[i] = T(0);
         a[k] += (double)b[i] * (double)b[i];
         a[3 + k] += (double)rr * (double)rr;
       }
+    }
   }
   double t[6];
   if (grid_sum<6>(a, partials, ticket, t)) red_finish<6>(red, CTL_BI_INIT, ctl, t);
@@ -747,17 +792,18 @@ __global__ void __launch_bounds__(kThreads) k_bi_init(DevMesh<T> M, const T* __r
 // 1 / diag for own + ghost rows (the Jacobi preconditioner applied as a product)
 template <class T>
 __global__ void k_recip(int n, const T* __restrict__ d, T* __restrict__ di) {
+  PDL_ENTRY();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) di[i] = T(1) / d[i];
 }
 
-// Per iteration (4 kernels): p update | v = A M^-1 p, rh.v -> alpha |
-// s = r - alpha v formed on the fly, t = A M^-1 s, t.s, t.t, s.s -> half-step
-// check, omega | x, r update, rh.r, r.r -> rho, check.  Neither y = M^-1 p nor
-// s is stored: the kernels that need them form them from p (r, v) and dinv.
+// Per iteration (4 kernels): y update | v = A y, v~, rh.v -> alpha |
+// z = r~ - alpha v~ on the fly, t = A z, t.s, t.t, s.s -> half-step check,
+// omega | x, r~ update, rh.r, r.r -> rho, check.
 
-// p = r + beta (p - omega v)
+// y = r~ + beta (y - omega v~)
 template <class T, int NC>
-__global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ p, const KCtl* ctl) {
+__global__ void k_bi_p(int n, const T* __restrict__ rs, const T* __restrict__ vs, T* __restrict__ y, const KCtl* ctl) {
+  PDL_ENTRY();
   if (all_done(ctl)) return;
   T beta[3], om[3];
   bool act[3];
@@ -772,69 +818,65 @@ __global__ void k_bi_p(int n, const T* __restrict__ r, const T* __restrict__ v, 
     for (int k = 0; k < NC; ++k) {
       if (!act[k]) continue;
       const int64_t j = NC * (int64_t)i + k;
-      p[j] = r[j] + beta[k] * (p[j] - om[k] * v[j]);
+      y[j] = rs[j] + beta[k] * (y[j] - om[k] * vs[j]);
     }
   }
 }
 
-// v = A (p / diag); partial (rh, v) -> alpha   (dinv = 1 / diag)
+// v = A y; v~ = v / diag; partial (rh, v) -> alpha
 template <class T, int NC, int KBV, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_bi_v(DevMesh<T> M, const T* __restrict__ diag,
-    const T* __restrict__ dinv, const T* __restrict__ coef, const T* __restrict__ p, const T* __restrict__ rh,
-    T* __restrict__ v, double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+    const T* __restrict__ dinv, const T* __restrict__ coef, const T* __restrict__ y, const T* __restrict__ rh,
+    T* __restrict__ vs, double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+  PDL_ENTRY();
   if (all_done(ctl)) return;
   double a[3] = {0, 0, 0};
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
     T acc[3];
-    const T d = live ? diag[row] : T(0), di = live ? dinv[row] : T(0);
+    const T d = live ? diag[row] : T(0);
 #pragma unroll
-    for (int k = 0; k < NC; ++k) acc[k] = live ? d * (p[NC * (int64_t)row + k] * di) : T(0);
+    for (int k = 0; k < NC; ++k) acc[k] = live ? d * y[NC * (int64_t)row + k] : T(0);
     const int len = __ldg(&M.ms_len[s]);
     const int base = __ldg(&M.ms_ptr[s]) + lane;
-    int j = 0;
-    for (; j + KBV <= len; j += KBV) {
-      T c[KBV], dn[KBV], pn[KBV][3];
+    for (int j = 0; j < len; j += KBV) {
+      T c[KBV], yn[KBV][3];
       int nn[KBV];
 #pragma unroll
-      for (int u = 0; u < KBV; ++u) { c[u] = __ldg(&coef[base + 32 * (j + u)]); nn[u] = __ldg(&M.mnb[base + 32 * (j + u)]); }
-#pragma unroll
       for (int u = 0; u < KBV; ++u) {
-        dn[u] = dinv[nn[u]];
-#pragma unroll
-        for (int k = 0; k < NC; ++k) pn[u][k] = p[NC * (int64_t)nn[u] + k];
+        const bool ok = j + u < len;
+        c[u] = ok ? __ldg(&coef[base + 32 * (j + u)]) : T(0);
+        nn[u] = ok ? __ldg(&M.mnb[base + 32 * (j + u)]) : 0;   // past the row's end: 0 * y_0
       }
+#pragma unroll
+      for (int u = 0; u < KBV; ++u) ldv<T, NC>(y, nn[u], yn[u]);
 #pragma unroll
       for (int u = 0; u < KBV; ++u)
 #pragma unroll
-        for (int k = 0; k < NC; ++k) acc[k] += c[u] * (pn[u][k] * dn[u]);
+        for (int k = 0; k < NC; ++k) acc[k] += c[u] * yn[u][k];
     }
-    for (; j < len; ++j) {
-      const T c = __ldg(&coef[base + 32 * j]);
-      const int nn = __ldg(&M.mnb[base + 32 * j]);
-      const T dn = dinv[nn];
-#pragma unroll
-      for (int k = 0; k < NC; ++k) acc[k] += c * (p[NC * (int64_t)nn + k] * dn);
-    }
-    if (live)
+    if (live) {
+      const T di = dinv[row];
 #pragma unroll
       for (int k = 0; k < NC; ++k) {
         const int64_t i = NC * (int64_t)row + k;
-        v[i] = acc[k];
+        vs[i] = acc[k] * di;
         a[k] += (double)rh[i] * (double)acc[k];
       }
+    }
   }
   double t[3];
   if (grid_sum<3>(a, partials, ticket, t)) red_finish<3>(red, CTL_BI_V, ctl, t);
 }
 
-// s = r - alpha v (own row and, on the fly, every neighbour); t = A (s / diag);
-// partials (t, s), (t, t), (s, s) -> half-step check, omega
+// z = r~ - alpha v~ (own row and, on the fly, every neighbour); t = A z;
+// s = diag z; partials (t, s), (t, t), (s, s) -> half-step check, omega
 template <class T, int NC, int KBT, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_bi_t(DevMesh<T> M, const T* __restrict__ dinv,
-    const T* __restrict__ coef, const T* __restrict__ r, const T* __restrict__ v, T* __restrict__ tv,
+__global__ void __launch_bounds__(kThreads, MINB) k_bi_t(DevMesh<T> M, const T* __restrict__ diag,
+    const T* __restrict__ coef, const T* __restrict__ rs, const T* __restrict__ vs, T* __restrict__ tv,
     double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+  PDL_ENTRY();
   if (all_done(ctl)) return;
   T al[3];
 #pragma unroll
@@ -844,38 +886,32 @@ __global__ void __launch_bounds__(kThreads, MINB) k_bi_t(DevMesh<T> M, const T* 
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
     T acc[3] = {T(0), T(0), T(0)}, sr[3] = {T(0), T(0), T(0)};
-    if (live)
+    if (live) {
+      const T d = diag[row];
 #pragma unroll
       for (int k = 0; k < NC; ++k) {
         const int64_t i = NC * (int64_t)row + k;
-        sr[k] = r[i] - al[k] * v[i];
-        acc[k] = sr[k];                    // diag * (s / diag)
+        sr[k] = d * (rs[i] - al[k] * vs[i]);
+        acc[k] = sr[k];                    // diag * z
       }
+    }
     const int len = __ldg(&M.ms_len[s]);
     const int base = __ldg(&M.ms_ptr[s]) + lane;
-    int j = 0;
-    for (; j + KBT <= len; j += KBT) {
-      T c[KBT], dn[KBT], rn[KBT][3], vn[KBT][3];
+    for (int j = 0; j < len; j += KBT) {
+      T c[KBT], rn[KBT][3], vn[KBT][3];
       int nn[KBT];
 #pragma unroll
-      for (int u = 0; u < KBT; ++u) { c[u] = __ldg(&coef[base + 32 * (j + u)]); nn[u] = __ldg(&M.mnb[base + 32 * (j + u)]); }
-#pragma unroll
       for (int u = 0; u < KBT; ++u) {
-        dn[u] = dinv[nn[u]];
-#pragma unroll
-        for (int k = 0; k < NC; ++k) { rn[u][k] = r[NC * (int64_t)nn[u] + k]; vn[u][k] = v[NC * (int64_t)nn[u] + k]; }
+        const bool ok = j + u < len;
+        c[u] = ok ? __ldg(&coef[base + 32 * (j + u)]) : T(0);
+        nn[u] = ok ? __ldg(&M.mnb[base + 32 * (j + u)]) : 0;   // past the row's end: 0 * z_0
       }
+#pragma unroll
+      for (int u = 0; u < KBT; ++u) { ldv<T, NC>(rs, nn[u], rn[u]); ldv<T, NC>(vs, nn[u], vn[u]); }
 #pragma unroll
       for (int u = 0; u < KBT; ++u)
 #pragma unroll
-        for (int k = 0; k < NC; ++k) acc[k] += c[u] * ((rn[u][k] - al[k] * vn[u][k]) * dn[u]);
-    }
-    for (; j < len; ++j) {
-      const T c = __ldg(&coef[base + 32 * j]);
-      const int nn = __ldg(&M.mnb[base + 32 * j]);
-      const T dn = dinv[nn];
-#pragma unroll
-      for (int k = 0; k < NC; ++k) acc[k] += c * ((r[NC * (int64_t)nn + k] - al[k] * v[NC * (int64_t)nn + k]) * dn);
+        for (int k = 0; k < NC; ++k) acc[k] += c[u] * (rn[u][k] - al[k] * vn[u][k]);
     }
     if (live)
 #pragma unroll
@@ -890,12 +926,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_bi_t(DevMesh<T> M, const T* 
   if (grid_sum<9>(a, partials, ticket, t)) red_finish<9>(red, CTL_BI_T, ctl, t);
 }
 
-// s = r - alpha v; x += alpha p/diag + omega s/diag; r = s - omega t;
-// partials (rh, r), (r, r)   (dinv = 1 / diag)
+// z = r~ - alpha v~; x += alpha y + omega z; r = diag z - omega t, r~ = r / diag;
+// partials (rh, r), (r, r)
 template <class T, int NC>
-__global__ void k_bi_x(int n, const T* __restrict__ dinv, const T* __restrict__ p, const T* __restrict__ v,
-                       const T* __restrict__ tv, const T* __restrict__ rh, T* __restrict__ x, T* __restrict__ r,
-                       double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+__global__ void k_bi_x(int n, const T* __restrict__ diag, const T* __restrict__ dinv, const T* __restrict__ y,
+                       const T* __restrict__ vs, const T* __restrict__ tv, const T* __restrict__ rh, T* __restrict__ x,
+                       T* __restrict__ rs, double* partials, unsigned* ticket, KCtl* ctl, Red red) {
+  PDL_ENTRY();
   if (all_done(ctl)) return;
   T al[3], om[3];
   int mode[3];   // 0 skip, 1 half step, 2 full step
@@ -906,16 +943,16 @@ __global__ void k_bi_x(int n, const T* __restrict__ dinv, const T* __restrict__ 
   }
   double a[6] = {0, 0, 0, 0, 0, 0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const T d = dinv[i];
+    const T d = diag[i], di = dinv[i];
 #pragma unroll
     for (int k = 0; k < NC; ++k) {
       const int64_t j = NC * (int64_t)i + k;
-      if (mode[k] == 1) { x[j] += al[k] * (p[j] * d); continue; }
+      if (mode[k] == 1) { x[j] += al[k] * y[j]; continue; }
       if (mode[k] != 2) continue;
-      const T ss = r[j] - al[k] * v[j];
-      x[j] += al[k] * (p[j] * d) + om[k] * (ss * d);
-      const T rr = ss - om[k] * tv[j];
-      r[j] = rr;
+      const T z = rs[j] - al[k] * vs[j];
+      x[j] += al[k] * y[j] + om[k] * z;
+      const T rr = d * z - om[k] * tv[j];
+      rs[j] = rr * di;
       a[k] += (double)rh[j] * (double)rr;
       a[3 + k] += (double)rr * (double)rr;
     }
@@ -1155,6 +1192,7 @@ static dfvm_status fin(dfvm_solver* S, SolverT<T>& X, int kind, int nv, cudaStre
 enum LoopKind { LOOP_CG = 0, LOOP_CG_AMG = 1, LOOP_BICGSTAB = 2, LOOP_BICGSTAB1 = 3 };
 
 __global__ void k_loop_cond(cudaGraphConditionalHandle h, const KCtl* ctl, int nc) {
+  PDL_ENTRY();
   int go = 0;
   for (int k = 0; k < nc; ++k) go |= !ctl[k].done;
   cudaGraphSetConditional(h, go ? 1u : 0u);
@@ -1162,6 +1200,7 @@ __global__ void k_loop_cond(cudaGraphConditionalHandle h, const KCtl* ctl, int n
 
 template <class T>
 __global__ void k_zero_if(int n, int nc, T* __restrict__ x, const KCtl* ctl) {
+  PDL_ENTRY();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     for (int k = 0; k < nc; ++k)
       if (ctl[k].zero_x) x[(int64_t)nc * i + k] = T(0);
@@ -1173,6 +1212,43 @@ static bool use_device_loops(dfvm_solver* S, SolverT<T>& X, cudaStream_t st) {
   const char* g = getenv("DFVM_GRAPHS");
   if (g && g[0] == '0') { X.loops_off = true; return false; }
   return S->m->part.P == 1 && st != nullptr && !S->pr() && !S->timing;
+}
+
+// Programmatic dependent launch inside a captured graph: every edge between
+// two kernel nodes becomes a programmatic one, so the downstream kernel's
+// blocks are scheduled as soon as the upstream kernel's blocks have all begun
+// (DFVM_PDL=2, default; the launch-completion port) or have all finished
+// (DFVM_PDL=1, the programmatic port: only the launch itself overlaps),
+// instead of after the upstream grid has drained and flushed.  Correctness
+// rests on PDL_ENTRY (dev.cuh): every kernel waits for its dependencies'
+// completion and memory before it touches anything.  DFVM_PDL=0: ordinary
+// edges.  Returns the number of edges converted.
+static int make_programmatic(cudaGraph_t g) {
+  const int mode = [] { const char* e = getenv("DFVM_PDL"); return e ? atoi(e) : 2; }();
+  if (mode <= 0) return 0;
+  size_t ne = 0;
+  if (cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne) != cudaSuccess || ne == 0) return 0;
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  std::vector<cudaGraphEdgeData> ed(ne);
+  if (cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne) != cudaSuccess) return 0;
+  int n = 0;
+  for (size_t k = 0; k < ne; ++k) {
+    cudaGraphNodeType ta, tb;
+    if (cudaGraphNodeGetType(from[k], &ta) != cudaSuccess || cudaGraphNodeGetType(to[k], &tb) != cudaSuccess) continue;
+    if (ta != cudaGraphNodeTypeKernel || tb != cudaGraphNodeTypeKernel) continue;
+    if (ed[k].type != cudaGraphDependencyTypeDefault || ed[k].from_port != 0) continue;
+    cudaGraphEdgeData pe = {};
+    pe.type = cudaGraphDependencyTypeProgrammatic;
+    pe.from_port = mode == 1 ? cudaGraphKernelNodePortProgrammatic : cudaGraphKernelNodePortLaunchCompletion;
+    if (cudaGraphRemoveDependencies_v2(g, &from[k], &to[k], &ed[k], 1) != cudaSuccess) continue;
+    if (cudaGraphAddDependencies_v2(g, &from[k], &to[k], &pe, 1) != cudaSuccess) {
+      cudaGraphAddDependencies_v2(g, &from[k], &to[k], &ed[k], 1);   // keep the ordinary edge
+      continue;
+    }
+    ++n;
+  }
+  cudaGetLastError();
+  return n;
 }
 
 template <class T, class Pro, class Body, class Epi>
@@ -1217,7 +1293,11 @@ static dfvm_status device_loop(dfvm_solver* S, SolverT<T>& X, int kind, const vo
         if (err == cudaSuccess) err = e2;
       }
     }
-    if (err == cudaSuccess && !ce) err = cudaGraphInstantiate(&ex, g, 0);
+    if (err == cudaSuccess && !ce) {
+      make_programmatic(g);
+      make_programmatic(bg);
+      err = cudaGraphInstantiate(&ex, g, 0);
+    }
     if (g) cudaGraphDestroy(g);
     if (ce) return ce;
     if (err != cudaSuccess) return cuda_error(err, "device-resident Krylov graph");
@@ -1531,9 +1611,9 @@ static dfvm_status run_cg_amg(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, d
 // 3-component BiCGStab on (udiag, ucoef): x = U (warm start), b = rhsU.
 // Right-preconditioned (Jacobi) van der Vorst BiCGStab, the three velocity
 // components advanced together over one coefficient stream; each component
-// keeps its own scalars and stops independently.  Ghosts: x and udiag are
-// exchanged by the caller (assemble); p, r and v are exchanged before the
-// applies that gather them.
+// keeps its own scalars and stops independently; vectors kept scaled by
+// 1 / diag (see k_bi_init).  Ghosts: x and udiag are exchanged by the caller
+// (assemble); y, r~ and v~ are exchanged before the applies that gather them.
 template <class T, int NC>
 static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x, double tol, double rel_tol,
                                 int maxit, dfvm_solve_report* rep, cudaStream_t st) {
@@ -1543,7 +1623,10 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   // k_bi_t: batch 4 at >= 3 blocks/SM (batch 2 at 4 blocks/SM measured equal on C5)
   // batch depth / min blocks per SM: measured on C5 against batch 2 and 1
   // with two-load 3-vector gathers (profiles/r01_bicgstab_variants_c5.txt)
-  const int gs = grid_slices(k_bi_v<T, NC, 4, 6>, M.n_slices), gt = grid_slices(k_bi_t<T, NC, 4, 3>, M.n_slices);
+  const int gs = grid_slices(k_bi_v<T, NC, 4, 6>, M.n_slices);
+  // DFVM_BI_T=2: k_bi_t in batches of 2 entries at >= 4 blocks/SM (A/B knob)
+  const int bi_t_var = [] { const char* e = getenv("DFVM_BI_T"); return e ? atoi(e) : 4; }();
+  const int gt = bi_t_var == 2 ? grid_slices(k_bi_t<T, NC, 2, 4>, M.n_slices) : grid_slices(k_bi_t<T, NC, 4, 3>, M.n_slices);
   // (measured on C5: flat [3n] p/x updates and shared-staged own rows in v/t
   // were 26 ms/step slower than these one-thread-per-row kernels)
   const int ge = grid_for(M.n_own);
@@ -1555,8 +1638,8 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
   auto pro = [&](int* nl) -> dfvm_status {
     PLAUNCH(pr, "k_recip", -1, 2 * v * M.n_cells, st,
             (k_recip<T><<<grid_for(M.n_cells), kThreads, 0, st>>>(M.n_cells, X.udiag, X.udinv)));
-    PLAUNCH(pr, "k_bi_init", -1, 4 * N + Z * (4 + v) + (1 + 6 * NC) * v * N, st,
-            (k_bi_init<T, NC><<<grid_slices(k_bi_init<T, NC>, M.n_slices), kThreads, 0, st>>>(M, X.udiag, X.ucoef, b, x, X.kr,
+    PLAUNCH(pr, "k_bi_init", -1, 4 * N + Z * (4 + v) + (2 + 6 * NC) * v * N, st,
+            (k_bi_init<T, NC><<<grid_slices(k_bi_init<T, NC>, M.n_slices), kThreads, 0, st>>>(M, X.udiag, X.udinv, X.ucoef, b, x, X.kr,
                                                                                      X.krh, X.kp, X.kv, X.partials,
                                                                                      X.ticket, X.d_ctl, red)));
     *nl += 2;
@@ -1572,11 +1655,16 @@ static dfvm_status run_bicgstab(dfvm_solver* S, SolverT<T>& X, const T* b, T* x,
     if ((e = fin(S, X, CTL_BI_V, 3, st))) return e;
     if ((e = halo_exchange(m, X.kr, NC, st)) || (e = halo_exchange(m, X.kv, NC, st))) return e;
     PLAUNCH(pr, "k_bi_t", -1, 4 * N + Z * (4 + v) + (1 + 3 * NC) * v * N, st,
-            (k_bi_t<T, NC, 4, 3><<<gt, kThreads, 0, st>>>(M, X.udinv, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket,
-                                                      X.d_ctl, red)));
+            if (bi_t_var == 2) {
+              k_bi_t<T, NC, 2, 4><<<gt, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket,
+                                                            X.d_ctl, red);
+            } else {
+              k_bi_t<T, NC, 4, 3><<<gt, kThreads, 0, st>>>(M, X.udiag, X.ucoef, X.kr, X.kv, X.kt, X.partials, X.ticket,
+                                                            X.d_ctl, red);
+            });
     if ((e = fin(S, X, CTL_BI_T, 9, st))) return e;
-    PLAUNCH(pr, "k_bi_x", -1, (1 + 8 * NC) * v * N, st,
-            (k_bi_x<T, NC><<<ge, kThreads, 0, st>>>(M.n_own, X.udinv, X.kp, X.kv, X.kt, X.krh, x, X.kr, X.partials,
+    PLAUNCH(pr, "k_bi_x", -1, (2 + 8 * NC) * v * N, st,
+            (k_bi_x<T, NC><<<ge, kThreads, 0, st>>>(M.n_own, X.udiag, X.udinv, X.kp, X.kv, X.kt, X.krh, x, X.kr, X.partials,
                                                 X.ticket, X.d_ctl, red)));
     if ((e = fin(S, X, CTL_BI_X, 6, st))) return e;
     *nl += 4;
@@ -1613,7 +1701,7 @@ static dfvm_status assemble(dfvm_solver* S, SolverT<T>& X, const T* U, const T* 
                                                                (T)theta_of(S->o), S->o.convection, S->kcorr, X.fdO,
                                                                X.fdN, X.udiag, X.bU, X.rhsU, X.ucoef, X.ucoefT)));
   S->n_launch++;
-  if ((s2 = halo_exchange(S->m, X.udiag, 1, st))) return s2;   // k_bi_t gathers s / diag
+  if ((s2 = halo_exchange(S->m, X.udiag, 1, st))) return s2;   // ghost diag: rAU of the neighbours (k_HbyA ...)
   X.assembled = true;
   DFVM_CUDA(cudaGetLastError());
   return DFVM_OK;

@@ -447,3 +447,60 @@ def test_amg_kernel_variants_bitwise(precond, size, monkeypatch):
         assert o[3] == out[0][3]
         for a, b in zip(out[0][:3], o[:3]):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("perm", ["1", "2"])
+def test_amg_sigma_storage_same_hierarchy(perm, monkeypatch):
+    # SELL-32-sigma storage of the coarse levels (DFVM_AMG_PERM=1: slot -> row
+    # indirection; 2: rows renumbered by slot on the device) keeps the host
+    # aggregation, hence the hierarchy and each row's sum order: same level
+    # sizes, same iteration counts, fields equal to the natural order up to
+    # the round-off of the fp32 coarsest dense inverse (taken in slot order),
+    # every pressure solve converged to TIGHT tolerances (no relative stop)
+    import ctypes
+    import torch
+    import cases
+    case = cases.c5(n_z=6)
+    mg = dfvm.Mesh(case.raw)
+    geo = mg.export_geometry()
+    U0, p0, phi0 = case.initial_state(geo["xc"], geo["xf"], geo["Sf"])
+    bg = case.apply_bcs(dfvm.BCs(mg))
+    s = torch.cuda.Stream()
+    sp = ctypes.c_void_p(s.cuda_stream)
+    out = []
+    for v in ("0", perm):
+        monkeypatch.setenv("DFVM_AMG_PERM", v)
+        Sg = dfvm.Solver(mg, bg, **dict(case.solver, p_precond="amg32", p_rel_tol=0.0, **TIGHT))
+        Ug, pg, phig = mg.field("cells", 3, U0, sp), mg.field("cells", 1, p0, sp), mg.field("flux", 1, phi0, sp)
+        reps = [Sg.step(Ug, pg, phig, sp) for _ in range(2)]
+        out.append((Ug.get(sp), pg.get(sp), phig.get(sp), [r["it"] for rep in reps for r in rep["p"]],
+                    Sg.amg_levels()))
+    assert out[0][4] == out[1][4] and len(out[0][4]) >= 3
+    assert sum(abs(a - b) for a, b in zip(out[0][3], out[1][3])) <= 2
+    for a, b in zip(out[0][:3], out[1][:3]):
+        assert rel_l2(b, a) <= 1e-10
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_programmatic_launch_bitwise(mode, monkeypatch):
+    # programmatic dependent launch inside the device-resident Krylov graphs
+    # (DFVM_PDL; every kernel waits for its dependencies first): the fields
+    # and iteration counts are bitwise those of ordinary graph edges
+    import ctypes
+    import torch
+    raw, mo, mg, bo, bg, kw = pipe_case(n=8, m_r=4, n_z=40)
+    U0, p0, phi0 = initial_state(mo)
+    s = torch.cuda.Stream()
+    sp = ctypes.c_void_p(s.cuda_stream)
+    out = []
+    for v in ("0", mode):
+        monkeypatch.setenv("DFVM_PDL", v)
+        for pc in ("amg32", "jacobi"):
+            Sg = dfvm.Solver(mg, bg, p_precond=pc, **kw, **TIGHT)
+            Ug, pg, phig = mg.field("cells", 3, U0, sp), mg.field("cells", 1, p0, sp), mg.field("flux", 1, phi0, sp)
+            reps = [Sg.step(Ug, pg, phig, sp) for _ in range(3)]
+            out.append((Ug.get(sp), pg.get(sp), phig.get(sp), [r["it"] for rep in reps for r in rep["p"]]))
+    for a, b in zip(out[:2], out[2:]):
+        assert a[3] == b[3]
+        for x, y in zip(a[:3], b[:3]):
+            assert np.array_equal(x, y)
