@@ -57,6 +57,7 @@ bool comm_is_local(const dfvm_comm* c);
 constexpr int kCoarseMax = 2048;     // shared-memory capacity of the one-block coarse solve
 constexpr int kDirectMax = 512;      // largest coarsest level solved with a dense inverse
 constexpr int kMaxLevels = 16;
+constexpr int kCsrChunk = 128;       // entries per warp chunk of the CSR-stream coarse kernels (4 per lane)
 
 // Tunables (defaults chosen from B200 measurements on the C5 pipe, DESIGN.md
 // §6); overridable through the environment for experiments:
@@ -109,6 +110,12 @@ struct AmgParams {
   int fused_from = 3;   // coarse levels >= this use the fused pre_resid / prolong_smooth kernels
   int agglom = 100000;  // several ranks: agglomerate the first coarse level with <= this many rows in total
   int renum = 0;        // 1: aggregates renumbered by their first member (locality order)
+  // 1: coarse levels with one thread per row use the CSR-stream kernels.
+  // Default 0 (SELL): measured on C5 round 2 at 334.4 / 336.6 ms/step with
+  // CSR-stream against 330.0 / 330.9 (profiles/r02_sweep_r2i_csr.jsonl) —
+  // the chunk's serial per-row sums over shared memory and the idle lanes
+  // of short chunks cost more than the coalesced, padding-free loads saved
+  int csr = 0;
   bool wcycle = true;
   double omega = 1.95;  // C5 amg32 (round 2): 344.0 ms, 11.33 it/solve (1.9: 349.6 ms, 11.58; 1.8: 360.2 ms, 12.17)
   AmgParams() {
@@ -122,6 +129,7 @@ struct AmgParams {
     if (const char* e = getenv("DFVM_AMG_FUSED_FROM")) fused_from = std::max(1, atoi(e));
     if (const char* e = getenv("DFVM_AMG_AGGLOM")) agglom = std::max(32, atoi(e));
     if (const char* e = getenv("DFVM_AMG_RENUM")) renum = atoi(e);
+    if (const char* e = getenv("DFVM_AMG_CSR")) csr = atoi(e);
   }
 };
 
@@ -268,6 +276,14 @@ struct AmgLevelDev {
   P *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr;
   P *e = nullptr, *r2 = nullptr;                  // W-cycle: second-visit solution / rhs
   int n_cells = 0;                                // owned + ghost rows (several ranks)
+  // CSR-stream copy of the matrix (serial coarse levels with one thread per
+  // row): warp chunks of whole rows with <= kCsrChunk entries (c_ptr: first
+  // row per chunk), the real entries of each row in SELL order (c_rp, c_col),
+  // their SELL positions (c_pos: c_coef is gathered from coef per update)
+  int n_chunk = 0;
+  int64_t nnz_csr = 0;
+  int *c_ptr = nullptr, *c_rp = nullptr, *c_col = nullptr, *c_pos = nullptr;
+  P* c_coef = nullptr;
   int G = 1;                                      // lanes per row of this level's matrix kernels
   int Gr = 1;                                     // lanes per row of the restriction INTO this level
 };
@@ -419,13 +435,13 @@ static dfvm_status coarsen_serial(AmgH<P>* A, std::vector<HostLevel>& H, int& le
     }
     C.mnb.assign(C.ms_ptr[S], 0);
     std::vector<int> gal_ptr(C.ms_ptr[S] + 1, 0), gal_idx;
-    std::vector<int> slot_entry(C.ms_ptr[S], -1);
+    std::vector<int> slot_entry(C.ms_ptr[S], -1), epos(ccol.size(), -1);
     for (int I = 0; I < nc; ++I) {
       const int q = C.slot(I), s = q / 32, lane = q % 32;
       for (int j = 0; j < C.ms_len[s]; ++j) {
         const int p = C.ms_ptr[s] + 32 * j + lane;
         const int e = crow_ptr[I] + j;
-        if (e < crow_ptr[I + 1]) { C.mnb[p] = ccol[e]; slot_entry[p] = e; }
+        if (e < crow_ptr[I + 1]) { C.mnb[p] = ccol[e]; slot_entry[p] = e; epos[e] = p; }
         else C.mnb[p] = I;   // padding: self, coefficient 0
       }
     }
@@ -500,6 +516,28 @@ static dfvm_status coarsen_serial(AmgH<P>* A, std::vector<HostLevel>& H, int& le
       unsigned char* d_rl = nullptr;
       if (fits && (st = A->up(&d_rl, rl))) return st;
       D.rlen = fits ? d_rl : nullptr;
+    }
+    if (A->prm.csr && A->prm.perm == 0) {
+      // CSR-stream copy: greedy warp chunks of whole rows (<= 32 rows,
+      // <= kCsrChunk entries); a row longer than a chunk disables it
+      std::vector<int> cptr(1, 0);
+      bool ok = true;
+      for (int I = 0; I < nc && ok;) {
+        int rows = 0, ent = 0;
+        while (I < nc && rows < 32 && ent + (crow_ptr[I + 1] - crow_ptr[I]) <= kCsrChunk) {
+          ent += crow_ptr[I + 1] - crow_ptr[I];
+          ++rows; ++I;
+        }
+        if (rows == 0) ok = false;
+        else cptr.push_back(I);
+      }
+      if (ok) {
+        D.n_chunk = (int)cptr.size() - 1;
+        D.nnz_csr = (int64_t)ccol.size();
+        if ((st = A->up(&D.c_ptr, cptr)) || (st = A->up(&D.c_rp, crow_ptr)) || (st = A->up(&D.c_col, ccol)) ||
+            (st = A->up(&D.c_pos, epos)) || (st = A->zalloc(&D.c_coef, ccol.size())))
+          return st;
+      }
     }
     H.push_back(std::move(C));
     ++lev;
@@ -1275,6 +1313,69 @@ __global__ void __launch_bounds__(kThreads) k_amg_dense(int n, const P* __restri
   }
 }
 
+// ---- CSR-stream coarse kernels (levels with one thread per row: C5 levels 1-2)
+// SELL-32 makes lane i gather row i's j-th neighbour: 32 rows' neighbours per
+// request, and 30-35 % padding on aggregation levels; ncu put those levels at
+// 4.1-4.6 TB/s of DRAM traffic with L1 and L2 well below their peaks (gather
+// latency bound).  Here a warp takes a chunk of whole consecutive rows (<= 32
+// rows, <= kCsrChunk entries): the lanes load the chunk's entries in CSR
+// order (coalesced coefficients and columns, no padding, neighbouring entries
+// of one row gathered by neighbouring lanes), stage coefficient and gathered
+// value in shared memory, and lane i then sums row i in its SELL entry order
+// (diag x_i first, one FMA per entry): bitwise the SELL kernels' sums.
+// c_coef = coef[c_pos] is refreshed with every Galerkin update.
+template <class T>
+__global__ void k_csr_coef(int64_t n, const int* __restrict__ pos, const T* __restrict__ coef, T* __restrict__ cc) {
+  PDL_ENTRY();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    cc[k] = coef[pos[k]];
+}
+// MODE 0: r = b - A x.  MODE 1: out = x + (b - A x) / d1 (accum: out += that)
+template <int MODE, class P>
+__global__ void __launch_bounds__(kThreads) k_amg_csr(int nchunk, const int* __restrict__ cptr,
+    const int* __restrict__ rp, const int* __restrict__ col, const P* __restrict__ cc, const P* __restrict__ diag,
+    const P* __restrict__ il1, const P* __restrict__ x, const P* __restrict__ b, P* __restrict__ out, int accum,
+    const int* done) {
+  PDL_ENTRY();
+  if (*done) return;
+  __shared__ P sa[kWarpsPerBlock][kCsrChunk], sx[kWarpsPerBlock][kCsrChunk];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunk; c += nw) {
+    const int r0 = __ldg(&cptr[c]), r1 = __ldg(&cptr[c + 1]);
+    const int e0 = __ldg(&rp[r0]), e1 = __ldg(&rp[r1]);
+    P a[kCsrChunk / 32];
+    int cl[kCsrChunk / 32];
+#pragma unroll
+    for (int u = 0; u < kCsrChunk / 32; ++u) {
+      const int k = e0 + lane + 32 * u;
+      const bool ok = k < e1;
+      a[u] = ok ? __ldg(&cc[k]) : P(0);
+      cl[u] = ok ? __ldg(&col[k]) : -1;
+    }
+    P v[kCsrChunk / 32];
+#pragma unroll
+    for (int u = 0; u < kCsrChunk / 32; ++u) v[u] = cl[u] >= 0 ? x[cl[u]] : P(0);
+#pragma unroll
+    for (int u = 0; u < kCsrChunk / 32; ++u)
+      if (cl[u] >= 0) { sa[w][lane + 32 * u] = a[u]; sx[w][lane + 32 * u] = v[u]; }
+    __syncwarp();
+    const int r = r0 + lane;
+    if (r < r1) {
+      P acc = diag[r] * x[r];
+      const int k0 = __ldg(&rp[r]) - e0, k1 = __ldg(&rp[r + 1]) - e0;
+      for (int k = k0; k < k1; ++k) acc += sa[w][k] * sx[w][k];
+      if (MODE == 0) {
+        out[r] = b[r] - acc;
+      } else {
+        const P z = x[r] + (b[r] - acc) * il1[r];
+        out[r] = accum ? out[r] + z : z;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // ---- host launchers for the group-templated kernels (G in {1,2,4,...,32})
 #define AMG_G_SWITCH(G, CALL)                      \
   switch (G) {                                     \
@@ -1315,6 +1416,25 @@ static void launch_smooth(int G, int n, const SellView& S, const P* coef, const 
                           const TB* b, TO* out, int accum, const int* done, cudaStream_t s) {
   AMG_G_SWITCH(G, (k_amg_smooth<kG, P, TB, TO><<<grid_group(n, kG), kThreads, 0, s>>>(n, S, coef, diag, il1, x, b,
                                                                                       out, accum, done)));
+}
+// a coarse level's residual / smoother: CSR-stream where the level has it
+template <class P>
+static void level_resid(const AmgLevelDev<P>& L, const P* x, const P* b, P* r, const int* done, cudaStream_t s) {
+  if (L.n_chunk > 0 && L.G == 1)
+    k_amg_csr<0, P><<<grid_for((int64_t)L.n_chunk * 32), kThreads, 0, s>>>(L.n_chunk, L.c_ptr, L.c_rp, L.c_col,
+                                                                            L.c_coef, L.diag, L.il1, x, b, r, 0, done);
+  else
+    launch_resid<P, P>(L.G, L.n, L.sv(), L.coef, L.diag, x, b, r, done, s);
+}
+template <class P>
+static void level_smooth(const AmgLevelDev<P>& L, const P* x, const P* b, P* out, int accum, const int* done,
+                         cudaStream_t s) {
+  if (L.n_chunk > 0 && L.G == 1)
+    k_amg_csr<1, P><<<grid_for((int64_t)L.n_chunk * 32), kThreads, 0, s>>>(L.n_chunk, L.c_ptr, L.c_rp, L.c_col,
+                                                                            L.c_coef, L.diag, L.il1, x, b, out, accum,
+                                                                            done);
+  else
+    launch_smooth<P, P, P>(L.G, L.n, L.sv(), L.coef, L.diag, L.il1, x, b, out, accum, done, s);
 }
 
 // ---- agglomeration of a distributed hierarchy (several ranks)
@@ -1410,6 +1530,11 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
     PLAUNCH(pr, "k_il1", l, (4 + pb) * (double)C.nnz + (4 + 2 * pb) * C.n, s,
             (k_il1<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, C.il1)));
     *nl += 3;
+    if (C.n_chunk > 0) {
+      PLAUNCH(pr, "k_csr_coef", l, (4 + 2 * pb) * (double)C.nnz_csr, s,
+              (k_csr_coef<P><<<grid_for(C.nnz_csr), kThreads, 0, s>>>(C.nnz_csr, C.c_pos, C.coef, C.c_coef)));
+      ++*nl;
+    }
   }
   if (A->ainv) {
     const AmgLevelDev<P>& C = A->L[A->nlev - 1];
@@ -1493,7 +1618,7 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
   } else {
     PLAUNCH(pr, "k_amg_pre", l, 3 * pb * n, s, (k_amg_pre<P, P, P><<<gF, kThreads, 0, s>>>(F.n, b, F.il1, F.t, done)));
     PLAUNCH(pr, "k_amg_resid", l, 4 * n + (4 + pb) * (double)F.nnz + 4 * pb * n, s,
-            launch_resid<P, P>(F.G, F.n, F.sv(), F.coef, F.diag, F.t, b, F.r, done, s));
+            level_resid<P>(F, F.t, b, F.r, done, s));
     ++*nl;
   }
   PLAUNCH(pr, "k_amg_restrict", l, (4 + pb) * (n + nc), s,
@@ -1502,7 +1627,7 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
   cycle_coarse(A, l + 1, C.b, C.x, done, s, nl);
   if (A->prm.wcycle && l + 1 < A->nlev - 1 && A->depth(l + 1) <= A->prm.wmax) {
     PLAUNCH(pr, "k_amg_resid", l + 1, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
-            launch_resid<P, P>(C.G, C.n, C.sv(), C.coef, C.diag, C.x, C.b, C.r2, done, s));
+            level_resid<P>(C, C.x, C.b, C.r2, done, s));
     ++*nl;
     if (accum_ok(A, l + 1)) {
       cycle_coarse(A, l + 1, C.r2, C.x, done, s, nl, true);   // x_c += M^-1 r2 in place
@@ -1523,7 +1648,7 @@ static void cycle_coarse(AmgH<P>* A, int l, const P* b, P* x, const int* done, c
     PLAUNCH(pr, "k_amg_prolong", l, (4 + 2 * pb) * n + pb * nc, s,
             (k_amg_prolong<P><<<gF, kThreads, 0, s>>>(F.n, F.agg, C.x, F.t, F.r, w, done)));
     PLAUNCH(pr, "k_amg_smooth", l, 4 * n + (4 + pb) * (double)F.nnz + 5 * pb * n + acc_b, s,
-            launch_smooth<P, P, P>(F.G, F.n, F.sv(), F.coef, F.diag, F.il1, F.r, b, x, accum ? 1 : 0, done, s));
+            level_smooth<P>(F, F.r, b, x, accum ? 1 : 0, done, s));
     ++*nl;
   }
   ++*nl;
@@ -1600,7 +1725,7 @@ static dfvm_status coarse_correction(AmgH<P>* A, int l, const int* done, cudaStr
   if (A->prm.wcycle && l < A->nlev - 1 && A->depth(l) <= A->prm.wmax) {
     if (A->dist && (e = halo_exchange_lists(A->m, A->halos[l], C.x, 1, f64, s))) return e;
     PLAUNCH(pr, "k_amg_resid", l, 4 * nc + (4 + pb) * (double)C.nnz + 4 * pb * nc, s,
-            launch_resid<P, P>(C.G, C.n, C.sv(), C.coef, C.diag, C.x, C.b, C.r2, done, s));
+            level_resid<P>(C, C.x, C.b, C.r2, done, s));
     ++*nl;
     if (!A->dist && accum_ok(A, l)) {
       cycle_coarse(A, l, C.r2, C.x, done, s, nl, true);   // x_c += M^-1 r2 in place

@@ -415,9 +415,10 @@ def test_c1_cavity_100_steps_trajectory():
 @pytest.mark.parametrize("precond", ["amg", "amg32"])
 @pytest.mark.parametrize("size", ["pipe_big", "c5_nz6"])
 def test_amg_kernel_variants_bitwise(precond, size, monkeypatch):
-    # the fused / unfused coarse kernels (DFVM_AMG_FUSED_FROM) change the
-    # memory traffic only: same rows, same per-row arithmetic in the same
-    # order, hence bitwise equal fields and identical iteration counts
+    # the fused / unfused coarse kernels (DFVM_AMG_FUSED_FROM) and the
+    # CSR-stream / SELL forms of the one-thread-per-row levels (DFVM_AMG_CSR)
+    # change the memory traffic only: same rows, same per-row arithmetic in
+    # the same order, hence bitwise equal fields and identical iteration counts
     import ctypes
     import torch
     import cases
@@ -435,7 +436,8 @@ def test_amg_kernel_variants_bitwise(precond, size, monkeypatch):
     s = torch.cuda.Stream()
     sp = ctypes.c_void_p(s.cuda_stream)
     out = []
-    for env in ({"DFVM_AMG_FUSED_FROM": "1"}, {"DFVM_AMG_FUSED_FROM": "3"}, {"DFVM_AMG_FUSED_FROM": "9"}):
+    for env in ({"DFVM_AMG_FUSED_FROM": "1"}, {"DFVM_AMG_FUSED_FROM": "3"}, {"DFVM_AMG_FUSED_FROM": "9"},
+                {"DFVM_AMG_FUSED_FROM": "3", "DFVM_AMG_CSR": "0"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         Sg = mk()
