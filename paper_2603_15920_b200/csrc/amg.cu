@@ -1090,14 +1090,36 @@ __device__ __forceinline__ T row_apply(const SellView& S, int q, int r, const T*
   return row_part<1>(S, q, 0, true, coef, diag[r] * x[r], [&](int c) { return x[c]; });
 }
 
+// Streaming AMG vector kernels: each thread takes kUnr rows per grid-stride
+// step (row i0 + u * stride, so every load stays coalesced across the warp)
+// and issues all their loads before any store — kUnr independent row chains
+// in flight per thread instead of one (the 4-byte vectors of the fp32
+// hierarchy left these kernels at 0.25-0.6 of the roofline).
+constexpr int kUnr = 4;
+#define AMG_UNR_LOOP(n)                                                                                \
+  const int64_t st_ = (int64_t)gridDim.x * blockDim.x;                                                 \
+  for (int64_t i0_ = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0_ < (n); i0_ += kUnr * st_)
+
 // x = b / d1 (pre-smoothing from a zero guess); b in the caller's type TB
 template <class P, class TB, class TX>
 __global__ void k_amg_pre(int n, const TB* __restrict__ b, const P* __restrict__ il1, TX* __restrict__ x,
                           const int* done) {
   PDL_ENTRY();
   if (*done) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    x[i] = (TX)((P)b[i] * il1[i]);
+  AMG_UNR_LOOP(n) {
+    P bv[kUnr], dv[kUnr];
+#pragma unroll
+    for (int u = 0; u < kUnr; ++u) {
+      const int64_t i = i0_ + u * st_;
+      bv[u] = i < n ? (P)b[i] : P(0);
+      dv[u] = i < n ? il1[i] : P(0);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnr; ++u) {
+      const int64_t i = i0_ + u * st_;
+      if (i < n) x[i] = (TX)(bv[u] * dv[u]);
+    }
+  }
 }
 // r = b - A x
 template <int G, class P, class TB>
@@ -1119,12 +1141,19 @@ __global__ void k_amg_restrict(int nc, const int* __restrict__ mp, const int* __
                                const T* __restrict__ rf, T* __restrict__ bc, const int* done) {
   PDL_ENTRY();
   if (*done) return;
+  if (G == 1) {
+    // one thread per coarse row (a kUnr-row unrolled variant was measured
+    // slower on C5: level-0 restriction 4.2 -> 5.7 ms/step)
+    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
+      T sm = T(0);
+      for (int k = __ldg(&mp[I]); k < __ldg(&mp[I + 1]); ++k) sm += rf[__ldg(&mem[k])];
+      bc[I] = sm;
+    }
+    return;
+  }
   AMG_GROUP_LOOP(nc, G) {
     const int k0 = live ? __ldg(&mp[q_]) : 0, k1 = live ? __ldg(&mp[q_ + 1]) : 0;
     T s = T(0);
-    if (G == 1)
-      for (int k = k0; k < k1; ++k) s += rf[__ldg(&mem[k])];
-    else
     for (int k = k0 + sub_; k < k1; k += 4 * G) {
       int f[4];
 #pragma unroll
@@ -1146,7 +1175,24 @@ __global__ void k_amg_prolong(int n, const int* __restrict__ agg, const T* __res
                               T* __restrict__ t, T w, const int* done) {
   PDL_ENTRY();
   if (*done) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) t[i] = x[i] + w * xc[agg[i]];
+  AMG_UNR_LOOP(n) {
+    int a[kUnr];
+    T xv[kUnr];
+#pragma unroll
+    for (int u = 0; u < kUnr; ++u) {
+      const int64_t i = i0_ + u * st_;
+      a[u] = i < n ? __ldg(&agg[i]) : 0;
+      xv[u] = i < n ? x[i] : T(0);
+    }
+    T cv[kUnr];
+#pragma unroll
+    for (int u = 0; u < kUnr; ++u) cv[u] = xc[a[u]];
+#pragma unroll
+    for (int u = 0; u < kUnr; ++u) {
+      const int64_t i = i0_ + u * st_;
+      if (i < n) t[i] = xv[u] + w * cv[u];
+    }
+  }
 }
 // fused pre-smooth + residual (rows without ghost columns): x0 = b / d1 for
 // the row and, on the fly, for every neighbour; writes x0 and r = b - A x0
@@ -1291,6 +1337,68 @@ __global__ void __launch_bounds__(1024) k_amg_dense_inv(int n, SellView S, const
     __syncthreads();
   }
 }
+
+// Dense inverse of the (SPD) coarsest matrix in SHARED memory by the
+// symmetric sweep operator on the packed lower triangle (round 2: the
+// global-memory Gauss-Jordan above re-read and re-wrote the whole n x n
+// matrix through L2 from one SM at every pivot — 2.4 ms per update for the
+// 240-row coarsest level of C2, a quarter of its step).  Pivot k, with
+// d = a_kk (a_ij for i < j read as a_ji):
+//   a_ij -= a_ik a_jk / d   (i, j != k);   a_ik /= d (i != k);   a_kk = -1/d
+// After all n pivots the packed matrix holds -A^-1 (no pivoting: the
+// Galerkin coarse matrix of an SPD operator is SPD).  The result is expanded
+// row-major into Ai (both triangles).  One block; dynamic shared memory
+// n (n + 1) / 2 + n values (fp32: n <= 340).
+template <class P>
+__global__ void __launch_bounds__(1024) k_amg_dense_inv_sym(int n, SellView S, const P* __restrict__ coef,
+                                                            const P* __restrict__ diag, P* __restrict__ Ai) {
+  PDL_ENTRY();
+  extern __shared__ unsigned char dyn_smem[];
+  P* a = reinterpret_cast<P*>(dyn_smem);            // packed lower triangle, a[i (i + 1) / 2 + j], j <= i
+  P* ck = a + (size_t)n * (n + 1) / 2;              // column k of the current pivot
+  auto at = [&](int i, int j) -> P& { return i >= j ? a[(size_t)i * (i + 1) / 2 + j] : a[(size_t)j * (j + 1) / 2 + i]; };
+  const int np = n * (n + 1) / 2;
+  for (int e = threadIdx.x; e < np; e += blockDim.x) a[e] = P(0);
+  __syncthreads();
+  // densify: slot q (row i) owns its row; only the lower triangle is stored
+  // (the Galerkin operator is symmetric: a_ij = a_ji)
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
+    const int i = slot_row(S, q);
+    at(i, i) = diag[i];
+    const int sl = q >> 5, lane = q & 31;
+    for (int j = 0; j < S.ms_len[sl]; ++j) {
+      const int p = S.ms_ptr[sl] + 32 * j + lane;
+      const int c = S.mnb[p];
+      if (c < i) at(i, c) += coef[p];
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = 0; k < n; ++k) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) ck[j] = at(j, k);
+    __syncthreads();
+    const P d = ck[k], rd = P(1) / d;
+    // rank-1 update of every (i, j) with j <= i, i != k, j != k: warp per row
+    for (int i = wid; i < n; i += nw) {
+      if (i == k) continue;
+      const P f = ck[i] * rd;
+      P* row = a + (size_t)i * (i + 1) / 2;
+      for (int j = lane; j <= i; j += 32)
+        if (j != k) row[j] -= f * ck[j];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) at(j, k) = (j == k) ? -rd : ck[j] * rd;
+    __syncthreads();
+  }
+  // Ai = -(swept matrix), row-major, both triangles
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    Ai[e] = -at(i, j);
+  }
+}
+template <class P>
+static size_t dense_inv_sym_smem(int n) { return ((size_t)n * (n + 1) / 2 + n) * sizeof(P); }
+constexpr size_t kSmemOptIn = 227 * 1024;
 
 // coarsest solve with the dense inverse: x_i = sum_j Ainv_ij b_j, one warp
 // per row (row-major Ainv: coalesced across the lanes, 4 loads in flight per
@@ -1538,8 +1646,18 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
   }
   if (A->ainv) {
     const AmgLevelDev<P>& C = A->L[A->nlev - 1];
-    PLAUNCH(pr, "k_amg_dense_inv", A->nlev - 1, 2 * pb * (double)C.n * C.n, s,
-            (k_amg_dense_inv<P><<<1, 1024, 0, s>>>(C.n, C.sv(), C.coef, C.diag, A->ainv)));
+    const size_t sm = dense_inv_sym_smem<P>(C.n);
+    const bool sym_on = [] { const char* e = getenv("DFVM_AMG_INV"); return !(e && atoi(e) == 0); }();
+    if (sym_on && sm <= kSmemOptIn &&
+        cudaFuncSetAttribute(k_amg_dense_inv_sym<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) ==
+            cudaSuccess) {
+      PLAUNCH(pr, "k_amg_dense_inv", A->nlev - 1, 2 * pb * (double)C.n * C.n, s,
+              (k_amg_dense_inv_sym<P><<<1, 1024, sm, s>>>(C.n, C.sv(), C.coef, C.diag, A->ainv)));
+    } else {
+      cudaGetLastError();
+      PLAUNCH(pr, "k_amg_dense_inv", A->nlev - 1, 2 * pb * (double)C.n * C.n, s,
+              (k_amg_dense_inv<P><<<1, 1024, 0, s>>>(C.n, C.sv(), C.coef, C.diag, A->ainv)));
+    }
     ++*nl;
   }
   DFVM_CUDA(cudaGetLastError());

@@ -78,14 +78,18 @@ __device__ __forceinline__ void sell_apply(const DevMesh<T>& M, int s, int lane,
 // 2/3: implicit upwind + explicit deferred correction m (x^HO - x_C)
 // (eq:deferred_correction, eq:sou P:200-206, SPEC.md:233 QUICK),
 // with dO = x_f - x_O, dN = x_f - x_N per face.
-template <class T, int NC>
+// HO: deferred-correction (SOU / QUICK) code compiled in; EXPL: theta != 1
+// (the explicit part A_s x^n).  The upwind / central backward-Euler variant
+// (the bench path) compiles without either (fewer registers, higher
+// occupancy; the same arithmetic).
+template <class T, int NC, bool HO = true, bool EXPL = true>
 __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, const T* __restrict__ U,
     const T* __restrict__ phi, const T* __restrict__ gU, const T* __restrict__ gp, const uint8_t* __restrict__ bk,
     const T* __restrict__ bv, T nu, T rdt, T theta, int conv, int kcorr, const V4<T>* __restrict__ fdO,
     const V4<T>* __restrict__ fdN, T* __restrict__ udiag, T* __restrict__ bU, T* __restrict__ rhsU,
     T* __restrict__ ucoef, T* __restrict__ ucoefT) {
   PDL_ENTRY();
-  const bool explicit_part = theta != T(1);
+  const bool explicit_part = EXPL && theta != T(1);
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
     const bool live = row < M.n_own;
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, c
                           c.y * (w * GO[3 * k + 1] + (T(1) - w) * GN[3 * k + 1]) +
                           c.z * (w * GO[3 * k + 2] + (T(1) - w) * GN[3 * k + 2]));
         }
-        if (conv >= 2) {
+        if (HO && conv >= 2) {
           const bool up_own = md >= T(0);
           const int Cc = up_own ? O : N, D = up_own ? N : O;
           const V4<T> a = ld4(up_own ? &fdO[f] : &fdN[f]);            // d_Cf = x_f - x_C
@@ -190,6 +194,22 @@ __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, c
       }
     }
   }
+}
+
+template <class T, int NC>
+static void launch_transport_assemble(int gs, cudaStream_t st, DevMesh<T> M, const T* U, const T* phi, const T* gU,
+                                      const T* gp, const uint8_t* bk, const T* bv, T nu, T rdt, T theta, int conv,
+                                      int kcorr, const V4<T>* fdO, const V4<T>* fdN, T* udiag, T* bU, T* rhsU, T* ucoef,
+                                      T* ucoefT) {
+  const bool ho = conv >= 2, ex = theta != T(1);
+#define KTA(H, E)                                                                                                   \
+  k_transport_assemble<T, NC, H, E><<<gs, kThreads, 0, st>>>(M, U, phi, gU, gp, bk, bv, nu, rdt, theta, conv, kcorr, \
+                                                              fdO, fdN, udiag, bU, rhsU, ucoef, ucoefT)
+  if (ho && ex) KTA(true, true);
+  else if (ho) KTA(true, false);
+  else if (ex) KTA(false, true);
+  else KTA(false, false);
+#undef KTA
 }
 
 template <class T, int NC>
@@ -365,7 +385,11 @@ __global__ void __launch_bounds__(kThreads) k_prhs(DevMesh<T> M, const T* __rest
     const bool live = row < M.n_own;
     const T ra = live ? rAU[row] : T(0);
     T acc = live ? prhs0[row] : T(0);
-    const T* Gc = gp + 3 * (int64_t)(live ? row : 0);
+    // the row's own gradient in registers: 3 gathered loads per incidence, not 6
+    T gc[3] = {T(0), T(0), T(0)};
+    if (live)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) gc[k] = gp[3 * (int64_t)row + k];
     const int len = __ldg(&M.sl_len[s]);
     const int2* e = M.inc + __ldg(&M.sl_ptr[s]) + lane;
     for (int j = 0; j < len; ++j) {
@@ -377,9 +401,13 @@ __global__ void __launch_bounds__(kThreads) k_prhs(DevMesh<T> M, const T* __rest
       const T w = __ldg(&M.fw[f]);
       const V4<T> c = ld4(&M.fcor[f]);
       const T rn = rAU[n];
-      const T* Gn = gp + 3 * (int64_t)n;
-      const T* GO = own ? Gc : Gn;
-      const T* GN = own ? Gn : Gc;
+      T gn[3], GO[3], GN[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        gn[k] = gp[3 * (int64_t)n + k];
+        GO[k] = own ? gc[k] : gn[k];
+        GN[k] = own ? gn[k] : gc[k];
+      }
       const T rf = w * (own ? ra : rn) + (T(1) - w) * (own ? rn : ra);
       const T kg = c.x * (w * GO[0] + (T(1) - w) * GN[0]) + c.y * (w * GO[1] + (T(1) - w) * GN[1]) +
                    c.z * (w * GO[2] + (T(1) - w) * GN[2]);
@@ -1696,10 +1724,9 @@ static dfvm_status assemble(dfvm_solver* S, SolverT<T>& X, const T* U, const T* 
   S->n_launch++;
   if ((s2 = halo_exchange(S->m, X.gU, 9, st))) return s2;
   PLAUNCH(pr, "k_transport_assemble", -1, 23 * v * N + (16 + 10 * v) * F + (9 + 8 * v) * Bf, st,
-          (k_transport_assemble<T, 3><<<gs, kThreads, 0, st>>>(M, U, phi, X.gU, X.gp, b->d_kind[0],
-                                                               (const T*)b->d_val[0], (T)S->o.nu, (T)(1.0 / S->o.dt),
-                                                               (T)theta_of(S->o), S->o.convection, S->kcorr, X.fdO,
-                                                               X.fdN, X.udiag, X.bU, X.rhsU, X.ucoef, X.ucoefT)));
+          launch_transport_assemble<T, 3>(gs, st, M, U, phi, X.gU, X.gp, b->d_kind[0], (const T*)b->d_val[0],
+                                          (T)S->o.nu, (T)(1.0 / S->o.dt), (T)theta_of(S->o), S->o.convection,
+                                          S->kcorr, X.fdO, X.fdN, X.udiag, X.bU, X.rhsU, X.ucoef, X.ucoefT));
   S->n_launch++;
   if ((s2 = halo_exchange(S->m, X.udiag, 1, st))) return s2;   // ghost diag: rAU of the neighbours (k_HbyA ...)
   X.assembled = true;
@@ -1880,9 +1907,9 @@ static dfvm_status transport_step_t(dfvm_solver* S, SolverT<T>& X, T* x, const T
   launch_grad<T>(M, x, 1, b->d_kind[2], (const T*)b->d_val[2], X.gp, st);
   if ((e = halo_exchange(S->m, X.gp, 3, st))) return e;
   const int gs = grid_for_slices(M.n_slices), ge = grid_for(M.n_own);
-  k_transport_assemble<T, 1><<<gs, kThreads, 0, st>>>(M, x, phi, X.gp, nullptr, b->d_kind[2], (const T*)b->d_val[2],
-                                                      (T)gamma, (T)(1.0 / S->o.dt), (T)theta_of(S->o), S->o.convection, S->kcorr,
-                                                      X.fdO, X.fdN, X.udiag, X.prhs0, X.prhs, X.ucoef, X.ucoefT);
+  launch_transport_assemble<T, 1>(gs, st, M, x, phi, X.gp, nullptr, b->d_kind[2], (const T*)b->d_val[2], (T)gamma,
+                                  (T)(1.0 / S->o.dt), (T)theta_of(S->o), S->o.convection, S->kcorr, X.fdO, X.fdN,
+                                  X.udiag, X.prhs0, X.prhs, X.ucoef, X.ucoefT);
   if ((e = halo_exchange(S->m, X.udiag, 1, st))) return e;
   S->n_launch += 2;
   X.assembled = true;

@@ -20,7 +20,7 @@ if mode == "launches":
         key = (r[col["Kernel Name"]].split("(")[0], r[col["Grid Size"]], r[col["Block Size"]])
         v = float(r[col["Metric Value"]].replace(",", ""))
         unit = r[col["Metric Unit"]]
-        v = v / 1000.0 if unit == "nsecond" else (v * 1000.0 if unit == "msecond" else v)   # -> usecond
+        v = v / 1000.0 if unit in ("nsecond", "ns") else (v * 1000.0 if unit in ("msecond", "ms") else v)   # -> usecond
         agg[key][0] += 1
         agg[key][1] += v
     tot = sum(v[1] for v in agg.values())
