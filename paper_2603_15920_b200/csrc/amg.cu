@@ -55,7 +55,8 @@ dfvm_status allgather_f64(dfvm_mesh* m, const double* local, double* gathered, i
 bool comm_is_local(const dfvm_comm* c);
 
 constexpr int kCoarseMax = 2048;     // shared-memory capacity of the one-block coarse solve
-constexpr int kDirectMax = 512;      // largest coarsest level solved with a dense inverse
+constexpr int kDirectMax = 512;      // largest coarsest level inverted by one block
+constexpr int kDirectBig = 4096;     // largest coarsest level inverted at all (multi-launch Gauss-Jordan above kDirectMax)
 constexpr int kMaxLevels = 16;
 constexpr int kCsrChunk = 128;       // entries per warp chunk of the CSR-stream coarse kernels (4 per lane)
 
@@ -119,10 +120,10 @@ struct AmgParams {
   bool wcycle = true;
   double omega = 1.95;  // C5 amg32 (round 2): 344.0 ms, 11.33 it/solve (1.9: 349.6 ms, 11.58; 1.8: 360.2 ms, 12.17)
   AmgParams() {
-    if (const char* e = getenv("DFVM_AMG_DIRECT")) direct = std::max(0, std::min(kDirectMax, atoi(e)));
+    if (const char* e = getenv("DFVM_AMG_DIRECT")) direct = std::max(0, std::min(kDirectBig, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_PERM")) perm = atoi(e);
     if (const char* e = getenv("DFVM_AMG_OMEGA")) omega = atof(e);
-    if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kCoarseMax, atoi(e)));
+    if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kDirectBig, atoi(e)));
     if (const char* e = getenv("DFVM_AMG_SWEEPS")) sweeps = std::max(1, atoi(e));
     if (const char* e = getenv("DFVM_AMG_CYCLE")) wcycle = (e[0] == 'W' || e[0] == 'w');
     if (const char* e = getenv("DFVM_AMG_WMAX")) wmax = std::max(0, atoi(e));
@@ -297,6 +298,7 @@ struct AmgH {
   Prof* prof = nullptr;             // per-kernel profile of the caller (may be null)
   AmgLevelDev<P> L[kMaxLevels];
   P* ainv = nullptr;                // dense inverse of the coarsest matrix (column-major n x n), or NULL
+  P* gj_buf = nullptr;              // pivot row / column of the multi-launch Gauss-Jordan
   // several ranks: levels 0..ld are distributed (owned aggregates of owned
   // rows, ghost aggregates of the neighbours, a halo per level); level ld+1
   // is the AGGLOMERATION of every rank's level-ld rows into one global
@@ -320,6 +322,7 @@ struct AmgH {
   std::vector<void*> allocs;
   int64_t bytes = 0;
   ~AmgH() {
+    if (gj_buf) dev_free(gj_buf, nullptr);
     for (void* p : allocs) dev_free(p, nullptr);
     for (auto& h : halos) { dev_free(h.d_send, nullptr); dev_free(h.d_send_idx, nullptr); }
   }
@@ -1141,16 +1144,9 @@ __global__ void k_amg_restrict(int nc, const int* __restrict__ mp, const int* __
                                const T* __restrict__ rf, T* __restrict__ bc, const int* done) {
   PDL_ENTRY();
   if (*done) return;
-  if (G == 1) {
-    // one thread per coarse row (a kUnr-row unrolled variant was measured
-    // slower on C5: level-0 restriction 4.2 -> 5.7 ms/step)
-    for (int I = blockIdx.x * blockDim.x + threadIdx.x; I < nc; I += gridDim.x * blockDim.x) {
-      T sm = T(0);
-      for (int k = __ldg(&mp[I]); k < __ldg(&mp[I + 1]); ++k) sm += rf[__ldg(&mem[k])];
-      bc[I] = sm;
-    }
-    return;
-  }
+  // (G = 1 too: the members in predicated batches of 4 — measured on C5 at
+  // 3.95 / 2.70 ms/step on levels 0 / 1 against 4.22 / 3.00 one member at a
+  // time, and 5.67 / 4.12 with 4 coarse rows per thread instead)
   AMG_GROUP_LOOP(nc, G) {
     const int k0 = live ? __ldg(&mp[q_]) : 0, k1 = live ? __ldg(&mp[q_ + 1]) : 0;
     T s = T(0);
@@ -1336,6 +1332,199 @@ __global__ void __launch_bounds__(1024) k_amg_dense_inv(int n, SellView S, const
     }
     __syncthreads();
   }
+}
+
+// Multi-launch Gauss-Jordan for coarsest levels above kDirectMax rows
+// (experimental, DFVM_AMG_COARSE / DFVM_AMG_DIRECT up to kDirectBig): densify,
+// then per pivot k one staging launch (row k / a_kk, column k) and one
+// update launch over all n^2 entries (same arithmetic as k_amg_dense_inv).
+template <class P>
+__global__ void k_dense_fill(int n, SellView S, const P* __restrict__ coef, const P* __restrict__ diag,
+                             P* __restrict__ A) {
+  PDL_ENTRY();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * n; e += (int64_t)gridDim.x * blockDim.x)
+    A[e] = P(0);
+}
+template <class P>
+__global__ void k_dense_rows(int n, SellView S, const P* __restrict__ coef, const P* __restrict__ diag,
+                             P* __restrict__ A) {
+  PDL_ENTRY();
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int i = slot_row(S, q);
+    A[(size_t)i * n + i] = diag[i];
+    const int sl = q >> 5, lane = q & 31;
+    for (int j = 0; j < S.ms_len[sl]; ++j) {
+      const int p = S.ms_ptr[sl] + 32 * j + lane;
+      if (S.mnb[p] < n) A[(size_t)i * n + S.mnb[p]] += coef[p];
+    }
+  }
+}
+template <class P>
+__global__ void k_gj_stage(int n, int k, const P* __restrict__ A, P* __restrict__ rowk, P* __restrict__ colk) {
+  PDL_ENTRY();
+  const P piv = A[(size_t)k * n + k];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    colk[i] = A[(size_t)i * n + k];
+    rowk[i] = (i == k ? P(1) : A[(size_t)k * n + i]) / piv;
+  }
+}
+template <class P>
+__global__ void k_gj_update(int n, int k, P* __restrict__ A, const P* __restrict__ rowk, const P* __restrict__ colk) {
+  PDL_ENTRY();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+    const P a = A[e];
+    A[e] = (i == k) ? rowk[j] : ((j == k ? P(0) : a) - colk[i] * rowk[j]);
+  }
+}
+
+// Blocked symmetric sweep for coarsest levels above kDirectMax rows (fp32):
+// the dense n x n matrix in global memory (L2 resident), pivot blocks of
+// kBlk rows.  Block step K (rows / cols k0 .. k0 + kb):
+//   S = A_KK^-1 (one CTA, shared-memory sweep);  P = A_:K S  (n x kb);
+//   A_ij -= P_i A_Kj  for i, j outside K   (the rank-kb update: a tiled SIMT
+//                                             GEMM, 2 n^2 kb flops);
+//   A_iK = P_i,  A_Kj = P_j^T (symmetry),  A_KK = -S.
+// After every block the matrix holds -A^-1 (the block form of the sweep
+// operator of k_amg_dense_inv_sym; no pivoting: SPD).  Densified from the
+// lower triangle and mirrored, so it stays symmetric.
+constexpr int kBlk = 64;
+constexpr int kTM = 128, kTN = 128;   // update tile
+template <class P>
+__global__ void k_dense_rows_sym(int n, SellView S, const P* __restrict__ coef, const P* __restrict__ diag,
+                                 P* __restrict__ A) {
+  PDL_ENTRY();
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int i = slot_row(S, q);
+    A[(size_t)i * n + i] = diag[i];
+    const int sl = q >> 5, lane = q & 31;
+    for (int j = 0; j < S.ms_len[sl]; ++j) {
+      const int p = S.ms_ptr[sl] + 32 * j + lane;
+      const int c = S.mnb[p];
+      if (c < i) { A[(size_t)i * n + c] += coef[p]; A[(size_t)c * n + i] += coef[p]; }
+    }
+  }
+}
+// S = A_KK^-1 by the sweep operator in shared memory (one CTA)
+template <class P>
+__global__ void __launch_bounds__(256) k_blk_inv(int n, int k0, int kb, const P* __restrict__ A, P* __restrict__ Sb) {
+  PDL_ENTRY();
+  __shared__ P a[kBlk][kBlk + 1];
+  __shared__ P ck[kBlk];
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int r = e / kb, c = e - r * kb;
+    a[r][c] = A[(size_t)(k0 + r) * n + k0 + c];
+  }
+  __syncthreads();
+  for (int k = 0; k < kb; ++k) {
+    for (int j = threadIdx.x; j < kb; j += blockDim.x) ck[j] = a[j][k];
+    __syncthreads();
+    const P rd = P(1) / ck[k];
+    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+      const int r = e / kb, c = e - r * kb;
+      if (r != k && c != k) a[r][c] -= ck[r] * rd * ck[c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < kb; j += blockDim.x) {
+      const P v = (j == k) ? -rd : ck[j] * rd;
+      a[j][k] = v;
+      a[k][j] = v;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int r = e / kb, c = e - r * kb;
+    Sb[r * kBlk + c] = -a[r][c];
+  }
+}
+// Pb[i][c] = sum_t A[i][k0 + t] S[t][c]  (4 rows per CTA)
+template <class P>
+__global__ void __launch_bounds__(256) k_blk_panel(int n, int k0, int kb, const P* __restrict__ A,
+                                                   const P* __restrict__ Sb, P* __restrict__ Pb) {
+  PDL_ENTRY();
+  __shared__ P s[kBlk][kBlk + 1];
+  __shared__ P ar[4][kBlk];
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) s[e / kb][e % kb] = Sb[(e / kb) * kBlk + e % kb];
+  for (int i0 = blockIdx.x * 4; i0 < n; i0 += gridDim.x * 4) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 4 * kb; e += blockDim.x) {
+      const int r = e / kb, t = e - r * kb;
+      ar[r][t] = (i0 + r < n) ? A[(size_t)(i0 + r) * n + k0 + t] : P(0);
+    }
+    __syncthreads();
+    const int r = threadIdx.x / kBlk, c = threadIdx.x % kBlk;
+    if (i0 + r < n && c < kb) {
+      P acc = P(0);
+      for (int t = 0; t < kb; ++t) acc += ar[r][t] * s[t][c];
+      Pb[(size_t)(i0 + r) * kBlk + c] = acc;
+    }
+  }
+}
+// A_ij -= sum_t Pb[i][t] A[k0 + t][j]  for i, j outside block K: 128 x 128
+// tile per CTA, 8 x 8 outputs per thread, both operands staged in shared memory
+template <class P>
+__global__ void __launch_bounds__(256) k_blk_update(int n, int k0, int kb, P* __restrict__ A, const P* __restrict__ Pb) {
+  PDL_ENTRY();
+  extern __shared__ unsigned char blk_smem[];
+  P* sP = reinterpret_cast<P*>(blk_smem);          // [kBlk][kTM]   Pb^T tile
+  P* sR = sP + kBlk * kTM;                          // [kBlk][kTN]   block-row tile
+  const int i0 = blockIdx.y * kTM, j0 = blockIdx.x * kTN;
+  for (int e = threadIdx.x; e < kTM * kBlk; e += blockDim.x) {
+    const int i = e / kBlk, t = e - i * kBlk;
+    sP[t * kTM + i] = (i0 + i < n && t < kb) ? Pb[(size_t)(i0 + i) * kBlk + t] : P(0);
+  }
+  for (int e = threadIdx.x; e < kBlk * kTN; e += blockDim.x) {
+    const int t = e / kTN, j = e - t * kTN;
+    sR[t * kTN + j] = (j0 + j < n && t < kb) ? A[(size_t)(k0 + t) * n + j0 + j] : P(0);
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  P acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = P(0);
+  for (int t = 0; t < kb; ++t) {
+    P a[8], b[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = sP[t * kTM + ty * 8 + r];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) b[c] = sR[t * kTN + tx * 8 + c];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] += a[r] * b[c];
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + ty * 8 + r;
+    if (i >= n || (i >= k0 && i < k0 + kb)) continue;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int j = j0 + tx * 8 + c;
+      if (j < n && !(j >= k0 && j < k0 + kb)) A[(size_t)i * n + j] -= acc[r][c];
+    }
+  }
+}
+// block column / row K <- P (and P^T), A_KK <- -S
+template <class P>
+__global__ void k_blk_finish(int n, int k0, int kb, P* __restrict__ A, const P* __restrict__ Pb, const P* __restrict__ Sb) {
+  PDL_ENTRY();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * kb; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / kb), c = (int)(e - (int64_t)i * kb);
+    if (i >= k0 && i < k0 + kb) {
+      A[(size_t)i * n + k0 + c] = -Sb[(i - k0) * kBlk + c];
+    } else {
+      const P v = Pb[(size_t)i * kBlk + c];
+      A[(size_t)i * n + k0 + c] = v;
+      A[(size_t)(k0 + c) * n + i] = v;
+    }
+  }
+}
+template <class P>
+__global__ void k_negate(int64_t n, P* __restrict__ A) {
+  PDL_ENTRY();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) A[e] = -A[e];
 }
 
 // Dense inverse of the (SPD) coarsest matrix in SHARED memory by the
@@ -1647,6 +1836,48 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
   if (A->ainv) {
     const AmgLevelDev<P>& C = A->L[A->nlev - 1];
     const size_t sm = dense_inv_sym_smem<P>(C.n);
+    if (C.n > kDirectMax && std::is_same<P, float>::value) {
+      // blocked symmetric sweep (fp32): 4 launches per block of kBlk pivots
+      const int n = C.n;
+      if (!A->gj_buf && (dev_alloc_n(&A->gj_buf, (size_t)n * kBlk + kBlk * kBlk, nullptr, true) != DFVM_OK))
+        return DFVM_E_CUDA;
+      P* Pb = A->gj_buf;
+      P* Sb = A->gj_buf + (size_t)n * kBlk;
+      const size_t usm = 2 * (size_t)kBlk * kTM * sizeof(P);
+      DFVM_CUDA(cudaFuncSetAttribute(k_blk_update<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
+      PLAUNCH(pr, "k_amg_dense_inv", A->nlev - 1, 2 * pb * (double)n * n, s, {
+        k_dense_fill<P><<<grid_for((int64_t)n * n), kThreads, 0, s>>>(n, C.sv(), C.coef, C.diag, A->ainv);
+        k_dense_rows_sym<P><<<grid_for(n), kThreads, 0, s>>>(n, C.sv(), C.coef, C.diag, A->ainv);
+        const dim3 tg((n + kTN - 1) / kTN, (n + kTM - 1) / kTM);
+        for (int k0 = 0; k0 < n; k0 += kBlk) {
+          const int kb = std::min(kBlk, n - k0);
+          k_blk_inv<P><<<1, 256, 0, s>>>(n, k0, kb, A->ainv, Sb);
+          k_blk_panel<P><<<std::min(grid_for(n), (n + 3) / 4), 256, 0, s>>>(n, k0, kb, A->ainv, Sb, Pb);
+          k_blk_update<P><<<tg, 256, usm, s>>>(n, k0, kb, A->ainv, Pb);
+          k_blk_finish<P><<<grid_for((int64_t)n * kb), kThreads, 0, s>>>(n, k0, kb, A->ainv, Pb, Sb);
+        }
+        k_negate<P><<<grid_for((int64_t)n * n), kThreads, 0, s>>>((int64_t)n * n, A->ainv);
+      });
+      *nl += 3 + 4 * ((n + kBlk - 1) / kBlk);
+      DFVM_CUDA(cudaGetLastError());
+      return DFVM_OK;
+    }
+    if (C.n > kDirectMax) {
+      // multi-launch Gauss-Jordan (fp64 large coarsest level)
+      if (!A->gj_buf && (dev_alloc_n(&A->gj_buf, 2 * (size_t)C.n, nullptr, true) != DFVM_OK)) return DFVM_E_CUDA;
+      P* rowk = A->gj_buf;
+      P* colk = A->gj_buf + C.n;
+      const int gn = grid_for((int64_t)C.n * C.n);
+      k_dense_fill<P><<<gn, kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, A->ainv);
+      k_dense_rows<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, C.sv(), C.coef, C.diag, A->ainv);
+      for (int k = 0; k < C.n; ++k) {
+        k_gj_stage<P><<<grid_for(C.n), kThreads, 0, s>>>(C.n, k, A->ainv, rowk, colk);
+        k_gj_update<P><<<gn, kThreads, 0, s>>>(C.n, k, A->ainv, rowk, colk);
+      }
+      *nl += 2 + 2 * C.n;
+      DFVM_CUDA(cudaGetLastError());
+      return DFVM_OK;
+    }
     const bool sym_on = [] { const char* e = getenv("DFVM_AMG_INV"); return !(e && atoi(e) == 0); }();
     if (sym_on && sm <= kSmemOptIn &&
         cudaFuncSetAttribute(k_amg_dense_inv_sym<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) ==

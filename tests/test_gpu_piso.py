@@ -506,3 +506,28 @@ def test_programmatic_launch_bitwise(mode, monkeypatch):
         assert a[3] == b[3]
         for x, y in zip(a[:3], b[:3]):
             assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("precond", ["amg32", "amg"])
+def test_amg_large_coarsest_inverse(precond, monkeypatch):
+    # coarsest levels above the one-block limit (512 rows) are inverted by the
+    # blocked symmetric sweep (fp32) / the multi-launch Gauss-Jordan (fp64):
+    # the converged pressure equals the oracle's, in no more PCG iterations
+    # than with the deeper hierarchy and its 512-row-capped dense coarsest
+    raw, mo, mg, bo, bg, kw = pipe_case(n=8, m_r=4, n_z=40)
+    So = oracle.Solver(mo, bo, **kw)
+    rAU = 0.01 * (1.5 + 0.5 * synth.cell_field(60, mo.N))
+    rhs = 1e-3 * synth.cell_field(61, mo.N)
+    po, ro = So.pressure_solve(rAU, rhs, p0=np.zeros(mo.N), tol=1e-14)
+    its = []
+    for coarse in ("256", "2000"):
+        monkeypatch.setenv("DFVM_AMG_COARSE", coarse)
+        monkeypatch.setenv("DFVM_AMG_DIRECT", "4000")
+        Sg = dfvm.Solver(mg, bg, p_precond=precond, **kw)
+        pg = mg.field("cells", 1)
+        rg = Sg.pressure_solve(mg.field("cells", 1, rAU), mg.field("cells", 1, rhs), pg, tol=1e-14)
+        lv = Sg.amg_levels()
+        assert rg["converged"] and rel_l2(pg.get(), po) <= 1e-8
+        its.append((rg["it"], lv))
+    assert its[1][1][-1] > 512, its          # the large-coarsest path ran
+    assert its[1][0] <= its[0][0] + 1, its
