@@ -22,11 +22,15 @@
 //    prolongation x = x0 + omega x_c[agg], l1-Jacobi post-smoothing (the
 //    adjoint of the pre-smoother); a W-cycle (two coarse visits, the second
 //    on the residual of the first) on levels <= 4 and a V-cycle below;
-//    coarsening stops at <= 256 rows (never below 32), and the coarsest level
-//    (<= 512 rows) is solved exactly with its dense inverse (Gauss-Jordan
-//    once per matrix update); a larger coarsest level (coarsening stalled)
-//    gets `sweeps` l1-Jacobi sweeps (one block up to 2048 rows, multi-block
-//    above).  Adjoint smoothers, a symmetric coarse solve and the W-cycle's
+//    coarsening stops at <= 256 rows (fp64 hierarchy) or <= 4000 rows (fp32:
+//    amg32 and the f32 solver; C5 stops at its 3 330-row level 4), never
+//    below 32, and the coarsest level is solved exactly with its dense
+//    inverse, refreshed once per step: one-block shared-memory symmetric
+//    sweep (fp32 <= 340 rows) or one-block Gauss-Jordan (<= 512 rows), the
+//    blocked symmetric sweep in global memory (fp32, <= 4096 rows) or a
+//    multi-launch Gauss-Jordan (fp64, <= 4096); a coarsest level beyond the
+//    direct bound (coarsening stalled) gets `sweeps` l1-Jacobi sweeps (one
+//    block up to 2048 rows, multi-block above).  Adjoint smoothers, a symmetric coarse solve and the W-cycle's
 //    2B - BAB keep M^-1 SPD, so CG stays CG.  The converged pressure is
 //    preconditioner independent (A-14).
 //  * precision: the hierarchy's type P is the solver's T ("amg"), or fp32
@@ -62,7 +66,7 @@ constexpr int kCsrChunk = 128;       // entries per warp chunk of the CSR-stream
 
 // Tunables (defaults chosen from B200 measurements on the C5 pipe, DESIGN.md
 // §6); overridable through the environment for experiments:
-//   DFVM_AMG_COARSE  coarsest-level size bound (rows)           default 256
+//   DFVM_AMG_COARSE  coarsest-level size bound (rows)   default 256 (fp32: 4000)
 //   DFVM_AMG_SWEEPS  l1-Jacobi sweeps of the coarsest solve       default 32
 //   DFVM_AMG_CYCLE   'V' or 'W'                                   default W
 //   DFVM_AMG_WMAX    deepest level visited twice by the W-cycle   default 4
@@ -102,7 +106,7 @@ constexpr int kCsrChunk = 128;       // entries per warp chunk of the CSR-stream
 //                    global level replicated on every rank (with the serial
 //                    hierarchy below it); the levels above are distributed
 //                                                               default 100000
-//   DFVM_AMG_DIRECT  coarsest levels with <= this many rows are solved
+//   DFVM_AMG_DIRECT  coarsest levels with <= this many rows (fp32 default 4096) are solved
 //                    exactly with a dense inverse (Gauss-Jordan once per
 //                    matrix update, one block), larger ones with
 //                    DFVM_AMG_SWEEPS l1-Jacobi sweeps (0: always sweeps)  default 512
@@ -119,11 +123,22 @@ struct AmgParams {
   int csr = 0;
   bool wcycle = true;
   double omega = 1.95;  // C5 amg32 (round 2): 344.0 ms, 11.33 it/solve (1.9: 349.6 ms, 11.58; 1.8: 360.2 ms, 12.17)
+  bool env_coarse = false, env_direct = false;
+  // fp32 hierarchies (amg32): coarsen only down to <= 4000 rows and solve
+  // that level exactly with the blocked dense inverse (C5: the 3 330-row
+  // level, no 144-row level below it) — measured on C5 round 2 at 313.4 /
+  // 313.4 ms/step and 10.3 PCG iterations per solve, against 324.5 / 327.3
+  // ms/step and 11.3 with the W-cycle to a 144-row exact level
+  // (profiles/r02_sweep_r2q_lvl4.jsonl); env overrides win
+  void fp32_defaults() {
+    if (!env_coarse) coarse = 4000;
+    if (!env_direct) direct = kDirectBig;
+  }
   AmgParams() {
-    if (const char* e = getenv("DFVM_AMG_DIRECT")) direct = std::max(0, std::min(kDirectBig, atoi(e)));
+    if (const char* e = getenv("DFVM_AMG_DIRECT")) { direct = std::max(0, std::min(kDirectBig, atoi(e))); env_direct = true; }
     if (const char* e = getenv("DFVM_AMG_PERM")) perm = atoi(e);
     if (const char* e = getenv("DFVM_AMG_OMEGA")) omega = atof(e);
-    if (const char* e = getenv("DFVM_AMG_COARSE")) coarse = std::max(16, std::min(kDirectBig, atoi(e)));
+    if (const char* e = getenv("DFVM_AMG_COARSE")) { coarse = std::max(16, std::min(kDirectBig, atoi(e))); env_coarse = true; }
     if (const char* e = getenv("DFVM_AMG_SWEEPS")) sweeps = std::max(1, atoi(e));
     if (const char* e = getenv("DFVM_AMG_CYCLE")) wcycle = (e[0] == 'W' || e[0] == 'w');
     if (const char* e = getenv("DFVM_AMG_WMAX")) wmax = std::max(0, atoi(e));
@@ -297,7 +312,8 @@ struct AmgH {
   AmgParams prm;
   Prof* prof = nullptr;             // per-kernel profile of the caller (may be null)
   AmgLevelDev<P> L[kMaxLevels];
-  P* ainv = nullptr;                // dense inverse of the coarsest matrix (column-major n x n), or NULL
+  P* ainv = nullptr;                // dense inverse of the coarsest matrix (row-major n x ainv_ld), or NULL
+  int ainv_ld = 0;                  // its row stride (n; rounded up to 4 for the blocked fp32 path)
   P* gj_buf = nullptr;              // pivot row / column of the multi-launch Gauss-Jordan
   // several ranks: levels 0..ld are distributed (owned aggregates of owned
   // rows, ghost aggregates of the neighbours, a halo per level); level ld+1
@@ -576,7 +592,10 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
               H[k].n, (long long)H[k].ms_ptr.back(), H[k].rp[H[k].n], (double)H[k].rp[H[k].n] / std::max(1, H[k].n),
               100.0 * (1.0 - (double)H[k].rp[H[k].n] / std::max<double>(1.0, (double)H[k].ms_ptr.back())));
   const int nc = A->L[lev].n;
-  if (lev > 0 && nc <= A->prm.direct && (st = A->zalloc(&A->ainv, (size_t)nc * nc))) return st;
+  if (lev > 0 && nc <= A->prm.direct) {
+    A->ainv_ld = (nc > kDirectMax && std::is_same<P, float>::value) ? (nc + 3) / 4 * 4 : nc;
+    if ((st = A->zalloc(&A->ainv, (size_t)nc * A->ainv_ld))) return st;
+  }
   return DFVM_OK;
 }
 
@@ -905,7 +924,10 @@ static dfvm_status build_dist(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A, cud
   if ((st = coarsen_serial(A, H, lev))) return st;
   A->nlev = lev + 1;
   const int ncs = A->L[lev].n;
-  if (lev > lg - 1 && ncs <= A->prm.direct && (st = A->zalloc(&A->ainv, (size_t)ncs * ncs))) return st;
+  if (lev > lg - 1 && ncs <= A->prm.direct) {
+    A->ainv_ld = (ncs > kDirectMax && std::is_same<P, float>::value) ? (ncs + 3) / 4 * 4 : ncs;
+    if ((st = A->zalloc(&A->ainv, (size_t)ncs * A->ainv_ld))) return st;
+  }
   if (getenv("DFVM_AMG_VERBOSE"))
     for (int k = 0; k <= lev; ++k)
       fprintf(stderr, "[amg r%d] level %d: rows %d + %d ghosts, entries %d + %d to ghosts%s\n", Pt.rank, k, H[k].n,
@@ -946,9 +968,11 @@ dfvm_status amg_create(dfvm_mesh* m, const DevMesh<T>& M, bool fp32, Amg<T>** ou
   const bool dist = m->part.P > 1;
   if (fp32 && !std::is_same<T, float>::value) {
     A->lo = new AmgH<float>();
+    A->lo->prm.fp32_defaults();
     st = dist ? build_dist<float, T>(m, M, A->lo, s) : build<float, T>(m, M, A->lo);
   } else {
     A->same = new AmgH<T>();
+    if (std::is_same<T, float>::value) A->same->prm.fp32_defaults();
     st = dist ? build_dist<T, T>(m, M, A->same, s) : build<T, T>(m, M, A->same);
   }
   if (st) { delete A; return st; }
@@ -1391,38 +1415,40 @@ __global__ void k_gj_update(int n, int k, P* __restrict__ A, const P* __restrict
 constexpr int kBlk = 64;
 constexpr int kTM = 128, kTN = 128;   // update tile
 template <class P>
-__global__ void k_dense_rows_sym(int n, SellView S, const P* __restrict__ coef, const P* __restrict__ diag,
+__global__ void k_dense_rows_sym(int n, int ld, SellView S, const P* __restrict__ coef, const P* __restrict__ diag,
                                  P* __restrict__ A) {
   PDL_ENTRY();
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
     const int i = slot_row(S, q);
-    A[(size_t)i * n + i] = diag[i];
+    A[(size_t)i * ld + i] = diag[i];
     const int sl = q >> 5, lane = q & 31;
     for (int j = 0; j < S.ms_len[sl]; ++j) {
       const int p = S.ms_ptr[sl] + 32 * j + lane;
       const int c = S.mnb[p];
-      if (c < i) { A[(size_t)i * n + c] += coef[p]; A[(size_t)c * n + i] += coef[p]; }
+      if (c < i) { A[(size_t)i * ld + c] += coef[p]; A[(size_t)c * ld + i] += coef[p]; }
     }
   }
 }
 // S = A_KK^-1 by the sweep operator in shared memory (one CTA)
 template <class P>
-__global__ void __launch_bounds__(256) k_blk_inv(int n, int k0, int kb, const P* __restrict__ A, P* __restrict__ Sb) {
+__global__ void __launch_bounds__(256) k_blk_inv(int n, int ld, int k0, int kb, const P* __restrict__ A, P* __restrict__ Sb) {
   PDL_ENTRY();
   __shared__ P a[kBlk][kBlk + 1];
   __shared__ P ck[kBlk];
   for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
     const int r = e / kb, c = e - r * kb;
-    a[r][c] = A[(size_t)(k0 + r) * n + k0 + c];
+    a[r][c] = A[(size_t)(k0 + r) * ld + k0 + c];
   }
   __syncthreads();
   for (int k = 0; k < kb; ++k) {
     for (int j = threadIdx.x; j < kb; j += blockDim.x) ck[j] = a[j][k];
     __syncthreads();
     const P rd = P(1) / ck[k];
-    for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
-      const int r = e / kb, c = e - r * kb;
-      if (r != k && c != k) a[r][c] -= ck[r] * rd * ck[c];
+    // the full kBlk x kBlk square with constant shifts (no runtime division)
+#pragma unroll 4
+    for (int e = threadIdx.x; e < kBlk * kBlk; e += 256) {
+      const int r = e / kBlk, c = e % kBlk;
+      if (r < kb && c < kb && r != k && c != k) a[r][c] -= ck[r] * rd * ck[c];
     }
     __syncthreads();
     for (int j = threadIdx.x; j < kb; j += blockDim.x) {
@@ -1439,7 +1465,7 @@ __global__ void __launch_bounds__(256) k_blk_inv(int n, int k0, int kb, const P*
 }
 // Pb[i][c] = sum_t A[i][k0 + t] S[t][c]  (4 rows per CTA)
 template <class P>
-__global__ void __launch_bounds__(256) k_blk_panel(int n, int k0, int kb, const P* __restrict__ A,
+__global__ void __launch_bounds__(256) k_blk_panel(int n, int ld, int k0, int kb, const P* __restrict__ A,
                                                    const P* __restrict__ Sb, P* __restrict__ Pb) {
   PDL_ENTRY();
   __shared__ P s[kBlk][kBlk + 1];
@@ -1449,7 +1475,7 @@ __global__ void __launch_bounds__(256) k_blk_panel(int n, int k0, int kb, const 
     __syncthreads();
     for (int e = threadIdx.x; e < 4 * kb; e += blockDim.x) {
       const int r = e / kb, t = e - r * kb;
-      ar[r][t] = (i0 + r < n) ? A[(size_t)(i0 + r) * n + k0 + t] : P(0);
+      ar[r][t] = (i0 + r < n) ? A[(size_t)(i0 + r) * ld + k0 + t] : P(0);
     }
     __syncthreads();
     const int r = threadIdx.x / kBlk, c = threadIdx.x % kBlk;
@@ -1462,20 +1488,21 @@ __global__ void __launch_bounds__(256) k_blk_panel(int n, int k0, int kb, const 
 }
 // A_ij -= sum_t Pb[i][t] A[k0 + t][j]  for i, j outside block K: 128 x 128
 // tile per CTA, 8 x 8 outputs per thread, both operands staged in shared memory
+constexpr int kSP = kTM + 4;   // padded shared-memory rows (16-byte aligned, 4-way store conflicts at most)
 template <class P>
-__global__ void __launch_bounds__(256) k_blk_update(int n, int k0, int kb, P* __restrict__ A, const P* __restrict__ Pb) {
+__global__ void __launch_bounds__(256) k_blk_update(int n, int ld, int k0, int kb, P* __restrict__ A, const P* __restrict__ Pb) {
   PDL_ENTRY();
-  extern __shared__ unsigned char blk_smem[];
-  P* sP = reinterpret_cast<P*>(blk_smem);          // [kBlk][kTM]   Pb^T tile
-  P* sR = sP + kBlk * kTM;                          // [kBlk][kTN]   block-row tile
+  extern __shared__ __align__(16) unsigned char blk_smem[];
+  P* sP = reinterpret_cast<P*>(blk_smem);          // [kBlk][kSP]   Pb^T tile
+  P* sR = sP + kBlk * kSP;                          // [kBlk][kSP]   block-row tile
   const int i0 = blockIdx.y * kTM, j0 = blockIdx.x * kTN;
   for (int e = threadIdx.x; e < kTM * kBlk; e += blockDim.x) {
     const int i = e / kBlk, t = e - i * kBlk;
-    sP[t * kTM + i] = (i0 + i < n && t < kb) ? Pb[(size_t)(i0 + i) * kBlk + t] : P(0);
+    sP[t * kSP + i] = (i0 + i < n && t < kb) ? Pb[(size_t)(i0 + i) * kBlk + t] : P(0);
   }
   for (int e = threadIdx.x; e < kBlk * kTN; e += blockDim.x) {
     const int t = e / kTN, j = e - t * kTN;
-    sR[t * kTN + j] = (j0 + j < n && t < kb) ? A[(size_t)(k0 + t) * n + j0 + j] : P(0);
+    sR[t * kSP + j] = (j0 + j < n && t < kb) ? A[(size_t)(k0 + t) * ld + j0 + j] : P(0);
   }
   __syncthreads();
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -1484,12 +1511,15 @@ __global__ void __launch_bounds__(256) k_blk_update(int n, int k0, int kb, P* __
   for (int r = 0; r < 8; ++r)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[r][c] = P(0);
+  // thread (tx, ty) owns rows ty + 16 r and columns tx + 16 c: the 16 lanes
+  // of a half-warp read 16 consecutive values (conflict free), two row
+  // values per warp are broadcasts, and the output stores are coalesced
   for (int t = 0; t < kb; ++t) {
     P a[8], b[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) a[r] = sP[t * kTM + ty * 8 + r];
+    for (int r = 0; r < 8; ++r) a[r] = sP[t * kSP + ty + 16 * r];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) b[c] = sR[t * kTN + tx * 8 + c];
+    for (int c = 0; c < 8; ++c) b[c] = sR[t * kSP + tx + 16 * c];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -1497,27 +1527,27 @@ __global__ void __launch_bounds__(256) k_blk_update(int n, int k0, int kb, P* __
   }
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const int i = i0 + ty * 8 + r;
+    const int i = i0 + ty + 16 * r;
     if (i >= n || (i >= k0 && i < k0 + kb)) continue;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      const int j = j0 + tx * 8 + c;
-      if (j < n && !(j >= k0 && j < k0 + kb)) A[(size_t)i * n + j] -= acc[r][c];
+      const int j = j0 + tx + 16 * c;
+      if (j < n && !(j >= k0 && j < k0 + kb)) A[(size_t)i * ld + j] -= acc[r][c];
     }
   }
 }
 // block column / row K <- P (and P^T), A_KK <- -S
 template <class P>
-__global__ void k_blk_finish(int n, int k0, int kb, P* __restrict__ A, const P* __restrict__ Pb, const P* __restrict__ Sb) {
+__global__ void k_blk_finish(int n, int ld, int k0, int kb, P* __restrict__ A, const P* __restrict__ Pb, const P* __restrict__ Sb) {
   PDL_ENTRY();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * kb; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e / kb), c = (int)(e - (int64_t)i * kb);
     if (i >= k0 && i < k0 + kb) {
-      A[(size_t)i * n + k0 + c] = -Sb[(i - k0) * kBlk + c];
+      A[(size_t)i * ld + k0 + c] = -Sb[(i - k0) * kBlk + c];
     } else {
       const P v = Pb[(size_t)i * kBlk + c];
-      A[(size_t)i * n + k0 + c] = v;
-      A[(size_t)(k0 + c) * n + i] = v;
+      A[(size_t)i * ld + k0 + c] = v;
+      A[(size_t)(k0 + c) * ld + i] = v;
     }
   }
 }
@@ -1593,6 +1623,31 @@ constexpr size_t kSmemOptIn = 227 * 1024;
 // per row (row-major Ainv: coalesced across the lanes, 4 loads in flight per
 // lane), shuffle tree; as many blocks as the rows need (was one block: a
 // 144-row solve took ~8 us).  accum: x += that (W-cycle second visit).
+// large coarsest levels (row stride ld, a multiple of 4): 16-byte loads of
+// the inverse's rows, 4 in flight per lane
+template <class P>
+__global__ void __launch_bounds__(kThreads) k_amg_dense_v4(int n, int ld, const P* __restrict__ Ai,
+                                                           const P* __restrict__ b, P* __restrict__ x, int accum,
+                                                           const int* done) {
+  PDL_ENTRY();
+  if (*done) return;
+  const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+  const int n4 = n / 4;
+  for (int i = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); i < n; i += nw) {
+    const float4* row = reinterpret_cast<const float4*>(Ai + (size_t)i * ld);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    P acc = P(0);
+#pragma unroll 4
+    for (int j = lane; j < n4; j += 32) {
+      const float4 a = __ldg(&row[j]), v = __ldg(&b4[j]);
+      acc += a.x * v.x + a.y * v.y + a.z * v.z + a.w * v.w;
+    }
+    for (int j = 4 * n4 + lane; j < n; j += 32) acc += Ai[(size_t)i * ld + j] * b[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) x[i] = accum ? x[i] + acc : acc;
+  }
+}
 template <class P, class TB, class TO>
 __global__ void __launch_bounds__(kThreads) k_amg_dense(int n, const P* __restrict__ Ai, const TB* __restrict__ b,
                                                         TO* __restrict__ x, int accum, const int* done) {
@@ -1843,22 +1898,23 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
         return DFVM_E_CUDA;
       P* Pb = A->gj_buf;
       P* Sb = A->gj_buf + (size_t)n * kBlk;
-      const size_t usm = 2 * (size_t)kBlk * kTM * sizeof(P);
+      const size_t usm = 2 * (size_t)kBlk * kSP * sizeof(P);
       DFVM_CUDA(cudaFuncSetAttribute(k_blk_update<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
       PLAUNCH(pr, "k_amg_dense_inv", A->nlev - 1, 2 * pb * (double)n * n, s, {
-        k_dense_fill<P><<<grid_for((int64_t)n * n), kThreads, 0, s>>>(n, C.sv(), C.coef, C.diag, A->ainv);
-        k_dense_rows_sym<P><<<grid_for(n), kThreads, 0, s>>>(n, C.sv(), C.coef, C.diag, A->ainv);
+        const int ld = A->ainv_ld;
+        cudaMemsetAsync(A->ainv, 0, sizeof(P) * (size_t)n * ld, s);
+        k_dense_rows_sym<P><<<grid_for(n), kThreads, 0, s>>>(n, ld, C.sv(), C.coef, C.diag, A->ainv);
         const dim3 tg((n + kTN - 1) / kTN, (n + kTM - 1) / kTM);
         for (int k0 = 0; k0 < n; k0 += kBlk) {
           const int kb = std::min(kBlk, n - k0);
-          k_blk_inv<P><<<1, 256, 0, s>>>(n, k0, kb, A->ainv, Sb);
-          k_blk_panel<P><<<std::min(grid_for(n), (n + 3) / 4), 256, 0, s>>>(n, k0, kb, A->ainv, Sb, Pb);
-          k_blk_update<P><<<tg, 256, usm, s>>>(n, k0, kb, A->ainv, Pb);
-          k_blk_finish<P><<<grid_for((int64_t)n * kb), kThreads, 0, s>>>(n, k0, kb, A->ainv, Pb, Sb);
+          k_blk_inv<P><<<1, 256, 0, s>>>(n, ld, k0, kb, A->ainv, Sb);
+          k_blk_panel<P><<<std::min(kMaxBlocks, (n + 3) / 4), 256, 0, s>>>(n, ld, k0, kb, A->ainv, Sb, Pb);
+          k_blk_update<P><<<tg, 256, usm, s>>>(n, ld, k0, kb, A->ainv, Pb);
+          k_blk_finish<P><<<grid_for((int64_t)n * kb), kThreads, 0, s>>>(n, ld, k0, kb, A->ainv, Pb, Sb);
         }
-        k_negate<P><<<grid_for((int64_t)n * n), kThreads, 0, s>>>((int64_t)n * n, A->ainv);
+        k_negate<P><<<grid_for((int64_t)n * ld), kThreads, 0, s>>>((int64_t)n * ld, A->ainv);
       });
-      *nl += 3 + 4 * ((n + kBlk - 1) / kBlk);
+      *nl += 2 + 4 * ((n + kBlk - 1) / kBlk);
       DFVM_CUDA(cudaGetLastError());
       return DFVM_OK;
     }
@@ -1909,7 +1965,12 @@ static void coarsest(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaS
   AmgLevelDev<P>& F = A->L[l];
   Prof* pr = A->prof;
   const double pb = sizeof(P), n = F.n;
-  if (A->ainv) {
+  if (A->ainv && F.n > kDirectMax && std::is_same<P, float>::value) {
+    PLAUNCH(pr, "k_amg_dense", l, pb * n * n + (accum ? 3 : 2) * pb * n, s,
+            (k_amg_dense_v4<P><<<grid_for((int64_t)F.n * 32), kThreads, 0, s>>>(F.n, A->ainv_ld, A->ainv, b, x,
+                                                                                 accum ? 1 : 0, done)));
+    ++*nl;
+  } else if (A->ainv) {
     PLAUNCH(pr, "k_amg_dense", l, pb * n * n + (accum ? 3 : 2) * pb * n, s,
             (k_amg_dense<P, P, P><<<grid_for((int64_t)F.n * 32), kThreads, 0, s>>>(F.n, A->ainv, b, x, accum ? 1 : 0,
                                                                                     done)));

@@ -232,10 +232,18 @@ __global__ void __launch_bounds__(kThreads) k_apply(DevMesh<T> M, const T* __res
   }
 }
 
+// rAU = V / a_P alone (the AMG side stream's pressure matrix, ahead of the
+// momentum solve); k_HbyA then leaves rAU alone (write_rau = 0)
+template <class T>
+__global__ void k_rAU(int n, const T* __restrict__ vol, const T* __restrict__ udiag, T* __restrict__ rAU) {
+  PDL_ENTRY();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) rAU[i] = vol[i] / udiag[i];
+}
+
 // H = b - sum_nb a U_nb; rAU = V / a_P; HbyA = H / a_P (eq:Ap_H P:333-335)
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_HbyA(DevMesh<T> M, const T* __restrict__ bU, const T* __restrict__ udiag,
-    const T* __restrict__ ucoef, const T* __restrict__ U, T* __restrict__ rAU, T* __restrict__ HbyA) {
+    const T* __restrict__ ucoef, const T* __restrict__ U, T* __restrict__ rAU, T* __restrict__ HbyA, int write_rau = 1) {
   PDL_ENTRY();
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
@@ -244,7 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_HbyA(DevMesh<T> M, const T* __rest
     sell_apply<T, 3>(M, s, lane, ucoef, U, acc);
     if (live) {
       const T d = udiag[row];
-      rAU[row] = M.vol[row] / d;
+      if (write_rau) rAU[row] = M.vol[row] / d;
 #pragma unroll
       for (int k = 0; k < 3; ++k) HbyA[3 * (int64_t)row + k] = (bU[3 * (int64_t)row + k] - acc[k]) / d;
     }
@@ -291,10 +299,13 @@ __global__ void k_phiHbyA(DevMesh<T> M, const T* __restrict__ HbyA, const uint8_
 
 // pressure coefficients (eq:pressure_poisson LHS; A-8): pcoef = -c_f,
 // pdiag = sum c_f + sum c_b, prhs0 = -D(phiHbyA) + sum c_b p_b, gauge (A-12)
+// mode: bit 0 writes the matrix (pcoef, pdiag), bit 1 the right-hand side
+// prhs0 (the matrix part alone runs ahead of the momentum solve on the AMG
+// side stream, the right-hand side in the corrector)
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_pcoef(DevMesh<T> M, const T* __restrict__ rAU,
     const T* __restrict__ phiHbyA, const uint8_t* __restrict__ bkp, const T* __restrict__ bvp, int ref_row,
-    T p_ref, T* __restrict__ pcoef, T* __restrict__ pdiag, T* __restrict__ prhs0) {
+    T p_ref, T* __restrict__ pcoef, T* __restrict__ pdiag, T* __restrict__ prhs0, int mode = 3) {
   PDL_ENTRY();
   SLICE_LOOP(M) {
     const int row = s * 32 + lane;
@@ -314,23 +325,24 @@ __global__ void __launch_bounds__(kThreads) k_pcoef(DevMesh<T> M, const T* __res
         const T d = ld4(&M.fcor[f]).w;
         const T rn = rAU[en.y];
         const T cf = (w * (own ? ra : rn) + (T(1) - w) * (own ? rn : ra)) * d;
-        pcoef[mbase + 32 * (mj++)] = -cf;
+        if (mode & 1) pcoef[mbase + 32 * mj] = -cf;
+        ++mj;
         diag += cf;
-        rhs -= own ? phiHbyA[f] : -phiHbyA[f];
+        if (mode & 2) rhs -= own ? phiHbyA[f] : -phiHbyA[f];
       } else if (en.y == -1) {
         const int b = en.x;
-        rhs -= phiHbyA[M.F + b];
+        if (mode & 2) rhs -= phiHbyA[M.F + b];
         if (bkp[b] == 0) {
           const T cb = ra * ld4(&M.bgeo[b]).w;
           diag += cb;
-          rhs += cb * bvp[b];
+          if (mode & 2) rhs += cb * bvp[b];
         }
       }
     }
     if (live) {
       if (row == ref_row) { rhs += diag * p_ref; diag = diag + diag; }
-      pdiag[row] = diag;
-      prhs0[row] = rhs;
+      if (mode & 1) pdiag[row] = diag;
+      if (mode & 2) prhs0[row] = rhs;
     }
   }
 }
@@ -1018,6 +1030,13 @@ struct SolverT : SolverBase {
   V4<T>* fdN = nullptr;
   Amg<T>* amg = nullptr;        // pressure preconditioner (p_precond 1 / 2), built lazily
   bool amg_dirty = true;        // pressure matrix changed since the last Galerkin update
+  // AMG side stream: the step's pressure matrix (rAU -> pcoef, pdiag) and
+  // the hierarchy values are computed there while the momentum BiCGStab
+  // runs on the caller's stream (one rank, no profiling); the first pressure
+  // solve of the step waits for side_done
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_start = nullptr, side_done = nullptr;
+  bool side_pending = false;
   T* kz = nullptr;              // preconditioned residual z = M^-1 r
   WKDev* d_wk = nullptr;
   WKDev* h_wk = nullptr;     // pinned
@@ -1038,6 +1057,9 @@ struct SolverT : SolverBase {
   T* Uold = nullptr;     // start-of-step U and phi (ddtCorr, A-42; allocated on first use)
   T* phiold = nullptr;
   ~SolverT() override {
+    if (side_start) cudaEventDestroy(side_start);
+    if (side_done) cudaEventDestroy(side_done);
+    if (side) cudaStreamDestroy(side);
     cudaDeviceSynchronize();
     for (auto& g : loops) cudaGraphExecDestroy(g.exec);
     if (h_slots) cudaFreeHost(h_slots);
@@ -1770,12 +1792,46 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
     DFVM_CUDA(cudaMemcpyAsync(X.Uold, U, 3 * (size_t)M.n_cells * sizeof(T), cudaMemcpyDeviceToDevice, st));
     DFVM_CUDA(cudaMemcpyAsync(X.phiold, phi, (size_t)M.F * sizeof(T), cudaMemcpyDeviceToDevice, st));
   }
+  // 1b. DFVM_AMG_OVERLAP=1: the step's pressure matrix and AMG values on a
+  // low-priority side stream, overlapping the predictor.  Default off:
+  // measured on C5 round 2 at 315.5 / 317.1 ms/step against 314.0 / 315.2
+  // in the first corrector (profiles/r02_sweep_r2s_overlap.jsonl) — the
+  // predictor's one-wave kernels leave the side stream no room until they
+  // drain, and the refresh's memory-bound kernels then compete with it
+  X.side_pending = false;
+  const bool overlap = X.amg && S->m->part.P == 1 && !pr && !S->timing && st != nullptr && [] {
+    const char* e = getenv("DFVM_AMG_OVERLAP");
+    return e && atoi(e) == 1;
+  }();
+  if (overlap) {
+    if (!X.side) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);   // lo: the lowest priority (greatest value)
+      DFVM_CUDA(cudaStreamCreateWithPriority(&X.side, cudaStreamNonBlocking, lo));
+      DFVM_CUDA(cudaEventCreateWithFlags(&X.side_start, cudaEventDisableTiming));
+      DFVM_CUDA(cudaEventCreateWithFlags(&X.side_done, cudaEventDisableTiming));
+    }
+    DFVM_CUDA(cudaEventRecord(X.side_start, st));
+    DFVM_CUDA(cudaStreamWaitEvent(X.side, X.side_start, 0));
+    k_rAU<T><<<grid_for(M.n_own), kThreads, 0, X.side>>>(M.n_own, M.vol, X.udiag, X.rAU);
+    k_pcoef<T><<<gs, kThreads, 0, X.side>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
+                                            (T)o.p_ref_value, X.pcoef, X.pdiag, X.prhs0, 1);
+    S->n_launch += 2;
+    if ((s2 = amg_update<T>(X.amg, X.pcoef, X.pdiag, X.side, &S->n_launch, nullptr))) return s2;
+    DFVM_CUDA(cudaEventRecord(X.side_done, X.side));
+    X.amg_dirty = false;
+    X.side_pending = true;
+  }
   // 2. predictor
   dfvm_status res = run_bicgstab<T, 3>(S, X, X.rhsU, U, o.U_tol, o.U_rel_tol, o.U_maxit, R->U, st);
   if (res != DFVM_OK && res != DFVM_E_NOT_CONVERGED) return res;   // breakdown, CUDA / NCCL errors
   const int n_wk = (int)S->wk.size();
   int np = 0;
   for (int corr = 1; corr <= o.n_corr; ++corr) {
+    if (X.side_pending) {   // rAU, the pressure matrix and the hierarchy from the side stream
+      DFVM_CUDA(cudaStreamWaitEvent(st, X.side_done, 0));
+      X.side_pending = false;
+    }
     // 3.1 Windkessel
     if (n_wk) {
       PLAUNCH(pr, "k_windkessel", -1, 0, st,
@@ -1792,7 +1848,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
     // 3.2 rAU, HbyA
     if ((s2 = halo_exchange(S->m, U, 3, st))) return s2;
     PLAUNCH(pr, "k_HbyA", -1, 4 * N + Z * (4 + v) + 12 * v * N, st,
-            (k_HbyA<T><<<gs, kThreads, 0, st>>>(M, X.bU, X.udiag, X.ucoef, U, X.rAU, X.HbyA)));
+            (k_HbyA<T><<<gs, kThreads, 0, st>>>(M, X.bU, X.udiag, X.ucoef, U, X.rAU, X.HbyA, overlap ? 0 : 1)));
     S->n_launch++;
     if ((s2 = halo_exchange(S->m, X.HbyA, 3, st)) || (s2 = halo_exchange(S->m, X.rAU, 1, st))) return s2;
     // 3.3 phiHbyA
@@ -1803,13 +1859,14 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
     // 3.4 pressure coefficients
     PLAUNCH(pr, "k_pcoef", -1, 3 * v * N + (16 + 5 * v) * F + (9 + 3 * v) * Bf, st,
             (k_pcoef<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
-                                                 (T)o.p_ref_value, X.pcoef, X.pdiag, X.prhs0)));
+                                                 (T)o.p_ref_value, X.pcoef, X.pdiag, X.prhs0, overlap ? 2 : 3)));
+
     // The pressure matrix depends on rAU = V / a_P only (the momentum
     // diagonal of this step's assembly), so it is the same in every corrector
     // of the step: the AMG hierarchy values (Galerkin products, l1
     // diagonals, coarsest inverse) are refreshed once per step, not per
     // corrector (the right-hand side prhs0 changes with phiHbyA).
-    if (corr == 1) X.amg_dirty = true;
+    if (corr == 1 && !overlap) X.amg_dirty = true;
     S->n_launch += 2;
     // 3.5 non-orthogonal loop
     for (int io = 0; io <= o.n_nonorth; ++io) {
