@@ -1076,7 +1076,7 @@ __device__ __forceinline__ T row_part(const SellView& S, int q, int sub, bool li
     }
     for (; j < len; ++j) acc += __ldg(&coef[base + 32 * j]) * nb(__ldg(&S.mnb[base + 32 * j]));
     return acc;
-  }
+  } else {
   for (int j = sub; j < len; j += 4 * G) {
     T a[4], v[4];
     int c[4];
@@ -1093,6 +1093,7 @@ __device__ __forceinline__ T row_part(const SellView& S, int q, int sub, bool li
       if (c[u] >= 0) acc += a[u] * v[u];
   }
   return acc;
+  }
 }
 template <int G, class T>
 __device__ __forceinline__ T group_sum(T v) {
@@ -1430,8 +1431,10 @@ __global__ void k_dense_rows_sym(int n, int ld, SellView S, const P* __restrict_
   }
 }
 // S = A_KK^-1 by the sweep operator in shared memory (one CTA)
+// (1024 threads: 4 entries per thread per pivot; 256 threads took 57 us per
+// 64-pivot block on C5, a third of each block step)
 template <class P>
-__global__ void __launch_bounds__(256) k_blk_inv(int n, int ld, int k0, int kb, const P* __restrict__ A, P* __restrict__ Sb) {
+__global__ void __launch_bounds__(1024) k_blk_inv(int n, int ld, int k0, int kb, const P* __restrict__ A, P* __restrict__ Sb) {
   PDL_ENTRY();
   __shared__ P a[kBlk][kBlk + 1];
   __shared__ P ck[kBlk];
@@ -1445,8 +1448,8 @@ __global__ void __launch_bounds__(256) k_blk_inv(int n, int ld, int k0, int kb, 
     __syncthreads();
     const P rd = P(1) / ck[k];
     // the full kBlk x kBlk square with constant shifts (no runtime division)
-#pragma unroll 4
-    for (int e = threadIdx.x; e < kBlk * kBlk; e += 256) {
+#pragma unroll
+    for (int e = threadIdx.x; e < kBlk * kBlk; e += 1024) {
       const int r = e / kBlk, c = e % kBlk;
       if (r < kb && c < kb && r != k && c != k) a[r][c] -= ck[r] * rd * ck[c];
     }
@@ -1555,6 +1558,160 @@ template <class P>
 __global__ void k_negate(int64_t n, P* __restrict__ A) {
   PDL_ENTRY();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) A[e] = -A[e];
+}
+
+// ---- lower-triangle form of the blocked sweep (the default): only the
+// lower triangle (i >= j) is kept valid; the panel kernel also saves the old
+// block column Q = A_:K, so the rank update A_ij -= P_i Q_j^T reads two n x kb
+// buffers (both coalesced) and touches only tiles on or below the diagonal —
+// half the flops of the full form.  The result is mirrored (and negated) at
+// the end.
+__device__ __forceinline__ size_t lo_at(int i, int j, int ld) {
+  return i >= j ? (size_t)i * ld + j : (size_t)j * ld + i;
+}
+template <class P>
+__global__ void k_dense_rows_lower(int n, int ld, SellView S, const P* __restrict__ coef, const P* __restrict__ diag,
+                                   P* __restrict__ A) {
+  PDL_ENTRY();
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int i = slot_row(S, q);
+    A[(size_t)i * ld + i] = diag[i];
+    const int sl = q >> 5, lane = q & 31;
+    for (int j = 0; j < S.ms_len[sl]; ++j) {
+      const int p = S.ms_ptr[sl] + 32 * j + lane;
+      const int c = S.mnb[p];
+      if (c < i) A[(size_t)i * ld + c] += coef[p];
+    }
+  }
+}
+template <class P>
+__global__ void __launch_bounds__(1024) k_blk_inv_lo(int n, int ld, int k0, int kb, const P* __restrict__ A,
+                                                     P* __restrict__ Sb) {
+  PDL_ENTRY();
+  __shared__ P a[kBlk][kBlk + 1];
+  __shared__ P ck[kBlk];
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int r = e / kb, c = e - r * kb;
+    a[r][c] = A[lo_at(k0 + r, k0 + c, ld)];
+  }
+  __syncthreads();
+  for (int k = 0; k < kb; ++k) {
+    for (int j = threadIdx.x; j < kb; j += blockDim.x) ck[j] = a[j][k];
+    __syncthreads();
+    const P rd = P(1) / ck[k];
+#pragma unroll
+    for (int e = threadIdx.x; e < kBlk * kBlk; e += 1024) {
+      const int r = e / kBlk, c = e % kBlk;
+      if (r < kb && c < kb && r != k && c != k) a[r][c] -= ck[r] * rd * ck[c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < kb; j += blockDim.x) {
+      const P v = (j == k) ? -rd : ck[j] * rd;
+      a[j][k] = v;
+      a[k][j] = v;
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) {
+    const int r = e / kb, c = e - r * kb;
+    Sb[r * kBlk + c] = -a[r][c];
+  }
+}
+// Qb[i][t] = old A_{i, k0+t} (through the lower triangle), Pb[i][c] = Qb[i] S[:, c]
+template <class P>
+__global__ void __launch_bounds__(256) k_blk_panel_lo(int n, int ld, int k0, int kb, const P* __restrict__ A,
+                                                      const P* __restrict__ Sb, P* __restrict__ Pb, P* __restrict__ Qb) {
+  PDL_ENTRY();
+  __shared__ P s[kBlk][kBlk + 1];
+  __shared__ P ar[4][kBlk];
+  for (int e = threadIdx.x; e < kb * kb; e += blockDim.x) s[e / kb][e % kb] = Sb[(e / kb) * kBlk + e % kb];
+  for (int i0 = blockIdx.x * 4; i0 < n; i0 += gridDim.x * 4) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 4 * kb; e += blockDim.x) {
+      const int r = e / kb, t = e - r * kb;
+      const P v = (i0 + r < n) ? A[lo_at(i0 + r, k0 + t, ld)] : P(0);
+      ar[r][t] = v;
+      if (i0 + r < n) Qb[(size_t)(i0 + r) * kBlk + t] = v;
+    }
+    __syncthreads();
+    const int r = threadIdx.x / kBlk, c = threadIdx.x % kBlk;
+    if (i0 + r < n && c < kb) {
+      P acc = P(0);
+      for (int t = 0; t < kb; ++t) acc += ar[r][t] * s[t][c];
+      Pb[(size_t)(i0 + r) * kBlk + c] = acc;
+    }
+  }
+}
+// A_ij -= sum_t Pb[i][t] Qb[j][t] for i >= j outside block K (tiles above the
+// diagonal return at once)
+template <class P>
+__global__ void __launch_bounds__(256) k_blk_update_lo(int n, int ld, int k0, int kb, P* __restrict__ A,
+                                                       const P* __restrict__ Pb, const P* __restrict__ Qb) {
+  PDL_ENTRY();
+  const int i0 = blockIdx.y * kTM, j0 = blockIdx.x * kTN;
+  if (j0 > i0 + kTM - 1) return;
+  extern __shared__ __align__(16) unsigned char blk_smem[];
+  P* sP = reinterpret_cast<P*>(blk_smem);          // [kBlk][kSP]   Pb^T tile
+  P* sR = sP + kBlk * kSP;                          // [kBlk][kSP]   Qb^T tile
+  for (int e = threadIdx.x; e < kTM * kBlk; e += blockDim.x) {
+    const int i = e / kBlk, t = e - i * kBlk;
+    sP[t * kSP + i] = (i0 + i < n && t < kb) ? Pb[(size_t)(i0 + i) * kBlk + t] : P(0);
+    sR[t * kSP + i] = (j0 + i < n && t < kb) ? Qb[(size_t)(j0 + i) * kBlk + t] : P(0);
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  P acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = P(0);
+  for (int t = 0; t < kb; ++t) {
+    P a[8], b[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = sP[t * kSP + ty + 16 * r];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) b[c] = sR[t * kSP + tx + 16 * c];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] += a[r] * b[c];
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + ty + 16 * r;
+    if (i >= n || (i >= k0 && i < k0 + kb)) continue;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int j = j0 + tx + 16 * c;
+      if (j <= i && !(j >= k0 && j < k0 + kb)) A[(size_t)i * ld + j] -= acc[r][c];
+    }
+  }
+}
+// new block column K (lower storage): A_{i,K} = P_i, A_KK = -S
+template <class P>
+__global__ void k_blk_finish_lo(int n, int ld, int k0, int kb, P* __restrict__ A, const P* __restrict__ Pb,
+                                const P* __restrict__ Sb) {
+  PDL_ENTRY();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * kb; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / kb), c = (int)(e - (int64_t)i * kb);
+    if (i >= k0 && i < k0 + kb) {
+      if (i - k0 >= c) A[(size_t)i * ld + k0 + c] = -Sb[(i - k0) * kBlk + c];
+    } else {
+      A[lo_at(i, k0 + c, ld)] = Pb[(size_t)i * kBlk + c];
+    }
+  }
+}
+// the inverse from the swept lower triangle: A_ij = A_ji = -(swept)_ij
+template <class P>
+__global__ void k_mirror_negate(int n, int ld, P* __restrict__ A) {
+  PDL_ENTRY();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e - (int64_t)i * n);
+    if (j > i) continue;
+    const P v = -A[(size_t)i * ld + j];
+    A[(size_t)i * ld + j] = v;
+    if (j < i) A[(size_t)j * ld + i] = v;
+  }
 }
 
 // Dense inverse of the (SPD) coarsest matrix in SHARED memory by the
@@ -1894,25 +2051,40 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
     if (C.n > kDirectMax && std::is_same<P, float>::value) {
       // blocked symmetric sweep (fp32): 4 launches per block of kBlk pivots
       const int n = C.n;
-      if (!A->gj_buf && (dev_alloc_n(&A->gj_buf, (size_t)n * kBlk + kBlk * kBlk, nullptr, true) != DFVM_OK))
+      const bool lower = [] { const char* e = getenv("DFVM_AMG_BLK"); return !(e && e[0] == 'f'); }();
+      if (!A->gj_buf && (dev_alloc_n(&A->gj_buf, 2 * (size_t)n * kBlk + kBlk * kBlk, nullptr, true) != DFVM_OK))
         return DFVM_E_CUDA;
       P* Pb = A->gj_buf;
       P* Sb = A->gj_buf + (size_t)n * kBlk;
       const size_t usm = 2 * (size_t)kBlk * kSP * sizeof(P);
       DFVM_CUDA(cudaFuncSetAttribute(k_blk_update<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
+      DFVM_CUDA(cudaFuncSetAttribute(k_blk_update_lo<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
       PLAUNCH(pr, "k_amg_dense_inv", A->nlev - 1, 2 * pb * (double)n * n, s, {
         const int ld = A->ainv_ld;
         cudaMemsetAsync(A->ainv, 0, sizeof(P) * (size_t)n * ld, s);
-        k_dense_rows_sym<P><<<grid_for(n), kThreads, 0, s>>>(n, ld, C.sv(), C.coef, C.diag, A->ainv);
         const dim3 tg((n + kTN - 1) / kTN, (n + kTM - 1) / kTM);
-        for (int k0 = 0; k0 < n; k0 += kBlk) {
-          const int kb = std::min(kBlk, n - k0);
-          k_blk_inv<P><<<1, 256, 0, s>>>(n, ld, k0, kb, A->ainv, Sb);
-          k_blk_panel<P><<<std::min(kMaxBlocks, (n + 3) / 4), 256, 0, s>>>(n, ld, k0, kb, A->ainv, Sb, Pb);
-          k_blk_update<P><<<tg, 256, usm, s>>>(n, ld, k0, kb, A->ainv, Pb);
-          k_blk_finish<P><<<grid_for((int64_t)n * kb), kThreads, 0, s>>>(n, ld, k0, kb, A->ainv, Pb, Sb);
+        if (lower) {
+          P* Qb = Pb + (size_t)n * kBlk + kBlk * kBlk;
+          k_dense_rows_lower<P><<<grid_for(n), kThreads, 0, s>>>(n, ld, C.sv(), C.coef, C.diag, A->ainv);
+          for (int k0 = 0; k0 < n; k0 += kBlk) {
+            const int kb = std::min(kBlk, n - k0);
+            k_blk_inv_lo<P><<<1, 1024, 0, s>>>(n, ld, k0, kb, A->ainv, Sb);
+            k_blk_panel_lo<P><<<std::min(kMaxBlocks, (n + 3) / 4), 256, 0, s>>>(n, ld, k0, kb, A->ainv, Sb, Pb, Qb);
+            k_blk_update_lo<P><<<tg, 256, usm, s>>>(n, ld, k0, kb, A->ainv, Pb, Qb);
+            k_blk_finish_lo<P><<<grid_for((int64_t)n * kb), kThreads, 0, s>>>(n, ld, k0, kb, A->ainv, Pb, Sb);
+          }
+          k_mirror_negate<P><<<grid_for((int64_t)n * n), kThreads, 0, s>>>(n, ld, A->ainv);
+        } else {
+          k_dense_rows_sym<P><<<grid_for(n), kThreads, 0, s>>>(n, ld, C.sv(), C.coef, C.diag, A->ainv);
+          for (int k0 = 0; k0 < n; k0 += kBlk) {
+            const int kb = std::min(kBlk, n - k0);
+            k_blk_inv<P><<<1, 1024, 0, s>>>(n, ld, k0, kb, A->ainv, Sb);
+            k_blk_panel<P><<<std::min(kMaxBlocks, (n + 3) / 4), 256, 0, s>>>(n, ld, k0, kb, A->ainv, Sb, Pb);
+            k_blk_update<P><<<tg, 256, usm, s>>>(n, ld, k0, kb, A->ainv, Pb);
+            k_blk_finish<P><<<grid_for((int64_t)n * kb), kThreads, 0, s>>>(n, ld, k0, kb, A->ainv, Pb, Sb);
+          }
+          k_negate<P><<<grid_for((int64_t)n * ld), kThreads, 0, s>>>((int64_t)n * ld, A->ainv);
         }
-        k_negate<P><<<grid_for((int64_t)n * ld), kThreads, 0, s>>>((int64_t)n * ld, A->ainv);
       });
       *nl += 2 + 4 * ((n + kBlk - 1) / kBlk);
       DFVM_CUDA(cudaGetLastError());
