@@ -46,6 +46,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cuda_bf16.h>
+
 #include "amg.h"
 #include "dev.cuh"
 #include "prof.h"
@@ -315,6 +317,7 @@ struct AmgH {
   P* ainv = nullptr;                // dense inverse of the coarsest matrix (row-major n x ainv_ld), or NULL
   int ainv_ld = 0;                  // its row stride (n; rounded up to 4 for the blocked fp32 path)
   P* gj_buf = nullptr;              // pivot row / column of the multi-launch Gauss-Jordan
+  __nv_bfloat16* ainv16 = nullptr;  // DFVM_AMG_INV16=1: bf16 copy of a large fp32 inverse (half the mat-vec bytes)
   // several ranks: levels 0..ld are distributed (owned aggregates of owned
   // rows, ghost aggregates of the neighbours, a halo per level); level ld+1
   // is the AGGLOMERATION of every rank's level-ld rows into one global
@@ -339,6 +342,7 @@ struct AmgH {
   int64_t bytes = 0;
   ~AmgH() {
     if (gj_buf) dev_free(gj_buf, nullptr);
+    if (ainv16) dev_free(ainv16, nullptr);
     for (void* p : allocs) dev_free(p, nullptr);
     for (auto& h : halos) { dev_free(h.d_send, nullptr); dev_free(h.d_send_idx, nullptr); }
   }
@@ -375,7 +379,11 @@ struct Amg {
 template <class P>
 static dfvm_status coarsen_serial(AmgH<P>* A, std::vector<HostLevel>& H, int& lev) {
   dfvm_status st;
-  while (H[lev].n > A->prm.coarse && lev + 1 < kMaxLevels) {
+  // (a level 0 above 256 rows is always coarsened once, so a mesh smaller
+  // than the fp32 bound still gets a two-level cycle with an exact coarse
+  // solve — C1's 400 cells: 7 PCG iterations against 11.6 with 32 l1-Jacobi
+  // sweeps on the single level)
+  while ((H[lev].n > A->prm.coarse || (lev == 0 && H[lev].n > 256)) && lev + 1 < kMaxLevels) {
     const HostLevel& F = H[lev];
     int nc = 0;
     std::vector<int> agg = aggregate(F, nc);
@@ -593,7 +601,7 @@ static dfvm_status build(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A) {
               100.0 * (1.0 - (double)H[k].rp[H[k].n] / std::max<double>(1.0, (double)H[k].ms_ptr.back())));
   const int nc = A->L[lev].n;
   if (lev > 0 && nc <= A->prm.direct) {
-    A->ainv_ld = (nc > kDirectMax && std::is_same<P, float>::value) ? (nc + 3) / 4 * 4 : nc;
+    A->ainv_ld = (nc > kDirectMax && std::is_same<P, float>::value) ? (nc + 7) / 8 * 8 : nc;
     if ((st = A->zalloc(&A->ainv, (size_t)nc * A->ainv_ld))) return st;
   }
   return DFVM_OK;
@@ -925,7 +933,7 @@ static dfvm_status build_dist(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A, cud
   A->nlev = lev + 1;
   const int ncs = A->L[lev].n;
   if (lev > lg - 1 && ncs <= A->prm.direct) {
-    A->ainv_ld = (ncs > kDirectMax && std::is_same<P, float>::value) ? (ncs + 3) / 4 * 4 : ncs;
+    A->ainv_ld = (ncs > kDirectMax && std::is_same<P, float>::value) ? (ncs + 7) / 8 * 8 : ncs;
     if ((st = A->zalloc(&A->ainv, (size_t)ncs * A->ainv_ld))) return st;
   }
   if (getenv("DFVM_AMG_VERBOSE"))
@@ -1805,6 +1813,39 @@ __global__ void __launch_bounds__(kThreads) k_amg_dense_v4(int n, int ld, const 
     if (lane == 0) x[i] = accum ? x[i] + acc : acc;
   }
 }
+// bf16 copy of the inverse and its mat-vec (16-byte loads = 8 entries, fp32 sums)
+__global__ void k_to_bf16(int64_t n, const float* __restrict__ a, __nv_bfloat16* __restrict__ o) {
+  PDL_ENTRY();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    o[e] = __float2bfloat16_rn(a[e]);
+}
+__global__ void __launch_bounds__(kThreads) k_amg_dense_bf16(int n, int ld, const __nv_bfloat16* __restrict__ Ai,
+                                                             const float* __restrict__ b, float* __restrict__ x,
+                                                             int accum, const int* done) {
+  PDL_ENTRY();
+  if (*done) return;
+  const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+  const int n8 = n / 8;
+  for (int i = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); i < n; i += nw) {
+    const uint4* row = reinterpret_cast<const uint4*>(Ai + (size_t)i * ld);
+    float acc = 0.f;
+#pragma unroll 4
+    for (int j = lane; j < n8; j += 32) {
+      const uint4 raw = __ldg(&row[j]);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(b) + 2 * j);
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(b) + 2 * j + 1);
+      const float2 a0 = __bfloat1622float2(h[0]), a1 = __bfloat1622float2(h[1]);
+      const float2 a2 = __bfloat1622float2(h[2]), a3 = __bfloat1622float2(h[3]);
+      acc += a0.x * b0.x + a0.y * b0.y + a1.x * b0.z + a1.y * b0.w + a2.x * b1.x + a2.y * b1.y + a3.x * b1.z +
+             a3.y * b1.w;
+    }
+    for (int j = 8 * n8 + lane; j < n; j += 32) acc += __bfloat162float(Ai[(size_t)i * ld + j]) * b[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) x[i] = accum ? x[i] + acc : acc;
+  }
+}
 template <class P, class TB, class TO>
 __global__ void __launch_bounds__(kThreads) k_amg_dense(int n, const P* __restrict__ Ai, const TB* __restrict__ b,
                                                         TO* __restrict__ x, int accum, const int* done) {
@@ -2052,6 +2093,11 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
       // blocked symmetric sweep (fp32): 4 launches per block of kBlk pivots
       const int n = C.n;
       const bool lower = [] { const char* e = getenv("DFVM_AMG_BLK"); return !(e && e[0] == 'f'); }();
+      const bool inv16 = [] { const char* e = getenv("DFVM_AMG_INV16"); return e && atoi(e) == 1; }() &&
+                         A->ainv_ld % 8 == 0;
+      if (inv16 && !A->ainv16 &&
+          dev_alloc_n(&A->ainv16, (size_t)n * A->ainv_ld, nullptr, true) != DFVM_OK)
+        return DFVM_E_CUDA;
       if (!A->gj_buf && (dev_alloc_n(&A->gj_buf, 2 * (size_t)n * kBlk + kBlk * kBlk, nullptr, true) != DFVM_OK))
         return DFVM_E_CUDA;
       P* Pb = A->gj_buf;
@@ -2084,6 +2130,10 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
             k_blk_finish<P><<<grid_for((int64_t)n * kb), kThreads, 0, s>>>(n, ld, k0, kb, A->ainv, Pb, Sb);
           }
           k_negate<P><<<grid_for((int64_t)n * ld), kThreads, 0, s>>>((int64_t)n * ld, A->ainv);
+        }
+        if (inv16) {
+          // ld is a multiple of 4; the bf16 rows need 16-byte alignment too: ld16 = ld rounded to 8
+          k_to_bf16<<<grid_for((int64_t)n * ld), kThreads, 0, s>>>((int64_t)n * ld, (const float*)A->ainv, A->ainv16);
         }
       });
       *nl += 2 + 4 * ((n + kBlk - 1) / kBlk);
@@ -2137,7 +2187,13 @@ static void coarsest(AmgH<P>* A, int l, const P* b, P* x, const int* done, cudaS
   AmgLevelDev<P>& F = A->L[l];
   Prof* pr = A->prof;
   const double pb = sizeof(P), n = F.n;
-  if (A->ainv && F.n > kDirectMax && std::is_same<P, float>::value) {
+  if (A->ainv16 && std::is_same<P, float>::value) {
+    PLAUNCH(pr, "k_amg_dense", l, 2 * n * n + (accum ? 3 : 2) * pb * n, s,
+            (k_amg_dense_bf16<<<grid_for((int64_t)F.n * 32), kThreads, 0, s>>>(F.n, A->ainv_ld, A->ainv16,
+                                                                              (const float*)b, (float*)x,
+                                                                              accum ? 1 : 0, done)));
+    ++*nl;
+  } else if (A->ainv && F.n > kDirectMax && std::is_same<P, float>::value) {
     PLAUNCH(pr, "k_amg_dense", l, pb * n * n + (accum ? 3 : 2) * pb * n, s,
             (k_amg_dense_v4<P><<<grid_for((int64_t)F.n * 32), kThreads, 0, s>>>(F.n, A->ainv_ld, A->ainv, b, x,
                                                                                  accum ? 1 : 0, done)));
