@@ -315,7 +315,8 @@ struct AmgH {
   Prof* prof = nullptr;             // per-kernel profile of the caller (may be null)
   AmgLevelDev<P> L[kMaxLevels];
   P* ainv = nullptr;                // dense inverse of the coarsest matrix (row-major n x ainv_ld), or NULL
-  int ainv_ld = 0;                  // its row stride (n; rounded up to 4 for the blocked fp32 path)
+  int ainv_ld = 0;                  // its row stride (n; rounded up to 8 for the blocked fp32 path)
+  int64_t inv_refreshes = 0;        // blocked inverse: updates seen (DFVM_AMG_INV_EVERY lags the refresh)
   P* gj_buf = nullptr;              // pivot row / column of the multi-launch Gauss-Jordan
   __nv_bfloat16* ainv16 = nullptr;  // DFVM_AMG_INV16=1: bf16 copy of a large fp32 inverse (half the mat-vec bytes)
   // several ranks: levels 0..ld are distributed (owned aggregates of owned
@@ -2089,6 +2090,15 @@ static dfvm_status update(AmgH<P>* A, const T* pcoef, const T* pdiag, cudaStream
   if (A->ainv) {
     const AmgLevelDev<P>& C = A->L[A->nlev - 1];
     const size_t sm = dense_inv_sym_smem<P>(C.n);
+    // DFVM_AMG_INV_EVERY=k (k > 1): the large coarsest inverse is refreshed on
+    // every k-th matrix update only (a lagged coarse solve; the Galerkin
+    // levels above it are always current, and the stale inverse is still an
+    // SPD coarse solve)
+    const int inv_every = [] { const char* e = getenv("DFVM_AMG_INV_EVERY"); return e ? std::max(1, atoi(e)) : 1; }();
+    if (C.n > kDirectMax && std::is_same<P, float>::value && (A->inv_refreshes++ % inv_every) != 0) {
+      DFVM_CUDA(cudaGetLastError());
+      return DFVM_OK;
+    }
     if (C.n > kDirectMax && std::is_same<P, float>::value) {
       // blocked symmetric sweep (fp32): 4 launches per block of kBlk pivots
       const int n = C.n;

@@ -531,3 +531,46 @@ def test_amg_large_coarsest_inverse(precond, monkeypatch):
         its.append((rg["it"], lv))
     assert its[1][1][-1] > 512, its          # the large-coarsest path ran
     assert its[1][0] <= its[0][0] + 1, its
+
+
+def test_amg_refresh_overlap_bitwise(monkeypatch):
+    # DFVM_AMG_OVERLAP=1 computes rAU, the pressure matrix and the AMG refresh
+    # on a side stream during the predictor: same inputs, same kernels, hence
+    # bitwise the fields and iteration counts of the in-corrector refresh
+    import ctypes
+    import torch
+    raw, mo, mg, bo, bg, kw = pipe_case(n=8, m_r=4, n_z=40)
+    U0, p0, phi0 = initial_state(mo)
+    s = torch.cuda.Stream()
+    sp = ctypes.c_void_p(s.cuda_stream)
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("DFVM_AMG_OVERLAP", v)
+        Sg = dfvm.Solver(mg, bg, p_precond="amg32", **kw, **TIGHT)
+        Ug, pg, phig = mg.field("cells", 3, U0, sp), mg.field("cells", 1, p0, sp), mg.field("flux", 1, phi0, sp)
+        reps = [Sg.step(Ug, pg, phig, sp) for _ in range(4)]
+        out.append((Ug.get(sp), pg.get(sp), phig.get(sp), [r["it"] for rep in reps for r in rep["p"]]))
+    assert out[0][3] == out[1][3]
+    for a, b in zip(out[0][:3], out[1][:3]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("env", [{"DFVM_AMG_INV16": "1"}, {"DFVM_AMG_INV_EVERY": "2"}])
+def test_amg_large_coarsest_variants(env, monkeypatch):
+    # bf16 copy of the blocked inverse / a refresh on every other update only:
+    # still an SPD coarse solve, the PISO fields converge to the oracle's
+    raw, mo, mg, bo, bg, kw = pipe_case(n=8, m_r=4, n_z=40)
+    monkeypatch.setenv("DFVM_AMG_COARSE", "2000")
+    monkeypatch.setenv("DFVM_AMG_DIRECT", "4000")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    U0, p0, phi0 = initial_state(mo)
+    So = oracle.Solver(mo, bo, **kw, **TIGHT)
+    Sg = dfvm.Solver(mg, bg, p_precond="amg32", **kw, **TIGHT)
+    U, p, phi = U0.copy(), p0.copy(), phi0.copy()
+    Ug, pg, phig = mg.field("cells", 3, U0), mg.field("cells", 1, p0), mg.field("flux", 1, phi0)
+    for _ in range(3):
+        So.step(U, p, phi)
+        Sg.step(Ug, pg, phig)
+    assert Sg.amg_levels()[-1] > 512
+    assert rel_l2(Ug.get(), U) <= 1e-8 and rel_l2(pg.get(), p) <= 1e-8 and rel_l2(phig.get(), phi) <= 1e-8
