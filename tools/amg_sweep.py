@@ -53,6 +53,8 @@ for line in open(cfgfile):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     its = [r["it"] for rep in reps for r in rep["p"]]
+    bits = [r["it"] for rep in reps for r in rep["U"]]
     print(json.dumps({"tag": parts[0], "ms_per_step": round(ms, 2), "pcg_its": float(np.mean(its)),
+                      "bicgstab_its": float(np.mean(bits)) if bits else None,
                       "levels": S.amg_levels(), "wall_s": round(time.time() - t0, 1)}), flush=True)
     del S, U, p, phi
