@@ -953,8 +953,10 @@ static dfvm_status build_dist(dfvm_mesh* m, const DevMesh<T>& M, AmgH<P>* A, cud
 // thread per row.  DFVM_AMG_GROUP=0: one thread per row everywhere.
 constexpr int64_t kGroupFill = 148 * 2048;
 static int group_for(int64_t n, double per_row, int gmax) {
+  // DFVM_AMG_GFILL: the thread count a level must reach (default kGroupFill)
+  const int64_t fill = [] { const char* e = getenv("DFVM_AMG_GFILL"); return e ? std::max<int64_t>(1, atoll(e)) : kGroupFill; }();
   int G = 1;
-  while (G < gmax && n * G < kGroupFill && G < per_row) G *= 2;
+  while (G < gmax && n * G < fill && G < per_row) G *= 2;
   return G;
 }
 template <class P>
