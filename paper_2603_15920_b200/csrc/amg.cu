@@ -1929,6 +1929,77 @@ __global__ void __launch_bounds__(kThreads) k_amg_csr(int nchunk, const int* __r
   }
 }
 
+// ---- software-pipelined one-thread-per-row residual / smoother (coarse
+// levels in natural slot order).  While row q's gathers are in flight the
+// thread already loads the next row's first entry batch (columns,
+// coefficients) and the row after that's slice metadata, so in steady state
+// a row costs one memory round trip (its gathers) plus its entries beyond
+// the first 4, instead of three dependent ones.  Same per-row sums in the
+// same order as row_part<1> (bitwise).
+// MODE 0: r = b - A x.  MODE 1: out = x + (b - A x) / d1 (accum: out += that)
+template <int MODE, class P>
+__global__ void __launch_bounds__(kThreads) k_amg_rowpf(int n, SellView S, const P* __restrict__ coef,
+    const P* __restrict__ diag, const P* __restrict__ il1, const P* __restrict__ x, const P* __restrict__ b,
+    P* __restrict__ out, int accum, const int* done) {
+  PDL_ENTRY();
+  if (*done) return;
+  const int st = gridDim.x * blockDim.x;
+  int q = blockIdx.x * blockDim.x + threadIdx.x;
+  auto meta = [&](int qq, int& ln, int& bs) {
+    if (qq < n) { ln = __ldg(&S.ms_len[qq >> 5]); bs = __ldg(&S.ms_ptr[qq >> 5]) + (qq & 31); }
+    else { ln = 0; bs = 0; }
+  };
+  auto batch = [&](int ln, int bs, P (&a)[4], int (&c)[4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = u < ln;
+      a[u] = ok ? __ldg(&coef[bs + 32 * u]) : P(0);
+      c[u] = ok ? __ldg(&S.mnb[bs + 32 * u]) : 0;
+    }
+  };
+  int len, base, len_n, base_n;
+  P a[4], a_n[4];
+  int c[4], c_n[4];
+  meta(q, len, base);
+  batch(len, base, a, c);
+  meta(q + st, len_n, base_n);
+  for (; q < n; q += st) {
+    P v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = x[c[u]];                 // this row's first gathers
+    batch(len_n, base_n, a_n, c_n);                             // next row's first batch
+    int len_nn, base_nn;
+    meta(q + 2 * st, len_nn, base_nn);                          // the row after's metadata
+    P acc = diag[q] * x[q];
+    const int j4 = len < 4 ? len : 4;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u < j4) acc += a[u] * v[u];
+    int j = 4;
+    for (; j + 4 <= len; j += 4) {
+      P aa[4], vv[4];
+      int cc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { aa[u] = __ldg(&coef[base + 32 * (j + u)]); cc[u] = __ldg(&S.mnb[base + 32 * (j + u)]); }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) vv[u] = x[cc[u]];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += aa[u] * vv[u];
+    }
+    for (; j < len; ++j) acc += __ldg(&coef[base + 32 * j]) * x[__ldg(&S.mnb[base + 32 * j])];
+    if (MODE == 0) {
+      out[q] = b[q] - acc;
+    } else {
+      const P z = x[q] + (b[q] - acc) * il1[q];
+      out[q] = accum ? out[q] + z : z;
+    }
+    len = len_n; base = base_n;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { a[u] = a_n[u]; c[u] = c_n[u]; }
+    len_n = len_nn; base_n = base_nn;
+  }
+}
+
 // ---- host launchers for the group-templated kernels (G in {1,2,4,...,32})
 #define AMG_G_SWITCH(G, CALL)                      \
   switch (G) {                                     \
@@ -1970,12 +2041,24 @@ static void launch_smooth(int G, int n, const SellView& S, const P* coef, const 
   AMG_G_SWITCH(G, (k_amg_smooth<kG, P, TB, TO><<<grid_group(n, kG), kThreads, 0, s>>>(n, S, coef, diag, il1, x, b,
                                                                                       out, accum, done)));
 }
+// DFVM_AMG_PF=1: the software-pipelined kernels on one-thread-per-row
+// coarse levels.  Default off: measured on C5 round 2 at 306.3 / 307.4
+// ms/step against 305.1 / 306.6 with the plain kernels
+// (profiles/r02_sweep_r2ee_pf.jsonl; 40 registers against 32 — 48 resident
+// warps per SM instead of 64 — cancel the deeper pipeline)
+static bool amg_pf() {
+  const char* e = getenv("DFVM_AMG_PF");
+  return e && atoi(e) == 1;
+}
 // a coarse level's residual / smoother: CSR-stream where the level has it
 template <class P>
 static void level_resid(const AmgLevelDev<P>& L, const P* x, const P* b, P* r, const int* done, cudaStream_t s) {
   if (L.n_chunk > 0 && L.G == 1)
     k_amg_csr<0, P><<<grid_for((int64_t)L.n_chunk * 32), kThreads, 0, s>>>(L.n_chunk, L.c_ptr, L.c_rp, L.c_col,
                                                                             L.c_coef, L.diag, L.il1, x, b, r, 0, done);
+  else if (L.G == 1 && !L.perm && amg_pf())
+    k_amg_rowpf<0, P><<<grid_rows(k_amg_rowpf<0, P>, L.n), kThreads, 0, s>>>(L.n, L.sv(), L.coef, L.diag, L.il1, x,
+                                                                             b, r, 0, done);
   else
     launch_resid<P, P>(L.G, L.n, L.sv(), L.coef, L.diag, x, b, r, done, s);
 }
@@ -1986,6 +2069,9 @@ static void level_smooth(const AmgLevelDev<P>& L, const P* x, const P* b, P* out
     k_amg_csr<1, P><<<grid_for((int64_t)L.n_chunk * 32), kThreads, 0, s>>>(L.n_chunk, L.c_ptr, L.c_rp, L.c_col,
                                                                             L.c_coef, L.diag, L.il1, x, b, out, accum,
                                                                             done);
+  else if (L.G == 1 && !L.perm && amg_pf())
+    k_amg_rowpf<1, P><<<grid_rows(k_amg_rowpf<1, P>, L.n), kThreads, 0, s>>>(L.n, L.sv(), L.coef, L.diag, L.il1, x,
+                                                                             b, out, accum, done);
   else
     launch_smooth<P, P, P>(L.G, L.n, L.sv(), L.coef, L.diag, L.il1, x, b, out, accum, done, s);
 }

@@ -437,7 +437,7 @@ def test_amg_kernel_variants_bitwise(precond, size, monkeypatch):
     sp = ctypes.c_void_p(s.cuda_stream)
     out = []
     for env in ({"DFVM_AMG_FUSED_FROM": "1"}, {"DFVM_AMG_FUSED_FROM": "3"}, {"DFVM_AMG_FUSED_FROM": "9"},
-                {"DFVM_AMG_FUSED_FROM": "3", "DFVM_AMG_CSR": "0"}):
+                {"DFVM_AMG_FUSED_FROM": "3", "DFVM_AMG_CSR": "0"}, {"DFVM_AMG_CSR": "0", "DFVM_AMG_PF": "1"}):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         Sg = mk()
