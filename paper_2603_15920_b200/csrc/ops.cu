@@ -381,9 +381,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_lap(DevMesh<T> M, const T* _
 // ------------------------------------------------------------ launchers
 template <class T>
 void launch_interpolate(const DevMesh<T>& M, const T* x, int nc, const uint8_t* bk, const T* bv, T* xf, cudaStream_t s) {
-  const int g = grid_for((int64_t)M.F + M.B + M.E);
-  if (nc == 1) k_interp<T, 1><<<g, kThreads, 0, s>>>(M, x, bk, bv, xf);
-  else k_interp<T, 3><<<g, kThreads, 0, s>>>(M, x, bk, bv, xf);
+  // one wave of resident blocks (the 3-vector variant holds 96 registers):
+  // a second wave would revisit the cells the first one left in L2 long ago
+  const int64_t nf = (int64_t)M.F + M.B + M.E;
+  if (nc == 1) k_interp<T, 1><<<grid_rows(k_interp<T, 1>, nf), kThreads, 0, s>>>(M, x, bk, bv, xf);
+  else k_interp<T, 3><<<grid_rows(k_interp<T, 3>, nf), kThreads, 0, s>>>(M, x, bk, bv, xf);
   count_launch();
 }
 // Batch depth KB and minimum resident blocks MINB (register cap 64), measured

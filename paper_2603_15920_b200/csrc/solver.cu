@@ -199,13 +199,14 @@ __global__ void __launch_bounds__(kThreads) k_transport_assemble(DevMesh<T> M, c
 }
 
 template <class T, int NC>
-static void launch_transport_assemble(int gs, cudaStream_t st, DevMesh<T> M, const T* U, const T* phi, const T* gU,
+static void launch_transport_assemble(int n_slices, cudaStream_t st, DevMesh<T> M, const T* U, const T* phi, const T* gU,
                                       const T* gp, const uint8_t* bk, const T* bv, T nu, T rdt, T theta, int conv,
                                       int kcorr, const V4<T>* fdO, const V4<T>* fdN, T* udiag, T* bU, T* rhsU, T* ucoef,
                                       T* ucoefT) {
   const bool ho = conv >= 2, ex = theta != T(1);
 #define KTA(H, E)                                                                                                   \
-  k_transport_assemble<T, NC, H, E><<<gs, kThreads, 0, st>>>(M, U, phi, gU, gp, bk, bv, nu, rdt, theta, conv, kcorr, \
+  k_transport_assemble<T, NC, H, E><<<grid_slices(k_transport_assemble<T, NC, H, E>, n_slices), kThreads, 0, st>>>( \
+      M, U, phi, gU, gp, bk, bv, nu, rdt, theta, conv, kcorr, \
                                                               fdO, fdN, udiag, bU, rhsU, ucoef, ucoefT)
   if (ho && ex) KTA(true, true);
   else if (ho) KTA(true, false);
@@ -1748,7 +1749,7 @@ static dfvm_status assemble(dfvm_solver* S, SolverT<T>& X, const T* U, const T* 
   S->n_launch++;
   if ((s2 = halo_exchange(S->m, X.gU, 9, st))) return s2;
   PLAUNCH(pr, "k_transport_assemble", -1, 23 * v * N + (16 + 10 * v) * F + (9 + 8 * v) * Bf, st,
-          launch_transport_assemble<T, 3>(gs, st, M, U, phi, X.gU, X.gp, b->d_kind[0], (const T*)b->d_val[0],
+          launch_transport_assemble<T, 3>(M.n_slices, st, M, U, phi, X.gU, X.gp, b->d_kind[0], (const T*)b->d_val[0],
                                           (T)S->o.nu, (T)(1.0 / S->o.dt), (T)theta_of(S->o), S->o.convection,
                                           S->kcorr, X.fdO, X.fdN, X.udiag, X.bU, X.rhsU, X.ucoef, X.ucoefT));
   S->n_launch++;
@@ -1814,7 +1815,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
     DFVM_CUDA(cudaEventRecord(X.side_start, st));
     DFVM_CUDA(cudaStreamWaitEvent(X.side, X.side_start, 0));
     k_rAU<T><<<grid_for(M.n_own), kThreads, 0, X.side>>>(M.n_own, M.vol, X.udiag, X.rAU);
-    k_pcoef<T><<<gs, kThreads, 0, X.side>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
+    k_pcoef<T><<<grid_slices(k_pcoef<T>, M.n_slices), kThreads, 0, X.side>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
                                             (T)o.p_ref_value, X.pcoef, X.pdiag, X.prhs0, 1);
     S->n_launch += 2;
     if ((s2 = amg_update<T>(X.amg, X.pcoef, X.pdiag, X.side, &S->n_launch, nullptr))) return s2;
@@ -1848,17 +1849,17 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
     // 3.2 rAU, HbyA
     if ((s2 = halo_exchange(S->m, U, 3, st))) return s2;
     PLAUNCH(pr, "k_HbyA", -1, 4 * N + Z * (4 + v) + 12 * v * N, st,
-            (k_HbyA<T><<<gs, kThreads, 0, st>>>(M, X.bU, X.udiag, X.ucoef, U, X.rAU, X.HbyA, overlap ? 0 : 1)));
+            (k_HbyA<T><<<grid_slices(k_HbyA<T>, M.n_slices), kThreads, 0, st>>>(M, X.bU, X.udiag, X.ucoef, U, X.rAU, X.HbyA, overlap ? 0 : 1)));
     S->n_launch++;
     if ((s2 = halo_exchange(S->m, X.HbyA, 3, st)) || (s2 = halo_exchange(S->m, X.rAU, 1, st))) return s2;
     // 3.3 phiHbyA
     PLAUNCH(pr, "k_phiHbyA", -1,
             3 * v * N + (8 + 5 * v) * F + (5 + 8 * v) * Bf + (o.ddt_corr ? 4 * v * N + v * F : 0.0), st,
-            (k_phiHbyA<T><<<gf, kThreads, 0, st>>>(M, X.HbyA, bkU, bvU, X.phiHbyA, o.ddt_corr ? X.Uold : nullptr,
+            (k_phiHbyA<T><<<grid_rows(k_phiHbyA<T>, (int64_t)M.F + M.B), kThreads, 0, st>>>(M, X.HbyA, bkU, bvU, X.phiHbyA, o.ddt_corr ? X.Uold : nullptr,
                                                    X.phiold, X.rAU, (T)(1.0 / o.dt))));
     // 3.4 pressure coefficients
     PLAUNCH(pr, "k_pcoef", -1, 3 * v * N + (16 + 5 * v) * F + (9 + 3 * v) * Bf, st,
-            (k_pcoef<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
+            (k_pcoef<T><<<grid_slices(k_pcoef<T>, M.n_slices), kThreads, 0, st>>>(M, X.rAU, X.phiHbyA, bkp, bvp, S->fixed_p ? -1 : S->ref_row,
                                                  (T)o.p_ref_value, X.pcoef, X.pdiag, X.prhs0, overlap ? 2 : 3)));
 
     // The pressure matrix depends on rAU = V / a_P only (the momentum
@@ -1881,7 +1882,7 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
         }
         if ((s2 = halo_exchange(S->m, X.gp, 3, st))) return s2;
         PLAUNCH(pr, "k_prhs", -1, 6 * v * N + (16 + 5 * v) * F, st,
-                (k_prhs<T><<<gs, kThreads, 0, st>>>(M, X.rAU, X.gp, X.prhs0, X.prhs)));
+                (k_prhs<T><<<grid_slices(k_prhs<T>, M.n_slices), kThreads, 0, st>>>(M, X.rAU, X.gp, X.prhs0, X.prhs)));
         S->n_launch++;
         rhs = X.prhs;
       }
@@ -1894,19 +1895,19 @@ static dfvm_status piso(dfvm_solver* S, SolverT<T>& X, T* U, T* p, T* phi, dfvm_
       if (io == o.n_nonorth) {
         if ((s2 = halo_exchange(S->m, p, 1, st))) return s2;
         PLAUNCH(pr, "k_fluxcorr", -1, 5 * v * N + (8 + 7 * v) * F + (5 + 4 * v) * Bf, st,
-                (k_fluxcorr<T><<<gf, kThreads, 0, st>>>(M, X.phiHbyA, p, X.rAU, X.gp, bkp, bvp, S->kcorr, phi)));
+                (k_fluxcorr<T><<<grid_rows(k_fluxcorr<T>, (int64_t)M.F + M.B), kThreads, 0, st>>>(M, X.phiHbyA, p, X.rAU, X.gp, bkp, bvp, S->kcorr, phi)));
         S->n_launch++;
       }
     }
     // 3.6 velocity correction (also refreshes grad p)
     PLAUNCH(pr, "k_Ucorr", -1, 12 * v * N + (16 + 4 * v) * F + (9 + 4 * v) * Bf, st,
-            (k_Ucorr<T><<<gs, kThreads, 0, st>>>(M, p, bkp, bvp, X.HbyA, X.rAU, U, X.gp)));
+            (k_Ucorr<T><<<grid_slices(k_Ucorr<T>, M.n_slices), kThreads, 0, st>>>(M, p, bkp, bvp, X.HbyA, X.rAU, U, X.gp)));
     S->n_launch++;
   }
   R->n_p = np;
   // 4. continuity + non-finite + Windkessel commit
   PLAUNCH(pr, "k_continuity", -1, 4 * v * N + (16 + v) * F + (8 + v) * Bf, st,
-          (k_continuity<T><<<gs, kThreads, 0, st>>>(M, phi, U, p, X.partials, X.ticket, X.d_cont, X.d_wk, n_wk,
+          (k_continuity<T><<<grid_slices(k_continuity<T>, M.n_slices), kThreads, 0, st>>>(M, phi, U, p, X.partials, X.ticket, X.d_cont, X.d_wk, n_wk,
                                                     Red{S->m->part.P, X.red_local})));
   S->n_launch++;
   if (S->m->part.P > 1) {
@@ -1971,7 +1972,7 @@ static dfvm_status transport_step_t(dfvm_solver* S, SolverT<T>& X, T* x, const T
   launch_grad<T>(M, x, 1, b->d_kind[2], (const T*)b->d_val[2], X.gp, st);
   if ((e = halo_exchange(S->m, X.gp, 3, st))) return e;
   const int gs = grid_for_slices(M.n_slices), ge = grid_for(M.n_own);
-  launch_transport_assemble<T, 1>(gs, st, M, x, phi, X.gp, nullptr, b->d_kind[2], (const T*)b->d_val[2], (T)gamma,
+  launch_transport_assemble<T, 1>(M.n_slices, st, M, x, phi, X.gp, nullptr, b->d_kind[2], (const T*)b->d_val[2], (T)gamma,
                                   (T)(1.0 / S->o.dt), (T)theta_of(S->o), S->o.convection, S->kcorr, X.fdO, X.fdN,
                                   X.udiag, X.prhs0, X.prhs, X.ucoef, X.ucoefT);
   if ((e = halo_exchange(S->m, X.udiag, 1, st))) return e;
