@@ -102,6 +102,17 @@ template <> __device__ __forceinline__ V4<float> ld4<float>(const V4<float>* p) 
   return V4<float>{a.x, a.y, a.z, a.w};
 }
 
+// A {a, b} pair stored 2-aligned (fp64 16 B / fp32 8 B): one load
+template <class T> __device__ __forceinline__ void ld2(const T* p, T& a, T& b);
+template <> __device__ __forceinline__ void ld2<double>(const double* p, double& a, double& b) {
+  const double2 u = __ldg(reinterpret_cast<const double2*>(p));
+  a = u.x; b = u.y;
+}
+template <> __device__ __forceinline__ void ld2<float>(const float* p, float& a, float& b) {
+  const float2 u = __ldg(reinterpret_cast<const float2*>(p));
+  a = u.x; b = u.y;
+}
+
 // Gather of a 3-vector from an AoS [n][3] array that is read-only during the
 // kernel: two loads (one 128-bit, one 64-bit, by the 16-byte parity of the
 // address) instead of three 64-bit ones — fewer L1 requests per gathered

@@ -322,8 +322,8 @@ __global__ void __launch_bounds__(kThreads) k_pcoef(DevMesh<T> M, const T* __res
       if (en.y >= 0) {
         const bool own = en.x >= 0;
         const int f = own ? en.x : ~en.x;
-        const T w = __ldg(&M.fw[f]);
-        const T d = ld4(&M.fcor[f]).w;
+        T w, d;
+        ld2(M.fwd + 2 * (int64_t)f, w, d);
         const T rn = rAU[en.y];
         const T cf = (w * (own ? ra : rn) + (T(1) - w) * (own ? rn : ra)) * d;
         if (mode & 1) pcoef[mbase + 32 * mj] = -cf;
