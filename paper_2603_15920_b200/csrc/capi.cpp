@@ -122,7 +122,7 @@ static dfvm_status upload_mesh(dfvm_mesh* m, DevMesh<T>& D) {
   D.nnz = mcnt[n_own];
   if (m->h_ms_ptr.empty()) { m->h_ms_ptr = ms_ptr; m->h_ms_len = ms_len; m->h_mnb = mnb; }   // AMG setup
   // face records
-  std::vector<V4<T>> fgeo(F_l), fcor(F_l), bgeo(P.n_lb);
+  std::vector<V4<T>> fgeo(F_l), fcor(F_l), fkw(F_l), bgeo(P.n_lb);
   std::vector<T> fw(F_l), fwd(2 * F_l);
   std::vector<int2> fcell(F_l);
   std::vector<int> bcell(P.n_lb);
@@ -132,6 +132,7 @@ static dfvm_status upload_mesh(dfvm_mesh* m, DevMesh<T>& D) {
     const double sg = H.flip_old[fo] ? -1.0 : 1.0;
     fgeo[i] = V4<T>{(T)(sg * H.Sf0[3 * fo]), (T)(sg * H.Sf0[3 * fo + 1]), (T)(sg * H.Sf0[3 * fo + 2]), (T)H.w[k]};
     fcor[i] = V4<T>{(T)H.k[3 * k], (T)H.k[3 * k + 1], (T)H.k[3 * k + 2], (T)H.delta[k]};
+    fkw[i] = V4<T>{(T)H.k[3 * k], (T)H.k[3 * k + 1], (T)H.k[3 * k + 2], (T)H.w[k]};
     fw[i] = (T)H.w[k];
     fwd[2 * i] = (T)H.w[k];
     fwd[2 * i + 1] = (T)H.delta[k];
@@ -146,7 +147,7 @@ static dfvm_status upload_mesh(dfvm_mesh* m, DevMesh<T>& D) {
   std::vector<T> vol(n_own);
   for (int64_t i = 0; i < n_own; ++i) vol[i] = (T)H.V0[H.old_of_new[P.cell_gid[i]]];
   dfvm_status st;
-  if ((st = upload(m, &D.fgeo, fgeo)) || (st = upload(m, &D.fcor, fcor)) || (st = upload(m, &D.fw, fw)) || (st = upload(m, &D.fwd, fwd)) ||
+  if ((st = upload(m, &D.fgeo, fgeo)) || (st = upload(m, &D.fcor, fcor)) || (st = upload(m, &D.fw, fw)) || (st = upload(m, &D.fwd, fwd)) || (st = upload(m, &D.fkw, fkw)) ||
       (st = upload(m, &D.fcell, fcell)) ||
       (st = upload(m, &D.bgeo, bgeo)) || (st = upload(m, &D.bcell, bcell)) || (st = upload(m, &D.vol, vol)) ||
       (st = upload(m, &D.sl_ptr, sl_ptr)) || (st = upload(m, &D.sl_len, sl_len)) || (st = upload(m, &D.inc, inc)) ||

@@ -106,6 +106,7 @@ struct DevMesh {
   V4<T>* fcor = nullptr;   // [F]
   T* fw = nullptr;         // [F] copy of the weights (kernels that need w alone read 8 B, not a 32 B record)
   T* fwd = nullptr;        // [2F] {w, delta} per face (k_pcoef: one 16 B load instead of 8 B + a 32 B record)
+  V4<T>* fkw = nullptr;    // [F] {k_x, k_y, k_z, w} (k_prhs: one 32 B load instead of 8 B + a 32 B record)
   int2* fcell = nullptr;   // [F]
   V4<T>* bgeo = nullptr;   // [B]
   int* bcell = nullptr;    // [B]

@@ -413,8 +413,8 @@ __global__ void __launch_bounds__(kThreads) k_prhs(DevMesh<T> M, const T* __rest
       const bool own = en.x >= 0;
       const int f = own ? en.x : ~en.x;
       const int n = en.y;
-      const T w = __ldg(&M.fw[f]);
-      const V4<T> c = ld4(&M.fcor[f]);
+      const V4<T> c = ld4(&M.fkw[f]);   // {k, w}
+      const T w = c.w;
       const T rn = rAU[n];
       T gn[3], GO[3], GN[3];
 #pragma unroll
